@@ -1,0 +1,304 @@
+// ref_capi.cpp -- TEST INFRASTRUCTURE ONLY.
+//
+// Exposes the *unmodified* reference implementation (compiled from the headers
+// under /root/reference/proj/include) through the same C ABI as the oracle
+// restatement (skrylov_oracle.h, prefix ref_ instead of orc_).  Built by
+// oracle/Makefile into oracle/_ref/libskref.so; used to pin the restatement and
+// as the reference CPU arm of bench.py.  No reference source is copied here:
+// this file only converts between C arrays and the reference's own types.
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <exception>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include <random>
+
+#include "skrylov/problem.hpp"
+#include "skrylov/sparse.hpp"
+#include "skrylov/sstep.hpp"
+#include "skrylov/solvers.hpp"
+#include "skrylov_oracle.h"
+
+using namespace skrylov;
+
+namespace {
+
+SparseMatrix to_sparse(const orc_csr* a) {
+  const std::size_t n = a->n;
+  std::vector<std::size_t> offs(a->row_offsets, a->row_offsets + n + 1);
+  const std::size_t nnz = offs.back();
+  std::vector<std::size_t> cols(a->col_indices, a->col_indices + nnz);
+  std::vector<double> vals(a->values, a->values + nnz);
+  return SparseMatrix(n, n, std::move(offs), std::move(cols), std::move(vals));
+}
+
+orc_counter conv(const OpCounter& c) {
+  return {c.dotprods, c.matvecs, c.vec_updates, c.stored_vectors, c.termination_dots};
+}
+
+void fill(orc_report* out, const SolveReport& rep) {
+  out->converged = rep.converged;
+  out->iterations = rep.iterations;
+  out->cycles = rep.cycles;
+  out->n_history = rep.residual_history.size();
+  out->history = static_cast<double*>(std::malloc(sizeof(double) * (out->n_history + 1)));
+  for (std::size_t i = 0; i < out->n_history; ++i) out->history[i] = rep.residual_history[i];
+  out->final_residual = rep.final_residual;
+  out->op_counts = conv(rep.op_counts);
+  out->n_op_history = rep.op_history.size();
+  out->op_history =
+      static_cast<orc_counter*>(std::malloc(sizeof(orc_counter) * (out->n_op_history + 1)));
+  for (std::size_t i = 0; i < out->n_op_history; ++i) out->op_history[i] = conv(rep.op_history[i]);
+  out->steady_iteration = rep.steady_iteration;
+  out->has_breakdown = rep.breakdown.has_value();
+  if (rep.breakdown)
+    std::snprintf(out->breakdown, sizeof out->breakdown, "%s", rep.breakdown->c_str());
+  out->fallback_cycles = rep.fallback_cycles;
+  out->n_notes = 0;
+  for (const auto& s : rep.notes)
+    if (out->n_notes < 4) std::snprintf(out->notes[out->n_notes++], 256, "%s", s.c_str());
+}
+
+SStepConfig sconf(const orc_sstep_cfg* c) {
+  SStepConfig s;
+  s.s = c->s;
+  s.k = c->k;
+  s.m = c->m;
+  s.tol = c->tol;
+  s.max_iterations = c->max_iterations;
+  s.precondition = c->precondition;
+  s.unbounded_window = c->unbounded_window;
+  s.debug_checks = c->debug_checks;
+  s.divergence_factor = c->divergence_factor;
+  return s;
+}
+
+SolverConfig oconf(const orc_solver_cfg* c) {
+  SolverConfig s;
+  s.method = static_cast<Method>(c->method);
+  s.k = c->k;
+  s.m = c->m;
+  s.tol = c->tol;
+  s.max_iterations = c->max_iterations;
+  s.precondition = c->precondition;
+  s.debug_checks = c->debug_checks;
+  s.divergence_factor = c->divergence_factor;
+  return s;
+}
+
+template <class F>
+int guarded(char* err, std::size_t cap, F&& body) {
+  try {
+    body();
+    return 0;
+  } catch (const breakdown_error& e) {
+    if (err) std::snprintf(err, cap, "%s", e.what());
+    return 2;
+  } catch (const std::invalid_argument& e) {
+    if (err) std::snprintf(err, cap, "%s", e.what());
+    return 1;
+  } catch (const std::logic_error& e) {
+    if (err) std::snprintf(err, cap, "%s", e.what());
+    return 3;
+  } catch (const std::exception& e) {
+    if (err) std::snprintf(err, cap, "%s", e.what());
+    return 4;
+  }
+}
+
+template <class Solve>
+int run_solver(const orc_csr* a, const double* f, double* x, orc_report* rep, Solve&& solve) {
+  return guarded(rep->error, sizeof rep->error, [&] {
+    SparseMatrix m = to_sparse(a);
+    LinearOperator op = as_operator(m);
+    std::span<const double> fs(f, a->n);
+    std::vector<double> xv(x, x + a->n);
+    SolveReport r = solve(op, fs, xv);
+    std::memcpy(x, xv.data(), sizeof(double) * a->n);
+    fill(rep, r);
+  });
+}
+
+}  // namespace
+
+extern "C" {
+
+void ref_report_init(orc_report* r) { std::memset(r, 0, sizeof *r); }
+void ref_report_free(orc_report* r) {
+  std::free(r->history);
+  std::free(r->op_history);
+  std::free(r->block_rho);
+  std::memset(r, 0, sizeof *r);
+}
+
+void ref_spmv(const orc_csr* a, const double* x, double* y) {
+  SparseMatrix m = to_sparse(a);
+  spmv(m, std::span<const double>(x, a->n), std::span<double>(y, a->n));
+}
+
+int ref_krylov_block(const orc_csr* a, const double* v, uint64_t s, double* out) {
+  return guarded(nullptr, 0, [&] {
+    SparseMatrix m = to_sparse(a);
+    LinearOperator op = as_operator(m);
+    DirectionBlock b = krylov_block(op, std::span<const double>(v, a->n), s);
+    for (std::size_t j = 0; j < s; ++j)
+      std::memcpy(out + j * a->n, b.column(j).data(), sizeof(double) * a->n);
+  });
+}
+
+int ref_gram_solve(uint64_t order, const double* w, uint64_t nrhs, const double* rhs, double* x_out,
+                   int32_t* used_ldlt, double* pivots_out, char* err, uint64_t errcap) {
+  return guarded(err, errcap, [&] {
+    Matrix wm(order, order);
+    for (std::size_t i = 0; i < order; ++i)
+      for (std::size_t j = 0; j < order; ++j) wm(i, j) = w[i * order + j];
+    GramSolver g(wm);
+    if (used_ldlt) *used_ldlt = g.used_ldlt();
+    if (pivots_out)
+      for (std::size_t i = 0; i < order; ++i) pivots_out[i] = g.pivots()[i];
+    if (nrhs) {
+      Matrix r(order, nrhs);
+      for (std::size_t i = 0; i < order; ++i)
+        for (std::size_t j = 0; j < nrhs; ++j) r(i, j) = rhs[i * nrhs + j];
+      Matrix xs = g.solve(r);
+      for (std::size_t i = 0; i < order; ++i)
+        for (std::size_t j = 0; j < nrhs; ++j) x_out[i * nrhs + j] = xs(i, j);
+    }
+  });
+}
+
+int ref_cholesky_upper(uint64_t order, const double* w, double* r_out, char* err, uint64_t errcap) {
+  return guarded(err, errcap, [&] {
+    Matrix wm(order, order);
+    for (std::size_t i = 0; i < order; ++i)
+      for (std::size_t j = 0; j < order; ++j) wm(i, j) = w[i * order + j];
+    Matrix r = cholesky_upper(wm);
+    for (std::size_t i = 0; i < order; ++i)
+      for (std::size_t j = 0; j < order; ++j) r_out[i * order + j] = r(i, j);
+  });
+}
+
+int ref_hessenberg_lsq(uint64_t rows, uint64_t cols, const double* g, double beta, double* y_out,
+                       double* residual_out, char* err, uint64_t errcap) {
+  return guarded(err, errcap, [&] {
+    Matrix gm(rows, cols);
+    for (std::size_t i = 0; i < rows; ++i)
+      for (std::size_t j = 0; j < cols; ++j) gm(i, j) = g[i * cols + j];
+    LsqSolution s = hessenberg_lsq(gm, beta);
+    for (std::size_t i = 0; i < s.y.size(); ++i) y_out[i] = s.y[i];
+    if (residual_out) *residual_out = s.residual_norm;
+  });
+}
+
+int ref_mr_solve(const orc_csr* a, const double* f, double* x, const orc_solver_cfg* cfg, orc_report* rep) {
+  return run_solver(a, f, x, rep, [&](auto& op, auto fs, auto& xv) { return mr_solve(op, fs, xv, oconf(cfg)); });
+}
+int ref_omin_solve(const orc_csr* a, const double* f, double* x, const orc_solver_cfg* cfg, orc_report* rep) {
+  return run_solver(a, f, x, rep, [&](auto& op, auto fs, auto& xv) { return omin_solve(op, fs, xv, oconf(cfg)); });
+}
+int ref_gmres_solve(const orc_csr* a, const double* f, double* x, const orc_solver_cfg* cfg, orc_report* rep) {
+  return run_solver(a, f, x, rep, [&](auto& op, auto fs, auto& xv) { return gmres_solve(op, fs, xv, oconf(cfg)); });
+}
+int ref_smr_solve(const orc_csr* a, const double* f, double* x, const orc_sstep_cfg* cfg, orc_report* rep) {
+  return run_solver(a, f, x, rep, [&](auto& op, auto fs, auto& xv) { return smr_solve(op, fs, xv, sconf(cfg)); });
+}
+int ref_somin_solve(const orc_csr* a, const double* f, double* x, const orc_sstep_cfg* cfg, orc_report* rep) {
+  return run_solver(a, f, x, rep, [&](auto& op, auto fs, auto& xv) { return somin_solve(op, fs, xv, sconf(cfg)); });
+}
+int ref_sgmres_solve(const orc_csr* a, const double* f, double* x, const orc_sstep_cfg* cfg, orc_report* rep) {
+  return run_solver(a, f, x, rep, [&](auto& op, auto fs, auto& xv) { return sgmres_solve(op, fs, xv, sconf(cfg)); });
+}
+
+int ref_smr_step(const orc_csr* a, double* x, double* r, uint64_t s, double* coeffs_out, orc_counter* c) {
+  return guarded(nullptr, 0, [&] {
+    SparseMatrix m = to_sparse(a);
+    LinearOperator op = as_operator(m);
+    std::vector<double> xv(x, x + a->n), rv(r, r + a->n);
+    OpCounter oc;
+    std::vector<double> co = smr_step(op, xv, rv, s, &oc);
+    std::memcpy(x, xv.data(), sizeof(double) * a->n);
+    std::memcpy(r, rv.data(), sizeof(double) * a->n);
+    if (coeffs_out) std::memcpy(coeffs_out, co.data(), sizeof(double) * co.size());
+    if (c) *c = conv(oc);
+  });
+}
+
+int ref_arnoldi(const orc_csr* a, const double* v1, uint64_t m, double* h_out, uint64_t* steps_out,
+                int32_t* happy_out) {
+  return guarded(nullptr, 0, [&] {
+    SparseMatrix sm = to_sparse(a);
+    LinearOperator op = as_operator(sm);
+    ArnoldiResult r = arnoldi(op, std::span<const double>(v1, a->n), m);
+    std::memset(h_out, 0, sizeof(double) * (m + 1) * m);
+    for (std::size_t i = 0; i < r.h.rows(); ++i)
+      for (std::size_t j = 0; j < r.h.cols(); ++j) h_out[i * m + j] = r.h(i, j);
+    *steps_out = r.steps;
+    *happy_out = r.happy;
+  });
+}
+
+int ref_sarnoldi(const orc_csr* a, const double* v1, uint64_t s, uint64_t m_blocks, double* blocks_out,
+                 double* grams_out, double* hess_out, double* seed_out, double* seed_norm_out,
+                 orc_counter* counter, char* err, uint64_t errcap) {
+  return guarded(err, errcap, [&] {
+    SparseMatrix sm = to_sparse(a);
+    LinearOperator op = as_operator(sm);
+    OpCounter oc;
+    SStepBasis b = sarnoldi(op, std::span<const double>(v1, a->n), s, m_blocks, &oc);
+    const std::size_t n = a->n;
+    for (std::size_t bi = 0; bi < b.blocks.size(); ++bi)
+      for (std::size_t j = 0; j < s; ++j)
+        std::memcpy(blocks_out + (bi * s + j) * n, b.blocks[bi].column(j).data(), sizeof(double) * n);
+    for (std::size_t bi = 0; bi < b.grams.size(); ++bi)
+      for (std::size_t i = 0; i < s; ++i)
+        for (std::size_t j = 0; j < s; ++j) grams_out[bi * s * s + i * s + j] = b.grams[bi](i, j);
+    for (std::size_t i = 0; i < b.hess.rows(); ++i)
+      for (std::size_t j = 0; j < b.hess.cols(); ++j) hess_out[i * b.hess.cols() + j] = b.hess(i, j);
+    std::memcpy(seed_out, b.next_seed.data(), sizeof(double) * n);
+    *seed_norm_out = b.next_seed_norm;
+    if (counter) *counter = conv(oc);
+  });
+}
+
+// Test-input helpers: the reference's own problem assembly (problem.hpp:138-199, out of
+// the hot-path scope but used by its KATs) and the std::mt19937 uniform stream its test
+// oracles draw from (tests/support/oracles.hpp:117-133).
+int ref_discretize(uint64_t nx, double beta, double gamma, int32_t symmetric, uint64_t** offs,
+                   uint64_t** cols, double** vals, double** rhs, double** x0) {
+  return guarded(nullptr, 0, [&] {
+    ProblemFunctions p = paper_problem(beta, gamma);
+    if (symmetric) {
+      p.d = [](double, double) { return 0.0; };
+      p.e = [](double, double) { return 0.0; };
+    }
+    DiscretizedProblem prob = assemble(nx, p);
+    const std::size_t n = prob.a.rows(), nnz = prob.a.nnz();
+    *offs = static_cast<uint64_t*>(std::malloc(sizeof(uint64_t) * (n + 1)));
+    *cols = static_cast<uint64_t*>(std::malloc(sizeof(uint64_t) * nnz));
+    *vals = static_cast<double*>(std::malloc(sizeof(double) * nnz));
+    *rhs = static_cast<double*>(std::malloc(sizeof(double) * n));
+    *x0 = static_cast<double*>(std::malloc(sizeof(double) * n));
+    for (std::size_t i = 0; i <= n; ++i) (*offs)[i] = prob.a.row_offsets()[i];
+    for (std::size_t i = 0; i < nnz; ++i) {
+      (*cols)[i] = prob.a.col_indices()[i];
+      (*vals)[i] = prob.a.values()[i];
+    }
+    for (std::size_t i = 0; i < n; ++i) {
+      (*rhs)[i] = prob.rhs[i];
+      (*x0)[i] = prob.x0[i];
+    }
+  });
+}
+
+void ref_free(void* p) { std::free(p); }
+
+void ref_mt_uniform(uint32_t seed, uint64_t count, double lo, double hi, double* out) {
+  std::mt19937 rng(seed);
+  std::uniform_real_distribution<double> dist(lo, hi);
+  for (uint64_t i = 0; i < count; ++i) out[i] = dist(rng);
+}
+
+}  // extern "C"

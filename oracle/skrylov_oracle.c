@@ -1,0 +1,1682 @@
+/*
+ * skrylov_oracle.c -- TEST INFRASTRUCTURE ONLY (see skrylov_oracle.h).
+ *
+ * Plain-C restatement of the reference s-step Orthomin / s-step GMRES path.
+ * Every routine follows the reference's arithmetic order so that, compiled
+ * with -ffp-contract=off and without -march (the reference's Release flags,
+ * proj/CMakeLists.txt:6-8), it reproduces the reference bit for bit.  Each
+ * function cites the reference lines it restates.
+ */
+#include "skrylov_oracle.h"
+
+#include <math.h>
+#include <stdarg.h>
+#include <stdio.h>
+#include <stdlib.h>
+#include <string.h>
+
+/* ------------------------------------------------------------------ */
+/* error plumbing: status codes mirror the reference's exception types */
+enum { ORC_OK = 0, ORC_EINVAL = 1, ORC_EBREAK = 2, ORC_ELOGIC = 3, ORC_ENOMEM = 4 };
+
+typedef struct {
+  int code;
+  char msg[512];
+} orc_err;
+
+static void err_set(orc_err* e, int code, const char* fmt, ...) {
+  va_list ap;
+  e->code = code;
+  va_start(ap, fmt);
+  vsnprintf(e->msg, sizeof e->msg, fmt, ap);
+  va_end(ap);
+}
+
+/* std::to_string(double) is "%f" */
+static void fmt_double(char* buf, size_t cap, double v) { snprintf(buf, cap, "%f", v); }
+
+#define REQUIRE(cond, e, text)          \
+  do {                                  \
+    if (!(cond)) {                      \
+      err_set((e), ORC_EINVAL, "%s", text); \
+      return (e)->code;                 \
+    }                                   \
+  } while (0)
+
+/* ------------------------------------------------------------------ */
+/* growable arrays for the report */
+static int push_d(double** a, uint64_t* n, double v) {
+  double* p = (double*)realloc(*a, (size_t)(*n + 1) * sizeof(double));
+  if (!p) return ORC_ENOMEM;
+  p[*n] = v;
+  *a = p;
+  ++*n;
+  return 0;
+}
+static int push_c(orc_counter** a, uint64_t* n, orc_counter v) {
+  orc_counter* p = (orc_counter*)realloc(*a, (size_t)(*n + 1) * sizeof(orc_counter));
+  if (!p) return ORC_ENOMEM;
+  p[*n] = v;
+  *a = p;
+  ++*n;
+  return 0;
+}
+static void add_note(orc_report* r, const char* s) {
+  if (r->n_notes < 4) snprintf(r->notes[r->n_notes++], 256, "%s", s);
+}
+static void set_breakdown(orc_report* r, const char* s) {
+  r->has_breakdown = 1;
+  snprintf(r->breakdown, sizeof r->breakdown, "%s", s);
+}
+
+void orc_report_init(orc_report* r) { memset(r, 0, sizeof *r); }
+void orc_report_free(orc_report* r) {
+  free(r->history);
+  free(r->op_history);
+  free(r->block_rho);
+  memset(r, 0, sizeof *r);
+}
+
+static void* xcalloc(size_t n, size_t sz) { return calloc(n ? n : 1, sz); }
+
+/* ------------------------------------------------------------------ */
+/* L0 kernels: kernels.hpp:45-74 (ascending-index summation) */
+double orc_dot(uint64_t n, const double* a, const double* b) {
+  double acc = 0.0;
+  for (uint64_t i = 0; i < n; ++i) acc += a[i] * b[i];
+  return acc;
+}
+static double norm2(uint64_t n, const double* v) { return sqrt(orc_dot(n, v, v)); }
+static void axpy(uint64_t n, double alpha, const double* x, double* y) {
+  for (uint64_t i = 0; i < n; ++i) y[i] += alpha * x[i];
+}
+static void scale(uint64_t n, double alpha, double* v) {
+  for (uint64_t i = 0; i < n; ++i) v[i] *= alpha;
+}
+static int is_zero(uint64_t n, const double* v) {
+  for (uint64_t i = 0; i < n; ++i)
+    if (v[i] != 0.0) return 0;
+  return 1;
+}
+
+/* sparse.hpp:135-146: per-row acc=0, ascending column order */
+void orc_spmv(const orc_csr* a, const double* x, double* y) {
+  for (uint64_t i = 0; i < a->n; ++i) {
+    double acc = 0.0;
+    for (uint64_t p = a->row_offsets[i]; p < a->row_offsets[i + 1]; ++p)
+      acc += a->values[p] * x[a->col_indices[p]];
+    y[i] = acc;
+  }
+}
+
+/* block.hpp:59-67 */
+int orc_krylov_block(const orc_csr* a, const double* v, uint64_t s, double* out) {
+  const uint64_t n = a->n;
+  memcpy(out, v, (size_t)n * sizeof(double));
+  for (uint64_t j = 1; j < s; ++j) orc_spmv(a, out + (j - 1) * n, out + j * n);
+  return 0;
+}
+
+/* block.hpp:70-76 (row-major s x t result) */
+static void block_gram(uint64_t n, const double* u, uint64_t su, const double* v, uint64_t sv,
+                       double* g) {
+  for (uint64_t j = 0; j < su; ++j)
+    for (uint64_t l = 0; l < sv; ++l) g[j * sv + l] = orc_dot(n, u + j * n, v + l * n);
+}
+/* block.hpp:80-91 */
+static void block_gram_self(uint64_t n, const double* u, uint64_t s, double* g) {
+  block_gram(n, u, s, u, s, g);
+  for (uint64_t j = 0; j < s; ++j)
+    for (uint64_t l = 0; l < s; ++l)
+      if (j < l) {
+        const double avg = (g[j * s + l] + g[l * s + j]) / 2.0;
+        g[j * s + l] = avg;
+        g[l * s + j] = avg;
+      }
+}
+/* block.hpp:94-99 */
+static void block_dot(uint64_t n, const double* u, uint64_t s, const double* r, double* out) {
+  for (uint64_t j = 0; j < s; ++j) out[j] = orc_dot(n, u + j * n, r);
+}
+/* block.hpp:109-116: Y += X C, result column outer, source column inner */
+static void block_axpy_inplace(uint64_t n, double* y, const double* x, uint64_t s, const double* c) {
+  for (uint64_t jc = 0; jc < s; ++jc)
+    for (uint64_t l = 0; l < s; ++l) axpy(n, c[l * s + jc], x + l * n, y + jc * n);
+}
+static double mat_trace(uint64_t r, uint64_t c, const double* m) {
+  double acc = 0.0;
+  uint64_t d = r < c ? r : c;
+  for (uint64_t i = 0; i < d; ++i) acc += m[i * c + i];
+  return acc;
+}
+static double mat_frob(uint64_t cnt, const double* m) {
+  double acc = 0.0;
+  for (uint64_t i = 0; i < cnt; ++i) acc += m[i] * m[i];
+  return sqrt(acc);
+}
+
+/* ------------------------------------------------------------------ */
+/* small_dense.hpp:42-186 GramSolver */
+#define GMAX 16
+typedef struct {
+  uint64_t order;
+  double w[GMAX * GMAX];
+  double fac[GMAX * GMAX];
+  double piv[GMAX];
+  uint64_t perm[GMAX];
+  int used_ldlt;
+} gram_t;
+
+static int gram_try_cholesky(gram_t* g) { /* small_dense.hpp:131-148 */
+  const uint64_t n = g->order;
+  const double floor_ = 1e-13 * fabs(mat_trace(n, n, g->w)) / (double)n;
+  memset(g->fac, 0, sizeof g->fac);
+  memset(g->piv, 0, sizeof g->piv);
+  for (uint64_t j = 0; j < n; ++j) {
+    double d = g->w[j * n + j];
+    for (uint64_t k = 0; k < j; ++k) d -= g->fac[j * n + k] * g->fac[j * n + k];
+    if (d <= floor_) return 0;
+    g->piv[j] = d;
+    g->fac[j * n + j] = sqrt(d);
+    for (uint64_t i = j + 1; i < n; ++i) {
+      double acc = g->w[i * n + j];
+      for (uint64_t k = 0; k < j; ++k) acc -= g->fac[i * n + k] * g->fac[j * n + k];
+      g->fac[i * n + j] = acc / g->fac[j * n + j];
+    }
+  }
+  return 1;
+}
+
+static void gram_factor_ldlt(gram_t* g) { /* small_dense.hpp:150-178 */
+  const uint64_t n = g->order;
+  double m[GMAX * GMAX];
+  g->used_ldlt = 1;
+  memcpy(m, g->w, sizeof m);
+  for (uint64_t i = 0; i < n; ++i) g->perm[i] = i;
+  memset(g->fac, 0, sizeof g->fac);
+  memset(g->piv, 0, sizeof g->piv);
+  for (uint64_t j = 0; j < n; ++j) {
+    uint64_t p = j;
+    for (uint64_t i = j + 1; i < n; ++i)
+      if (fabs(m[i * n + i]) > fabs(m[p * n + p])) p = i;
+    if (p != j) {
+      for (uint64_t t = 0; t < n; ++t) {
+        double tmp = m[j * n + t];
+        m[j * n + t] = m[p * n + t];
+        m[p * n + t] = tmp;
+      }
+      for (uint64_t t = 0; t < n; ++t) {
+        double tmp = m[t * n + j];
+        m[t * n + j] = m[t * n + p];
+        m[t * n + p] = tmp;
+      }
+      for (uint64_t t = 0; t < j; ++t) {
+        double tmp = g->fac[j * n + t];
+        g->fac[j * n + t] = g->fac[p * n + t];
+        g->fac[p * n + t] = tmp;
+      }
+      uint64_t tp = g->perm[j];
+      g->perm[j] = g->perm[p];
+      g->perm[p] = tp;
+    }
+    const double d = m[j * n + j];
+    g->piv[j] = d;
+    g->fac[j * n + j] = 1.0;
+    if (d == 0.0) continue;
+    for (uint64_t i = j + 1; i < n; ++i) g->fac[i * n + j] = m[i * n + j] / d;
+    for (uint64_t i = j + 1; i < n; ++i)
+      for (uint64_t k = j + 1; k <= i; ++k) {
+        m[i * n + k] -= g->fac[i * n + j] * d * g->fac[k * n + j];
+        m[k * n + i] = m[i * n + k];
+      }
+  }
+}
+
+static int gram_init(gram_t* g, uint64_t order, const double* w, orc_err* e) { /* :45-65 */
+  if (order < 1 || order > GMAX) {
+    err_set(e, ORC_EINVAL, "GramSolver: empty matrix");
+    return e->code;
+  }
+  memset(g, 0, sizeof *g);
+  g->order = order;
+  memcpy(g->w, w, (size_t)(order * order) * sizeof(double));
+  if (order == 1) {
+    g->piv[0] = w[0];
+    if (w[0] == 0.0) {
+      err_set(e, ORC_EBREAK, "sym_solve: singular 1x1 Gram system");
+      return e->code;
+    }
+    return 0;
+  }
+  if (!gram_try_cholesky(g)) gram_factor_ldlt(g);
+  double pmin = fabs(g->piv[0]), pmax = pmin;
+  for (uint64_t i = 0; i < order; ++i) {
+    double a = fabs(g->piv[i]);
+    if (a < pmin) pmin = a;
+    if (a > pmax) pmax = a;
+  }
+  if (pmax == 0.0 || pmin / pmax < 1e-15) {
+    char num[64];
+    fmt_double(num, sizeof num, pmax == 0.0 ? 0.0 : pmin / pmax);
+    err_set(e, ORC_EBREAK, "sym_solve: numerically singular Gram system (pivot ratio %s)", num);
+    return e->code;
+  }
+  return 0;
+}
+
+static void gram_solve_vec(const gram_t* g, const double* rhs, double* x) { /* :75-112 */
+  const uint64_t n = g->order;
+  if (n == 1) {
+    x[0] = rhs[0] / g->w[0];
+    return;
+  }
+  if (!g->used_ldlt) {
+    for (uint64_t i = 0; i < n; ++i) {
+      double acc = rhs[i];
+      for (uint64_t k = 0; k < i; ++k) acc -= g->fac[i * n + k] * x[k];
+      x[i] = acc / g->fac[i * n + i];
+    }
+    for (uint64_t ii = n; ii-- > 0;) {
+      double acc = x[ii];
+      for (uint64_t k = ii + 1; k < n; ++k) acc -= g->fac[k * n + ii] * x[k];
+      x[ii] = acc / g->fac[ii * n + ii];
+    }
+    return;
+  }
+  double b[GMAX];
+  for (uint64_t i = 0; i < n; ++i) b[i] = rhs[g->perm[i]];
+  for (uint64_t i = 0; i < n; ++i) {
+    double acc = b[i];
+    for (uint64_t k = 0; k < i; ++k) acc -= g->fac[i * n + k] * b[k];
+    b[i] = acc;
+  }
+  for (uint64_t i = 0; i < n; ++i) b[i] /= g->piv[i];
+  for (uint64_t ii = n; ii-- > 0;) {
+    double acc = b[ii];
+    for (uint64_t k = ii + 1; k < n; ++k) acc -= g->fac[k * n + ii] * b[k];
+    b[ii] = acc;
+  }
+  for (uint64_t i = 0; i < n; ++i) x[g->perm[i]] = b[i];
+}
+
+/* :115-128 column-wise matrix solve; rhs/out are order x ncols row-major */
+static void gram_solve_mat(const gram_t* g, uint64_t ncols, const double* rhs, double* out) {
+  const uint64_t n = g->order;
+  double col[GMAX], sol[GMAX];
+  for (uint64_t j = 0; j < ncols; ++j) {
+    for (uint64_t i = 0; i < n; ++i) col[i] = rhs[i * ncols + j];
+    gram_solve_vec(g, col, sol);
+    for (uint64_t i = 0; i < n; ++i) out[i * ncols + j] = sol[i];
+  }
+}
+
+/* small_dense.hpp:190-206 */
+static int cholesky_upper(uint64_t n, const double* w, double* r, orc_err* e) {
+  memset(r, 0, (size_t)(n * n) * sizeof(double));
+  for (uint64_t i = 0; i < n; ++i) {
+    double d = w[i * n + i];
+    for (uint64_t k = 0; k < i; ++k) d -= r[k * n + i] * r[k * n + i];
+    if (d <= 0.0) {
+      err_set(e, ORC_EBREAK, "cholesky: matrix not positive definite");
+      return e->code;
+    }
+    r[i * n + i] = sqrt(d);
+    for (uint64_t j = i + 1; j < n; ++j) {
+      double acc = w[i * n + j];
+      for (uint64_t k = 0; k < i; ++k) acc -= r[k * n + i] * r[k * n + j];
+      r[i * n + j] = acc / r[i * n + i];
+    }
+  }
+  return 0;
+}
+
+/* small_dense.hpp:239-307 incremental Givens LSQ. Columns stored packed: column j holds j+1 entries. */
+typedef struct {
+  uint64_t cols, cap;
+  double* rcols; /* packed: column j starts at j*(j+1)/2 */
+  double *cs, *sn, *rhs;
+  double residual, gnorm_sq;
+} hlsq_t;
+
+static int hlsq_init(hlsq_t* h, double beta, uint64_t cap) {
+  memset(h, 0, sizeof *h);
+  h->cap = cap;
+  h->rcols = (double*)xcalloc((size_t)(cap * (cap + 1) / 2 + 1), sizeof(double));
+  h->cs = (double*)xcalloc((size_t)cap + 1, sizeof(double));
+  h->sn = (double*)xcalloc((size_t)cap + 1, sizeof(double));
+  h->rhs = (double*)xcalloc((size_t)cap + 2, sizeof(double));
+  if (!h->rcols || !h->cs || !h->sn || !h->rhs) return ORC_ENOMEM;
+  h->rhs[0] = beta;
+  h->residual = fabs(beta);
+  return 0;
+}
+static void hlsq_free(hlsq_t* h) {
+  free(h->rcols);
+  free(h->cs);
+  free(h->sn);
+  free(h->rhs);
+}
+static double hlsq_append(hlsq_t* h, double* col /* j+2 entries, modified */) {
+  const uint64_t j = h->cols;
+  for (uint64_t t = 0; t < j + 2; ++t) h->gnorm_sq += col[t] * col[t];
+  for (uint64_t t = 0; t < j; ++t) {
+    const double a = col[t], b = col[t + 1];
+    col[t] = h->cs[t] * a + h->sn[t] * b;
+    col[t + 1] = -h->sn[t] * a + h->cs[t] * b;
+  }
+  const double a = col[j], b = col[j + 1];
+  const double r = hypot(a, b);
+  double c = 1.0, s = 0.0;
+  if (r != 0.0) {
+    c = a / r;
+    s = b / r;
+  }
+  h->cs[j] = c;
+  h->sn[j] = s;
+  col[j] = r;
+  memcpy(h->rcols + j * (j + 1) / 2, col, (size_t)(j + 1) * sizeof(double));
+  h->cols = j + 1;
+  h->rhs[j + 1] = 0.0;
+  const double ra = h->rhs[j], rb = h->rhs[j + 1];
+  h->rhs[j] = c * ra + s * rb;
+  h->rhs[j + 1] = -s * ra + c * rb;
+  h->residual = fabs(h->rhs[j + 1]);
+  return h->residual;
+}
+static double hlsq_r(const hlsq_t* h, uint64_t col, uint64_t row) { return h->rcols[col * (col + 1) / 2 + row]; }
+static int hlsq_solve(const hlsq_t* h, double* y, orc_err* e) { /* :287-300 */
+  const uint64_t m = h->cols;
+  const double tol = 1e-14 * sqrt(h->gnorm_sq);
+  for (uint64_t i = 0; i < m; ++i) y[i] = 0.0;
+  for (uint64_t ii = m; ii-- > 0;) {
+    double acc = h->rhs[ii];
+    for (uint64_t k = ii + 1; k < m; ++k) acc -= hlsq_r(h, k, ii) * y[k];
+    if (fabs(hlsq_r(h, ii, ii)) <= tol) {
+      err_set(e, ORC_EBREAK, "hessenberg lsq: rank-deficient R diagonal at column %llu",
+              (unsigned long long)(ii + 1));
+      return e->code;
+    }
+    y[ii] = acc / hlsq_r(h, ii, ii);
+  }
+  return 0;
+}
+
+/* ------------------------------------------------------------------ */
+/* exported small-dense entry points (test hooks) */
+int orc_gram_solve(uint64_t order, const double* w, uint64_t nrhs, const double* rhs, double* x_out,
+                   int32_t* used_ldlt, double* pivots_out, char* err, uint64_t errcap) {
+  orc_err e = {0, ""};
+  gram_t g;
+  int st = gram_init(&g, order, w, &e);
+  if (used_ldlt) *used_ldlt = g.used_ldlt;
+  if (pivots_out && order <= GMAX) memcpy(pivots_out, g.piv, (size_t)order * sizeof(double));
+  if (st) {
+    if (err) snprintf(err, errcap, "%s", e.msg);
+    return st;
+  }
+  if (nrhs) gram_solve_mat(&g, nrhs, rhs, x_out);
+  return 0;
+}
+
+int orc_cholesky_upper(uint64_t order, const double* w, double* r_out, char* err, uint64_t errcap) {
+  orc_err e = {0, ""};
+  int st = cholesky_upper(order, w, r_out, &e);
+  if (st && err) snprintf(err, errcap, "%s", e.msg);
+  return st;
+}
+
+int orc_hessenberg_lsq(uint64_t rows, uint64_t cols, const double* g, double beta, double* y_out,
+                       double* residual_out, char* err, uint64_t errcap) {
+  /* small_dense.hpp:316-331 */
+  orc_err e = {0, ""};
+  if (!(rows >= cols + 1)) {
+    if (err) snprintf(err, errcap, "hessenberg_lsq: G must have more rows than columns");
+    return ORC_EINVAL;
+  }
+  if (!(beta >= 0.0)) {
+    if (err) snprintf(err, errcap, "hessenberg_lsq: beta must be non-negative");
+    return ORC_EINVAL;
+  }
+  hlsq_t h;
+  if (hlsq_init(&h, beta, cols)) return ORC_ENOMEM;
+  double* col = (double*)xcalloc((size_t)cols + 2, sizeof(double));
+  for (uint64_t j = 0; j < cols; ++j) {
+    for (uint64_t i = j + 2; i < rows; ++i)
+      if (g[i * cols + j] != 0.0) {
+        if (err) snprintf(err, errcap, "hessenberg_lsq: G is not Hessenberg-banded");
+        free(col);
+        hlsq_free(&h);
+        return ORC_EINVAL;
+      }
+    for (uint64_t i = 0; i <= j + 1; ++i) col[i] = g[i * cols + j];
+    hlsq_append(&h, col);
+  }
+  int st = hlsq_solve(&h, y_out, &e);
+  if (residual_out) *residual_out = h.residual;
+  if (st && err) snprintf(err, errcap, "%s", e.msg);
+  free(col);
+  hlsq_free(&h);
+  return st;
+}
+
+/* ------------------------------------------------------------------ */
+/* solvers.hpp:58-76 */
+static void initial_residual(const orc_csr* a, const double* f, const double* x, double* r,
+                             orc_counter* c) {
+  const uint64_t n = a->n;
+  memcpy(r, f, (size_t)n * sizeof(double));
+  if (!is_zero(n, x)) {
+    double* ax = (double*)xcalloc((size_t)n, sizeof(double));
+    orc_spmv(a, x, ax);
+    ++c->matvecs;
+    for (uint64_t i = 0; i < n; ++i) r[i] -= ax[i];
+    ++c->vec_updates;
+    free(ax);
+  }
+}
+static double checked_norm(uint64_t n, const double* r, orc_counter* c) {
+  ++c->termination_dots;
+  return norm2(n, r);
+}
+
+/* solvers.hpp:86-110 MGS Arnoldi step; q is an array of nq vectors (capacity >= nq+1) */
+static int arnoldi_step(const orc_csr* a, double** q, uint64_t* nq, double* col /* nq+1 */,
+                        orc_counter* c) {
+  const uint64_t n = a->n, j = *nq;
+  double* w = (double*)xcalloc((size_t)n, sizeof(double));
+  orc_spmv(a, q[j - 1], w);
+  ++c->matvecs;
+  for (uint64_t i = 0; i < j; ++i) {
+    col[i] = orc_dot(n, q[i], w);
+    axpy(n, -col[i], q[i], w);
+  }
+  c->dotprods += j;
+  c->vec_updates += j;
+  const double hsub = norm2(n, w);
+  ++c->dotprods;
+  col[j] = hsub;
+  const int happy = hsub <= 1e-14 * norm2(j + 1, col);
+  if (!happy) {
+    scale(n, 1.0 / hsub, w);
+    ++c->vec_updates;
+    q[j] = w;
+    *nq = j + 1;
+  } else {
+    free(w);
+  }
+  return happy;
+}
+
+int orc_arnoldi(const orc_csr* a, const double* v1, uint64_t m, double* h_out, uint64_t* steps_out,
+                int32_t* happy_out) { /* solvers.hpp:125-151 */
+  const uint64_t n = a->n;
+  if (m < 1) return ORC_EINVAL;
+  const double nv = norm2(n, v1);
+  if (!(nv > 0.0)) return ORC_EINVAL;
+  orc_counter c = {0, 0, 0, 0, 0};
+  double** q = (double**)xcalloc((size_t)m + 2, sizeof(double*));
+  double* cols = (double*)xcalloc((size_t)((m + 1) * m), sizeof(double));
+  q[0] = (double*)xcalloc((size_t)n, sizeof(double));
+  memcpy(q[0], v1, (size_t)n * sizeof(double));
+  scale(n, 1.0 / nv, q[0]);
+  uint64_t nq = 1, steps = 0;
+  int happy = 0;
+  for (uint64_t j = 0; j < m; ++j) {
+    double* col = cols + j * (m + 1);
+    happy = arnoldi_step(a, q, &nq, col, &c);
+    ++steps;
+    if (happy) break;
+  }
+  memset(h_out, 0, (size_t)((m + 1) * m) * sizeof(double));
+  for (uint64_t j = 0; j < steps; ++j)
+    for (uint64_t i = 0; i <= j + 1 && i <= steps; ++i) h_out[i * m + j] = cols[j * (m + 1) + i];
+  *steps_out = steps;
+  *happy_out = happy;
+  for (uint64_t i = 0; i < nq; ++i) free(q[i]);
+  free(q);
+  free(cols);
+  return 0;
+}
+
+/* solvers.hpp:155-187 */
+int orc_mr_solve(const orc_csr* a, const double* f, double* x, const orc_solver_cfg* cfg,
+                 orc_report* rep) {
+  const uint64_t n = a->n;
+  orc_counter* c = &rep->op_counts;
+  double* r = (double*)xcalloc((size_t)n, sizeof(double));
+  double* ar = (double*)xcalloc((size_t)n, sizeof(double));
+  initial_residual(a, f, x, r, c);
+  double rn = checked_norm(n, r, c);
+  push_d(&rep->history, &rep->n_history, rn);
+  c->stored_vectors = 3;
+  push_c(&rep->op_history, &rep->n_op_history, *c);
+  while (rn > cfg->tol && rep->iterations < cfg->max_iterations) {
+    orc_spmv(a, r, ar);
+    ++c->matvecs;
+    const double den = orc_dot(n, ar, ar);
+    const double num = orc_dot(n, r, ar);
+    c->dotprods += 2;
+    if (den == 0.0) {
+      set_breakdown(rep, "stagnation: A r vanished while r is nonzero");
+      break;
+    }
+    const double al = num / den;
+    axpy(n, al, r, x);
+    axpy(n, -al, ar, r);
+    c->vec_updates += 2;
+    ++rep->iterations;
+    rn = checked_norm(n, r, c);
+    push_d(&rep->history, &rep->n_history, rn);
+    push_c(&rep->op_history, &rep->n_op_history, *c);
+  }
+  rep->converged = rn <= cfg->tol;
+  rep->final_residual = rep->history[rep->n_history - 1];
+  free(r);
+  free(ar);
+  return 0;
+}
+
+/* solvers.hpp:193-291 Orthomin(k)/GCR with a ring of directions */
+int orc_omin_solve(const orc_csr* a, const double* f, double* x, const orc_solver_cfg* cfg,
+                   orc_report* rep) {
+  orc_err e = {0, ""};
+  const int gcr = cfg->method == 2;
+  if (!(gcr || cfg->k >= 1)) {
+    snprintf(rep->error, sizeof rep->error, "omin: window k must be at least 1");
+    return ORC_EINVAL;
+  }
+  const uint64_t n = a->n;
+  orc_counter* c = &rep->op_counts;
+  rep->steady_iteration = gcr ? cfg->max_iterations + 1 : cfg->k;
+  double* r = (double*)xcalloc((size_t)n, sizeof(double));
+  initial_residual(a, f, x, r, c);
+  const double r0n = checked_norm(n, r, c);
+  double rn = r0n;
+  push_d(&rep->history, &rep->n_history, rn);
+
+  /* window as a growable deque: arrays of pointers, head index */
+  uint64_t cap = 16, head = 0, size = 0, peak = 0;
+  double** P = (double**)xcalloc((size_t)cap, sizeof(double*));
+  double** AP = (double**)xcalloc((size_t)cap, sizeof(double*));
+  double* apap = (double*)xcalloc((size_t)cap, sizeof(double));
+#define WIN(i) ((head + (i)) % cap)
+  if (rn > cfg->tol) {
+    P[0] = (double*)xcalloc((size_t)n, sizeof(double));
+    AP[0] = (double*)xcalloc((size_t)n, sizeof(double));
+    memcpy(P[0], r, (size_t)n * sizeof(double));
+    orc_spmv(a, P[0], AP[0]);
+    ++c->matvecs;
+    apap[0] = orc_dot(n, AP[0], AP[0]);
+    ++c->dotprods;
+    size = 1;
+    peak = 1;
+  }
+  push_c(&rep->op_history, &rep->n_op_history, *c);
+  double* b = NULL;
+  while (rn > cfg->tol && rep->iterations < cfg->max_iterations) {
+    const uint64_t cur = WIN(size - 1);
+    if (apap[cur] == 0.0) {
+      set_breakdown(rep, "breakdown: (A p)^T (A p) vanished");
+      break;
+    }
+    const double num = orc_dot(n, r, AP[cur]);
+    ++c->dotprods;
+    const double al = num / apap[cur];
+    axpy(n, al, P[cur], x);
+    axpy(n, -al, AP[cur], r);
+    c->vec_updates += 2;
+    ++rep->iterations;
+    rn = checked_norm(n, r, c);
+    push_d(&rep->history, &rep->n_history, rn);
+    if (rn <= cfg->tol) break;
+    if (rn > cfg->divergence_factor * r0n) {
+      char num_s[64], msg[256];
+      fmt_double(num_s, sizeof num_s, cfg->divergence_factor);
+      snprintf(msg, sizeof msg, "divergence: residual grew beyond %sx the initial norm", num_s);
+      set_breakdown(rep, msg);
+      break;
+    }
+    if (rep->iterations >= cfg->max_iterations) break;
+
+    double* ar = (double*)xcalloc((size_t)n, sizeof(double));
+    orc_spmv(a, r, ar);
+    ++c->matvecs;
+    b = (double*)realloc(b, (size_t)(size + 1) * sizeof(double));
+    for (uint64_t j = 0; j < size; ++j) b[j] = orc_dot(n, ar, AP[WIN(j)]);
+    c->dotprods += size;
+    double* np = (double*)xcalloc((size_t)n, sizeof(double));
+    memcpy(np, r, (size_t)n * sizeof(double));
+    double* nap = ar;
+    for (uint64_t j = 0; j < size; ++j) {
+      const double coef = -(b[j] / apap[WIN(j)]);
+      axpy(n, coef, P[WIN(j)], np);
+      axpy(n, coef, AP[WIN(j)], nap);
+    }
+    c->vec_updates += 2 * size;
+    const double napap = orc_dot(n, nap, nap);
+    ++c->dotprods;
+    if (cfg->debug_checks) {
+      const double nn = norm2(n, nap);
+      for (uint64_t j = 0; j < size; ++j) {
+        const double cross = fabs(orc_dot(n, nap, AP[WIN(j)]));
+        if (cross > 1e-8 * nn * norm2(n, AP[WIN(j)])) {
+          err_set(&e, ORC_ELOGIC, "omin: window A-direction orthogonality lost");
+          goto fail;
+        }
+      }
+      if (rep->iterations % 10 == 0) {
+        double* tr = (double*)xcalloc((size_t)n, sizeof(double));
+        orc_spmv(a, x, tr);
+        for (uint64_t i = 0; i < n; ++i) tr[i] = f[i] - tr[i];
+        axpy(n, -1.0, r, tr);
+        const int bad = norm2(n, tr) > 1e-9 * norm2(n, f);
+        free(tr);
+        if (bad) {
+          err_set(&e, ORC_ELOGIC, "omin: recursive residual drifted from f - A x");
+          goto fail;
+        }
+      }
+    }
+    /* push_back; grow ring if needed */
+    if (size == cap) {
+      uint64_t ncap = cap * 2;
+      double** nP = (double**)xcalloc((size_t)ncap, sizeof(double*));
+      double** nAP = (double**)xcalloc((size_t)ncap, sizeof(double*));
+      double* nq = (double*)xcalloc((size_t)ncap, sizeof(double));
+      for (uint64_t j = 0; j < size; ++j) {
+        nP[j] = P[WIN(j)];
+        nAP[j] = AP[WIN(j)];
+        nq[j] = apap[WIN(j)];
+      }
+      free(P);
+      free(AP);
+      free(apap);
+      P = nP;
+      AP = nAP;
+      apap = nq;
+      cap = ncap;
+      head = 0;
+    }
+    {
+      const uint64_t slot = WIN(size);
+      P[slot] = np;
+      AP[slot] = nap;
+      apap[slot] = napap;
+      ++size;
+    }
+    if (size > peak) peak = size;
+    if (!gcr && size > cfg->k) {
+      free(P[head]);
+      free(AP[head]);
+      P[head] = AP[head] = NULL;
+      head = (head + 1) % cap;
+      --size;
+    }
+    push_c(&rep->op_history, &rep->n_op_history, *c);
+  }
+  c->stored_vectors = 2 + 2 * peak;
+  rep->converged = rn <= cfg->tol;
+  rep->final_residual = rep->history[rep->n_history - 1];
+fail:
+  for (uint64_t j = 0; j < size; ++j) {
+    free(P[WIN(j)]);
+    free(AP[WIN(j)]);
+  }
+#undef WIN
+  free(P);
+  free(AP);
+  free(apap);
+  free(b);
+  free(r);
+  if (e.code) snprintf(rep->error, sizeof rep->error, "%s", e.msg);
+  return e.code;
+}
+
+/* solvers.hpp:297-359 restarted MGS-GMRES(m) */
+int orc_gmres_solve(const orc_csr* a, const double* f, double* x, const orc_solver_cfg* cfg,
+                    orc_report* rep) {
+  orc_err e = {0, ""};
+  if (!(cfg->m >= 1)) {
+    snprintf(rep->error, sizeof rep->error, "gmres: restart length m must be at least 1");
+    return ORC_EINVAL;
+  }
+  const uint64_t m = cfg->m, n = a->n;
+  orc_counter* c = &rep->op_counts;
+  c->stored_vectors = m + 4;
+  double* r = (double*)xcalloc((size_t)n, sizeof(double));
+  double* ax = (double*)xcalloc((size_t)n, sizeof(double));
+  double** q = (double**)xcalloc((size_t)m + 2, sizeof(double*));
+  double* col = (double*)xcalloc((size_t)m + 2, sizeof(double));
+  double* y = (double*)xcalloc((size_t)m + 1, sizeof(double));
+  initial_residual(a, f, x, r, c);
+  double rn = checked_norm(n, r, c);
+  push_d(&rep->history, &rep->n_history, rn);
+  push_c(&rep->op_history, &rep->n_op_history, *c);
+  while (rn > cfg->tol && rep->iterations < cfg->max_iterations) {
+    uint64_t nq = 1;
+    q[0] = (double*)xcalloc((size_t)n, sizeof(double));
+    memcpy(q[0], r, (size_t)n * sizeof(double));
+    scale(n, 1.0 / rn, q[0]);
+    ++c->vec_updates;
+    hlsq_t lsq;
+    hlsq_init(&lsq, rn, m);
+    int happy = 0;
+    uint64_t inner = 0;
+    while (inner < m && rep->iterations < cfg->max_iterations) {
+      int h = arnoldi_step(a, q, &nq, col, c);
+      ++inner;
+      ++rep->iterations;
+      const double rho = hlsq_append(&lsq, col);
+      if (h) {
+        happy = 1;
+        break;
+      }
+      if (rho <= cfg->tol) break;
+    }
+    int st = hlsq_solve(&lsq, y, &e);
+    if (st) {
+      set_breakdown(rep, e.msg);
+      e.code = 0;
+      hlsq_free(&lsq);
+      for (uint64_t i = 0; i < nq; ++i) free(q[i]);
+      break;
+    }
+    for (uint64_t i = 0; i < lsq.cols; ++i) axpy(n, y[i], q[i], x);
+    c->vec_updates += lsq.cols;
+    hlsq_free(&lsq);
+    for (uint64_t i = 0; i < nq; ++i) free(q[i]);
+    orc_spmv(a, x, ax);
+    ++c->matvecs;
+    for (uint64_t i = 0; i < n; ++i) r[i] = f[i] - ax[i];
+    ++c->vec_updates;
+    ++rep->cycles;
+    rn = checked_norm(n, r, c);
+    push_d(&rep->history, &rep->n_history, rn);
+    if (inner == m && !happy) push_c(&rep->op_history, &rep->n_op_history, *c);
+    if (happy && rn > cfg->tol) {
+      set_breakdown(rep, "happy breakdown but residual above threshold");
+      break;
+    }
+  }
+  rep->converged = rn <= cfg->tol;
+  rep->final_residual = rep->history[rep->n_history - 1];
+  free(r);
+  free(ax);
+  free(q);
+  free(col);
+  free(y);
+  return 0;
+}
+
+/* ------------------------------------------------------------------ */
+/* sstep.hpp:62-67 */
+static int validate_block_size(const orc_sstep_cfg* cfg, orc_report* rep, orc_err* e) {
+  if (!(cfg->s >= 1 && cfg->s <= 8)) {
+    err_set(e, ORC_EINVAL, "s-step: s must be in 1..8");
+    return e->code;
+  }
+  if (cfg->s > 5) {
+    char msg[256];
+    snprintf(msg, sizeof msg, "s=%llu exceeds the stability guideline of 5; expect basis collapse",
+             (unsigned long long)cfg->s);
+    add_note(rep, msg);
+  }
+  return 0;
+}
+
+/* sstep.hpp:71-81: R = [v, ..., A^{s-1} v], AR = [A v, ..., A^s v] */
+static void krylov_pair(const orc_csr* a, const double* v, uint64_t s, double* R, double* AR,
+                        orc_counter* c) {
+  const uint64_t n = a->n;
+  orc_krylov_block(a, v, s, R);
+  c->matvecs += s - 1;
+  for (uint64_t j = 0; j + 1 < s; ++j) memcpy(AR + j * n, R + (j + 1) * n, (size_t)n * sizeof(double));
+  orc_spmv(a, R + (s - 1) * n, AR + (s - 1) * n);
+  ++c->matvecs;
+}
+
+/* sstep.hpp:89-106 */
+static int smr_step_impl(const orc_csr* a, double* x, double* r, uint64_t s, double* coeffs,
+                         orc_counter* c, orc_err* e) {
+  const uint64_t n = a->n;
+  if (!(s >= 1)) {
+    err_set(e, ORC_EINVAL, "smr_step: s must be at least 1");
+    return e->code;
+  }
+  double* R = (double*)xcalloc((size_t)(n * s), sizeof(double));
+  double* AR = (double*)xcalloc((size_t)(n * s), sizeof(double));
+  double w[GMAX * GMAX], mvec[GMAX], av[GMAX];
+  krylov_pair(a, r, s, R, AR, c);
+  block_gram_self(n, AR, s, w);
+  c->dotprods += s * (s + 1) / 2;
+  block_dot(n, AR, s, r, mvec);
+  c->dotprods += s;
+  gram_t g;
+  int st = gram_init(&g, s, w, e);
+  if (!st) {
+    gram_solve_vec(&g, mvec, av);
+    for (uint64_t l = 0; l < s; ++l) axpy(n, av[l], R + l * n, x);
+    for (uint64_t l = 0; l < s; ++l) axpy(n, -av[l], AR + l * n, r);
+    c->vec_updates += 2 * s;
+    if (coeffs) memcpy(coeffs, av, (size_t)s * sizeof(double));
+  }
+  free(R);
+  free(AR);
+  return st;
+}
+
+int orc_smr_step(const orc_csr* a, double* x, double* r, uint64_t s, double* coeffs_out, orc_counter* c) {
+  orc_err e = {0, ""};
+  orc_counter local = {0, 0, 0, 0, 0};
+  return smr_step_impl(a, x, r, s, coeffs_out, c ? c : &local, &e);
+}
+
+/* sstep.hpp:109-135 */
+int orc_smr_solve(const orc_csr* a, const double* f, double* x, const orc_sstep_cfg* cfg,
+                  orc_report* rep) {
+  orc_err e = {0, ""};
+  if (validate_block_size(cfg, rep, &e)) {
+    snprintf(rep->error, sizeof rep->error, "%s", e.msg);
+    return e.code;
+  }
+  const uint64_t n = a->n;
+  orc_counter* c = &rep->op_counts;
+  double* r = (double*)xcalloc((size_t)n, sizeof(double));
+  initial_residual(a, f, x, r, c);
+  double rn = checked_norm(n, r, c);
+  push_d(&rep->history, &rep->n_history, rn);
+  c->stored_vectors = 2 + 2 * cfg->s;
+  push_c(&rep->op_history, &rep->n_op_history, *c);
+  while (rn > cfg->tol && rep->iterations < cfg->max_iterations) {
+    int st = smr_step_impl(a, x, r, cfg->s, NULL, c, &e);
+    if (st == ORC_EBREAK) {
+      char msg[512];
+      snprintf(msg, sizeof msg, "basis collapse at iteration %llu (%s); reduce s",
+               (unsigned long long)rep->iterations, e.msg);
+      set_breakdown(rep, msg);
+      e.code = 0;
+      break;
+    }
+    ++rep->iterations;
+    rn = checked_norm(n, r, c);
+    push_d(&rep->history, &rep->n_history, rn);
+    push_c(&rep->op_history, &rep->n_op_history, *c);
+  }
+  rep->converged = rn <= cfg->tol;
+  rep->final_residual = rep->history[rep->n_history - 1];
+  free(r);
+  return 0;
+}
+
+/* sstep.hpp:142-249 s-step Orthomin(k) / s-GCR */
+typedef struct {
+  double *p, *ap;
+  gram_t w;
+} somin_entry;
+
+int orc_somin_solve(const orc_csr* a, const double* f, double* x, const orc_sstep_cfg* cfg,
+                    orc_report* rep) {
+  orc_err e = {0, ""};
+  const int gcr = cfg->unbounded_window != 0;
+  if (!(gcr || cfg->k >= 1)) {
+    snprintf(rep->error, sizeof rep->error, "s-omin: window k must be at least 1");
+    return ORC_EINVAL;
+  }
+  if (validate_block_size(cfg, rep, &e)) {
+    snprintf(rep->error, sizeof rep->error, "%s", e.msg);
+    return e.code;
+  }
+  const uint64_t n = a->n, s = cfg->s;
+  orc_counter* c = &rep->op_counts;
+  rep->steady_iteration = gcr ? cfg->max_iterations + 1 : cfg->k;
+
+  double* r = (double*)xcalloc((size_t)n, sizeof(double));
+  initial_residual(a, f, x, r, c);
+  const double r0n = checked_norm(n, r, c);
+  double rn = r0n;
+  push_d(&rep->history, &rep->n_history, rn);
+
+  uint64_t cap = 16, head = 0, size = 0, peak = 0;
+  somin_entry* win = (somin_entry*)xcalloc((size_t)cap, sizeof(somin_entry));
+#define SW(i) (&win[(head + (i)) % cap])
+  double wmat[GMAX * GMAX], mvec[GMAX], av[GMAX];
+  double* cj = (double*)xcalloc((size_t)(s * s), sizeof(double));
+  double* bcoef = NULL;
+
+  if (rn > cfg->tol) {
+    double* R = (double*)xcalloc((size_t)(n * s), sizeof(double));
+    double* AR = (double*)xcalloc((size_t)(n * s), sizeof(double));
+    krylov_pair(a, r, s, R, AR, c);
+    block_gram_self(n, AR, s, wmat);
+    c->dotprods += s * (s + 1) / 2;
+    if (gram_init(&win[0].w, s, wmat, &e)) {
+      char msg[512];
+      snprintf(msg, sizeof msg, "basis collapse at setup (%s)", e.msg);
+      set_breakdown(rep, msg);
+      e.code = 0;
+      push_c(&rep->op_history, &rep->n_op_history, *c);
+      rep->converged = 0;
+      rep->final_residual = rn;
+      free(R);
+      free(AR);
+      goto done;
+    }
+    win[0].p = R;
+    win[0].ap = AR;
+    size = 1;
+    peak = 1;
+  }
+  push_c(&rep->op_history, &rep->n_op_history, *c);
+
+  while (rn > cfg->tol && rep->iterations < cfg->max_iterations && !rep->has_breakdown) {
+    {
+      const somin_entry* cur = SW(size - 1);
+      block_dot(n, cur->ap, s, r, mvec);
+      c->dotprods += s;
+      gram_solve_vec(&cur->w, mvec, av);
+      for (uint64_t l = 0; l < s; ++l) axpy(n, av[l], cur->p + l * n, x);
+      for (uint64_t l = 0; l < s; ++l) axpy(n, -av[l], cur->ap + l * n, r);
+      c->vec_updates += 2 * s;
+    }
+    ++rep->iterations;
+    rn = checked_norm(n, r, c);
+    push_d(&rep->history, &rep->n_history, rn);
+    if (rn <= cfg->tol) break;
+    if (rn > cfg->divergence_factor * r0n) {
+      char num_s[64], msg[256];
+      fmt_double(num_s, sizeof num_s, cfg->divergence_factor);
+      snprintf(msg, sizeof msg, "divergence: residual grew beyond %sx the initial norm", num_s);
+      set_breakdown(rep, msg);
+      break;
+    }
+    if (rep->iterations >= cfg->max_iterations) break;
+
+    double* R = (double*)xcalloc((size_t)(n * s), sizeof(double));
+    double* AR = (double*)xcalloc((size_t)(n * s), sizeof(double));
+    krylov_pair(a, r, s, R, AR, c);
+    /* Scalar2 against the pristine A R block (sstep.hpp:204-214) */
+    bcoef = (double*)realloc(bcoef, (size_t)(size * s * s) * sizeof(double));
+    for (uint64_t wi = 0; wi < size; ++wi) {
+      const somin_entry* en = SW(wi);
+      block_gram(n, en->ap, s, AR, s, cj);
+      c->dotprods += s * s;
+      double* bj = bcoef + wi * s * s;
+      gram_solve_mat(&en->w, s, cj, bj);
+      for (uint64_t i = 0; i < s * s; ++i) bj[i] = -bj[i];
+    }
+    for (uint64_t wi = 0; wi < size; ++wi) {
+      const somin_entry* en = SW(wi);
+      block_axpy_inplace(n, R, en->p, s, bcoef + wi * s * s);
+      block_axpy_inplace(n, AR, en->ap, s, bcoef + wi * s * s);
+      c->vec_updates += 2 * s * s;
+    }
+    block_gram_self(n, AR, s, wmat);
+    c->dotprods += s * (s + 1) / 2;
+    if (cfg->debug_checks) { /* sstep.hpp:225-233 */
+      const double nn = sqrt(mat_trace(s, s, wmat));
+      double cross[GMAX * GMAX], wj[GMAX * GMAX];
+      for (uint64_t wi = 0; wi < size; ++wi) {
+        const somin_entry* en = SW(wi);
+        block_gram(n, en->ap, s, AR, s, cross);
+        block_gram_self(n, en->ap, s, wj);
+        if (mat_frob(s * s, cross) > 1e-7 * nn * sqrt(mat_trace(s, s, wj))) {
+          err_set(&e, ORC_ELOGIC, "s-omin: block A-direction orthogonality lost");
+          free(R);
+          free(AR);
+          goto done;
+        }
+      }
+    }
+    gram_t gnew;
+    if (gram_init(&gnew, s, wmat, &e)) {
+      char msg[512];
+      snprintf(msg, sizeof msg, "basis collapse at iteration %llu (%s)",
+               (unsigned long long)rep->iterations, e.msg);
+      set_breakdown(rep, msg);
+      e.code = 0;
+      free(R);
+      free(AR);
+      break;
+    }
+    if (size == cap) { /* grow ring (s-GCR) */
+      uint64_t ncap = cap * 2;
+      somin_entry* nw = (somin_entry*)xcalloc((size_t)ncap, sizeof(somin_entry));
+      for (uint64_t j = 0; j < size; ++j) nw[j] = *SW(j);
+      free(win);
+      win = nw;
+      cap = ncap;
+      head = 0;
+    }
+    {
+      somin_entry* slot = SW(size);
+      slot->p = R;
+      slot->ap = AR;
+      slot->w = gnew;
+      ++size;
+    }
+    if (size > peak) peak = size;
+    if (!gcr && size > cfg->k) {
+      free(win[head].p);
+      free(win[head].ap);
+      win[head].p = win[head].ap = NULL;
+      head = (head + 1) % cap;
+      --size;
+    }
+    push_c(&rep->op_history, &rep->n_op_history, *c);
+  }
+  c->stored_vectors = 2 + 2 * s * peak;
+  rep->converged = rn <= cfg->tol;
+  rep->final_residual = rep->history[rep->n_history - 1];
+done:
+  for (uint64_t j = 0; j < size; ++j) {
+    free(SW(j)->p);
+    free(SW(j)->ap);
+  }
+#undef SW
+  free(win);
+  free(cj);
+  free(bcoef);
+  free(r);
+  if (e.code) snprintf(rep->error, sizeof rep->error, "%s", e.msg);
+  return e.code;
+}
+
+/* ------------------------------------------------------------------ */
+/* sstep.hpp:271-458 incremental s-step Arnoldi engine */
+typedef struct {
+  const orc_csr* a;
+  uint64_t s, n, cap_blocks;
+  orc_counter* c;
+  double orth_tol;
+  uint64_t nblocks;
+  double** blocks;  /* n*s each */
+  double* grams;    /* cap_blocks * s*s */
+  gram_t* solvers;
+  double** tco;     /* per block: (#earlier blocks) * s*s, NULL for block 0 */
+  uint64_t ngcols;
+  double** gcols;
+  uint64_t* glen;
+  double* seed;
+  double seed_norm;
+} sarn_t;
+
+static int sarn_push_block(sarn_t* E, double* b, orc_err* e) { /* :392-399 */
+  const uint64_t s = E->s;
+  double w[GMAX * GMAX];
+  block_gram_self(E->n, b, s, w);
+  E->c->dotprods += s * (s + 1) / 2;
+  gram_t g;
+  if (gram_init(&g, s, w, e)) return e->code;
+  E->blocks[E->nblocks] = b;
+  memcpy(E->grams + E->nblocks * s * s, w, (size_t)(s * s) * sizeof(double));
+  E->solvers[E->nblocks] = g;
+  ++E->nblocks;
+  return 0;
+}
+
+static int sarn_init(sarn_t* E, const orc_csr* a, const double* v1, uint64_t s, uint64_t cap_blocks,
+                     orc_counter* c, orc_err* e) { /* :273-285 */
+  memset(E, 0, sizeof *E);
+  E->a = a;
+  E->s = s;
+  E->n = a->n;
+  E->c = c;
+  E->orth_tol = 1e-8;
+  E->cap_blocks = cap_blocks;
+  const uint64_t n = a->n;
+  E->blocks = (double**)xcalloc((size_t)cap_blocks + 1, sizeof(double*));
+  E->grams = (double*)xcalloc((size_t)((cap_blocks + 1) * s * s), sizeof(double));
+  E->solvers = (gram_t*)xcalloc((size_t)cap_blocks + 1, sizeof(gram_t));
+  E->tco = (double**)xcalloc((size_t)cap_blocks + 1, sizeof(double*));
+  E->gcols = (double**)xcalloc((size_t)((cap_blocks + 1) * s), sizeof(double*));
+  E->glen = (uint64_t*)xcalloc((size_t)((cap_blocks + 1) * s), sizeof(uint64_t));
+  E->seed = (double*)xcalloc((size_t)n, sizeof(double));
+  const double nv = norm2(n, v1);
+  if (!(nv > 0.0)) {
+    err_set(e, ORC_EINVAL, "s-arnoldi: start vector is zero");
+    return e->code;
+  }
+  double* v = (double*)xcalloc((size_t)n, sizeof(double));
+  memcpy(v, v1, (size_t)n * sizeof(double));
+  scale(n, 1.0 / nv, v);
+  ++c->vec_updates;
+  double* b = (double*)xcalloc((size_t)(n * s), sizeof(double));
+  orc_krylov_block(a, v, s, b);
+  free(v);
+  c->matvecs += s - 1;
+  if (sarn_push_block(E, b, e)) {
+    free(b);
+    return e->code;
+  }
+  E->tco[0] = NULL;
+  return 0;
+}
+
+static void sarn_free(sarn_t* E) {
+  for (uint64_t i = 0; i < E->nblocks; ++i) free(E->blocks[i]);
+  for (uint64_t i = 0; i <= E->cap_blocks; ++i) free(E->tco[i]);
+  for (uint64_t i = 0; i < E->ngcols; ++i) free(E->gcols[i]);
+  free(E->blocks);
+  free(E->grams);
+  free(E->solvers);
+  free(E->tco);
+  free(E->gcols);
+  free(E->glen);
+  free(E->seed);
+}
+
+/* :401-414 */
+static int sarn_needs_reorth(sarn_t* E, const double* cand) {
+  const uint64_t s = E->s, n = E->n;
+  double cn2 = 0.0;
+  for (uint64_t jc = 0; jc < s; ++jc) cn2 += orc_dot(n, cand + jc * n, cand + jc * n);
+  E->c->dotprods += s;
+  double cross[GMAX * GMAX];
+  for (uint64_t i = 0; i < E->nblocks; ++i) {
+    block_gram(n, E->blocks[i], s, cand, s, cross);
+    E->c->dotprods += s * s;
+    if (mat_frob(s * s, cross) > E->orth_tol * sqrt(mat_trace(s, s, E->grams + i * s * s)) * sqrt(cn2))
+      return 1;
+  }
+  return 0;
+}
+
+/* :422-445 */
+static void sarn_append_g(sarn_t* E, uint64_t k, const double* hcoef /* k*s */, double nu) {
+  const uint64_t s = E->s, q = k - 1;
+  const double* tq = E->tco[q];
+  const uint64_t ntq = q; /* block q was orthogonalized against blocks 0..q-1 */
+  for (uint64_t cloc = 0; cloc + 1 < s; ++cloc) {
+    const uint64_t len = q * s + cloc + 2;
+    double* col = (double*)xcalloc((size_t)len, sizeof(double));
+    col[q * s + cloc + 1] += 1.0;
+    for (uint64_t i = 0; i < ntq && tq; ++i) {
+      const double* ti = tq + i * s * s;
+      for (uint64_t l = 0; l < s; ++l) col[i * s + l] += ti[l * s + cloc + 1];
+      for (uint64_t lc = 0; lc < s; ++lc) {
+        const double coef = ti[lc * s + cloc];
+        if (coef == 0.0) continue;
+        const double* prev = E->gcols[i * s + lc];
+        const uint64_t plen = E->glen[i * s + lc];
+        for (uint64_t row = 0; row < plen; ++row) col[row] -= coef * prev[row];
+      }
+    }
+    E->gcols[E->ngcols] = col;
+    E->glen[E->ngcols] = len;
+    ++E->ngcols;
+  }
+  const uint64_t len = k * s + 1;
+  double* last = (double*)xcalloc((size_t)len, sizeof(double));
+  for (uint64_t i = 0; i < k; ++i)
+    for (uint64_t l = 0; l < s; ++l) last[i * s + l] = hcoef[i * s + l];
+  last[k * s] = nu;
+  E->gcols[E->ngcols] = last;
+  E->glen[E->ngcols] = len;
+  ++E->ngcols;
+}
+
+/* :297-379 one block iteration; returns 1 (more), 0 (invariant), <0 on error (e set) */
+static int sarn_advance(sarn_t* E, int build_next, orc_err* e) {
+  const uint64_t k = E->nblocks, s = E->s, n = E->n;
+  orc_counter* c = E->c;
+  double* z = (double*)xcalloc((size_t)n, sizeof(double));
+  orc_spmv(E->a, E->blocks[k - 1] + (s - 1) * n, z);
+  ++c->matvecs;
+  const double zn = norm2(n, z);
+  double* hcoef = (double*)xcalloc((size_t)(k * s), sizeof(double));
+  double rhs[GMAX];
+  for (uint64_t i = 0; i < k; ++i) {
+    block_dot(n, E->blocks[i], s, z, rhs);
+    c->dotprods += s;
+    gram_solve_vec(&E->solvers[i], rhs, hcoef + i * s);
+  }
+  double* seed = z;
+  for (uint64_t i = 0; i < k; ++i)
+    for (uint64_t l = 0; l < s; ++l) axpy(n, -hcoef[i * s + l], E->blocks[i] + l * n, seed);
+  c->vec_updates += k * s;
+  const double nu = norm2(n, seed);
+  ++c->dotprods;
+  sarn_append_g(E, k, hcoef, nu);
+  free(hcoef);
+  if (nu <= 1e-14 * zn) {
+    memset(E->seed, 0, (size_t)n * sizeof(double));
+    E->seed_norm = 0.0;
+    free(seed);
+    return 0;
+  }
+  scale(n, 1.0 / nu, seed);
+  ++c->vec_updates;
+  memcpy(E->seed, seed, (size_t)n * sizeof(double));
+  E->seed_norm = nu;
+  free(seed);
+
+  double* cand = (double*)xcalloc((size_t)(n * s), sizeof(double));
+  orc_krylov_block(E->a, E->seed, s, cand);
+  c->matvecs += s - 1;
+  if (build_next) {
+    double* tacc = (double*)xcalloc((size_t)(k * s * s), sizeof(double));
+    double rhsm[GMAX * GMAX], t[GMAX * GMAX], d[GMAX];
+    for (uint64_t i = 0; i < k; ++i) {
+      const uint64_t nc = s > 1 ? s - 1 : 0;
+      for (uint64_t jc = 1; jc < s; ++jc) {
+        block_dot(n, E->blocks[i], s, cand + jc * n, d);
+        c->dotprods += s;
+        for (uint64_t l = 0; l < s; ++l) rhsm[l * nc + (jc - 1)] = d[l];
+      }
+      if (s > 1) {
+        gram_solve_mat(&E->solvers[i], nc, rhsm, t);
+        for (uint64_t jc = 1; jc < s; ++jc)
+          for (uint64_t l = 0; l < s; ++l) {
+            axpy(n, -t[l * nc + (jc - 1)], E->blocks[i] + l * n, cand + jc * n);
+            tacc[i * s * s + l * s + jc] = t[l * nc + (jc - 1)];
+          }
+        c->vec_updates += s * (s - 1);
+      }
+    }
+    if (s > 1 && sarn_needs_reorth(E, cand)) {
+      const uint64_t nc = s - 1;
+      for (uint64_t i = 0; i < k; ++i) {
+        for (uint64_t jc = 1; jc < s; ++jc) {
+          block_dot(n, E->blocks[i], s, cand + jc * n, d);
+          c->dotprods += s;
+          for (uint64_t l = 0; l < s; ++l) rhsm[l * nc + (jc - 1)] = d[l];
+        }
+        gram_solve_mat(&E->solvers[i], nc, rhsm, t);
+        for (uint64_t jc = 1; jc < s; ++jc)
+          for (uint64_t l = 0; l < s; ++l) {
+            axpy(n, -t[l * nc + (jc - 1)], E->blocks[i] + l * n, cand + jc * n);
+            tacc[i * s * s + l * s + jc] += t[l * nc + (jc - 1)];
+          }
+        c->vec_updates += s * (s - 1);
+      }
+    }
+    if (sarn_push_block(E, cand, e)) {
+      free(cand);
+      free(tacc);
+      return -1;
+    }
+    E->tco[k] = tacc;
+  } else {
+    free(cand);
+  }
+  return 1;
+}
+
+int orc_sarnoldi(const orc_csr* a, const double* v1, uint64_t s, uint64_t m_blocks, double* blocks_out,
+                 double* grams_out, double* hess_out, double* seed_out, double* seed_norm_out,
+                 orc_counter* counter, char* err, uint64_t errcap) { /* :465-485 */
+  orc_err e = {0, ""};
+  const uint64_t n = a->n;
+  if (!(s >= 1)) { err_set(&e, ORC_EINVAL, "sarnoldi: s must be at least 1"); goto out0; }
+  if (!(m_blocks >= 1)) { err_set(&e, ORC_EINVAL, "sarnoldi: m_blocks must be at least 1"); goto out0; }
+  if (!(s * m_blocks <= n)) { err_set(&e, ORC_EINVAL, "sarnoldi: s * m_blocks exceeds the dimension"); goto out0; }
+  if (s > GMAX) { err_set(&e, ORC_EINVAL, "sarnoldi: s exceeds the oracle's limit"); goto out0; }
+  {
+    orc_counter local = {0, 0, 0, 0, 0};
+    orc_counter* c = counter ? counter : &local;
+    sarn_t E;
+    if (sarn_init(&E, a, v1, s, m_blocks, c, &e)) {
+      sarn_free(&E);
+      goto out0;
+    }
+    for (uint64_t k = 1; k <= m_blocks; ++k) {
+      int more = sarn_advance(&E, k < m_blocks, &e);
+      if (more < 0) break;
+      if (more == 0) {
+        err_set(&e, ORC_EBREAK, "sarnoldi: invariant subspace at block %llu", (unsigned long long)k);
+        break;
+      }
+    }
+    if (!e.code) {
+      for (uint64_t b = 0; b < E.nblocks; ++b) memcpy(blocks_out + b * n * s, E.blocks[b], (size_t)(n * s) * sizeof(double));
+      memcpy(grams_out, E.grams, (size_t)(E.nblocks * s * s) * sizeof(double));
+      const uint64_t kc = E.ngcols / s, rows = (kc + 1) * s, cols = kc * s;
+      memset(hess_out, 0, (size_t)(rows * cols) * sizeof(double));
+      for (uint64_t j = 0; j < E.ngcols; ++j)
+        for (uint64_t i = 0; i < E.glen[j]; ++i) hess_out[i * cols + j] = E.gcols[j][i];
+      memcpy(seed_out, E.seed, (size_t)n * sizeof(double));
+      *seed_norm_out = E.seed_norm;
+    }
+    sarn_free(&E);
+  }
+out0:
+  if (e.code && err) snprintf(err, errcap, "%s", e.msg);
+  return e.code;
+}
+
+/* sstep.hpp:493-654 restarted s-step GMRES(m) */
+int orc_sgmres_solve(const orc_csr* a, const double* f, double* x, const orc_sstep_cfg* cfg,
+                     orc_report* rep) {
+  orc_err e = {0, ""};
+  if (!(cfg->m >= 1)) {
+    snprintf(rep->error, sizeof rep->error, "s-gmres: m must be at least 1");
+    return ORC_EINVAL;
+  }
+  if (validate_block_size(cfg, rep, &e)) {
+    snprintf(rep->error, sizeof rep->error, "%s", e.msg);
+    return e.code;
+  }
+  if (cfg->s == 1) { /* :498-508 */
+    orc_solver_cfg sc = {3, 4, cfg->m, cfg->tol, cfg->max_iterations, 0, cfg->debug_checks, 10.0};
+    int nn = rep->n_notes;
+    char notes[4][256];
+    memcpy(notes, rep->notes, sizeof notes);
+    int st = orc_gmres_solve(a, f, x, &sc, rep);
+    rep->n_notes = nn;
+    memcpy(rep->notes, notes, sizeof notes);
+    return st;
+  }
+  const uint64_t s = cfg->s, m = cfg->m, n = a->n;
+  orc_counter* c = &rep->op_counts;
+  c->stored_vectors = (m + 2) * s + 2;
+  double* r = (double*)xcalloc((size_t)n, sizeof(double));
+  double* ax = (double*)xcalloc((size_t)n, sizeof(double));
+  double* xl = (double*)xcalloc((size_t)n, sizeof(double));
+  double* y = (double*)xcalloc((size_t)(m * s + 1), sizeof(double));
+  double* gl = (double*)xcalloc((size_t)(m * s + 2), sizeof(double));
+  double* lblocks = (double*)xcalloc((size_t)((m + 1) * s * s), sizeof(double));
+  initial_residual(a, f, x, r, c);
+  double rn = checked_norm(n, r, c);
+  push_d(&rep->history, &rep->n_history, rn);
+  push_c(&rep->op_history, &rep->n_op_history, *c);
+
+  /* :518-543 one standard GMRES(s m) cycle */
+#define RUN_FALLBACK(result)                                                           \
+  do {                                                                                 \
+    orc_solver_cfg gc = {3, 4, s * m, cfg->tol, s * m, 0, 0, 10.0};                    \
+    orc_report sub;                                                                    \
+    orc_report_init(&sub);                                                             \
+    memcpy(xl, x, (size_t)n * sizeof(double));                                         \
+    orc_gmres_solve(a, f, xl, &gc, &sub);                                              \
+    memcpy(x, xl, (size_t)n * sizeof(double));                                         \
+    rep->iterations += sub.iterations;                                                 \
+    rep->cycles += sub.cycles;                                                         \
+    ++rep->fallback_cycles;                                                            \
+    c->dotprods += sub.op_counts.dotprods;                                             \
+    c->matvecs += sub.op_counts.matvecs;                                               \
+    c->vec_updates += sub.op_counts.vec_updates;                                       \
+    c->termination_dots += sub.op_counts.termination_dots;                             \
+    for (uint64_t i_ = 1; i_ < sub.n_history; ++i_)                                    \
+      push_d(&rep->history, &rep->n_history, sub.history[i_]);                         \
+    orc_report_free(&sub);                                                             \
+    orc_spmv(a, x, ax);                                                                \
+    ++c->matvecs;                                                                      \
+    for (uint64_t i_ = 0; i_ < n; ++i_) r[i_] = f[i_] - ax[i_];                        \
+    ++c->vec_updates;                                                                  \
+    rn = checked_norm(n, r, c);                                                        \
+    push_c(&rep->op_history, &rep->n_op_history, *c);                                  \
+    (result) = rn <= cfg->tol;                                                         \
+  } while (0)
+
+  while (rn > cfg->tol && rep->iterations < cfg->max_iterations) {
+    int collapsed = 0, exhausted = 0, fb = 0;
+    char collapse_msg[512] = "";
+    uint64_t blocks_done = 0;
+    sarn_t E;
+    if (sarn_init(&E, a, r, s, m, c, &e)) {
+      sarn_free(&E);
+      if (e.code != ORC_EBREAK) goto done;
+      snprintf(collapse_msg, sizeof collapse_msg, "%s", e.msg);
+      e.code = 0;
+      RUN_FALLBACK(fb);
+      if (!fb) {
+        if (rep->iterations >= cfg->max_iterations) break;
+        continue;
+      }
+      break;
+    }
+    uint64_t nl = 0;
+    if (cholesky_upper(s, E.grams, lblocks, &e)) { /* escapes the reference solver */
+      sarn_free(&E);
+      goto done;
+    }
+    nl = 1;
+    hlsq_t lsq;
+    hlsq_init(&lsq, rn * lblocks[0], m * s);
+    for (uint64_t k = 1; k <= m; ++k) {
+      int more = sarn_advance(&E, k < m, &e);
+      if (more < 0) {
+        collapsed = 1;
+        snprintf(collapse_msg, sizeof collapse_msg, "%s", e.msg);
+        e.code = 0;
+        break;
+      }
+      if (k < m && more) {
+        if (cholesky_upper(s, E.grams + k * s * s, lblocks + nl * s * s, &e)) {
+          collapsed = 1;
+          snprintf(collapse_msg, sizeof collapse_msg, "%s", e.msg);
+          e.code = 0;
+          break;
+        }
+        ++nl;
+      }
+      double rho = lsq.residual;
+      for (uint64_t lc = 0; lc < s; ++lc) {
+        const uint64_t gi = (k - 1) * s + lc;
+        const double* g = E.gcols[gi];
+        const uint64_t gsz = E.glen[gi];
+        memcpy(gl, g, (size_t)gsz * sizeof(double));
+        /* apply_l (sstep.hpp:566-579) */
+        for (uint64_t bi = 0; bi < nl && bi * s < gsz; ++bi) {
+          const double* lb = lblocks + bi * s * s;
+          const uint64_t off = bi * s;
+          for (uint64_t rl = 0; rl < s && off + rl < gsz; ++rl) {
+            double acc = 0.0;
+            for (uint64_t jl = rl; jl < s && off + jl < gsz; ++jl) acc += lb[rl * s + jl] * g[off + jl];
+            gl[off + rl] = acc;
+          }
+        }
+        rho = hlsq_append(&lsq, gl);
+      }
+      push_d(&rep->block_rho, &rep->n_block_rho, rho);
+      rep->iterations += s;
+      blocks_done = k;
+      if (!more) {
+        exhausted = 1;
+        break;
+      }
+      if (rho <= cfg->tol) break;
+    }
+    const int attainable = lsq.cols > 0 && lsq.residual <= cfg->tol;
+    if (collapsed && !attainable) {
+      hlsq_free(&lsq);
+      sarn_free(&E);
+      RUN_FALLBACK(fb);
+      if (!fb) {
+        if (rep->iterations >= cfg->max_iterations) {
+          char msg[600];
+          snprintf(msg, sizeof msg, "basis collapse (%s)", collapse_msg);
+          set_breakdown(rep, msg);
+          break;
+        }
+        continue;
+      }
+      break;
+    }
+    if (hlsq_solve(&lsq, y, &e)) {
+      set_breakdown(rep, e.msg);
+      e.code = 0;
+      hlsq_free(&lsq);
+      sarn_free(&E);
+      break;
+    }
+    hlsq_free(&lsq);
+    for (uint64_t bi = 0; bi < blocks_done; ++bi)
+      for (uint64_t lc = 0; lc < s; ++lc) axpy(n, y[bi * s + lc], E.blocks[bi] + lc * n, x);
+    c->vec_updates += blocks_done * s;
+    sarn_free(&E);
+    orc_spmv(a, x, ax);
+    ++c->matvecs;
+    for (uint64_t i = 0; i < n; ++i) r[i] = f[i] - ax[i];
+    ++c->vec_updates;
+    ++rep->cycles;
+    rn = checked_norm(n, r, c);
+    push_d(&rep->history, &rep->n_history, rn);
+    if (blocks_done == m && !exhausted && !collapsed) push_c(&rep->op_history, &rep->n_op_history, *c);
+    if (rn <= cfg->tol) break;
+    if (collapsed) {
+      RUN_FALLBACK(fb);
+      if (!fb && rep->iterations >= cfg->max_iterations) {
+        char msg[600];
+        snprintf(msg, sizeof msg, "basis collapse (%s)", collapse_msg);
+        set_breakdown(rep, msg);
+        break;
+      }
+      if (rn <= cfg->tol) break;
+      continue;
+    }
+    if (exhausted) {
+      set_breakdown(rep, "invariant subspace reached with residual above threshold");
+      break;
+    }
+  }
+#undef RUN_FALLBACK
+  rep->converged = rn <= cfg->tol;
+  rep->final_residual = rep->history[rep->n_history - 1];
+done:
+  free(r);
+  free(ax);
+  free(xl);
+  free(y);
+  free(gl);
+  free(lblocks);
+  if (e.code) snprintf(rep->error, sizeof rep->error, "%s", e.msg);
+  return e.code;
+}
+
+/* ------------------------------------------------------------------ */
+/* problem generators (ours) */
+uint64_t orc_splitmix64(uint64_t* state) {
+  uint64_t z = (*state += 0x9E3779B97F4A7C15ULL);
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+  return z ^ (z >> 31);
+}
+
+/* element i is output number i+1 of the splitmix64 stream seeded with `seed` */
+void orc_fill_uniform(uint64_t seed, uint64_t offset, uint64_t n, double* out) {
+  for (uint64_t i = 0; i < n; ++i) {
+    uint64_t st = seed + (offset + i) * 0x9E3779B97F4A7C15ULL;
+    const uint64_t z = orc_splitmix64(&st);
+    const double u = (double)(z >> 11) * 0x1.0p-53;
+    out[i] = 2.0 * u - 1.0;
+  }
+}
+
+void orc_fill_lognormal(uint64_t seed, uint64_t n, double* out) {
+  const double two_pi = 6.283185307179586476925286766559;
+  for (uint64_t i = 0; i < n; ++i) {
+    uint64_t st = seed + (2 * i) * 0x9E3779B97F4A7C15ULL;
+    const uint64_t z1 = orc_splitmix64(&st);
+    const uint64_t z2 = orc_splitmix64(&st);
+    const double u1 = ((double)(z1 >> 11) + 1.0) * 0x1.0p-53; /* (0,1] */
+    const double u2 = (double)(z2 >> 11) * 0x1.0p-53;
+    const double g = sqrt(-2.0 * log(u1)) * cos(two_pi * u2);
+    out[i] = exp(g);
+  }
+}
+
+/* face coefficient of the variable-k operator: harmonic mean, own k on boundary faces */
+static double face_k(double kp, double kq) { return (2.0 * kp * kq) / (kp + kq); }
+
+/* Per-row stencil values in ascending-column order (-z,-y,-x,C,+x,+y,+z); present[] marks
+ * in-grid neighbours. 2D uses slots 1..5. */
+static void stencil_row(int32_t dim, uint64_t nx, uint64_t ny, uint64_t nz, const double* coef,
+                        const double* kcell, double ch2, uint64_t i, uint64_t j, uint64_t l,
+                        double val[7], int present[7], uint64_t nb[7]) {
+  const uint64_t plane = nx * ny;
+  const uint64_t row = l * plane + j * nx + i;
+  present[0] = dim == 3 && l > 0;
+  present[1] = j > 0;
+  present[2] = i > 0;
+  present[3] = 1;
+  present[4] = i + 1 < nx;
+  present[5] = j + 1 < ny;
+  present[6] = dim == 3 && l + 1 < nz;
+  nb[0] = row - plane;
+  nb[1] = row - nx;
+  nb[2] = row - 1;
+  nb[3] = row;
+  nb[4] = row + 1;
+  nb[5] = row + nx;
+  nb[6] = row + plane;
+  for (int t = 0; t < 7; ++t) val[t] = 0.0;
+  if (!kcell) {
+    for (int t = 0; t < 7; ++t) val[t] = coef[t];
+    return;
+  }
+  /* faces in order -z,-y,-x,+x,+y,+z */
+  const double kp = kcell[row];
+  static const int slot[6] = {0, 1, 2, 4, 5, 6};
+  double d = 0.0;
+  int first = 1;
+  for (int f = 0; f < 6; ++f) {
+    const int t = slot[f];
+    if (dim == 2 && (t == 0 || t == 6)) continue;
+    const double kf = present[t] ? face_k(kp, kcell[nb[t]]) : kp;
+    d = first ? kf : d + kf;
+    first = 0;
+    val[t] = t < 3 ? -kf - ch2 : -kf + ch2;
+  }
+  val[3] = d;
+}
+
+int orc_build_stencil_csr(int32_t dim, uint64_t nx, uint64_t ny, uint64_t nz, const double* coef,
+                          const double* kcell, double ch2, uint64_t** offs, uint64_t** cols,
+                          double** vals) {
+  if (dim == 2) nz = 1;
+  const uint64_t n = nx * ny * nz;
+  uint64_t* o = (uint64_t*)malloc((size_t)(n + 1) * sizeof(uint64_t));
+  uint64_t* c = (uint64_t*)malloc((size_t)(n * (dim == 3 ? 7 : 5)) * sizeof(uint64_t));
+  double* v = (double*)malloc((size_t)(n * (dim == 3 ? 7 : 5)) * sizeof(double));
+  if (!o || !c || !v) {
+    free(o);
+    free(c);
+    free(v);
+    return ORC_ENOMEM;
+  }
+  uint64_t p = 0;
+  o[0] = 0;
+  for (uint64_t l = 0; l < nz; ++l)
+    for (uint64_t j = 0; j < ny; ++j)
+      for (uint64_t i = 0; i < nx; ++i) {
+        double val[7];
+        int present[7];
+        uint64_t nb[7];
+        stencil_row(dim, nx, ny, nz, coef, kcell, ch2, i, j, l, val, present, nb);
+        for (int t = 0; t < 7; ++t)
+          if (present[t]) {
+            c[p] = nb[t];
+            v[p] = val[t];
+            ++p;
+          }
+        o[l * nx * ny + j * nx + i + 1] = p;
+      }
+  *offs = o;
+  *cols = c;
+  *vals = v;
+  return 0;
+}
+
+void orc_csr_free(uint64_t* offs, uint64_t* cols, double* vals) {
+  free(offs);
+  free(cols);
+  free(vals);
+}
+
+void orc_stencil_apply(int32_t dim, uint64_t nx, uint64_t ny, uint64_t nz, const double* coef,
+                       const double* kcell, double ch2, const double* x, double* y) {
+  if (dim == 2) nz = 1;
+  for (uint64_t l = 0; l < nz; ++l)
+    for (uint64_t j = 0; j < ny; ++j)
+      for (uint64_t i = 0; i < nx; ++i) {
+        double val[7];
+        int present[7];
+        uint64_t nb[7];
+        stencil_row(dim, nx, ny, nz, coef, kcell, ch2, i, j, l, val, present, nb);
+        double acc = 0.0;
+        for (int t = 0; t < 7; ++t)
+          if (present[t]) acc += val[t] * x[nb[t]];
+        y[l * nx * ny + j * nx + i] = acc;
+      }
+}
