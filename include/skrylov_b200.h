@@ -1,0 +1,190 @@
+/*
+ * skrylov_b200.h -- C ABI of the B200 s-step Orthomin / s-step GMRES library
+ * (libskrylov_b200.so).  Plain C types only: a cgo / JNI / ctypes / Rust binding can
+ * bind it directly.  See INTEGRATION.md for the reference-side bindings.
+ *
+ * Each entry point replaces one reference interface (file:line under
+ * /root/reference/proj/include/skrylov/):
+ *
+ *   skc_somin_solve   <- somin_solve(const LinearOperator&, span f, vector& x, const SStepConfig&)  sstep.hpp:142-143
+ *   skc_sgmres_solve  <- sgmres_solve(...same...)                                                   sstep.hpp:493-494
+ *   skc_smr_solve     <- smr_solve(...same...)                                                      sstep.hpp:109-110
+ *   skc_smr_step      <- smr_step(op, x, r, s, OpCounter*)                                          sstep.hpp:89-91
+ *   skc_gmres_solve   <- gmres_solve(op, f, x, const SolverConfig&)  (s=1 path and fallback)        solvers.hpp:297-298
+ *   skc_sarnoldi      <- sarnoldi(op, v1, s, m_blocks, OpCounter*) -> SStepBasis                    sstep.hpp:465-467
+ *   skc_op_apply      <- LinearOperator::apply(x, y)                                                operator.hpp:43-46
+ *   skc_krylov_block  <- krylov_block(op, v, s)                                                     block.hpp:59-67
+ *   skc_op_create_csr <- as_operator(const SparseMatrix&)                                           sparse.hpp:155-160
+ *   skc_op_create_stencil (new: device-describable 5/7-point operator)
+ *   skc_gram_solve / skc_cholesky_upper / skc_hessenberg_lsq <- GramSolver / cholesky_upper /
+ *                      hessenberg_lsq (small_dense.hpp:42-331); host-only, no GPU needed.
+ *
+ * Error convention (mirrors the reference's exceptions):
+ *   SKC_OK                0
+ *   SKC_EINVAL            1  std::invalid_argument from require() (kernels.hpp:41-43)
+ *   SKC_EBREAKDOWN        2  skrylov::breakdown_error escaping the call (sarnoldi, or a
+ *                            Cholesky failure of the first s-GMRES block)
+ *   SKC_ELOGIC            3  std::logic_error from debug_checks
+ *   SKC_ECUDA             4  CUDA runtime failure (std::runtime_error in the C++ wrapper)
+ *   SKC_ENCCL             5  NCCL failure
+ *   SKC_ENOMEM            6  device allocation failure
+ * Numerical breakdown inside the solvers is NOT an error: it is reported in the report's
+ * breakdown string with the reference's prefixes ("basis collapse at setup (",
+ * "basis collapse at iteration N (", "divergence: ", "basis collapse (",
+ * "invariant subspace reached...").  skc_last_error() returns the message of the last
+ * failing call on the calling thread.
+ */
+#ifndef SKRYLOV_B200_H
+#define SKRYLOV_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SKC_OK 0
+#define SKC_EINVAL 1
+#define SKC_EBREAKDOWN 2
+#define SKC_ELOGIC 3
+#define SKC_ECUDA 4
+#define SKC_ENCCL 5
+#define SKC_ENOMEM 6
+
+typedef struct skc_ctx skc_ctx;
+typedef struct skc_op skc_op;
+typedef struct skc_report skc_report;
+
+/* report.hpp:35-41 */
+typedef struct {
+  uint64_t dotprods, matvecs, vec_updates, stored_vectors, termination_dots;
+} skc_op_counter;
+
+/* sstep.hpp:48-58 SStepConfig (same field meaning and defaults; see skc_sstep_config_default) */
+typedef struct {
+  uint64_t s, k, m;
+  double tol; /* absolute threshold on ||r||_2 */
+  uint64_t max_iterations;
+  int32_t precondition; /* ILU(0) is out of scope: must be 0 (SKC_EINVAL otherwise) */
+  int32_t unbounded_window;
+  int32_t debug_checks;
+  double divergence_factor;
+} skc_sstep_config;
+
+/* solvers.hpp:45-54 SolverConfig, restricted to method = gmres (3) */
+typedef struct {
+  int32_t method;
+  uint64_t k, m;
+  double tol;
+  uint64_t max_iterations;
+  int32_t precondition, debug_checks;
+  double divergence_factor;
+} skc_solver_config;
+
+/* Device-describable stencil operator (h^2-scaled 5/7-point convection-diffusion).
+ * Natural ordering, x fastest. coef = {-z,-y,-x,C,+x,+y,+z} (2D ignores the z slots).
+ * kind 0: constant coefficients; kind 1: variable diffusion k per cell (kcell array, n
+ * entries, harmonic-mean faces, own k on boundary faces) with convection half-coefficient
+ * ch2: lower neighbours -k_f - ch2, upper -k_f + ch2, diagonal sum of the face k_f. */
+typedef struct {
+  int32_t dim; /* 2 or 3 */
+  int32_t kind;
+  uint64_t nx, ny, nz;
+  double coef[7];
+  double ch2;
+} skc_stencil_desc;
+
+typedef struct {
+  int32_t converged;
+  uint64_t iterations, cycles;
+  double final_residual;
+  skc_op_counter op_counts;
+  uint64_t steady_iteration;
+  int32_t has_breakdown;
+  uint64_t fallback_cycles;
+  uint64_t n_history, n_op_history, n_notes, n_block_rho;
+} skc_report_summary;
+
+/* ---- library / context ---- */
+const char* skc_last_error(void);
+const char* skc_version(void);
+int skc_device_count(int* count);
+/* One context per calling thread (the reference is single-threaded). */
+int skc_ctx_create(int device, skc_ctx** out);
+int skc_ctx_destroy(skc_ctx* ctx);
+/* Use an external CUDA stream (cudaStream_t as uintptr_t, 0 = the context's own). */
+int skc_ctx_set_stream(skc_ctx* ctx, uintptr_t stream);
+/* Kernel timing: when enabled every hot kernel launch is bracketed by CUDA events on its
+ * stream; skc_ctx_kernel_stats returns (launches, total ms, algorithmic bytes) per class. */
+int skc_ctx_set_profiling(skc_ctx* ctx, int enable);
+int skc_ctx_kernel_stats(skc_ctx* ctx, const char* name, uint64_t* launches, double* total_ms,
+                         double* alg_bytes);
+int skc_ctx_kernel_names(skc_ctx* ctx, char* buf, size_t cap); /* comma separated */
+int skc_ctx_reset_stats(skc_ctx* ctx);
+/* Number of device kernel launches issued by the library since the last reset. */
+int skc_ctx_launch_count(skc_ctx* ctx, uint64_t* launches);
+
+/* ---- operators ---- */
+int skc_op_create_stencil(skc_ctx* ctx, const skc_stencil_desc* desc, const double* kcell_host,
+                          skc_op** out);
+/* CSR (size_t indices, ascending columns per row; sparse.hpp:37-132).  A 5/7-point grid
+ * pattern (column offsets {0,+-1,+-nx[,+-nx*ny]} with no wrap-around) is recognized and
+ * run by the stencil kernels from per-cell diagonals; anything else runs the CSR kernel. */
+int skc_op_create_csr(skc_ctx* ctx, uint64_t n, const uint64_t* row_offsets, const uint64_t* col_indices,
+                      const double* values, skc_op** out);
+int skc_op_destroy(skc_op* op);
+int skc_op_size(const skc_op* op, uint64_t* n);
+/* 0 = general CSR, 1 = 2D stencil, 2 = 3D stencil */
+int skc_op_kind(const skc_op* op, int* kind);
+/* y = A x on host buffers (bit-identical to the reference spmv for the same values) */
+int skc_op_apply(skc_ctx* ctx, const skc_op* op, const double* x, double* y);
+/* [v, A v, ..., A^{s-1} v], out is n*s column-major, host buffers */
+int skc_krylov_block(skc_ctx* ctx, const skc_op* op, const double* v, uint64_t s, double* out);
+
+/* ---- reports ---- */
+int skc_report_create(skc_report** out);
+int skc_report_destroy(skc_report* rep);
+int skc_report_get_summary(const skc_report* rep, skc_report_summary* out);
+uint64_t skc_report_get_history(const skc_report* rep, double* out, uint64_t cap);
+uint64_t skc_report_get_op_history(const skc_report* rep, skc_op_counter* out, uint64_t cap);
+/* per-block-step LSQ residual estimates of s-GMRES (extension; not in SolveReport) */
+uint64_t skc_report_get_block_rho(const skc_report* rep, double* out, uint64_t cap);
+/* copies the string (NUL terminated, truncated to cap) and returns its full length */
+uint64_t skc_report_get_breakdown(const skc_report* rep, char* out, uint64_t cap);
+uint64_t skc_report_get_note(const skc_report* rep, uint64_t idx, char* out, uint64_t cap);
+
+/* ---- solvers (host buffers: f read, x in/out; all device traffic inside the call) ---- */
+int skc_somin_solve(skc_ctx* ctx, const skc_op* op, const double* f, double* x,
+                    const skc_sstep_config* cfg, skc_report* rep);
+int skc_sgmres_solve(skc_ctx* ctx, const skc_op* op, const double* f, double* x,
+                     const skc_sstep_config* cfg, skc_report* rep);
+int skc_smr_solve(skc_ctx* ctx, const skc_op* op, const double* f, double* x,
+                  const skc_sstep_config* cfg, skc_report* rep);
+int skc_gmres_solve(skc_ctx* ctx, const skc_op* op, const double* f, double* x,
+                    const skc_solver_config* cfg, skc_report* rep);
+/* x, r in/out; coeffs_out (s entries) and counter may be NULL */
+int skc_smr_step(skc_ctx* ctx, const skc_op* op, double* x, double* r, uint64_t s, double* coeffs_out,
+                 skc_op_counter* counter);
+/* Device-resident variants: f_dev / x_dev are device pointers on ctx's device. */
+int skc_somin_solve_device(skc_ctx* ctx, const skc_op* op, const double* f_dev, double* x_dev,
+                           const skc_sstep_config* cfg, skc_report* rep);
+int skc_sgmres_solve_device(skc_ctx* ctx, const skc_op* op, const double* f_dev, double* x_dev,
+                            const skc_sstep_config* cfg, skc_report* rep);
+/* blocks_out: m_blocks*s*n (block-major, column-major inside); grams_out: m_blocks*s*s;
+ * hess_out: ((m_blocks+1)*s) x (m_blocks*s) row-major; seed_out: n. Host buffers. */
+int skc_sarnoldi(skc_ctx* ctx, const skc_op* op, const double* v1, uint64_t s, uint64_t m_blocks,
+                 double* blocks_out, double* grams_out, double* hess_out, double* seed_out,
+                 double* seed_norm_out, skc_op_counter* counter);
+
+/* ---- host small-dense (no GPU needed; the same code runs inside the scalar kernels) ---- */
+int skc_gram_solve(uint64_t order, const double* w, uint64_t nrhs, const double* rhs, double* x_out,
+                   int32_t* used_ldlt, double* pivots_out);
+int skc_cholesky_upper(uint64_t order, const double* w, double* r_out);
+int skc_hessenberg_lsq(uint64_t rows, uint64_t cols, const double* g, double beta, double* y_out,
+                       double* residual_out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,464 @@
+// capi.cu -- the C ABI (include/skrylov_b200.h) over the C++ solvers.
+#include <cstring>
+#include <string>
+
+#include "skc_internal.hpp"
+
+struct skc_ctx {
+  skc::Ctx c;
+};
+struct skc_op {
+  skc::Op o;
+};
+struct skc_report {
+  skc::Report r;
+};
+
+namespace {
+
+thread_local std::string g_last_error;
+
+template <class F>
+int guarded(F&& body) {
+  try {
+    body();
+    return SKC_OK;
+  } catch (const skc::Error& e) {
+    g_last_error = e.msg;
+    return e.code;
+  } catch (const std::bad_alloc&) {
+    g_last_error = "host allocation failure";
+    return SKC_ENOMEM;
+  } catch (const std::exception& e) {
+    g_last_error = e.what();
+    return SKC_ECUDA;
+  }
+}
+
+skc::SStepCfg conv(const skc_sstep_config* c) {
+  skc::require(c != nullptr, "null config");
+  skc::SStepCfg s;
+  s.s = c->s;
+  s.k = c->k;
+  s.m = c->m;
+  s.tol = c->tol;
+  s.max_iterations = c->max_iterations;
+  s.precondition = c->precondition != 0;
+  s.unbounded_window = c->unbounded_window != 0;
+  s.debug_checks = c->debug_checks != 0;
+  s.divergence_factor = c->divergence_factor;
+  // bench.hpp:160-166 wraps ILU(0) when precondition is set; not provided on the GPU path
+  skc::require(!s.precondition, "precondition: ILU(0) right preconditioning is not provided by the B200 path");
+  return s;
+}
+
+void set_device(skc_ctx* ctx) { CK(cudaSetDevice(ctx->c.device)); }
+
+// host f/x wrapper around a device solver
+template <class Solve>
+int host_solve(skc_ctx* ctx, const skc_op* op, const double* f, double* x, skc_report* rep, Solve&& solve) {
+  return guarded([&] {
+    skc::require(ctx && op && f && x && rep, "null argument");
+    set_device(ctx);
+    skc::Ctx& c = ctx->c;
+    const size_t n = (size_t)op->o.n;
+    double* fd = (double*)c.workspace("io_f", n * sizeof(double));
+    double* xd = (double*)c.workspace("io_x", n * sizeof(double));
+    CK(cudaMemcpyAsync(fd, f, n * sizeof(double), cudaMemcpyHostToDevice, c.stream));
+    CK(cudaMemcpyAsync(xd, x, n * sizeof(double), cudaMemcpyHostToDevice, c.stream));
+    rep->r = skc::Report{};
+    solve(c, op->o, fd, xd, rep->r);
+    CK(cudaMemcpyAsync(x, xd, n * sizeof(double), cudaMemcpyDeviceToHost, c.stream));
+    c.sync();
+  });
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* skc_last_error(void) { return g_last_error.c_str(); }
+const char* skc_version(void) { return "skrylov_b200 0.1 (sm_100a)"; }
+
+int skc_device_count(int* count) {
+  return guarded([&] { CK(cudaGetDeviceCount(count)); });
+}
+
+int skc_ctx_create(int device, skc_ctx** out) {
+  return guarded([&] {
+    skc::require(out != nullptr, "null output");
+    int ndev = 0;
+    CK(cudaGetDeviceCount(&ndev));
+    skc::require(device >= 0 && device < ndev, "skc_ctx_create: device index out of range");
+    CK(cudaSetDevice(device));
+    cudaDeviceProp p;
+    CK(cudaGetDeviceProperties(&p, device));
+    auto* ctx = new skc_ctx;
+    ctx->c.device = device;
+    ctx->c.sm_count = p.multiProcessorCount;
+    CK(cudaStreamCreateWithFlags(&ctx->c.own_stream, cudaStreamNonBlocking));
+    ctx->c.stream = ctx->c.own_stream;
+    *out = ctx;
+  });
+}
+
+int skc_ctx_destroy(skc_ctx* ctx) {
+  return guarded([&] { delete ctx; });
+}
+
+int skc_ctx_set_stream(skc_ctx* ctx, uintptr_t stream) {
+  return guarded([&] {
+    skc::require(ctx != nullptr, "null context");
+    ctx->c.stream = stream ? reinterpret_cast<cudaStream_t>(stream) : ctx->c.own_stream;
+  });
+}
+
+int skc_ctx_set_profiling(skc_ctx* ctx, int enable) {
+  return guarded([&] {
+    skc::require(ctx != nullptr, "null context");
+    set_device(ctx);
+    ctx->c.sync();
+    ctx->c.profiling = enable != 0;
+  });
+}
+
+int skc_ctx_kernel_stats(skc_ctx* ctx, const char* name, uint64_t* launches, double* total_ms, double* alg_bytes) {
+  return guarded([&] {
+    skc::require(ctx && name, "null argument");
+    auto it = ctx->c.stats.find(name);
+    const skc::KStat s = it == ctx->c.stats.end() ? skc::KStat{} : it->second;
+    if (launches) *launches = s.launches;
+    if (total_ms) *total_ms = s.ms;
+    if (alg_bytes) *alg_bytes = s.bytes;
+  });
+}
+
+int skc_ctx_kernel_names(skc_ctx* ctx, char* buf, size_t cap) {
+  return guarded([&] {
+    skc::require(ctx && buf && cap > 0, "null argument");
+    std::string all;
+    for (auto& kv : ctx->c.stats) {
+      if (!all.empty()) all += ",";
+      all += kv.first;
+    }
+    std::snprintf(buf, cap, "%s", all.c_str());
+  });
+}
+
+int skc_ctx_reset_stats(skc_ctx* ctx) {
+  return guarded([&] {
+    skc::require(ctx != nullptr, "null context");
+    set_device(ctx);
+    ctx->c.sync();
+    ctx->c.stats.clear();
+    ctx->c.launches = 0;
+  });
+}
+
+int skc_ctx_launch_count(skc_ctx* ctx, uint64_t* launches) {
+  return guarded([&] {
+    skc::require(ctx && launches, "null argument");
+    *launches = ctx->c.launches;
+  });
+}
+
+// ---------------------------------------------------------------- operators
+int skc_op_create_stencil(skc_ctx* ctx, const skc_stencil_desc* desc, const double* kcell_host, skc_op** out) {
+  return guarded([&] {
+    skc::require(ctx && desc && out, "null argument");
+    set_device(ctx);
+    auto* op = new skc_op;
+    try {
+      skc::build_stencil_op(ctx->c, op->o, *desc, kcell_host);
+    } catch (...) {
+      delete op;
+      throw;
+    }
+    *out = op;
+  });
+}
+
+int skc_op_create_csr(skc_ctx* ctx, uint64_t n, const uint64_t* row_offsets, const uint64_t* col_indices,
+                      const double* values, skc_op** out) {
+  return guarded([&] {
+    skc::require(ctx && row_offsets && out, "null argument");
+    skc::require(n == 0 || (col_indices && values) || row_offsets[n] == 0, "null argument");
+    set_device(ctx);
+    auto* op = new skc_op;
+    try {
+      skc::build_csr_op(ctx->c, op->o, (int64_t)n, row_offsets, col_indices, values);
+    } catch (...) {
+      delete op;
+      throw;
+    }
+    *out = op;
+  });
+}
+
+int skc_op_destroy(skc_op* op) {
+  return guarded([&] { delete op; });
+}
+
+int skc_op_size(const skc_op* op, uint64_t* n) {
+  return guarded([&] {
+    skc::require(op && n, "null argument");
+    *n = (uint64_t)op->o.n;
+  });
+}
+
+int skc_op_kind(const skc_op* op, int* kind) {
+  return guarded([&] {
+    skc::require(op && kind, "null argument");
+    *kind = op->o.d.kind == skc::kCsr ? 0 : op->o.d.dim;
+  });
+}
+
+int skc_op_apply(skc_ctx* ctx, const skc_op* op, const double* x, double* y) {
+  return guarded([&] {
+    skc::require(ctx && op && x && y, "null argument");
+    set_device(ctx);
+    skc::Ctx& c = ctx->c;
+    const size_t n = (size_t)op->o.n;
+    double* xd = (double*)c.workspace("io_x", n * sizeof(double));
+    double* yd = (double*)c.workspace("io_f", n * sizeof(double));
+    CK(cudaMemcpyAsync(xd, x, n * sizeof(double), cudaMemcpyHostToDevice, c.stream));
+    skc::launch_apply(c, op->o.d, xd, yd, nullptr, nullptr);
+    CK(cudaMemcpyAsync(y, yd, n * sizeof(double), cudaMemcpyDeviceToHost, c.stream));
+    c.sync();
+  });
+}
+
+int skc_krylov_block(skc_ctx* ctx, const skc_op* op, const double* v, uint64_t s, double* out) {
+  return guarded([&] {
+    skc::require(ctx && op && v && out, "null argument");
+    skc::require(s >= 1, "krylov_block: s must be at least 1");
+    set_device(ctx);
+    skc::Ctx& c = ctx->c;
+    const size_t n = (size_t)op->o.n;
+    double* b = (double*)c.workspace("io_block", n * s * sizeof(double));
+    CK(cudaMemcpyAsync(b, v, n * sizeof(double), cudaMemcpyHostToDevice, c.stream));
+    for (uint64_t j = 1; j < s; ++j) skc::launch_apply(c, op->o.d, b + (j - 1) * n, b + j * n, nullptr, nullptr);
+    CK(cudaMemcpyAsync(out, b, n * s * sizeof(double), cudaMemcpyDeviceToHost, c.stream));
+    c.sync();
+  });
+}
+
+// ---------------------------------------------------------------- reports
+int skc_report_create(skc_report** out) {
+  return guarded([&] {
+    skc::require(out != nullptr, "null output");
+    *out = new skc_report;
+  });
+}
+int skc_report_destroy(skc_report* rep) {
+  return guarded([&] { delete rep; });
+}
+
+int skc_report_get_summary(const skc_report* rep, skc_report_summary* o) {
+  return guarded([&] {
+    skc::require(rep && o, "null argument");
+    const skc::Report& r = rep->r;
+    o->converged = r.converged;
+    o->iterations = r.iterations;
+    o->cycles = r.cycles;
+    o->final_residual = r.final_residual;
+    o->op_counts = r.op_counts;
+    o->steady_iteration = r.steady_iteration;
+    o->has_breakdown = r.breakdown.has_value();
+    o->fallback_cycles = r.fallback_cycles;
+    o->n_history = r.history.size();
+    o->n_op_history = r.op_history.size();
+    o->n_notes = r.notes.size();
+    o->n_block_rho = r.block_rho.size();
+  });
+}
+
+uint64_t skc_report_get_history(const skc_report* rep, double* out, uint64_t cap) {
+  if (!rep) return 0;
+  const auto& h = rep->r.history;
+  const uint64_t k = std::min<uint64_t>(cap, h.size());
+  if (out) std::memcpy(out, h.data(), k * sizeof(double));
+  return h.size();
+}
+
+uint64_t skc_report_get_op_history(const skc_report* rep, skc_op_counter* out, uint64_t cap) {
+  if (!rep) return 0;
+  const auto& h = rep->r.op_history;
+  const uint64_t k = std::min<uint64_t>(cap, h.size());
+  if (out) std::memcpy(out, h.data(), k * sizeof(skc_op_counter));
+  return h.size();
+}
+
+uint64_t skc_report_get_block_rho(const skc_report* rep, double* out, uint64_t cap) {
+  if (!rep) return 0;
+  const auto& h = rep->r.block_rho;
+  const uint64_t k = std::min<uint64_t>(cap, h.size());
+  if (out) std::memcpy(out, h.data(), k * sizeof(double));
+  return h.size();
+}
+
+static uint64_t copy_str(const std::string& s, char* out, uint64_t cap) {
+  if (out && cap) {
+    const size_t k = std::min<size_t>(cap - 1, s.size());
+    std::memcpy(out, s.data(), k);
+    out[k] = 0;
+  }
+  return s.size();
+}
+
+uint64_t skc_report_get_breakdown(const skc_report* rep, char* out, uint64_t cap) {
+  if (!rep || !rep->r.breakdown) return copy_str("", out, cap);
+  return copy_str(*rep->r.breakdown, out, cap);
+}
+
+uint64_t skc_report_get_note(const skc_report* rep, uint64_t idx, char* out, uint64_t cap) {
+  if (!rep || idx >= rep->r.notes.size()) return copy_str("", out, cap);
+  return copy_str(rep->r.notes[idx], out, cap);
+}
+
+// ---------------------------------------------------------------- solvers
+int skc_somin_solve(skc_ctx* ctx, const skc_op* op, const double* f, double* x, const skc_sstep_config* cfg,
+                    skc_report* rep) {
+  return host_solve(ctx, op, f, x, rep, [&](skc::Ctx& c, const skc::Op& o, const double* fd, double* xd,
+                                            skc::Report& r) { skc::somin_device(c, o, fd, xd, conv(cfg), r); });
+}
+
+int skc_sgmres_solve(skc_ctx* ctx, const skc_op* op, const double* f, double* x, const skc_sstep_config* cfg,
+                     skc_report* rep) {
+  return host_solve(ctx, op, f, x, rep, [&](skc::Ctx& c, const skc::Op& o, const double* fd, double* xd,
+                                            skc::Report& r) { skc::sgmres_device(c, o, fd, xd, conv(cfg), r); });
+}
+
+int skc_smr_solve(skc_ctx* ctx, const skc_op* op, const double* f, double* x, const skc_sstep_config* cfg,
+                  skc_report* rep) {
+  return host_solve(ctx, op, f, x, rep, [&](skc::Ctx& c, const skc::Op& o, const double* fd, double* xd,
+                                            skc::Report& r) { skc::smr_device(c, o, fd, xd, conv(cfg), r); });
+}
+
+int skc_gmres_solve(skc_ctx* ctx, const skc_op* op, const double* f, double* x, const skc_solver_config* cfg,
+                    skc_report* rep) {
+  return host_solve(ctx, op, f, x, rep, [&](skc::Ctx& c, const skc::Op& o, const double* fd, double* xd,
+                                            skc::Report& r) {
+    skc::require(cfg != nullptr, "null config");
+    skc::require(cfg->method == 3, "gmres: only method = gmres (3) runs on the B200 path");
+    skc::require(!cfg->precondition, "precondition: ILU(0) right preconditioning is not provided by the B200 path");
+    skc::gmres_device(c, o, fd, xd, cfg->m, cfg->tol, cfg->max_iterations, r);
+  });
+}
+
+int skc_smr_step(skc_ctx* ctx, const skc_op* op, double* x, double* r, uint64_t s, double* coeffs_out,
+                 skc_op_counter* counter) {
+  return guarded([&] {
+    skc::require(ctx && op && x && r, "null argument");
+    set_device(ctx);
+    skc::Ctx& c = ctx->c;
+    const size_t n = (size_t)op->o.n;
+    double* xd = (double*)c.workspace("io_x", n * sizeof(double));
+    double* rd = (double*)c.workspace("io_f", n * sizeof(double));
+    CK(cudaMemcpyAsync(xd, x, n * sizeof(double), cudaMemcpyHostToDevice, c.stream));
+    CK(cudaMemcpyAsync(rd, r, n * sizeof(double), cudaMemcpyHostToDevice, c.stream));
+    skc::smr_step_device(c, op->o, xd, rd, s, coeffs_out, counter);
+    CK(cudaMemcpyAsync(x, xd, n * sizeof(double), cudaMemcpyDeviceToHost, c.stream));
+    CK(cudaMemcpyAsync(r, rd, n * sizeof(double), cudaMemcpyDeviceToHost, c.stream));
+    c.sync();
+  });
+}
+
+int skc_somin_solve_device(skc_ctx* ctx, const skc_op* op, const double* f_dev, double* x_dev,
+                           const skc_sstep_config* cfg, skc_report* rep) {
+  return guarded([&] {
+    skc::require(ctx && op && f_dev && x_dev && rep, "null argument");
+    set_device(ctx);
+    rep->r = skc::Report{};
+    skc::somin_device(ctx->c, op->o, f_dev, x_dev, conv(cfg), rep->r);
+    ctx->c.sync();
+  });
+}
+
+int skc_sgmres_solve_device(skc_ctx* ctx, const skc_op* op, const double* f_dev, double* x_dev,
+                            const skc_sstep_config* cfg, skc_report* rep) {
+  return guarded([&] {
+    skc::require(ctx && op && f_dev && x_dev && rep, "null argument");
+    set_device(ctx);
+    rep->r = skc::Report{};
+    skc::sgmres_device(ctx->c, op->o, f_dev, x_dev, conv(cfg), rep->r);
+    ctx->c.sync();
+  });
+}
+
+int skc_sarnoldi(skc_ctx* ctx, const skc_op* op, const double* v1, uint64_t s, uint64_t m_blocks, double* blocks_out,
+                 double* grams_out, double* hess_out, double* seed_out, double* seed_norm_out,
+                 skc_op_counter* counter) {
+  return guarded([&] {
+    skc::require(ctx && op && v1, "null argument");
+    set_device(ctx);
+    skc::Ctx& c = ctx->c;
+    const size_t n = (size_t)op->o.n;
+    double* vd = (double*)c.workspace("io_f", n * sizeof(double));
+    CK(cudaMemcpyAsync(vd, v1, n * sizeof(double), cudaMemcpyHostToDevice, c.stream));
+    skc::BasisOut b;
+    skc::sarnoldi_device(c, op->o, vd, s, m_blocks, b);
+    if (blocks_out) std::memcpy(blocks_out, b.blocks.data(), b.blocks.size() * sizeof(double));
+    if (grams_out) std::memcpy(grams_out, b.grams.data(), b.grams.size() * sizeof(double));
+    if (hess_out) std::memcpy(hess_out, b.hess.data(), b.hess.size() * sizeof(double));
+    if (seed_out) std::memcpy(seed_out, b.seed.data(), b.seed.size() * sizeof(double));
+    if (seed_norm_out) *seed_norm_out = b.seed_norm;
+    if (counter) {
+      counter->dotprods += b.counter.dotprods;
+      counter->matvecs += b.counter.matvecs;
+      counter->vec_updates += b.counter.vec_updates;
+      counter->termination_dots += b.counter.termination_dots;
+    }
+  });
+}
+
+// ---------------------------------------------------------------- host small dense
+int skc_gram_solve(uint64_t order, const double* w, uint64_t nrhs, const double* rhs, double* x_out,
+                   int32_t* used_ldlt, double* pivots_out) {
+  return guarded([&] {
+    skc::require(order >= 1, "GramSolver: empty matrix");
+    skc::require(order <= (uint64_t)skc::kMaxS, "GramSolver: order above 8");
+    skc::Gram g;
+    skc::gram_factor(g, w, (int)order);
+    if (used_ldlt) *used_ldlt = g.used_ldlt;
+    if (pivots_out)
+      for (uint64_t i = 0; i < order; ++i) pivots_out[i] = g.piv[i];
+    if (!g.ok) skc::fail(SKC_EBREAKDOWN, g.singular1 ? "sym_solve: singular 1x1 Gram system"
+                                                     : "sym_solve: numerically singular Gram system (pivot ratio " +
+                                                           skc::fmt_double(g.ratio) + ")");
+    for (uint64_t j = 0; j < nrhs; ++j) {
+      double col[skc::kMaxS], sol[skc::kMaxS];
+      for (uint64_t i = 0; i < order; ++i) col[i] = rhs[i * nrhs + j];
+      skc::gram_solve(g, col, sol);
+      for (uint64_t i = 0; i < order; ++i) x_out[i * nrhs + j] = sol[i];
+    }
+  });
+}
+
+int skc_cholesky_upper(uint64_t order, const double* w, double* r_out) {
+  return guarded([&] {
+    skc::require(order >= 1 && order <= (uint64_t)skc::kMaxS, "cholesky_upper: order out of range");
+    if (!skc::cholesky_upper(w, (int)order, r_out)) skc::fail(SKC_EBREAKDOWN, "cholesky: matrix not positive definite");
+  });
+}
+
+int skc_hessenberg_lsq(uint64_t rows, uint64_t cols, const double* g, double beta, double* y_out,
+                       double* residual_out) {
+  return guarded([&] {
+    skc::require(rows >= cols + 1, "hessenberg_lsq: G must have more rows than columns");
+    skc::require(beta >= 0.0, "hessenberg_lsq: beta must be non-negative");
+    skc::HessLsq lsq(beta);
+    for (uint64_t j = 0; j < cols; ++j) {
+      for (uint64_t i = j + 2; i < rows; ++i)
+        skc::require(g[i * cols + j] == 0.0, "hessenberg_lsq: G is not Hessenberg-banded");
+      std::vector<double> col(j + 2);
+      for (uint64_t i = 0; i <= j + 1; ++i) col[i] = g[i * cols + j];
+      lsq.append_column(std::move(col));
+    }
+    std::vector<double> y = lsq.solve();
+    std::memcpy(y_out, y.data(), y.size() * sizeof(double));
+    if (residual_out) *residual_out = lsq.residual_norm();
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,891 @@
+// sgmres.cu -- device-resident s-step Arnoldi (sstep.hpp:271-458), s-step GMRES(m)
+// (sstep.hpp:493-654), sarnoldi (sstep.hpp:465-485) and the standard MGS-GMRES(m) used for
+// s = 1 and as the basis-collapse fallback (solvers.hpp:86-110, 297-359).
+//
+// One restart cycle (constructor + m block iterations, every Scalar1/Scalar2 Gram solve,
+// block-MGS pass, reorthogonalization test and basis push) is enqueued without a host
+// round trip: the s x s solves run in single-CTA scalar kernels and write the update
+// coefficients consumed by the next streaming kernel; the conditional reorthogonalization
+// pass is predicated on a device flag.  The host synchronizes once per cycle, then runs
+// the reference's host-side recurrences on the recorded coefficients: block-Hessenberg
+// reconstruction (append_g_columns), cholesky_upper of each Gram block, the Givens
+// least-squares update and the early-exit/collapse/fallback decisions, exactly in the
+// reference's order.  A second short enqueue applies x += V y and recomputes r = f - A x.
+#include <cmath>
+#include <cstring>
+
+#include "device_util.cuh"
+#include "solver_util.hpp"
+
+namespace skc {
+
+namespace {
+
+enum : int { kArnRunning = 0, kArnCtorZero = 1, kArnCtorCollapse = 2, kArnInvariant = 3, kArnPushCollapse = 4 };
+
+struct ArnState {
+  int status;
+  int halt;
+  int block;   // block iteration that stopped the cycle
+  int reorth;  // reorthogonalization flag of the current block iteration
+  double rn;   // latest residual norm (also the constructor's ||r||)
+};
+
+// record layout per block iteration k (0 = constructor)
+struct RecLayout {
+  int s, m;
+  __host__ __device__ int size() const { return 8 + s * s + (m + 1) * s + (m + 1) * s * s; }
+  static constexpr int kZn = 0, kNu = 1, kInv = 2, kReorth = 3, kFirst = 4, kOk = 5, kRatio = 6, kSing = 7, kW = 8;
+  __host__ __device__ int h() const { return 8 + s * s; }
+  __host__ __device__ int t() const { return 8 + s * s + (m + 1) * s; }
+};
+
+// coefficient layout
+struct CoefLayout {
+  int s, m;
+  int H() const { return 0; }
+  int T() const { return m * s; }
+  int Inv() const { return m * s + s * s; }
+  int Y() const { return Inv() + 1; }
+  int M1() const { return Y() + (m + 1) * s; }
+  int size() const { return M1() + 1; }
+};
+
+// dot-region layout
+struct DotLayout {
+  int s, m;
+  int Z() const { return 0; }
+  int Seed() const { return m * s + 1; }
+  int D() const { return Seed() + 1; }
+  int Cross() const { return D() + s * s; }
+  int Wa() const { return Cross() + m * s * s; }
+  int Wb() const { return Wa() + s * s; }
+  int RR() const { return Wb() + s * s; }
+  int size() const { return RR() + 1; }
+};
+
+__device__ __forceinline__ bool arn_skip(const ArnState* st) { return st->halt != 0; }
+
+// SStepArnoldi ctor scale (sstep.hpp:276-279). use_rn: reuse the residual norm computed by
+// checked_norm (same vector, same reduction => same value as the reference's norm2(v1)).
+__global__ void k_arn_ctor(ArnState* st, int use_rn, const double* partials, int G, int dNV, double* rec0,
+                           double* coef, int cInv) {
+  __shared__ double v[1];
+  if (!use_rn) reduce_dots_dev(partials, G, dNV, 1, v);
+  if (threadIdx.x == 0) {
+    st->status = kArnRunning;
+    st->halt = 0;
+    st->block = 0;
+    st->reorth = 0;
+    const double nv = use_rn ? st->rn : sqrt(v[0]);
+    rec0[RecLayout::kZn] = nv;
+    if (!(nv > 0.0)) {
+      st->status = kArnCtorZero;
+      st->halt = 1;
+      return;
+    }
+    coef[cInv] = 1.0 / nv;
+  }
+}
+
+// push_block (sstep.hpp:392-399): W = gram_self(block) -> GramSolver; breakdown = collapse
+__global__ void k_arn_push(ArnState* st, Gram* grams, int k, double* rec, const double* partials, int G, int dWa,
+                           int dWb, int s) {
+  if (arn_skip(st)) return;
+  __shared__ double v[kMaxS * kMaxS];
+  const int dW = st->reorth ? dWb : dWa;
+  reduce_dots_dev(partials, G, dW, s * s, v);
+  if (threadIdx.x == 0) {
+    double W[kMaxS * kMaxS];
+    for (int q = 0; q < s * s; ++q) W[q] = v[q];
+    for (int j = 0; j < s; ++j)
+      for (int l = j + 1; l < s; ++l) {
+        const double avg = (W[j * s + l] + W[l * s + j]) / 2.0;
+        W[j * s + l] = avg;
+        W[l * s + j] = avg;
+      }
+    for (int q = 0; q < s * s; ++q) rec[RecLayout::kW + q] = W[q];
+    Gram g;
+    gram_factor(g, W, s);
+    rec[RecLayout::kOk] = g.ok;
+    rec[RecLayout::kRatio] = g.ratio;
+    rec[RecLayout::kSing] = g.singular1;
+    if (!g.ok) {
+      st->status = k == 0 ? kArnCtorCollapse : kArnPushCollapse;
+      st->block = k;
+      st->halt = 1;
+      return;
+    }
+    grams[k] = g;
+  }
+}
+
+// Scalar1 (sstep.hpp:301-310): zn = ||z||, h_i = W_i^{-1} V_i^T z
+__global__ void k_arn_s1(ArnState* st, const Gram* grams, int k, double* rec, double* coef, const double* partials,
+                         int G, int dZ, int s, int cH, double* scratch) {
+  if (arn_skip(st)) return;
+  reduce_dots_dev(partials, G, dZ, k * s + 1, scratch);
+  if (threadIdx.x == 0) {
+    rec[RecLayout::kZn] = sqrt(scratch[k * s]);
+    rec[RecLayout::kReorth] = 0.0;
+    rec[RecLayout::kFirst] = -1.0;
+    st->reorth = 0;
+  }
+  const int hoff = RecLayout{s, 0}.h();
+  for (int i = threadIdx.x; i < k; i += blockDim.x) {
+    double rhs[kMaxS], h[kMaxS];
+    for (int l = 0; l < s; ++l) rhs[l] = scratch[i * s + l];
+    gram_solve(grams[i], rhs, h);
+    for (int l = 0; l < s; ++l) {
+      rec[hoff + i * s + l] = h[l];
+      coef[cH + i * s + l] = -h[l];
+    }
+  }
+}
+
+// nu = ||seed|| and the invariant-subspace test (sstep.hpp:315-324)
+__global__ void k_arn_s2(ArnState* st, int k, double* rec, double* coef, const double* partials, int G, int dSeed,
+                         int cInv) {
+  if (arn_skip(st)) return;
+  __shared__ double v[1];
+  reduce_dots_dev(partials, G, dSeed, 1, v);
+  if (threadIdx.x == 0) {
+    const double nu = sqrt(v[0]);
+    const double zn = rec[RecLayout::kZn];
+    rec[RecLayout::kNu] = nu;
+    if (nu <= 1e-14 * zn) {
+      rec[RecLayout::kInv] = 1.0;
+      st->status = kArnInvariant;
+      st->block = k;
+      st->halt = 1;
+      return;
+    }
+    coef[cInv] = 1.0 / nu;
+  }
+}
+
+// block-MGS Scalar2 against block i (sstep.hpp:338-353): t = W_i^{-1} (V_i^T cand[:,1:])
+__global__ void k_arn_t(ArnState* st, const Gram* grams, int i, double* rec, double* coef, const double* partials,
+                        int G, int dD, int s, int cT, int reorth_pass) {
+  if (arn_skip(st)) return;
+  if (reorth_pass && !st->reorth) return;
+  __shared__ double v[kMaxS * kMaxS];
+  const int nc = s - 1;
+  reduce_dots_dev(partials, G, dD, s * nc, v);
+  for (int jc = threadIdx.x; jc < nc; jc += blockDim.x) {
+    double rhs[kMaxS], t[kMaxS];
+    for (int l = 0; l < s; ++l) rhs[l] = v[l * nc + jc];
+    gram_solve(grams[i], rhs, t);
+    for (int l = 0; l < s; ++l) {
+      coef[cT + l * nc + jc] = -t[l];
+      double* ta = rec + i * s * s + l * s + (jc + 1);  // rec points at this block's T area
+      *ta = reorth_pass ? *ta + t[l] : t[l];
+    }
+  }
+}
+
+// needs_reorth (sstep.hpp:401-414) on the device-computed cross products
+__global__ void k_arn_check(ArnState* st, const Gram* grams, int k, double* rec, const double* partials, int G,
+                            int dCross, int dWa, int s, double orth_tol, double* scratch) {
+  if (arn_skip(st)) return;
+  reduce_dots_dev(partials, G, dCross, k * s * s, scratch);
+  reduce_dots_dev(partials, G, dWa, s * s, scratch + k * s * s);
+  if (threadIdx.x == 0) {
+    const double* W = scratch + k * s * s;
+    double cn2 = 0.0;
+    for (int jc = 0; jc < s; ++jc) cn2 += W[jc * s + jc];
+    int first = -1;
+    for (int i = 0; i < k; ++i) {
+      double acc = 0.0;
+      for (int q = 0; q < s * s; ++q) acc += scratch[i * s * s + q] * scratch[i * s * s + q];
+      if (sqrt(acc) > orth_tol * sqrt(sd_trace(grams[i].w, s)) * sqrt(cn2)) {
+        first = i;
+        break;
+      }
+    }
+    rec[RecLayout::kFirst] = first;
+    rec[RecLayout::kReorth] = first >= 0 ? 1.0 : 0.0;
+    st->reorth = first >= 0;
+  }
+}
+
+// r-norm after the cycle's residual update
+__global__ void k_arn_rn(ArnState* st, const double* partials, int G, int dRR, double* out) {
+  __shared__ double v[1];
+  reduce_dots_dev(partials, G, dRR, 1, v);
+  if (threadIdx.x == 0) {
+    st->rn = sqrt(v[0]);
+    *out = st->rn;
+  }
+}
+
+// ---------------------------------------------------------------- standard GMRES pieces
+struct GmState {
+  int status;  // 0 running, 1 happy breakdown
+  int halt;
+  int step;
+  int pad;
+  double rn;
+};
+
+__global__ void k_gm_start(GmState* st, double* coef, int cInv) {
+  if (threadIdx.x == 0) {
+    st->status = 0;
+    st->halt = 0;
+    st->step = 0;
+    coef[cInv] = 1.0 / st->rn;
+  }
+}
+
+// col_i = q_i . w ; coefficient -col_i for the MGS update (solvers.hpp:94-97)
+__global__ void k_gm_col(GmState* st, double* col, int i, double* coef, int cC, const double* partials, int G,
+                         int d0) {
+  if (st->halt) return;
+  __shared__ double v[1];
+  reduce_dots_dev(partials, G, d0, 1, v);
+  if (threadIdx.x == 0) {
+    col[i] = v[0];
+    coef[cC] = -v[0];
+  }
+}
+
+// hsub = ||w||, happy-breakdown test against ||col|| (solvers.hpp:100-109)
+__global__ void k_gm_sub(GmState* st, int j, double* col, double* coef, int cInv, const double* partials, int G,
+                         int d0) {
+  if (st->halt) return;
+  __shared__ double v[1];
+  reduce_dots_dev(partials, G, d0, 1, v);
+  if (threadIdx.x == 0) {
+    const double hsub = sqrt(v[0]);
+    col[j] = hsub;
+    double acc = 0.0;
+    for (int t = 0; t <= j; ++t) acc += col[t] * col[t];
+    const bool happy = hsub <= 1e-14 * sqrt(acc);
+    col[j + 1] = happy ? 1.0 : 0.0;  // flag stored past the column
+    st->step = j;
+    if (happy) {
+      st->status = 1;
+      st->halt = 1;
+      return;
+    }
+    coef[cInv] = 1.0 / hsub;
+  }
+}
+
+__global__ void k_gm_rn(GmState* st, const double* partials, int G, int d0) {
+  __shared__ double v[1];
+  reduce_dots_dev(partials, G, d0, 1, v);
+  if (threadIdx.x == 0) st->rn = sqrt(v[0]);
+}
+
+}  // namespace
+
+// ============================================================================ standard GMRES
+void gmres_device(Ctx& c, const Op& op, const double* f, double* x, uint64_t m64, double tol, uint64_t max_iterations,
+                  Report& rep) {
+  require(m64 >= 1, "gmres: restart length m must be at least 1");
+  require(m64 <= 4096, "gmres: restart length above the device limit of 4096");
+  const int m = (int)m64;
+  const int64_t n = op.n;
+  const size_t np = pad_n(n);
+  const Geo g = make_geo(n, c.sm_count);
+  skc_op_counter& cnt = rep.op_counts;
+  cnt.stored_vectors = m64 + 4;
+  double* V = (double*)c.workspace("gm_vec", (size_t)(m + 4) * np * sizeof(double));
+  double *r = V, *w = V + np, *ax = V + 2 * np, *Q = V + 3 * np;
+  auto q = [&](int i) { return Q + (size_t)i * np; };
+  const int cC = 0, cInv = 1, cM1 = 2, cY = 3, ncoef = 3 + m + 1;
+  double* coef = (double*)c.workspace("gm_coef", ncoef * sizeof(double));
+  double* partials = (double*)c.workspace("gm_partials", (size_t)2 * g.G * sizeof(double));
+  const int rstride = m + 3;
+  double* cols = (double*)c.workspace("gm_cols", (size_t)(m + 1) * rstride * sizeof(double));
+  GmState* st = (GmState*)c.workspace("gm_state", sizeof(GmState));
+  const int* halt = &st->halt;
+  {
+    double hc[3] = {0.0, 0.0, -1.0};
+    CK(cudaMemcpyAsync(coef, hc, sizeof hc, cudaMemcpyHostToDevice, c.stream));
+    GmState h{};
+    CK(cudaMemcpyAsync(st, &h, sizeof h, cudaMemcpyHostToDevice, c.stream));
+  }
+  auto residual = [&](bool x_zero) {
+    LinBuilder lb;
+    if (!x_zero) {
+      launch_apply(c, op.d, x, ax, nullptr, nullptr);
+      lb.add_out(r, f);
+      lb.add_term(ax, 1u, cM1);
+    } else {
+      lb.add_out(r, f);
+    }
+    lb.add_dot(0, 0);
+    lb.launch(c, g, coef, ncoef, partials, 0, nullptr, nullptr, "residual");
+    k_gm_rn<<<1, 256, 0, c.stream>>>(st, partials, g.G, 0);
+    ++c.launches;
+    GmState h;
+    CK(cudaMemcpyAsync(&h, st, sizeof h, cudaMemcpyDeviceToHost, c.stream));
+    c.sync();
+    return h.rn;
+  };
+  const bool x_zero = device_is_zero(c, x, n);
+  if (!x_zero) add(cnt, 0, 1, 1);
+  double rn = residual(x_zero);
+  cnt.termination_dots += 1;
+  rep.history.push_back(rn);
+  rep.op_history.push_back(cnt);
+  std::vector<double> hcols((size_t)(m + 1) * rstride);
+  while (rn > tol && rep.iterations < max_iterations) {
+    const int steps = (int)std::min<uint64_t>((uint64_t)m, max_iterations - rep.iterations);
+    CK(cudaMemsetAsync(cols, 0, (size_t)(m + 1) * rstride * sizeof(double), c.stream));
+    k_gm_start<<<1, 32, 0, c.stream>>>(st, coef, cInv);
+    ++c.launches;
+    {
+      LinBuilder lb;  // q_0 = r / ||r||
+      lb.add_out(q(0), r, cInv);
+      lb.launch(c, g, coef, ncoef, partials, 0, halt, nullptr, "scale");
+    }
+    for (int j = 1; j <= steps; ++j) {
+      double* col = cols + (size_t)j * rstride;
+      launch_apply(c, op.d, q(j - 1), w, halt, nullptr);
+      launch_gram_list(c, g, {q(0)}, {w}, partials, 0, halt, nullptr, "gram");
+      for (int i = 0; i < j; ++i) {
+        k_gm_col<<<1, 256, 0, c.stream>>>(st, col, i, coef, cC, partials, g.G, 0);
+        ++c.launches;
+        LinBuilder lb;  // w -= col_i q_i ; next dot
+        lb.add_out(w, w);
+        lb.add_term(q(i), 1u, cC);
+        if (i + 1 < j) {
+          lb.add_extra(q(i + 1));
+          lb.add_dot(1, 0);
+        } else {
+          lb.add_dot(0, 0);
+        }
+        lb.launch(c, g, coef, ncoef, partials, 0, halt, nullptr, "mgs_update");
+      }
+      k_gm_sub<<<1, 256, 0, c.stream>>>(st, j, col, coef, cInv, partials, g.G, 0);
+      ++c.launches;
+      LinBuilder lb;
+      lb.add_out(q(j), w, cInv);
+      lb.launch(c, g, coef, ncoef, partials, 0, halt, nullptr, "scale");
+    }
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(hcols.data(), cols, hcols.size() * sizeof(double), cudaMemcpyDeviceToHost, c.stream));
+    c.sync();
+    // host: the reference's inner loop on the recorded columns
+    add(cnt, 0, 0, 1);  // q1 scaling
+    HessLsq lsq(rn);
+    bool happy = false;
+    int inner = 0;
+    for (int j = 1; j <= steps; ++j) {
+      const double* col = hcols.data() + (size_t)j * rstride;
+      const bool hp = col[j + 1] != 0.0;
+      add(cnt, (uint64_t)j + 1, 1, (uint64_t)j + (hp ? 0 : 1));
+      ++inner;
+      ++rep.iterations;
+      const double rho = lsq.append_column(std::vector<double>(col, col + j + 1));
+      if (hp) {
+        happy = true;
+        break;
+      }
+      if (rho <= tol) break;
+    }
+    std::vector<double> y;
+    try {
+      y = lsq.solve();
+    } catch (const Error& e) {
+      rep.breakdown = e.msg;
+      break;
+    }
+    CK(cudaMemcpyAsync(coef + cY, y.data(), y.size() * sizeof(double), cudaMemcpyHostToDevice, c.stream));
+    {
+      LinBuilder lb;  // x += sum y_i q_i
+      lb.add_out(x, x);
+      for (size_t i = 0; i < y.size(); ++i) lb.add_term(q((int)i), 1u, cY + (int)i);
+      lb.launch(c, g, coef, ncoef, partials, 0, nullptr, nullptr, "x_update");
+    }
+    add(cnt, 0, 0, y.size());
+    add(cnt, 0, 1, 1);
+    ++rep.cycles;
+    rn = residual(false);
+    cnt.termination_dots += 1;
+    rep.history.push_back(rn);
+    if (inner == m && !happy) rep.op_history.push_back(cnt);
+    if (happy && rn > tol) {
+      rep.breakdown = "happy breakdown but residual above threshold";
+      break;
+    }
+  }
+  rep.converged = rn <= tol;
+  rep.final_residual = rep.history.back();
+}
+
+// ============================================================================ s-step Arnoldi engine
+namespace {
+
+struct Engine {
+  Ctx& c;
+  const Op& op;
+  int s, m;
+  Geo g;
+  size_t np;
+  RecLayout rl;
+  CoefLayout cl;
+  DotLayout dl;
+  double* V;  // (m+1) blocks of s columns
+  double *z, *seed, *r, *ax;
+  double* coef;
+  double* partials;
+  double* rec;
+  double* scratch;
+  double* rn_out;
+  Gram* grams;
+  ArnState* st;
+  const int* halt;
+
+  Engine(Ctx& ctx, const Op& o, int s_, int m_)
+      : c(ctx), op(o), s(s_), m(m_), rl{s_, m_}, cl{s_, m_}, dl{s_, m_} {
+    g = make_geo(op.n, c.sm_count);
+    np = pad_n(op.n);
+    const size_t nvec = (size_t)(m + 1) * s + 4;
+    V = (double*)c.workspace("arn_vec", nvec * np * sizeof(double));
+    z = V + (size_t)(m + 1) * s * np;
+    seed = z + np;
+    r = seed + np;
+    ax = r + np;
+    coef = (double*)c.workspace("arn_coef", (size_t)cl.size() * sizeof(double));
+    partials = (double*)c.workspace("arn_partials", (size_t)dl.size() * g.G * sizeof(double));
+    rec = (double*)c.workspace("arn_rec", (size_t)(m + 1) * rl.size() * sizeof(double));
+    scratch = (double*)c.workspace("arn_scratch", (size_t)(m * s * s + s * s + m * s + 8) * sizeof(double));
+    rn_out = (double*)c.workspace("arn_rn", 8 * sizeof(double));
+    grams = (Gram*)c.workspace("arn_grams", (size_t)(m + 1) * sizeof(Gram));
+    st = (ArnState*)c.workspace("arn_state", sizeof(ArnState));
+    halt = &st->halt;
+    std::vector<double> hc(cl.size(), 0.0);
+    hc[cl.M1()] = -1.0;
+    CK(cudaMemcpyAsync(coef, hc.data(), hc.size() * sizeof(double), cudaMemcpyHostToDevice, c.stream));
+    ArnState h{};
+    CK(cudaMemcpyAsync(st, &h, sizeof h, cudaMemcpyHostToDevice, c.stream));
+  }
+
+  double* col(int block, int j) const { return V + ((size_t)block * s + j) * np; }
+  double* recp(int k) const { return rec + (size_t)k * rl.size(); }
+
+  // [v, A v, .., A^{s-1} v] of v = src * coef[Inv] into block slot b
+  void krylov_into(int b, const double* src) {
+    LinBuilder lb;
+    lb.add_out(col(b, 0), src, cl.Inv());
+    lb.launch(c, g, coef, cl.size(), partials, 0, halt, nullptr, "scale");
+    for (int j = 1; j < s; ++j) launch_apply(c, op.d, col(b, j - 1), col(b, j), halt, nullptr);
+  }
+
+  void gram_self_into(int b, int dW, const int* cond) {
+    std::vector<const double*> B;
+    for (int j = 0; j < s; ++j) B.push_back(col(b, j));
+    launch_gram_list(c, g, B, B, partials, dW, halt, cond, "gram_w");
+  }
+
+  // SStepArnoldi ctor on device vector v (use_rn: its norm is st->rn)
+  void ctor(const double* v, bool use_rn) {
+    CK(cudaMemsetAsync(rec, 0, (size_t)(m + 1) * rl.size() * sizeof(double), c.stream));
+    if (!use_rn) launch_gram_list(c, g, {v}, {v}, partials, dl.RR(), nullptr, nullptr, "gram");
+    k_arn_ctor<<<1, 256, 0, c.stream>>>(st, use_rn ? 1 : 0, partials, g.G, dl.RR(), recp(0), coef, cl.Inv());
+    ++c.launches;
+    krylov_into(0, v);
+    gram_self_into(0, dl.Wa(), nullptr);
+    k_arn_push<<<1, 256, 0, c.stream>>>(st, grams, 0, recp(0), partials, g.G, dl.Wa(), dl.Wb(), s);
+    ++c.launches;
+    CK(cudaGetLastError());
+  }
+
+  // SStepArnoldi::advance for block iteration k (1-based), sstep.hpp:297-379
+  void advance(int k, bool build_next) {
+    double* rk = recp(k);
+    // z = A v_k^s ; Scalar1 dots V_i^T z and ||z||^2
+    launch_apply(c, op.d, col(k - 1, s - 1), z, halt, nullptr);
+    {
+      std::vector<const double*> L;
+      for (int i = 0; i < k; ++i)
+        for (int l = 0; l < s; ++l) L.push_back(col(i, l));
+      L.push_back(z);
+      launch_gram_list(c, g, L, {z}, partials, dl.Z(), halt, nullptr, "gram_z");
+    }
+    k_arn_s1<<<1, 256, 0, c.stream>>>(st, grams, k, rk, coef, partials, g.G, dl.Z(), s, cl.H(), scratch);
+    ++c.launches;
+    // seed = z - sum_i V_i h_i ; ||seed||^2
+    {
+      LinBuilder lb;
+      lb.add_out(seed, z);
+      for (int i = 0; i < k; ++i)
+        for (int l = 0; l < s; ++l) lb.add_term(col(i, l), 1u, cl.H() + i * s + l);
+      lb.add_dot(0, 0);
+      lb.launch(c, g, coef, cl.size(), partials, dl.Seed(), halt, nullptr, "seed_update");
+    }
+    k_arn_s2<<<1, 256, 0, c.stream>>>(st, k, rk, coef, partials, g.G, dl.Seed(), cl.Inv());
+    ++c.launches;
+    // candidate block [v, .., A^{s-1} v] of the normalized seed (also on the last block)
+    const int cb = k;  // block slot k (slot m is scratch when k == m)
+    krylov_into(cb, seed);
+    if (!build_next) {
+      CK(cudaGetLastError());
+      return;
+    }
+    double* tk = rk + rl.t();
+    if (s > 1) {
+      for (int pass = 0; pass < 2; ++pass) {
+        const int* cond = pass ? &st->reorth : nullptr;
+        std::vector<const double*> Cr;
+        for (int jc = 1; jc < s; ++jc) Cr.push_back(col(cb, jc));
+        {
+          std::vector<const double*> L;
+          for (int l = 0; l < s; ++l) L.push_back(col(0, l));
+          launch_gram_list(c, g, L, Cr, partials, dl.D(), halt, cond, "gram_mgs");
+        }
+        for (int i = 0; i < k; ++i) {
+          k_arn_t<<<1, 256, 0, c.stream>>>(st, grams, i, tk, coef, partials, g.G, dl.D(), s, cl.T(), pass);
+          ++c.launches;
+          LinBuilder lb;  // cand[:,jc] -= sum_l t(l,jc-1) V_i[:,l]  (+ dots with V_{i+1})
+          for (int jc = 1; jc < s; ++jc) lb.add_out(col(cb, jc), col(cb, jc));
+          const uint16_t mask = (uint16_t)((1u << (s - 1)) - 1u);
+          for (int l = 0; l < s; ++l) lb.add_term(col(i, l), mask, cl.T() + l * (s - 1));
+          if (i + 1 < k) {
+            for (int l = 0; l < s; ++l) lb.add_extra(col(i + 1, l));
+            for (int l = 0; l < s; ++l)
+              for (int jc = 1; jc < s; ++jc) lb.add_dot((s - 1) + l, jc - 1);
+          }
+          lb.launch(c, g, coef, cl.size(), partials, dl.D(), halt, cond, "mgs_update");
+        }
+        if (pass == 0) {
+          // reorthogonalization test: V_i^T cand (all columns) and cand^T cand
+          std::vector<const double*> L, Cc;
+          for (int i = 0; i < k; ++i)
+            for (int l = 0; l < s; ++l) L.push_back(col(i, l));
+          for (int jc = 0; jc < s; ++jc) Cc.push_back(col(cb, jc));
+          launch_gram_list(c, g, L, Cc, partials, dl.Cross(), halt, nullptr, "gram_cross");
+          gram_self_into(cb, dl.Wa(), nullptr);
+          k_arn_check<<<1, 256, 0, c.stream>>>(st, grams, k, rk, partials, g.G, dl.Cross(), dl.Wa(), s, 1e-8,
+                                               scratch);
+          ++c.launches;
+        } else {
+          gram_self_into(cb, dl.Wb(), cond);
+        }
+      }
+    } else {
+      gram_self_into(cb, dl.Wa(), nullptr);
+    }
+    k_arn_push<<<1, 256, 0, c.stream>>>(st, grams, cb, rk, partials, g.G, dl.Wa(), dl.Wb(), s);
+    ++c.launches;
+    CK(cudaGetLastError());
+  }
+
+  ArnState read_state() {
+    ArnState h;
+    CK(cudaMemcpyAsync(&h, st, sizeof h, cudaMemcpyDeviceToHost, c.stream));
+    c.sync();
+    return h;
+  }
+};
+
+// Host mirror of the engine bookkeeping that the reference keeps (tcoeffs_, gcols_) and the
+// op counts of each advance (sstep.hpp:297-379).
+struct HostArn {
+  int s, m;
+  RecLayout rl;
+  std::vector<double> recs;  // copied records
+  std::vector<std::vector<double>> gcols;
+
+  const double* rec(int k) const { return recs.data() + (size_t)k * rl.size(); }
+  double tco(int q, int i, int l, int c) const { return rec(q)[rl.t() + i * s * s + l * s + c]; }
+
+  // append_g_columns (sstep.hpp:422-445); tcoeffs_[q] = records of block iteration q (q>=1)
+  void append_g(int k) {
+    const int q = k - 1;
+    const double* rk = rec(k);
+    for (int cloc = 0; cloc + 1 < s; ++cloc) {
+      std::vector<double> col((size_t)q * s + cloc + 2, 0.0);
+      col[(size_t)q * s + cloc + 1] += 1.0;
+      const int ntq = q;  // block q was orthogonalized against blocks 0..q-1
+      for (int i = 0; i < ntq; ++i) {
+        for (int l = 0; l < s; ++l) col[(size_t)i * s + l] += tco(q, i, l, cloc + 1);
+        for (int lc = 0; lc < s; ++lc) {
+          const double coefv = tco(q, i, lc, cloc);
+          if (coefv == 0.0) continue;
+          const auto& prev = gcols[(size_t)i * s + lc];
+          for (size_t row = 0; row < prev.size(); ++row) col[row] -= coefv * prev[row];
+        }
+      }
+      gcols.push_back(std::move(col));
+    }
+    std::vector<double> last((size_t)k * s + 1, 0.0);
+    for (int i = 0; i < k; ++i)
+      for (int l = 0; l < s; ++l) last[(size_t)i * s + l] = rk[rl.h() + i * s + l];
+    last[(size_t)k * s] = rk[RecLayout::kNu];
+    gcols.push_back(std::move(last));
+  }
+
+  std::vector<double> W(int k) const {
+    const double* r = rec(k);
+    return std::vector<double>(r + RecLayout::kW, r + RecLayout::kW + s * s);
+  }
+
+  // op counts of advance(k, build_next); stage: 0 = complete, 1 = invariant return,
+  // 2 = push_block threw (counts through the Gram products)
+  void count_advance(skc_op_counter& c, int k, bool build_next, int stage) const {
+    const uint64_t S = s;
+    add(c, (uint64_t)k * S + 1, 1, (uint64_t)k * S);  // z, Scalar1, seed, nu
+    if (stage == 1) return;
+    add(c, 0, S - 1, 1);  // scale + candidate block
+    if (!build_next) return;
+    if (s > 1) {
+      add(c, (uint64_t)k * S * (S - 1), 0, (uint64_t)k * S * (S - 1));
+      const double* r = rec(k);
+      const int first = (int)r[RecLayout::kFirst];
+      const bool reorth = r[RecLayout::kReorth] != 0.0;
+      add(c, S + S * S * (uint64_t)(reorth ? first + 1 : k), 0, 0);
+      if (reorth) add(c, (uint64_t)k * S * (S - 1), 0, (uint64_t)k * S * (S - 1));
+    }
+    add(c, S * (S + 1) / 2, 0, 0);  // push_block Gram
+  }
+};
+
+}  // namespace
+
+// ============================================================================ s-GMRES
+void sgmres_device(Ctx& c, const Op& op, const double* f, double* x, const SStepCfg& cfg, Report& rep) {
+  require(cfg.m >= 1, "s-gmres: m must be at least 1");
+  validate_block_size(cfg, rep);
+  if (cfg.s == 1) {  // sstep.hpp:498-508
+    Report sub;
+    gmres_device(c, op, f, x, cfg.m, cfg.tol, cfg.max_iterations, sub);
+    sub.notes = rep.notes;
+    rep = std::move(sub);
+    return;
+  }
+  require(cfg.m <= 64, "s-gmres: m above the device limit of 64 blocks");
+  const int s = (int)cfg.s, m = (int)cfg.m;
+  skc_op_counter& cnt = rep.op_counts;
+  cnt.stored_vectors = (uint64_t)(m + 2) * s + 2;
+  Engine E(c, op, s, m);
+  HostArn H{s, m, E.rl, {}, {}};
+  H.recs.resize((size_t)(m + 1) * E.rl.size());
+
+  const bool x_zero = device_is_zero(c, x, op.n);
+  auto residual = [&](bool xz) {
+    LinBuilder lb;
+    if (!xz) {
+      launch_apply(c, op.d, x, E.ax, nullptr, nullptr);
+      lb.add_out(E.r, f);
+      lb.add_term(E.ax, 1u, E.cl.M1());
+    } else {
+      lb.add_out(E.r, f);
+    }
+    lb.add_dot(0, 0);
+    lb.launch(c, E.g, E.coef, E.cl.size(), E.partials, E.dl.RR(), nullptr, nullptr, "residual");
+    k_arn_rn<<<1, 256, 0, c.stream>>>(E.st, E.partials, E.g.G, E.dl.RR(), E.rn_out);
+    ++c.launches;
+    double h;
+    CK(cudaMemcpyAsync(&h, E.rn_out, sizeof h, cudaMemcpyDeviceToHost, c.stream));
+    c.sync();
+    return h;
+  };
+  if (!x_zero) add(cnt, 0, 1, 1);
+  double rn = residual(x_zero);
+  cnt.termination_dots += 1;
+  rep.history.push_back(rn);
+  rep.op_history.push_back(cnt);
+
+  // sstep.hpp:518-543
+  auto run_fallback = [&]() -> bool {
+    Report sub;
+    gmres_device(c, op, f, x, (uint64_t)s * m, cfg.tol, (uint64_t)s * m, sub);
+    rep.iterations += sub.iterations;
+    rep.cycles += sub.cycles;
+    ++rep.fallback_cycles;
+    cnt.dotprods += sub.op_counts.dotprods;
+    cnt.matvecs += sub.op_counts.matvecs;
+    cnt.vec_updates += sub.op_counts.vec_updates;
+    cnt.termination_dots += sub.op_counts.termination_dots;
+    for (size_t i = 1; i < sub.history.size(); ++i) rep.history.push_back(sub.history[i]);
+    add(cnt, 0, 1, 1);
+    rn = residual(false);
+    cnt.termination_dots += 1;
+    rep.op_history.push_back(cnt);
+    return rn <= cfg.tol;
+  };
+
+  while (rn > cfg.tol && rep.iterations < cfg.max_iterations) {
+    bool collapsed = false, exhausted = false;
+    std::string collapse_msg;
+    int blocks_done = 0;
+    // ---- enqueue the whole cycle, then read it back
+    E.ctor(E.r, true);
+    for (int k = 1; k <= m; ++k) E.advance(k, k < m);
+    ArnState hs = E.read_state();
+    CK(cudaMemcpy(H.recs.data(), E.rec, H.recs.size() * sizeof(double), cudaMemcpyDeviceToHost));
+    H.gcols.clear();
+    if (hs.status == kArnCtorZero) fail(SKC_EINVAL, "s-arnoldi: start vector is zero");
+    add(cnt, (uint64_t)s * (s + 1) / 2, (uint64_t)s - 1, 1);  // ctor: scale, krylov_block, push
+    if (hs.status == kArnCtorCollapse) {
+      collapse_msg = gram_message((int)H.rec(0)[RecLayout::kSing], H.rec(0)[RecLayout::kRatio]);
+      if (!run_fallback()) {
+        if (rep.iterations >= cfg.max_iterations) break;
+        continue;
+      }
+      break;
+    }
+    std::vector<std::vector<double>> lblocks;
+    {
+      std::vector<double> L0(s * s);
+      if (!cholesky_upper(H.W(0).data(), s, L0.data())) fail(SKC_EBREAKDOWN, "cholesky: matrix not positive definite");
+      lblocks.push_back(L0);
+    }
+    HessLsq lsq(rn * lblocks[0][0]);
+    auto apply_l = [&](const std::vector<double>& gv) {  // sstep.hpp:566-579
+      std::vector<double> out(gv);
+      for (size_t bi = 0; bi < lblocks.size() && bi * s < gv.size(); ++bi) {
+        const std::vector<double>& lb = lblocks[bi];
+        const size_t off = bi * s;
+        for (size_t rl = 0; rl < (size_t)s && off + rl < gv.size(); ++rl) {
+          double acc = 0.0;
+          for (size_t jl = rl; jl < (size_t)s && off + jl < gv.size(); ++jl) acc += lb[rl * s + jl] * gv[off + jl];
+          out[off + rl] = acc;
+        }
+      }
+      return out;
+    };
+    for (int k = 1; k <= m; ++k) {
+      const bool stopped_here = hs.status != kArnRunning && hs.block == k;
+      const bool invariant = stopped_here && hs.status == kArnInvariant;
+      const bool push_fail = stopped_here && hs.status == kArnPushCollapse;
+      H.count_advance(cnt, k, k < m, invariant ? 1 : 0);
+      H.append_g(k);
+      if (push_fail) {
+        collapsed = true;
+        collapse_msg = gram_message((int)H.rec(k)[RecLayout::kSing], H.rec(k)[RecLayout::kRatio]);
+        break;
+      }
+      const bool more = !invariant;
+      if (k < m && more) {
+        std::vector<double> Lk(s * s);
+        if (!cholesky_upper(H.W(k).data(), s, Lk.data())) {
+          collapsed = true;
+          collapse_msg = "cholesky: matrix not positive definite";
+          break;
+        }
+        lblocks.push_back(Lk);
+      }
+      double rho = lsq.residual_norm();
+      for (int lc = 0; lc < s; ++lc) rho = lsq.append_column(apply_l(H.gcols[(size_t)(k - 1) * s + lc]));
+      rep.block_rho.push_back(rho);
+      rep.iterations += s;
+      blocks_done = k;
+      if (!more) {
+        exhausted = true;
+        break;
+      }
+      if (rho <= cfg.tol) break;
+    }
+    const bool attainable = lsq.columns() > 0 && lsq.residual_norm() <= cfg.tol;
+    if (collapsed && !attainable) {
+      if (!run_fallback()) {
+        if (rep.iterations >= cfg.max_iterations) {
+          rep.breakdown = "basis collapse (" + collapse_msg + ")";
+          break;
+        }
+        continue;
+      }
+      break;
+    }
+    std::vector<double> y;
+    try {
+      y = lsq.solve();
+    } catch (const Error& e) {
+      rep.breakdown = e.msg;
+      break;
+    }
+    // x += sum_bi sum_lc y V ; r = f - A x (sstep.hpp:622-633)
+    CK(cudaMemcpyAsync(E.coef + E.cl.Y(), y.data(), y.size() * sizeof(double), cudaMemcpyHostToDevice, c.stream));
+    {
+      LinBuilder lb;
+      lb.add_out(x, x);
+      for (int bi = 0; bi < blocks_done; ++bi)
+        for (int lc = 0; lc < s; ++lc) lb.add_term(E.col(bi, lc), 1u, E.cl.Y() + bi * s + lc);
+      lb.launch(c, E.g, E.coef, E.cl.size(), E.partials, 0, nullptr, nullptr, "x_update");
+    }
+    add(cnt, 0, 0, (uint64_t)blocks_done * s);
+    add(cnt, 0, 1, 1);
+    ++rep.cycles;
+    rn = residual(false);
+    cnt.termination_dots += 1;
+    rep.history.push_back(rn);
+    if (blocks_done == m && !exhausted && !collapsed) rep.op_history.push_back(cnt);
+    if (rn <= cfg.tol) break;
+    if (collapsed) {
+      if (!run_fallback() && rep.iterations >= cfg.max_iterations) {
+        rep.breakdown = "basis collapse (" + collapse_msg + ")";
+        break;
+      }
+      if (rn <= cfg.tol) break;
+      continue;
+    }
+    if (exhausted) {
+      rep.breakdown = "invariant subspace reached with residual above threshold";
+      break;
+    }
+  }
+  rep.converged = rn <= cfg.tol;
+  rep.final_residual = rep.history.back();
+}
+
+// ============================================================================ sarnoldi
+void sarnoldi_device(Ctx& c, const Op& op, const double* v1, uint64_t s64, uint64_t m64, BasisOut& out) {
+  require(s64 >= 1, "sarnoldi: s must be at least 1");
+  require(m64 >= 1, "sarnoldi: m_blocks must be at least 1");
+  require(s64 * m64 <= (uint64_t)op.n, "sarnoldi: s * m_blocks exceeds the dimension");
+  require(s64 <= (uint64_t)kMaxS, "sarnoldi: s above the supported block width 8");
+  require(m64 <= 64, "sarnoldi: m_blocks above the device limit of 64");
+  const int s = (int)s64, m = (int)m64;
+  Engine E(c, op, s, m);
+  HostArn H{s, m, E.rl, {}, {}};
+  H.recs.resize((size_t)(m + 1) * E.rl.size());
+  E.ctor(v1, false);
+  for (int k = 1; k <= m; ++k) E.advance(k, k < m);
+  ArnState hs = E.read_state();
+  CK(cudaMemcpy(H.recs.data(), E.rec, H.recs.size() * sizeof(double), cudaMemcpyDeviceToHost));
+  if (hs.status == kArnCtorZero) fail(SKC_EINVAL, "s-arnoldi: start vector is zero");
+  if (hs.status == kArnCtorCollapse)
+    fail(SKC_EBREAKDOWN, gram_message((int)H.rec(0)[RecLayout::kSing], H.rec(0)[RecLayout::kRatio]));
+  skc_op_counter& cnt = out.counter;
+  add(cnt, (uint64_t)s * (s + 1) / 2, (uint64_t)s - 1, 1);
+  for (int k = 1; k <= m; ++k) {
+    const bool stopped_here = hs.status != kArnRunning && hs.block == k;
+    if (stopped_here && hs.status == kArnPushCollapse) {
+      H.count_advance(cnt, k, k < m, 0);
+      fail(SKC_EBREAKDOWN, gram_message((int)H.rec(k)[RecLayout::kSing], H.rec(k)[RecLayout::kRatio]));
+    }
+    if (stopped_here && hs.status == kArnInvariant) {
+      H.count_advance(cnt, k, k < m, 1);
+      fail(SKC_EBREAKDOWN, "sarnoldi: invariant subspace at block " + std::to_string(k));
+    }
+    H.count_advance(cnt, k, k < m, 0);
+    H.append_g(k);
+  }
+  const size_t n = (size_t)op.n, np = E.np;
+  out.blocks.assign((size_t)m * s * n, 0.0);
+  for (int b = 0; b < m; ++b)
+    for (int j = 0; j < s; ++j)
+      CK(cudaMemcpy(out.blocks.data() + ((size_t)b * s + j) * n, E.col(b, j), n * sizeof(double),
+                    cudaMemcpyDeviceToHost));
+  out.grams.assign((size_t)m * s * s, 0.0);
+  for (int b = 0; b < m; ++b) {
+    const auto w = H.W(b);
+    std::copy(w.begin(), w.end(), out.grams.begin() + (size_t)b * s * s);
+  }
+  const size_t rows = (size_t)(m + 1) * s, cols = (size_t)m * s;
+  out.hess.assign(rows * cols, 0.0);
+  for (size_t j = 0; j < H.gcols.size(); ++j)
+    for (size_t i = 0; i < H.gcols[j].size(); ++i) out.hess[i * cols + j] = H.gcols[j][i];
+  out.seed.assign(n, 0.0);
+  CK(cudaMemcpy(out.seed.data(), E.col(m, 0), n * sizeof(double), cudaMemcpyDeviceToHost));
+  out.seed_norm = H.rec(m)[RecLayout::kNu];
+  (void)np;
+}
+
+}  // namespace skc

@@ -1,0 +1,220 @@
+// skc_internal.hpp -- shared types of libskrylov_b200: device operator descriptor,
+// streaming-kernel descriptors, the per-thread context and error plumbing.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdint>
+#include <map>
+#include <memory>
+#include <optional>
+#include <string>
+#include <vector>
+
+#include "../../include/skrylov_b200.h"
+#include "small_dense.cuh"
+
+namespace skc {
+
+// ---------------------------------------------------------------- errors
+struct Error {
+  int code;
+  std::string msg;
+};
+[[noreturn]] void fail(int code, const std::string& msg);
+void require(bool ok, const std::string& what);  // kernels.hpp:41-43 -> SKC_EINVAL
+void cuda_check(cudaError_t e, const char* what, const char* file, int line);
+#define CK(call) ::skc::cuda_check((call), #call, __FILE__, __LINE__)
+
+// ---------------------------------------------------------------- operator
+enum OpKind : int { kCsr = 0, kStencilConst = 1, kStencilVarK = 2, kStencilDia = 3 };
+
+// Passed by value to kernels. Natural ordering, x fastest.
+struct DevOp {
+  int kind;
+  int dim;
+  int64_t nx, ny, nz, n;
+  double coef[7];  // -z,-y,-x,C,+x,+y,+z
+  double ch2;
+  const double* kcell;   // kStencilVarK
+  const double* dia;     // kStencilDia: 7 slabs of n values (slot-major), 0 where absent
+  const int64_t* rowptr; // kCsr
+  const int32_t* colidx;
+  const double* vals;
+};
+
+struct Op {
+  DevOp d{};
+  int64_t n = 0;
+  int64_t rows = 1;      // grid rows (2D: ny, 3D: ny*nz) for reporting
+  std::vector<void*> owned;  // device allocations
+  int device = 0;
+  ~Op();
+};
+
+// ---------------------------------------------------------------- streaming geometry
+// Every streaming kernel of a solve uses the same fixed CTA decomposition of [0, n):
+// CTA g owns the contiguous range [g*range, min(n,(g+1)*range)) and writes one partial per
+// dot, so reductions are deterministic (fixed order, no atomics).
+struct Geo {
+  int64_t n = 0;
+  int G = 1;
+  int64_t range = 0;
+};
+Geo make_geo(int64_t n, int sm_count);
+
+constexpr int kThreads = 256;
+
+// y_o = base_o [* coef[bscale_o]] + sum_j coef[cbase_j + o] * in_j   (j ascending, o in mask_j)
+// then dots over value ids: 0..nout-1 = outputs, nout..nout+nx-1 = extra inputs.
+constexpr int LC_MAXIN = 40, LC_MAXOUT = 16, LC_MAXX = 8, LC_MAXD = 64;
+struct LinDesc {
+  int nin, nout, nx, nd;
+  int ncoef;
+  const double* in[LC_MAXIN];
+  uint16_t mask[LC_MAXIN];
+  int16_t cbase[LC_MAXIN];
+  double* out[LC_MAXOUT];
+  const double* base[LC_MAXOUT];
+  int16_t bscale[LC_MAXOUT];
+  const double* xin[LC_MAXX];
+  uint8_t da[LC_MAXD], db[LC_MAXD];
+  const double* coef;  // device coefficient array
+  double* partials;    // [(dot0 + d) * G + g]
+  int dot0, G;
+  int64_t n, range;
+  const int* halt;     // skip when *halt != 0
+  const int* cond;     // skip when cond != nullptr && *cond == 0
+};
+
+// dots L_l . R_r, dot index (l * nr + r)
+constexpr int GR_MAXL = 80, GR_MAXR = 8, GR_LB = 4;
+struct GramDesc {
+  int nl, nr;
+  const double* L[GR_MAXL];
+  const double* R[GR_MAXR];
+  double* partials;
+  int dot0, G;
+  int64_t n, range;
+  const int* halt;
+  const int* cond;
+};
+
+// ---------------------------------------------------------------- context
+struct KStat {
+  uint64_t launches = 0;
+  double ms = 0.0;
+  double bytes = 0.0;
+};
+
+struct Ctx {
+  int device = 0;
+  int sm_count = 148;
+  cudaStream_t stream = nullptr;
+  cudaStream_t own_stream = nullptr;
+  uint64_t launches = 0;
+  bool profiling = false;
+  std::map<std::string, KStat> stats;
+  struct Pending {
+    std::string name;
+    cudaEvent_t a, b;
+    double bytes;
+  };
+  std::vector<Pending> pending;
+  std::vector<cudaEvent_t> event_pool;
+  // workspace cache (grows, never shrinks while the context lives)
+  std::map<std::string, std::pair<void*, size_t>> ws;
+  double* pinned = nullptr;
+  size_t pinned_cap = 0;
+
+  void* workspace(const std::string& tag, size_t bytes);
+  double* host_stage(size_t doubles);
+  // profiling bracket around one launch
+  int prof_begin();
+  void prof_end(int token, const char* name, double bytes);
+  void prof_collect();
+  void sync();
+  ~Ctx();
+};
+
+// RAII launch bracket
+struct Launch {
+  Ctx& c;
+  int tok;
+  const char* name;
+  double bytes;
+  Launch(Ctx& ctx, const char* nm, double b) : c(ctx), tok(ctx.prof_begin()), name(nm), bytes(b) {
+    ++ctx.launches;
+  }
+  ~Launch() { c.prof_end(tok, name, bytes); }
+};
+
+// ---------------------------------------------------------------- kernel launchers (kernels.cu)
+void launch_apply(Ctx& c, const DevOp& op, const double* x, double* y, const int* halt, const int* cond);
+void launch_lincomb(Ctx& c, const LinDesc& d, const char* name = "lincomb");
+void launch_gram(Ctx& c, const GramDesc& d, const char* name = "gram");
+void launch_fill(Ctx& c, double* p, double v, int64_t n);
+// operator helpers
+void build_stencil_op(Ctx& c, Op& op, const skc_stencil_desc& d, const double* kcell_host);
+void build_csr_op(Ctx& c, Op& op, int64_t n, const uint64_t* offs, const uint64_t* cols, const double* vals);
+
+// ---------------------------------------------------------------- reports (host)
+struct Report {
+  bool converged = false;
+  uint64_t iterations = 0, cycles = 0;
+  std::vector<double> history;
+  double final_residual = 0.0;
+  skc_op_counter op_counts{};
+  std::vector<skc_op_counter> op_history;
+  uint64_t steady_iteration = 0;
+  std::optional<std::string> breakdown;
+  uint64_t fallback_cycles = 0;
+  std::vector<std::string> notes;
+  std::vector<double> block_rho;
+};
+
+struct SStepCfg {
+  uint64_t s = 2, k = 2, m = 5;
+  double tol = 1e-6;
+  uint64_t max_iterations = 100000;
+  bool precondition = false, unbounded_window = false, debug_checks = false;
+  double divergence_factor = 10.0;
+};
+
+// solver entry points (device pointers f, x)
+void somin_device(Ctx& c, const Op& op, const double* f, double* x, const SStepCfg& cfg, Report& rep);
+void smr_device(Ctx& c, const Op& op, const double* f, double* x, const SStepCfg& cfg, Report& rep);
+void sgmres_device(Ctx& c, const Op& op, const double* f, double* x, const SStepCfg& cfg, Report& rep);
+void gmres_device(Ctx& c, const Op& op, const double* f, double* x, uint64_t m, double tol,
+                  uint64_t max_iterations, Report& rep);
+struct BasisOut {
+  std::vector<double> blocks, grams, hess, seed;
+  double seed_norm = 0.0;
+  skc_op_counter counter{};
+};
+void sarnoldi_device(Ctx& c, const Op& op, const double* v1_dev, uint64_t s, uint64_t m_blocks, BasisOut& out);
+void smr_step_device(Ctx& c, const Op& op, double* x, double* r, uint64_t s, double* coeffs,
+                     skc_op_counter* counter);
+
+// host Hessenberg LSQ (small_dense.hpp:239-307), run on the host on device-computed columns
+class HessLsq {
+ public:
+  explicit HessLsq(double beta) : rhs_{beta}, residual_(std::fabs(beta)) {}
+  size_t columns() const { return rcols_.size(); }
+  double residual_norm() const { return residual_; }
+  double matrix_norm() const;
+  double append_column(std::vector<double> col);
+  // throws Error{SKC_EBREAKDOWN} on rank deficiency
+  std::vector<double> solve() const;
+
+ private:
+  std::vector<std::vector<double>> rcols_;
+  std::vector<double> cos_, sin_, rhs_;
+  double residual_;
+  double gnorm_sq_ = 0.0;
+};
+
+std::string fmt_double(double v);  // std::to_string(double)
+
+}  // namespace skc
