@@ -191,6 +191,11 @@ class Oracle:
             self.lib.orc_build_stencil_csr.restype = C.c_int
             self.lib.orc_csr_free.argtypes = [P(u64), P(u64), P(dbl)]
             self.lib.orc_stencil_apply.argtypes = [i32, u64, u64, u64, P(dbl), P(dbl), dbl, P(dbl), P(dbl)]
+            self.lib.orc_set_dot_mode.argtypes = [C.c_int]
+
+    def set_dot_mode(self, mode: int):
+        """0: the reference's sequential summation; 1: blocked/tree (envelope measurement only)."""
+        self.lib.orc_set_dot_mode(mode)
 
     # ------------------------------------------------------------------ solvers
     def _collect(self, rep, x):

@@ -81,7 +81,58 @@ static void* xcalloc(size_t n, size_t sz) { return calloc(n ? n : 1, sz); }
 
 /* ------------------------------------------------------------------ */
 /* L0 kernels: kernels.hpp:45-74 (ascending-index summation) */
+/* Summation-order perturbation used only to MEASURE the reference's own rounding envelope
+ * (SURVEY.md 8(c)): mode 0 = the reference's sequential order; mode 1 = 8-lane partials in
+ * 1024-element chunks combined by a pairwise tree (GPU-like); mode 2 = reversed order;
+ * mode 3 = compensated (near-exact) summation. */
+static int g_dot_mode = 0;
+void orc_set_dot_mode(int mode) { g_dot_mode = mode; }
+
+static double dot_tree(uint64_t n, const double* a, const double* b) {
+  enum { CH = 1024, LANES = 8 };
+  const uint64_t nch = (n + CH - 1) / CH;
+  double stackbuf[64];
+  double* part = nch <= 64 ? stackbuf : (double*)malloc((size_t)nch * sizeof(double));
+  for (uint64_t c = 0; c < nch; ++c) {
+    double lane[LANES] = {0};
+    const uint64_t i0 = c * CH, i1 = i0 + CH < n ? i0 + CH : n;
+    for (uint64_t i = i0; i < i1; ++i) lane[(i - i0) % LANES] += a[i] * b[i];
+    for (int w = LANES / 2; w >= 1; w /= 2)
+      for (int l = 0; l < w; ++l) lane[l] += lane[l + w];
+    part[c] = lane[0];
+  }
+  uint64_t m = nch;
+  while (m > 1) {
+    const uint64_t h = (m + 1) / 2;
+    for (uint64_t i = 0; i + h < m; ++i) part[i] += part[i + h];
+    m = h;
+  }
+  const double r = nch ? part[0] : 0.0;
+  if (part != stackbuf) free(part);
+  return r;
+}
+
+static double dot_reverse(uint64_t n, const double* a, const double* b) {
+  double acc = 0.0;
+  for (uint64_t i = n; i-- > 0;) acc += a[i] * b[i];
+  return acc;
+}
+
+static double dot_compensated(uint64_t n, const double* a, const double* b) {
+  /* Neumaier-compensated sum of the rounded products: close to the exact sum */
+  double s = 0.0, c = 0.0;
+  for (uint64_t i = 0; i < n; ++i) {
+    const double p = a[i] * b[i], t = s + p;
+    c += fabs(s) >= fabs(p) ? (s - t) + p : (p - t) + s;
+    s = t;
+  }
+  return s + c;
+}
+
 double orc_dot(uint64_t n, const double* a, const double* b) {
+  if (g_dot_mode == 1) return dot_tree(n, a, b);
+  if (g_dot_mode == 2) return dot_reverse(n, a, b);
+  if (g_dot_mode == 3) return dot_compensated(n, a, b);
   double acc = 0.0;
   for (uint64_t i = 0; i < n; ++i) acc += a[i] * b[i];
   return acc;

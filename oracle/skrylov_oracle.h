@@ -80,6 +80,8 @@ void orc_report_free(orc_report* r);
 /* kernels.hpp / sparse.hpp */
 void orc_spmv(const orc_csr* a, const double* x, double* y);
 double orc_dot(uint64_t n, const double* a, const double* b);
+/* 0 = reference sequential order (default); 1 = blocked/tree order to measure the envelope */
+void orc_set_dot_mode(int mode);
 int orc_krylov_block(const orc_csr* a, const double* v, uint64_t s, double* out /* n*s col-major */);
 
 /* small_dense.hpp: Gram solver (order <= 16). Returns 0 or 2 (breakdown) with message. */

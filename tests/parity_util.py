@@ -7,12 +7,19 @@ import numpy as np
 from golden_util import case, matrix
 
 
-def rel_hist(h1, h2, upto=51):
+def rel_hist(h1, h2, upto=51, floor=1e-9):
+    """max relative difference over the first `upto` entries, skipping entries below
+    floor * h[0] in both histories (the reference KATs' convention, test_sstep.cpp:214,362)."""
     k = min(len(h1), len(h2), upto)
-    a, b = np.asarray(h1[:k]), np.asarray(h2[:k])
+    a, b = np.asarray(h1[:k], dtype=float), np.asarray(h2[:k], dtype=float)
+    if k and floor:
+        keep = np.maximum(np.abs(a), np.abs(b)) >= floor * max(abs(a[0]), abs(b[0]))
+        a, b = a[keep], b[keep]
+    if a.size == 0:
+        return 0.0
     s = np.maximum(np.abs(a), np.abs(b))
     d = np.where(s == 0, 0.0, np.abs(a - b) / np.where(s == 0, 1.0, s))
-    return float(d.max()) if k else 0.0
+    return float(d.max())
 
 
 def rel_vec(x, y):

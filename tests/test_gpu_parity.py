@@ -1,0 +1,360 @@
+"""GPU parity tests: the B200 library (through its C ABI) against the reference.
+
+Protocol:
+  * non-reduction kernels (stencil/CSR apply, Krylov powers) are bit-exact;
+  * s-Omin (s <= 4), s-MR and the strict s-GMRES anchor 2-GMRES(5): residual history within
+    1e-9 relative over the first 50 s-steps (entries >= 1e-9 r0, the reference KAT
+    convention), final iterate within 1e-8 relative, identical iteration counts (+-1 when
+    the stop is a tolerance crossing), op counters, breakdown strings and notes;
+  * chaotic cases (s-GMRES s=4 m=10, s=8): the same structure, history within 10x the
+    reference's own summation-order envelope (tests/golden/envelope.json), first-block
+    LSQ residual within 1e-9, and the true residual of the GPU iterate below tol.
+"""
+import json
+import os
+
+import numpy as np
+import pytest
+
+from golden_util import GOLDEN, MANIFEST, case, matrix, names, rel_diff
+from oracle import Oracle
+from parity_util import gpu_operator, rel_hist, rel_vec, run_gpu_case
+
+pytestmark = pytest.mark.gpu
+
+ENVELOPE = json.load(open(os.path.join(GOLDEN, "envelope.json")))
+CHAOTIC = {"C2shape_sgmres_s4_m10_64", "C4shape_sgmres_s8_m8_64"}
+GPU_METHODS = {"somin", "sgmres", "smr", "gmres"}
+SOLVE_CASES = [n for n in names("solve") if MANIFEST[n]["method"] in GPU_METHODS]
+
+
+@pytest.fixture(scope="module")
+def ctx():
+    from paper_2001_04886_b200 import Context
+    return Context(0)
+
+
+@pytest.fixture(scope="module")
+def port():
+    return Oracle("port")
+
+
+def _check_structure(meta, arr, rep):
+    ref_oh = [tuple(int(v) for v in row) for row in arr["op_history"]]
+    tol_crossing = meta["converged"] and meta["cfg"].get("tol", 0.0) > 0.0
+    if tol_crossing:
+        assert abs(rep.iterations - meta["iterations"]) <= (meta["cfg"].get("s", 1) if meta["method"] == "sgmres" else 1)
+    else:
+        assert rep.iterations == meta["iterations"]
+    if rep.iterations == meta["iterations"]:
+        assert rep.cycles == meta["cycles"]
+        assert rep.op_history == ref_oh
+        assert tuple(rep.op_counts) == tuple(int(v) for v in arr["op_counts"])
+    assert rep.converged == meta["converged"]
+    assert rep.breakdown == meta["breakdown"]
+    assert rep.notes == meta["notes"]
+    assert rep.fallback_cycles == meta["fallback_cycles"]
+    assert rep.steady_iteration == meta["steady_iteration"]
+
+
+@pytest.mark.parametrize("prefer_stencil", [True, False], ids=["stencil", "csr"])
+@pytest.mark.parametrize("name", SOLVE_CASES)
+def test_solve_matches_reference(ctx, port, name, prefer_stencil):
+    meta = MANIFEST[name]
+    if not prefer_stencil and "stencil" not in meta:
+        pytest.skip("case has no stencil form")
+    meta, arr, rep, x, op = run_gpu_case(ctx, name, prefer_stencil)
+    _check_structure(meta, arr, rep)
+    env = ENVELOPE[name]
+    h = rel_hist(rep.residual_history, arr["history"])
+    if name in CHAOTIC:
+        assert h <= max(1e-9, 10.0 * env["hist50"]), (h, env["hist50"])
+        a = matrix(arr)
+        ref = port.sstep(meta["method"], a, arr["f"], arr["x0"], **meta["cfg"])
+        assert rel_diff(rep.block_rho[0], ref.block_rho[0]) <= 1e-9
+        if meta["converged"]:
+            true_r = np.linalg.norm(arr["f"] - port.spmv(a, x))
+            assert true_r <= meta["cfg"]["tol"] * (1 + 1e-6)
+    else:
+        assert h <= 1e-9, h
+        if meta["converged"]:
+            assert rel_vec(x, arr["x"]) <= max(1e-8, 10.0 * env["x"])
+
+
+def test_strict_anchor_block_residuals(ctx, port):
+    """2-GMRES(5) on the C1 operator: per-block LSQ residuals within 1e-9 for 50 block steps."""
+    meta, arr, rep, x, op = run_gpu_case(ctx, "C1op_sgmres_s2_m5_128")
+    ref = port.sstep("sgmres", matrix(arr), arr["f"], arr["x0"], **meta["cfg"])
+    assert len(rep.block_rho) == len(ref.block_rho)
+    assert rel_hist(rep.block_rho, ref.block_rho, upto=50) <= 1e-9
+
+
+# ------------------------------------------------------------------ kernels: bit-exact
+@pytest.mark.parametrize("dim,nx,conv,vark", [(2, 37, 10.0, False), (3, 11, 20.0, False), (3, 9, 20.0, True),
+                                              (2, 13, 50.0, True)])
+def test_apply_bit_exact(ctx, port, dim, nx, conv, vark):
+    from paper_2001_04886_b200 import convection_diffusion, splitmix64_uniform
+    st = convection_diffusion(dim, nx, conv, variable_k=vark)
+    k = port.lognormal(5, st.n) if vark else None
+    a = port.stencil_csr(dim, st.nx, st.ny, st.nz, st.coef, kcell=k, ch2=st.ch2)
+    xv = splitmix64_uniform(11, st.n)
+    want = port.spmv(a, xv)
+    for op in (ctx.stencil(st, kcell=k), ctx.csr(a.offs, a.cols, a.vals)):
+        assert op.kind == f"stencil{dim}d"
+        assert np.array_equal(op.apply(xv), want)
+
+
+def test_apply_general_csr_bit_exact(ctx, port):
+    from paper_2001_04886_b200 import splitmix64_uniform
+    meta, arr = case("sgmres_s2_m4_dense40")
+    a = matrix(arr)
+    op = ctx.csr(a.offs, a.cols, a.vals)
+    assert op.kind == "csr"
+    xv = splitmix64_uniform(2, a.n)
+    assert np.array_equal(op.apply(xv), port.spmv(a, xv))
+
+
+def test_krylov_block_recurrence_bit_exact(ctx, port):
+    """test_block.cpp:49-60 on the paper problem nx=3 (gamma 50)."""
+    from paper_2001_04886_b200 import krylov_block
+    meta, arr = case("krylov_block_nx3_s4")
+    op = gpu_operator(ctx, meta, arr)
+    kb = krylov_block(op, arr["v"], meta["s"])
+    assert np.array_equal(kb, arr["blocks"])
+    for j in range(meta["s"] - 1):
+        assert np.array_equal(kb[j + 1], op.apply(kb[j]))
+
+
+# ------------------------------------------------------------------ reference KATs (test_sstep.cpp)
+def test_smr_step_s1_is_one_mr_step(ctx):
+    """:45-69"""
+    from paper_2001_04886_b200 import smr_step
+    meta, arr = case("smr_step_s1_nx5")
+    op = gpu_operator(ctx, meta, arr)
+    x, r = arr["x0"].copy(), arr["r0"].copy()
+    smr_step(op, x, r, 1)
+    mr = case("mr_nx5_max1")[1]
+    assert max(rel_diff(a, b) for a, b in zip(x, mr["x"])) <= 1e-14
+    assert rel_diff(np.linalg.norm(r), mr["history"][-1]) <= 1e-14
+
+
+def test_smr_step_attains_gmres_optimum(ctx):
+    """:82-102 and :104-127 (orthogonality of the new residual to A R)."""
+    from paper_2001_04886_b200 import krylov_block, smr_step
+    meta, arr = case("smr_step_s3_nx3")
+    op = gpu_operator(ctx, meta, arr)
+    x, r = arr["x0"].copy(), arr["r0"].copy()
+    smr_step(op, x, r, 3)
+    g = case("gmres_m3_nx3")[1]
+    assert rel_diff(np.linalg.norm(r), g["history"][-1]) <= 1e-9
+    meta5, arr5 = case("smr_step_s3_nx5")
+    op5 = gpu_operator(ctx, meta5, arr5)
+    x5, r5 = arr5["x0"].copy(), arr5["r0"].copy()
+    kb = krylov_block(op5, r5, 4)
+    smr_step(op5, x5, r5, 3)
+    for j in range(1, 4):
+        cos = abs(kb[j] @ r5) / (np.linalg.norm(kb[j]) * np.linalg.norm(r5))
+        assert cos <= 1e-8
+
+
+def test_smr_identity_annihilates(ctx):
+    """:71-80"""
+    from paper_2001_04886_b200 import smr_step
+    op = ctx.csr(np.arange(7), np.arange(6), np.ones(6))
+    x = np.zeros(6)
+    r = np.array([0.3, -0.2, 0.9, 0.1, -0.5, 0.7])
+    a = smr_step(op, x, r, 1)
+    assert abs(a[0] - 1.0) <= 1e-14 and np.linalg.norm(r) <= 1e-14
+
+
+def test_somin_s1_reproduces_omin(ctx):
+    """:151-189 (unpreconditioned half): s-Omin(s=1,k=4) vs the reference Omin(4) history."""
+    meta, arr, rep, x, op = run_gpu_case(ctx, "somin_s1_k4_nx7")
+    om = case("omin_k4_nx7")[1]["history"]
+    assert rep.converged and len(rep.residual_history) == len(om)
+    assert all(rel_diff(a, b) <= 1e-12 for a, b in zip(rep.residual_history, om))
+
+
+def test_somin_window1_matches_sgcr_on_symmetric_problem(ctx):
+    """:191-220"""
+    _, _, a, _, _ = run_gpu_case(ctx, "somin_s2_k1_sym")
+    _, _, b, _, _ = run_gpu_case(ctx, "sgcr_s2_sym")
+    r0 = a.residual_history[0]
+    for u, v in zip(a.residual_history, b.residual_history):
+        if u < 1e-3 * r0:
+            break
+        assert rel_diff(u, v) <= 1e-8
+
+
+def test_somin_residuals_never_increase_with_debug_checks(ctx):
+    """:222-238 (debug A-orthogonality checks run on the device)"""
+    meta, arr, rep, x, op = run_gpu_case(ctx, "somin_s2_k2_debug_nx7")
+    assert rep.converged
+    h = rep.residual_history
+    assert all(h[t] <= h[t - 1] * (1 + 1e-12) for t in range(1, len(h)))
+
+
+def test_sarnoldi_kats(ctx):
+    """:240-311 -- s=1 matches Arnoldi's Hessenberg, single block = krylov block bit-exactly,
+    A V = U G and cross-block orthogonality."""
+    from paper_2001_04886_b200 import krylov_block, sarnoldi
+    meta, arr = case("sarnoldi_s1_m6_dense25")
+    op = gpu_operator(ctx, meta, arr)
+    b = sarnoldi(op, arr["v1"], 1, 6)
+    H = arr["arnoldi_h"]
+    for j in range(6):
+        for i in range(j + 2):
+            assert abs(b.hess[i, j] - H[i, j]) <= 1e-10 * max(1.0, abs(H[i, j]))
+    meta, arr = case("sarnoldi_s3_m1_nx3")
+    op = gpu_operator(ctx, meta, arr)
+    b = sarnoldi(op, arr["v1"], 3, 1)
+    vhat = np.zeros(9)
+    vhat[0] = 1.0
+    assert np.array_equal(b.blocks[0], krylov_block(op, vhat, 3))
+    for nm in ("sarnoldi_s2_m3_dense30", "sarnoldi_s3_m5_dense30"):
+        meta, arr = case(nm)
+        s, k = meta["s"], meta["m_blocks"]
+        a = matrix(arr)
+        op = gpu_operator(ctx, meta, arr)
+        b = sarnoldi(op, arr["v1"], s, k)
+        A = a.to_dense()
+        err2 = 0.0
+        for bc in range(k):
+            for lc in range(s):
+                av = A @ b.blocks[bc][lc]
+                col = bc * s + lc
+                for br in range(k):
+                    for lr in range(s):
+                        av -= b.hess[br * s + lr, col] * b.blocks[br][lr]
+                av -= b.hess[k * s, col] * b.next_seed
+                err2 += av @ av
+        assert np.sqrt(err2) <= 1e-8 * np.linalg.norm(a.vals)
+        for i in range(k):
+            for j in range(i + 1, k):
+                cross = b.blocks[i] @ b.blocks[j].T
+                ni, nj = np.sqrt(np.trace(b.grams[i])), np.sqrt(np.trace(b.grams[j]))
+                assert np.linalg.norm(cross) <= 1e-8 * ni * nj
+        # against the reference basis itself
+        assert np.allclose(b.hess, arr["hess"], rtol=1e-8, atol=1e-10 * np.abs(arr["hess"]).max())
+        assert list(b.counter)[:3] == meta["counter"][:3]
+
+
+def test_sarnoldi_errors(ctx):
+    from paper_2001_04886_b200 import sarnoldi
+    meta, arr = case("sarnoldi_s3_m1_nx3")
+    op = gpu_operator(ctx, meta, arr)
+    with pytest.raises(ValueError):
+        sarnoldi(op, arr["v1"], 3, 4)  # s * m_blocks > n
+    with pytest.raises(ValueError):
+        sarnoldi(op, np.zeros(9), 2, 1)  # zero start vector
+
+
+def test_sgmres_s1_shares_gmres_history(ctx):
+    """:313-336 -- s=1 delegates to the standard GMRES path (bit-identical on the device)."""
+    from paper_2001_04886_b200 import SolverConfig, SStepConfig, gmres_solve, sgmres_solve
+    meta, arr = case("sgmres_s1_m5_nx7")
+    op = gpu_operator(ctx, meta, arr)
+    x1, x2 = arr["x0"].copy(), arr["x0"].copy()
+    a = sgmres_solve(op, arr["f"], x1, SStepConfig(s=1, m=5, tol=1e-6, max_iterations=5000))
+    b = gmres_solve(op, arr["f"], x2, SolverConfig(m=5, tol=1e-6, max_iterations=5000))
+    assert a.converged
+    assert all(rel_diff(u, v) <= 1e-10 for u, v in zip(a.residual_history, b.residual_history))
+
+
+def test_sgmres_matches_gmres_ms_cycle_for_cycle(ctx):
+    """:338-368 Remark 4.1 on the dense 40x40 system."""
+    _, _, rep, _, _ = run_gpu_case(ctx, "sgmres_s2_m4_dense40")
+    g = case("gmres_m8_dense40")[1]["history"]
+    r0 = rep.residual_history[0]
+    assert min(len(rep.residual_history), len(g)) >= 3
+    for u, v in zip(rep.residual_history, g):
+        if u < 1e-9 * r0:
+            break
+        assert rel_diff(u, v) <= 1e-6
+
+
+def test_matvec_budgets(ctx):
+    """:370-405"""
+    _, _, rep, _, _ = run_gpu_case(ctx, "sgmres_s2_m3_nx7_budget")
+    mv = [c[1] for c in rep.op_history]
+    assert len(mv) >= 3 and all(b - a == 2 * 4 for a, b in zip(mv, mv[1:]))
+    _, _, rep, _, _ = run_gpu_case(ctx, "somin_s3_k2_nx7_budget")
+    mv = [c[1] for c in rep.op_history]
+    assert len(mv) >= 3 and all(b - a == 3 for a, b in zip(mv, mv[1:]))
+
+
+def test_sgmres_recovers_through_fallback(ctx, port):
+    """:407-434 I+N nilpotent operator, s=6: fallback GMRES(sm) on the device."""
+    meta, arr, rep, x, op = run_gpu_case(ctx, "sgmres_s6_m2_nilpotent")
+    assert rep.converged and rep.fallback_cycles >= 1 and rep.notes
+    assert np.linalg.norm(port.spmv(matrix(arr), x) - arr["f"]) <= 1e-9 * np.linalg.norm(arr["f"])
+
+
+def test_somin_reports_basis_collapse(ctx):
+    """:436-457"""
+    _, _, rep, _, _ = run_gpu_case(ctx, "somin_s6_k2_nilpotent")
+    assert not rep.converged and rep.breakdown and "basis collapse" in rep.breakdown
+
+
+def test_config_errors(ctx):
+    from paper_2001_04886_b200 import SStepConfig, sgmres_solve, somin_solve
+    meta, arr = case("somin_s2_k2_nx7_audit")
+    op = gpu_operator(ctx, meta, arr)
+    f, x = arr["f"], arr["x0"].copy()
+    with pytest.raises(ValueError, match="s must be in 1..8"):
+        somin_solve(op, f, x, SStepConfig(s=9))
+    with pytest.raises(ValueError, match="window k"):
+        somin_solve(op, f, x, SStepConfig(s=2, k=0))
+    with pytest.raises(ValueError, match="m must be at least 1"):
+        sgmres_solve(op, f, x, SStepConfig(s=2, m=0))
+    with pytest.raises(ValueError, match="ILU"):
+        somin_solve(op, f, x, SStepConfig(s=2, precondition=True))
+    with pytest.raises(ValueError):
+        somin_solve(op, f[:-1], x, SStepConfig(s=2))
+
+
+def test_zero_rhs_and_exact_guess(ctx, port):
+    """A zero residual spends no iterations (test_accounting.cpp:143-158)."""
+    from paper_2001_04886_b200 import SStepConfig, sgmres_solve, somin_solve
+    meta, arr = case("somin_s2_k2_nx7_audit")
+    op = gpu_operator(ctx, meta, arr)
+    f = port.spmv(matrix(arr), arr["x0"])
+    for fn in (somin_solve, sgmres_solve):
+        x = arr["x0"].copy()
+        rep = fn(op, f, x, SStepConfig(s=2))
+        assert rep.converged and rep.iterations == 0 and rep.op_counts[1] <= 1
+
+
+# ------------------------------------------------------------------ full-size properties
+@pytest.mark.slow
+def test_c2_full_size_converges_with_true_residual(ctx, port):
+    """BASELINE configs[1] at its full 1024^2 size: converges to rel 1e-8; the GPU iterate's
+    true residual (CPU stencil) matches the reported final residual and is below tol."""
+    from paper_2001_04886_b200 import SStepConfig, convection_diffusion, sgmres_solve, splitmix64_uniform
+    st = convection_diffusion(2, 1024, 50.0)
+    f = splitmix64_uniform(20010486, st.n)
+    tol = 1e-8 * np.linalg.norm(f)
+    op = ctx.stencil(st)
+    x = np.zeros(st.n)
+    rep = sgmres_solve(op, f, x, SStepConfig(s=4, m=10, tol=tol))
+    assert rep.converged and rep.fallback_cycles == 0
+    r = f - port.stencil_apply(2, st.nx, st.ny, 1, st.coef, x)
+    assert np.linalg.norm(r) <= tol * (1 + 1e-6)
+    assert rel_diff(np.linalg.norm(r), rep.final_residual) <= 1e-6
+    assert 80 <= rep.cycles <= 130  # reference: 102 cycles with its own f
+
+
+@pytest.mark.slow
+def test_c3_full_size_monotone_and_consistent(ctx, port):
+    """BASELINE configs[2] at 256^3, s=4, 8 s-steps: non-increasing residuals (Orthomin
+    minimizes over the window) and recursive residual == true residual to 1e-9."""
+    from paper_2001_04886_b200 import SStepConfig, convection_diffusion, somin_solve, splitmix64_uniform
+    st = convection_diffusion(3, 256, 20.0)
+    f = splitmix64_uniform(20010486, st.n)
+    op = ctx.stencil(st)
+    x = np.zeros(st.n)
+    rep = somin_solve(op, f, x, SStepConfig(s=4, k=2, tol=0.0, max_iterations=8))
+    h = rep.residual_history
+    assert rep.iterations == 8 and all(h[t] <= h[t - 1] * (1 + 1e-12) for t in range(1, len(h)))
+    r = f - port.stencil_apply(3, st.nx, st.ny, st.nz, st.coef, x)
+    assert rel_diff(np.linalg.norm(r), h[-1]) <= 1e-9
