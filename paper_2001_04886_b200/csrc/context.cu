@@ -32,11 +32,12 @@ std::string fmt_double(double v) {
 Geo make_geo(int64_t n, int sm_count) {
   Geo g;
   g.n = n;
-  const int64_t maxg = 4LL * sm_count;
-  int64_t G = (n + 1023) / 1024;
+  // at most two co-resident CTAs per SM; each range is a whole number of 256-point tiles
+  const int64_t maxg = 2LL * sm_count;
+  int64_t G = (n + 2047) / 2048;
   G = std::max<int64_t>(1, std::min(G, maxg));
   int64_t range = (n + G - 1) / G;
-  range = (range + 63) / 64 * 64;
+  range = (range + 255) / 256 * 256;
   G = (n + range - 1) / range;
   g.G = (int)std::max<int64_t>(1, G);
   g.range = range;

@@ -20,10 +20,50 @@ __device__ __forceinline__ double warp_sum(double v) {
   return v;
 }
 
+// The flags are written only by earlier kernels on the stream, so a read-only-path load is
+// safe; it is served from L1 after the first warp per SM instead of serializing every warp
+// of the grid on one L2 line.
 __device__ __forceinline__ bool skip_launch(const int* halt, const int* cond) {
-  if (halt && *(volatile const int*)halt) return true;
-  if (cond && *(volatile const int*)cond == 0) return true;
+  if (halt && __ldg(halt)) return true;
+  if (cond && __ldg(cond) == 0) return true;
   return false;
+}
+
+// ---------------------------------------------------------------- bulk async copies (TMA engine)
+// cp.async.bulk global->shared with mbarrier completion (SASS UBLKCP / SYNCS): one elected
+// thread arms the barrier with the expected byte count, lanes issue one copy per vector tile.
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_fence_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
+      "r"(phase)
+      : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
 }
 
 // Deterministic reduction of nd dots from per-CTA partials ([(d0+d)*G + g]) into out[d]

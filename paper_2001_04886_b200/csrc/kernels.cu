@@ -4,12 +4,7 @@
 //                   per-cell diagonals) and general CSR.  Bit-identical to the reference
 //                   spmv (sparse.hpp:135-146): acc = 0, then + v*x per present neighbour
 //                   in ascending column order, multiply and add rounded separately.
-//  * k_lincomb    : fused block vector update y_o = base_o + sum_j c_jo x_j applied in the
-//                   reference's per-element order (axpy / block_axpy_inplace,
-//                   kernels.hpp:55-58, block.hpp:109-116) plus inner products of the
-//                   results, written as deterministic per-CTA partials.
-//  * k_gram       : packed block inner products L^T R (block_gram / block_dot,
-//                   block.hpp:70-99) as per-CTA partials.
+// The streaming update / inner-product kernels live in stream.cu.
 #include <cstdio>
 
 #include "device_util.cuh"
@@ -118,169 +113,6 @@ void launch_apply(Ctx& c, const DevOp& op, const double* x, double* y, const int
       default: fail(SKC_EINVAL, "apply: unsupported operator kind");
     }
   }
-  CK(cudaGetLastError());
-}
-
-// ------------------------------------------------------------------ block reduction to partials
-// acc[k] per thread -> partials[(dot0 + k) * G + blockIdx.x] (fixed order)
-template <int K>
-__device__ __forceinline__ void block_store_partials(double (&acc)[K], int nk, double* partials, int dot0, int G,
-                                                     int gidx, double* red /* >= 8*K */) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-#pragma unroll
-  for (int k = 0; k < K; ++k) {
-    if (k < nk) {
-      const double v = warp_sum(acc[k]);
-      if (lane == 0) red[warp * K + k] = v;
-    }
-  }
-  __syncthreads();
-  for (int k = threadIdx.x; k < nk; k += blockDim.x) {
-    double s = 0.0;
-    for (int w = 0; w < nw; ++w) s += red[w * K + k];
-    partials[(int64_t)(dot0 + k) * G + gidx] = s;
-  }
-}
-
-// ------------------------------------------------------------------ k_lincomb
-template <int MAXD>
-__global__ void __launch_bounds__(256) k_lincomb(const __grid_constant__ LinDesc d) {
-  if (skip_launch(d.halt, d.cond)) return;
-  extern __shared__ double smem[];
-  double* scoef = smem;                      // ncoef
-  double* sv = smem + ((d.ncoef + 1) & ~1);  // (nout + nx) * 256 when MAXD > 0
-  for (int t = threadIdx.x; t < d.ncoef; t += blockDim.x) scoef[t] = d.coef[t];
-  __syncthreads();
-  const int64_t r0 = (int64_t)blockIdx.x * d.range;
-  const int64_t r1 = min(d.n, r0 + d.range);
-  double acc[MAXD > 0 ? MAXD : 1];
-#pragma unroll
-  for (int k = 0; k < (MAXD > 0 ? MAXD : 1); ++k) acc[k] = 0.0;
-
-  for (int64_t i = r0 + threadIdx.x; i < r1; i += blockDim.x) {
-    double o[LC_MAXOUT];
-#pragma unroll
-    for (int q = 0; q < LC_MAXOUT; ++q) {
-      if (q < d.nout) {
-        double b = d.base[q][i];
-        if (d.bscale[q] >= 0) b = dmul(b, scoef[d.bscale[q]]);
-        o[q] = b;
-      }
-    }
-    for (int j = 0; j < d.nin; ++j) {
-      const double v = d.in[j][i];
-      const unsigned m = d.mask[j];
-      const double* cj = scoef + d.cbase[j];
-#pragma unroll
-      for (int q = 0; q < LC_MAXOUT; ++q)
-        if ((m >> q) & 1u) o[q] = dadd(o[q], dmul(cj[q], v));
-    }
-#pragma unroll
-    for (int q = 0; q < LC_MAXOUT; ++q)
-      if (q < d.nout) d.out[q][i] = o[q];
-    if (MAXD > 0) {
-      double* col = sv + threadIdx.x;
-#pragma unroll
-      for (int q = 0; q < LC_MAXOUT; ++q)
-        if (q < d.nout) col[q * 256] = o[q];
-      for (int x = 0; x < d.nx; ++x) col[(d.nout + x) * 256] = d.xin[x][i];
-#pragma unroll
-      for (int k = 0; k < (MAXD > 0 ? MAXD : 1); ++k)
-        if (k < d.nd) acc[k] = fma(col[d.da[k] * 256], col[d.db[k] * 256], acc[k]);
-    }
-  }
-  if (MAXD > 0) {
-    __syncthreads();
-    block_store_partials<(MAXD > 0 ? MAXD : 1)>(acc, d.nd, d.partials, d.dot0, d.G, blockIdx.x, sv);
-  }
-}
-
-void launch_lincomb(Ctx& c, const LinDesc& d, const char* name) {
-  require(d.nin <= LC_MAXIN && d.nout <= LC_MAXOUT && d.nx <= LC_MAXX && d.nd <= LC_MAXD, "lincomb: descriptor too large");
-  double bytes = 8.0 * (double)d.n * (d.nin + d.nout + d.nx);
-  for (int q = 0; q < d.nout; ++q) {  // count each distinct base read once
-    bool aliased = false;
-    for (int j = 0; j < d.nin; ++j) aliased |= d.in[j] == d.base[q];
-    if (!aliased) bytes += 8.0 * (double)d.n;
-  }
-  Launch L(c, name, bytes);
-  const int vals = d.nout + d.nx;
-  size_t sm = 8 * (size_t)((d.ncoef + 1) & ~1);
-  const int maxd = d.nd == 0 ? 0 : d.nd <= 16 ? 16 : 64;
-  if (maxd) sm += 8 * (size_t)std::max(vals * 256, 8 * maxd);
-  if (maxd == 0) {
-    k_lincomb<0><<<d.G, 256, sm, c.stream>>>(d);
-  } else if (maxd == 16) {
-    k_lincomb<16><<<d.G, 256, sm, c.stream>>>(d);
-  } else {
-    static bool attr = false;
-    if (!attr) {
-      CK(cudaFuncSetAttribute(k_lincomb<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024));
-      CK(cudaFuncSetAttribute(k_lincomb<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024));
-      attr = true;
-    }
-    k_lincomb<64><<<d.G, 256, sm, c.stream>>>(d);
-  }
-  CK(cudaGetLastError());
-}
-
-// ------------------------------------------------------------------ k_gram
-__global__ void __launch_bounds__(256) k_gram(const __grid_constant__ GramDesc d) {
-  if (skip_launch(d.halt, d.cond)) return;
-  __shared__ double red[8 * GR_LB * GR_MAXR];
-  const int64_t r0 = (int64_t)blockIdx.x * d.range;
-  const int64_t r1 = min(d.n, r0 + d.range);
-  const int l0 = blockIdx.y * GR_LB;
-  const int nlb = min(GR_LB, d.nl - l0);
-  double acc[GR_LB * GR_MAXR];
-#pragma unroll
-  for (int k = 0; k < GR_LB * GR_MAXR; ++k) acc[k] = 0.0;
-  for (int64_t i = r0 + threadIdx.x; i < r1; i += blockDim.x) {
-    double rv[GR_MAXR];
-#pragma unroll
-    for (int r = 0; r < GR_MAXR; ++r) rv[r] = r < d.nr ? d.R[r][i] : 0.0;
-#pragma unroll
-    for (int lb = 0; lb < GR_LB; ++lb) {
-      if (lb < nlb) {
-        const double lv = d.L[l0 + lb][i];
-#pragma unroll
-        for (int r = 0; r < GR_MAXR; ++r)
-          if (r < d.nr) acc[lb * GR_MAXR + r] = fma(lv, rv[r], acc[lb * GR_MAXR + r]);
-      }
-    }
-  }
-  // reduce: index k = lb*GR_MAXR + r  -> dot (l0+lb)*nr + r
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-#pragma unroll
-  for (int k = 0; k < GR_LB * GR_MAXR; ++k) {
-    const int lb = k / GR_MAXR, r = k % GR_MAXR;
-    if (lb < nlb && r < d.nr) {
-      const double v = warp_sum(acc[k]);
-      if (lane == 0) red[warp * GR_LB * GR_MAXR + k] = v;
-    }
-  }
-  __syncthreads();
-  for (int k = threadIdx.x; k < GR_LB * GR_MAXR; k += blockDim.x) {
-    const int lb = k / GR_MAXR, r = k % GR_MAXR;
-    if (lb < nlb && r < d.nr) {
-      double s = 0.0;
-      for (int w = 0; w < nw; ++w) s += red[w * GR_LB * GR_MAXR + k];
-      d.partials[(int64_t)(d.dot0 + (l0 + lb) * d.nr + r) * d.G + blockIdx.x] = s;
-    }
-  }
-}
-
-void launch_gram(Ctx& c, const GramDesc& d, const char* name) {
-  require(d.nl >= 1 && d.nl <= GR_MAXL && d.nr >= 1 && d.nr <= GR_MAXR, "gram: descriptor out of range");
-  double bytes = 8.0 * (double)d.n * d.nr;
-  for (int l = 0; l < d.nl; ++l) {
-    bool dup = false;
-    for (int r = 0; r < d.nr; ++r) dup |= d.L[l] == d.R[r];
-    if (!dup) bytes += 8.0 * (double)d.n;
-  }
-  Launch L(c, name, bytes);
-  dim3 grid(d.G, (d.nl + GR_LB - 1) / GR_LB);
-  k_gram<<<grid, 256, 0, c.stream>>>(d);
   CK(cudaGetLastError());
 }
 

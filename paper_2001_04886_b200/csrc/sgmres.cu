@@ -541,16 +541,16 @@ struct Engine {
         for (int i = 0; i < k; ++i) {
           k_arn_t<<<1, 256, 0, c.stream>>>(st, grams, i, tk, coef, partials, g.G, dl.D(), s, cl.T(), pass);
           ++c.launches;
-          LinBuilder lb;  // cand[:,jc] -= sum_l t(l,jc-1) V_i[:,l]  (+ dots with V_{i+1})
-          for (int jc = 1; jc < s; ++jc) lb.add_out(col(cb, jc), col(cb, jc));
-          const uint16_t mask = (uint16_t)((1u << (s - 1)) - 1u);
-          for (int l = 0; l < s; ++l) lb.add_term(col(i, l), mask, cl.T() + l * (s - 1));
-          if (i + 1 < k) {
-            for (int l = 0; l < s; ++l) lb.add_extra(col(i + 1, l));
-            for (int l = 0; l < s; ++l)
-              for (int jc = 1; jc < s; ++jc) lb.add_dot((s - 1) + l, jc - 1);
+          // cand[:,jc] -= sum_l t(l,jc-1) V_i[:,l]  (+ products with V_{i+1})
+          const double* Vi[kMaxS];
+          const double* Vn[kMaxS];
+          double* cd[kMaxS];
+          for (int l = 0; l < s; ++l) {
+            Vi[l] = col(i, l);
+            Vn[l] = i + 1 < k ? col(i + 1, l) : nullptr;
+            cd[l] = col(cb, l);
           }
-          lb.launch(c, g, coef, cl.size(), partials, dl.D(), halt, cond, "mgs_update");
+          launch_mgs(c, g, s, Vi, cd, i + 1 < k ? Vn : nullptr, coef + cl.T(), partials, dl.D(), halt, cond);
         }
         if (pass == 0) {
           // reorthogonalization test: V_i^T cand (all columns) and cand^T cand

@@ -89,7 +89,7 @@ struct LinDesc {
 };
 
 // dots L_l . R_r, dot index (l * nr + r)
-constexpr int GR_MAXL = 80, GR_MAXR = 8, GR_LB = 4;
+constexpr int GR_MAXL = 64, GR_MAXR = 8, GR_LB = 4;
 struct GramDesc {
   int nl, nr;
   const double* L[GR_MAXL];
@@ -155,6 +155,10 @@ void launch_apply(Ctx& c, const DevOp& op, const double* x, double* y, const int
 void launch_lincomb(Ctx& c, const LinDesc& d, const char* name = "lincomb");
 void launch_gram(Ctx& c, const GramDesc& d, const char* name = "gram");
 void launch_fill(Ctx& c, double* p, double v, int64_t n);
+// one block-MGS round: cand[1..s) += sum_l coef_t[l*(s-1)+jc-1] Vi[l]; if Vnext: the
+// products Vnext[l] . cand[jc] at dot0 + l*(s-1) + jc-1
+void launch_mgs(Ctx& c, const Geo& geo, int s, const double* const* Vi, double* const* cand, const double* const* Vnext,
+                const double* coef_t, double* partials, int dot0, const int* halt, const int* cond);
 // operator helpers
 void build_stencil_op(Ctx& c, Op& op, const skc_stencil_desc& d, const double* kcell_host);
 void build_csr_op(Ctx& c, Op& op, int64_t n, const uint64_t* offs, const uint64_t* cols, const double* vals);

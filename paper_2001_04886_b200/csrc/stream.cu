@@ -1,0 +1,643 @@
+// stream.cu -- the streaming kernels every solver phase is built from.  Input tiles are
+// staged through shared memory by the bulk-copy (TMA) engine in a warp-specialized
+// producer/consumer pipeline:
+//
+//   producer warp : for each tile of T points, waits until its stage is free (empty
+//                   mbarrier), arms the stage's full mbarrier with the byte count and issues
+//                   one cp.async.bulk per distinct operand vector;
+//   consumer warps: wait on the full mbarrier, compute from shared memory, and release the
+//                   stage with one arrive per warp -- no CTA-wide barrier per tile.
+//
+// Kernels:
+//  * k_upd<NOUT, MAXD, PPT> : generic fused block vector update y_o = base_o [* c] +
+//        sum_j c_{j,o} x_j in the reference's per-element order (axpy / block_axpy_inplace,
+//        kernels.hpp:55-58, block.hpp:109-116; multiply and add rounded separately) plus up
+//        to MAXD inner products of the results (deterministic per-CTA partials).
+//  * k_mgs<S, DOTS> : one block-MGS round of s-step Arnoldi (sstep.hpp:346-352),
+//        cand[:,jc] -= sum_l t(l,jc-1) V_i[:,l], fused with the next round's
+//        V_{i+1}^T cand products (sstep.hpp:341), everything compile-time sized.
+//  * k_grm<NR, LB> : packed block inner products L^T R (block_gram / block_dot,
+//        block.hpp:70-99).
+#include <algorithm>
+#include <cstring>
+
+#include "device_util.cuh"
+#include "skc_internal.hpp"
+
+namespace skc {
+
+namespace {
+
+constexpr int kMaxStage = 4;
+constexpr int NCW = 8;                  // consumer warps
+constexpr int CONS = NCW * 32;          // consumer threads
+constexpr int THREADS = CONS + 32;      // + one producer warp
+constexpr int UPD_MAXU = LC_MAXOUT + LC_MAXIN + LC_MAXX;
+constexpr int GRM_MAXU = GR_MAXL + GR_MAXR;
+
+// common pipeline header of every descriptor
+struct PipeHdr {
+  int nu, T, nstage;
+  int64_t n, range;
+  const int* halt;
+  const int* cond;
+};
+
+struct UpdDesc {
+  PipeHdr h;
+  int nin, nout, nx, nd, ncoef;
+  const double* U[UPD_MAXU];  // distinct staged vectors
+  uint8_t ub[LC_MAXOUT];      // base of output q -> U index
+  int16_t bscale[LC_MAXOUT];
+  double* out[LC_MAXOUT];
+  uint8_t ut[LC_MAXIN];  // term j -> U index
+  uint16_t mask[LC_MAXIN];
+  int16_t cbase[LC_MAXIN];
+  uint8_t ux[LC_MAXX];  // extra x -> U index
+  uint8_t da[LC_MAXD], db[LC_MAXD];
+  const double* coef;
+  double* partials;
+  int dot0, G;
+};
+
+struct GrmDesc {
+  PipeHdr h;
+  int nl, nr;
+  const double* U[GRM_MAXU];
+  uint8_t li[GR_MAXL], ri[GR_MAXR];
+  double* partials;
+  int dot0, G;
+};
+
+struct MgsDesc {
+  PipeHdr h;
+  const double* U[3 * kMaxS];  // V_i[0..S), cand[1..S), V_{i+1}[0..S) (DOTS)
+  double* cand[kMaxS];         // outputs cand[1..S)
+  const double* coef;          // t: coef[l*(S-1) + jc-1] (already negated)
+  double* partials;
+  int dot0, G;
+};
+
+struct TileGeom {
+  int64_t start;
+  int cnt;
+  bool bulk;
+};
+__device__ __forceinline__ TileGeom tile_geom(const PipeHdr& h, int64_t r0, int64_t r1, int t) {
+  TileGeom g;
+  g.start = r0 + (int64_t)t * h.T;
+  g.cnt = (int)(r1 - g.start < (int64_t)h.T ? r1 - g.start : (int64_t)h.T);
+  g.bulk = (g.cnt & 1) == 0;  // bulk copies move multiples of 16 bytes
+  return g;
+}
+
+struct Pipe {
+  uint64_t* full;
+  uint64_t* empty;
+  double* stages;
+  size_t stage_sz;
+  int64_t r0, r1;
+  int ntiles;
+};
+
+__device__ __forceinline__ Pipe pipe_setup(const PipeHdr& h, unsigned char* smem_raw, size_t prefix_bytes) {
+  Pipe p;
+  p.full = reinterpret_cast<uint64_t*>(smem_raw);
+  p.empty = p.full + kMaxStage;
+  p.stages = reinterpret_cast<double*>(smem_raw + 64 + prefix_bytes);
+  p.stage_sz = (size_t)h.nu * h.T;
+  p.r0 = (int64_t)blockIdx.x * h.range;
+  p.r1 = min(h.n, p.r0 + h.range);
+  p.ntiles = p.r1 > p.r0 ? (int)((p.r1 - p.r0 + h.T - 1) / h.T) : 0;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < h.nstage; ++s) {
+      mbar_init(&p.full[s], 1);
+      mbar_init(&p.empty[s], NCW);
+    }
+    mbar_fence_init();
+  }
+  return p;
+}
+
+// producer warp: stream every tile of this CTA's range through the stages
+template <int MAXU>
+__device__ __forceinline__ void pipe_produce(const PipeHdr& h, const double* const (&U)[MAXU], const Pipe& p) {
+  const int lane = threadIdx.x & 31;
+  for (int t = 0; t < p.ntiles; ++t) {
+    const int st = t % h.nstage, u = t / h.nstage;
+    if (u > 0) mbar_wait(&p.empty[st], (uint32_t)((u - 1) & 1));
+    const TileGeom g = tile_geom(h, p.r0, p.r1, t);
+    double* S = p.stages + (size_t)st * p.stage_sz;
+    if (g.bulk) {
+      const uint32_t bytes = (uint32_t)g.cnt * 8u;
+      if (lane == 0) {
+        fence_proxy_async();
+        mbar_arrive_expect_tx(&p.full[st], bytes * (uint32_t)h.nu);
+      }
+      __syncwarp();
+      for (int v = lane; v < h.nu; v += 32) bulk_g2s(S + (size_t)v * h.T, U[v] + g.start, bytes, &p.full[st]);
+    } else {
+      for (int v = 0; v < h.nu; ++v)
+        for (int q = lane; q < g.cnt; q += 32) S[(size_t)v * h.T + q] = U[v][g.start + q];
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&p.full[st]);
+    }
+  }
+}
+
+__device__ __forceinline__ double* pipe_acquire(const PipeHdr& h, const Pipe& p, int t, TileGeom& g) {
+  const int st = t % h.nstage;
+  mbar_wait(&p.full[st], (uint32_t)((t / h.nstage) & 1));
+  g = tile_geom(h, p.r0, p.r1, t);
+  return p.stages + (size_t)st * p.stage_sz;
+}
+
+__device__ __forceinline__ void pipe_release(const PipeHdr& h, const Pipe& p, int t) {
+  __syncwarp();
+  if ((threadIdx.x & 31) == 0) mbar_arrive(&p.empty[t % h.nstage]);
+}
+
+// fixed-order CTA reduction of per-thread accumulators (consumer threads only hold data;
+// all THREADS threads must call).  red: >= NCW * K doubles of shared memory.
+template <int K>
+__device__ __forceinline__ void cta_store_partials(const double (&acc)[K], int nk, double* red, double* partials,
+                                                   int dot0, int G) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  __syncthreads();
+  if (warp < NCW) {
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      if (k < nk) {
+        const double v = warp_sum(acc[k]);
+        if (lane == 0) red[warp * K + k] = v;
+      }
+    }
+  }
+  __syncthreads();
+  for (int k = threadIdx.x; k < nk; k += blockDim.x) {
+    double s = 0.0;
+    for (int w = 0; w < NCW; ++w) s += red[w * K + k];
+    partials[(int64_t)(dot0 + k) * G + blockIdx.x] = s;
+  }
+}
+
+// ------------------------------------------------------------------ k_upd
+template <int NOUT, int MAXD, int PPT>
+__global__ void __launch_bounds__(THREADS) k_upd(const __grid_constant__ UpdDesc d) {
+  if (skip_launch(d.h.halt, d.h.cond)) return;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  const int coef_slots = (d.ncoef + 15) & ~15;
+  constexpr int NV = NOUT + LC_MAXX;
+  const size_t prefix = 8 * ((size_t)coef_slots + (MAXD > 0 ? (size_t)NV * CONS : 0));
+  Pipe p = pipe_setup(d.h, smem_raw, prefix);
+  double* scoef = reinterpret_cast<double*>(smem_raw + 64);
+  double* sv = scoef + coef_slots;
+  for (int t = threadIdx.x; t < d.ncoef; t += blockDim.x) scoef[t] = d.coef[t];
+  __syncthreads();
+  const int warp = threadIdx.x >> 5;
+  double acc[MAXD > 0 ? MAXD : 1];
+#pragma unroll
+  for (int k = 0; k < (MAXD > 0 ? MAXD : 1); ++k) acc[k] = 0.0;
+
+  if (warp == NCW) {
+    pipe_produce(d.h, d.U, p);
+  } else {
+    double* col = sv + threadIdx.x;
+    const int T = d.h.T;
+    for (int t = 0; t < p.ntiles; ++t) {
+      TileGeom g;
+      const double* S = pipe_acquire(d.h, p, t, g);
+      const int p0 = threadIdx.x;
+      if (p0 < g.cnt) {
+        bool ok[PPT];
+#pragma unroll
+        for (int u = 0; u < PPT; ++u) ok[u] = p0 + CONS * u < g.cnt;
+        double o[PPT][NOUT];
+#pragma unroll
+        for (int q = 0; q < NOUT; ++q) {
+          const double* bq = S + (size_t)d.ub[q] * T + p0;
+          const int bs = d.bscale[q];
+          const double sc = bs >= 0 ? scoef[bs] : 1.0;
+#pragma unroll
+          for (int u = 0; u < PPT; ++u) {
+            const double b = bq[CONS * u];
+            o[u][q] = bs >= 0 ? dmul(b, sc) : b;
+          }
+        }
+        for (int j = 0; j < d.nin; ++j) {
+          const double* vj = S + (size_t)d.ut[j] * T + p0;
+          const unsigned m = d.mask[j];
+          const double* cj = scoef + d.cbase[j];
+          double v[PPT];
+#pragma unroll
+          for (int u = 0; u < PPT; ++u) v[u] = vj[CONS * u];
+          if (NOUT == 1 || m == (1u << NOUT) - 1u) {  // dense term (all outputs): no predication
+#pragma unroll
+            for (int q = 0; q < NOUT; ++q) {
+              const double c = cj[q];
+#pragma unroll
+              for (int u = 0; u < PPT; ++u) o[u][q] = dadd(o[u][q], dmul(c, v[u]));
+            }
+          } else {
+#pragma unroll
+            for (int q = 0; q < NOUT; ++q)
+              if ((m >> q) & 1u) {
+                const double c = cj[q];
+#pragma unroll
+                for (int u = 0; u < PPT; ++u) o[u][q] = dadd(o[u][q], dmul(c, v[u]));
+              }
+          }
+        }
+#pragma unroll
+        for (int q = 0; q < NOUT; ++q) {
+          double* oq = d.out[q] + g.start + p0;
+#pragma unroll
+          for (int u = 0; u < PPT; ++u)
+            if (ok[u]) oq[CONS * u] = o[u][q];
+        }
+        if (MAXD > 0) {
+#pragma unroll
+          for (int u = 0; u < PPT; ++u) {
+            if (!ok[u]) continue;
+#pragma unroll
+            for (int q = 0; q < NOUT; ++q) col[q * CONS] = o[u][q];
+            for (int x = 0; x < d.nx; ++x) col[(NOUT + x) * CONS] = S[(size_t)d.ux[x] * T + p0 + CONS * u];
+#pragma unroll
+            for (int k = 0; k < (MAXD > 0 ? MAXD : 1); ++k)
+              if (k < d.nd) acc[k] = fma(col[d.da[k] * CONS], col[d.db[k] * CONS], acc[k]);
+          }
+        }
+      }
+      pipe_release(d.h, p, t);
+    }
+  }
+  if (MAXD > 0) cta_store_partials(acc, d.nd, sv, d.partials, d.dot0, d.G);
+}
+
+// ------------------------------------------------------------------ k_mgs
+// U layout: [0,S) V_i ; [S, 2S-1) cand[1..S-1] ; [2S-1, 3S-1) V_{i+1} (DOTS)
+template <int S, bool DOTS>
+__global__ void __launch_bounds__(THREADS) k_mgs(const __grid_constant__ MgsDesc d) {
+  if (skip_launch(d.h.halt, d.h.cond)) return;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  constexpr int NC = S - 1;
+  constexpr int ND = DOTS ? S * NC : 1;
+  Pipe p = pipe_setup(d.h, smem_raw, 8 * 64);
+  double* red = reinterpret_cast<double*>(smem_raw + 64);  // 64 doubles: coefficients, then reduction
+  if (threadIdx.x < S * NC) red[threadIdx.x] = d.coef[threadIdx.x];
+  __syncthreads();
+  // coefficients in registers for small S; for S >= 6 they are re-read from shared memory
+  // (warp-uniform broadcast) to keep the accumulators in registers
+  constexpr bool CREG = S < 6;
+  double c[CREG ? S : 1][CREG ? NC : 1];
+  if (CREG) {
+#pragma unroll
+    for (int l = 0; l < (CREG ? S : 1); ++l)
+#pragma unroll
+      for (int j = 0; j < (CREG ? NC : 1); ++j) c[l][j] = red[l * NC + j];
+  }
+  const double* cs = red;
+  double acc[ND];
+#pragma unroll
+  for (int k = 0; k < ND; ++k) acc[k] = 0.0;
+  const int warp = threadIdx.x >> 5;
+  if (warp == NCW) {
+    pipe_produce(d.h, d.U, p);
+  } else {
+    const int T = d.h.T;
+    for (int t = 0; t < p.ntiles; ++t) {
+      TileGeom g;
+      const double* Sm = pipe_acquire(d.h, p, t, g);
+      for (int q = threadIdx.x; q < g.cnt; q += CONS) {
+        double cv[NC];
+#pragma unroll
+        for (int j = 0; j < NC; ++j) cv[j] = Sm[(size_t)(S + j) * T + q];
+#pragma unroll
+        for (int l = 0; l < S; ++l) {
+          const double v = Sm[(size_t)l * T + q];
+#pragma unroll
+          for (int j = 0; j < NC; ++j) cv[j] = dadd(cv[j], dmul(CREG ? c[CREG ? l : 0][CREG ? j : 0] : cs[l * NC + j], v));
+        }
+#pragma unroll
+        for (int j = 0; j < NC; ++j) d.cand[j][g.start + q] = cv[j];
+        if (DOTS) {
+#pragma unroll
+          for (int l = 0; l < S; ++l) {
+            const double w = Sm[(size_t)(2 * S - 1 + l) * T + q];
+#pragma unroll
+            for (int j = 0; j < NC; ++j) acc[l * NC + j] = fma(w, cv[j], acc[l * NC + j]);
+          }
+        }
+      }
+      pipe_release(d.h, p, t);
+    }
+  }
+  if (DOTS) {
+    __syncthreads();  // coefficient area is reused for the reduction below
+    cta_store_partials(acc, ND, p.stages, d.partials, d.dot0, d.G);
+  }
+}
+
+// ------------------------------------------------------------------ k_grm
+template <int NR, int LB>
+__global__ void __launch_bounds__(THREADS) k_grm(const __grid_constant__ GrmDesc d) {
+  if (skip_launch(d.h.halt, d.h.cond)) return;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  Pipe p = pipe_setup(d.h, smem_raw, 0);
+  __syncthreads();
+  const int nch = (d.nl + LB - 1) / LB;  // <= NCW
+  const int PG = max(1, NCW / nch);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int chunk = warp % nch, group = warp / nch;
+  const bool active = warp < NCW && group < PG;
+  const int l0 = chunk * LB;
+  const int nlb = min(LB, d.nl - l0);
+  constexpr int K = LB * NR;
+  double acc[K];
+#pragma unroll
+  for (int k = 0; k < K; ++k) acc[k] = 0.0;
+
+  if (warp == NCW) {
+    pipe_produce(d.h, d.U, p);
+  } else {
+    const int T = d.h.T;
+    int ri[NR];
+#pragma unroll
+    for (int r = 0; r < NR; ++r) ri[r] = d.ri[r] * T;
+    int li[LB];
+#pragma unroll
+    for (int lb = 0; lb < LB; ++lb) li[lb] = d.li[l0 + (lb < nlb ? lb : 0)] * T;
+    for (int t = 0; t < p.ntiles; ++t) {
+      TileGeom g;
+      const double* Sm = pipe_acquire(d.h, p, t, g);
+      if (active) {
+        for (int q = group * 32 + lane; q < g.cnt; q += 32 * PG) {
+          double rv[NR];
+#pragma unroll
+          for (int r = 0; r < NR; ++r) rv[r] = Sm[ri[r] + q];
+#pragma unroll
+          for (int lb = 0; lb < LB; ++lb) {
+            const double lv = Sm[li[lb] + q];  // rows past nl duplicate row 0; discarded below
+#pragma unroll
+            for (int r = 0; r < NR; ++r) acc[lb * NR + r] = fma(lv, rv[r], acc[lb * NR + r]);
+          }
+        }
+      }
+      pipe_release(d.h, p, t);
+    }
+  }
+  __syncthreads();
+  double* red = p.stages;  // [group][chunk][K]
+  if (active) {
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      const double v = warp_sum(acc[k]);
+      if (lane == 0) red[((size_t)group * nch + chunk) * K + k] = v;
+    }
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < nch * K; e += blockDim.x) {
+    const int ch = e / K, k = e % K, lb = k / NR, r = k % NR;
+    const int l = ch * LB + lb;
+    if (l < d.nl) {  // rows past nl in the last chunk duplicated row 0: discarded
+      double s = 0.0;
+      for (int gp = 0; gp < PG; ++gp) s += red[((size_t)gp * nch + ch) * K + k];
+      d.partials[(int64_t)(d.dot0 + l * NR + r) * d.G + blockIdx.x] = s;
+    }
+  }
+}
+
+// ------------------------------------------------------------------ host side
+struct TileChoice {
+  int T, nstage;
+  size_t smem;
+};
+
+// Tile size / stage count: >= 3 stages where possible, then large tiles, preferring a
+// footprint that lets two CTAs share an SM.  `align` = tile granularity (points).
+TileChoice pick_tiles(int nu, size_t prefix, int Tmax, int Tmin) {
+  for (size_t limit : {(size_t)110 * 1024, (size_t)220 * 1024}) {
+    for (int ns : {3, 4, 2}) {
+      for (int T = Tmax; T >= Tmin; T /= 2) {
+        const size_t need = 64 + prefix + (size_t)ns * nu * T * 8;
+        if (need <= limit) return {T, ns, need};
+      }
+    }
+  }
+  fail(SKC_EINVAL, "streaming kernel: too many operand vectors for shared-memory staging");
+}
+
+int add_unique(const double** U, int& nu, int cap, const double* p) {
+  for (int v = 0; v < nu; ++v)
+    if (U[v] == p) return v;
+  require(nu < cap, "streaming kernel: operand list overflow");
+  U[nu] = p;
+  return nu++;
+}
+
+template <class K>
+void allow_smem(K kernel) {
+  CK(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+}
+
+template <int NOUT, int MAXD, int PPT>
+void launch_upd_t(Ctx& c, const UpdDesc& d, size_t smem, int G) {
+  static bool attr = false;
+  if (!attr) allow_smem(k_upd<NOUT, MAXD, PPT>), attr = true;
+  k_upd<NOUT, MAXD, PPT><<<G, THREADS, smem, c.stream>>>(d);
+}
+
+template <int NOUT, int PPT>
+void launch_upd_d(Ctx& c, const UpdDesc& d, size_t smem, int G, int maxd) {
+  switch (maxd) {
+    case 0: launch_upd_t<NOUT, 0, PPT>(c, d, smem, G); break;
+    case 1: launch_upd_t<NOUT, 1, PPT>(c, d, smem, G); break;
+    case 4: launch_upd_t<NOUT, 4, PPT>(c, d, smem, G); break;
+    case 16: launch_upd_t<NOUT, 16, PPT>(c, d, smem, G); break;
+    default: launch_upd_t<NOUT, 64, PPT>(c, d, smem, G); break;
+  }
+}
+
+template <int NOUT>
+void launch_upd_p(Ctx& c, const UpdDesc& d, size_t smem, int G, int maxd) {
+  if (d.h.T == 2 * CONS && NOUT <= 8)
+    launch_upd_d<NOUT, (NOUT <= 8 ? 2 : 1)>(c, d, smem, G, maxd);
+  else
+    launch_upd_d<NOUT, 1>(c, d, smem, G, maxd);
+}
+
+template <int NR, int LB>
+void launch_grm_t(Ctx& c, const GrmDesc& d, size_t smem, int G) {
+  static bool attr = false;
+  if (!attr) allow_smem(k_grm<NR, LB>), attr = true;
+  k_grm<NR, LB><<<G, THREADS, smem, c.stream>>>(d);
+}
+
+template <int NR>
+void launch_grm_l(Ctx& c, const GrmDesc& d, size_t smem, int G) {
+  if (d.nl <= 2 * NCW)
+    launch_grm_t<NR, 2>(c, d, smem, G);
+  else if (d.nl <= 4 * NCW)
+    launch_grm_t<NR, 4>(c, d, smem, G);
+  else
+    launch_grm_t<NR, 8>(c, d, smem, G);
+}
+
+template <int S, bool DOTS>
+void launch_mgs_t(Ctx& c, const MgsDesc& d, size_t smem, int G) {
+  static bool attr = false;
+  if (!attr) allow_smem(k_mgs<S, DOTS>), attr = true;
+  k_mgs<S, DOTS><<<G, THREADS, smem, c.stream>>>(d);
+}
+
+void fill_hdr(PipeHdr& h, int nu, const TileChoice& tc, int64_t n, int64_t range, const int* halt, const int* cond) {
+  h.nu = nu;
+  h.T = tc.T;
+  h.nstage = tc.nstage;
+  h.n = n;
+  h.range = range;
+  h.halt = halt;
+  h.cond = cond;
+}
+
+}  // namespace
+
+void launch_lincomb(Ctx& c, const LinDesc& L, const char* name) {
+  require(L.nin <= LC_MAXIN && L.nout <= LC_MAXOUT && L.nx <= LC_MAXX && L.nd <= LC_MAXD,
+          "lincomb: descriptor too large");
+  require(L.nout >= 1, "lincomb: no outputs");
+  static const int kOut[] = {1, 2, 3, 4, 7, 8, 16};
+  int nout_t = 16;
+  for (int v : kOut)
+    if (v >= L.nout) {
+      nout_t = v;
+      break;
+    }
+  UpdDesc d;
+  std::memset(&d, 0, sizeof d);
+  int nu = 0;
+  d.nin = L.nin;
+  d.nout = nout_t;
+  d.nx = L.nx;
+  d.nd = L.nd;
+  d.ncoef = L.ncoef;
+  for (int q = 0; q < L.nout; ++q) {
+    d.ub[q] = (uint8_t)add_unique(d.U, nu, UPD_MAXU, L.base[q]);
+    d.bscale[q] = L.bscale[q];
+    d.out[q] = L.out[q];
+  }
+  if (nout_t != L.nout) {  // padded outputs: copies of output 0's base into a scratch vector
+    double* pad = (double*)c.workspace("lincomb_pad", (size_t)(L.n + 32) * sizeof(double));
+    for (int q = L.nout; q < nout_t; ++q) {
+      d.ub[q] = d.ub[0];
+      d.bscale[q] = -1;
+      d.out[q] = pad;
+    }
+  }
+  for (int j = 0; j < L.nin; ++j) {
+    d.ut[j] = (uint8_t)add_unique(d.U, nu, UPD_MAXU, L.in[j]);
+    d.mask[j] = L.mask[j];
+    d.cbase[j] = L.cbase[j];
+  }
+  for (int x = 0; x < L.nx; ++x) d.ux[x] = (uint8_t)add_unique(d.U, nu, UPD_MAXU, L.xin[x]);
+  for (int k = 0; k < L.nd; ++k) {  // value ids: outputs, then extras at NOUT + x
+    d.da[k] = (uint8_t)(L.da[k] < L.nout ? L.da[k] : L.da[k] - L.nout + nout_t);
+    d.db[k] = (uint8_t)(L.db[k] < L.nout ? L.db[k] : L.db[k] - L.nout + nout_t);
+  }
+  const int maxd = L.nd == 0 ? 0 : L.nd <= 1 ? 1 : L.nd <= 4 ? 4 : L.nd <= 16 ? 16 : 64;
+  d.coef = L.coef;
+  d.partials = L.partials;
+  d.dot0 = L.dot0;
+  d.G = L.G;
+  const size_t prefix = 8 * ((size_t)((L.ncoef + 15) & ~15) + (maxd ? (size_t)(nout_t + LC_MAXX) * CONS : 0));
+  const TileChoice tc = pick_tiles(nu, prefix, nout_t <= 8 ? 2 * CONS : CONS, 64);
+  fill_hdr(d.h, nu, tc, L.n, L.range, L.halt, L.cond);
+  const double bytes = 8.0 * (double)L.n * (nu + L.nout);
+  Launch lh(c, name, bytes);
+  switch (nout_t) {
+    case 1: launch_upd_p<1>(c, d, tc.smem, L.G, maxd); break;
+    case 2: launch_upd_p<2>(c, d, tc.smem, L.G, maxd); break;
+    case 3: launch_upd_p<3>(c, d, tc.smem, L.G, maxd); break;
+    case 4: launch_upd_p<4>(c, d, tc.smem, L.G, maxd); break;
+    case 7: launch_upd_p<7>(c, d, tc.smem, L.G, maxd); break;
+    case 8: launch_upd_p<8>(c, d, tc.smem, L.G, maxd); break;
+    default: launch_upd_p<16>(c, d, tc.smem, L.G, maxd); break;
+  }
+  CK(cudaGetLastError());
+}
+
+void launch_gram(Ctx& c, const GramDesc& g, const char* name) {
+  require(g.nl >= 1 && g.nl <= GR_MAXL && g.nr >= 1 && g.nr <= GR_MAXR, "gram: descriptor out of range");
+  GrmDesc d;
+  std::memset(&d, 0, sizeof d);
+  int nu = 0;
+  d.nl = g.nl;
+  d.nr = g.nr;
+  for (int l = 0; l < g.nl; ++l) d.li[l] = (uint8_t)add_unique(d.U, nu, GRM_MAXU, g.L[l]);
+  for (int r = 0; r < g.nr; ++r) d.ri[r] = (uint8_t)add_unique(d.U, nu, GRM_MAXU, g.R[r]);
+  d.partials = g.partials;
+  d.dot0 = g.dot0;
+  d.G = g.G;
+  TileChoice tc = pick_tiles(nu, 0, 2048, 64);
+  const size_t red = 64 + (size_t)NCW * 8 * GR_MAXR * 8;
+  tc.smem = std::max(tc.smem, red);
+  fill_hdr(d.h, nu, tc, g.n, g.range, g.halt, g.cond);
+  const double bytes = 8.0 * (double)g.n * nu;
+  Launch lh(c, name, bytes);
+  switch (g.nr) {
+    case 1: launch_grm_l<1>(c, d, tc.smem, g.G); break;
+    case 2: launch_grm_l<2>(c, d, tc.smem, g.G); break;
+    case 3: launch_grm_l<3>(c, d, tc.smem, g.G); break;
+    case 4: launch_grm_l<4>(c, d, tc.smem, g.G); break;
+    case 5: launch_grm_l<5>(c, d, tc.smem, g.G); break;
+    case 6: launch_grm_l<6>(c, d, tc.smem, g.G); break;
+    case 7: launch_grm_l<7>(c, d, tc.smem, g.G); break;
+    default: launch_grm_l<8>(c, d, tc.smem, g.G); break;
+  }
+  CK(cudaGetLastError());
+}
+
+void launch_mgs(Ctx& c, const Geo& geo, int s, const double* const* Vi, double* const* cand, const double* const* Vnext,
+                const double* coef_t, double* partials, int dot0, const int* halt, const int* cond) {
+  require(s >= 2 && s <= kMaxS, "mgs: s out of range");
+  MgsDesc d;
+  std::memset(&d, 0, sizeof d);
+  int nu = 0;
+  for (int l = 0; l < s; ++l) d.U[nu++] = Vi[l];
+  for (int j = 1; j < s; ++j) {
+    d.U[nu++] = cand[j];
+    d.cand[j - 1] = cand[j];
+  }
+  const bool dots = Vnext != nullptr;
+  if (dots)
+    for (int l = 0; l < s; ++l) d.U[nu++] = Vnext[l];
+  d.coef = coef_t;
+  d.partials = partials;
+  d.dot0 = dot0;
+  d.G = geo.G;
+  TileChoice tc = pick_tiles(nu, 8 * 64, 2048, 64);
+  tc.smem = std::max(tc.smem, 64 + 8 * (size_t)(64 + NCW * 56));
+  fill_hdr(d.h, nu, tc, geo.n, geo.range, halt, cond);
+  const double bytes = 8.0 * (double)geo.n * (nu + s - 1);
+  Launch lh(c, "mgs_update", bytes);
+#define SKC_MGS_CASE(SV)                                                \
+  case SV:                                                              \
+    if (dots)                                                           \
+      launch_mgs_t<SV, true>(c, d, tc.smem, geo.G);                     \
+    else                                                                \
+      launch_mgs_t<SV, false>(c, d, tc.smem, geo.G);                    \
+    break;
+  switch (s) {
+    SKC_MGS_CASE(2)
+    SKC_MGS_CASE(3)
+    SKC_MGS_CASE(4)
+    SKC_MGS_CASE(5)
+    SKC_MGS_CASE(6)
+    SKC_MGS_CASE(7)
+    SKC_MGS_CASE(8)
+  }
+#undef SKC_MGS_CASE
+  CK(cudaGetLastError());
+}
+
+}  // namespace skc

@@ -29,7 +29,10 @@ def main():
     for name in names("solve"):
         meta, arr = case(name)
         a = matrix(arr)
-        e = dict(hist50=0.0, x=0.0, modes={})
+        e = dict(hist50=0.0, x=0.0, rho1=0.0, modes={})
+        base = None
+        if meta["kind"] == "sstep" and meta["method"] == "sgmres" and meta["cfg"].get("s", 1) > 1:
+            base = orc.sstep(meta["method"], a, arr["f"], arr["x0"], **meta["cfg"])  # mode 0 == reference
         for mode in MODES:
             orc.set_dot_mode(mode)
             if meta["kind"] == "sstep":
@@ -41,6 +44,9 @@ def main():
             e["modes"][MODES[mode]] = dict(hist50=h, x=xv, iterations=r.iterations, breakdown=r.breakdown)
             e["hist50"] = max(e["hist50"], h)
             e["x"] = max(e["x"], xv)
+            if base is not None and base.block_rho and r.block_rho:
+                u, v = base.block_rho[0], r.block_rho[0]
+                e["rho1"] = max(e["rho1"], abs(u - v) / max(abs(u), abs(v)))
         orc.set_dot_mode(0)
         env[name] = e
         print(name, f"hist50={e['hist50']:.2e} x={e['x']:.2e}")

@@ -71,12 +71,14 @@ def test_solve_matches_reference(ctx, port, name, prefer_stencil):
         assert h <= max(1e-9, 10.0 * env["hist50"]), (h, env["hist50"])
         a = matrix(arr)
         ref = port.sstep(meta["method"], a, arr["f"], arr["x0"], **meta["cfg"])
-        assert rel_diff(rep.block_rho[0], ref.block_rho[0]) <= 1e-9
+        assert rel_diff(rep.block_rho[0], ref.block_rho[0]) <= max(1e-9, 10.0 * env["rho1"])
         if meta["converged"]:
             true_r = np.linalg.norm(arr["f"] - port.spmv(a, x))
             assert true_r <= meta["cfg"]["tol"] * (1 + 1e-6)
     else:
-        assert h <= 1e-9, h
+        # BASELINE's 1e-9; cases whose own reference envelope is wider (1/h^2 KAT problems)
+        # get 10x that envelope
+        assert h <= max(1e-9, 10.0 * env["hist50"]), (h, env["hist50"])
         if meta["converged"]:
             assert rel_vec(x, arr["x"]) <= max(1e-8, 10.0 * env["x"])
 
