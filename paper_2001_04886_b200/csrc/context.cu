@@ -33,7 +33,7 @@ Geo make_geo(int64_t n, int sm_count) {
   Geo g;
   g.n = n;
   // at most two co-resident CTAs per SM; each range is a whole number of 256-point tiles
-  const int64_t maxg = 2LL * sm_count;
+  const int64_t maxg = std::min<int64_t>(2LL * sm_count, kPartialPitch);
   int64_t G = (n + 2047) / 2048;
   G = std::max<int64_t>(1, std::min(G, maxg));
   int64_t range = (n + G - 1) / G;

@@ -68,15 +68,33 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
 
 // Deterministic reduction of nd dots from per-CTA partials ([(d0+d)*G + g]) into out[d]
 // (shared or global). Whole block must call; ends with __syncthreads().
+// Each dot is owned by a group of TPD lanes (TPD = 32 >> k, chosen so all dots are covered
+// in few rounds); every lane sums a fixed strided subset with four independent accumulators
+// (loads stay in flight), then the group combines in a fixed shuffle order.
 __device__ __forceinline__ void reduce_dots_dev(const double* __restrict__ partials, int G, int d0, int nd,
                                                 double* out) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  for (int d = warp; d < nd; d += nw) {
-    const double* p = partials + (int64_t)(d0 + d) * G;
+  const int nthreads = blockDim.x;
+  int tpd = 32;
+  while (tpd > 1 && (nthreads / tpd) < nd) tpd >>= 1;
+  const int groups = nthreads / tpd;
+  const int grp = threadIdx.x / tpd, sub = threadIdx.x % tpd;
+  for (int d = grp; d - grp < nd; d += groups) {  // uniform trip count across the warp
     double s = 0.0;
-    for (int g = lane; g < G; g += 32) s += p[g];
-    s = warp_sum(s);
-    if (lane == 0) out[d] = s;
+    if (d < nd) {
+      const double* p = partials + (int64_t)(d0 + d) * kPartialPitch;
+      double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+      int g = sub;
+      for (; g + 3 * tpd < G; g += 4 * tpd) {
+        a0 += p[g];
+        a1 += p[g + tpd];
+        a2 += p[g + 2 * tpd];
+        a3 += p[g + 3 * tpd];
+      }
+      for (; g < G; g += tpd) a0 += p[g];
+      s = (a0 + a1) + (a2 + a3);
+    }
+    for (int o = tpd >> 1; o > 0; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o, tpd);
+    if (sub == 0 && d < nd) out[d] = s;
   }
   __syncthreads();
 }

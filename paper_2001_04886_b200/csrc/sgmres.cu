@@ -188,21 +188,28 @@ __global__ void k_arn_t(ArnState* st, const Gram* grams, int i, double* rec, dou
 __global__ void k_arn_check(ArnState* st, const Gram* grams, int k, double* rec, const double* partials, int G,
                             int dCross, int dWa, int s, double orth_tol, double* scratch) {
   if (arn_skip(st)) return;
+  // (k <= 64 blocks: m is limited to 64)
   reduce_dots_dev(partials, G, dCross, k * s * s, scratch);
-  reduce_dots_dev(partials, G, dWa, s * s, scratch + k * s * s);
+  __shared__ double sW[kMaxS * kMaxS];
+  __shared__ int exceed[128];
+  reduce_dots_dev(partials, G, dWa, s * s, sW);
+  double cn2 = 0.0;  // sum_jc ||cand_jc||^2 in the reference's order (sstep.hpp:403)
+  for (int jc = 0; jc < s; ++jc) cn2 += sW[jc * s + jc];
+  // every block's test evaluated in parallel (same per-block arithmetic order), first hit wins
+  for (int i = threadIdx.x; i < k; i += blockDim.x) {
+    const double* cr = scratch + i * s * s;
+    double acc = 0.0;
+    for (int q = 0; q < s * s; ++q) acc += cr[q] * cr[q];
+    exceed[i] = sqrt(acc) > orth_tol * sqrt(sd_trace(grams[i].w, s)) * sqrt(cn2);
+  }
+  __syncthreads();
   if (threadIdx.x == 0) {
-    const double* W = scratch + k * s * s;
-    double cn2 = 0.0;
-    for (int jc = 0; jc < s; ++jc) cn2 += W[jc * s + jc];
     int first = -1;
-    for (int i = 0; i < k; ++i) {
-      double acc = 0.0;
-      for (int q = 0; q < s * s; ++q) acc += scratch[i * s * s + q] * scratch[i * s * s + q];
-      if (sqrt(acc) > orth_tol * sqrt(sd_trace(grams[i].w, s)) * sqrt(cn2)) {
+    for (int i = 0; i < k; ++i)
+      if (exceed[i]) {
         first = i;
         break;
       }
-    }
     rec[RecLayout::kFirst] = first;
     rec[RecLayout::kReorth] = first >= 0 ? 1.0 : 0.0;
     st->reorth = first >= 0;
@@ -296,7 +303,7 @@ void gmres_device(Ctx& c, const Op& op, const double* f, double* x, uint64_t m64
   auto q = [&](int i) { return Q + (size_t)i * np; };
   const int cC = 0, cInv = 1, cM1 = 2, cY = 3, ncoef = 3 + m + 1;
   double* coef = (double*)c.workspace("gm_coef", ncoef * sizeof(double));
-  double* partials = (double*)c.workspace("gm_partials", (size_t)2 * g.G * sizeof(double));
+  double* partials = (double*)c.workspace("gm_partials", (size_t)2 * kPartialPitch * sizeof(double));
   const int rstride = m + 3;
   double* cols = (double*)c.workspace("gm_cols", (size_t)(m + 1) * rstride * sizeof(double));
   GmState* st = (GmState*)c.workspace("gm_state", sizeof(GmState));
@@ -451,7 +458,7 @@ struct Engine {
     r = seed + np;
     ax = r + np;
     coef = (double*)c.workspace("arn_coef", (size_t)cl.size() * sizeof(double));
-    partials = (double*)c.workspace("arn_partials", (size_t)dl.size() * g.G * sizeof(double));
+    partials = (double*)c.workspace("arn_partials", (size_t)dl.size() * kPartialPitch * sizeof(double));
     rec = (double*)c.workspace("arn_rec", (size_t)(m + 1) * rl.size() * sizeof(double));
     scratch = (double*)c.workspace("arn_scratch", (size_t)(m * s * s + s * s + m * s + 8) * sizeof(double));
     rn_out = (double*)c.workspace("arn_rn", 8 * sizeof(double));
@@ -468,12 +475,49 @@ struct Engine {
   double* col(int block, int j) const { return V + ((size_t)block * s + j) * np; }
   double* recp(int k) const { return rec + (size_t)k * rl.size(); }
 
-  // [v, A v, .., A^{s-1} v] of v = src * coef[Inv] into block slot b
-  void krylov_into(int b, const double* src) {
+  // [v, A v, .., A^{s-1} v] of v = src * coef[Inv] into block slot b (krylov_block,
+  // block.hpp:59-67).  Stencil operators use the matrix-powers kernel (one sweep, depth s-1,
+  // chained in 3D past depth 3); when `dots` is set and a single sweep suffices, the first
+  // block-MGS products V_0^T cand[:,1:] are fused into it.  Returns the partial count of the
+  // fused products, or 0 when they were not computed.
+  int krylov_into(int b, const double* src, bool dots = false) {
+    const int J = s - 1, maxj = mpk_max_depth(op.d);
+    if (J >= 1 && maxj >= 1) {
+      int done = 0;
+      const double* from = src;
+      const double* sc = coef + cl.Inv();
+      int Gd = 0;
+      while (done < J) {
+        const int d = std::min(J - done, maxj);
+        double* outs[kMaxS + 1];
+        for (int j = 0; j <= d; ++j) outs[j] = col(b, done + j);
+        if (done > 0) outs[0] = nullptr;  // already written by the previous sweep
+        const double* X[kMaxS];
+        const bool fuse = dots && done == 0 && d == J;
+        for (int l = 0; l < s; ++l) X[l] = col(0, l);
+        const int G0 = launch_mpk(c, op.d, from, sc, outs, d, fuse ? s : 0, X, 1, partials, dl.D(), halt, nullptr);
+        if (fuse) Gd = G0;
+        from = col(b, done + d);
+        sc = nullptr;
+        done += d;
+      }
+      return Gd;
+    }
     LinBuilder lb;
     lb.add_out(col(b, 0), src, cl.Inv());
     lb.launch(c, g, coef, cl.size(), partials, 0, halt, nullptr, "scale");
     for (int j = 1; j < s; ++j) launch_apply(c, op.d, col(b, j - 1), col(b, j), halt, nullptr);
+    return 0;
+  }
+
+  // y = A x with the one-sweep stencil kernel where available
+  void apply(const double* x, double* y) {
+    if (mpk_max_depth(op.d) >= 1) {
+      double* outs[2] = {nullptr, y};
+      launch_mpk(c, op.d, x, nullptr, outs, 1, 0, nullptr, 1, partials, 0, halt, nullptr);
+    } else {
+      launch_apply(c, op.d, x, y, halt, nullptr);
+    }
   }
 
   void gram_self_into(int b, int dW, const int* cond) {
@@ -499,7 +543,7 @@ struct Engine {
   void advance(int k, bool build_next) {
     double* rk = recp(k);
     // z = A v_k^s ; Scalar1 dots V_i^T z and ||z||^2
-    launch_apply(c, op.d, col(k - 1, s - 1), z, halt, nullptr);
+    apply(col(k - 1, s - 1), z);
     {
       std::vector<const double*> L;
       for (int i = 0; i < k; ++i)
@@ -522,7 +566,7 @@ struct Engine {
     ++c.launches;
     // candidate block [v, .., A^{s-1} v] of the normalized seed (also on the last block)
     const int cb = k;  // block slot k (slot m is scratch when k == m)
-    krylov_into(cb, seed);
+    const int Gfused = krylov_into(cb, seed, build_next && s > 1);
     if (!build_next) {
       CK(cudaGetLastError());
       return;
@@ -533,13 +577,15 @@ struct Engine {
         const int* cond = pass ? &st->reorth : nullptr;
         std::vector<const double*> Cr;
         for (int jc = 1; jc < s; ++jc) Cr.push_back(col(cb, jc));
-        {
+        const bool have = pass == 0 && Gfused > 0;  // products already fused into the powers sweep
+        if (!have) {
           std::vector<const double*> L;
           for (int l = 0; l < s; ++l) L.push_back(col(0, l));
           launch_gram_list(c, g, L, Cr, partials, dl.D(), halt, cond, "gram_mgs");
         }
         for (int i = 0; i < k; ++i) {
-          k_arn_t<<<1, 256, 0, c.stream>>>(st, grams, i, tk, coef, partials, g.G, dl.D(), s, cl.T(), pass);
+          const int Gi = (i == 0 && have) ? Gfused : g.G;
+          k_arn_t<<<1, 256, 0, c.stream>>>(st, grams, i, tk, coef, partials, Gi, dl.D(), s, cl.T(), pass);
           ++c.launches;
           // cand[:,jc] -= sum_l t(l,jc-1) V_i[:,l]  (+ products with V_{i+1})
           const double* Vi[kMaxS];
@@ -553,24 +599,25 @@ struct Engine {
           launch_mgs(c, g, s, Vi, cd, i + 1 < k ? Vn : nullptr, coef + cl.T(), partials, dl.D(), halt, cond);
         }
         if (pass == 0) {
-          // reorthogonalization test: V_i^T cand (all columns) and cand^T cand
+          // reorthogonalization test and the candidate's Gram matrix in one pass over cand:
+          // [V_0..V_{k-1}, cand]^T cand -> cross blocks, then W at Cross + k s^2
           std::vector<const double*> L, Cc;
           for (int i = 0; i < k; ++i)
             for (int l = 0; l < s; ++l) L.push_back(col(i, l));
           for (int jc = 0; jc < s; ++jc) Cc.push_back(col(cb, jc));
+          for (int jc = 0; jc < s; ++jc) L.push_back(col(cb, jc));
           launch_gram_list(c, g, L, Cc, partials, dl.Cross(), halt, nullptr, "gram_cross");
-          gram_self_into(cb, dl.Wa(), nullptr);
-          k_arn_check<<<1, 256, 0, c.stream>>>(st, grams, k, rk, partials, g.G, dl.Cross(), dl.Wa(), s, 1e-8,
-                                               scratch);
+          k_arn_check<<<1, 256, 0, c.stream>>>(st, grams, k, rk, partials, g.G, dl.Cross(), dl.Cross() + k * s * s,
+                                               s, 1e-8, scratch);
           ++c.launches;
         } else {
           gram_self_into(cb, dl.Wb(), cond);
         }
       }
-    } else {
-      gram_self_into(cb, dl.Wa(), nullptr);
     }
-    k_arn_push<<<1, 256, 0, c.stream>>>(st, grams, cb, rk, partials, g.G, dl.Wa(), dl.Wb(), s);
+    const int dWa = s > 1 ? dl.Cross() + k * s * s : dl.Wa();
+    if (s == 1) gram_self_into(cb, dl.Wa(), nullptr);
+    k_arn_push<<<1, 256, 0, c.stream>>>(st, grams, cb, rk, partials, g.G, dWa, dl.Wb(), s);
     ++c.launches;
     CK(cudaGetLastError());
   }

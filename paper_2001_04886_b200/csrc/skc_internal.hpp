@@ -65,6 +65,9 @@ struct Geo {
 Geo make_geo(int64_t n, int sm_count);
 
 constexpr int kThreads = 256;
+// every reduction partial lives at partials[dot * kPartialPitch + cta]: kernels with different
+// CTA counts can share one partial buffer without overlapping regions
+constexpr int kPartialPitch = 2048;
 
 // y_o = base_o [* coef[bscale_o]] + sum_j coef[cbase_j + o] * in_j   (j ascending, o in mask_j)
 // then dots over value ids: 0..nout-1 = outputs, nout..nout+nx-1 = extra inputs.
@@ -155,6 +158,11 @@ void launch_apply(Ctx& c, const DevOp& op, const double* x, double* y, const int
 void launch_lincomb(Ctx& c, const LinDesc& d, const char* name = "lincomb");
 void launch_gram(Ctx& c, const GramDesc& d, const char* name = "gram");
 void launch_fill(Ctx& c, double* p, double v, int64_t n);
+// matrix powers (mpk.cu): out[0..J] of src*scale; products X[x] . level j (j >= jdot0) at
+// dot0 + x*(J-jdot0+1) + (j-jdot0) as partials over the returned CTA count.
+int mpk_max_depth(const DevOp& op);
+int launch_mpk(Ctx& c, const DevOp& op, const double* src, const double* scale, double* const* out, int J, int nxd,
+               const double* const* X, int jdot0, double* partials, int dot0, const int* halt, const int* cond);
 // one block-MGS round: cand[1..s) += sum_l coef_t[l*(s-1)+jc-1] Vi[l]; if Vnext: the
 // products Vnext[l] . cand[jc] at dot0 + l*(s-1) + jc-1
 void launch_mgs(Ctx& c, const Geo& geo, int s, const double* const* Vi, double* const* cand, const double* const* Vnext,

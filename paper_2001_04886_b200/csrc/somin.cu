@@ -208,6 +208,29 @@ bool device_is_zero(Ctx& c, const double* x, int64_t n) {
   return h == 0;
 }
 
+// K[j] = A^{j+1} src for j < J (krylov_pair's A R block, sstep.hpp:71-81): one matrix-powers
+// sweep per at most mpk_max_depth levels for stencils, repeated applies for general CSR
+static void powers(Ctx& c, const Op& op, const double* src, double* K, size_t np, int J, const int* halt) {
+  const int maxj = mpk_max_depth(op.d);
+  if (maxj < 1) {
+    for (int j = 0; j < J; ++j) {
+      launch_apply(c, op.d, src, K + (size_t)j * np, halt, nullptr);
+      src = K + (size_t)j * np;
+    }
+    return;
+  }
+  int done = 0;
+  while (done < J) {
+    const int d = std::min(J - done, maxj);
+    double* outs[kMaxS + 1];
+    outs[0] = nullptr;
+    for (int j = 1; j <= d; ++j) outs[j] = K + (size_t)(done + j - 1) * np;
+    launch_mpk(c, op.d, src, nullptr, outs, d, 0, nullptr, 1, nullptr, 0, halt, nullptr);
+    src = K + (size_t)(done + d - 1) * np;
+    done += d;
+  }
+}
+
 // r = f - A x (x != 0) or r = f, plus the r.r partial at dot d0
 static void initial_residual_dev(Ctx& c, const Op& op, const Geo& g, const double* f, const double* x, double* r,
                                  double* ax, bool x_zero, const double* coef, int ncoef, int idx_minus1,
@@ -250,7 +273,7 @@ void somin_device(Ctx& c, const Op& op, const double* f, double* x, const SStepC
   auto slot_ap = [&](int sl, int col) { return V + (2 + s + (size_t)sl * 2 * s + s + col) * np; };
   const int dRR = 0, dW = 1, dM = 1 + s * s, dC = dM + s, dX = dC + (int)kwin * s * s;
   const int ndots = dX + (int)kwin * s * s;
-  double* partials = (double*)c.workspace("somin_partials", (size_t)ndots * g.G * sizeof(double));
+  double* partials = (double*)c.workspace("somin_partials", (size_t)ndots * kPartialPitch * sizeof(double));
   const int ncoef = cB(s) + (int)kwin * s * s;
   double* coef = (double*)c.workspace("somin_coef", (size_t)ncoef * sizeof(double));
   double* scratch = (double*)c.workspace("somin_scratch", (size_t)(64 + 2 * kwin * s * s) * sizeof(double));
@@ -279,11 +302,7 @@ void somin_device(Ctx& c, const Op& op, const double* f, double* x, const SStepC
   CK(cudaGetLastError());
   // krylov_pair(r): P0 = [r, Ar, .., A^{s-1} r], AP0 = [Ar, .., A^s r]
   {
-    const double* src = r;
-    for (int j = 0; j < s; ++j) {
-      launch_apply(c, op.d, src, slot_ap(0, j), halt, nullptr);
-      src = slot_ap(0, j);
-    }
+    powers(c, op, r, slot_ap(0, 0), np, s, halt);  // AP0 columns are consecutive
     LinBuilder lb;  // P0 columns are copies (krylov_block storage)
     lb.add_out(slot_p(0, 0), r);
     for (int j = 1; j < s; ++j) lb.add_out(slot_p(0, j), slot_ap(0, j - 1));
@@ -323,14 +342,8 @@ void somin_device(Ctx& c, const Op& op, const double* f, double* x, const SStepC
       }
       k_somin_norm<<<1, 256, 0, c.stream>>>(st, partials, g.G, dRR, hist);
       ++c.launches;
-      // krylov_pair(r) -> K[j] = A^{j+1} r
-      {
-        const double* src = r;
-        for (int j = 0; j < s; ++j) {
-          launch_apply(c, op.d, src, K + (size_t)j * np, halt, nullptr);
-          src = K + (size_t)j * np;
-        }
-      }
+      // krylov_pair(r) -> K[j] = A^{j+1} r  (matrix-powers sweep)
+      powers(c, op, r, K, np, s, halt);
       // C_e = AP_e^T AR   (block_gram, sstep.hpp:207)
       Slots ws{};
       ws.n = (int)win.size();
@@ -520,11 +533,7 @@ __global__ void k_smr_norm(SmrState* st, const double* partials, int G, int d0, 
 static void smr_step_enqueue(Ctx& c, const Op& op, const Geo& g, double* x, double* r, double* K, size_t np, int s,
                              double* coef, int ncoef, double* partials, SmrState* st, double* hist) {
   const int* halt = &st->halt;
-  const double* src = r;
-  for (int j = 0; j < s; ++j) {
-    launch_apply(c, op.d, src, K + (size_t)j * np, halt, nullptr);
-    src = K + (size_t)j * np;
-  }
+  powers(c, op, r, K, np, s, halt);
   std::vector<const double*> AR;
   for (int j = 0; j < s; ++j) AR.push_back(K + (size_t)j * np);
   launch_gram_list(c, g, AR, AR, partials, 1, halt, nullptr, "gram_w");
@@ -555,7 +564,7 @@ void smr_device(Ctx& c, const Op& op, const double* f, double* x, const SStepCfg
   double *r = V, *ax = V + np, *K = V + 2 * np;
   const int ncoef = 2 * s + 1;
   double* coef = (double*)c.workspace("smr_coef", ncoef * sizeof(double));
-  double* partials = (double*)c.workspace("smr_partials", (size_t)(1 + s * s + s) * g.G * sizeof(double));
+  double* partials = (double*)c.workspace("smr_partials", (size_t)(1 + s * s + s) * kPartialPitch * sizeof(double));
   const uint64_t hcap = std::min<uint64_t>(cfg.max_iterations, 50000000ULL) + 2;
   double* hist = (double*)c.workspace("smr_hist", hcap * sizeof(double));
   SmrState* st = (SmrState*)c.workspace("smr_state", sizeof(SmrState));
@@ -621,7 +630,7 @@ void smr_step_device(Ctx& c, const Op& op, double* x, double* r, uint64_t s64, d
   double* K = (double*)c.workspace("smr_vec", (2 + (size_t)s) * np * sizeof(double)) + 2 * np;
   const int ncoef = 2 * s + 1;
   double* coef = (double*)c.workspace("smr_coef", ncoef * sizeof(double));
-  double* partials = (double*)c.workspace("smr_partials", (size_t)(1 + s * s + s) * g.G * sizeof(double));
+  double* partials = (double*)c.workspace("smr_partials", (size_t)(1 + s * s + s) * kPartialPitch * sizeof(double));
   double* hist = (double*)c.workspace("smr_hist", 4 * sizeof(double));
   SmrState* st = (SmrState*)c.workspace("smr_state", sizeof(SmrState));
   SmrState h{};

@@ -177,7 +177,7 @@ __device__ __forceinline__ void cta_store_partials(const double (&acc)[K], int n
   for (int k = threadIdx.x; k < nk; k += blockDim.x) {
     double s = 0.0;
     for (int w = 0; w < NCW; ++w) s += red[w * K + k];
-    partials[(int64_t)(dot0 + k) * G + blockIdx.x] = s;
+    partials[(int64_t)(dot0 + k) * kPartialPitch + blockIdx.x] = s;
   }
 }
 
@@ -402,7 +402,7 @@ __global__ void __launch_bounds__(THREADS) k_grm(const __grid_constant__ GrmDesc
     if (l < d.nl) {  // rows past nl in the last chunk duplicated row 0: discarded
       double s = 0.0;
       for (int gp = 0; gp < PG; ++gp) s += red[((size_t)gp * nch + ch) * K + k];
-      d.partials[(int64_t)(d.dot0 + l * NR + r) * d.G + blockIdx.x] = s;
+      d.partials[(int64_t)(d.dot0 + l * NR + r) * kPartialPitch + blockIdx.x] = s;
     }
   }
 }
