@@ -473,14 +473,19 @@ void launch_grm_t(Ctx& c, const GrmDesc& d, size_t smem, int G) {
   k_grm<NR, LB><<<G, THREADS, smem, c.stream>>>(d);
 }
 
+// LB = ceil(nl / 8) rows per warp so all eight consumer warps carry a share of the rows
 template <int NR>
 void launch_grm_l(Ctx& c, const GrmDesc& d, size_t smem, int G) {
-  if (d.nl <= 2 * NCW)
-    launch_grm_t<NR, 2>(c, d, smem, G);
-  else if (d.nl <= 4 * NCW)
-    launch_grm_t<NR, 4>(c, d, smem, G);
-  else
-    launch_grm_t<NR, 8>(c, d, smem, G);
+  switch ((d.nl + NCW - 1) / NCW) {
+    case 1: launch_grm_t<NR, 1>(c, d, smem, G); break;
+    case 2: launch_grm_t<NR, 2>(c, d, smem, G); break;
+    case 3: launch_grm_t<NR, 3>(c, d, smem, G); break;
+    case 4: launch_grm_t<NR, 4>(c, d, smem, G); break;
+    case 5: launch_grm_t<NR, 5>(c, d, smem, G); break;
+    case 6: launch_grm_t<NR, 6>(c, d, smem, G); break;
+    case 7: launch_grm_t<NR, 7>(c, d, smem, G); break;
+    default: launch_grm_t<NR, 8>(c, d, smem, G); break;
+  }
 }
 
 template <int S, bool DOTS>
