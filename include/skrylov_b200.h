@@ -177,6 +177,29 @@ int skc_sarnoldi(skc_ctx* ctx, const skc_op* op, const double* v1, uint64_t s, u
                  double* blocks_out, double* grams_out, double* hess_out, double* seed_out,
                  double* seed_norm_out, skc_op_counter* counter);
 
+/* ---- multi-GPU row-slab decomposition (new -- the reference is single-threaded) ----
+ * One process (context) per GPU.  The slowest grid dimension (y in 2D, z in 3D) is split into
+ * contiguous slabs, rank r owning global rows [lo, hi) = [R*r/P, R*(r+1)/P).  Solves then take
+ * the rank's slab of f and x (the unknowns of rows lo..hi-1, natural order) and every rank
+ * returns the same report; ghost rows of width <= 8 are exchanged before each matrix-powers
+ * sweep and the per-rank dot sums are allgathered and added in rank order at every reduction.
+ * NCCL: rank 0 calls skc_nccl_unique_id, the caller broadcasts the 128 bytes, every rank calls
+ * skc_ctx_create_nccl.  The callback backend stages through host memory and lets several
+ * processes share one GPU (tests). */
+typedef int (*skc_allgather_fn)(void* user, const double* send, double* recv, uint64_t n);
+typedef int (*skc_halo_fn)(void* user, const double* lo_send, double* lo_recv, uint64_t n_lo,
+                           const double* hi_send, double* hi_recv, uint64_t n_hi);
+int skc_nccl_unique_id(void* out128);
+int skc_ctx_create_nccl(int device, int rank, int world, const void* id128, skc_ctx** out);
+int skc_ctx_create_callback(int device, int rank, int world, skc_allgather_fn allgather, skc_halo_fn halo,
+                            void* user, skc_ctx** out);
+int skc_ctx_world(const skc_ctx* ctx, int* rank, int* world);
+/* slab of the global stencil owned by ctx's rank; kcell_global (n_global entries) for kind 1 */
+int skc_op_create_stencil_slab(skc_ctx* ctx, const skc_stencil_desc* global_desc, const double* kcell_global,
+                               uint64_t* row_lo, uint64_t* row_hi, skc_op** out);
+/* the partition rule above (pure function, no GPU) */
+int skc_slab_range(uint64_t rows, int world, int rank, uint64_t* lo, uint64_t* hi);
+
 /* ---- host small-dense (no GPU needed; the same code runs inside the scalar kernels) ---- */
 int skc_gram_solve(uint64_t order, const double* w, uint64_t nrhs, const double* rhs, double* x_out,
                    int32_t* used_ldlt, double* pivots_out);

@@ -72,7 +72,12 @@ EXPORTS = [
     "skc_report_get_breakdown", "skc_report_get_note", "skc_somin_solve", "skc_sgmres_solve", "skc_smr_solve",
     "skc_gmres_solve", "skc_smr_step", "skc_somin_solve_device", "skc_sgmres_solve_device", "skc_sarnoldi",
     "skc_gram_solve", "skc_cholesky_upper", "skc_hessenberg_lsq",
+    "skc_nccl_unique_id", "skc_ctx_create_nccl", "skc_ctx_create_callback", "skc_ctx_world",
+    "skc_op_create_stencil_slab", "skc_slab_range",
 ]
+
+ALLGATHER_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, P(dbl), P(dbl), u64)
+HALO_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, P(dbl), P(dbl), u64, P(dbl), P(dbl), u64)
 
 _lib = None
 
@@ -119,6 +124,12 @@ def lib():
         "skc_gram_solve": [u64, P(dbl), u64, P(dbl), P(dbl), P(i32), P(dbl)],
         "skc_cholesky_upper": [u64, P(dbl), P(dbl)],
         "skc_hessenberg_lsq": [u64, u64, P(dbl), dbl, P(dbl), P(dbl)],
+        "skc_nccl_unique_id": [vp],
+        "skc_ctx_create_nccl": [C.c_int, C.c_int, C.c_int, vp, P(vp)],
+        "skc_ctx_create_callback": [C.c_int, C.c_int, C.c_int, ALLGATHER_FN, HALO_FN, vp, P(vp)],
+        "skc_ctx_world": [vp, P(C.c_int), P(C.c_int)],
+        "skc_op_create_stencil_slab": [vp, P(StencilDescC), P(dbl), P(u64), P(u64), P(vp)],
+        "skc_slab_range": [u64, C.c_int, C.c_int, P(u64), P(u64)],
     }
     for name, args in sig.items():
         fn = getattr(L, name)

@@ -75,6 +75,21 @@ int host_solve(skc_ctx* ctx, const skc_op* op, const double* f, double* x, skc_r
 
 }  // namespace
 
+skc_ctx* make_ctx(int device) {
+  int ndev = 0;
+  CK(cudaGetDeviceCount(&ndev));
+  skc::require(device >= 0 && device < ndev, "skc_ctx_create: device index out of range");
+  CK(cudaSetDevice(device));
+  cudaDeviceProp p;
+  CK(cudaGetDeviceProperties(&p, device));
+  auto* ctx = new skc_ctx;
+  ctx->c.device = device;
+  ctx->c.sm_count = p.multiProcessorCount;
+  CK(cudaStreamCreateWithFlags(&ctx->c.own_stream, cudaStreamNonBlocking));
+  ctx->c.stream = ctx->c.own_stream;
+  return ctx;
+}
+
 extern "C" {
 
 const char* skc_last_error(void) { return g_last_error.c_str(); }
@@ -87,18 +102,7 @@ int skc_device_count(int* count) {
 int skc_ctx_create(int device, skc_ctx** out) {
   return guarded([&] {
     skc::require(out != nullptr, "null output");
-    int ndev = 0;
-    CK(cudaGetDeviceCount(&ndev));
-    skc::require(device >= 0 && device < ndev, "skc_ctx_create: device index out of range");
-    CK(cudaSetDevice(device));
-    cudaDeviceProp p;
-    CK(cudaGetDeviceProperties(&p, device));
-    auto* ctx = new skc_ctx;
-    ctx->c.device = device;
-    ctx->c.sm_count = p.multiProcessorCount;
-    CK(cudaStreamCreateWithFlags(&ctx->c.own_stream, cudaStreamNonBlocking));
-    ctx->c.stream = ctx->c.own_stream;
-    *out = ctx;
+    *out = make_ctx(device);
   });
 }
 
@@ -409,6 +413,76 @@ int skc_sarnoldi(skc_ctx* ctx, const skc_op* op, const double* v1, uint64_t s, u
       counter->vec_updates += b.counter.vec_updates;
       counter->termination_dots += b.counter.termination_dots;
     }
+  });
+}
+
+// ---------------------------------------------------------------- multi-GPU
+int skc_nccl_unique_id(void* out128) {
+  return guarded([&] {
+    skc::require(out128 != nullptr, "null output");
+    skc::nccl_unique_id(out128);
+  });
+}
+
+int skc_ctx_create_nccl(int device, int rank, int world, const void* id128, skc_ctx** out) {
+  return guarded([&] {
+    skc::require(out && id128, "null argument");
+    skc::require(world >= 1 && rank >= 0 && rank < world, "skc_ctx_create_nccl: bad rank/world");
+    skc_ctx* ctx = make_ctx(device);
+    try {
+      ctx->c.comm = skc::make_nccl_comm(rank, world, id128);
+    } catch (...) {
+      delete ctx;
+      throw;
+    }
+    *out = ctx;
+  });
+}
+
+int skc_ctx_create_callback(int device, int rank, int world, skc_allgather_fn allgather, skc_halo_fn halo,
+                            void* user, skc_ctx** out) {
+  return guarded([&] {
+    skc::require(out && allgather && halo, "null argument");
+    skc::require(world >= 1 && rank >= 0 && rank < world, "skc_ctx_create_callback: bad rank/world");
+    skc_ctx* ctx = make_ctx(device);
+    ctx->c.comm = skc::make_callback_comm(rank, world, allgather, halo, user);
+    *out = ctx;
+  });
+}
+
+int skc_ctx_world(const skc_ctx* ctx, int* rank, int* world) {
+  return guarded([&] {
+    skc::require(ctx != nullptr, "null context");
+    if (rank) *rank = ctx->c.rank();
+    if (world) *world = ctx->c.world();
+  });
+}
+
+int skc_op_create_stencil_slab(skc_ctx* ctx, const skc_stencil_desc* desc, const double* kcell_global,
+                               uint64_t* row_lo, uint64_t* row_hi, skc_op** out) {
+  return guarded([&] {
+    skc::require(ctx && desc && out, "null argument");
+    set_device(ctx);
+    auto* op = new skc_op;
+    try {
+      skc::build_stencil_op(ctx->c, op->o, *desc, kcell_global);
+    } catch (...) {
+      delete op;
+      throw;
+    }
+    if (row_lo) *row_lo = (uint64_t)op->o.d.row0;
+    if (row_hi) *row_hi = (uint64_t)(op->o.d.row0 + op->o.n / op->o.rowlen);
+    *out = op;
+  });
+}
+
+int skc_slab_range(uint64_t rows, int world, int rank, uint64_t* lo, uint64_t* hi) {
+  return guarded([&] {
+    skc::require(world >= 1 && rank >= 0 && rank < world && lo && hi, "skc_slab_range: bad arguments");
+    int64_t l = 0, h = 0;
+    skc::slab_range((int64_t)rows, world, rank, l, h);
+    *lo = (uint64_t)l;
+    *hi = (uint64_t)h;
   });
 }
 

@@ -133,12 +133,65 @@ Op::~Op() {
   for (void* p : owned) cudaFree(p);
 }
 
+// ---------------------------------------------------------------- multi-rank reductions / halos
+namespace {
+// per-rank sums of dots [d0, d0+nd) over G CTA partials (same fixed order as the scalar kernels)
+__global__ void k_local_reduce(const double* partials, int G, int d0, int nd, double* out) {
+  for (int d = blockIdx.x; d < nd; d += gridDim.x) {  // one warp per dot, fixed lane order
+    const double* p = partials + (int64_t)(d0 + d) * kPartialPitch;
+    double s = 0.0;
+    for (int g = threadIdx.x; g < G; g += 32) s += p[g];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (threadIdx.x == 0) out[d] = s;
+  }
+}
+// recv[r*nd + d] -> partials[(d0+d)*pitch + r]
+__global__ void k_scatter_ranks(const double* recv, int world, int nd, double* partials, int d0) {
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < world * nd; e += gridDim.x * blockDim.x) {
+    const int r = e / nd, d = e % nd;
+    partials[(int64_t)(d0 + d) * kPartialPitch + r] = recv[e];
+  }
+}
+}  // namespace
+
+int Ctx::reduce_point(double* partials, int G, int d0, int nd) {
+  if (!comm || comm->world == 1 || nd <= 0) return G;
+  const int W = comm->world;
+  constexpr int kRing = 16;
+  double* buf = (double*)workspace("reduce_ring", (size_t)kRing * 2 * 4096 * sizeof(double));
+  require(nd <= 4096 && (size_t)W * nd <= 4096 * 2 - 4096, "reduce_point: too many dots for one exchange");
+  double* send = buf + (size_t)(reduce_ring % kRing) * 2 * 4096;
+  double* recv = send + 4096;
+  ++reduce_ring;
+  ++launches;
+  k_local_reduce<<<std::min(nd, 64), 32, 0, stream>>>(partials, G, d0, nd, send);
+  CK(cudaGetLastError());
+  comm->allgather(send, recv, (size_t)nd, stream);
+  ++launches;
+  k_scatter_ranks<<<std::max(1, std::min(64, (W * nd + 255) / 256)), 256, 0, stream>>>(recv, W, nd, partials, d0);
+  CK(cudaGetLastError());
+  return W;
+}
+
+void Ctx::halo_exchange(const DevOp& op, const double* v, int J) {
+  if (!comm || comm->world == 1 || J <= 0 || op.halo_rows == 0) return;
+  require(J <= op.halo_rows, "halo exchange deeper than the operator's halo");
+  const int64_t L = op.dim == 2 ? op.nx : op.nx * op.ny;
+  const int64_t nrows = op.n / L;
+  require(nrows >= J, "slab thinner than the halo width");
+  double* hlo = const_cast<double*>(op.hlo);
+  double* hhi = const_cast<double*>(op.hhi);
+  ++launches;
+  comm->halo(v, hlo + (op.halo_rows - J) * L, (size_t)(J * L), v + (nrows - J) * L, hhi, (size_t)(J * L), stream);
+}
+
 // ---------------------------------------------------------------- operators
 static void* dev_upload(Op& op, const void* host, size_t bytes) {
   void* p = nullptr;
   CK(cudaMalloc(&p, std::max<size_t>(bytes, 16)));
   op.owned.push_back(p);
-  if (bytes) CK(cudaMemcpy(p, host, bytes, cudaMemcpyHostToDevice));
+  if (bytes && host) CK(cudaMemcpy(p, host, bytes, cudaMemcpyHostToDevice));
   return p;
 }
 
@@ -154,13 +207,43 @@ void build_stencil_op(Ctx& c, Op& op, const skc_stencil_desc& d, const double* k
   o.nx = (int64_t)d.nx;
   o.ny = (int64_t)d.ny;
   o.nz = d.dim == 3 ? (int64_t)d.nz : 1;
-  o.n = o.nx * o.ny * o.nz;
   for (int t = 0; t < 7; ++t) o.coef[t] = d.coef[t];
   o.ch2 = d.ch2;
+  // row slab of the slowest dimension owned by this rank (the whole grid on one GPU)
+  const int64_t R = d.dim == 2 ? o.ny : o.nz;
+  op.rowlen = d.dim == 2 ? o.nx : o.nx * o.ny;
+  int64_t lo = 0, hi = R;
+  slab_range(R, c.world(), c.rank(), lo, hi);
+  const int64_t H = c.world() > 1 ? kMaxS : 0;
+  require(hi - lo >= std::max<int64_t>(H, 1), "stencil slab: fewer rows per rank than the halo width (8)");
+  if (d.dim == 2)
+    o.ny = hi - lo;
+  else
+    o.nz = hi - lo;
+  o.n = o.nx * o.ny * o.nz;
+  o.row0 = lo;
+  o.rows_global = R;
+  o.halo_rows = H;
+  if (H > 0) {
+    op.hlo = (double*)dev_upload(op, nullptr, sizeof(double) * (size_t)(H * op.rowlen));
+    op.hhi = (double*)dev_upload(op, nullptr, sizeof(double) * (size_t)(H * op.rowlen));
+    CK(cudaMemset(op.hlo, 0, sizeof(double) * (size_t)(H * op.rowlen)));
+    CK(cudaMemset(op.hhi, 0, sizeof(double) * (size_t)(H * op.rowlen)));
+    o.hlo = op.hlo;
+    o.hhi = op.hhi;
+  }
   if (d.kind == 1) {
     require(kcell_host != nullptr, "stencil: variable-k operator needs the kcell array");
     o.kind = kStencilVarK;
-    o.kcell = (const double*)dev_upload(op, kcell_host, sizeof(double) * (size_t)o.n);
+    // k for the owned rows plus H+1 rows each side (clamped to the grid; 1.0 past the edge)
+    const int64_t pad = H > 0 ? H + 1 : 0;
+    std::vector<double> kp((size_t)((hi - lo + 2 * pad) * op.rowlen), 1.0);
+    for (int64_t rr = lo - pad; rr < hi + pad; ++rr)
+      if (rr >= 0 && rr < R)
+        std::memcpy(kp.data() + (rr - lo + pad) * op.rowlen, kcell_host + rr * op.rowlen,
+                    sizeof(double) * (size_t)op.rowlen);
+    const double* base = (const double*)dev_upload(op, kp.data(), sizeof(double) * kp.size());
+    o.kcell = base + pad * op.rowlen;
   } else {
     o.kind = kStencilConst;
   }
@@ -232,6 +315,7 @@ void build_csr_op(Ctx& c, Op& op, int64_t n, const uint64_t* offs, const uint64_
     }
   }
   require(n <= 0x7fffffff, "csr: n exceeds the int32 column-index range");
+  require(c.world() == 1, "csr operators are single-GPU; use skc_op_create_stencil_slab across ranks");
   op.device = c.device;
   DevOp& o = op.d;
   std::memset(&o, 0, sizeof o);
@@ -255,6 +339,8 @@ void build_csr_op(Ctx& c, Op& op, int64_t n, const uint64_t* offs, const uint64_
       }
     o.dia = (const double*)dev_upload(op, dia.data(), sizeof(double) * dia.size());
     op.rows = ny * nz;
+    o.rows_global = dim == 2 ? ny : nz;
+    op.rowlen = dim == 2 ? nx : nx * ny;
   } else {
     o.kind = kCsr;
     o.dim = 0;

@@ -94,6 +94,11 @@ __global__ void __launch_bounds__(256) k_apply_csr(const __grid_constant__ DevOp
 }
 
 void launch_apply(Ctx& c, const DevOp& op, const double* x, double* y, const int* halt, const int* cond) {
+  if (op.kind != kCsr) {  // stencils: depth-1 matrix-powers sweep (handles slab halos)
+    double* outs[2] = {nullptr, y};
+    launch_mpk(c, op, x, nullptr, outs, 1, 0, nullptr, 1, nullptr, 0, halt, cond);
+    return;
+  }
   const double bytes = 16.0 * op.n + (op.kind == kStencilVarK ? 8.0 * op.n : 0.0) +
                        (op.kind == kStencilDia ? 8.0 * (op.dim == 2 ? 5 : 7) * op.n : 0.0);
   Launch L(c, "apply", bytes);

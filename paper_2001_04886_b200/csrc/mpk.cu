@@ -104,29 +104,32 @@ __global__ void __launch_bounds__(288) k_mpk2d(const __grid_constant__ MpkDesc d
   double acc[NACC];
 #pragma unroll
   for (int q = 0; q < NACC; ++q) acc[q] = 0.0;
-  const double* csrc = d.src + c;
+  // slab geometry: local row t is global row row0 + t; rows just outside the slab come from
+  // the halo buffers (filled by the exchange), rows outside the grid are Dirichlet zeros
+  const int64_t row0 = d.op.row0, rows_g = d.op.rows_global;
+  const int H = (int)d.op.halo_rows;
+  auto fetch = [&](int t) -> double {
+    const int64_t tg = row0 + t;
+    if (!colin || tg < 0 || tg >= rows_g || t < y0 - J || t >= y1 + J) return 0.0;
+    const double* rowp = t < 0 ? d.op.hlo + (int64_t)(t + H) * nx
+                               : (t >= ny ? d.op.hhi + (int64_t)(t - ny) * nx : d.src + (int64_t)t * nx);
+    return rowp[c];
+  };
 
   // level-0 rows are prefetched PF steps ahead so each thread keeps PF loads in flight
   constexpr int PF = 8;
-  const int tend = min(ny, y1 + J);
   double pf[PF];
 #pragma unroll
-  for (int k = 0; k < PF; ++k) {
-    const int tr = y0 - J + k;
-    pf[k] = (colin && tr >= 0 && tr < tend) ? csrc[(int64_t)tr * nx] : 0.0;
-  }
+  for (int k = 0; k < PF; ++k) pf[k] = fetch(y0 - J + k);
   for (int t = y0 - J; t < y1 + J; ++t) {
     const int par = t & 1;
     // level 0: row t
     const double s0 = pf[0];
 #pragma unroll
     for (int k = 0; k + 1 < PF; ++k) pf[k] = pf[k + 1];
-    {
-      const int tr = t + PF;
-      pf[PF - 1] = (colin && tr >= 0 && tr < tend) ? csrc[(int64_t)tr * nx] : 0.0;
-    }
+    pf[PF - 1] = fetch(t + PF);
     double v0 = 0.0;
-    if (colin && t >= 0 && t < ny) v0 = d.scale ? __dmul_rn(s0, scale) : s0;
+    if (colin && row0 + t >= 0 && row0 + t < rows_g) v0 = d.scale ? __dmul_rn(s0, scale) : s0;
     win[0][0] = win[0][1];
     win[0][1] = win[0][2];
     win[0][2] = v0;
@@ -136,16 +139,18 @@ __global__ void __launch_bounds__(288) k_mpk2d(const __grid_constant__ MpkDesc d
 #pragma unroll
     for (int j = 1; j <= J; ++j) {
       const int r = t - j;
+      const int64_t rg = row0 + r;
       double v = 0.0;
-      if (colin && r >= 0 && r < ny) {
+      // level j is needed (and its inputs valid) only within J-j rows of the CTA's rows
+      if (colin && rg >= 0 && rg < rows_g && r >= y0 - (J - j) && r < y1 + (J - j)) {
         // x-neighbours of level j-1 at row r: its line written one step ago
         const double* ln = line[j - 1][par ^ 1];
         // (tile-edge threads see a zero instead of the neighbour: they are ghost columns whose
         // values never reach an output)
         const double xw = (hasW && tid > 0) ? ln[tid - 1] : 0.0;
         const double xe = (hasE && tid + 1 < 288) ? ln[tid + 1] : 0.0;
-        const double ys = r > 0 ? win[j - 1][0] : 0.0;
-        const double yn = r + 1 < ny ? win[j - 1][2] : 0.0;
+        const double ys = rg > 0 ? win[j - 1][0] : 0.0;
+        const double yn = rg + 1 < rows_g ? win[j - 1][2] : 0.0;
         double cS, cW, cC, cE, cN;
         if (KIND == kStencilConst) {
           cS = d.op.coef[1], cW = d.op.coef[2], cC = d.op.coef[3], cE = d.op.coef[4], cN = d.op.coef[5];
@@ -154,11 +159,11 @@ __global__ void __launch_bounds__(288) k_mpk2d(const __grid_constant__ MpkDesc d
           int64_t nb[7];
           const int64_t p = (int64_t)r * nx + c;
           pres[0] = pres[6] = false;
-          pres[1] = r > 0;
+          pres[1] = rg > 0;
           pres[2] = hasW;
           pres[3] = true;
           pres[4] = hasE;
-          pres[5] = r + 1 < ny;
+          pres[5] = rg + 1 < rows_g;
           nb[0] = nb[6] = nb[3] = p;
           nb[1] = p - nx;
           nb[2] = p - 1;
@@ -235,25 +240,29 @@ __global__ void __launch_bounds__(TXE* TYE) k_mpk3d(const __grid_constant__ MpkD
 #pragma unroll
   for (int q = 0; q < NACC; ++q) acc[q] = 0.0;
 
+  // z-slab geometry (see the 2D kernel): plane t is global plane row0 + t
+  const int64_t row0 = d.op.row0, rows_g = d.op.rows_global;
+  const int64_t H = d.op.halo_rows;
+  const int64_t xy = y * nx + x;
+  auto fetch = [&](int64_t t) -> double {
+    const int64_t tg = row0 + t;
+    if (!in || tg < 0 || tg >= rows_g || t < z0 - J || t >= z1 + J) return 0.0;
+    const double* pp =
+        t < 0 ? d.op.hlo + (t + H) * pl : (t >= nz ? d.op.hhi + (t - nz) * pl : d.src + t * pl);
+    return pp[xy];
+  };
   constexpr int PF = 4;
-  const int64_t tend = min(nz, z1 + J);
   double pf[PF];
 #pragma unroll
-  for (int k = 0; k < PF; ++k) {
-    const int64_t tr = z0 - J + k;
-    pf[k] = (in && tr >= 0 && tr < tend) ? d.src[tr * pl + y * nx + x] : 0.0;
-  }
+  for (int k = 0; k < PF; ++k) pf[k] = fetch(z0 - J + k);
   for (int64_t t = z0 - J; t < z1 + J; ++t) {
     const int par = (int)(t & 1);
     const double s0 = pf[0];
 #pragma unroll
     for (int k = 0; k + 1 < PF; ++k) pf[k] = pf[k + 1];
-    {
-      const int64_t tr = t + PF;
-      pf[PF - 1] = (in && tr >= 0 && tr < tend) ? d.src[tr * pl + y * nx + x] : 0.0;
-    }
+    pf[PF - 1] = fetch(t + PF);
     double v0 = 0.0;
-    if (in && t >= 0 && t < nz) v0 = d.scale ? __dmul_rn(s0, scale) : s0;
+    if (in && row0 + t >= 0 && row0 + t < rows_g) v0 = d.scale ? __dmul_rn(s0, scale) : s0;
     win[0][0] = win[0][1];
     win[0][1] = win[0][2];
     win[0][2] = v0;
@@ -262,8 +271,9 @@ __global__ void __launch_bounds__(TXE* TYE) k_mpk3d(const __grid_constant__ MpkD
 #pragma unroll
     for (int j = 1; j <= J; ++j) {
       const int64_t r = t - j;  // plane computed by level j
+      const int64_t rg = row0 + r;
       double v = 0.0;
-      if (in && r >= 0 && r < nz) {
+      if (in && rg >= 0 && rg < rows_g && r >= z0 - (J - j) && r < z1 + (J - j)) {
         const auto& P = plane[j - 1][par ^ 1];
         const double ys = ly > 0 ? P[ly - 1][lx] : 0.0;
         const double xw = lx > 0 ? P[ly][lx - 1] : 0.0;
@@ -272,13 +282,13 @@ __global__ void __launch_bounds__(TXE* TYE) k_mpk3d(const __grid_constant__ MpkD
         bool pres[7];
         int64_t nb[7];
         const int64_t p = r * pl + y * nx + x;
-        pres[0] = r > 0;
+        pres[0] = rg > 0;
         pres[1] = y > 0;
         pres[2] = x > 0;
         pres[3] = true;
         pres[4] = x + 1 < nx;
         pres[5] = y + 1 < ny;
-        pres[6] = r + 1 < nz;
+        pres[6] = rg + 1 < rows_g;
         nb[0] = p - pl;
         nb[1] = p - nx;
         nb[2] = p - 1;
@@ -418,6 +428,8 @@ int launch_mpk(Ctx& c, const DevOp& op, const double* src, const double* scale, 
   d.dot0 = dot0;
   d.halt = halt;
   d.cond = cond;
+  // ghost rows of the source from the neighbouring slabs (no-op on one GPU)
+  c.halo_exchange(op, src, J);
   int nout = 0;
   for (int j = 0; j <= J; ++j) nout += out[j] != nullptr;
   const double bytes = 8.0 * (double)op.n * (1 + nout + nxd) + (op.kind == kStencilVarK ? 8.0 * op.n : 0.0) +

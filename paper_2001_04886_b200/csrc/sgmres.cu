@@ -325,7 +325,7 @@ void gmres_device(Ctx& c, const Op& op, const double* f, double* x, uint64_t m64
     }
     lb.add_dot(0, 0);
     lb.launch(c, g, coef, ncoef, partials, 0, nullptr, nullptr, "residual");
-    k_gm_rn<<<1, 256, 0, c.stream>>>(st, partials, g.G, 0);
+    k_gm_rn<<<1, 256, 0, c.stream>>>(st, partials, c.reduce_point(partials, g.G, 0, 1), 0);
     ++c.launches;
     GmState h;
     CK(cudaMemcpyAsync(&h, st, sizeof h, cudaMemcpyDeviceToHost, c.stream));
@@ -354,7 +354,7 @@ void gmres_device(Ctx& c, const Op& op, const double* f, double* x, uint64_t m64
       launch_apply(c, op.d, q(j - 1), w, halt, nullptr);
       launch_gram_list(c, g, {q(0)}, {w}, partials, 0, halt, nullptr, "gram");
       for (int i = 0; i < j; ++i) {
-        k_gm_col<<<1, 256, 0, c.stream>>>(st, col, i, coef, cC, partials, g.G, 0);
+        k_gm_col<<<1, 256, 0, c.stream>>>(st, col, i, coef, cC, partials, c.reduce_point(partials, g.G, 0, 1), 0);
         ++c.launches;
         LinBuilder lb;  // w -= col_i q_i ; next dot
         lb.add_out(w, w);
@@ -367,7 +367,7 @@ void gmres_device(Ctx& c, const Op& op, const double* f, double* x, uint64_t m64
         }
         lb.launch(c, g, coef, ncoef, partials, 0, halt, nullptr, "mgs_update");
       }
-      k_gm_sub<<<1, 256, 0, c.stream>>>(st, j, col, coef, cInv, partials, g.G, 0);
+      k_gm_sub<<<1, 256, 0, c.stream>>>(st, j, col, coef, cInv, partials, c.reduce_point(partials, g.G, 0, 1), 0);
       ++c.launches;
       LinBuilder lb;
       lb.add_out(q(j), w, cInv);
@@ -530,11 +530,13 @@ struct Engine {
   void ctor(const double* v, bool use_rn) {
     CK(cudaMemsetAsync(rec, 0, (size_t)(m + 1) * rl.size() * sizeof(double), c.stream));
     if (!use_rn) launch_gram_list(c, g, {v}, {v}, partials, dl.RR(), nullptr, nullptr, "gram");
-    k_arn_ctor<<<1, 256, 0, c.stream>>>(st, use_rn ? 1 : 0, partials, g.G, dl.RR(), recp(0), coef, cl.Inv());
+    const int Gc = use_rn ? g.G : c.reduce_point(partials, g.G, dl.RR(), 1);
+    k_arn_ctor<<<1, 256, 0, c.stream>>>(st, use_rn ? 1 : 0, partials, Gc, dl.RR(), recp(0), coef, cl.Inv());
     ++c.launches;
     krylov_into(0, v);
     gram_self_into(0, dl.Wa(), nullptr);
-    k_arn_push<<<1, 256, 0, c.stream>>>(st, grams, 0, recp(0), partials, g.G, dl.Wa(), dl.Wb(), s);
+    k_arn_push<<<1, 256, 0, c.stream>>>(st, grams, 0, recp(0), partials,
+                                        c.reduce_point(partials, g.G, dl.Wa(), s * s), dl.Wa(), dl.Wb(), s);
     ++c.launches;
     CK(cudaGetLastError());
   }
@@ -551,7 +553,8 @@ struct Engine {
       L.push_back(z);
       launch_gram_list(c, g, L, {z}, partials, dl.Z(), halt, nullptr, "gram_z");
     }
-    k_arn_s1<<<1, 256, 0, c.stream>>>(st, grams, k, rk, coef, partials, g.G, dl.Z(), s, cl.H(), scratch);
+    k_arn_s1<<<1, 256, 0, c.stream>>>(st, grams, k, rk, coef, partials, c.reduce_point(partials, g.G, dl.Z(), k * s + 1),
+                                      dl.Z(), s, cl.H(), scratch);
     ++c.launches;
     // seed = z - sum_i V_i h_i ; ||seed||^2
     {
@@ -562,7 +565,8 @@ struct Engine {
       lb.add_dot(0, 0);
       lb.launch(c, g, coef, cl.size(), partials, dl.Seed(), halt, nullptr, "seed_update");
     }
-    k_arn_s2<<<1, 256, 0, c.stream>>>(st, k, rk, coef, partials, g.G, dl.Seed(), cl.Inv());
+    k_arn_s2<<<1, 256, 0, c.stream>>>(st, k, rk, coef, partials, c.reduce_point(partials, g.G, dl.Seed(), 1),
+                                      dl.Seed(), cl.Inv());
     ++c.launches;
     // candidate block [v, .., A^{s-1} v] of the normalized seed (also on the last block)
     const int cb = k;  // block slot k (slot m is scratch when k == m)
@@ -585,7 +589,8 @@ struct Engine {
         }
         for (int i = 0; i < k; ++i) {
           const int Gi = (i == 0 && have) ? Gfused : g.G;
-          k_arn_t<<<1, 256, 0, c.stream>>>(st, grams, i, tk, coef, partials, Gi, dl.D(), s, cl.T(), pass);
+          k_arn_t<<<1, 256, 0, c.stream>>>(st, grams, i, tk, coef, partials,
+                                           c.reduce_point(partials, Gi, dl.D(), s * (s - 1)), dl.D(), s, cl.T(), pass);
           ++c.launches;
           // cand[:,jc] -= sum_l t(l,jc-1) V_i[:,l]  (+ products with V_{i+1})
           const double* Vi[kMaxS];
@@ -607,7 +612,9 @@ struct Engine {
           for (int jc = 0; jc < s; ++jc) Cc.push_back(col(cb, jc));
           for (int jc = 0; jc < s; ++jc) L.push_back(col(cb, jc));
           launch_gram_list(c, g, L, Cc, partials, dl.Cross(), halt, nullptr, "gram_cross");
-          k_arn_check<<<1, 256, 0, c.stream>>>(st, grams, k, rk, partials, g.G, dl.Cross(), dl.Cross() + k * s * s,
+          k_arn_check<<<1, 256, 0, c.stream>>>(st, grams, k, rk, partials,
+                                               c.reduce_point(partials, g.G, dl.Cross(), k * s * s + s * s), dl.Cross(),
+                                               dl.Cross() + k * s * s,
                                                s, 1e-8, scratch);
           ++c.launches;
         } else {
@@ -617,7 +624,11 @@ struct Engine {
     }
     const int dWa = s > 1 ? dl.Cross() + k * s * s : dl.Wa();
     if (s == 1) gram_self_into(cb, dl.Wa(), nullptr);
-    k_arn_push<<<1, 256, 0, c.stream>>>(st, grams, cb, rk, partials, g.G, dWa, dl.Wb(), s);
+    // the push reads W from the reorthogonalized region when the device flag says so: make
+    // both regions global (the unused one is stale but harmless)
+    // (for s > 1 the dWa region was already made global together with the cross products)
+    const int Gw = s > 1 ? c.reduce_point(partials, g.G, dl.Wb(), s * s) : c.reduce_point(partials, g.G, dWa, s * s);
+    k_arn_push<<<1, 256, 0, c.stream>>>(st, grams, cb, rk, partials, Gw, dWa, dl.Wb(), s);
     ++c.launches;
     CK(cudaGetLastError());
   }
@@ -725,7 +736,8 @@ void sgmres_device(Ctx& c, const Op& op, const double* f, double* x, const SStep
     }
     lb.add_dot(0, 0);
     lb.launch(c, E.g, E.coef, E.cl.size(), E.partials, E.dl.RR(), nullptr, nullptr, "residual");
-    k_arn_rn<<<1, 256, 0, c.stream>>>(E.st, E.partials, E.g.G, E.dl.RR(), E.rn_out);
+    k_arn_rn<<<1, 256, 0, c.stream>>>(E.st, E.partials, c.reduce_point(E.partials, E.g.G, E.dl.RR(), 1), E.dl.RR(),
+                                      E.rn_out);
     ++c.launches;
     double h;
     CK(cudaMemcpyAsync(&h, E.rn_out, sizeof h, cudaMemcpyDeviceToHost, c.stream));

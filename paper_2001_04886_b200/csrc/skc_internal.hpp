@@ -42,6 +42,14 @@ struct DevOp {
   const int64_t* rowptr; // kCsr
   const int32_t* colidx;
   const double* vals;
+  // row-slab decomposition of the slowest dimension (y in 2D, z in 3D): this rank owns
+  // global rows [row0, row0 + local rows); halo_rows ghost rows on each side are received
+  // into the operator's halo buffers before a sweep (0 on a single GPU).
+  int64_t row0;
+  int64_t rows_global;
+  int64_t halo_rows;
+  const double* hlo;  // halo rows -halo_rows..-1 of the sweep source (valid after an exchange)
+  const double* hhi;  // halo rows nrows..nrows+halo_rows-1
 };
 
 struct Op {
@@ -50,6 +58,9 @@ struct Op {
   int64_t rows = 1;      // grid rows (2D: ny, 3D: ny*nz) for reporting
   std::vector<void*> owned;  // device allocations
   int device = 0;
+  double* hlo = nullptr;  // halo_rows rows below the slab (rows -halo_rows..-1)
+  double* hhi = nullptr;  // halo_rows rows above the slab
+  int64_t rowlen = 0;     // points per slowest-dimension row (2D: nx, 3D: nx*ny)
   ~Op();
 };
 
@@ -104,6 +115,22 @@ struct GramDesc {
   const int* cond;
 };
 
+// ---------------------------------------------------------------- multi-GPU exchanges (comm.cu)
+struct Comm {
+  int rank = 0, world = 1;
+  virtual ~Comm() = default;
+  // every rank sends n doubles, receives world*n (rank-major); stream-ordered
+  virtual void allgather(const double* send, double* recv, size_t n, cudaStream_t s) = 0;
+  // lo_* with rank-1, hi_* with rank+1 (skipped at the ends)
+  virtual void halo(const double* lo_send, double* lo_recv, size_t n_lo, const double* hi_send, double* hi_recv,
+                    size_t n_hi, cudaStream_t s) = 0;
+  virtual const char* name() const = 0;
+};
+void nccl_unique_id(void* out128);
+std::unique_ptr<Comm> make_nccl_comm(int rank, int world, const void* id);
+std::unique_ptr<Comm> make_callback_comm(int rank, int world, skc_allgather_fn ag, skc_halo_fn hl, void* user);
+void slab_range(int64_t rows, int world, int rank, int64_t& lo, int64_t& hi);
+
 // ---------------------------------------------------------------- context
 struct KStat {
   uint64_t launches = 0;
@@ -130,6 +157,17 @@ struct Ctx {
   std::map<std::string, std::pair<void*, size_t>> ws;
   double* pinned = nullptr;
   size_t pinned_cap = 0;
+  std::unique_ptr<Comm> comm;  // null on a single GPU
+  int reduce_ring = 0;
+
+  int world() const { return comm ? comm->world : 1; }
+  int rank() const { return comm ? comm->rank : 0; }
+  // Make the dots [d0, d0+nd) of a partial buffer (written by G CTAs) global: on one GPU a
+  // no-op returning G; across ranks the per-rank sums are allgathered and scattered back
+  // into the first `world` partial columns, so the scalar kernels read them unchanged.
+  int reduce_point(double* partials, int G, int d0, int nd);
+  // fill op.hlo / op.hhi with the J rows of v owned by the neighbouring ranks
+  void halo_exchange(const DevOp& op, const double* v, int J);
 
   void* workspace(const std::string& tag, size_t bytes);
   double* host_stage(size_t doubles);

@@ -196,16 +196,23 @@ __global__ void k_any_nonzero(const double* x, int64_t n, int* flag) {
 
 }  // namespace
 
+__global__ void k_flag_to_partial(const int* flag, double* partials) { partials[0] = *flag ? 1.0 : 0.0; }
+
 bool device_is_zero(Ctx& c, const double* x, int64_t n) {
   int* flag = (int*)c.workspace("is_zero_flag", sizeof(int));
   CK(cudaMemsetAsync(flag, 0, sizeof(int), c.stream));
   ++c.launches;
   k_any_nonzero<<<std::min<int64_t>(1184, (n + 255) / 256), 256, 0, c.stream>>>(x, n, flag);
   CK(cudaGetLastError());
-  int h = 0;
-  CK(cudaMemcpyAsync(&h, flag, sizeof(int), cudaMemcpyDeviceToHost, c.stream));
+  double* p = (double*)c.workspace("is_zero_partial", sizeof(double) * kPartialPitch);
+  k_flag_to_partial<<<1, 1, 0, c.stream>>>(flag, p);
+  const int G = c.reduce_point(p, 1, 0, 1);  // across ranks: every rank sees every flag
+  std::vector<double> h(G);
+  CK(cudaMemcpyAsync(h.data(), p, sizeof(double) * G, cudaMemcpyDeviceToHost, c.stream));
   CK(cudaStreamSynchronize(c.stream));
-  return h == 0;
+  for (double v : h)
+    if (v != 0.0) return false;
+  return true;
 }
 
 // K[j] = A^{j+1} src for j < J (krylov_pair's A R block, sstep.hpp:71-81): one matrix-powers
@@ -297,7 +304,7 @@ void somin_device(Ctx& c, const Op& op, const double* f, double* x, const SStepC
   // ---- initial residual (solvers.hpp:58-76) and setup (sstep.hpp:164-178)
   const bool x_zero = device_is_zero(c, x, n);
   initial_residual_dev(c, op, g, f, x, r, ax, x_zero, coef, ncoef, cMinus1(s), partials, dRR);
-  k_somin_start<<<1, 256, 0, c.stream>>>(st, partials, g.G, dRR);
+  k_somin_start<<<1, 256, 0, c.stream>>>(st, partials, c.reduce_point(partials, g.G, dRR, 1), dRR);
   ++c.launches;
   CK(cudaGetLastError());
   // krylov_pair(r): P0 = [r, Ar, .., A^{s-1} r], AP0 = [Ar, .., A^s r]
@@ -311,7 +318,8 @@ void somin_device(Ctx& c, const Op& op, const double* f, double* x, const SStepC
     for (int j = 0; j < s; ++j) L.push_back(slot_ap(0, j));
     launch_gram_list(c, g, L, L, partials, dW, halt, nullptr, "gram_w");
     launch_gram_list(c, g, L, {r}, partials, dM, halt, nullptr, "gram_m");
-    k_somin_setup<<<1, 256, 0, c.stream>>>(st, grams, coef, partials, g.G, dW, dM, s);
+    k_somin_setup<<<1, 256, 0, c.stream>>>(st, grams, coef, partials, c.reduce_point(partials, g.G, dW, s * s + s),
+                                           dW, dM, s);
     ++c.launches;
     CK(cudaGetLastError());
   }
@@ -340,7 +348,7 @@ void somin_device(Ctx& c, const Op& op, const double* f, double* x, const SStepC
         lb.add_dot(1, 1);
         lb.launch(c, g, coef, ncoef, partials, dRR, halt, nullptr, "xr_update");
       }
-      k_somin_norm<<<1, 256, 0, c.stream>>>(st, partials, g.G, dRR, hist);
+      k_somin_norm<<<1, 256, 0, c.stream>>>(st, partials, c.reduce_point(partials, g.G, dRR, 1), dRR, hist);
       ++c.launches;
       // krylov_pair(r) -> K[j] = A^{j+1} r  (matrix-powers sweep)
       powers(c, op, r, K, np, s, halt);
@@ -355,7 +363,8 @@ void somin_device(Ctx& c, const Op& op, const double* f, double* x, const SStepC
         for (int j = 0; j < s; ++j) R.push_back(K + (size_t)j * np);
         launch_gram_list(c, g, L, R, partials, dC, halt, nullptr, "gram_c");
       }
-      k_somin_proj<<<1, 256, 0, c.stream>>>(st, grams, ws, coef, partials, g.G, dC, s, scratch);
+      k_somin_proj<<<1, 256, 0, c.stream>>>(st, grams, ws, coef, partials,
+                                            c.reduce_point(partials, g.G, dC, ws.n * s * s), dC, s, scratch);
       ++c.launches;
       // new slot: P = R + sum_e P_e b_e ; AP = AR + sum_e AP_e b_e ; W ; m  (sstep.hpp:215-222)
       if (free_slots.empty()) {  // s-GCR window at the device limit
@@ -386,7 +395,9 @@ void somin_device(Ctx& c, const Op& op, const double* f, double* x, const SStepC
         for (int j = 0; j < s; ++j) R.push_back(slot_ap(nsl, j));
         launch_gram_list(c, g, L, R, partials, dX, halt, nullptr, "gram_debug");
       }
-      k_somin_push<<<1, 256, 0, c.stream>>>(st, grams, nsl, coef, partials, g.G, dW, dW + s * (s + 1) / 2, s,
+      int Gp = c.reduce_point(partials, g.G, dW, s * (s + 1) / 2 + s);
+      if (cfg.debug_checks) Gp = c.reduce_point(partials, g.G, dX, ws.n * s * s);
+      k_somin_push<<<1, 256, 0, c.stream>>>(st, grams, nsl, coef, partials, Gp, dW, dW + s * (s + 1) / 2, s,
                                             cfg.debug_checks ? 1 : 0, ws, dX, scratch);
       ++c.launches;
       CK(cudaGetLastError());
@@ -538,7 +549,8 @@ static void smr_step_enqueue(Ctx& c, const Op& op, const Geo& g, double* x, doub
   for (int j = 0; j < s; ++j) AR.push_back(K + (size_t)j * np);
   launch_gram_list(c, g, AR, AR, partials, 1, halt, nullptr, "gram_w");
   launch_gram_list(c, g, AR, {r}, partials, 1 + s * s, halt, nullptr, "gram_m");
-  k_smr_solve<<<1, 256, 0, c.stream>>>(st, coef, partials, g.G, 1, 1 + s * s, s);
+  k_smr_solve<<<1, 256, 0, c.stream>>>(st, coef, partials, c.reduce_point(partials, g.G, 1, s * s + s), 1,
+                                        1 + s * s, s);
   ++c.launches;
   // x += R a (R = [r, A r, .., A^{s-1} r]); r -= AR a  (sstep.hpp:102-103)
   LinBuilder lb;
@@ -549,7 +561,7 @@ static void smr_step_enqueue(Ctx& c, const Op& op, const Geo& g, double* x, doub
   for (int l = 0; l < s; ++l) lb.add_term(K + (size_t)l * np, 2u, s + l - 1);
   lb.add_dot(1, 1);
   lb.launch(c, g, coef, ncoef, partials, 0, halt, nullptr, "xr_update");
-  k_smr_norm<<<1, 256, 0, c.stream>>>(st, partials, g.G, 0, hist);
+  k_smr_norm<<<1, 256, 0, c.stream>>>(st, partials, c.reduce_point(partials, g.G, 0, 1), 0, hist);
   ++c.launches;
   CK(cudaGetLastError());
 }
@@ -579,7 +591,7 @@ void smr_device(Ctx& c, const Op& op, const double* f, double* x, const SStepCfg
   }
   const bool x_zero = device_is_zero(c, x, n);
   initial_residual_dev(c, op, g, f, x, r, ax, x_zero, coef, ncoef, 2 * s, partials, 0);
-  k_smr_start<<<1, 256, 0, c.stream>>>(st, partials, g.G, 0, hist);
+  k_smr_start<<<1, 256, 0, c.stream>>>(st, partials, c.reduce_point(partials, g.G, 0, 1), 0, hist);
   ++c.launches;
   uint64_t enq = 0;
   const uint64_t batch = n <= (1 << 16) ? 32 : 8;
