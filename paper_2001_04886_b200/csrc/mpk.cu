@@ -7,11 +7,11 @@
 // rounded multiplies and adds; out-of-domain neighbours enter as exact zeros, which leaves
 // the sum's bits unchanged (adding +-0.0 to a sum that starts at +0.0).
 //
-// 2D: a CTA owns an output strip of W columns x R rows and streams it in y.  Each thread owns
-// one column of the strip extended by J on both sides; level j keeps its last three rows in
-// registers (the y-neighbours) and its newest row in a double-buffered shared-memory line
-// (the x-neighbours).  Level j at step t produces row t-j, so one __syncthreads per row step
-// advances all J levels.  3D works the same with an (x,y) tile streamed in z.
+// 2D: a warp owns an output strip of W columns x R rows and streams it in y (no block-level
+// synchronisation: x-neighbours by warp shuffles, y-neighbours in registers).  Level j at
+// step t produces row t-j.  3D: a CTA owns an (x,y) tile extended by J on each side and
+// streams it in z; each level's newest plane is shared through double-buffered shared memory
+// with one __syncthreads per plane step.
 //
 // Optionally the kernel fuses the products X_l . (A^j v) of the produced powers with up to
 // MPK_MAXX extra vectors (the first block-MGS round of s-step Arnoldi, sstep.hpp:341),
@@ -77,29 +77,89 @@ __device__ __forceinline__ void coefs(const DevOp& op, int64_t p, const bool (&p
   }
 }
 
+// Source rows are staged into shared-memory rings by per-thread cp.async copies (each thread
+// copies its own column(s); one commit group per row step), PF rows ahead of the row being
+// consumed.  The ring has PF+1 slots: a step refills the slot consumed one step earlier.  With
+// DOTS the X rows of the row the last level completes ride in the same groups.
+//
+// Stencil value at a point: S, W, C, E, N (2D) or -z,-y,-x,C,+x,+y,+z (3D) in ascending column
+// order with separately rounded multiplies and adds; absent neighbours are exact zeros.
+
 // ------------------------------------------------------------------ 2D
+// Warp strips: a warp owns W = 64 - 2J output columns (two adjacent columns per lane, J ghost
+// columns each side) of R rows and streams them in y with no block-level synchronisation:
+// level j keeps its last three rows per column in registers (the y-neighbours), and the
+// x-neighbours of a lane's column pair are the adjacent lanes' columns, read with warp
+// shuffles.  Lane-edge columns see a neighbour from the wrong end of the warp; they are ghost
+// columns, and level j is valid on columns [j, 64-j) of the strip, so the J levels leave the
+// W middle columns exact.  Source rows (and, with DOTS, the X rows of the row the last level
+// completes) arrive PF rows ahead through per-lane cp.async rings in shared memory.
+constexpr int MW_WARPS = 4;           // independent strips per CTA
+constexpr int MW_PF = 4, MW_NS = 5;   // prefetch distance, ring slots (PF + 1)
+
+template <int J, bool DOTS>
+constexpr size_t mpk2w_smem() {
+  return sizeof(double) * MW_WARPS * 64 * MW_NS * (1 + (DOTS ? (size_t)J + 1 : 0));
+}
+
+template <int KIND>
+__device__ __forceinline__ double point2d(const DevOp& op, int64_t r, int64_t rg, int64_t rows_g, int c, int nx,
+                                          double ys, double xw, double cc, double xe, double yn) {
+  double cS, cW, cC, cE, cN;
+  const bool hasS = rg > 0, hasN = rg + 1 < rows_g, hasW = c > 0, hasE = c + 1 < nx;
+  if (KIND == kStencilConst) {
+    cS = op.coef[1], cW = op.coef[2], cC = op.coef[3], cE = op.coef[4], cN = op.coef[5];
+  } else {
+    bool pres[7];
+    int64_t nb[7];
+    const int64_t p = r * nx + c;
+    pres[0] = pres[6] = false;
+    pres[1] = hasS;
+    pres[2] = hasW;
+    pres[3] = true;
+    pres[4] = hasE;
+    pres[5] = hasN;
+    nb[0] = nb[6] = nb[3] = p;
+    nb[1] = p - nx;
+    nb[2] = p - 1;
+    nb[4] = p + 1;
+    nb[5] = p + nx;
+    double val[7];
+    coefs<2, KIND>(op, p, pres, nb, val);
+    cS = val[1], cW = val[2], cC = val[3], cE = val[4], cN = val[5];
+  }
+  double a = 0.0;
+  a = __dadd_rn(a, __dmul_rn(cS, hasS ? ys : 0.0));
+  a = __dadd_rn(a, __dmul_rn(cW, hasW ? xw : 0.0));
+  a = __dadd_rn(a, __dmul_rn(cC, cc));
+  a = __dadd_rn(a, __dmul_rn(cE, hasE ? xe : 0.0));
+  a = __dadd_rn(a, __dmul_rn(cN, hasN ? yn : 0.0));
+  return a;
+}
+
 template <int KIND, int J, bool DOTS>
-__global__ void __launch_bounds__(288) k_mpk2d(const __grid_constant__ MpkDesc d) {
+__global__ void __launch_bounds__(MW_WARPS * 32) k_mpk2w(const __grid_constant__ MpkDesc d) {
+  static_assert(!DOTS || J <= 3, "fused products read level values from the 3-row windows");
   if (skip_launch(d.halt, d.cond)) return;
-  __shared__ double line[J][2][288];  // level j's newest row, double-buffered by step parity
-  const int tid = threadIdx.x;
+  constexpr int PF = MW_PF, NS = MW_NS, NX = J + 1;
+  constexpr unsigned FULL = 0xffffffffu;
+  extern __shared__ __align__(16) double dsm[];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  double* ring = dsm + (size_t)wid * NS * 64;                        // [NS][64] per warp
+  double* xring = dsm + (size_t)MW_WARPS * NS * 64 + (size_t)wid * NX * NS * 64;  // [NX][NS][64]
   const int nx = (int)d.op.nx, ny = (int)d.op.ny;
-  const int tx = blockIdx.x % d.tiles_x, ty = blockIdx.x / d.tiles_x;
-  const int x0 = tx * d.W, y0 = ty * d.R;
-  const int y1 = min(ny, y0 + d.R);
-  const int c = x0 - J + tid;  // this thread's column
-  const bool colin = c >= 0 && c < nx && tid < d.W + 2 * J;
-  const bool outcol = tid >= J && tid < J + d.W && c < nx;
-  const bool hasW = c > 0, hasE = c + 1 < nx;
+  const int task = blockIdx.x * MW_WARPS + wid;
+  const bool active = task < d.tiles_x * d.tiles_y;  // warp-uniform
+  const int tx = active ? task % d.tiles_x : 0, ty = active ? task / d.tiles_x : 0;
+  const int y0 = ty * d.R, y1 = min(ny, y0 + d.R);
+  const int ca = tx * d.W - J + 2 * lane, cb = ca + 1;  // this lane's columns
+  const bool inA = ca >= 0 && ca < nx, inB = cb >= 0 && cb < nx;
+  const bool outA = 2 * lane >= J && 2 * lane < J + d.W && inA;
+  const bool outB = 2 * lane + 1 >= J && 2 * lane + 1 < J + d.W && inB;
   const double scale = d.scale ? *d.scale : 1.0;
-  double* outs[J + 1];
+  double wa[J + 1][3], wb[J + 1][3];  // per level: rows (r-1, r, r+1), columns a and b
 #pragma unroll
-  for (int j = 0; j <= J; ++j) outs[j] = d.out[j];
-  double win[J + 1][3];  // per level: rows (r-1, r, r+1) around the row the next level computes
-#pragma unroll
-  for (int j = 0; j <= J; ++j) win[j][0] = win[j][1] = win[j][2] = 0.0;
-  // fused products: the J+1 extra vectors X_l against every produced level 1..J
-  constexpr int NX = J + 1;
+  for (int j = 0; j <= J; ++j) wa[j][0] = wa[j][1] = wa[j][2] = wb[j][0] = wb[j][1] = wb[j][2] = 0.0;
   constexpr int NACC = DOTS ? NX * J : 1;
   double acc[NACC];
 #pragma unroll
@@ -108,120 +168,128 @@ __global__ void __launch_bounds__(288) k_mpk2d(const __grid_constant__ MpkDesc d
   // the halo buffers (filled by the exchange), rows outside the grid are Dirichlet zeros
   const int64_t row0 = d.op.row0, rows_g = d.op.rows_global;
   const int H = (int)d.op.halo_rows;
-  auto fetch = [&](int t) -> double {
+  const int tb = y0 - J, te = y1 + J;
+  auto issue = [&](int t) {
+    const int slot = (t - tb) % NS;
     const int64_t tg = row0 + t;
-    if (!colin || tg < 0 || tg >= rows_g || t < y0 - J || t >= y1 + J) return 0.0;
-    const double* rowp = t < 0 ? d.op.hlo + (int64_t)(t + H) * nx
-                               : (t >= ny ? d.op.hhi + (int64_t)(t - ny) * nx : d.src + (int64_t)t * nx);
-    return rowp[c];
-  };
-
-  // level-0 rows are prefetched PF steps ahead so each thread keeps PF loads in flight
-  constexpr int PF = 8;
-  double pf[PF];
+    const bool rowok = active && tg >= 0 && tg < rows_g && t < te;
+    const double* rowp = d.src;
+    if (rowok)
+      rowp = t < 0 ? d.op.hlo + (int64_t)(t + H) * nx
+                   : (t >= ny ? d.op.hhi + (int64_t)(t - ny) * nx : d.src + (int64_t)t * nx);
+    double* rs = ring + slot * 64 + 2 * lane;
+    cp_async8(rs, rowok && inA ? rowp + ca : d.src, rowok && inA);
+    cp_async8(rs + 1, rowok && inB ? rowp + cb : d.src, rowok && inB);
+    if (DOTS) {
+      const int r = t - J;
+      const bool rok = active && r >= y0 && r < y1;
 #pragma unroll
-  for (int k = 0; k < PF; ++k) pf[k] = fetch(y0 - J + k);
-  for (int t = y0 - J; t < y1 + J; ++t) {
-    const int par = t & 1;
-    // level 0: row t
-    const double s0 = pf[0];
-#pragma unroll
-    for (int k = 0; k + 1 < PF; ++k) pf[k] = pf[k + 1];
-    pf[PF - 1] = fetch(t + PF);
-    double v0 = 0.0;
-    if (colin && row0 + t >= 0 && row0 + t < rows_g) v0 = d.scale ? __dmul_rn(s0, scale) : s0;
-    win[0][0] = win[0][1];
-    win[0][1] = win[0][2];
-    win[0][2] = v0;
-    line[0][par][tid] = v0;
-    if (outs[0] && outcol && t >= y0 && t < y1) outs[0][(int64_t)t * nx + c] = v0;
-    // levels 1..J: level j computes row r = t - j
-#pragma unroll
-    for (int j = 1; j <= J; ++j) {
-      const int r = t - j;
-      const int64_t rg = row0 + r;
-      double v = 0.0;
-      // level j is needed (and its inputs valid) only within J-j rows of the CTA's rows
-      if (colin && rg >= 0 && rg < rows_g && r >= y0 - (J - j) && r < y1 + (J - j)) {
-        // x-neighbours of level j-1 at row r: its line written one step ago
-        const double* ln = line[j - 1][par ^ 1];
-        // (tile-edge threads see a zero instead of the neighbour: they are ghost columns whose
-        // values never reach an output)
-        const double xw = (hasW && tid > 0) ? ln[tid - 1] : 0.0;
-        const double xe = (hasE && tid + 1 < 288) ? ln[tid + 1] : 0.0;
-        const double ys = rg > 0 ? win[j - 1][0] : 0.0;
-        const double yn = rg + 1 < rows_g ? win[j - 1][2] : 0.0;
-        double cS, cW, cC, cE, cN;
-        if (KIND == kStencilConst) {
-          cS = d.op.coef[1], cW = d.op.coef[2], cC = d.op.coef[3], cE = d.op.coef[4], cN = d.op.coef[5];
-        } else {
-          bool pres[7];
-          int64_t nb[7];
-          const int64_t p = (int64_t)r * nx + c;
-          pres[0] = pres[6] = false;
-          pres[1] = rg > 0;
-          pres[2] = hasW;
-          pres[3] = true;
-          pres[4] = hasE;
-          pres[5] = rg + 1 < rows_g;
-          nb[0] = nb[6] = nb[3] = p;
-          nb[1] = p - nx;
-          nb[2] = p - 1;
-          nb[4] = p + 1;
-          nb[5] = p + nx;
-          double val[7];
-          coefs<2, KIND>(d.op, p, pres, nb, val);
-          cS = val[1], cW = val[2], cC = val[3], cE = val[4], cN = val[5];
-        }
-        // S, W, C, E, N (ascending column); absent neighbours are exact zeros
-        double a = 0.0;
-        a = __dadd_rn(a, __dmul_rn(cS, ys));
-        a = __dadd_rn(a, __dmul_rn(cW, xw));
-        a = __dadd_rn(a, __dmul_rn(cC, win[j - 1][1]));
-        a = __dadd_rn(a, __dmul_rn(cE, xe));
-        a = __dadd_rn(a, __dmul_rn(cN, yn));
-        v = a;
-      }
-      win[j][0] = win[j][1];
-      win[j][1] = win[j][2];
-      win[j][2] = v;
-      if (j < J) line[j < J ? j : 0][par][tid] = v;
-      if (outcol && r >= y0 && r < y1) {
-        const int64_t p = (int64_t)r * nx + c;
-        if (outs[j]) outs[j][p] = v;
-        if (DOTS) {
-#pragma unroll
-          for (int x = 0; x < NX; ++x) acc[x * J + (j - 1)] = fma(d.X[x][p], v, acc[x * J + (j - 1)]);
-        }
+      for (int x = 0; x < NX; ++x) {
+        const double* xr = d.X[x] + (int64_t)r * nx;
+        double* xs = xring + (x * NS + slot) * 64 + 2 * lane;
+        cp_async8(xs, rok && outA ? xr + ca : d.src, rok && outA);
+        cp_async8(xs + 1, rok && outB ? xr + cb : d.src, rok && outB);
       }
     }
-    __syncthreads();
+    cp_async_commit();
+  };
+  if (active) {
+#pragma unroll 1
+    for (int k = 0; k < PF; ++k) issue(tb + k);
+#pragma unroll 1
+    for (int t = tb; t < te; ++t) {
+      const int slot = (t - tb) % NS;
+      cp_async_wait<PF - 1>();
+      const bool rowin = row0 + t >= 0 && row0 + t < rows_g;
+      {
+        const double sa = ring[slot * 64 + 2 * lane], sb = ring[slot * 64 + 2 * lane + 1];
+        const double va = inA && rowin ? (d.scale ? __dmul_rn(sa, scale) : sa) : 0.0;
+        const double vb = inB && rowin ? (d.scale ? __dmul_rn(sb, scale) : sb) : 0.0;
+        wa[0][0] = wa[0][1], wa[0][1] = wa[0][2], wa[0][2] = va;
+        wb[0][0] = wb[0][1], wb[0][1] = wb[0][2], wb[0][2] = vb;
+        if (d.out[0] && t >= y0 && t < y1) {
+          double* o = d.out[0] + (int64_t)t * nx;
+          if (outA) o[ca] = va;
+          if (outB) o[cb] = vb;
+        }
+      }
+#pragma unroll
+      for (int j = 1; j <= J; ++j) {
+        const int r = t - j;  // row level j computes
+        const int64_t rg = row0 + r;
+        // x-neighbours of level j-1 at row r
+        const double ma = wa[j - 1][1], mb = wb[j - 1][1];
+        const double wA = __shfl_up_sync(FULL, mb, 1);    // column ca-1 (lane-1's b)
+        const double eB = __shfl_down_sync(FULL, ma, 1);  // column cb+1 (lane+1's a)
+        double va = 0.0, vb = 0.0;
+        if (rg >= 0 && rg < rows_g && r >= y0 - (J - j) && r < y1 + (J - j)) {
+          if (inA) va = point2d<KIND>(d.op, r, rg, rows_g, ca, nx, wa[j - 1][0], wA, ma, mb, wa[j - 1][2]);
+          if (inB) vb = point2d<KIND>(d.op, r, rg, rows_g, cb, nx, wb[j - 1][0], ma, mb, eB, wb[j - 1][2]);
+        }
+        wa[j][0] = wa[j][1], wa[j][1] = wa[j][2], wa[j][2] = va;
+        wb[j][0] = wb[j][1], wb[j][1] = wb[j][2], wb[j][2] = vb;
+        if (d.out[j] && r >= y0 && r < y1) {
+          double* o = d.out[j] + (int64_t)r * nx;
+          if (outA) o[ca] = va;
+          if (outB) o[cb] = vb;
+        }
+      }
+      // products of row t-J, complete at every level: level j's value sits J-j rows back
+      if (DOTS) {
+        const int r = t - J;
+        if (r >= y0 && r < y1) {
+#pragma unroll
+          for (int x = 0; x < NX; ++x) {
+            const double* xs = xring + (x * NS + slot) * 64 + 2 * lane;
+            const double xa = xs[0], xb = xs[1];  // zero-filled outside the output columns
+#pragma unroll
+            for (int j = 1; j <= J; ++j) {
+              acc[x * J + (j - 1)] = fma(xa, wa[j][2 - (J - j)], acc[x * J + (j - 1)]);
+              acc[x * J + (j - 1)] = fma(xb, wb[j][2 - (J - j)], acc[x * J + (j - 1)]);
+            }
+          }
+        }
+      }
+      issue(t + PF);  // refills the slot consumed at step t-1 (its reads retired in order)
+    }
   }
   if (DOTS) {
     // fixed-order CTA reduction: product (x, level j) -> dot0 + x*J + (j-1)
-    __shared__ double red[9][NACC];
-    const int lane = tid & 31, warp = tid >> 5;
+    __shared__ double red[MW_WARPS][NACC];
 #pragma unroll
     for (int q = 0; q < NACC; ++q) {
       const double v = warp_sum(acc[q]);
-      if (lane == 0) red[warp][q] = v;
+      if (lane == 0) red[wid][q] = v;
     }
     __syncthreads();
-    for (int e = tid; e < NACC; e += blockDim.x) {
+    for (int e = threadIdx.x; e < NACC; e += blockDim.x) {
       double s = 0.0;
-      for (int w = 0; w < 9; ++w) s += red[w][e];
+      for (int w = 0; w < MW_WARPS; ++w) s += red[w][e];
       d.partials[(int64_t)(d.dot0 + e) * kPartialPitch + blockIdx.x] = s;
     }
   }
 }
 
 // ------------------------------------------------------------------ 3D
-// tile: TXe x TYe threads (extended by J each side), streamed over d.Z planes
+// tile: TXE x TYE threads (extended by J each side), streamed over d.Z planes
+constexpr int PF3 = 4;
+
+template <int J, int NT, bool DOTS>
+constexpr size_t mpk3d_smem() {
+  return sizeof(double) * NT * ((size_t)2 * J + (PF3 + 1) * (DOTS ? (size_t)J + 2 : 1));
+}
+
 template <int KIND, int J, int TXE, int TYE, bool DOTS>
 __global__ void __launch_bounds__(TXE* TYE) k_mpk3d(const __grid_constant__ MpkDesc d) {
+  static_assert(!DOTS || J <= 3, "fused products read level values from the 3-row windows");
   if (skip_launch(d.halt, d.cond)) return;
-  __shared__ double plane[J][2][TYE][TXE];
-  const int lx = threadIdx.x % TXE, ly = threadIdx.x / TXE;
+  constexpr int NT = TXE * TYE, PF = PF3, NS = PF3 + 1, NX = J + 1;
+  extern __shared__ __align__(16) double dsm[];
+  double* plane = dsm;                 // [J][2][TYE][TXE]
+  double* ring = plane + 2 * J * NT;   // [NS][NT]
+  double* xring = ring + NS * NT;      // [NX][NS][NT]
+  const int tid = threadIdx.x;
+  const int lx = tid % TXE, ly = tid / TXE;
   const int64_t nx = d.op.nx, ny = d.op.ny, nz = d.op.nz;
   const int64_t pl = nx * ny;
   const int ntile = d.tiles_x * d.tiles_y;
@@ -235,7 +303,7 @@ __global__ void __launch_bounds__(TXE* TYE) k_mpk3d(const __grid_constant__ MpkD
   double win[J + 1][3];
 #pragma unroll
   for (int j = 0; j <= J; ++j) win[j][0] = win[j][1] = win[j][2] = 0.0;
-  constexpr int NACC = DOTS ? (J + 1) * J : 1;
+  constexpr int NACC = DOTS ? NX * J : 1;
   double acc[NACC];
 #pragma unroll
   for (int q = 0; q < NACC; ++q) acc[q] = 0.0;
@@ -244,44 +312,51 @@ __global__ void __launch_bounds__(TXE* TYE) k_mpk3d(const __grid_constant__ MpkD
   const int64_t row0 = d.op.row0, rows_g = d.op.rows_global;
   const int64_t H = d.op.halo_rows;
   const int64_t xy = y * nx + x;
-  auto fetch = [&](int64_t t) -> double {
+  const int64_t tb = z0 - J, te = z1 + J;
+  auto issue = [&](int64_t t) {
+    const int slot = (int)((t - tb) % NS);
     const int64_t tg = row0 + t;
-    if (!in || tg < 0 || tg >= rows_g || t < z0 - J || t >= z1 + J) return 0.0;
-    const double* pp =
-        t < 0 ? d.op.hlo + (t + H) * pl : (t >= nz ? d.op.hhi + (t - nz) * pl : d.src + t * pl);
-    return pp[xy];
+    const bool ok = in && tg >= 0 && tg < rows_g && t < te;
+    const double* pp = d.src;
+    if (ok) pp = (t < 0 ? d.op.hlo + (t + H) * pl : (t >= nz ? d.op.hhi + (t - nz) * pl : d.src + t * pl)) + xy;
+    cp_async8(ring + slot * NT + tid, pp, ok);
+    if (DOTS) {
+      const int64_t r = t - J;
+      const bool okx = outp && r >= z0 && r < z1;
+#pragma unroll
+      for (int q = 0; q < NX; ++q) cp_async8(xring + (q * NS + slot) * NT + tid, okx ? d.X[q] + r * pl + xy : d.src, okx);
+    }
+    cp_async_commit();
   };
-  constexpr int PF = 4;
-  double pf[PF];
-#pragma unroll
-  for (int k = 0; k < PF; ++k) pf[k] = fetch(z0 - J + k);
-  for (int64_t t = z0 - J; t < z1 + J; ++t) {
+#pragma unroll 1
+  for (int k = 0; k < PF; ++k) issue(tb + k);
+#pragma unroll 1
+  for (int64_t t = tb; t < te; ++t) {
     const int par = (int)(t & 1);
-    const double s0 = pf[0];
-#pragma unroll
-    for (int k = 0; k + 1 < PF; ++k) pf[k] = pf[k + 1];
-    pf[PF - 1] = fetch(t + PF);
+    const int slot = (int)((t - tb) % NS);
+    cp_async_wait<PF - 1>();
+    const double s0 = ring[slot * NT + tid];
     double v0 = 0.0;
     if (in && row0 + t >= 0 && row0 + t < rows_g) v0 = d.scale ? __dmul_rn(s0, scale) : s0;
     win[0][0] = win[0][1];
     win[0][1] = win[0][2];
     win[0][2] = v0;
-    plane[0][par][ly][lx] = v0;
-    if (d.out[0] && outp && t >= z0 && t < z1) d.out[0][t * pl + y * nx + x] = v0;
+    plane[par * NT + tid] = v0;
+    if (d.out[0] && outp && t >= z0 && t < z1) d.out[0][t * pl + xy] = v0;
 #pragma unroll
     for (int j = 1; j <= J; ++j) {
       const int64_t r = t - j;  // plane computed by level j
       const int64_t rg = row0 + r;
       double v = 0.0;
       if (in && rg >= 0 && rg < rows_g && r >= z0 - (J - j) && r < z1 + (J - j)) {
-        const auto& P = plane[j - 1][par ^ 1];
-        const double ys = ly > 0 ? P[ly - 1][lx] : 0.0;
-        const double xw = lx > 0 ? P[ly][lx - 1] : 0.0;
-        const double xe = lx + 1 < TXE ? P[ly][lx + 1] : 0.0;
-        const double yn = ly + 1 < TYE ? P[ly + 1][lx] : 0.0;
+        const double* P = plane + ((j - 1) * 2 + (par ^ 1)) * NT;
+        const double ys = ly > 0 ? P[tid - TXE] : 0.0;
+        const double xw = lx > 0 ? P[tid - 1] : 0.0;
+        const double xe = lx + 1 < TXE ? P[tid + 1] : 0.0;
+        const double yn = ly + 1 < TYE ? P[tid + TXE] : 0.0;
         bool pres[7];
         int64_t nb[7];
-        const int64_t p = r * pl + y * nx + x;
+        const int64_t p = r * pl + xy;
         pres[0] = rg > 0;
         pres[1] = y > 0;
         pres[2] = x > 0;
@@ -311,29 +386,34 @@ __global__ void __launch_bounds__(TXE* TYE) k_mpk3d(const __grid_constant__ MpkD
       win[j][0] = win[j][1];
       win[j][1] = win[j][2];
       win[j][2] = v;
-      if (j < J) plane[j < J ? j : 0][par][ly][lx] = v;
+      if (j < J) plane[(j * 2 + par) * NT + tid] = v;
+      if (d.out[j] && outp && r >= z0 && r < z1) d.out[j][r * pl + xy] = v;
+    }
+    if (DOTS) {
+      const int64_t r = t - J;
       if (outp && r >= z0 && r < z1) {
-        const int64_t p = r * pl + y * nx + x;
-        if (d.out[j]) d.out[j][p] = v;
-        if (DOTS) {
 #pragma unroll
-          for (int q = 0; q < J + 1; ++q) acc[q * J + (j - 1)] = fma(d.X[q][p], v, acc[q * J + (j - 1)]);
+        for (int q = 0; q < NX; ++q) {
+          const double xv = xring[(q * NS + slot) * NT + tid];
+#pragma unroll
+          for (int j = 1; j <= J; ++j) acc[q * J + (j - 1)] = fma(xv, win[j][2 - (J - j)], acc[q * J + (j - 1)]);
         }
       }
     }
+    issue(t + PF);
     __syncthreads();
   }
   if (DOTS) {
-    constexpr int NW = TXE * TYE / 32;
+    constexpr int NW = NT / 32;
     __shared__ double red[NW][NACC];
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int lane = tid & 31, warp = tid >> 5;
 #pragma unroll
     for (int q = 0; q < NACC; ++q) {
       const double v = warp_sum(acc[q]);
       if (lane == 0) red[warp][q] = v;
     }
     __syncthreads();
-    for (int e = threadIdx.x; e < NACC; e += blockDim.x) {
+    for (int e = tid; e < NACC; e += blockDim.x) {
       double s = 0.0;
       for (int w = 0; w < NW; ++w) s += red[w][e];
       d.partials[(int64_t)(d.dot0 + e) * kPartialPitch + blockIdx.x] = s;
@@ -341,22 +421,44 @@ __global__ void __launch_bounds__(TXE* TYE) k_mpk3d(const __grid_constant__ MpkD
   }
 }
 
+template <class K>
+void mpk_smem_attr(K kernel, size_t bytes) {
+  if (bytes > 48 * 1024) CK(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+}
+
+template <int KIND, int J, bool DOTS>
+void run2d(Ctx& c, const MpkDesc& d) {
+  constexpr size_t smem = mpk2w_smem<J, DOTS>();
+  static bool attr = false;
+  if (!attr) mpk_smem_attr(k_mpk2w<KIND, J, DOTS>, smem), attr = true;
+  k_mpk2w<KIND, J, DOTS><<<d.G, MW_WARPS * 32, smem, c.stream>>>(d);
+}
+
 template <int KIND, int J>
 void launch2d(Ctx& c, MpkDesc& d) {
   const int64_t nx = d.op.nx, ny = d.op.ny;
-  d.W = (int)std::min<int64_t>(nx, 288 - 2 * J);
+  d.W = 64 - 2 * J;
   d.tiles_x = (int)((nx + d.W - 1) / d.W);
-  // rows per CTA: aim for ~2 CTAs per SM, at least 4J rows to bound the ghost-row overhead
-  const int64_t target = 2LL * c.sm_count;
-  int64_t R = std::max<int64_t>(4 * J, (ny * d.tiles_x + target - 1) / target);
+  // rows per warp strip: ~16 strips per SM, at least 3J rows to bound the ghost-row overhead
+  const int64_t target = 16LL * c.sm_count;
+  int64_t R = std::max<int64_t>(3 * J, (ny * d.tiles_x + target - 1) / target);
   R = std::min<int64_t>(R, ny);
   d.R = (int)R;
   d.tiles_y = (int)((ny + R - 1) / R);
-  d.G = d.tiles_x * d.tiles_y;
-  if (d.nx_dots)
-    k_mpk2d<KIND, J, true><<<d.G, 288, 0, c.stream>>>(d);
-  else
-    k_mpk2d<KIND, J, false><<<d.G, 288, 0, c.stream>>>(d);
+  d.G = (d.tiles_x * d.tiles_y + MW_WARPS - 1) / MW_WARPS;
+  if constexpr (J <= 3) {
+    if (d.nx_dots) return run2d<KIND, J, true>(c, d);
+  }
+  run2d<KIND, J, false>(c, d);
+}
+
+template <int KIND, int J, bool DOTS>
+void run3d(Ctx& c, const MpkDesc& d) {
+  constexpr int TXE = 32, TYE = 16;
+  constexpr size_t smem = mpk3d_smem<J, TXE * TYE, DOTS>();
+  static bool attr = false;
+  if (!attr) mpk_smem_attr(k_mpk3d<KIND, J, TXE, TYE, DOTS>, smem), attr = true;
+  k_mpk3d<KIND, J, TXE, TYE, DOTS><<<d.G, TXE * TYE, smem, c.stream>>>(d);
 }
 
 template <int KIND, int J>
@@ -375,9 +477,9 @@ void launch3d(Ctx& c, MpkDesc& d) {
   d.Z = (int)Z;
   d.G = (int)(ntile * ((nz + Z - 1) / Z));
   if (d.nx_dots)
-    k_mpk3d<KIND, J, TXE, TYE, true><<<d.G, TXE * TYE, 0, c.stream>>>(d);
+    run3d<KIND, J, true>(c, d);
   else
-    k_mpk3d<KIND, J, TXE, TYE, false><<<d.G, TXE * TYE, 0, c.stream>>>(d);
+    run3d<KIND, J, false>(c, d);
 }
 
 template <int KIND>
@@ -413,7 +515,8 @@ int launch_mpk(Ctx& c, const DevOp& op, const double* src, const double* scale, 
                const int* cond) {
   require(op.kind != kCsr, "mpk: general CSR operators use repeated applies");
   require(J >= 1 && J <= mpk_max_depth(op), "mpk: depth out of range");
-  require(nxd == 0 || (nxd == J + 1 && jdot0 <= 1), "mpk: fused products need J+1 vectors against levels 1..J");
+  require(nxd == 0 || (nxd == J + 1 && jdot0 <= 1 && J <= kMpkMaxDotDepth),
+          "mpk: fused products need J+1 vectors against levels 1..J (J <= 3)");
   MpkDesc d;
   std::memset(&d, 0, sizeof d);
   d.op = op;

@@ -493,7 +493,7 @@ struct Engine {
         for (int j = 0; j <= d; ++j) outs[j] = col(b, done + j);
         if (done > 0) outs[0] = nullptr;  // already written by the previous sweep
         const double* X[kMaxS];
-        const bool fuse = dots && done == 0 && d == J;
+        const bool fuse = dots && done == 0 && d == J && J <= kMpkMaxDotDepth;
         for (int l = 0; l < s; ++l) X[l] = col(0, l);
         const int G0 = launch_mpk(c, op.d, from, sc, outs, d, fuse ? s : 0, X, 1, partials, dl.D(), halt, nullptr);
         if (fuse) Gd = G0;

@@ -199,6 +199,8 @@ void launch_fill(Ctx& c, double* p, double v, int64_t n);
 // matrix powers (mpk.cu): out[0..J] of src*scale; products X[x] . level j (j >= jdot0) at
 // dot0 + x*(J-jdot0+1) + (j-jdot0) as partials over the returned CTA count.
 int mpk_max_depth(const DevOp& op);
+constexpr int kMpkMaxDotDepth = 3;
+enum : uint8_t { kHintNormal = 0, kHintFirst = 1, kHintLast = 2 };  // L2 policies of streamed vectors  // deepest sweep that can fuse products (launch_mpk)
 int launch_mpk(Ctx& c, const DevOp& op, const double* src, const double* scale, double* const* out, int J, int nxd,
                const double* const* X, int jdot0, double* partials, int dot0, const int* halt, const int* cond);
 // one block-MGS round: cand[1..s) += sum_l coef_t[l*(s-1)+jc-1] Vi[l]; if Vnext: the

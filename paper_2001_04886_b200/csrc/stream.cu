@@ -338,6 +338,71 @@ __global__ void __launch_bounds__(THREADS) k_mgs(const __grid_constant__ MgsDesc
   }
 }
 
+// Two-phase variant for S >= 6, where S(S-1) per-thread accumulators would spill: the tile's
+// new candidate columns are written back into their stage slots, the consumer warps meet at a
+// named barrier, and the products with V_{i+1} are taken from shared memory with one warp per
+// V_{i+1} column (S-1 accumulators per thread).  Partial layout as in k_mgs.
+template <int S>
+__global__ void __launch_bounds__(THREADS) k_mgs2(const __grid_constant__ MgsDesc d) {
+  static_assert(S <= NCW, "one warp per V_{i+1} column");
+  if (skip_launch(d.h.halt, d.h.cond)) return;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  constexpr int NC = S - 1;
+  Pipe p = pipe_setup(d.h, smem_raw, 8 * 64);
+  double* cs = reinterpret_cast<double*>(smem_raw + 64);
+  if (threadIdx.x < S * NC) cs[threadIdx.x] = d.coef[threadIdx.x];
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const bool dotw = warp < S;  // warp l owns the products with V_{i+1}[:, l]
+  double acc[NC];
+#pragma unroll
+  for (int k = 0; k < NC; ++k) acc[k] = 0.0;
+  if (warp == NCW) {
+    pipe_produce(d.h, d.U, p);
+  } else {
+    const int T = d.h.T;
+    for (int t = 0; t < p.ntiles; ++t) {
+      TileGeom g;
+      double* Sm = pipe_acquire(d.h, p, t, g);
+      for (int q = threadIdx.x; q < g.cnt; q += CONS) {
+        double cv[NC];
+#pragma unroll
+        for (int j = 0; j < NC; ++j) cv[j] = Sm[(size_t)(S + j) * T + q];
+#pragma unroll
+        for (int l = 0; l < S; ++l) {
+          const double v = Sm[(size_t)l * T + q];
+#pragma unroll
+          for (int j = 0; j < NC; ++j) cv[j] = dadd(cv[j], dmul(cs[l * NC + j], v));
+        }
+#pragma unroll
+        for (int j = 0; j < NC; ++j) {
+          d.cand[j][g.start + q] = cv[j];
+          Sm[(size_t)(S + j) * T + q] = cv[j];
+        }
+      }
+      asm volatile("bar.sync 1, %0;" ::"n"(CONS) : "memory");
+      if (dotw) {
+        const double* wl = Sm + (size_t)(2 * S - 1 + warp) * T;
+        for (int q = lane; q < g.cnt; q += 32) {
+          const double w = wl[q];
+#pragma unroll
+          for (int j = 0; j < NC; ++j) acc[j] = fma(w, Sm[(size_t)(S + j) * T + q], acc[j]);
+        }
+      }
+      fence_proxy_async();  // generic writes to the stage before the producer's next bulk copy
+      pipe_release(d.h, p, t);
+    }
+  }
+  __syncthreads();
+  if (dotw) {
+#pragma unroll
+    for (int j = 0; j < NC; ++j) {
+      const double v = warp_sum(acc[j]);
+      if (lane == 0) d.partials[(int64_t)(d.dot0 + warp * NC + j) * kPartialPitch + blockIdx.x] = v;
+    }
+  }
+}
+
 // ------------------------------------------------------------------ k_grm
 template <int NR, int LB>
 __global__ void __launch_bounds__(THREADS) k_grm(const __grid_constant__ GrmDesc d) {
@@ -415,12 +480,15 @@ struct TileChoice {
 
 // Tile size / stage count: >= 3 stages where possible, then large tiles, preferring a
 // footprint that lets two CTAs share an SM.  `align` = tile granularity (points).
-TileChoice pick_tiles(int nu, size_t prefix, int Tmax, int Tmin) {
+TileChoice pick_tiles(int nu, size_t prefix, int Tmax, int Tmin, bool fine = true) {
   for (size_t limit : {(size_t)110 * 1024, (size_t)220 * 1024}) {
     for (int ns : {3, 4, 2}) {
-      for (int T = Tmax; T >= Tmin; T /= 2) {
-        const size_t need = 64 + prefix + (size_t)ns * nu * T * 8;
-        if (need <= limit) return {T, ns, need};
+      for (int T2 = 2 * Tmax; T2 >= 2 * Tmin; T2 /= 2) {
+        for (int T : {T2 / 2 + T2 / 4, T2 / 2}) {  // 3/4 and 1/2 of T2: 1536, 1024, .., 96, 64
+          if (T > Tmax || T < Tmin || (!fine && T != T2 / 2)) continue;
+          const size_t need = 64 + prefix + (size_t)ns * nu * T * 8;
+          if (need <= limit) return {T, ns, need};
+        }
       }
     }
   }
@@ -490,9 +558,15 @@ void launch_grm_l(Ctx& c, const GrmDesc& d, size_t smem, int G) {
 
 template <int S, bool DOTS>
 void launch_mgs_t(Ctx& c, const MgsDesc& d, size_t smem, int G) {
-  static bool attr = false;
-  if (!attr) allow_smem(k_mgs<S, DOTS>), attr = true;
-  k_mgs<S, DOTS><<<G, THREADS, smem, c.stream>>>(d);
+  if constexpr (DOTS && S >= 6) {
+    static bool attr = false;
+    if (!attr) allow_smem(k_mgs2<S>), attr = true;
+    k_mgs2<S><<<G, THREADS, smem, c.stream>>>(d);
+  } else {
+    static bool attr = false;
+    if (!attr) allow_smem(k_mgs<S, DOTS>), attr = true;
+    k_mgs<S, DOTS><<<G, THREADS, smem, c.stream>>>(d);
+  }
 }
 
 void fill_hdr(PipeHdr& h, int nu, const TileChoice& tc, int64_t n, int64_t range, const int* halt, const int* cond) {
@@ -555,7 +629,8 @@ void launch_lincomb(Ctx& c, const LinDesc& L, const char* name) {
   d.dot0 = L.dot0;
   d.G = L.G;
   const size_t prefix = 8 * ((size_t)((L.ncoef + 15) & ~15) + (maxd ? (size_t)(nout_t + LC_MAXX) * CONS : 0));
-  const TileChoice tc = pick_tiles(nu, prefix, nout_t <= 8 ? 2 * CONS : CONS, 64);
+  // k_upd covers T <= CONS * PPT points per tile: powers of two only
+  const TileChoice tc = pick_tiles(nu, prefix, nout_t <= 8 ? 2 * CONS : CONS, 64, false);
   fill_hdr(d.h, nu, tc, L.n, L.range, L.halt, L.cond);
   const double bytes = 8.0 * (double)L.n * (nu + L.nout);
   Launch lh(c, name, bytes);
