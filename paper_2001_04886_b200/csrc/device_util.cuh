@@ -117,6 +117,7 @@ __device__ __forceinline__ void reduce_dots_dev(const double* __restrict__ parti
       const double* p = partials + (int64_t)(d0 + d) * kPartialPitch;
       double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
       int g = sub;
+#pragma unroll 4
       for (; g + 3 * tpd < G; g += 4 * tpd) {
         a0 += p[g];
         a1 += p[g + tpd];

@@ -57,7 +57,9 @@ struct DotLayout {
   int Z() const { return 0; }
   int Seed() const { return m * s + 1; }
   int D() const { return Seed() + 1; }
-  int Cross() const { return D() + s * s; }
+  // block-MGS products, double-buffered by round: round i reads Dr(i) and writes Dr(i+1)
+  int Dr(int i) const { return D() + (i & 1) * s * s; }
+  int Cross() const { return D() + 2 * s * s; }
   int Wa() const { return Cross() + m * s * s; }
   int Wb() const { return Wa() + s * s; }
   int RR() const { return Wb() + s * s; }
@@ -161,26 +163,6 @@ __global__ void k_arn_s2(ArnState* st, int k, double* rec, double* coef, const d
       return;
     }
     coef[cInv] = 1.0 / nu;
-  }
-}
-
-// block-MGS Scalar2 against block i (sstep.hpp:338-353): t = W_i^{-1} (V_i^T cand[:,1:])
-__global__ void k_arn_t(ArnState* st, const Gram* grams, int i, double* rec, double* coef, const double* partials,
-                        int G, int dD, int s, int cT, int reorth_pass) {
-  if (arn_skip(st)) return;
-  if (reorth_pass && !st->reorth) return;
-  __shared__ double v[kMaxS * kMaxS];
-  const int nc = s - 1;
-  reduce_dots_dev(partials, G, dD, s * nc, v);
-  for (int jc = threadIdx.x; jc < nc; jc += blockDim.x) {
-    double rhs[kMaxS], t[kMaxS];
-    for (int l = 0; l < s; ++l) rhs[l] = v[l * nc + jc];
-    gram_solve(grams[i], rhs, t);
-    for (int l = 0; l < s; ++l) {
-      coef[cT + l * nc + jc] = -t[l];
-      double* ta = rec + i * s * s + l * s + (jc + 1);  // rec points at this block's T area
-      *ta = reorth_pass ? *ta + t[l] : t[l];
-    }
   }
 }
 
@@ -589,9 +571,10 @@ struct Engine {
         }
         for (int i = 0; i < k; ++i) {
           const int Gi = (i == 0 && have) ? Gfused : g.G;
-          k_arn_t<<<1, 256, 0, c.stream>>>(st, grams, i, tk, coef, partials,
-                                           c.reduce_point(partials, Gi, dl.D(), s * (s - 1)), dl.D(), s, cl.T(), pass);
-          ++c.launches;
+          // Scalar2 against block i (sstep.hpp:338-353) runs in the update kernel's prologue:
+          // t = W_i^{-1} V_i^T cand[:,1:], recorded at block i of this iteration's T area
+          const MgsScalar sc{partials, c.reduce_point(partials, Gi, dl.Dr(i), s * (s - 1)), dl.Dr(i), grams + i,
+                             tk + i * s * s, pass};
           // cand[:,jc] -= sum_l t(l,jc-1) V_i[:,l]  (+ products with V_{i+1})
           const double* Vi[kMaxS];
           const double* Vn[kMaxS];
@@ -601,7 +584,7 @@ struct Engine {
             Vn[l] = i + 1 < k ? col(i + 1, l) : nullptr;
             cd[l] = col(cb, l);
           }
-          launch_mgs(c, g, s, Vi, cd, i + 1 < k ? Vn : nullptr, coef + cl.T(), partials, dl.D(), halt, cond);
+          launch_mgs(c, g, s, Vi, cd, i + 1 < k ? Vn : nullptr, sc, partials, dl.Dr(i + 1), halt, cond);
         }
         if (pass == 0) {
           // reorthogonalization test and the candidate's Gram matrix in one pass over cand:

@@ -199,14 +199,26 @@ void launch_fill(Ctx& c, double* p, double v, int64_t n);
 // matrix powers (mpk.cu): out[0..J] of src*scale; products X[x] . level j (j >= jdot0) at
 // dot0 + x*(J-jdot0+1) + (j-jdot0) as partials over the returned CTA count.
 int mpk_max_depth(const DevOp& op);
-constexpr int kMpkMaxDotDepth = 3;
-enum : uint8_t { kHintNormal = 0, kHintFirst = 1, kHintLast = 2 };  // L2 policies of streamed vectors  // deepest sweep that can fuse products (launch_mpk)
+constexpr int kMpkMaxDotDepth = 3;  // deepest sweep that can fuse products (launch_mpk)
+enum : uint8_t { kHintNormal = 0, kHintFirst = 1, kHintLast = 2 };  // L2 policies of streamed vectors
 int launch_mpk(Ctx& c, const DevOp& op, const double* src, const double* scale, double* const* out, int J, int nxd,
                const double* const* X, int jdot0, double* partials, int dot0, const int* halt, const int* cond);
-// one block-MGS round: cand[1..s) += sum_l coef_t[l*(s-1)+jc-1] Vi[l]; if Vnext: the
-// products Vnext[l] . cand[jc] at dot0 + l*(s-1) + jc-1
+// One block-MGS round of s-step Arnoldi (Scalar2 + update, sstep.hpp:338-353).  The kernel
+// prologue is the round's scalar step, computed redundantly by every CTA: reduce the incoming
+// products V_i^T cand[:,1:] (partials `src` rows src_d0.., src_G columns, fixed order), solve
+// W_i t = (V_i^T cand) with block i's Gram factor; CTA 0 records t into rec_t (row l, column
+// jc at l*s + jc; added to the stored value on the reorthogonalization pass).  Then
+// cand[:,jc] -= sum_l t(l,jc-1) V_i[:,l], fused with the next round's products
+// Vnext[l] . cand[jc] at dot0 + l*(s-1) + jc-1 when Vnext is given.
+struct MgsScalar {
+  const double* src;
+  int src_G, src_d0;
+  const Gram* gram;
+  double* rec_t;
+  int accumulate;
+};
 void launch_mgs(Ctx& c, const Geo& geo, int s, const double* const* Vi, double* const* cand, const double* const* Vnext,
-                const double* coef_t, double* partials, int dot0, const int* halt, const int* cond);
+                const MgsScalar& sc, double* partials, int dot0, const int* halt, const int* cond);
 // operator helpers
 void build_stencil_op(Ctx& c, Op& op, const skc_stencil_desc& d, const double* kcell_host);
 void build_csr_op(Ctx& c, Op& op, int64_t n, const uint64_t* offs, const uint64_t* cols, const double* vals);

@@ -73,7 +73,7 @@ struct MgsDesc {
   PipeHdr h;
   const double* U[3 * kMaxS];  // V_i[0..S), cand[1..S), V_{i+1}[0..S) (DOTS)
   double* cand[kMaxS];         // outputs cand[1..S)
-  const double* coef;          // t: coef[l*(S-1) + jc-1] (already negated)
+  MgsScalar sc;                // the round's scalar step (prologue)
   double* partials;
   int dot0, G;
 };
@@ -121,9 +121,11 @@ __device__ __forceinline__ Pipe pipe_setup(const PipeHdr& h, unsigned char* smem
 
 // producer warp: stream every tile of this CTA's range through the stages
 template <int MAXU>
-__device__ __forceinline__ void pipe_produce(const PipeHdr& h, const double* const (&U)[MAXU], const Pipe& p) {
+__device__ __forceinline__ void pipe_produce(const PipeHdr& h, const double* const (&U)[MAXU], const Pipe& p,
+                                             int t0 = 0, int t1 = -1) {
   const int lane = threadIdx.x & 31;
-  for (int t = 0; t < p.ntiles; ++t) {
+  if (t1 < 0 || t1 > p.ntiles) t1 = p.ntiles;
+  for (int t = t0; t < t1; ++t) {
     const int st = t % h.nstage, u = t / h.nstage;
     if (u > 0) mbar_wait(&p.empty[st], (uint32_t)((u - 1) & 1));
     const TileGeom g = tile_geom(h, p.r0, p.r1, t);
@@ -275,6 +277,42 @@ __global__ void __launch_bounds__(THREADS) k_upd(const __grid_constant__ UpdDesc
 }
 
 // ------------------------------------------------------------------ k_mgs
+// The round's scalar step (see launch_mgs): every CTA reduces the incoming products in the
+// same fixed order and solves the same s x s system, so all CTAs apply identical t.  Whole
+// block calls; coefficients -t land in cs[l*(S-1) + jc-1].
+constexpr int kGramWords = (int)((sizeof(Gram) + 7) / 8);
+// coefficients, products, Gram copy; a multiple of 128 bytes so the stages stay aligned
+constexpr int kMgsPrefix = (8 * (64 + 64 + kGramWords) + 127) / 128 * 128;
+
+template <int S>
+__device__ __forceinline__ void mgs_scalar(const MgsScalar& sc, double* cs, double* tmp, Gram* gs) {
+  constexpr int NC = S - 1;
+  {  // stage block i's factor in shared memory: the serial solve then reads it at smem latency
+    const uint64_t* src = reinterpret_cast<const uint64_t*>(sc.gram);
+    uint64_t* dst = reinterpret_cast<uint64_t*>(gs);
+    for (int w = threadIdx.x; w < (int)(sizeof(Gram) / 8); w += blockDim.x) dst[w] = src[w];
+  }
+  reduce_dots_dev(sc.src, sc.src_G, sc.src_d0, S * NC, tmp);  // ends with __syncthreads
+  if (threadIdx.x < NC) {
+    const int jc = threadIdx.x;
+    double rhs[kMaxS], t[kMaxS];
+#pragma unroll
+    for (int l = 0; l < S; ++l) rhs[l] = tmp[l * NC + jc];
+    gram_solve(*gs, rhs, t);
+#pragma unroll
+    for (int l = 0; l < S; ++l) {
+      cs[l * NC + jc] = -t[l];
+      if (blockIdx.x == 0) {
+        double* ta = sc.rec_t + l * S + (jc + 1);
+        *ta = sc.accumulate ? *ta + t[l] : t[l];
+      }
+    }
+  }
+  __syncthreads();
+}
+
+// The producer warp puts the first stages in flight before the scalar step so the tile loads
+// overlap the reduction.
 // U layout: [0,S) V_i ; [S, 2S-1) cand[1..S-1] ; [2S-1, 3S-1) V_{i+1} (DOTS)
 template <int S, bool DOTS>
 __global__ void __launch_bounds__(THREADS) k_mgs(const __grid_constant__ MgsDesc d) {
@@ -282,10 +320,12 @@ __global__ void __launch_bounds__(THREADS) k_mgs(const __grid_constant__ MgsDesc
   extern __shared__ __align__(128) unsigned char smem_raw[];
   constexpr int NC = S - 1;
   constexpr int ND = DOTS ? S * NC : 1;
-  Pipe p = pipe_setup(d.h, smem_raw, 8 * 64);
-  double* red = reinterpret_cast<double*>(smem_raw + 64);  // 64 doubles: coefficients, then reduction
-  if (threadIdx.x < S * NC) red[threadIdx.x] = d.coef[threadIdx.x];
+  Pipe p = pipe_setup(d.h, smem_raw, kMgsPrefix);
+  double* red = reinterpret_cast<double*>(smem_raw + 64);  // 64 coefficients + 64 scratch doubles
+  const int warp = threadIdx.x >> 5;
   __syncthreads();
+  if (warp == NCW) pipe_produce(d.h, d.U, p, 0, d.h.nstage);
+  mgs_scalar<S>(d.sc, red, red + 64, reinterpret_cast<Gram*>(red + 128));
   // coefficients in registers for small S; for S >= 6 they are re-read from shared memory
   // (warp-uniform broadcast) to keep the accumulators in registers
   constexpr bool CREG = S < 6;
@@ -300,9 +340,8 @@ __global__ void __launch_bounds__(THREADS) k_mgs(const __grid_constant__ MgsDesc
   double acc[ND];
 #pragma unroll
   for (int k = 0; k < ND; ++k) acc[k] = 0.0;
-  const int warp = threadIdx.x >> 5;
   if (warp == NCW) {
-    pipe_produce(d.h, d.U, p);
+    pipe_produce(d.h, d.U, p, d.h.nstage);
   } else {
     const int T = d.h.T;
     for (int t = 0; t < p.ntiles; ++t) {
@@ -348,17 +387,18 @@ __global__ void __launch_bounds__(THREADS) k_mgs2(const __grid_constant__ MgsDes
   if (skip_launch(d.h.halt, d.h.cond)) return;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   constexpr int NC = S - 1;
-  Pipe p = pipe_setup(d.h, smem_raw, 8 * 64);
+  Pipe p = pipe_setup(d.h, smem_raw, kMgsPrefix);
   double* cs = reinterpret_cast<double*>(smem_raw + 64);
-  if (threadIdx.x < S * NC) cs[threadIdx.x] = d.coef[threadIdx.x];
-  __syncthreads();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  __syncthreads();
+  if (warp == NCW) pipe_produce(d.h, d.U, p, 0, d.h.nstage);
+  mgs_scalar<S>(d.sc, cs, cs + 64, reinterpret_cast<Gram*>(cs + 128));
   const bool dotw = warp < S;  // warp l owns the products with V_{i+1}[:, l]
   double acc[NC];
 #pragma unroll
   for (int k = 0; k < NC; ++k) acc[k] = 0.0;
   if (warp == NCW) {
-    pipe_produce(d.h, d.U, p);
+    pipe_produce(d.h, d.U, p, d.h.nstage);
   } else {
     const int T = d.h.T;
     for (int t = 0; t < p.ntiles; ++t) {
@@ -678,7 +718,7 @@ void launch_gram(Ctx& c, const GramDesc& g, const char* name) {
 }
 
 void launch_mgs(Ctx& c, const Geo& geo, int s, const double* const* Vi, double* const* cand, const double* const* Vnext,
-                const double* coef_t, double* partials, int dot0, const int* halt, const int* cond) {
+                const MgsScalar& sc, double* partials, int dot0, const int* halt, const int* cond) {
   require(s >= 2 && s <= kMaxS, "mgs: s out of range");
   MgsDesc d;
   std::memset(&d, 0, sizeof d);
@@ -691,12 +731,12 @@ void launch_mgs(Ctx& c, const Geo& geo, int s, const double* const* Vi, double* 
   const bool dots = Vnext != nullptr;
   if (dots)
     for (int l = 0; l < s; ++l) d.U[nu++] = Vnext[l];
-  d.coef = coef_t;
+  d.sc = sc;
   d.partials = partials;
   d.dot0 = dot0;
   d.G = geo.G;
-  TileChoice tc = pick_tiles(nu, 8 * 64, 2048, 64);
-  tc.smem = std::max(tc.smem, 64 + 8 * (size_t)(64 + NCW * 56));
+  TileChoice tc = pick_tiles(nu, kMgsPrefix, 2048, 64);
+  tc.smem = std::max(tc.smem, 64 + (size_t)kMgsPrefix + 8 * (size_t)NCW * 56);
   fill_hdr(d.h, nu, tc, geo.n, geo.range, halt, cond);
   const double bytes = 8.0 * (double)geo.n * (nu + s - 1);
   Launch lh(c, "mgs_update", bytes);
