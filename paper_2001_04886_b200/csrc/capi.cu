@@ -1,4 +1,5 @@
 // capi.cu -- the C ABI (include/skrylov_b200.h) over the C++ solvers.
+#include <cstdlib>
 #include <cstring>
 #include <string>
 
@@ -87,6 +88,7 @@ skc_ctx* make_ctx(int device) {
   ctx->c.sm_count = p.multiProcessorCount;
   CK(cudaStreamCreateWithFlags(&ctx->c.own_stream, cudaStreamNonBlocking));
   ctx->c.stream = ctx->c.own_stream;
+  if (const char* e = std::getenv("SKC_PDL")) ctx->c.pdl = std::atoi(e) != 0;
   return ctx;
 }
 

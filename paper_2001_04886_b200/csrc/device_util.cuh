@@ -14,6 +14,15 @@ __device__ __forceinline__ double dmul(double a, double b) { return __dmul_rn(a,
 __device__ __forceinline__ double dadd(double a, double b) { return __dadd_rn(a, b); }
 __device__ __forceinline__ double dsub(double a, double b) { return __dsub_rn(a, b); }
 
+// Kernel entry under programmatic dependent launch: release the next kernel on the stream for
+// scheduling, then wait until the previous grid has completed and its memory is visible
+// (both are no-ops for an ordinary launch).  Every kernel starts with this.
+#define SKC_PDL_ENTRY()                                          \
+  do {                                                           \
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); \
+    asm volatile("griddepcontrol.wait;" ::: "memory");              \
+  } while (0)
+
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);

@@ -73,6 +73,7 @@ __device__ __forceinline__ double stencil_point(const DevOp& op, const double* _
 template <int DIM, int KIND>
 __global__ void __launch_bounds__(256) k_apply(const __grid_constant__ DevOp op, const double* __restrict__ x,
                                                double* __restrict__ y, const int* halt, const int* cond) {
+  SKC_PDL_ENTRY();
   if (skip_launch(halt, cond)) return;
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t j = blockIdx.y;
@@ -84,6 +85,7 @@ __global__ void __launch_bounds__(256) k_apply(const __grid_constant__ DevOp op,
 
 __global__ void __launch_bounds__(256) k_apply_csr(const __grid_constant__ DevOp op, const double* __restrict__ x,
                                                    double* __restrict__ y, const int* halt, const int* cond) {
+  SKC_PDL_ENTRY();
   if (skip_launch(halt, cond)) return;
   const int64_t row = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (row >= op.n) return;
@@ -104,17 +106,17 @@ void launch_apply(Ctx& c, const DevOp& op, const double* x, double* y, const int
   Launch L(c, "apply", bytes);
   if (op.kind == kCsr) {
     const unsigned blocks = (unsigned)((op.n + 255) / 256);
-    k_apply_csr<<<blocks, 256, 0, c.stream>>>(op, x, y, halt, cond);
+    launch_k(c, k_apply_csr, blocks, 256, 0, op, x, y, halt, cond);
   } else {
     dim3 grid((unsigned)((op.nx + 255) / 256), (unsigned)op.ny, (unsigned)(op.dim == 3 ? op.nz : 1));
     const int key = op.dim * 10 + op.kind;
     switch (key) {
-      case 21: k_apply<2, kStencilConst><<<grid, 256, 0, c.stream>>>(op, x, y, halt, cond); break;
-      case 22: k_apply<2, kStencilVarK><<<grid, 256, 0, c.stream>>>(op, x, y, halt, cond); break;
-      case 23: k_apply<2, kStencilDia><<<grid, 256, 0, c.stream>>>(op, x, y, halt, cond); break;
-      case 31: k_apply<3, kStencilConst><<<grid, 256, 0, c.stream>>>(op, x, y, halt, cond); break;
-      case 32: k_apply<3, kStencilVarK><<<grid, 256, 0, c.stream>>>(op, x, y, halt, cond); break;
-      case 33: k_apply<3, kStencilDia><<<grid, 256, 0, c.stream>>>(op, x, y, halt, cond); break;
+      case 21: launch_k(c, k_apply<2, kStencilConst>, grid, 256, 0, op, x, y, halt, cond); break;
+      case 22: launch_k(c, k_apply<2, kStencilVarK>, grid, 256, 0, op, x, y, halt, cond); break;
+      case 23: launch_k(c, k_apply<2, kStencilDia>, grid, 256, 0, op, x, y, halt, cond); break;
+      case 31: launch_k(c, k_apply<3, kStencilConst>, grid, 256, 0, op, x, y, halt, cond); break;
+      case 32: launch_k(c, k_apply<3, kStencilVarK>, grid, 256, 0, op, x, y, halt, cond); break;
+      case 33: launch_k(c, k_apply<3, kStencilDia>, grid, 256, 0, op, x, y, halt, cond); break;
       default: fail(SKC_EINVAL, "apply: unsupported operator kind");
     }
   }
@@ -123,13 +125,14 @@ void launch_apply(Ctx& c, const DevOp& op, const double* x, double* y, const int
 
 // ------------------------------------------------------------------ misc
 __global__ void k_fill(double* p, double v, int64_t n) {
+  SKC_PDL_ENTRY();
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
     p[i] = v;
 }
 
 void launch_fill(Ctx& c, double* p, double v, int64_t n) {
   ++c.launches;
-  k_fill<<<std::min<int64_t>(1184, (n + 255) / 256 + 1), 256, 0, c.stream>>>(p, v, n);
+  launch_k(c, k_fill, std::min<int64_t>(1184, (n + 255) / 256 + 1), 256, 0, p, v, n);
   CK(cudaGetLastError());
 }
 

@@ -139,6 +139,7 @@ __device__ __forceinline__ double point2d(const DevOp& op, int64_t r, int64_t rg
 
 template <int KIND, int J, bool DOTS>
 __global__ void __launch_bounds__(MW_WARPS * 32) k_mpk2w(const __grid_constant__ MpkDesc d) {
+  SKC_PDL_ENTRY();
   static_assert(!DOTS || J <= 3, "fused products read level values from the 3-row windows");
   if (skip_launch(d.halt, d.cond)) return;
   constexpr int PF = MW_PF, NS = MW_NS, NX = J + 1;
@@ -281,6 +282,7 @@ constexpr size_t mpk3d_smem() {
 
 template <int KIND, int J, int TXE, int TYE, bool DOTS>
 __global__ void __launch_bounds__(TXE* TYE) k_mpk3d(const __grid_constant__ MpkDesc d) {
+  SKC_PDL_ENTRY();
   static_assert(!DOTS || J <= 3, "fused products read level values from the 3-row windows");
   if (skip_launch(d.halt, d.cond)) return;
   constexpr int NT = TXE * TYE, PF = PF3, NS = PF3 + 1, NX = J + 1;
@@ -431,7 +433,7 @@ void run2d(Ctx& c, const MpkDesc& d) {
   constexpr size_t smem = mpk2w_smem<J, DOTS>();
   static bool attr = false;
   if (!attr) mpk_smem_attr(k_mpk2w<KIND, J, DOTS>, smem), attr = true;
-  k_mpk2w<KIND, J, DOTS><<<d.G, MW_WARPS * 32, smem, c.stream>>>(d);
+  launch_k(c, k_mpk2w<KIND, J, DOTS>, d.G, MW_WARPS * 32, smem, d);
 }
 
 template <int KIND, int J>
@@ -458,7 +460,7 @@ void run3d(Ctx& c, const MpkDesc& d) {
   constexpr size_t smem = mpk3d_smem<J, TXE * TYE, DOTS>();
   static bool attr = false;
   if (!attr) mpk_smem_attr(k_mpk3d<KIND, J, TXE, TYE, DOTS>, smem), attr = true;
-  k_mpk3d<KIND, J, TXE, TYE, DOTS><<<d.G, TXE * TYE, smem, c.stream>>>(d);
+  launch_k(c, k_mpk3d<KIND, J, TXE, TYE, DOTS>, d.G, TXE * TYE, smem, d);
 }
 
 template <int KIND, int J>
@@ -512,7 +514,7 @@ int mpk_max_depth(const DevOp& op) { return op.kind == kCsr ? 0 : op.dim == 2 ? 
 // j >= jdot0 are written at dot0 + x*(J-jdot0+1) + (j-jdot0); returns the partial count G.
 int launch_mpk(Ctx& c, const DevOp& op, const double* src, const double* scale, double* const* out, int J,
                int nxd, const double* const* X, int jdot0, double* partials, int dot0, const int* halt,
-               const int* cond) {
+               const int* cond, const char* name) {
   require(op.kind != kCsr, "mpk: general CSR operators use repeated applies");
   require(J >= 1 && J <= mpk_max_depth(op), "mpk: depth out of range");
   require(nxd == 0 || (nxd == J + 1 && jdot0 <= 1 && J <= kMpkMaxDotDepth),
@@ -537,7 +539,7 @@ int launch_mpk(Ctx& c, const DevOp& op, const double* src, const double* scale, 
   for (int j = 0; j <= J; ++j) nout += out[j] != nullptr;
   const double bytes = 8.0 * (double)op.n * (1 + nout + nxd) + (op.kind == kStencilVarK ? 8.0 * op.n : 0.0) +
                        (op.kind == kStencilDia ? 8.0 * (op.dim == 2 ? 5 : 7) * op.n : 0.0);
-  Launch lh(c, "mpk", bytes);
+  Launch lh(c, name, bytes);
   switch (op.kind) {
     case kStencilConst: dispatch_j<kStencilConst>(c, d); break;
     case kStencilVarK: dispatch_j<kStencilVarK>(c, d); break;

@@ -12,6 +12,8 @@
 // least-squares update and the early-exit/collapse/fallback decisions, exactly in the
 // reference's order.  A second short enqueue applies x += V y and recomputes r = f - A x.
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 
 #include "device_util.cuh"
@@ -72,6 +74,7 @@ __device__ __forceinline__ bool arn_skip(const ArnState* st) { return st->halt !
 // checked_norm (same vector, same reduction => same value as the reference's norm2(v1)).
 __global__ void k_arn_ctor(ArnState* st, int use_rn, const double* partials, int G, int dNV, double* rec0,
                            double* coef, int cInv) {
+  SKC_PDL_ENTRY();
   __shared__ double v[1];
   if (!use_rn) reduce_dots_dev(partials, G, dNV, 1, v);
   if (threadIdx.x == 0) {
@@ -93,6 +96,7 @@ __global__ void k_arn_ctor(ArnState* st, int use_rn, const double* partials, int
 // push_block (sstep.hpp:392-399): W = gram_self(block) -> GramSolver; breakdown = collapse
 __global__ void k_arn_push(ArnState* st, Gram* grams, int k, double* rec, const double* partials, int G, int dWa,
                            int dWb, int s) {
+  SKC_PDL_ENTRY();
   if (arn_skip(st)) return;
   __shared__ double v[kMaxS * kMaxS];
   const int dW = st->reorth ? dWb : dWa;
@@ -125,6 +129,7 @@ __global__ void k_arn_push(ArnState* st, Gram* grams, int k, double* rec, const 
 // Scalar1 (sstep.hpp:301-310): zn = ||z||, h_i = W_i^{-1} V_i^T z
 __global__ void k_arn_s1(ArnState* st, const Gram* grams, int k, double* rec, double* coef, const double* partials,
                          int G, int dZ, int s, int cH, double* scratch) {
+  SKC_PDL_ENTRY();
   if (arn_skip(st)) return;
   reduce_dots_dev(partials, G, dZ, k * s + 1, scratch);
   if (threadIdx.x == 0) {
@@ -148,6 +153,7 @@ __global__ void k_arn_s1(ArnState* st, const Gram* grams, int k, double* rec, do
 // nu = ||seed|| and the invariant-subspace test (sstep.hpp:315-324)
 __global__ void k_arn_s2(ArnState* st, int k, double* rec, double* coef, const double* partials, int G, int dSeed,
                          int cInv) {
+  SKC_PDL_ENTRY();
   if (arn_skip(st)) return;
   __shared__ double v[1];
   reduce_dots_dev(partials, G, dSeed, 1, v);
@@ -169,6 +175,7 @@ __global__ void k_arn_s2(ArnState* st, int k, double* rec, double* coef, const d
 // needs_reorth (sstep.hpp:401-414) on the device-computed cross products
 __global__ void k_arn_check(ArnState* st, const Gram* grams, int k, double* rec, const double* partials, int G,
                             int dCross, int dWa, int s, double orth_tol, double* scratch) {
+  SKC_PDL_ENTRY();
   if (arn_skip(st)) return;
   // (k <= 64 blocks: m is limited to 64)
   reduce_dots_dev(partials, G, dCross, k * s * s, scratch);
@@ -200,6 +207,7 @@ __global__ void k_arn_check(ArnState* st, const Gram* grams, int k, double* rec,
 
 // r-norm after the cycle's residual update
 __global__ void k_arn_rn(ArnState* st, const double* partials, int G, int dRR, double* out) {
+  SKC_PDL_ENTRY();
   __shared__ double v[1];
   reduce_dots_dev(partials, G, dRR, 1, v);
   if (threadIdx.x == 0) {
@@ -218,6 +226,7 @@ struct GmState {
 };
 
 __global__ void k_gm_start(GmState* st, double* coef, int cInv) {
+  SKC_PDL_ENTRY();
   if (threadIdx.x == 0) {
     st->status = 0;
     st->halt = 0;
@@ -229,6 +238,7 @@ __global__ void k_gm_start(GmState* st, double* coef, int cInv) {
 // col_i = q_i . w ; coefficient -col_i for the MGS update (solvers.hpp:94-97)
 __global__ void k_gm_col(GmState* st, double* col, int i, double* coef, int cC, const double* partials, int G,
                          int d0) {
+  SKC_PDL_ENTRY();
   if (st->halt) return;
   __shared__ double v[1];
   reduce_dots_dev(partials, G, d0, 1, v);
@@ -241,6 +251,7 @@ __global__ void k_gm_col(GmState* st, double* col, int i, double* coef, int cC, 
 // hsub = ||w||, happy-breakdown test against ||col|| (solvers.hpp:100-109)
 __global__ void k_gm_sub(GmState* st, int j, double* col, double* coef, int cInv, const double* partials, int G,
                          int d0) {
+  SKC_PDL_ENTRY();
   if (st->halt) return;
   __shared__ double v[1];
   reduce_dots_dev(partials, G, d0, 1, v);
@@ -262,6 +273,7 @@ __global__ void k_gm_sub(GmState* st, int j, double* col, double* coef, int cInv
 }
 
 __global__ void k_gm_rn(GmState* st, const double* partials, int G, int d0) {
+  SKC_PDL_ENTRY();
   __shared__ double v[1];
   reduce_dots_dev(partials, G, d0, 1, v);
   if (threadIdx.x == 0) st->rn = sqrt(v[0]);
@@ -307,7 +319,7 @@ void gmres_device(Ctx& c, const Op& op, const double* f, double* x, uint64_t m64
     }
     lb.add_dot(0, 0);
     lb.launch(c, g, coef, ncoef, partials, 0, nullptr, nullptr, "residual");
-    k_gm_rn<<<1, 256, 0, c.stream>>>(st, partials, c.reduce_point(partials, g.G, 0, 1), 0);
+    launch_k(c, k_gm_rn, 1, 256, 0, st, partials, c.reduce_point(partials, g.G, 0, 1), 0);
     ++c.launches;
     GmState h;
     CK(cudaMemcpyAsync(&h, st, sizeof h, cudaMemcpyDeviceToHost, c.stream));
@@ -324,7 +336,7 @@ void gmres_device(Ctx& c, const Op& op, const double* f, double* x, uint64_t m64
   while (rn > tol && rep.iterations < max_iterations) {
     const int steps = (int)std::min<uint64_t>((uint64_t)m, max_iterations - rep.iterations);
     CK(cudaMemsetAsync(cols, 0, (size_t)(m + 1) * rstride * sizeof(double), c.stream));
-    k_gm_start<<<1, 32, 0, c.stream>>>(st, coef, cInv);
+    launch_k(c, k_gm_start, 1, 32, 0, st, coef, cInv);
     ++c.launches;
     {
       LinBuilder lb;  // q_0 = r / ||r||
@@ -336,7 +348,7 @@ void gmres_device(Ctx& c, const Op& op, const double* f, double* x, uint64_t m64
       launch_apply(c, op.d, q(j - 1), w, halt, nullptr);
       launch_gram_list(c, g, {q(0)}, {w}, partials, 0, halt, nullptr, "gram");
       for (int i = 0; i < j; ++i) {
-        k_gm_col<<<1, 256, 0, c.stream>>>(st, col, i, coef, cC, partials, c.reduce_point(partials, g.G, 0, 1), 0);
+        launch_k(c, k_gm_col, 1, 256, 0, st, col, i, coef, cC, partials, c.reduce_point(partials, g.G, 0, 1), 0);
         ++c.launches;
         LinBuilder lb;  // w -= col_i q_i ; next dot
         lb.add_out(w, w);
@@ -349,7 +361,7 @@ void gmres_device(Ctx& c, const Op& op, const double* f, double* x, uint64_t m64
         }
         lb.launch(c, g, coef, ncoef, partials, 0, halt, nullptr, "mgs_update");
       }
-      k_gm_sub<<<1, 256, 0, c.stream>>>(st, j, col, coef, cInv, partials, c.reduce_point(partials, g.G, 0, 1), 0);
+      launch_k(c, k_gm_sub, 1, 256, 0, st, j, col, coef, cInv, partials, c.reduce_point(partials, g.G, 0, 1), 0);
       ++c.launches;
       LinBuilder lb;
       lb.add_out(q(j), w, cInv);
@@ -428,6 +440,56 @@ struct Engine {
   Gram* grams;
   ArnState* st;
   const int* halt;
+  bool zfused = false;  // the next block iteration's z and Scalar1 products are already computed
+  // the restart cycle as a CUDA graph: its launch sequence and arguments are identical for
+  // every cycle of a solve (all control flow is device-side), so after one direct enqueue
+  // (which also performs first-use allocations and kernel attribute setup) it is captured
+  // once and replayed with a single launch per cycle
+  cudaGraphExec_t cycle_exec = nullptr;
+  uint64_t cycle_launches = 0;
+  int cycles_enqueued = 0;
+
+  Engine(const Engine&) = delete;
+  Engine& operator=(const Engine&) = delete;
+  ~Engine() {
+    if (cycle_exec) cudaGraphExecDestroy(cycle_exec);
+  }
+
+  void enqueue_cycle_direct() {
+    ctor(r, true);
+    for (int k = 1; k <= m; ++k) advance(k, k < m);
+  }
+
+  // ctor(r) + the m block iterations of one restart cycle
+  void enqueue_cycle() {
+    static const bool graphs = [] {
+      const char* e = std::getenv("SKC_GRAPH");
+      return !e || std::atoi(e) != 0;
+    }();
+    const bool use_graph = graphs && c.world() == 1 && !c.profiling;
+    if (!use_graph || cycles_enqueued++ == 0) return enqueue_cycle_direct();
+    if (!cycle_exec) {
+      const uint64_t l0 = c.launches;
+      CK(cudaStreamBeginCapture(c.stream, cudaStreamCaptureModeThreadLocal));
+      try {
+        enqueue_cycle_direct();
+      } catch (...) {
+        cudaGraph_t g = nullptr;
+        cudaStreamEndCapture(c.stream, &g);
+        if (g) cudaGraphDestroy(g);
+        throw;
+      }
+      cudaGraph_t graph = nullptr;
+      CK(cudaStreamEndCapture(c.stream, &graph));
+      const cudaError_t e = cudaGraphInstantiate(&cycle_exec, graph, 0);
+      cudaGraphDestroy(graph);
+      CK(e);
+      cycle_launches = c.launches - l0;
+      c.launches = l0;
+    }
+    CK(cudaGraphLaunch(cycle_exec, c.stream));
+    c.launches += cycle_launches;
+  }
 
   Engine(Ctx& ctx, const Op& o, int s_, int m_)
       : c(ctx), op(o), s(s_), m(m_), rl{s_, m_}, cl{s_, m_}, dl{s_, m_} {
@@ -492,33 +554,33 @@ struct Engine {
     return 0;
   }
 
-  // y = A x with the one-sweep stencil kernel where available
-  void apply(const double* x, double* y) {
+  // y = A x with the one-sweep stencil kernel where available (skipped unless *cond when given)
+  void apply(const double* x, double* y, const int* cond = nullptr) {
     if (mpk_max_depth(op.d) >= 1) {
       double* outs[2] = {nullptr, y};
-      launch_mpk(c, op.d, x, nullptr, outs, 1, 0, nullptr, 1, partials, 0, halt, nullptr);
+      launch_mpk(c, op.d, x, nullptr, outs, 1, 0, nullptr, 1, partials, 0, halt, cond, cond ? "mpk_redo" : "mpk");
     } else {
-      launch_apply(c, op.d, x, y, halt, nullptr);
+      launch_apply(c, op.d, x, y, halt, cond);
     }
   }
 
-  void gram_self_into(int b, int dW, const int* cond) {
+  void gram_self_into(int b, int dW, const int* cond, const char* name = "gram_w") {
     std::vector<const double*> B;
     for (int j = 0; j < s; ++j) B.push_back(col(b, j));
-    launch_gram_list(c, g, B, B, partials, dW, halt, cond, "gram_w");
+    launch_gram_list(c, g, B, B, partials, dW, halt, cond, name);
   }
 
   // SStepArnoldi ctor on device vector v (use_rn: its norm is st->rn)
   void ctor(const double* v, bool use_rn) {
+    zfused = false;
     CK(cudaMemsetAsync(rec, 0, (size_t)(m + 1) * rl.size() * sizeof(double), c.stream));
     if (!use_rn) launch_gram_list(c, g, {v}, {v}, partials, dl.RR(), nullptr, nullptr, "gram");
     const int Gc = use_rn ? g.G : c.reduce_point(partials, g.G, dl.RR(), 1);
-    k_arn_ctor<<<1, 256, 0, c.stream>>>(st, use_rn ? 1 : 0, partials, Gc, dl.RR(), recp(0), coef, cl.Inv());
+    launch_k(c, k_arn_ctor, 1, 256, 0, st, use_rn ? 1 : 0, partials, Gc, dl.RR(), recp(0), coef, cl.Inv());
     ++c.launches;
     krylov_into(0, v);
     gram_self_into(0, dl.Wa(), nullptr);
-    k_arn_push<<<1, 256, 0, c.stream>>>(st, grams, 0, recp(0), partials,
-                                        c.reduce_point(partials, g.G, dl.Wa(), s * s), dl.Wa(), dl.Wb(), s);
+    launch_k(c, k_arn_push, 1, 256, 0, st, grams, 0, recp(0), partials, c.reduce_point(partials, g.G, dl.Wa(), s * s), dl.Wa(), dl.Wb(), s);
     ++c.launches;
     CK(cudaGetLastError());
   }
@@ -526,17 +588,20 @@ struct Engine {
   // SStepArnoldi::advance for block iteration k (1-based), sstep.hpp:297-379
   void advance(int k, bool build_next) {
     double* rk = recp(k);
-    // z = A v_k^s ; Scalar1 dots V_i^T z and ||z||^2
-    apply(col(k - 1, s - 1), z);
+    // z = A v_k^s ; Scalar1 dots V_i^T z and ||z||^2.  After a block iteration that fused them
+    // into its cross-product pass (zfused) they are already in place, unless that iteration's
+    // reorthogonalization pass changed the block: then (device flag) they are recomputed.
+    const int* zcond = zfused ? &st->reorth : nullptr;
+    zfused = false;
+    apply(col(k - 1, s - 1), z, zcond);
     {
       std::vector<const double*> L;
       for (int i = 0; i < k; ++i)
         for (int l = 0; l < s; ++l) L.push_back(col(i, l));
       L.push_back(z);
-      launch_gram_list(c, g, L, {z}, partials, dl.Z(), halt, nullptr, "gram_z");
+      launch_gram_list(c, g, L, {z}, partials, dl.Z(), halt, zcond, zcond ? "gram_z_redo" : "gram_z");
     }
-    k_arn_s1<<<1, 256, 0, c.stream>>>(st, grams, k, rk, coef, partials, c.reduce_point(partials, g.G, dl.Z(), k * s + 1),
-                                      dl.Z(), s, cl.H(), scratch);
+    launch_k(c, k_arn_s1, 1, 256, 0, st, grams, k, rk, coef, partials, c.reduce_point(partials, g.G, dl.Z(), k * s + 1), dl.Z(), s, cl.H(), scratch);
     ++c.launches;
     // seed = z - sum_i V_i h_i ; ||seed||^2
     {
@@ -547,8 +612,7 @@ struct Engine {
       lb.add_dot(0, 0);
       lb.launch(c, g, coef, cl.size(), partials, dl.Seed(), halt, nullptr, "seed_update");
     }
-    k_arn_s2<<<1, 256, 0, c.stream>>>(st, k, rk, coef, partials, c.reduce_point(partials, g.G, dl.Seed(), 1),
-                                      dl.Seed(), cl.Inv());
+    launch_k(c, k_arn_s2, 1, 256, 0, st, k, rk, coef, partials, c.reduce_point(partials, g.G, dl.Seed(), 1), dl.Seed(), cl.Inv());
     ++c.launches;
     // candidate block [v, .., A^{s-1} v] of the normalized seed (also on the last block)
     const int cb = k;  // block slot k (slot m is scratch when k == m)
@@ -567,7 +631,7 @@ struct Engine {
         if (!have) {
           std::vector<const double*> L;
           for (int l = 0; l < s; ++l) L.push_back(col(0, l));
-          launch_gram_list(c, g, L, Cr, partials, dl.D(), halt, cond, "gram_mgs");
+          launch_gram_list(c, g, L, Cr, partials, dl.D(), halt, cond, pass ? "gram_mgs_reorth" : "gram_mgs");
         }
         for (int i = 0; i < k; ++i) {
           const int Gi = (i == 0 && have) ? Gfused : g.G;
@@ -584,24 +648,35 @@ struct Engine {
             Vn[l] = i + 1 < k ? col(i + 1, l) : nullptr;
             cd[l] = col(cb, l);
           }
-          launch_mgs(c, g, s, Vi, cd, i + 1 < k ? Vn : nullptr, sc, partials, dl.Dr(i + 1), halt, cond);
+          launch_mgs(c, g, s, Vi, cd, i + 1 < k ? Vn : nullptr, sc, partials, dl.Dr(i + 1), halt, cond,
+                     pass ? "mgs_update_reorth" : "mgs_update");
         }
         if (pass == 0) {
           // reorthogonalization test and the candidate's Gram matrix in one pass over cand:
-          // [V_0..V_{k-1}, cand]^T cand -> cross blocks, then W at Cross + k s^2
-          std::vector<const double*> L, Cc;
+          // [V_0..V_{k-1}, cand]^T cand -> cross blocks, then W at Cross + k s^2.  When the
+          // next block iteration follows, its z = A cand[:,s-1] is formed now and its Scalar1
+          // products [V_0..V_{k-1}, cand, z]^T z ride in the same pass (Z region).
+          std::vector<const double*> L, R;
+          std::vector<GramCol> cols;
           for (int i = 0; i < k; ++i)
             for (int l = 0; l < s; ++l) L.push_back(col(i, l));
-          for (int jc = 0; jc < s; ++jc) Cc.push_back(col(cb, jc));
-          for (int jc = 0; jc < s; ++jc) L.push_back(col(cb, jc));
-          launch_gram_list(c, g, L, Cc, partials, dl.Cross(), halt, nullptr, "gram_cross");
-          k_arn_check<<<1, 256, 0, c.stream>>>(st, grams, k, rk, partials,
-                                               c.reduce_point(partials, g.G, dl.Cross(), k * s * s + s * s), dl.Cross(),
-                                               dl.Cross() + k * s * s,
-                                               s, 1e-8, scratch);
+          for (int jc = 0; jc < s; ++jc) {
+            L.push_back(col(cb, jc));
+            R.push_back(col(cb, jc));
+            cols.push_back({dl.Cross() + jc, s, (k + 1) * s});
+          }
+          if (s + 1 <= GR_MAXR) {
+            apply(col(cb, s - 1), z);
+            L.push_back(z);
+            R.push_back(z);
+            cols.push_back({dl.Z(), 1, (k + 1) * s + 1});
+            zfused = true;
+          }
+          launch_gram_map(c, g, L, R, cols, partials, halt, nullptr, "gram_cross");
+          launch_k(c, k_arn_check, 1, 256, 0, st, grams, k, rk, partials, c.reduce_point(partials, g.G, dl.Cross(), k * s * s + s * s), dl.Cross(), dl.Cross() + k * s * s, s, 1e-8, scratch);
           ++c.launches;
         } else {
-          gram_self_into(cb, dl.Wb(), cond);
+          gram_self_into(cb, dl.Wb(), cond, "gram_w_reorth");
         }
       }
     }
@@ -611,7 +686,7 @@ struct Engine {
     // both regions global (the unused one is stale but harmless)
     // (for s > 1 the dWa region was already made global together with the cross products)
     const int Gw = s > 1 ? c.reduce_point(partials, g.G, dl.Wb(), s * s) : c.reduce_point(partials, g.G, dWa, s * s);
-    k_arn_push<<<1, 256, 0, c.stream>>>(st, grams, cb, rk, partials, Gw, dWa, dl.Wb(), s);
+    launch_k(c, k_arn_push, 1, 256, 0, st, grams, cb, rk, partials, Gw, dWa, dl.Wb(), s);
     ++c.launches;
     CK(cudaGetLastError());
   }
@@ -668,6 +743,7 @@ struct HostArn {
 
   // op counts of advance(k, build_next); stage: 0 = complete, 1 = invariant return,
   // 2 = push_block threw (counts through the Gram products)
+  mutable uint64_t reorth_passes = 0;  // diagnostics (SKC_TRACE)
   void count_advance(skc_op_counter& c, int k, bool build_next, int stage) const {
     const uint64_t S = s;
     add(c, (uint64_t)k * S + 1, 1, (uint64_t)k * S);  // z, Scalar1, seed, nu
@@ -679,6 +755,7 @@ struct HostArn {
       const double* r = rec(k);
       const int first = (int)r[RecLayout::kFirst];
       const bool reorth = r[RecLayout::kReorth] != 0.0;
+      if (reorth) ++reorth_passes;
       add(c, S + S * S * (uint64_t)(reorth ? first + 1 : k), 0, 0);
       if (reorth) add(c, (uint64_t)k * S * (S - 1), 0, (uint64_t)k * S * (S - 1));
     }
@@ -719,8 +796,7 @@ void sgmres_device(Ctx& c, const Op& op, const double* f, double* x, const SStep
     }
     lb.add_dot(0, 0);
     lb.launch(c, E.g, E.coef, E.cl.size(), E.partials, E.dl.RR(), nullptr, nullptr, "residual");
-    k_arn_rn<<<1, 256, 0, c.stream>>>(E.st, E.partials, c.reduce_point(E.partials, E.g.G, E.dl.RR(), 1), E.dl.RR(),
-                                      E.rn_out);
+    launch_k(c, k_arn_rn, 1, 256, 0, E.st, E.partials, c.reduce_point(E.partials, E.g.G, E.dl.RR(), 1), E.dl.RR(), E.rn_out);
     ++c.launches;
     double h;
     CK(cudaMemcpyAsync(&h, E.rn_out, sizeof h, cudaMemcpyDeviceToHost, c.stream));
@@ -757,8 +833,7 @@ void sgmres_device(Ctx& c, const Op& op, const double* f, double* x, const SStep
     std::string collapse_msg;
     int blocks_done = 0;
     // ---- enqueue the whole cycle, then read it back
-    E.ctor(E.r, true);
-    for (int k = 1; k <= m; ++k) E.advance(k, k < m);
+    E.enqueue_cycle();
     ArnState hs = E.read_state();
     CK(cudaMemcpy(H.recs.data(), E.rec, H.recs.size() * sizeof(double), cudaMemcpyDeviceToHost));
     H.gcols.clear();
@@ -873,6 +948,9 @@ void sgmres_device(Ctx& c, const Op& op, const double* f, double* x, const SStep
     }
   }
   rep.converged = rn <= cfg.tol;
+  if (std::getenv("SKC_TRACE"))
+    std::fprintf(stderr, "[skc] s-gmres: %llu cycles, %llu reorthogonalization passes\n",
+                 (unsigned long long)rep.cycles, (unsigned long long)H.reorth_passes);
   rep.final_residual = rep.history.back();
 }
 

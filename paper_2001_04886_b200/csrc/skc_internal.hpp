@@ -10,6 +10,7 @@
 #include <memory>
 #include <optional>
 #include <string>
+#include <utility>
 #include <vector>
 
 #include "../../include/skrylov_b200.h"
@@ -110,6 +111,10 @@ struct GramDesc {
   const double* R[GR_MAXR];
   double* partials;
   int dot0, G;
+  // optional per-column output map (mapped != 0): L[l] . R[r] goes to dot rbase[r] + l*rstride[r]
+  // and rows l >= lmax[r] are not stored; default: dot0 + l*nr + r
+  int mapped;
+  int rbase[GR_MAXR], rstride[GR_MAXR], lmax[GR_MAXR];
   int64_t n, range;
   const int* halt;
   const int* cond;
@@ -145,6 +150,7 @@ struct Ctx {
   cudaStream_t own_stream = nullptr;
   uint64_t launches = 0;
   bool profiling = false;
+  bool pdl = true;  // programmatic dependent launch for solver kernels (SKC_PDL=0 disables)
   std::map<std::string, KStat> stats;
   struct Pending {
     std::string name;
@@ -179,6 +185,24 @@ struct Ctx {
   ~Ctx();
 };
 
+// Kernel launch with programmatic dependent launch: the grid may be scheduled while the
+// previous kernel on the stream drains (its CTAs set up, then wait in SKC_PDL_ENTRY until the
+// previous grid has completed and its writes are visible), hiding the launch gap.
+template <typename... KArgs, typename... Args>
+inline void launch_k(Ctx& c, void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, Args&&... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = c.stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = c.pdl ? 1 : 0;
+  CK(cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...));
+}
+
 // RAII launch bracket
 struct Launch {
   Ctx& c;
@@ -202,7 +226,8 @@ int mpk_max_depth(const DevOp& op);
 constexpr int kMpkMaxDotDepth = 3;  // deepest sweep that can fuse products (launch_mpk)
 enum : uint8_t { kHintNormal = 0, kHintFirst = 1, kHintLast = 2 };  // L2 policies of streamed vectors
 int launch_mpk(Ctx& c, const DevOp& op, const double* src, const double* scale, double* const* out, int J, int nxd,
-               const double* const* X, int jdot0, double* partials, int dot0, const int* halt, const int* cond);
+               const double* const* X, int jdot0, double* partials, int dot0, const int* halt, const int* cond,
+               const char* name = "mpk");
 // One block-MGS round of s-step Arnoldi (Scalar2 + update, sstep.hpp:338-353).  The kernel
 // prologue is the round's scalar step, computed redundantly by every CTA: reduce the incoming
 // products V_i^T cand[:,1:] (partials `src` rows src_d0.., src_G columns, fixed order), solve
@@ -218,7 +243,8 @@ struct MgsScalar {
   int accumulate;
 };
 void launch_mgs(Ctx& c, const Geo& geo, int s, const double* const* Vi, double* const* cand, const double* const* Vnext,
-                const MgsScalar& sc, double* partials, int dot0, const int* halt, const int* cond);
+                const MgsScalar& sc, double* partials, int dot0, const int* halt, const int* cond,
+                const char* name = "mgs_update");
 // operator helpers
 void build_stencil_op(Ctx& c, Op& op, const skc_stencil_desc& d, const double* kcell_host);
 void build_csr_op(Ctx& c, Op& op, int64_t n, const uint64_t* offs, const uint64_t* cols, const double* vals);

@@ -136,6 +136,39 @@ inline void launch_gram_list(Ctx& c, const Geo& g, const std::vector<const doubl
   }
 }
 
+// Gram products with an explicit output map per right operand: L[l] . R[r] -> dot
+// col[r].base + l*col[r].stride for l < col[r].lmax (one pass over L and R).
+struct GramCol {
+  int base, stride, lmax;
+};
+inline void launch_gram_map(Ctx& c, const Geo& g, const std::vector<const double*>& L,
+                            const std::vector<const double*>& R, const std::vector<GramCol>& cols, double* partials,
+                            const int* halt, const int* cond, const char* name) {
+  require(!R.empty() && R.size() <= (size_t)GR_MAXR && cols.size() == R.size(), "gram: right operand count out of range");
+  for (size_t l0 = 0; l0 < L.size(); l0 += GR_MAXL) {
+    const size_t l1 = std::min(L.size(), l0 + (size_t)GR_MAXL);
+    GramDesc d;
+    std::memset(&d, 0, sizeof d);
+    d.nl = (int)(l1 - l0);
+    d.nr = (int)R.size();
+    for (size_t l = l0; l < l1; ++l) d.L[l - l0] = L[l];
+    d.mapped = 1;
+    for (size_t r = 0; r < R.size(); ++r) {
+      d.R[r] = R[r];
+      d.rbase[r] = cols[r].base + (int)l0 * cols[r].stride;
+      d.rstride[r] = cols[r].stride;
+      d.lmax[r] = std::max(0, cols[r].lmax - (int)l0);
+    }
+    d.partials = partials;
+    d.G = g.G;
+    d.n = g.n;
+    d.range = g.range;
+    d.halt = halt;
+    d.cond = cond;
+    launch_gram(c, d, name);
+  }
+}
+
 // x == 0 test on the device (initial_residual's is_zero, kernels.hpp:70-74)
 bool device_is_zero(Ctx& c, const double* x, int64_t n);
 

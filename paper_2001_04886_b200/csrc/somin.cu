@@ -52,6 +52,7 @@ __host__ __device__ constexpr int cMinus1(int s) { return 2 * s; }
 __host__ __device__ constexpr int cB(int s) { return 2 * s + 1; }
 
 __global__ void k_somin_start(SominState* st, const double* partials, int G, int d0) {
+  SKC_PDL_ENTRY();
   __shared__ double v[1];
   reduce_dots_dev(partials, G, d0, 1, v);
   if (threadIdx.x == 0) {
@@ -90,6 +91,7 @@ __device__ void somin_factor_solve(SominState* st, Gram* gslot, double* coef, co
 // setup: W0 = gram(AR0, AR0) (s*s dots, full), m0 = AR0^T r (s dots)
 __global__ void k_somin_setup(SominState* st, Gram* grams, double* coef, const double* partials, int G, int dW,
                               int dm, int s) {
+  SKC_PDL_ENTRY();
   if (st->halt) return;
   __shared__ double v[kMaxS * kMaxS + kMaxS];
   reduce_dots_dev(partials, G, dW, s * s, v);
@@ -110,6 +112,7 @@ __global__ void k_somin_setup(SominState* st, Gram* grams, double* coef, const d
 }
 
 __global__ void k_somin_norm(SominState* st, const double* partials, int G, int d0, double* hist) {
+  SKC_PDL_ENTRY();
   if (st->halt) return;
   __shared__ double v[1];
   reduce_dots_dev(partials, G, d0, 1, v);
@@ -135,6 +138,7 @@ __global__ void k_somin_norm(SominState* st, const double* partials, int G, int 
 // Scalar2 (sstep.hpp:204-214): b_e = -W_e^{-1} C_e for every window entry e
 __global__ void k_somin_proj(SominState* st, const Gram* grams, const __grid_constant__ Slots win, double* coef,
                              const double* partials, int G, int dC, int s, double* scratch) {
+  SKC_PDL_ENTRY();
   if (st->halt) return;
   reduce_dots_dev(partials, G, dC, win.n * s * s, scratch);
   for (int t = threadIdx.x; t < win.n * s; t += blockDim.x) {
@@ -151,6 +155,7 @@ __global__ void k_somin_proj(SominState* st, const Gram* grams, const __grid_con
 __global__ void k_somin_push(SominState* st, Gram* grams, int slot_new, double* coef, const double* partials, int G,
                              int dW, int dm, int s, int debug, const __grid_constant__ Slots win, int dX,
                              double* scratch) {
+  SKC_PDL_ENTRY();
   if (st->halt) return;
   const int ntri = s * (s + 1) / 2;
   reduce_dots_dev(partials, G, dW, ntri, scratch);
@@ -187,6 +192,7 @@ __global__ void k_somin_push(SominState* st, Gram* grams, int slot_new, double* 
 }
 
 __global__ void k_any_nonzero(const double* x, int64_t n, int* flag) {
+  SKC_PDL_ENTRY();
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
     if (x[i] != 0.0) {
       *flag = 1;
@@ -196,16 +202,17 @@ __global__ void k_any_nonzero(const double* x, int64_t n, int* flag) {
 
 }  // namespace
 
-__global__ void k_flag_to_partial(const int* flag, double* partials) { partials[0] = *flag ? 1.0 : 0.0; }
+__global__ void k_flag_to_partial(const int* flag, double* partials) {
+  SKC_PDL_ENTRY(); partials[0] = *flag ? 1.0 : 0.0; }
 
 bool device_is_zero(Ctx& c, const double* x, int64_t n) {
   int* flag = (int*)c.workspace("is_zero_flag", sizeof(int));
   CK(cudaMemsetAsync(flag, 0, sizeof(int), c.stream));
   ++c.launches;
-  k_any_nonzero<<<std::min<int64_t>(1184, (n + 255) / 256), 256, 0, c.stream>>>(x, n, flag);
+  launch_k(c, k_any_nonzero, std::min<int64_t>(1184, (n + 255) / 256), 256, 0, x, n, flag);
   CK(cudaGetLastError());
   double* p = (double*)c.workspace("is_zero_partial", sizeof(double) * kPartialPitch);
-  k_flag_to_partial<<<1, 1, 0, c.stream>>>(flag, p);
+  launch_k(c, k_flag_to_partial, 1, 1, 0, flag, p);
   const int G = c.reduce_point(p, 1, 0, 1);  // across ranks: every rank sees every flag
   std::vector<double> h(G);
   CK(cudaMemcpyAsync(h.data(), p, sizeof(double) * G, cudaMemcpyDeviceToHost, c.stream));
@@ -304,7 +311,7 @@ void somin_device(Ctx& c, const Op& op, const double* f, double* x, const SStepC
   // ---- initial residual (solvers.hpp:58-76) and setup (sstep.hpp:164-178)
   const bool x_zero = device_is_zero(c, x, n);
   initial_residual_dev(c, op, g, f, x, r, ax, x_zero, coef, ncoef, cMinus1(s), partials, dRR);
-  k_somin_start<<<1, 256, 0, c.stream>>>(st, partials, c.reduce_point(partials, g.G, dRR, 1), dRR);
+  launch_k(c, k_somin_start, 1, 256, 0, st, partials, c.reduce_point(partials, g.G, dRR, 1), dRR);
   ++c.launches;
   CK(cudaGetLastError());
   // krylov_pair(r): P0 = [r, Ar, .., A^{s-1} r], AP0 = [Ar, .., A^s r]
@@ -318,8 +325,7 @@ void somin_device(Ctx& c, const Op& op, const double* f, double* x, const SStepC
     for (int j = 0; j < s; ++j) L.push_back(slot_ap(0, j));
     launch_gram_list(c, g, L, L, partials, dW, halt, nullptr, "gram_w");
     launch_gram_list(c, g, L, {r}, partials, dM, halt, nullptr, "gram_m");
-    k_somin_setup<<<1, 256, 0, c.stream>>>(st, grams, coef, partials, c.reduce_point(partials, g.G, dW, s * s + s),
-                                           dW, dM, s);
+    launch_k(c, k_somin_setup, 1, 256, 0, st, grams, coef, partials, c.reduce_point(partials, g.G, dW, s * s + s), dW, dM, s);
     ++c.launches;
     CK(cudaGetLastError());
   }
@@ -348,7 +354,7 @@ void somin_device(Ctx& c, const Op& op, const double* f, double* x, const SStepC
         lb.add_dot(1, 1);
         lb.launch(c, g, coef, ncoef, partials, dRR, halt, nullptr, "xr_update");
       }
-      k_somin_norm<<<1, 256, 0, c.stream>>>(st, partials, c.reduce_point(partials, g.G, dRR, 1), dRR, hist);
+      launch_k(c, k_somin_norm, 1, 256, 0, st, partials, c.reduce_point(partials, g.G, dRR, 1), dRR, hist);
       ++c.launches;
       // krylov_pair(r) -> K[j] = A^{j+1} r  (matrix-powers sweep)
       powers(c, op, r, K, np, s, halt);
@@ -363,8 +369,7 @@ void somin_device(Ctx& c, const Op& op, const double* f, double* x, const SStepC
         for (int j = 0; j < s; ++j) R.push_back(K + (size_t)j * np);
         launch_gram_list(c, g, L, R, partials, dC, halt, nullptr, "gram_c");
       }
-      k_somin_proj<<<1, 256, 0, c.stream>>>(st, grams, ws, coef, partials,
-                                            c.reduce_point(partials, g.G, dC, ws.n * s * s), dC, s, scratch);
+      launch_k(c, k_somin_proj, 1, 256, 0, st, grams, ws, coef, partials, c.reduce_point(partials, g.G, dC, ws.n * s * s), dC, s, scratch);
       ++c.launches;
       // new slot: P = R + sum_e P_e b_e ; AP = AR + sum_e AP_e b_e ; W ; m  (sstep.hpp:215-222)
       if (free_slots.empty()) {  // s-GCR window at the device limit
@@ -397,8 +402,7 @@ void somin_device(Ctx& c, const Op& op, const double* f, double* x, const SStepC
       }
       int Gp = c.reduce_point(partials, g.G, dW, s * (s + 1) / 2 + s);
       if (cfg.debug_checks) Gp = c.reduce_point(partials, g.G, dX, ws.n * s * s);
-      k_somin_push<<<1, 256, 0, c.stream>>>(st, grams, nsl, coef, partials, Gp, dW, dW + s * (s + 1) / 2, s,
-                                            cfg.debug_checks ? 1 : 0, ws, dX, scratch);
+      launch_k(c, k_somin_push, 1, 256, 0, st, grams, nsl, coef, partials, Gp, dW, dW + s * (s + 1) / 2, s, cfg.debug_checks ? 1 : 0, ws, dX, scratch);
       ++c.launches;
       CK(cudaGetLastError());
       // deque bookkeeping (sstep.hpp:235-237)
@@ -476,6 +480,7 @@ struct SmrState {
 };
 
 __global__ void k_smr_start(SmrState* st, const double* partials, int G, int d0, double* hist) {
+  SKC_PDL_ENTRY();
   __shared__ double v[1];
   reduce_dots_dev(partials, G, d0, 1, v);
   if (threadIdx.x == 0) {
@@ -491,6 +496,7 @@ __global__ void k_smr_start(SmrState* st, const double* partials, int G, int d0,
 
 // W = gram_self(AR), m = AR^T r, a = W^{-1} m (sstep.hpp:96-101)
 __global__ void k_smr_solve(SmrState* st, double* coef, const double* partials, int G, int dW, int dm, int s) {
+  SKC_PDL_ENTRY();
   if (st->halt) return;
   __shared__ double v[kMaxS * kMaxS + kMaxS];
   reduce_dots_dev(partials, G, dW, s * s, v);
@@ -523,6 +529,7 @@ __global__ void k_smr_solve(SmrState* st, double* coef, const double* partials, 
 }
 
 __global__ void k_smr_norm(SmrState* st, const double* partials, int G, int d0, double* hist) {
+  SKC_PDL_ENTRY();
   if (st->halt) return;
   __shared__ double v[1];
   reduce_dots_dev(partials, G, d0, 1, v);
@@ -549,8 +556,7 @@ static void smr_step_enqueue(Ctx& c, const Op& op, const Geo& g, double* x, doub
   for (int j = 0; j < s; ++j) AR.push_back(K + (size_t)j * np);
   launch_gram_list(c, g, AR, AR, partials, 1, halt, nullptr, "gram_w");
   launch_gram_list(c, g, AR, {r}, partials, 1 + s * s, halt, nullptr, "gram_m");
-  k_smr_solve<<<1, 256, 0, c.stream>>>(st, coef, partials, c.reduce_point(partials, g.G, 1, s * s + s), 1,
-                                        1 + s * s, s);
+  launch_k(c, k_smr_solve, 1, 256, 0, st, coef, partials, c.reduce_point(partials, g.G, 1, s * s + s), 1, 1 + s * s, s);
   ++c.launches;
   // x += R a (R = [r, A r, .., A^{s-1} r]); r -= AR a  (sstep.hpp:102-103)
   LinBuilder lb;
@@ -561,7 +567,7 @@ static void smr_step_enqueue(Ctx& c, const Op& op, const Geo& g, double* x, doub
   for (int l = 0; l < s; ++l) lb.add_term(K + (size_t)l * np, 2u, s + l - 1);
   lb.add_dot(1, 1);
   lb.launch(c, g, coef, ncoef, partials, 0, halt, nullptr, "xr_update");
-  k_smr_norm<<<1, 256, 0, c.stream>>>(st, partials, c.reduce_point(partials, g.G, 0, 1), 0, hist);
+  launch_k(c, k_smr_norm, 1, 256, 0, st, partials, c.reduce_point(partials, g.G, 0, 1), 0, hist);
   ++c.launches;
   CK(cudaGetLastError());
 }
@@ -591,7 +597,7 @@ void smr_device(Ctx& c, const Op& op, const double* f, double* x, const SStepCfg
   }
   const bool x_zero = device_is_zero(c, x, n);
   initial_residual_dev(c, op, g, f, x, r, ax, x_zero, coef, ncoef, 2 * s, partials, 0);
-  k_smr_start<<<1, 256, 0, c.stream>>>(st, partials, c.reduce_point(partials, g.G, 0, 1), 0, hist);
+  launch_k(c, k_smr_start, 1, 256, 0, st, partials, c.reduce_point(partials, g.G, 0, 1), 0, hist);
   ++c.launches;
   uint64_t enq = 0;
   const uint64_t batch = n <= (1 << 16) ? 32 : 8;

@@ -66,7 +66,8 @@ struct GrmDesc {
   const double* U[GRM_MAXU];
   uint8_t li[GR_MAXL], ri[GR_MAXR];
   double* partials;
-  int dot0, G;
+  int G;
+  int rbase[GR_MAXR], rstride[GR_MAXR], lmax[GR_MAXR];  // output map (see GramDesc)
 };
 
 struct MgsDesc {
@@ -186,6 +187,7 @@ __device__ __forceinline__ void cta_store_partials(const double (&acc)[K], int n
 // ------------------------------------------------------------------ k_upd
 template <int NOUT, int MAXD, int PPT>
 __global__ void __launch_bounds__(THREADS) k_upd(const __grid_constant__ UpdDesc d) {
+  SKC_PDL_ENTRY();
   if (skip_launch(d.h.halt, d.h.cond)) return;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   const int coef_slots = (d.ncoef + 15) & ~15;
@@ -316,6 +318,7 @@ __device__ __forceinline__ void mgs_scalar(const MgsScalar& sc, double* cs, doub
 // U layout: [0,S) V_i ; [S, 2S-1) cand[1..S-1] ; [2S-1, 3S-1) V_{i+1} (DOTS)
 template <int S, bool DOTS>
 __global__ void __launch_bounds__(THREADS) k_mgs(const __grid_constant__ MgsDesc d) {
+  SKC_PDL_ENTRY();
   if (skip_launch(d.h.halt, d.h.cond)) return;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   constexpr int NC = S - 1;
@@ -383,6 +386,7 @@ __global__ void __launch_bounds__(THREADS) k_mgs(const __grid_constant__ MgsDesc
 // V_{i+1} column (S-1 accumulators per thread).  Partial layout as in k_mgs.
 template <int S>
 __global__ void __launch_bounds__(THREADS) k_mgs2(const __grid_constant__ MgsDesc d) {
+  SKC_PDL_ENTRY();
   static_assert(S <= NCW, "one warp per V_{i+1} column");
   if (skip_launch(d.h.halt, d.h.cond)) return;
   extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -446,6 +450,7 @@ __global__ void __launch_bounds__(THREADS) k_mgs2(const __grid_constant__ MgsDes
 // ------------------------------------------------------------------ k_grm
 template <int NR, int LB>
 __global__ void __launch_bounds__(THREADS) k_grm(const __grid_constant__ GrmDesc d) {
+  SKC_PDL_ENTRY();
   if (skip_launch(d.h.halt, d.h.cond)) return;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   Pipe p = pipe_setup(d.h, smem_raw, 0);
@@ -504,10 +509,10 @@ __global__ void __launch_bounds__(THREADS) k_grm(const __grid_constant__ GrmDesc
   for (int e = threadIdx.x; e < nch * K; e += blockDim.x) {
     const int ch = e / K, k = e % K, lb = k / NR, r = k % NR;
     const int l = ch * LB + lb;
-    if (l < d.nl) {  // rows past nl in the last chunk duplicated row 0: discarded
+    if (l < d.nl && l < d.lmax[r]) {  // rows past nl in the last chunk duplicated row 0: discarded
       double s = 0.0;
       for (int gp = 0; gp < PG; ++gp) s += red[((size_t)gp * nch + ch) * K + k];
-      d.partials[(int64_t)(d.dot0 + l * NR + r) * kPartialPitch + blockIdx.x] = s;
+      d.partials[(int64_t)(d.rbase[r] + l * d.rstride[r]) * kPartialPitch + blockIdx.x] = s;
     }
   }
 }
@@ -552,7 +557,7 @@ template <int NOUT, int MAXD, int PPT>
 void launch_upd_t(Ctx& c, const UpdDesc& d, size_t smem, int G) {
   static bool attr = false;
   if (!attr) allow_smem(k_upd<NOUT, MAXD, PPT>), attr = true;
-  k_upd<NOUT, MAXD, PPT><<<G, THREADS, smem, c.stream>>>(d);
+  launch_k(c, k_upd<NOUT, MAXD, PPT>, G, THREADS, smem, d);
 }
 
 template <int NOUT, int PPT>
@@ -578,7 +583,7 @@ template <int NR, int LB>
 void launch_grm_t(Ctx& c, const GrmDesc& d, size_t smem, int G) {
   static bool attr = false;
   if (!attr) allow_smem(k_grm<NR, LB>), attr = true;
-  k_grm<NR, LB><<<G, THREADS, smem, c.stream>>>(d);
+  launch_k(c, k_grm<NR, LB>, G, THREADS, smem, d);
 }
 
 // LB = ceil(nl / 8) rows per warp so all eight consumer warps carry a share of the rows
@@ -601,11 +606,11 @@ void launch_mgs_t(Ctx& c, const MgsDesc& d, size_t smem, int G) {
   if constexpr (DOTS && S >= 6) {
     static bool attr = false;
     if (!attr) allow_smem(k_mgs2<S>), attr = true;
-    k_mgs2<S><<<G, THREADS, smem, c.stream>>>(d);
+    launch_k(c, k_mgs2<S>, G, THREADS, smem, d);
   } else {
     static bool attr = false;
     if (!attr) allow_smem(k_mgs<S, DOTS>), attr = true;
-    k_mgs<S, DOTS><<<G, THREADS, smem, c.stream>>>(d);
+    launch_k(c, k_mgs<S, DOTS>, G, THREADS, smem, d);
   }
 }
 
@@ -694,9 +699,13 @@ void launch_gram(Ctx& c, const GramDesc& g, const char* name) {
   d.nl = g.nl;
   d.nr = g.nr;
   for (int l = 0; l < g.nl; ++l) d.li[l] = (uint8_t)add_unique(d.U, nu, GRM_MAXU, g.L[l]);
-  for (int r = 0; r < g.nr; ++r) d.ri[r] = (uint8_t)add_unique(d.U, nu, GRM_MAXU, g.R[r]);
+  for (int r = 0; r < g.nr; ++r) {
+    d.ri[r] = (uint8_t)add_unique(d.U, nu, GRM_MAXU, g.R[r]);
+    d.rbase[r] = g.mapped ? g.rbase[r] : g.dot0 + r;
+    d.rstride[r] = g.mapped ? g.rstride[r] : g.nr;
+    d.lmax[r] = g.mapped ? g.lmax[r] : g.nl;
+  }
   d.partials = g.partials;
-  d.dot0 = g.dot0;
   d.G = g.G;
   TileChoice tc = pick_tiles(nu, 0, 2048, 64);
   const size_t red = 64 + (size_t)NCW * 8 * GR_MAXR * 8;
@@ -718,7 +727,8 @@ void launch_gram(Ctx& c, const GramDesc& g, const char* name) {
 }
 
 void launch_mgs(Ctx& c, const Geo& geo, int s, const double* const* Vi, double* const* cand, const double* const* Vnext,
-                const MgsScalar& sc, double* partials, int dot0, const int* halt, const int* cond) {
+                const MgsScalar& sc, double* partials, int dot0, const int* halt, const int* cond,
+                const char* name) {
   require(s >= 2 && s <= kMaxS, "mgs: s out of range");
   MgsDesc d;
   std::memset(&d, 0, sizeof d);
@@ -739,7 +749,7 @@ void launch_mgs(Ctx& c, const Geo& geo, int s, const double* const* Vi, double* 
   tc.smem = std::max(tc.smem, 64 + (size_t)kMgsPrefix + 8 * (size_t)NCW * 56);
   fill_hdr(d.h, nu, tc, geo.n, geo.range, halt, cond);
   const double bytes = 8.0 * (double)geo.n * (nu + s - 1);
-  Launch lh(c, "mgs_update", bytes);
+  Launch lh(c, name, bytes);
 #define SKC_MGS_CASE(SV)                                                \
   case SV:                                                              \
     if (dots)                                                           \
