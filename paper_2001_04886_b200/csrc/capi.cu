@@ -89,6 +89,7 @@ skc_ctx* make_ctx(int device) {
   CK(cudaStreamCreateWithFlags(&ctx->c.own_stream, cudaStreamNonBlocking));
   ctx->c.stream = ctx->c.own_stream;
   if (const char* e = std::getenv("SKC_PDL")) ctx->c.pdl = std::atoi(e) != 0;
+  if (const char* e = std::getenv("SKC_ORTH")) ctx->c.orth = std::atoi(e) != 0;
   return ctx;
 }
 

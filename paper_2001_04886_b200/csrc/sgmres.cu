@@ -11,6 +11,8 @@
 // reconstruction (append_g_columns), cholesky_upper of each Gram block, the Givens
 // least-squares update and the early-exit/collapse/fallback decisions, exactly in the
 // reference's order.  A second short enqueue applies x += V y and recomputes r = f - A x.
+#include <cooperative_groups.h>
+
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -203,6 +205,326 @@ __global__ void k_arn_check(ArnState* st, const Gram* grams, int k, double* rec,
     rec[RecLayout::kReorth] = first >= 0 ? 1.0 : 0.0;
     st->reorth = first >= 0;
   }
+}
+
+// ---------------------------------------------------------------- on-chip block orthogonalization
+// One cooperative kernel for the whole block-MGS stage of a block iteration (sstep.hpp:331-379)
+// when the candidate columns cand[:,1:] of every CTA's point slice fit in its shared memory:
+// one CTA per SM owns points [b*P, (b+1)*P) and keeps its slice of cand[:,1:] on chip for
+//   pass 0: k rounds  (Scalar2 solve in every CTA, cand -= V_i t, products V_{i+1}^T cand),
+//   the cross products [V_0..V_{k-1}, cand]^T cand and the reorthogonalization test,
+//   pass 1 (only when the test fires): V_0^T cand, k more rounds (t accumulated), W = cand^T cand,
+// separated by grid-wide barriers; cand[:,1:] is written back once at the end.  Only the basis
+// blocks stream from memory.  Every CTA reduces the per-CTA partials in the same fixed order,
+// so all CTAs take identical coefficients and the same reorthogonalization decision; CTA 0
+// writes the records and the device flags.
+constexpr int ORTH_NT = 512;
+constexpr size_t kOrthSmemCap = 220 * 1024;  // <= the 226 KB dynamic limit set at launch
+// reduced-product capacity: the cross test needs (k+1) s^2, a round s(s-1); even count keeps
+// the Gram copy 16-byte aligned
+__host__ __device__ inline int orth_prod_cap(int k, int s) { return ((k + 1) * s * s + 1) & ~1; }
+
+struct OrthDesc {
+  int s, k;
+  int64_t n, P;           // points, points per CTA
+  const double* V;        // basis: block i column l at V + (i*s + l)*np
+  int64_t np;
+  const double* cand0;    // candidate column 0 (read only)
+  double* cand[kMaxS];    // candidate columns 1..s-1 (written back)
+  double* partials;
+  int src_G0;             // partial columns of the incoming round-0 products
+  int dr0, dr1, dcross, dwb;
+  const Gram* grams;
+  double* rec;            // this block iteration's record
+  int rec_t;
+  ArnState* st;
+  double orth_tol;
+  unsigned long long* trace;  // optional phase timestamps (CTA 0), diagnostics
+};
+
+__device__ __forceinline__ void orth_mark(const OrthDesc& d, int slot) {
+  if (d.trace && blockIdx.x == 0 && threadIdx.x == 0) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    d.trace[slot] = t;
+  }
+}
+
+// fixed-order CTA reduction of K per-thread accumulators into partial column blockIdx.x
+template <int K>
+__device__ __forceinline__ void orth_store(const double (&acc)[K], double* red, double* partials, int d0) {
+  constexpr int NW = ORTH_NT / 32;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int q = 0; q < K; ++q) {
+    const double v = warp_sum(acc[q]);
+    if (lane == 0) red[warp * K + q] = v;
+  }
+  __syncthreads();
+  if (threadIdx.x < K) {
+    double s = 0.0;
+    for (int w = 0; w < NW; ++w) s += red[w * K + threadIdx.x];
+    partials[(int64_t)(d0 + threadIdx.x) * kPartialPitch + blockIdx.x] = s;
+  }
+  __syncthreads();
+}
+
+template <int S>
+__global__ void __launch_bounds__(ORTH_NT, 1) k_orth(const __grid_constant__ OrthDesc d) {
+  SKC_PDL_ENTRY();
+  if (__ldg(&d.st->halt)) return;  // block-uniform, before any barrier
+  namespace cg = cooperative_groups;
+  cg::grid_group grid = cg::this_grid();
+  constexpr int NC = S - 1;
+  extern __shared__ __align__(16) double dsm[];
+  // coefficients -t [64] | reduced products [(k+1) s^2] | Gram copy | reduction scratch
+  // [32 warps][s^2] | candidate slice [s-1][P]
+  double* tc = dsm;
+  double* prod = dsm + 64;
+  Gram* gs = reinterpret_cast<Gram*>(prod + orth_prod_cap(d.k, S));
+  double* red = reinterpret_cast<double*>(gs + 1);
+  double* sc = red + (ORTH_NT / 32) * S * S;
+  __shared__ int exceed[64];
+  __shared__ int s_first;
+  const int tid = threadIdx.x;
+  const int64_t base = (int64_t)blockIdx.x * d.P;
+  const int64_t rem = d.n - base;
+  const int cnt = rem <= 0 ? 0 : (int)(rem < d.P ? rem : d.P);
+  const int G = gridDim.x;
+  auto colp = [&](int i, int l) { return d.V + ((int64_t)i * S + l) * d.np + base; };
+
+  // load this CTA's slice of cand[:,1:]
+  for (int j = 0; j < NC; ++j)
+    for (int p = tid; p < cnt; p += ORTH_NT) sc[(int64_t)j * d.P + p] = d.cand[j][base + p];
+
+  // Scalar2 for block i from partials (src, srcG): every CTA solves W_i t = V_i^T cand[:,1:]
+  auto scalar = [&](int i, int src, int srcG, int accumulate) {
+    {
+      const uint64_t* gsrc = reinterpret_cast<const uint64_t*>(d.grams + i);
+      uint64_t* gdst = reinterpret_cast<uint64_t*>(gs);
+      for (int w = tid; w < (int)(sizeof(Gram) / 8); w += ORTH_NT) gdst[w] = gsrc[w];
+    }
+    reduce_dots_dev(d.partials, srcG, src, S * NC, prod);  // ends with __syncthreads
+    if (tid < NC) {
+      const int jc = tid;
+      double rhs[kMaxS], t[kMaxS];
+#pragma unroll
+      for (int l = 0; l < S; ++l) rhs[l] = prod[l * NC + jc];
+      gram_solve(*gs, rhs, t);
+#pragma unroll
+      for (int l = 0; l < S; ++l) {
+        tc[l * NC + jc] = -t[l];
+        if (blockIdx.x == 0) {
+          double* ta = d.rec + d.rec_t + i * S * S + l * S + (jc + 1);
+          *ta = accumulate ? *ta + t[l] : t[l];
+        }
+      }
+    }
+    __syncthreads();
+  };
+
+  // cand[:,1:] -= V_i t ; products V_{i+1}^T cand[:,1:] -> partials dst (when i+1 < k).
+  // Points go in pairs (p, p + NT) with every basis load of the pair issued before the
+  // arithmetic, so each thread keeps 2s (4s with the products) loads in flight; the products
+  // still accumulate in ascending point order.
+  auto round = [&](int i, int dst) {
+    const bool dots = i + 1 < d.k;
+    const double* Vi = colp(i, 0);
+    const double* Vn = colp(dots ? i + 1 : i, 0);
+    const int64_t np = d.np;
+    double acc[S * NC];
+#pragma unroll
+    for (int q = 0; q < S * NC; ++q) acc[q] = 0.0;
+    for (int p0 = tid; p0 < cnt; p0 += 2 * ORTH_NT) {
+      const int p1 = p0 + ORTH_NT;
+      const bool has1 = p1 < cnt;
+      double v0[S], v1[S], w0[S], w1[S];
+#pragma unroll
+      for (int l = 0; l < S; ++l) {
+        v0[l] = Vi[l * np + p0];
+        v1[l] = has1 ? Vi[l * np + p1] : 0.0;
+        w0[l] = dots ? Vn[l * np + p0] : 0.0;
+        w1[l] = dots && has1 ? Vn[l * np + p1] : 0.0;
+      }
+      double c0[NC], c1[NC];
+#pragma unroll
+      for (int j = 0; j < NC; ++j) {
+        c0[j] = sc[(int64_t)j * d.P + p0];
+        c1[j] = has1 ? sc[(int64_t)j * d.P + p1] : 0.0;
+      }
+#pragma unroll
+      for (int l = 0; l < S; ++l)
+#pragma unroll
+        for (int j = 0; j < NC; ++j) {
+          const double t = tc[l * NC + j];
+          c0[j] = dadd(c0[j], dmul(t, v0[l]));
+          c1[j] = dadd(c1[j], dmul(t, v1[l]));
+        }
+#pragma unroll
+      for (int j = 0; j < NC; ++j) {
+        sc[(int64_t)j * d.P + p0] = c0[j];
+        if (has1) sc[(int64_t)j * d.P + p1] = c1[j];
+      }
+      if (dots) {
+#pragma unroll
+        for (int l = 0; l < S; ++l)
+#pragma unroll
+          for (int j = 0; j < NC; ++j) acc[l * NC + j] = fma(w0[l], c0[j], acc[l * NC + j]);
+        if (has1) {
+#pragma unroll
+          for (int l = 0; l < S; ++l)
+#pragma unroll
+            for (int j = 0; j < NC; ++j) acc[l * NC + j] = fma(w1[l], c1[j], acc[l * NC + j]);
+        }
+      }
+    }
+    if (dots) orth_store(acc, red, d.partials, dst);
+  };
+
+  // L-block products with the full candidate: lhs(l) . cand[:,jc] for one block of s columns
+  // (block i of the basis, or the candidate itself when i == k) -> partials d0 + l*s + jc
+  auto cross_block = [&](int i, int d0) {
+    double acc[S * S];
+#pragma unroll
+    for (int q = 0; q < S * S; ++q) acc[q] = 0.0;
+    const double* c0p = d.cand0 + base;
+    const bool basis = i < d.k;
+    const double* Li = basis ? colp(i, 0) : c0p;
+    const int64_t np = d.np;
+    for (int p0 = tid; p0 < cnt; p0 += 2 * ORTH_NT) {
+      const int p1 = p0 + ORTH_NT;
+      const bool has1 = p1 < cnt;
+      double a0[S], a1[S], b0[S], b1[S];
+      b0[0] = c0p[p0];
+      b1[0] = has1 ? c0p[p1] : 0.0;
+#pragma unroll
+      for (int l = 0; l < S; ++l) {
+        a0[l] = basis ? Li[l * np + p0] : 0.0;
+        a1[l] = basis && has1 ? Li[l * np + p1] : 0.0;
+      }
+#pragma unroll
+      for (int j = 1; j < S; ++j) {
+        b0[j] = sc[(int64_t)(j - 1) * d.P + p0];
+        b1[j] = has1 ? sc[(int64_t)(j - 1) * d.P + p1] : 0.0;
+      }
+      if (!basis) {
+#pragma unroll
+        for (int l = 0; l < S; ++l) a0[l] = b0[l], a1[l] = b1[l];
+      }
+#pragma unroll
+      for (int l = 0; l < S; ++l)
+#pragma unroll
+        for (int jc = 0; jc < S; ++jc) acc[l * S + jc] = fma(a0[l], b0[jc], acc[l * S + jc]);
+      if (has1) {
+#pragma unroll
+        for (int l = 0; l < S; ++l)
+#pragma unroll
+          for (int jc = 0; jc < S; ++jc) acc[l * S + jc] = fma(a1[l], b1[jc], acc[l * S + jc]);
+      }
+    }
+    orth_store(acc, red, d.partials, d0);
+  };
+
+  const int K = d.k;
+  orth_mark(d, 0);
+  // ---- pass 0 (round 0 products arrive from the powers sweep or a Gram launch)
+  for (int i = 0; i < K; ++i) {
+    scalar(i, (i & 1) ? d.dr1 : d.dr0, i == 0 ? d.src_G0 : G, 0);
+    orth_mark(d, 8 + 3 * i);
+    round(i, ((i + 1) & 1) ? d.dr1 : d.dr0);
+    orth_mark(d, 9 + 3 * i);
+    if (i + 1 < K) grid.sync();
+    orth_mark(d, 10 + 3 * i);
+  }
+  // ---- cross products and W (needs_reorth, sstep.hpp:401-414)
+  for (int i = 0; i <= K; ++i) cross_block(i, d.dcross + i * S * S);
+  orth_mark(d, 1);
+  grid.sync();
+  orth_mark(d, 2);
+  reduce_dots_dev(d.partials, G, d.dcross, (K + 1) * S * S, prod);
+  {
+    const double* sW = prod + K * S * S;
+    double cn2 = 0.0;
+    for (int jc = 0; jc < S; ++jc) cn2 += sW[jc * S + jc];
+    for (int i = tid; i < K; i += ORTH_NT) {
+      const double* cr = prod + i * S * S;
+      double acc = 0.0;
+      for (int q = 0; q < S * S; ++q) acc += cr[q] * cr[q];
+      exceed[i] = sqrt(acc) > d.orth_tol * sqrt(sd_trace(d.grams[i].w, S)) * sqrt(cn2);
+    }
+    __syncthreads();
+    if (tid == 0) {
+      int first = -1;
+      for (int i = 0; i < K; ++i)
+        if (exceed[i]) {
+          first = i;
+          break;
+        }
+      s_first = first;
+      if (blockIdx.x == 0) {
+        d.rec[RecLayout::kFirst] = first;
+        d.rec[RecLayout::kReorth] = first >= 0 ? 1.0 : 0.0;
+        d.st->reorth = first >= 0;
+      }
+    }
+    __syncthreads();
+  }
+  orth_mark(d, 3);
+  if (s_first >= 0) {
+    // ---- pass 1: V_0^T cand[:,1:], k rounds with t accumulated, then W of the new candidate
+    {
+      double acc[S * NC];
+#pragma unroll
+      for (int q = 0; q < S * NC; ++q) acc[q] = 0.0;
+      const double* V0[S];
+#pragma unroll
+      for (int l = 0; l < S; ++l) V0[l] = colp(0, l);
+      for (int p = tid; p < cnt; p += ORTH_NT) {
+#pragma unroll
+        for (int l = 0; l < S; ++l) {
+          const double lv = V0[l][p];
+#pragma unroll
+          for (int j = 0; j < NC; ++j) acc[l * NC + j] = fma(lv, sc[(int64_t)j * d.P + p], acc[l * NC + j]);
+        }
+      }
+      orth_store(acc, red, d.partials, d.dr0);
+    }
+    grid.sync();
+    for (int i = 0; i < K; ++i) {
+      scalar(i, (i & 1) ? d.dr1 : d.dr0, G, 1);
+      round(i, ((i + 1) & 1) ? d.dr1 : d.dr0);
+      if (i + 1 < K) grid.sync();
+    }
+    cross_block(K, d.dwb);
+  }
+  orth_mark(d, 4);
+  // write the candidate columns back
+  for (int j = 0; j < NC; ++j)
+    for (int p = tid; p < cnt; p += ORTH_NT) d.cand[j][base + p] = sc[(int64_t)j * d.P + p];
+  orth_mark(d, 5);
+}
+
+size_t orth_smem(int s, int k, int64_t P) {
+  return sizeof(double) * (64 + (size_t)orth_prod_cap(k, s)) + sizeof(Gram) + sizeof(double) * (ORTH_NT / 32) * s * s +
+         sizeof(double) * (size_t)(s - 1) * (size_t)P;
+}
+
+template <int S>
+void run_orth(Ctx& c, const OrthDesc& d, int G, size_t smem) {
+  static bool attr = false;
+  // (227 KB per block less the kernel's static shared memory)
+  if (!attr) CK(cudaFuncSetAttribute(k_orth<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, 226 * 1024)), attr = true;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = G;
+  cfg.blockDim = ORTH_NT;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = c.stream;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeCooperative;
+  at[0].val.cooperative = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  CK(cudaLaunchKernelEx(&cfg, k_orth<S>, d));
 }
 
 // r-norm after the cycle's residual update
@@ -455,6 +777,68 @@ struct Engine {
     if (cycle_exec) cudaGraphExecDestroy(cycle_exec);
   }
 
+  // points per CTA of the on-chip orthogonalization (one CTA per SM), or 0 when it is off or
+  // the candidate slices do not fit in shared memory
+  int64_t orth_points() const {
+    if (!c.orth || c.world() != 1 || s < 2) return 0;
+    const int64_t P = ((op.n + c.sm_count - 1) / c.sm_count + 1) & ~(int64_t)1;
+    return orth_smem(s, m, P) <= kOrthSmemCap ? P : 0;
+  }
+
+  // the block-MGS stage of block iteration k in one cooperative kernel; returns the partial
+  // column count of the products it leaves (cross, W, Wb)
+  int launch_orth(int k, int cb, int G0) {
+    OrthDesc d;
+    std::memset(&d, 0, sizeof d);
+    d.s = s;
+    d.k = k;
+    d.n = op.n;
+    d.P = orth_points();
+    d.V = V;
+    d.np = np;
+    d.cand0 = col(cb, 0);
+    for (int j = 1; j < s; ++j) d.cand[j - 1] = col(cb, j);
+    d.partials = partials;
+    d.src_G0 = G0;
+    d.dr0 = dl.Dr(0);
+    d.dr1 = dl.Dr(1);
+    d.dcross = dl.Cross();
+    d.dwb = dl.Wb();
+    d.grams = grams;
+    d.rec = recp(k);
+    d.rec_t = rl.t();
+    d.st = st;
+    d.orth_tol = 1e-8;
+    static const bool trace = std::getenv("SKC_TRACE_ORTH") != nullptr;
+    if (trace) d.trace = (unsigned long long*)c.workspace("orth_trace", 256 * sizeof(unsigned long long));
+    const int G = c.sm_count;
+    const size_t smem = orth_smem(s, k, d.P);
+    // algorithmic bytes of pass 0 + the cross products (pass 1 is data dependent)
+    const double bytes = 8.0 * (double)op.n * ((2.0 * k - 1.0) * s + (double)k * s + (k + 1) + 2.0 * (s - 1));
+    Launch lh(c, "orth", bytes);
+    switch (s) {
+      case 2: run_orth<2>(c, d, G, smem); break;
+      case 3: run_orth<3>(c, d, G, smem); break;
+      case 4: run_orth<4>(c, d, G, smem); break;
+      case 5: run_orth<5>(c, d, G, smem); break;
+      case 6: run_orth<6>(c, d, G, smem); break;
+      case 7: run_orth<7>(c, d, G, smem); break;
+      default: run_orth<8>(c, d, G, smem); break;
+    }
+    if (trace) {
+      unsigned long long t[256];
+      CK(cudaMemcpyAsync(t, d.trace, sizeof t, cudaMemcpyDeviceToHost, c.stream));
+      c.sync();
+      std::fprintf(stderr, "[orth k=%d] rounds:", k);
+      for (int i = 0; i < k; ++i)
+        std::fprintf(stderr, " (scal %.1f, upd %.1f, sync %.1f)", (t[8 + 3 * i] - (i ? t[7 + 3 * i] : t[0])) * 1e-3,
+                     (t[9 + 3 * i] - t[8 + 3 * i]) * 1e-3, (t[10 + 3 * i] - t[9 + 3 * i]) * 1e-3);
+      std::fprintf(stderr, " | cross %.1f sync %.1f check %.1f pass1 %.1f write %.1f us\n", (t[1] - t[7 + 3 * k]) * 1e-3,
+                   (t[2] - t[1]) * 1e-3, (t[3] - t[2]) * 1e-3, (t[4] - t[3]) * 1e-3, (t[5] - t[4]) * 1e-3);
+    }
+    return G;
+  }
+
   void enqueue_cycle_direct() {
     ctor(r, true);
     for (int k = 1; k <= m; ++k) advance(k, k < m);
@@ -622,7 +1006,19 @@ struct Engine {
       return;
     }
     double* tk = rk + rl.t();
-    if (s > 1) {
+    int Gorth = 0;
+    if (s > 1 && orth_points() > 0) {
+      // whole block-MGS stage on chip; round-0 products from the powers sweep or a Gram pass
+      int G0 = Gfused;
+      if (G0 == 0) {
+        std::vector<const double*> L, Cr;
+        for (int l = 0; l < s; ++l) L.push_back(col(0, l));
+        for (int jc = 1; jc < s; ++jc) Cr.push_back(col(cb, jc));
+        launch_gram_list(c, g, L, Cr, partials, dl.D(), halt, nullptr, "gram_mgs");
+        G0 = g.G;
+      }
+      Gorth = launch_orth(k, cb, G0);
+    } else if (s > 1) {
       for (int pass = 0; pass < 2; ++pass) {
         const int* cond = pass ? &st->reorth : nullptr;
         std::vector<const double*> Cr;
@@ -685,7 +1081,9 @@ struct Engine {
     // the push reads W from the reorthogonalized region when the device flag says so: make
     // both regions global (the unused one is stale but harmless)
     // (for s > 1 the dWa region was already made global together with the cross products)
-    const int Gw = s > 1 ? c.reduce_point(partials, g.G, dl.Wb(), s * s) : c.reduce_point(partials, g.G, dWa, s * s);
+    const int Gw = Gorth > 0 ? Gorth
+                   : s > 1  ? c.reduce_point(partials, g.G, dl.Wb(), s * s)
+                            : c.reduce_point(partials, g.G, dWa, s * s);
     launch_k(c, k_arn_push, 1, 256, 0, st, grams, cb, rk, partials, Gw, dWa, dl.Wb(), s);
     ++c.launches;
     CK(cudaGetLastError());

@@ -150,7 +150,8 @@ struct Ctx {
   cudaStream_t own_stream = nullptr;
   uint64_t launches = 0;
   bool profiling = false;
-  bool pdl = true;  // programmatic dependent launch for solver kernels (SKC_PDL=0 disables)
+  bool pdl = true;   // programmatic dependent launch for solver kernels (SKC_PDL=0 disables)
+  bool orth = true;  // on-chip block orthogonalization when it fits (SKC_ORTH=0 disables)
   std::map<std::string, KStat> stats;
   struct Pending {
     std::string name;

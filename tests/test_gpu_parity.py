@@ -73,7 +73,20 @@ def test_solve_matches_reference(ctx, port, name, prefer_stencil):
     meta = MANIFEST[name]
     if not prefer_stencil and "stencil" not in meta:
         pytest.skip("case has no stencil form")
-    meta, arr, rep, x, op = run_gpu_case(ctx, name, prefer_stencil)
+    _check_case(port, name, *run_gpu_case(ctx, name, prefer_stencil))
+
+
+@pytest.mark.parametrize("name", [n for n in SOLVE_CASES if MANIFEST[n]["method"] == "sgmres"])
+def test_sgmres_per_round_kernel_path(port, name, monkeypatch):
+    """The per-round block-MGS kernels (taken when the candidate block does not fit in shared
+    memory, and across GPUs) against the reference on the same cases; small problems otherwise
+    run the on-chip orthogonalization kernel."""
+    from paper_2001_04886_b200 import Context
+    monkeypatch.setenv("SKC_ORTH", "0")
+    _check_case(port, name, *run_gpu_case(Context(0), name, True))
+
+
+def _check_case(port, name, meta, arr, rep, x, op):
     _check_structure(meta, arr, rep, chaotic=name in CHAOTIC)
     env = ENVELOPE[name]
     h = rel_hist(rep.residual_history, arr["history"])
