@@ -525,19 +525,29 @@ struct TileChoice {
 
 // Tile size / stage count: >= 3 stages where possible, then large tiles, preferring a
 // footprint that lets two CTAs share an SM.  `align` = tile granularity (points).
-TileChoice pick_tiles(int nu, size_t prefix, int Tmax, int Tmin, bool fine = true) {
+bool try_pick_tiles(int nu, size_t prefix, int Tmax, int Tmin, bool fine, TileChoice& out) {
   for (size_t limit : {(size_t)110 * 1024, (size_t)220 * 1024}) {
     for (int ns : {3, 4, 2}) {
       for (int T2 = 2 * Tmax; T2 >= 2 * Tmin; T2 /= 2) {
         for (int T : {T2 / 2 + T2 / 4, T2 / 2}) {  // 3/4 and 1/2 of T2: 1536, 1024, .., 96, 64
           if (T > Tmax || T < Tmin || (!fine && T != T2 / 2)) continue;
           const size_t need = 64 + prefix + (size_t)ns * nu * T * 8;
-          if (need <= limit) return {T, ns, need};
+          if (need <= limit) {
+            out = {T, ns, need};
+            return true;
+          }
         }
       }
     }
   }
-  fail(SKC_EINVAL, "streaming kernel: too many operand vectors for shared-memory staging");
+  return false;
+}
+
+TileChoice pick_tiles(int nu, size_t prefix, int Tmax, int Tmin, bool fine = true) {
+  TileChoice tc;
+  if (!try_pick_tiles(nu, prefix, Tmax, Tmin, fine, tc))
+    fail(SKC_EINVAL, "streaming kernel: too many operand vectors for shared-memory staging");
+  return tc;
 }
 
 int add_unique(const double** U, int& nu, int cap, const double* p) {
@@ -674,8 +684,12 @@ void launch_lincomb(Ctx& c, const LinDesc& L, const char* name) {
   d.dot0 = L.dot0;
   d.G = L.G;
   const size_t prefix = 8 * ((size_t)((L.ncoef + 15) & ~15) + (maxd ? (size_t)(nout_t + LC_MAXX) * CONS : 0));
-  // k_upd covers T <= CONS * PPT points per tile: powers of two only
-  const TileChoice tc = pick_tiles(nu, prefix, nout_t <= 8 ? 2 * CONS : CONS, 64, false);
+  // k_upd covers T <= CONS * PPT points per tile (powers of two only).  A tile of at least CONS
+  // points keeps every consumer thread busy (one point each) -- worth one CTA per SM with
+  // fewer stages for wide updates (the seed and x updates stream up to 4 + m s vectors).
+  TileChoice tc;
+  const int Tmax = nout_t <= 8 ? 2 * CONS : CONS;
+  if (!try_pick_tiles(nu, prefix, Tmax, CONS, false, tc)) tc = pick_tiles(nu, prefix, Tmax, 64, false);
   fill_hdr(d.h, nu, tc, L.n, L.range, L.halt, L.cond);
   const double bytes = 8.0 * (double)L.n * (nu + L.nout);
   Launch lh(c, name, bytes);
