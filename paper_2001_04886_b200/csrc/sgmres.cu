@@ -219,6 +219,8 @@ __global__ void k_arn_check(ArnState* st, const Gram* grams, int k, double* rec,
 // so all CTAs take identical coefficients and the same reorthogonalization decision; CTA 0
 // writes the records and the device flags.
 constexpr int ORTH_NT = 512;
+// points per thread per iteration, all their loads issued first (MGS update / cross products)
+constexpr int ORTH_UU = 2, ORTH_UC = 4;
 constexpr size_t kOrthSmemCap = 220 * 1024;  // <= the 226 KB dynamic limit set at launch
 // reduced-product capacity: the cross test needs (k+1) s^2, a round s(s-1); even count keeps
 // the Gram copy 16-byte aligned
@@ -335,46 +337,41 @@ __global__ void __launch_bounds__(ORTH_NT, 1) k_orth(const __grid_constant__ Ort
     double acc[S * NC];
 #pragma unroll
     for (int q = 0; q < S * NC; ++q) acc[q] = 0.0;
-    for (int p0 = tid; p0 < cnt; p0 += 2 * ORTH_NT) {
-      const int p1 = p0 + ORTH_NT;
-      const bool has1 = p1 < cnt;
-      double v0[S], v1[S], w0[S], w1[S];
+    for (int p0 = tid; p0 < cnt; p0 += ORTH_UU * ORTH_NT) {
+      bool has[ORTH_UU];
+      double v[ORTH_UU][S], w[ORTH_UU][S], cv[ORTH_UU][NC];
 #pragma unroll
-      for (int l = 0; l < S; ++l) {
-        v0[l] = Vi[l * np + p0];
-        v1[l] = has1 ? Vi[l * np + p1] : 0.0;
-        w0[l] = dots ? Vn[l * np + p0] : 0.0;
-        w1[l] = dots && has1 ? Vn[l * np + p1] : 0.0;
-      }
-      double c0[NC], c1[NC];
+      for (int u = 0; u < ORTH_UU; ++u) {
+        const int p = p0 + u * ORTH_NT;
+        has[u] = p < cnt;
 #pragma unroll
-      for (int j = 0; j < NC; ++j) {
-        c0[j] = sc[(int64_t)j * d.P + p0];
-        c1[j] = has1 ? sc[(int64_t)j * d.P + p1] : 0.0;
+        for (int l = 0; l < S; ++l) {
+          v[u][l] = has[u] ? Vi[l * np + p] : 0.0;
+          w[u][l] = dots && has[u] ? Vn[l * np + p] : 0.0;
+        }
       }
+#pragma unroll
+      for (int u = 0; u < ORTH_UU; ++u)
+#pragma unroll
+        for (int j = 0; j < NC; ++j) cv[u][j] = has[u] ? sc[(int64_t)j * d.P + p0 + u * ORTH_NT] : 0.0;
 #pragma unroll
       for (int l = 0; l < S; ++l)
 #pragma unroll
         for (int j = 0; j < NC; ++j) {
           const double t = tc[l * NC + j];
-          c0[j] = dadd(c0[j], dmul(t, v0[l]));
-          c1[j] = dadd(c1[j], dmul(t, v1[l]));
+#pragma unroll
+          for (int u = 0; u < ORTH_UU; ++u) cv[u][j] = dadd(cv[u][j], dmul(t, v[u][l]));
         }
 #pragma unroll
-      for (int j = 0; j < NC; ++j) {
-        sc[(int64_t)j * d.P + p0] = c0[j];
-        if (has1) sc[(int64_t)j * d.P + p1] = c1[j];
-      }
-      if (dots) {
+      for (int u = 0; u < ORTH_UU; ++u) {
+        if (!has[u]) continue;
 #pragma unroll
-        for (int l = 0; l < S; ++l)
-#pragma unroll
-          for (int j = 0; j < NC; ++j) acc[l * NC + j] = fma(w0[l], c0[j], acc[l * NC + j]);
-        if (has1) {
+        for (int j = 0; j < NC; ++j) sc[(int64_t)j * d.P + p0 + u * ORTH_NT] = cv[u][j];
+        if (dots) {
 #pragma unroll
           for (int l = 0; l < S; ++l)
 #pragma unroll
-            for (int j = 0; j < NC; ++j) acc[l * NC + j] = fma(w1[l], c1[j], acc[l * NC + j]);
+            for (int j = 0; j < NC; ++j) acc[l * NC + j] = fma(w[u][l], cv[u][j], acc[l * NC + j]);
         }
       }
     }
@@ -391,35 +388,28 @@ __global__ void __launch_bounds__(ORTH_NT, 1) k_orth(const __grid_constant__ Ort
     const bool basis = i < d.k;
     const double* Li = basis ? colp(i, 0) : c0p;
     const int64_t np = d.np;
-    for (int p0 = tid; p0 < cnt; p0 += 2 * ORTH_NT) {
-      const int p1 = p0 + ORTH_NT;
-      const bool has1 = p1 < cnt;
-      double a0[S], a1[S], b0[S], b1[S];
-      b0[0] = c0p[p0];
-      b1[0] = has1 ? c0p[p1] : 0.0;
+    for (int p0 = tid; p0 < cnt; p0 += ORTH_UC * ORTH_NT) {
+      bool has[ORTH_UC];
+      double a[ORTH_UC][S], b[ORTH_UC][S];
 #pragma unroll
-      for (int l = 0; l < S; ++l) {
-        a0[l] = basis ? Li[l * np + p0] : 0.0;
-        a1[l] = basis && has1 ? Li[l * np + p1] : 0.0;
+      for (int u = 0; u < ORTH_UC; ++u) {
+        const int p = p0 + u * ORTH_NT;
+        has[u] = p < cnt;
+        b[u][0] = has[u] ? c0p[p] : 0.0;
+#pragma unroll
+        for (int l = 0; l < S; ++l) a[u][l] = basis && has[u] ? Li[l * np + p] : 0.0;
+#pragma unroll
+        for (int j = 1; j < S; ++j) b[u][j] = has[u] ? sc[(int64_t)(j - 1) * d.P + p] : 0.0;
       }
 #pragma unroll
-      for (int j = 1; j < S; ++j) {
-        b0[j] = sc[(int64_t)(j - 1) * d.P + p0];
-        b1[j] = has1 ? sc[(int64_t)(j - 1) * d.P + p1] : 0.0;
-      }
-      if (!basis) {
+      for (int u = 0; u < ORTH_UC; ++u) {
+        if (!has[u]) continue;
 #pragma unroll
-        for (int l = 0; l < S; ++l) a0[l] = b0[l], a1[l] = b1[l];
-      }
+        for (int l = 0; l < S; ++l) {
+          const double av = basis ? a[u][l] : b[u][l];
 #pragma unroll
-      for (int l = 0; l < S; ++l)
-#pragma unroll
-        for (int jc = 0; jc < S; ++jc) acc[l * S + jc] = fma(a0[l], b0[jc], acc[l * S + jc]);
-      if (has1) {
-#pragma unroll
-        for (int l = 0; l < S; ++l)
-#pragma unroll
-          for (int jc = 0; jc < S; ++jc) acc[l * S + jc] = fma(a1[l], b1[jc], acc[l * S + jc]);
+          for (int jc = 0; jc < S; ++jc) acc[l * S + jc] = fma(av, b[u][jc], acc[l * S + jc]);
+        }
       }
     }
     orth_store(acc, red, d.partials, d0);
