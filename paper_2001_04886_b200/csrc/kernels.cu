@@ -96,7 +96,7 @@ __global__ void __launch_bounds__(256) k_apply_csr(const __grid_constant__ DevOp
 }
 
 void launch_apply(Ctx& c, const DevOp& op, const double* x, double* y, const int* halt, const int* cond) {
-  if (op.kind != kCsr) {  // stencils: depth-1 matrix-powers sweep (handles slab halos)
+  if (op.kind != kCsr && c.world() > 1) {  // slabs: depth-1 matrix-powers sweep (halo exchange)
     double* outs[2] = {nullptr, y};
     launch_mpk(c, op, x, nullptr, outs, 1, 0, nullptr, 1, nullptr, 0, halt, cond);
     return;

@@ -167,12 +167,19 @@ __global__ void __launch_bounds__(MW_WARPS * 32) k_mpk2w(const __grid_constant__
   for (int q = 0; q < NACC; ++q) acc[q] = 0.0;
   // slab geometry: local row t is global row row0 + t; rows just outside the slab come from
   // the halo buffers (filled by the exchange), rows outside the grid are Dirichlet zeros
-  const int64_t row0 = d.op.row0, rows_g = d.op.rows_global;
+  const int row0 = (int)d.op.row0, rows_g = (int)d.op.rows_global;
   const int H = (int)d.op.halo_rows;
   const int tb = y0 - J, te = y1 + J;
+  // lane constants: neighbour presence of the two columns, the outputs, the constant stencil
+  const bool hWa = ca > 0, hEa = cb < nx, hWb = ca >= 0, hEb = cb + 1 < nx;
+  double* outs[J + 1];
+#pragma unroll
+  for (int j = 0; j <= J; ++j) outs[j] = d.out[j];
+  double cS = 0.0, cW = 0.0, cC = 0.0, cE = 0.0, cN = 0.0;
+  if (KIND == kStencilConst) cS = d.op.coef[1], cW = d.op.coef[2], cC = d.op.coef[3], cE = d.op.coef[4], cN = d.op.coef[5];
   auto issue = [&](int t) {
     const int slot = (t - tb) % NS;
-    const int64_t tg = row0 + t;
+    const int tg = row0 + t;
     const bool rowok = active && tg >= 0 && tg < rows_g && t < te;
     const double* rowp = d.src;
     if (rowok)
@@ -208,8 +215,8 @@ __global__ void __launch_bounds__(MW_WARPS * 32) k_mpk2w(const __grid_constant__
         const double vb = inB && rowin ? (d.scale ? __dmul_rn(sb, scale) : sb) : 0.0;
         wa[0][0] = wa[0][1], wa[0][1] = wa[0][2], wa[0][2] = va;
         wb[0][0] = wb[0][1], wb[0][1] = wb[0][2], wb[0][2] = vb;
-        if (d.out[0] && t >= y0 && t < y1) {
-          double* o = d.out[0] + (int64_t)t * nx;
+        if (outs[0] && t >= y0 && t < y1) {
+          double* o = outs[0] + (int64_t)t * nx;
           if (outA) o[ca] = va;
           if (outB) o[cb] = vb;
         }
@@ -217,20 +224,41 @@ __global__ void __launch_bounds__(MW_WARPS * 32) k_mpk2w(const __grid_constant__
 #pragma unroll
       for (int j = 1; j <= J; ++j) {
         const int r = t - j;  // row level j computes
-        const int64_t rg = row0 + r;
+        const int rg = row0 + r;
         // x-neighbours of level j-1 at row r
         const double ma = wa[j - 1][1], mb = wb[j - 1][1];
         const double wA = __shfl_up_sync(FULL, mb, 1);    // column ca-1 (lane-1's b)
         const double eB = __shfl_down_sync(FULL, ma, 1);  // column cb+1 (lane+1's a)
-        double va = 0.0, vb = 0.0;
-        if (rg >= 0 && rg < rows_g && r >= y0 - (J - j) && r < y1 + (J - j)) {
-          if (inA) va = point2d<KIND>(d.op, r, rg, rows_g, ca, nx, wa[j - 1][0], wA, ma, mb, wa[j - 1][2]);
-          if (inB) vb = point2d<KIND>(d.op, r, rg, rows_g, cb, nx, wb[j - 1][0], ma, mb, eB, wb[j - 1][2]);
+        // level j is needed (and its inputs valid) only within J-j rows of the warp's rows
+        const bool rv = rg >= 0 && rg < rows_g && r >= y0 - (J - j) && r < y1 + (J - j);  // warp-uniform
+        double va, vb;
+        if (KIND == kStencilConst) {
+          // S, W, C, E, N (ascending column), separately rounded; absent neighbours are zeros
+          const bool hS = rg > 0, hN = rg + 1 < rows_g;
+          double a = 0.0, b = 0.0;
+          a = __dadd_rn(a, __dmul_rn(cS, hS ? wa[j - 1][0] : 0.0));
+          b = __dadd_rn(b, __dmul_rn(cS, hS ? wb[j - 1][0] : 0.0));
+          a = __dadd_rn(a, __dmul_rn(cW, hWa ? wA : 0.0));
+          b = __dadd_rn(b, __dmul_rn(cW, hWb ? ma : 0.0));
+          a = __dadd_rn(a, __dmul_rn(cC, ma));
+          b = __dadd_rn(b, __dmul_rn(cC, mb));
+          a = __dadd_rn(a, __dmul_rn(cE, hEa ? mb : 0.0));
+          b = __dadd_rn(b, __dmul_rn(cE, hEb ? eB : 0.0));
+          a = __dadd_rn(a, __dmul_rn(cN, hN ? wa[j - 1][2] : 0.0));
+          b = __dadd_rn(b, __dmul_rn(cN, hN ? wb[j - 1][2] : 0.0));
+          va = rv && inA ? a : 0.0;
+          vb = rv && inB ? b : 0.0;
+        } else {
+          va = 0.0, vb = 0.0;
+          if (rv) {
+            if (inA) va = point2d<KIND>(d.op, r, rg, rows_g, ca, nx, wa[j - 1][0], wA, ma, mb, wa[j - 1][2]);
+            if (inB) vb = point2d<KIND>(d.op, r, rg, rows_g, cb, nx, wb[j - 1][0], ma, mb, eB, wb[j - 1][2]);
+          }
         }
         wa[j][0] = wa[j][1], wa[j][1] = wa[j][2], wa[j][2] = va;
         wb[j][0] = wb[j][1], wb[j][1] = wb[j][2], wb[j][2] = vb;
-        if (d.out[j] && r >= y0 && r < y1) {
-          double* o = d.out[j] + (int64_t)r * nx;
+        if (outs[j] && r >= y0 && r < y1) {
+          double* o = outs[j] + (int64_t)r * nx;
           if (outA) o[ca] = va;
           if (outB) o[cb] = vb;
         }

@@ -928,15 +928,8 @@ struct Engine {
     return 0;
   }
 
-  // y = A x with the one-sweep stencil kernel where available (skipped unless *cond when given)
-  void apply(const double* x, double* y, const int* cond = nullptr) {
-    if (mpk_max_depth(op.d) >= 1) {
-      double* outs[2] = {nullptr, y};
-      launch_mpk(c, op.d, x, nullptr, outs, 1, 0, nullptr, 1, partials, 0, halt, cond, cond ? "mpk_redo" : "mpk");
-    } else {
-      launch_apply(c, op.d, x, y, halt, cond);
-    }
-  }
+  // y = A x (skipped unless *cond when given)
+  void apply(const double* x, double* y, const int* cond = nullptr) { launch_apply(c, op.d, x, y, halt, cond); }
 
   void gram_self_into(int b, int dW, const int* cond, const char* name = "gram_w") {
     std::vector<const double*> B;
