@@ -9,66 +9,9 @@
 
 #include "device_util.cuh"
 #include "skc_internal.hpp"
+#include "stencil.cuh"
 
 namespace skc {
-
-// ------------------------------------------------------------------ stencil point
-__device__ __forceinline__ double face_k(double kp, double kq) {
-  return __ddiv_rn(__dmul_rn(__dmul_rn(2.0, kp), kq), __dadd_rn(kp, kq));
-}
-
-template <int DIM, int KIND>
-__device__ __forceinline__ double stencil_point(const DevOp& op, const double* __restrict__ x, int64_t i,
-                                                int64_t j, int64_t l) {
-  const int64_t nx = op.nx, ny = op.ny;
-  const int64_t plane = nx * ny;
-  const int64_t p = (DIM == 3 ? l * plane : 0) + j * nx + i;
-  bool pres[7];
-  int64_t nb[7];
-  pres[0] = DIM == 3 && l > 0;
-  pres[1] = j > 0;
-  pres[2] = i > 0;
-  pres[3] = true;
-  pres[4] = i + 1 < nx;
-  pres[5] = j + 1 < ny;
-  pres[6] = DIM == 3 && l + 1 < op.nz;
-  nb[0] = p - plane;
-  nb[1] = p - nx;
-  nb[2] = p - 1;
-  nb[3] = p;
-  nb[4] = p + 1;
-  nb[5] = p + nx;
-  nb[6] = p + plane;
-  double val[7];
-  if (KIND == kStencilConst) {
-#pragma unroll
-    for (int t = 0; t < 7; ++t) val[t] = op.coef[t];
-  } else if (KIND == kStencilDia) {
-#pragma unroll
-    for (int t = 0; t < 7; ++t) val[t] = (DIM == 2 && (t == 0 || t == 6)) ? 0.0 : op.dia[t * op.n + p];
-  } else {  // variable k, faces -z,-y,-x,+x,+y,+z; own k on boundary faces
-    const double kp = op.kcell[p];
-    double d = 0.0;
-    bool first = true;
-#pragma unroll
-    for (int t = 0; t < 7; ++t) {
-      if (t == 3) continue;
-      if (DIM == 2 && (t == 0 || t == 6)) continue;
-      const double kf = pres[t] ? face_k(kp, op.kcell[nb[t]]) : kp;
-      d = first ? kf : __dadd_rn(d, kf);
-      first = false;
-      val[t] = t < 3 ? __dsub_rn(-kf, op.ch2) : __dadd_rn(-kf, op.ch2);
-    }
-    val[3] = d;
-  }
-  double acc = 0.0;
-#pragma unroll
-  for (int t = 0; t < 7; ++t) {
-    if (DIM == 2 && (t == 0 || t == 6)) continue;
-    if (pres[t]) acc = __dadd_rn(acc, __dmul_rn(val[t], x[nb[t]]));
-  }
-  return acc;
-}
 
 template <int DIM, int KIND>
 __global__ void __launch_bounds__(256) k_apply(const __grid_constant__ DevOp op, const double* __restrict__ x,

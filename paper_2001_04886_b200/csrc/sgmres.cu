@@ -20,6 +20,7 @@
 
 #include "device_util.cuh"
 #include "solver_util.hpp"
+#include "stencil.cuh"
 
 namespace skc {
 
@@ -95,7 +96,32 @@ __global__ void k_arn_ctor(ArnState* st, int use_rn, const double* partials, int
   }
 }
 
-// push_block (sstep.hpp:392-399): W = gram_self(block) -> GramSolver; breakdown = collapse
+// push_block (sstep.hpp:392-399): W = gram_self(block) -> GramSolver; breakdown = collapse.
+// One thread, on the reduced s x s products v; the factor is built in g (scratch) and stored
+// to grams[k] by the caller when the status stays running.
+__device__ bool arn_push_body(ArnState* st, Gram& g, int k, double* rec, const double* v, int s) {
+  double W[kMaxS * kMaxS];
+  for (int q = 0; q < s * s; ++q) W[q] = v[q];
+  for (int j = 0; j < s; ++j)
+    for (int l = j + 1; l < s; ++l) {
+      const double avg = (W[j * s + l] + W[l * s + j]) / 2.0;
+      W[j * s + l] = avg;
+      W[l * s + j] = avg;
+    }
+  for (int q = 0; q < s * s; ++q) rec[RecLayout::kW + q] = W[q];
+  gram_factor(g, W, s);
+  rec[RecLayout::kOk] = g.ok;
+  rec[RecLayout::kRatio] = g.ratio;
+  rec[RecLayout::kSing] = g.singular1;
+  if (!g.ok) {
+    st->status = k == 0 ? kArnCtorCollapse : kArnPushCollapse;
+    st->block = k;
+    st->halt = 1;
+    return false;
+  }
+  return true;
+}
+
 __global__ void k_arn_push(ArnState* st, Gram* grams, int k, double* rec, const double* partials, int G, int dWa,
                            int dWb, int s) {
   SKC_PDL_ENTRY();
@@ -104,27 +130,8 @@ __global__ void k_arn_push(ArnState* st, Gram* grams, int k, double* rec, const 
   const int dW = st->reorth ? dWb : dWa;
   reduce_dots_dev(partials, G, dW, s * s, v);
   if (threadIdx.x == 0) {
-    double W[kMaxS * kMaxS];
-    for (int q = 0; q < s * s; ++q) W[q] = v[q];
-    for (int j = 0; j < s; ++j)
-      for (int l = j + 1; l < s; ++l) {
-        const double avg = (W[j * s + l] + W[l * s + j]) / 2.0;
-        W[j * s + l] = avg;
-        W[l * s + j] = avg;
-      }
-    for (int q = 0; q < s * s; ++q) rec[RecLayout::kW + q] = W[q];
     Gram g;
-    gram_factor(g, W, s);
-    rec[RecLayout::kOk] = g.ok;
-    rec[RecLayout::kRatio] = g.ratio;
-    rec[RecLayout::kSing] = g.singular1;
-    if (!g.ok) {
-      st->status = k == 0 ? kArnCtorCollapse : kArnPushCollapse;
-      st->block = k;
-      st->halt = 1;
-      return;
-    }
-    grams[k] = g;
+    if (arn_push_body(st, g, k, rec, v, s)) grams[k] = g;
   }
 }
 
@@ -225,20 +232,24 @@ constexpr size_t kOrthSmemCap = 220 * 1024;  // <= the 226 KB dynamic limit set 
 // reduced-product capacity: the cross test needs (k+1) s^2, a round s(s-1); even count keeps
 // the Gram copy 16-byte aligned
 __host__ __device__ inline int orth_prod_cap(int k, int s) { return ((k + 1) * s * s + 1) & ~1; }
+constexpr int kStepH = 64 * kMaxS;  // -h coefficients of Scalar1 (k s <= 512)
 
 struct OrthDesc {
-  int s, k;
+  int s, k, build_next;
   int64_t n, P;           // points, points per CTA
+  DevOp op;
+  const double* vin;      // v_{k-1}^{s-1}: z = A vin
+  double* z;
+  double* seed;
   const double* V;        // basis: block i column l at V + (i*s + l)*np
   int64_t np;
-  const double* cand0;    // candidate column 0 (read only)
-  double* cand[kMaxS];    // candidate columns 1..s-1 (written back)
+  const double* cand0;    // candidate column 0 (= cand[0] below, written by the powers phase)
+  double* cand[kMaxS];    // candidate columns 0..s-1 of block slot k
   double* partials;
-  int src_G0;             // partial columns of the incoming round-0 products
-  int dr0, dr1, dcross, dwb;
-  const Gram* grams;
+  int dz, dseed, dr0, dr1, dcross, dwb;
+  Gram* grams;
   double* rec;            // this block iteration's record
-  int rec_t;
+  int rec_t, rec_h;
   ArnState* st;
   double orth_tol;
   unsigned long long* trace;  // optional phase timestamps (CTA 0), diagnostics
@@ -272,7 +283,7 @@ __device__ __forceinline__ void orth_store(const double (&acc)[K], double* red, 
 }
 
 template <int S>
-__global__ void __launch_bounds__(ORTH_NT, 1) k_orth(const __grid_constant__ OrthDesc d) {
+__global__ void __launch_bounds__(ORTH_NT, 1) k_arn_step(const __grid_constant__ OrthDesc d) {
   SKC_PDL_ENTRY();
   if (__ldg(&d.st->halt)) return;  // block-uniform, before any barrier
   namespace cg = cooperative_groups;
@@ -282,7 +293,8 @@ __global__ void __launch_bounds__(ORTH_NT, 1) k_orth(const __grid_constant__ Ort
   // coefficients -t [64] | reduced products [(k+1) s^2] | Gram copy | reduction scratch
   // [32 warps][s^2] | candidate slice [s-1][P]
   double* tc = dsm;
-  double* prod = dsm + 64;
+  double* hc = dsm + 64;
+  double* prod = hc + kStepH;
   Gram* gs = reinterpret_cast<Gram*>(prod + orth_prod_cap(d.k, S));
   double* red = reinterpret_cast<double*>(gs + 1);
   double* sc = red + (ORTH_NT / 32) * S * S;
@@ -295,9 +307,6 @@ __global__ void __launch_bounds__(ORTH_NT, 1) k_orth(const __grid_constant__ Ort
   const int G = gridDim.x;
   auto colp = [&](int i, int l) { return d.V + ((int64_t)i * S + l) * d.np + base; };
 
-  // load this CTA's slice of cand[:,1:]
-  for (int j = 0; j < NC; ++j)
-    for (int p = tid; p < cnt; p += ORTH_NT) sc[(int64_t)j * d.P + p] = d.cand[j][base + p];
 
   // Scalar2 for block i from partials (src, srcG): every CTA solves W_i t = V_i^T cand[:,1:]
   auto scalar = [&](int i, int src, int srcG, int accumulate) {
@@ -416,10 +425,209 @@ __global__ void __launch_bounds__(ORTH_NT, 1) k_orth(const __grid_constant__ Ort
   };
 
   const int K = d.k;
+  const int64_t np = d.np;
+  orth_mark(d, 39);
+  // ---- z = A v_{k-1}^{s-1} on this slice (the source is stable; neighbours read from memory)
+  // y = A x on this slice; xs (optional) is this slice of x in shared memory, read in place of
+  // memory for the points it covers.  The 2D constant stencil takes a 32-bit fast path (same
+  // arithmetic: S, W, C, E, N in ascending column order, absent neighbours skipped).
+  auto apply_slice = [&](const double* x, const double* xs, auto&& put) {
+    if (d.op.kind == kStencilConst && d.op.dim == 2) {
+      const int nx = (int)d.op.nx, ny = (int)d.op.ny;
+      const double cS = d.op.coef[1], cW = d.op.coef[2], cC = d.op.coef[3], cE = d.op.coef[4], cN = d.op.coef[5];
+      const double* xb = x + base;  // slice-relative view of x in memory
+      auto get = [&](int o) { return xs && o >= 0 && o < cnt ? xs[o] : xb[o]; };
+      // four points per thread per iteration, every neighbour load issued before the sums
+      constexpr int U = 4;
+      int i[U], jr[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int64_t q = base + tid + u * ORTH_NT;
+        i[u] = (int)(q % nx), jr[u] = (int)(q / nx);
+      }
+      for (int p0 = tid; p0 < cnt; p0 += U * ORTH_NT) {
+        double vs[U], vw[U], vc[U], ve[U], vn[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int p = p0 + u * ORTH_NT;
+          const bool in = p < cnt;
+          vs[u] = in && jr[u] > 0 ? get(p - nx) : 0.0;
+          vw[u] = in && i[u] > 0 ? get(p - 1) : 0.0;
+          vc[u] = in ? get(p) : 0.0;
+          ve[u] = in && i[u] + 1 < nx ? get(p + 1) : 0.0;
+          vn[u] = in && jr[u] + 1 < ny ? get(p + nx) : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int p = p0 + u * ORTH_NT;
+          if (p < cnt) {
+            double a = 0.0;
+            if (jr[u] > 0) a = __dadd_rn(a, __dmul_rn(cS, vs[u]));
+            if (i[u] > 0) a = __dadd_rn(a, __dmul_rn(cW, vw[u]));
+            a = __dadd_rn(a, __dmul_rn(cC, vc[u]));
+            if (i[u] + 1 < nx) a = __dadd_rn(a, __dmul_rn(cE, ve[u]));
+            if (jr[u] + 1 < ny) a = __dadd_rn(a, __dmul_rn(cN, vn[u]));
+            put(p, a);
+          }
+          i[u] += U * ORTH_NT;
+          while (i[u] >= nx) i[u] -= nx, ++jr[u];
+        }
+      }
+      return;
+    }
+    GridWalk w;
+    if (tid < cnt) w.init(d.op, base + tid);
+    if (xs) {
+      auto fetch = [&](int64_t q) {
+        const int64_t o = q - base;
+        return o >= 0 && o < cnt ? xs[o] : x[q];
+      };
+      for (int p = tid; p < cnt; p += ORTH_NT, w.step(d.op, ORTH_NT)) put(p, apply_point(d.op, fetch, base + p, w));
+    } else {
+      auto fetch = [&](int64_t q) { return x[q]; };
+      for (int p = tid; p < cnt; p += ORTH_NT, w.step(d.op, ORTH_NT)) put(p, apply_point(d.op, fetch, base + p, w));
+    }
+  };
+  apply_slice(d.vin, nullptr, [&](int p, double v) { d.z[base + p] = v; });
+  orth_mark(d, 40);
+  // ---- Scalar1 products V_i^T z (i < k) -> dz + i s + l, and z.z -> dz + k s (each thread
+  //      reads back its own z)
+  {
+    double zz[1] = {0.0};
+    for (int i = 0; i < K; ++i) {
+      double acc[S];
+#pragma unroll
+      for (int q = 0; q < S; ++q) acc[q] = 0.0;
+      const double* Vi = colp(i, 0);
+      for (int p0 = tid; p0 < cnt; p0 += ORTH_UC * ORTH_NT) {
+        double zv[ORTH_UC], v[ORTH_UC][S];
+#pragma unroll
+        for (int u = 0; u < ORTH_UC; ++u) {
+          const int p = p0 + u * ORTH_NT;
+          const bool h = p < cnt;
+          zv[u] = h ? d.z[base + p] : 0.0;
+#pragma unroll
+          for (int l = 0; l < S; ++l) v[u][l] = h ? Vi[l * np + p] : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < ORTH_UC; ++u) {
+          if (p0 + u * ORTH_NT >= cnt) continue;
+#pragma unroll
+          for (int l = 0; l < S; ++l) acc[l] = fma(v[u][l], zv[u], acc[l]);
+          if (i == 0) zz[0] = fma(zv[u], zv[u], zz[0]);
+        }
+      }
+      orth_store(acc, red, d.partials, d.dz + i * S);
+    }
+    orth_store(zz, red, d.partials, d.dz + K * S);
+  }
+  orth_mark(d, 6);
+  grid.sync();
+  // ---- Scalar1 (sstep.hpp:301-310): zn, h_i = W_i^{-1} V_i^T z in every CTA; CTA 0 records
+  // Gram factors of the k blocks into the (still unused) candidate area of shared memory when
+  // it is large enough (the serial solves then read them at shared-memory latency)
+  const bool gram_smem = (int64_t)K * (int64_t)sizeof(Gram) <= (int64_t)(S - 1) * d.P * 8;
+  const Gram* gk = gram_smem ? reinterpret_cast<const Gram*>(sc) : d.grams;
+  if (gram_smem) {
+    const uint64_t* gsrc = reinterpret_cast<const uint64_t*>(d.grams);
+    uint64_t* gdst = reinterpret_cast<uint64_t*>(sc);
+    for (int w = tid; w < (int)(K * sizeof(Gram) / 8); w += ORTH_NT) gdst[w] = gsrc[w];
+  }
+  reduce_dots_dev(d.partials, G, d.dz, K * S + 1, prod);  // (ends with __syncthreads)
+  const double zn = sqrt(prod[K * S]);
+  if (blockIdx.x == 0 && tid == 0) {
+    d.rec[RecLayout::kZn] = zn;
+    d.rec[RecLayout::kReorth] = 0.0;
+    d.rec[RecLayout::kFirst] = -1.0;
+    d.st->reorth = 0;
+  }
+  for (int i = tid; i < K; i += ORTH_NT) {
+    double rhs[kMaxS], h[kMaxS];
+    for (int l = 0; l < S; ++l) rhs[l] = prod[i * S + l];
+    gram_solve(gk[i], rhs, h);
+    for (int l = 0; l < S; ++l) {
+      hc[i * S + l] = -h[l];
+      if (blockIdx.x == 0) d.rec[d.rec_h + i * S + l] = h[l];
+    }
+  }
+  __syncthreads();
+  orth_mark(d, 41);
+  // ---- seed = z - sum_i V_i h_i (terms in block order, multiply and add rounded separately)
+  //      and ||seed||^2
+  {
+    double acc[1] = {0.0};
+    for (int p = tid; p < cnt; p += ORTH_NT) {
+      double o = d.z[base + p];
+      for (int i = 0; i < K; ++i) {
+        const double* Vi = colp(i, 0);
+        double v[S];
+#pragma unroll
+        for (int l = 0; l < S; ++l) v[l] = Vi[l * np + p];
+#pragma unroll
+        for (int l = 0; l < S; ++l) o = dadd(o, dmul(hc[i * S + l], v[l]));
+      }
+      d.seed[base + p] = o;
+      acc[0] = fma(o, o, acc[0]);
+    }
+    orth_store(acc, red, d.partials, d.dseed);
+  }
+  orth_mark(d, 7);
+  grid.sync();
+  // ---- nu = ||seed|| and the invariant-subspace test (sstep.hpp:315-324)
+  reduce_dots_dev(d.partials, G, d.dseed, 1, prod);
+  const double nu = sqrt(prod[0]);
+  if (blockIdx.x == 0 && tid == 0) d.rec[RecLayout::kNu] = nu;
+  if (nu <= 1e-14 * zn) {  // identical decision in every CTA
+    if (blockIdx.x == 0 && tid == 0) {
+      d.rec[RecLayout::kInv] = 1.0;
+      d.st->status = kArnInvariant;
+      d.st->block = K;
+      d.st->halt = 1;
+    }
+    return;
+  }
+  const double inv = 1.0 / nu;
+  orth_mark(d, 42);
+  // ---- candidate block [v, A v, .., A^{s-1} v], v = seed / nu (krylov_block, block.hpp:59-67):
+  //      every level is an exact spmv of the previous one; levels 1..s-1 stay in shared memory,
+  //      levels 0..s-2 also go to memory for the neighbours' next level
+  for (int p = tid; p < cnt; p += ORTH_NT) d.cand[0][base + p] = __dmul_rn(d.seed[base + p], inv);
+  orth_mark(d, 44);
+  for (int j = 1; j < S; ++j) {
+    grid.sync();
+    orth_mark(d, 44 + 2 * j - 1);
+    const bool to_mem = j + 1 < S || !d.build_next;
+    // level j-1 >= 1 is also in shared memory for this slice (only slice-edge neighbours come
+    // from memory)
+    apply_slice(d.cand[j - 1], j >= 2 ? sc + (int64_t)(j - 2) * d.P : nullptr, [&](int p, double v) {
+      sc[(int64_t)(j - 1) * d.P + p] = v;
+      if (to_mem) d.cand[j][base + p] = v;
+    });
+    orth_mark(d, 44 + 2 * j);
+  }
+  orth_mark(d, 43);
+  if (!d.build_next) return;  // the last block iteration builds the candidate only
+  // ---- round-0 products V_0^T cand[:,1:] (sstep.hpp:341)
+  {
+    double acc[S * NC];
+#pragma unroll
+    for (int q = 0; q < S * NC; ++q) acc[q] = 0.0;
+    const double* V0 = colp(0, 0);
+    for (int p = tid; p < cnt; p += ORTH_NT) {
+#pragma unroll
+      for (int l = 0; l < S; ++l) {
+        const double lv = V0[l * np + p];
+#pragma unroll
+        for (int j = 0; j < NC; ++j) acc[l * NC + j] = fma(lv, sc[(int64_t)j * d.P + p], acc[l * NC + j]);
+      }
+    }
+    orth_store(acc, red, d.partials, d.dr0);
+  }
+  grid.sync();
   orth_mark(d, 0);
-  // ---- pass 0 (round 0 products arrive from the powers sweep or a Gram launch)
+  // ---- pass 0
   for (int i = 0; i < K; ++i) {
-    scalar(i, (i & 1) ? d.dr1 : d.dr0, i == 0 ? d.src_G0 : G, 0);
+    scalar(i, (i & 1) ? d.dr1 : d.dr0, G, 0);
     orth_mark(d, 8 + 3 * i);
     round(i, ((i + 1) & 1) ? d.dr1 : d.dr0);
     orth_mark(d, 9 + 3 * i);
@@ -486,16 +694,29 @@ __global__ void __launch_bounds__(ORTH_NT, 1) k_orth(const __grid_constant__ Ort
       if (i + 1 < K) grid.sync();
     }
     cross_block(K, d.dwb);
+    grid.sync();
   }
   orth_mark(d, 4);
   // write the candidate columns back
   for (int j = 0; j < NC; ++j)
-    for (int p = tid; p < cnt; p += ORTH_NT) d.cand[j][base + p] = sc[(int64_t)j * d.P + p];
+    for (int p = tid; p < cnt; p += ORTH_NT) d.cand[j + 1][base + p] = sc[(int64_t)j * d.P + p];
+  // ---- push_block of the new block (CTA 0): W from the pass that produced it
+  if (blockIdx.x == 0) {
+    reduce_dots_dev(d.partials, G, s_first >= 0 ? d.dwb : d.dcross + K * S * S, S * S, prod);
+    __shared__ int s_ok;
+    if (tid == 0) s_ok = arn_push_body(d.st, *gs, K, d.rec, prod, S);
+    __syncthreads();
+    if (s_ok) {
+      const uint64_t* gsrc = reinterpret_cast<const uint64_t*>(gs);
+      uint64_t* gdst = reinterpret_cast<uint64_t*>(d.grams + K);
+      for (int w = tid; w < (int)(sizeof(Gram) / 8); w += ORTH_NT) gdst[w] = gsrc[w];
+    }
+  }
   orth_mark(d, 5);
 }
 
 size_t orth_smem(int s, int k, int64_t P) {
-  return sizeof(double) * (64 + (size_t)orth_prod_cap(k, s)) + sizeof(Gram) + sizeof(double) * (ORTH_NT / 32) * s * s +
+  return sizeof(double) * (64 + kStepH + (size_t)orth_prod_cap(k, s)) + sizeof(Gram) + sizeof(double) * (ORTH_NT / 32) * s * s +
          sizeof(double) * (size_t)(s - 1) * (size_t)P;
 }
 
@@ -503,7 +724,7 @@ template <int S>
 void run_orth(Ctx& c, const OrthDesc& d, int G, size_t smem) {
   static bool attr = false;
   // (227 KB per block less the kernel's static shared memory)
-  if (!attr) CK(cudaFuncSetAttribute(k_orth<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, 226 * 1024)), attr = true;
+  if (!attr) CK(cudaFuncSetAttribute(k_arn_step<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, 226 * 1024)), attr = true;
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = G;
   cfg.blockDim = ORTH_NT;
@@ -514,7 +735,7 @@ void run_orth(Ctx& c, const OrthDesc& d, int G, size_t smem) {
   at[0].val.cooperative = 1;
   cfg.attrs = at;
   cfg.numAttrs = 1;
-  CK(cudaLaunchKernelEx(&cfg, k_orth<S>, d));
+  CK(cudaLaunchKernelEx(&cfg, k_arn_step<S>, d));
 }
 
 // r-norm after the cycle's residual update
@@ -775,21 +996,27 @@ struct Engine {
     return orth_smem(s, m, P) <= kOrthSmemCap ? P : 0;
   }
 
-  // the block-MGS stage of block iteration k in one cooperative kernel; returns the partial
-  // column count of the products it leaves (cross, W, Wb)
-  int launch_orth(int k, int cb, int G0) {
+  // block iteration k (z, Scalar1, seed, nu, candidate block, block MGS, reorthogonalization,
+  // push) in one cooperative kernel
+  void launch_step(int k, bool build_next) {
     OrthDesc d;
     std::memset(&d, 0, sizeof d);
     d.s = s;
     d.k = k;
+    d.build_next = build_next ? 1 : 0;
     d.n = op.n;
     d.P = orth_points();
+    d.op = op.d;
+    d.vin = col(k - 1, s - 1);
+    d.z = z;
+    d.seed = seed;
     d.V = V;
     d.np = np;
-    d.cand0 = col(cb, 0);
-    for (int j = 1; j < s; ++j) d.cand[j - 1] = col(cb, j);
+    d.cand0 = col(k, 0);
+    for (int j = 0; j < s; ++j) d.cand[j] = col(k, j);
     d.partials = partials;
-    d.src_G0 = G0;
+    d.dz = dl.Z();
+    d.dseed = dl.Seed();
     d.dr0 = dl.Dr(0);
     d.dr1 = dl.Dr(1);
     d.dcross = dl.Cross();
@@ -797,15 +1024,19 @@ struct Engine {
     d.grams = grams;
     d.rec = recp(k);
     d.rec_t = rl.t();
+    d.rec_h = rl.h();
     d.st = st;
     d.orth_tol = 1e-8;
     static const bool trace = std::getenv("SKC_TRACE_ORTH") != nullptr;
     if (trace) d.trace = (unsigned long long*)c.workspace("orth_trace", 256 * sizeof(unsigned long long));
     const int G = c.sm_count;
     const size_t smem = orth_smem(s, k, d.P);
-    // algorithmic bytes of pass 0 + the cross products (pass 1 is data dependent)
-    const double bytes = 8.0 * (double)op.n * ((2.0 * k - 1.0) * s + (double)k * s + (k + 1) + 2.0 * (s - 1));
-    Launch lh(c, "orth", bytes);
+    // algorithmic bytes: z, Scalar1 products, seed, the powers, round-0 products, pass 0 of the
+    // MGS and the cross products (the data-dependent second pass is not counted)
+    const double ks = (double)k * s;
+    const double bytes = 8.0 * (double)op.n *
+                         (2 + (ks + 1) + (ks + 2) + 3.0 * s + (build_next ? (2.0 * k - 1.0) * s + ks + (k + 1) + (s - 1) : 0.0));
+    Launch lh(c, "arn_step", bytes);
     switch (s) {
       case 2: run_orth<2>(c, d, G, smem); break;
       case 3: run_orth<3>(c, d, G, smem); break;
@@ -819,14 +1050,20 @@ struct Engine {
       unsigned long long t[256];
       CK(cudaMemcpyAsync(t, d.trace, sizeof t, cudaMemcpyDeviceToHost, c.stream));
       c.sync();
-      std::fprintf(stderr, "[orth k=%d] rounds:", k);
+      std::fprintf(stderr, "[step k=%d] z %.1f Zdots %.1f s1 %.1f seed %.1f s2 %.1f powers %.1f r0dots %.1f | rounds:", k,
+                   (t[40] - t[39]) * 1e-3, (t[6] - t[40]) * 1e-3, (t[41] - t[6]) * 1e-3, (t[7] - t[41]) * 1e-3,
+                   (t[42] - t[7]) * 1e-3, (t[43] - t[42]) * 1e-3, (t[0] - t[43]) * 1e-3);
+      std::fprintf(stderr, " [lvl0 %.1f", (t[44] - t[42]) * 1e-3);
+      for (int j = 1; j < s; ++j)
+        std::fprintf(stderr, " sync %.1f lvl%d %.1f", (t[44 + 2 * j - 1] - t[44 + 2 * j - 2]) * 1e-3, j,
+                     (t[44 + 2 * j] - t[44 + 2 * j - 1]) * 1e-3);
+      std::fprintf(stderr, "]");
       for (int i = 0; i < k; ++i)
         std::fprintf(stderr, " (scal %.1f, upd %.1f, sync %.1f)", (t[8 + 3 * i] - (i ? t[7 + 3 * i] : t[0])) * 1e-3,
                      (t[9 + 3 * i] - t[8 + 3 * i]) * 1e-3, (t[10 + 3 * i] - t[9 + 3 * i]) * 1e-3);
       std::fprintf(stderr, " | cross %.1f sync %.1f check %.1f pass1 %.1f write %.1f us\n", (t[1] - t[7 + 3 * k]) * 1e-3,
                    (t[2] - t[1]) * 1e-3, (t[3] - t[2]) * 1e-3, (t[4] - t[3]) * 1e-3, (t[5] - t[4]) * 1e-3);
     }
-    return G;
   }
 
   void enqueue_cycle_direct() {
@@ -954,6 +1191,10 @@ struct Engine {
 
   // SStepArnoldi::advance for block iteration k (1-based), sstep.hpp:297-379
   void advance(int k, bool build_next) {
+    if (orth_points() > 0) {  // the whole block iteration on chip
+      launch_step(k, build_next);
+      return;
+    }
     double* rk = recp(k);
     // z = A v_k^s ; Scalar1 dots V_i^T z and ||z||^2.  After a block iteration that fused them
     // into its cross-product pass (zfused) they are already in place, unless that iteration's
@@ -989,19 +1230,7 @@ struct Engine {
       return;
     }
     double* tk = rk + rl.t();
-    int Gorth = 0;
-    if (s > 1 && orth_points() > 0) {
-      // whole block-MGS stage on chip; round-0 products from the powers sweep or a Gram pass
-      int G0 = Gfused;
-      if (G0 == 0) {
-        std::vector<const double*> L, Cr;
-        for (int l = 0; l < s; ++l) L.push_back(col(0, l));
-        for (int jc = 1; jc < s; ++jc) Cr.push_back(col(cb, jc));
-        launch_gram_list(c, g, L, Cr, partials, dl.D(), halt, nullptr, "gram_mgs");
-        G0 = g.G;
-      }
-      Gorth = launch_orth(k, cb, G0);
-    } else if (s > 1) {
+    if (s > 1) {
       for (int pass = 0; pass < 2; ++pass) {
         const int* cond = pass ? &st->reorth : nullptr;
         std::vector<const double*> Cr;
@@ -1064,9 +1293,7 @@ struct Engine {
     // the push reads W from the reorthogonalized region when the device flag says so: make
     // both regions global (the unused one is stale but harmless)
     // (for s > 1 the dWa region was already made global together with the cross products)
-    const int Gw = Gorth > 0 ? Gorth
-                   : s > 1  ? c.reduce_point(partials, g.G, dl.Wb(), s * s)
-                            : c.reduce_point(partials, g.G, dWa, s * s);
+    const int Gw = s > 1 ? c.reduce_point(partials, g.G, dl.Wb(), s * s) : c.reduce_point(partials, g.G, dWa, s * s);
     launch_k(c, k_arn_push, 1, 256, 0, st, grams, cb, rk, partials, Gw, dWa, dl.Wb(), s);
     ++c.launches;
     CK(cudaGetLastError());
