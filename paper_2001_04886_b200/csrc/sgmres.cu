@@ -431,12 +431,18 @@ __global__ void __launch_bounds__(ORTH_NT, 1) k_arn_step(const __grid_constant__
   // y = A x on this slice; xs (optional) is this slice of x in shared memory, read in place of
   // memory for the points it covers.  The 2D constant stencil takes a 32-bit fast path (same
   // arithmetic: S, W, C, E, N in ascending column order, absent neighbours skipped).
-  auto apply_slice = [&](const double* x, const double* xs, auto&& put) {
+  // xscale (when nonzero) multiplies every source value as it is read (the source is then
+  // seed and the values level 0 = seed / nu, rounded exactly as when stored); put(p, y, x_p)
+  // also receives the point's own source value
+  auto apply_slice = [&](const double* x, const double* xs, double xscale, auto&& put) {
     if (d.op.kind == kStencilConst && d.op.dim == 2) {
       const int nx = (int)d.op.nx, ny = (int)d.op.ny;
       const double cS = d.op.coef[1], cW = d.op.coef[2], cC = d.op.coef[3], cE = d.op.coef[4], cN = d.op.coef[5];
       const double* xb = x + base;  // slice-relative view of x in memory
-      auto get = [&](int o) { return xs && o >= 0 && o < cnt ? xs[o] : xb[o]; };
+      auto get = [&](int o) {
+        const double v = xs && o >= 0 && o < cnt ? xs[o] : xb[o];
+        return xscale != 0.0 ? __dmul_rn(v, xscale) : v;
+      };
       // four points per thread per iteration, every neighbour load issued before the sums
       constexpr int U = 4;
       int i[U], jr[U];
@@ -467,7 +473,7 @@ __global__ void __launch_bounds__(ORTH_NT, 1) k_arn_step(const __grid_constant__
             a = __dadd_rn(a, __dmul_rn(cC, vc[u]));
             if (i[u] + 1 < nx) a = __dadd_rn(a, __dmul_rn(cE, ve[u]));
             if (jr[u] + 1 < ny) a = __dadd_rn(a, __dmul_rn(cN, vn[u]));
-            put(p, a);
+            put(p, a, vc[u]);
           }
           i[u] += U * ORTH_NT;
           while (i[u] >= nx) i[u] -= nx, ++jr[u];
@@ -477,18 +483,15 @@ __global__ void __launch_bounds__(ORTH_NT, 1) k_arn_step(const __grid_constant__
     }
     GridWalk w;
     if (tid < cnt) w.init(d.op, base + tid);
-    if (xs) {
-      auto fetch = [&](int64_t q) {
-        const int64_t o = q - base;
-        return o >= 0 && o < cnt ? xs[o] : x[q];
-      };
-      for (int p = tid; p < cnt; p += ORTH_NT, w.step(d.op, ORTH_NT)) put(p, apply_point(d.op, fetch, base + p, w));
-    } else {
-      auto fetch = [&](int64_t q) { return x[q]; };
-      for (int p = tid; p < cnt; p += ORTH_NT, w.step(d.op, ORTH_NT)) put(p, apply_point(d.op, fetch, base + p, w));
-    }
+    auto fetch = [&](int64_t q) {
+      const int64_t o = q - base;
+      const double v = xs && o >= 0 && o < cnt ? xs[o] : x[q];
+      return xscale != 0.0 ? __dmul_rn(v, xscale) : v;
+    };
+    for (int p = tid; p < cnt; p += ORTH_NT, w.step(d.op, ORTH_NT))
+      put(p, apply_point(d.op, fetch, base + p, w), fetch(base + p));
   };
-  apply_slice(d.vin, nullptr, [&](int p, double v) { d.z[base + p] = v; });
+  apply_slice(d.vin, nullptr, 0.0, [&](int p, double v, double) { d.z[base + p] = v; });
   orth_mark(d, 40);
   // ---- Scalar1 products V_i^T z (i < k) -> dz + i s + l, and z.z -> dz + k s (each thread
   //      reads back its own z)
@@ -591,18 +594,19 @@ __global__ void __launch_bounds__(ORTH_NT, 1) k_arn_step(const __grid_constant__
   // ---- candidate block [v, A v, .., A^{s-1} v], v = seed / nu (krylov_block, block.hpp:59-67):
   //      every level is an exact spmv of the previous one; levels 1..s-1 stay in shared memory,
   //      levels 0..s-2 also go to memory for the neighbours' next level
-  for (int p = tid; p < cnt; p += ORTH_NT) d.cand[0][base + p] = __dmul_rn(d.seed[base + p], inv);
   orth_mark(d, 44);
+  // level 1 reads seed / nu on the fly (level 0 is stored by the same sweep); levels >= 2 read
+  // their source from shared memory inside the slice
   for (int j = 1; j < S; ++j) {
-    grid.sync();
+    if (j > 1) grid.sync();
     orth_mark(d, 44 + 2 * j - 1);
     const bool to_mem = j + 1 < S || !d.build_next;
-    // level j-1 >= 1 is also in shared memory for this slice (only slice-edge neighbours come
-    // from memory)
-    apply_slice(d.cand[j - 1], j >= 2 ? sc + (int64_t)(j - 2) * d.P : nullptr, [&](int p, double v) {
-      sc[(int64_t)(j - 1) * d.P + p] = v;
-      if (to_mem) d.cand[j][base + p] = v;
-    });
+    apply_slice(j == 1 ? d.seed : d.cand[j - 1], j >= 2 ? sc + (int64_t)(j - 2) * d.P : nullptr, j == 1 ? inv : 0.0,
+                [&](int p, double v, double xc) {
+                  if (j == 1) d.cand[0][base + p] = xc;
+                  sc[(int64_t)(j - 1) * d.P + p] = v;
+                  if (to_mem) d.cand[j][base + p] = v;
+                });
     orth_mark(d, 44 + 2 * j);
   }
   orth_mark(d, 43);
