@@ -491,7 +491,11 @@ __global__ void __launch_bounds__(ORTH_NT, 1) k_arn_step(const __grid_constant__
     for (int p = tid; p < cnt; p += ORTH_NT, w.step(d.op, ORTH_NT))
       put(p, apply_point(d.op, fetch, base + p, w), fetch(base + p));
   };
-  apply_slice(d.vin, nullptr, 0.0, [&](int p, double v, double) { d.z[base + p] = v; });
+  // z and seed of this slice stay in shared memory (candidate columns 0 and s-2, free until
+  // the powers reach them; with s = 2 seed also goes to memory for its neighbours)
+  double* zs = sc;
+  double* seeds = S > 2 ? sc + (int64_t)(S - 2) * d.P : nullptr;
+  apply_slice(d.vin, nullptr, 0.0, [&](int p, double v, double) { zs[p] = v; });
   orth_mark(d, 40);
   // ---- Scalar1 products V_i^T z (i < k) -> dz + i s + l, and z.z -> dz + k s (each thread
   //      reads back its own z)
@@ -508,7 +512,7 @@ __global__ void __launch_bounds__(ORTH_NT, 1) k_arn_step(const __grid_constant__
         for (int u = 0; u < ORTH_UC; ++u) {
           const int p = p0 + u * ORTH_NT;
           const bool h = p < cnt;
-          zv[u] = h ? d.z[base + p] : 0.0;
+          zv[u] = h ? zs[p] : 0.0;
 #pragma unroll
           for (int l = 0; l < S; ++l) v[u][l] = h ? Vi[l * np + p] : 0.0;
         }
@@ -527,13 +531,14 @@ __global__ void __launch_bounds__(ORTH_NT, 1) k_arn_step(const __grid_constant__
   orth_mark(d, 6);
   grid.sync();
   // ---- Scalar1 (sstep.hpp:301-310): zn, h_i = W_i^{-1} V_i^T z in every CTA; CTA 0 records
-  // Gram factors of the k blocks into the (still unused) candidate area of shared memory when
-  // it is large enough (the serial solves then read them at shared-memory latency)
-  const bool gram_smem = (int64_t)K * (int64_t)sizeof(Gram) <= (int64_t)(S - 1) * d.P * 8;
-  const Gram* gk = gram_smem ? reinterpret_cast<const Gram*>(sc) : d.grams;
+  // Gram factors of the k blocks into candidate column 1 of shared memory (free until the seed
+  // sweep; column 0 holds z) when it is large enough: the serial solves then read them at
+  // shared-memory latency
+  const bool gram_smem = S > 2 && (int64_t)K * (int64_t)sizeof(Gram) <= d.P * 8;
+  const Gram* gk = gram_smem ? reinterpret_cast<const Gram*>(sc + d.P) : d.grams;
   if (gram_smem) {
     const uint64_t* gsrc = reinterpret_cast<const uint64_t*>(d.grams);
-    uint64_t* gdst = reinterpret_cast<uint64_t*>(sc);
+    uint64_t* gdst = reinterpret_cast<uint64_t*>(sc + d.P);
     for (int w = tid; w < (int)(K * sizeof(Gram) / 8); w += ORTH_NT) gdst[w] = gsrc[w];
   }
   reduce_dots_dev(d.partials, G, d.dz, K * S + 1, prod);  // (ends with __syncthreads)
@@ -560,7 +565,7 @@ __global__ void __launch_bounds__(ORTH_NT, 1) k_arn_step(const __grid_constant__
   {
     double acc[1] = {0.0};
     for (int p = tid; p < cnt; p += ORTH_NT) {
-      double o = d.z[base + p];
+      double o = zs[p];
       for (int i = 0; i < K; ++i) {
         const double* Vi = colp(i, 0);
         double v[S];
@@ -570,6 +575,7 @@ __global__ void __launch_bounds__(ORTH_NT, 1) k_arn_step(const __grid_constant__
         for (int l = 0; l < S; ++l) o = dadd(o, dmul(hc[i * S + l], v[l]));
       }
       d.seed[base + p] = o;
+      if (seeds) seeds[p] = o;
       acc[0] = fma(o, o, acc[0]);
     }
     orth_store(acc, red, d.partials, d.dseed);
@@ -601,7 +607,7 @@ __global__ void __launch_bounds__(ORTH_NT, 1) k_arn_step(const __grid_constant__
     if (j > 1) grid.sync();
     orth_mark(d, 44 + 2 * j - 1);
     const bool to_mem = j + 1 < S || !d.build_next;
-    apply_slice(j == 1 ? d.seed : d.cand[j - 1], j >= 2 ? sc + (int64_t)(j - 2) * d.P : nullptr, j == 1 ? inv : 0.0,
+    apply_slice(j == 1 ? d.seed : d.cand[j - 1], j >= 2 ? sc + (int64_t)(j - 2) * d.P : seeds, j == 1 ? inv : 0.0,
                 [&](int p, double v, double xc) {
                   if (j == 1) d.cand[0][base + p] = xc;
                   sc[(int64_t)(j - 1) * d.P + p] = v;
