@@ -1146,7 +1146,7 @@ struct Engine {
   // block-MGS products V_0^T cand[:,1:] are fused into it.  Returns the partial count of the
   // fused products, or 0 when they were not computed.
   int krylov_into(int b, const double* src, bool dots = false) {
-    const int J = s - 1, maxj = mpk_max_depth(op.d);
+    const int J = s - 1, maxj = powers_depth(c, op.d);
     if (J >= 1 && maxj >= 1) {
       int done = 0;
       const double* from = src;

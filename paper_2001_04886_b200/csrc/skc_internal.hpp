@@ -224,6 +224,9 @@ void launch_fill(Ctx& c, double* p, double v, int64_t n);
 // matrix powers (mpk.cu): out[0..J] of src*scale; products X[x] . level j (j >= jdot0) at
 // dot0 + x*(J-jdot0+1) + (j-jdot0) as partials over the returned CTA count.
 int mpk_max_depth(const DevOp& op);
+// depth to use for a powers sweep: on one GPU the 3D sweep (CTA tile with a J-wide ghost
+// zone, one barrier per plane) loses to J single-level applies; slabs need it for the halos
+int powers_depth(const Ctx& c, const DevOp& op);
 constexpr int kMpkMaxDotDepth = 3;  // deepest sweep that can fuse products (launch_mpk)
 enum : uint8_t { kHintNormal = 0, kHintFirst = 1, kHintLast = 2 };  // L2 policies of streamed vectors
 int launch_mpk(Ctx& c, const DevOp& op, const double* src, const double* scale, double* const* out, int J, int nxd,

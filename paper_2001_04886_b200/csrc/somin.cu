@@ -225,7 +225,7 @@ bool device_is_zero(Ctx& c, const double* x, int64_t n) {
 // K[j] = A^{j+1} src for j < J (krylov_pair's A R block, sstep.hpp:71-81): one matrix-powers
 // sweep per at most mpk_max_depth levels for stencils, repeated applies for general CSR
 static void powers(Ctx& c, const Op& op, const double* src, double* K, size_t np, int J, const int* halt) {
-  const int maxj = mpk_max_depth(op.d);
+  const int maxj = powers_depth(c, op.d);
   if (maxj < 1) {
     for (int j = 0; j < J; ++j) {
       launch_apply(c, op.d, src, K + (size_t)j * np, halt, nullptr);

@@ -46,6 +46,7 @@ struct PipeHdr {
 struct UpdDesc {
   PipeHdr h;
   int nin, nout, nx, nd, ncoef;
+  int nin0;  // SPLIT: terms [0, nin0) feed outputs [0, NOUT/2), the rest [NOUT/2, NOUT)
   const double* U[UPD_MAXU];  // distinct staged vectors
   uint8_t ub[LC_MAXOUT];      // base of output q -> U index
   int16_t bscale[LC_MAXOUT];
@@ -185,14 +186,14 @@ __device__ __forceinline__ void cta_store_partials(const double (&acc)[K], int n
 }
 
 // ------------------------------------------------------------------ k_upd
-template <int NOUT, int MAXD, int PPT>
+template <int NOUT, int MAXD, int PPT, bool SPLIT>
 __global__ void __launch_bounds__(THREADS) k_upd(const __grid_constant__ UpdDesc d) {
   SKC_PDL_ENTRY();
   if (skip_launch(d.h.halt, d.h.cond)) return;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   const int coef_slots = (d.ncoef + 15) & ~15;
-  constexpr int NV = NOUT + LC_MAXX;
-  const size_t prefix = 8 * ((size_t)coef_slots + (MAXD > 0 ? (size_t)NV * CONS : 0));
+  // per-thread value columns for the fused products: the outputs, then the nx extra inputs
+  const size_t prefix = 8 * ((size_t)coef_slots + (MAXD > 0 ? (size_t)(NOUT + d.nx) * CONS : 0));
   Pipe p = pipe_setup(d.h, smem_raw, prefix);
   double* scoef = reinterpret_cast<double*>(smem_raw + 64);
   double* sv = scoef + coef_slots;
@@ -228,7 +229,34 @@ __global__ void __launch_bounds__(THREADS) k_upd(const __grid_constant__ UpdDesc
             o[u][q] = bs >= 0 ? dmul(b, sc) : b;
           }
         }
-        for (int j = 0; j < d.nin; ++j) {
+        if (SPLIT) {
+          // two output halves, each fed by its own run of terms (term order within a half is
+          // the reference's order for each of its outputs)
+          constexpr int H = NOUT / 2;
+          for (int j = 0; j < d.nin; ++j) {
+            const double* vj = S + (size_t)d.ut[j] * T + p0;
+            const double* cj = scoef + d.cbase[j];
+            double v[PPT];
+#pragma unroll
+            for (int u = 0; u < PPT; ++u) v[u] = vj[CONS * u];
+            if (j < d.nin0) {
+#pragma unroll
+              for (int q = 0; q < H; ++q) {
+                const double c = cj[q];
+#pragma unroll
+                for (int u = 0; u < PPT; ++u) o[u][q] = dadd(o[u][q], dmul(c, v[u]));
+              }
+            } else {
+#pragma unroll
+              for (int q = H; q < NOUT; ++q) {
+                const double c = cj[q];
+#pragma unroll
+                for (int u = 0; u < PPT; ++u) o[u][q] = dadd(o[u][q], dmul(c, v[u]));
+              }
+            }
+          }
+        }
+        for (int j = 0; j < (SPLIT ? 0 : d.nin); ++j) {
           const double* vj = S + (size_t)d.ut[j] * T + p0;
           const unsigned m = d.mask[j];
           const double* cj = scoef + d.cbase[j];
@@ -563,21 +591,30 @@ void allow_smem(K kernel) {
   CK(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
 }
 
-template <int NOUT, int MAXD, int PPT>
+template <int NOUT, int MAXD, int PPT, bool SPLIT>
 void launch_upd_t(Ctx& c, const UpdDesc& d, size_t smem, int G) {
   static bool attr = false;
-  if (!attr) allow_smem(k_upd<NOUT, MAXD, PPT>), attr = true;
-  launch_k(c, k_upd<NOUT, MAXD, PPT>, G, THREADS, smem, d);
+  if (!attr) allow_smem(k_upd<NOUT, MAXD, PPT, SPLIT>), attr = true;
+  launch_k(c, k_upd<NOUT, MAXD, PPT, SPLIT>, G, THREADS, smem, d);
+}
+
+template <int NOUT, int MAXD, int PPT>
+void launch_upd_s(Ctx& c, const UpdDesc& d, size_t smem, int G) {
+  // the half-split form exists for the s-Omin block update shapes (2s outputs, s = 1, 2, 4, 8)
+  if constexpr (NOUT == 2 || NOUT == 4 || NOUT == 8 || NOUT == 16) {
+    if (d.nin0 >= 0) return launch_upd_t<NOUT, MAXD, PPT, true>(c, d, smem, G);
+  }
+  launch_upd_t<NOUT, MAXD, PPT, false>(c, d, smem, G);
 }
 
 template <int NOUT, int PPT>
 void launch_upd_d(Ctx& c, const UpdDesc& d, size_t smem, int G, int maxd) {
   switch (maxd) {
-    case 0: launch_upd_t<NOUT, 0, PPT>(c, d, smem, G); break;
-    case 1: launch_upd_t<NOUT, 1, PPT>(c, d, smem, G); break;
-    case 4: launch_upd_t<NOUT, 4, PPT>(c, d, smem, G); break;
-    case 16: launch_upd_t<NOUT, 16, PPT>(c, d, smem, G); break;
-    default: launch_upd_t<NOUT, 64, PPT>(c, d, smem, G); break;
+    case 0: launch_upd_s<NOUT, 0, PPT>(c, d, smem, G); break;
+    case 1: launch_upd_s<NOUT, 1, PPT>(c, d, smem, G); break;
+    case 4: launch_upd_s<NOUT, 4, PPT>(c, d, smem, G); break;
+    case 16: launch_upd_s<NOUT, 16, PPT>(c, d, smem, G); break;
+    default: launch_upd_s<NOUT, 64, PPT>(c, d, smem, G); break;
   }
 }
 
@@ -668,10 +705,34 @@ void launch_lincomb(Ctx& c, const LinDesc& L, const char* name) {
       d.out[q] = pad;
     }
   }
-  for (int j = 0; j < L.nin; ++j) {
-    d.ut[j] = (uint8_t)add_unique(d.U, nu, UPD_MAXU, L.in[j]);
-    d.mask[j] = L.mask[j];
-    d.cbase[j] = L.cbase[j];
+  // half-split shape: every term feeds exactly the first or the second half of the outputs
+  // (s-Omin's P / AP block update).  Terms are then ordered low half first, each half in its
+  // original order -- the per-output accumulation order is unchanged.
+  d.nin0 = -1;
+  if (nout_t == L.nout && L.nout % 2 == 0 && L.nout >= 2) {
+    const unsigned lo = (1u << (L.nout / 2)) - 1u, hi = lo << (L.nout / 2);
+    bool split = true;
+    for (int j = 0; j < L.nin && split; ++j) split = L.mask[j] == lo || L.mask[j] == hi;
+    if (split) {
+      int w = 0;
+      for (int pass = 0; pass < 2; ++pass)
+        for (int j = 0; j < L.nin; ++j)
+          if ((L.mask[j] == lo) == (pass == 0)) {
+            d.ut[w] = (uint8_t)add_unique(d.U, nu, UPD_MAXU, L.in[j]);
+            d.mask[w] = L.mask[j];
+            d.cbase[w] = L.cbase[j];
+            ++w;
+          }
+      d.nin0 = 0;
+      for (int j = 0; j < L.nin; ++j) d.nin0 += L.mask[j] == lo;
+    }
+  }
+  if (d.nin0 < 0) {
+    for (int j = 0; j < L.nin; ++j) {
+      d.ut[j] = (uint8_t)add_unique(d.U, nu, UPD_MAXU, L.in[j]);
+      d.mask[j] = L.mask[j];
+      d.cbase[j] = L.cbase[j];
+    }
   }
   for (int x = 0; x < L.nx; ++x) d.ux[x] = (uint8_t)add_unique(d.U, nu, UPD_MAXU, L.xin[x]);
   for (int k = 0; k < L.nd; ++k) {  // value ids: outputs, then extras at NOUT + x
@@ -683,7 +744,7 @@ void launch_lincomb(Ctx& c, const LinDesc& L, const char* name) {
   d.partials = L.partials;
   d.dot0 = L.dot0;
   d.G = L.G;
-  const size_t prefix = 8 * ((size_t)((L.ncoef + 15) & ~15) + (maxd ? (size_t)(nout_t + LC_MAXX) * CONS : 0));
+  const size_t prefix = 8 * ((size_t)((L.ncoef + 15) & ~15) + (maxd ? (size_t)(nout_t + L.nx) * CONS : 0));
   // k_upd covers T <= CONS * PPT points per tile (powers of two only).  A tile of at least CONS
   // points keeps every consumer thread busy (one point each) -- worth one CTA per SM with
   // fewer stages for wide updates (the seed and x updates stream up to 4 + m s vectors).
