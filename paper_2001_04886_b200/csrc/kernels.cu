@@ -26,6 +26,46 @@ __global__ void __launch_bounds__(256) k_apply(const __grid_constant__ DevOp op,
   y[p] = stencil_point<DIM, KIND>(op, x, i, j, l);
 }
 
+// 3D constant stencil, z-marching: a 32 x 8 thread tile of (x, y) columns walks KZ planes; the
+// -z / centre / +z values of a column stay in registers (one new plane load per point), the
+// x / y neighbours come through L1.  Same arithmetic order as stencil_point.
+constexpr int AZ_TX = 32, AZ_TY = 8, AZ_KZ = 16;
+__global__ void __launch_bounds__(AZ_TX* AZ_TY) k_apply3z(const __grid_constant__ DevOp op,
+                                                         const double* __restrict__ x, double* __restrict__ y,
+                                                         const int* halt, const int* cond) {
+  SKC_PDL_ENTRY();
+  if (skip_launch(halt, cond)) return;
+  const int nx = (int)op.nx, ny = (int)op.ny, nz = (int)op.nz;
+  const int i = blockIdx.x * AZ_TX + threadIdx.x % AZ_TX;
+  const int j = blockIdx.y * AZ_TY + threadIdx.x / AZ_TX;
+  if (i >= nx || j >= ny) return;
+  const int l0 = blockIdx.z * AZ_KZ, l1 = min(nz, l0 + AZ_KZ);
+  const int64_t plane = (int64_t)nx * ny;
+  const double c0 = op.coef[0], c1 = op.coef[1], c2 = op.coef[2], c3 = op.coef[3], c4 = op.coef[4],
+               c5 = op.coef[5], c6 = op.coef[6];
+  const bool hW = i > 0, hE = i + 1 < nx, hS = j > 0, hN = j + 1 < ny;
+  const double* col = x + (int64_t)j * nx + i;
+  double zm = l0 > 0 ? __ldg(col + (int64_t)(l0 - 1) * plane) : 0.0;
+  double zc = __ldg(col + (int64_t)l0 * plane);
+  for (int l = l0; l < l1; ++l) {
+    const double* pc = col + (int64_t)l * plane;
+    const double zp = l + 1 < nz ? __ldg(pc + plane) : 0.0;
+    const double vs = hS ? __ldg(pc - nx) : 0.0, vw = hW ? __ldg(pc - 1) : 0.0;
+    const double ve = hE ? __ldg(pc + 1) : 0.0, vn = hN ? __ldg(pc + nx) : 0.0;
+    double a = 0.0;
+    if (l > 0) a = __dadd_rn(a, __dmul_rn(c0, zm));
+    if (hS) a = __dadd_rn(a, __dmul_rn(c1, vs));
+    if (hW) a = __dadd_rn(a, __dmul_rn(c2, vw));
+    a = __dadd_rn(a, __dmul_rn(c3, zc));
+    if (hE) a = __dadd_rn(a, __dmul_rn(c4, ve));
+    if (hN) a = __dadd_rn(a, __dmul_rn(c5, vn));
+    if (l + 1 < nz) a = __dadd_rn(a, __dmul_rn(c6, zp));
+    y[(int64_t)l * plane + (int64_t)j * nx + i] = a;
+    zm = zc;
+    zc = zp;
+  }
+}
+
 __global__ void __launch_bounds__(256) k_apply_csr(const __grid_constant__ DevOp op, const double* __restrict__ x,
                                                    double* __restrict__ y, const int* halt, const int* cond) {
   SKC_PDL_ENTRY();
@@ -57,7 +97,12 @@ void launch_apply(Ctx& c, const DevOp& op, const double* x, double* y, const int
       case 21: launch_k(c, k_apply<2, kStencilConst>, grid, 256, 0, op, x, y, halt, cond); break;
       case 22: launch_k(c, k_apply<2, kStencilVarK>, grid, 256, 0, op, x, y, halt, cond); break;
       case 23: launch_k(c, k_apply<2, kStencilDia>, grid, 256, 0, op, x, y, halt, cond); break;
-      case 31: launch_k(c, k_apply<3, kStencilConst>, grid, 256, 0, op, x, y, halt, cond); break;
+      case 31: {
+        const dim3 gz((unsigned)((op.nx + AZ_TX - 1) / AZ_TX), (unsigned)((op.ny + AZ_TY - 1) / AZ_TY),
+                      (unsigned)((op.nz + AZ_KZ - 1) / AZ_KZ));
+        launch_k(c, k_apply3z, gz, AZ_TX * AZ_TY, 0, op, x, y, halt, cond);
+        break;
+      }
       case 32: launch_k(c, k_apply<3, kStencilVarK>, grid, 256, 0, op, x, y, halt, cond); break;
       case 33: launch_k(c, k_apply<3, kStencilDia>, grid, 256, 0, op, x, y, halt, cond); break;
       default: fail(SKC_EINVAL, "apply: unsupported operator kind");
