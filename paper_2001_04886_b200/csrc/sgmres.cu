@@ -34,6 +34,8 @@ struct ArnState {
   int block;   // block iteration that stopped the cycle
   int reorth;  // reorthogonalization flag of the current block iteration
   double rn;   // latest residual norm (also the constructor's ||r||)
+  int zready;  // the last block iteration's cross pass produced the next z and its products
+  int pad;
 };
 
 // record layout per block iteration k (0 = constructor)
@@ -85,6 +87,7 @@ __global__ void k_arn_ctor(ArnState* st, int use_rn, const double* partials, int
     st->halt = 0;
     st->block = 0;
     st->reorth = 0;
+    st->zready = 0;
     const double nv = use_rn ? st->rn : sqrt(v[0]);
     rec0[RecLayout::kZn] = nv;
     if (!(nv > 0.0)) {
@@ -226,8 +229,8 @@ __global__ void k_arn_check(ArnState* st, const Gram* grams, int k, double* rec,
 // so all CTAs take identical coefficients and the same reorthogonalization decision; CTA 0
 // writes the records and the device flags.
 constexpr int ORTH_NT = 512;
-// points per thread per iteration, all their loads issued first (MGS update / cross products)
-constexpr int ORTH_UU = 2, ORTH_UC = 4;
+// points per thread per iteration, all their loads issued first (Scalar1 products, seed)
+constexpr int ORTH_UC = 4;
 constexpr size_t kOrthSmemCap = 220 * 1024;  // <= the 226 KB dynamic limit set at launch
 // reduced-product capacity: the cross test needs (k+1) s^2, a round s(s-1); even count keeps
 // the Gram copy 16-byte aligned
@@ -236,6 +239,7 @@ constexpr int kStepH = 64 * kMaxS;  // -h coefficients of Scalar1 (k s <= 512)
 
 struct OrthDesc {
   int s, k, build_next;
+  int zfuse;              // form the next iteration's z and Scalar1 products in the cross pass
   int64_t n, P;           // points, points per CTA
   DevOp op;
   const double* vin;      // v_{k-1}^{s-1}: z = A vin
@@ -282,6 +286,26 @@ __device__ __forceinline__ void orth_store(const double (&acc)[K], double* red, 
   __syncthreads();
 }
 
+// as orth_store, products q < K1 to partials d0 + q and the rest to d1 + (q - K1)
+template <int K, int K1>
+__device__ __forceinline__ void orth_store2(const double (&acc)[K], double* red, double* partials, int d0, int d1) {
+  constexpr int NW = ORTH_NT / 32;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int q = 0; q < K; ++q) {
+    const double v = warp_sum(acc[q]);
+    if (lane == 0) red[warp * K + q] = v;
+  }
+  __syncthreads();
+  if (threadIdx.x < K) {
+    double s = 0.0;
+    for (int w = 0; w < NW; ++w) s += red[w * K + threadIdx.x];
+    const int q = threadIdx.x;
+    partials[(int64_t)(q < K1 ? d0 + q : d1 + (q - K1)) * kPartialPitch + blockIdx.x] = s;
+  }
+  __syncthreads();
+}
+
 template <int S>
 __global__ void __launch_bounds__(ORTH_NT, 1) k_arn_step(const __grid_constant__ OrthDesc d) {
   SKC_PDL_ENTRY();
@@ -290,14 +314,15 @@ __global__ void __launch_bounds__(ORTH_NT, 1) k_arn_step(const __grid_constant__
   cg::grid_group grid = cg::this_grid();
   constexpr int NC = S - 1;
   extern __shared__ __align__(16) double dsm[];
-  // coefficients -t [64] | reduced products [(k+1) s^2] | Gram copy | reduction scratch
-  // [32 warps][s^2] | candidate slice [s-1][P]
+  // coefficients -t [64] | reduced products [(k+1) s^2] | Gram scratch | Gram factors of the
+  // k blocks | reduction scratch [16 warps][s^2 + s] | candidate slice [s-1][P]
   double* tc = dsm;
   double* hc = dsm + 64;
   double* prod = hc + kStepH;
   Gram* gs = reinterpret_cast<Gram*>(prod + orth_prod_cap(d.k, S));
-  double* red = reinterpret_cast<double*>(gs + 1);
-  double* sc = red + (ORTH_NT / 32) * S * S;
+  Gram* gk = gs + 1;
+  double* red = reinterpret_cast<double*>(gk + d.k);
+  double* sc = red + (ORTH_NT / 32) * (S * S + S);
   __shared__ int exceed[64];
   __shared__ int s_first;
   const int tid = threadIdx.x;
@@ -310,18 +335,13 @@ __global__ void __launch_bounds__(ORTH_NT, 1) k_arn_step(const __grid_constant__
 
   // Scalar2 for block i from partials (src, srcG): every CTA solves W_i t = V_i^T cand[:,1:]
   auto scalar = [&](int i, int src, int srcG, int accumulate) {
-    {
-      const uint64_t* gsrc = reinterpret_cast<const uint64_t*>(d.grams + i);
-      uint64_t* gdst = reinterpret_cast<uint64_t*>(gs);
-      for (int w = tid; w < (int)(sizeof(Gram) / 8); w += ORTH_NT) gdst[w] = gsrc[w];
-    }
     reduce_dots_dev(d.partials, srcG, src, S * NC, prod);  // ends with __syncthreads
     if (tid < NC) {
       const int jc = tid;
       double rhs[kMaxS], t[kMaxS];
 #pragma unroll
       for (int l = 0; l < S; ++l) rhs[l] = prod[l * NC + jc];
-      gram_solve(*gs, rhs, t);
+      gram_solve(gk[i], rhs, t);
 #pragma unroll
       for (int l = 0; l < S; ++l) {
         tc[l * NC + jc] = -t[l];
@@ -338,7 +358,7 @@ __global__ void __launch_bounds__(ORTH_NT, 1) k_arn_step(const __grid_constant__
   // Points go in pairs (p, p + NT) with every basis load of the pair issued before the
   // arithmetic, so each thread keeps 2s (4s with the products) loads in flight; the products
   // still accumulate in ascending point order.
-  auto round = [&](int i, int dst) {
+  auto round = [&](int i, int dst, bool wb) {
     const bool dots = i + 1 < d.k;
     const double* Vi = colp(i, 0);
     const double* Vn = colp(dots ? i + 1 : i, 0);
@@ -346,11 +366,12 @@ __global__ void __launch_bounds__(ORTH_NT, 1) k_arn_step(const __grid_constant__
     double acc[S * NC];
 #pragma unroll
     for (int q = 0; q < S * NC; ++q) acc[q] = 0.0;
-    for (int p0 = tid; p0 < cnt; p0 += ORTH_UU * ORTH_NT) {
-      bool has[ORTH_UU];
-      double v[ORTH_UU][S], w[ORTH_UU][S], cv[ORTH_UU][NC];
+    constexpr int UU = S <= 3 ? 4 : S == 4 ? 3 : S <= 6 ? 2 : 1;
+    for (int p0 = tid; p0 < cnt; p0 += UU * ORTH_NT) {
+      bool has[UU];
+      double v[UU][S], w[UU][S], cv[UU][NC];
 #pragma unroll
-      for (int u = 0; u < ORTH_UU; ++u) {
+      for (int u = 0; u < UU; ++u) {
         const int p = p0 + u * ORTH_NT;
         has[u] = p < cnt;
 #pragma unroll
@@ -360,7 +381,7 @@ __global__ void __launch_bounds__(ORTH_NT, 1) k_arn_step(const __grid_constant__
         }
       }
 #pragma unroll
-      for (int u = 0; u < ORTH_UU; ++u)
+      for (int u = 0; u < UU; ++u)
 #pragma unroll
         for (int j = 0; j < NC; ++j) cv[u][j] = has[u] ? sc[(int64_t)j * d.P + p0 + u * ORTH_NT] : 0.0;
 #pragma unroll
@@ -369,13 +390,17 @@ __global__ void __launch_bounds__(ORTH_NT, 1) k_arn_step(const __grid_constant__
         for (int j = 0; j < NC; ++j) {
           const double t = tc[l * NC + j];
 #pragma unroll
-          for (int u = 0; u < ORTH_UU; ++u) cv[u][j] = dadd(cv[u][j], dmul(t, v[u][l]));
+          for (int u = 0; u < UU; ++u) cv[u][j] = dadd(cv[u][j], dmul(t, v[u][l]));
         }
 #pragma unroll
-      for (int u = 0; u < ORTH_UU; ++u) {
+      for (int u = 0; u < UU; ++u) {
         if (!has[u]) continue;
 #pragma unroll
         for (int j = 0; j < NC; ++j) sc[(int64_t)j * d.P + p0 + u * ORTH_NT] = cv[u][j];
+        if (wb) {
+#pragma unroll
+          for (int j = 0; j < NC; ++j) d.cand[j + 1][base + p0 + u * ORTH_NT] = cv[u][j];
+        }
         if (dots) {
 #pragma unroll
           for (int l = 0; l < S; ++l)
@@ -388,44 +413,63 @@ __global__ void __launch_bounds__(ORTH_NT, 1) k_arn_step(const __grid_constant__
   };
 
   // L-block products with the full candidate: lhs(l) . cand[:,jc] for one block of s columns
-  // (block i of the basis, or the candidate itself when i == k) -> partials d0 + l*s + jc
-  auto cross_block = [&](int i, int d0) {
-    double acc[S * S];
+  // (block i of the basis, or the candidate itself when i == k) -> partials d0 + l*s + jc.
+  // With ZD also lhs(l) . z -> partials dz0 + l: the next block iteration's Scalar1 products
+  // (z = A cand[:,s-1] of the final candidate, in memory at zg)
+  auto cross_block = [&](auto zd, int i, int d0, int dz0) {
+    constexpr bool ZD = decltype(zd)::value;
+    // points per thread in flight, bounded by the accumulator count (no spills at 128 registers)
+    constexpr int U = ZD ? (S <= 3 ? 4 : S == 4 ? 3 : S <= 6 ? 2 : 1) : (S <= 4 ? 4 : S <= 6 ? 2 : 1);
+    constexpr int NA = S * S + (ZD ? S : 0);
+    double acc[NA];
 #pragma unroll
-    for (int q = 0; q < S * S; ++q) acc[q] = 0.0;
+    for (int q = 0; q < NA; ++q) acc[q] = 0.0;
     const double* c0p = d.cand0 + base;
+    const double* zg = d.z + base;
     const bool basis = i < d.k;
     const double* Li = basis ? colp(i, 0) : c0p;
     const int64_t np = d.np;
-    for (int p0 = tid; p0 < cnt; p0 += ORTH_UC * ORTH_NT) {
-      bool has[ORTH_UC];
-      double a[ORTH_UC][S], b[ORTH_UC][S];
+    for (int p0 = tid; p0 < cnt; p0 += U * ORTH_NT) {
+      bool has[U];
+      double a[U][S], b[U][S], zv[U];
 #pragma unroll
-      for (int u = 0; u < ORTH_UC; ++u) {
+      for (int u = 0; u < U; ++u) {
         const int p = p0 + u * ORTH_NT;
         has[u] = p < cnt;
         b[u][0] = has[u] ? c0p[p] : 0.0;
+        zv[u] = ZD && has[u] ? zg[p] : 0.0;
 #pragma unroll
         for (int l = 0; l < S; ++l) a[u][l] = basis && has[u] ? Li[l * np + p] : 0.0;
 #pragma unroll
         for (int j = 1; j < S; ++j) b[u][j] = has[u] ? sc[(int64_t)(j - 1) * d.P + p] : 0.0;
       }
 #pragma unroll
-      for (int u = 0; u < ORTH_UC; ++u) {
+      for (int u = 0; u < U; ++u) {
         if (!has[u]) continue;
 #pragma unroll
         for (int l = 0; l < S; ++l) {
           const double av = basis ? a[u][l] : b[u][l];
 #pragma unroll
           for (int jc = 0; jc < S; ++jc) acc[l * S + jc] = fma(av, b[u][jc], acc[l * S + jc]);
+          if constexpr (ZD) acc[S * S + l] = fma(av, zv[u], acc[S * S + l]);
         }
       }
     }
-    orth_store(acc, red, d.partials, d0);
+    orth_store2<NA, S * S>(acc, red, d.partials, d0, dz0);
   };
 
   const int K = d.k;
   const int64_t np = d.np;
+  // the previous block iteration's cross pass already produced z (in memory) and this
+  // iteration's Scalar1 products (partials dz), unless it ran a reorthogonalization pass
+  const bool zready = d.zfuse && K > 1 && __ldg(&d.st->zready) != 0;
+  // the k Gram factors into shared memory (asynchronous; waited for before Scalar1)
+  {
+    const char* gsrc = reinterpret_cast<const char*>(d.grams);
+    char* gdst = reinterpret_cast<char*>(gk);
+    for (int w = tid; w < (int)(K * sizeof(Gram) / 8); w += ORTH_NT) cp_async8(gdst + 8 * w, gsrc + 8 * w, true);
+    cp_async_commit();
+  }
   orth_mark(d, 39);
   // ---- z = A v_{k-1}^{s-1} on this slice (the source is stable; neighbours read from memory)
   // y = A x on this slice; xs (optional) is this slice of x in shared memory, read in place of
@@ -443,6 +487,12 @@ __global__ void __launch_bounds__(ORTH_NT, 1) k_arn_step(const __grid_constant__
         const double v = xs && o >= 0 && o < cnt ? xs[o] : xb[o];
         return xscale != 0.0 ? __dmul_rn(v, xscale) : v;
       };
+      const uint32_t xs32 = xs ? smem_u32(xs) : 0u;
+      auto gets = [&](int o) {  // (o inside the slice)
+        double v;
+        asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(xs32 + 8u * (uint32_t)o));
+        return xscale != 0.0 ? __dmul_rn(v, xscale) : v;
+      };
       // four points per thread per iteration, every neighbour load issued before the sums
       constexpr int U = 4;
       int i[U], jr[U];
@@ -457,11 +507,20 @@ __global__ void __launch_bounds__(ORTH_NT, 1) k_arn_step(const __grid_constant__
         for (int u = 0; u < U; ++u) {
           const int p = p0 + u * ORTH_NT;
           const bool in = p < cnt;
-          vs[u] = in && jr[u] > 0 ? get(p - nx) : 0.0;
-          vw[u] = in && i[u] > 0 ? get(p - 1) : 0.0;
-          vc[u] = in ? get(p) : 0.0;
-          ve[u] = in && i[u] + 1 < nx ? get(p + 1) : 0.0;
-          vn[u] = in && jr[u] + 1 < ny ? get(p + nx) : 0.0;
+          if (xs && in && p >= nx && p + nx < cnt && i[u] > 0 && i[u] + 1 < nx) {
+            // interior of the slice: every neighbour present and in shared memory
+            vs[u] = gets(p - nx);
+            vw[u] = gets(p - 1);
+            vc[u] = gets(p);
+            ve[u] = gets(p + 1);
+            vn[u] = gets(p + nx);
+          } else {
+            vs[u] = in && jr[u] > 0 ? get(p - nx) : 0.0;
+            vw[u] = in && i[u] > 0 ? get(p - 1) : 0.0;
+            vc[u] = in ? get(p) : 0.0;
+            ve[u] = in && i[u] + 1 < nx ? get(p + 1) : 0.0;
+            vn[u] = in && jr[u] + 1 < ny ? get(p + nx) : 0.0;
+          }
         }
 #pragma unroll
         for (int u = 0; u < U; ++u) {
@@ -495,13 +554,18 @@ __global__ void __launch_bounds__(ORTH_NT, 1) k_arn_step(const __grid_constant__
   // the powers reach them; with s = 2 seed also goes to memory for its neighbours)
   double* zs = sc;
   double* seeds = S > 2 ? sc + (int64_t)(S - 2) * d.P : nullptr;
-  apply_slice(d.vin, nullptr, 0.0, [&](int p, double v, double) { zs[p] = v; });
+  if (zready) {
+    for (int p = tid; p < cnt; p += ORTH_NT) zs[p] = d.z[base + p];
+  } else {
+    apply_slice(d.vin, nullptr, 0.0, [&](int p, double v, double) { zs[p] = v; });
+  }
   orth_mark(d, 40);
   // ---- Scalar1 products V_i^T z (i < k) -> dz + i s + l, and z.z -> dz + k s (each thread
-  //      reads back its own z)
-  {
+  //      reads back its own z); blocks in descending order, so the seed sweep's first blocks
+  //      are still in L2
+  if (!zready) {
     double zz[1] = {0.0};
-    for (int i = 0; i < K; ++i) {
+    for (int i = K - 1; i >= 0; --i) {
       double acc[S];
 #pragma unroll
       for (int q = 0; q < S; ++q) acc[q] = 0.0;
@@ -530,17 +594,10 @@ __global__ void __launch_bounds__(ORTH_NT, 1) k_arn_step(const __grid_constant__
   }
   orth_mark(d, 6);
   grid.sync();
-  // ---- Scalar1 (sstep.hpp:301-310): zn, h_i = W_i^{-1} V_i^T z in every CTA; CTA 0 records
-  // Gram factors of the k blocks into candidate column 1 of shared memory (free until the seed
-  // sweep; column 0 holds z) when it is large enough: the serial solves then read them at
-  // shared-memory latency
-  const bool gram_smem = S > 2 && (int64_t)K * (int64_t)sizeof(Gram) <= d.P * 8;
-  const Gram* gk = gram_smem ? reinterpret_cast<const Gram*>(sc + d.P) : d.grams;
-  if (gram_smem) {
-    const uint64_t* gsrc = reinterpret_cast<const uint64_t*>(d.grams);
-    uint64_t* gdst = reinterpret_cast<uint64_t*>(sc + d.P);
-    for (int w = tid; w < (int)(K * sizeof(Gram) / 8); w += ORTH_NT) gdst[w] = gsrc[w];
-  }
+  // ---- Scalar1 (sstep.hpp:301-310): zn, h_i = W_i^{-1} V_i^T z in every CTA (Gram factors
+  // from shared memory); CTA 0 records
+  cp_async_wait<0>();
+  __syncthreads();
   reduce_dots_dev(d.partials, G, d.dz, K * S + 1, prod);  // (ends with __syncthreads)
   const double zn = sqrt(prod[K * S]);
   if (blockIdx.x == 0 && tid == 0) {
@@ -560,20 +617,38 @@ __global__ void __launch_bounds__(ORTH_NT, 1) k_arn_step(const __grid_constant__
   }
   __syncthreads();
   orth_mark(d, 41);
-  // ---- seed = z - sum_i V_i h_i (terms in block order, multiply and add rounded separately)
-  //      and ||seed||^2
+  // ---- seed = z - sum_i V_i h_i (terms in block order, multiply and add rounded separately),
+  //      one sweep per block with the running sum in shared memory (every point stays with
+  //      its thread), then ||seed||^2
   {
+    for (int i = 0; i < K; ++i) {
+      const double* Vi = colp(i, 0);
+      double hl[S];
+#pragma unroll
+      for (int l = 0; l < S; ++l) hl[l] = hc[i * S + l];
+      for (int p0 = tid; p0 < cnt; p0 += ORTH_UC * ORTH_NT) {
+        double v[ORTH_UC][S], o[ORTH_UC];
+#pragma unroll
+        for (int u = 0; u < ORTH_UC; ++u) {
+          const int p = p0 + u * ORTH_NT;
+          const bool h = p < cnt;
+          o[u] = h ? zs[p] : 0.0;
+#pragma unroll
+          for (int l = 0; l < S; ++l) v[u][l] = h ? Vi[l * np + p] : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < ORTH_UC; ++u) {
+          const int p = p0 + u * ORTH_NT;
+          if (p >= cnt) continue;
+#pragma unroll
+          for (int l = 0; l < S; ++l) o[u] = dadd(o[u], dmul(hl[l], v[u][l]));
+          zs[p] = o[u];
+        }
+      }
+    }
     double acc[1] = {0.0};
     for (int p = tid; p < cnt; p += ORTH_NT) {
-      double o = zs[p];
-      for (int i = 0; i < K; ++i) {
-        const double* Vi = colp(i, 0);
-        double v[S];
-#pragma unroll
-        for (int l = 0; l < S; ++l) v[l] = Vi[l * np + p];
-#pragma unroll
-        for (int l = 0; l < S; ++l) o = dadd(o, dmul(hc[i * S + l], v[l]));
-      }
+      const double o = zs[p];
       d.seed[base + p] = o;
       if (seeds) seeds[p] = o;
       acc[0] = fma(o, o, acc[0]);
@@ -635,17 +710,36 @@ __global__ void __launch_bounds__(ORTH_NT, 1) k_arn_step(const __grid_constant__
   }
   grid.sync();
   orth_mark(d, 0);
-  // ---- pass 0
+  // ---- pass 0; the last round also writes the candidate back (final unless a second pass
+  //      runs) and, with zfuse, is followed by a barrier so z = A cand[:,s-1] can be formed
   for (int i = 0; i < K; ++i) {
     scalar(i, (i & 1) ? d.dr1 : d.dr0, G, 0);
     orth_mark(d, 8 + 3 * i);
-    round(i, ((i + 1) & 1) ? d.dr1 : d.dr0);
+    round(i, ((i + 1) & 1) ? d.dr1 : d.dr0, i + 1 == K);
     orth_mark(d, 9 + 3 * i);
-    if (i + 1 < K) grid.sync();
+    if (i + 1 < K || d.zfuse) grid.sync();
     orth_mark(d, 10 + 3 * i);
   }
-  // ---- cross products and W (needs_reorth, sstep.hpp:401-414)
-  for (int i = 0; i <= K; ++i) cross_block(i, d.dcross + i * S * S);
+  // ---- the next block iteration's z = A cand[:,s-1] (to memory) and z.z -> dz + (k+1) s
+  if (d.zfuse) {
+    double zz[1] = {0.0};
+    double* zg = d.z + base;
+    apply_slice(d.cand[S - 1], sc + (int64_t)(S - 2) * d.P, 0.0, [&](int p, double v, double) {
+      zg[p] = v;
+      zz[0] = fma(v, v, zz[0]);
+    });
+    orth_store(zz, red, d.partials, d.dz + (K + 1) * S);
+  }
+  orth_mark(d, 60);
+  // ---- cross products and W (needs_reorth, sstep.hpp:401-414), with zfuse also the next
+  //      iteration's Scalar1 products [V_0..V_{k-1}, cand]^T z; blocks in descending order (the
+  //      last rounds' blocks are still in L2, and the next seed sweep starts at block 0)
+  for (int i = K; i >= 0; --i) {
+    if (d.zfuse)
+      cross_block(std::true_type{}, i, d.dcross + i * S * S, d.dz + i * S);
+    else
+      cross_block(std::false_type{}, i, d.dcross + i * S * S, 0);
+  }
   orth_mark(d, 1);
   grid.sync();
   orth_mark(d, 2);
@@ -658,7 +752,7 @@ __global__ void __launch_bounds__(ORTH_NT, 1) k_arn_step(const __grid_constant__
       const double* cr = prod + i * S * S;
       double acc = 0.0;
       for (int q = 0; q < S * S; ++q) acc += cr[q] * cr[q];
-      exceed[i] = sqrt(acc) > d.orth_tol * sqrt(sd_trace(d.grams[i].w, S)) * sqrt(cn2);
+      exceed[i] = sqrt(acc) > d.orth_tol * sqrt(sd_trace(gk[i].w, S)) * sqrt(cn2);
     }
     __syncthreads();
     if (tid == 0) {
@@ -673,6 +767,7 @@ __global__ void __launch_bounds__(ORTH_NT, 1) k_arn_step(const __grid_constant__
         d.rec[RecLayout::kFirst] = first;
         d.rec[RecLayout::kReorth] = first >= 0 ? 1.0 : 0.0;
         d.st->reorth = first >= 0;
+        d.st->zready = d.zfuse && first < 0;
       }
     }
     __syncthreads();
@@ -700,16 +795,13 @@ __global__ void __launch_bounds__(ORTH_NT, 1) k_arn_step(const __grid_constant__
     grid.sync();
     for (int i = 0; i < K; ++i) {
       scalar(i, (i & 1) ? d.dr1 : d.dr0, G, 1);
-      round(i, ((i + 1) & 1) ? d.dr1 : d.dr0);
+      round(i, ((i + 1) & 1) ? d.dr1 : d.dr0, i + 1 == K);
       if (i + 1 < K) grid.sync();
     }
-    cross_block(K, d.dwb);
+    cross_block(std::false_type{}, K, d.dwb, 0);
     grid.sync();
   }
   orth_mark(d, 4);
-  // write the candidate columns back
-  for (int j = 0; j < NC; ++j)
-    for (int p = tid; p < cnt; p += ORTH_NT) d.cand[j + 1][base + p] = sc[(int64_t)j * d.P + p];
   // ---- push_block of the new block (CTA 0): W from the pass that produced it
   if (blockIdx.x == 0) {
     reduce_dots_dev(d.partials, G, s_first >= 0 ? d.dwb : d.dcross + K * S * S, S * S, prod);
@@ -726,7 +818,8 @@ __global__ void __launch_bounds__(ORTH_NT, 1) k_arn_step(const __grid_constant__
 }
 
 size_t orth_smem(int s, int k, int64_t P) {
-  return sizeof(double) * (64 + kStepH + (size_t)orth_prod_cap(k, s)) + sizeof(Gram) + sizeof(double) * (ORTH_NT / 32) * s * s +
+  return sizeof(double) * (64 + kStepH + (size_t)orth_prod_cap(k, s)) + sizeof(Gram) * (1 + (size_t)k) +
+         sizeof(double) * (ORTH_NT / 32) * (s * s + s) +
          sizeof(double) * (size_t)(s - 1) * (size_t)P;
 }
 
@@ -1014,6 +1107,11 @@ struct Engine {
     d.s = s;
     d.k = k;
     d.build_next = build_next ? 1 : 0;
+    static const int zfuse_env = [] {
+      const char* e = std::getenv("SKC_ZFUSE");
+      return e ? std::atoi(e) : 1;
+    }();
+    d.zfuse = build_next && zfuse_env ? 1 : 0;
     d.n = op.n;
     d.P = orth_points();
     d.op = op.d;
@@ -1071,7 +1169,7 @@ struct Engine {
       for (int i = 0; i < k; ++i)
         std::fprintf(stderr, " (scal %.1f, upd %.1f, sync %.1f)", (t[8 + 3 * i] - (i ? t[7 + 3 * i] : t[0])) * 1e-3,
                      (t[9 + 3 * i] - t[8 + 3 * i]) * 1e-3, (t[10 + 3 * i] - t[9 + 3 * i]) * 1e-3);
-      std::fprintf(stderr, " | cross %.1f sync %.1f check %.1f pass1 %.1f write %.1f us\n", (t[1] - t[7 + 3 * k]) * 1e-3,
+      std::fprintf(stderr, " | znext %.1f cross %.1f sync %.1f check %.1f pass1 %.1f push %.1f us\n", (t[60] - t[7 + 3 * k]) * 1e-3, (t[1] - t[60]) * 1e-3,
                    (t[2] - t[1]) * 1e-3, (t[3] - t[2]) * 1e-3, (t[4] - t[3]) * 1e-3, (t[5] - t[4]) * 1e-3);
     }
   }
