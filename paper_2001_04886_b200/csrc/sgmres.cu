@@ -101,18 +101,34 @@ __global__ void k_arn_ctor(ArnState* st, int use_rn, const double* partials, int
 
 // push_block (sstep.hpp:392-399): W = gram_self(block) -> GramSolver; breakdown = collapse.
 // One thread, on the reduced s x s products v; the factor is built in g (scratch) and stored
-// to grams[k] by the caller when the status stays running.
-__device__ bool arn_push_body(ArnState* st, Gram& g, int k, double* rec, const double* v, int s) {
+// to grams[k] by the caller when the status stays running.  S > 0: compile-time order.
+template <int S = 0>
+__device__ bool arn_push_body(ArnState* st, Gram& g, int k, double* rec, const double* v, int s, bool record = true) {
   double W[kMaxS * kMaxS];
-  for (int q = 0; q < s * s; ++q) W[q] = v[q];
-  for (int j = 0; j < s; ++j)
-    for (int l = j + 1; l < s; ++l) {
-      const double avg = (W[j * s + l] + W[l * s + j]) / 2.0;
-      W[j * s + l] = avg;
-      W[l * s + j] = avg;
-    }
+  if constexpr (S > 0) {
+#pragma unroll
+    for (int q = 0; q < S * S; ++q) W[q] = v[q];
+#pragma unroll
+    for (int j = 0; j < S; ++j)
+#pragma unroll
+      for (int l = j + 1; l < S; ++l) {
+        const double avg = (W[j * S + l] + W[l * S + j]) / 2.0;
+        W[j * S + l] = avg;
+        W[l * S + j] = avg;
+      }
+    gram_factor_t<S>(g, W);
+  } else {
+    for (int q = 0; q < s * s; ++q) W[q] = v[q];
+    for (int j = 0; j < s; ++j)
+      for (int l = j + 1; l < s; ++l) {
+        const double avg = (W[j * s + l] + W[l * s + j]) / 2.0;
+        W[j * s + l] = avg;
+        W[l * s + j] = avg;
+      }
+    gram_factor(g, W, s);
+  }
+  if (!record) return g.ok;
   for (int q = 0; q < s * s; ++q) rec[RecLayout::kW + q] = W[q];
-  gram_factor(g, W, s);
   rec[RecLayout::kOk] = g.ok;
   rec[RecLayout::kRatio] = g.ratio;
   rec[RecLayout::kSing] = g.singular1;
@@ -253,11 +269,21 @@ struct OrthDesc {
   int dz, dseed, dr0, dr1, dcross, dwb;
   Gram* grams;
   double* rec;            // this block iteration's record
+  double* rec_push;       // the previous block iteration's record (its push_block)
   int rec_t, rec_h;
   ArnState* st;
   double orth_tol;
   unsigned long long* trace;  // optional phase timestamps (CTA 0), diagnostics
 };
+
+// per-CTA completion time of a phase (diagnostics): slot base + CTA index
+__device__ __forceinline__ void orth_mark_all(const OrthDesc& d, int base) {
+  if (d.trace && threadIdx.x == 0) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    d.trace[base + blockIdx.x] = t;
+  }
+}
 
 __device__ __forceinline__ void orth_mark(const OrthDesc& d, int slot) {
   if (d.trace && blockIdx.x == 0 && threadIdx.x == 0) {
@@ -341,7 +367,7 @@ __global__ void __launch_bounds__(ORTH_NT, 1) k_arn_step(const __grid_constant__
       double rhs[kMaxS], t[kMaxS];
 #pragma unroll
       for (int l = 0; l < S; ++l) rhs[l] = prod[l * NC + jc];
-      gram_solve(gk[i], rhs, t);
+      gram_solve_t<S>(gk[i], rhs, t);
 #pragma unroll
       for (int l = 0; l < S; ++l) {
         tc[l * NC + jc] = -t[l];
@@ -463,11 +489,18 @@ __global__ void __launch_bounds__(ORTH_NT, 1) k_arn_step(const __grid_constant__
   // the previous block iteration's cross pass already produced z (in memory) and this
   // iteration's Scalar1 products (partials dz), unless it ran a reorthogonalization pass
   const bool zready = d.zfuse && K > 1 && __ldg(&d.st->zready) != 0;
-  // the k Gram factors into shared memory (asynchronous; waited for before Scalar1)
+  // push_block of the previous block iteration's candidate (sstep.hpp:375, 392-399) runs here,
+  // off the previous kernel's tail: every CTA reduces its W (from the pass that produced the
+  // candidate) and factors it in the Scalar1 phase; CTA 0 records it and stores the factor
+  const bool push = K >= 2;
+  if (push) reduce_dots_dev(d.partials, G, __ldg(&d.st->reorth) ? d.dwb : d.dcross + (K - 1) * S * S, S * S, tc);
+  // the Gram factors of blocks 0..k-1 (k-2 with the push) into shared memory (asynchronous;
+  // waited for before Scalar1)
   {
     const char* gsrc = reinterpret_cast<const char*>(d.grams);
     char* gdst = reinterpret_cast<char*>(gk);
-    for (int w = tid; w < (int)(K * sizeof(Gram) / 8); w += ORTH_NT) cp_async8(gdst + 8 * w, gsrc + 8 * w, true);
+    for (int w = tid; w < (int)((push ? K - 1 : K) * sizeof(Gram) / 8); w += ORTH_NT)
+      cp_async8(gdst + 8 * w, gsrc + 8 * w, true);
     cp_async_commit();
   }
   orth_mark(d, 39);
@@ -593,23 +626,32 @@ __global__ void __launch_bounds__(ORTH_NT, 1) k_arn_step(const __grid_constant__
     orth_store(zz, red, d.partials, d.dz + K * S);
   }
   orth_mark(d, 6);
-  grid.sync();
+  orth_mark_all(d, 256);
+  if (!zready) grid.sync();  // (with zready the products come from the previous launch)
   // ---- Scalar1 (sstep.hpp:301-310): zn, h_i = W_i^{-1} V_i^T z in every CTA (Gram factors
   // from shared memory); CTA 0 records
   cp_async_wait<0>();
-  __syncthreads();
   reduce_dots_dev(d.partials, G, d.dz, K * S + 1, prod);  // (ends with __syncthreads)
+  if (push) {
+    __shared__ int s_push_ok;
+    if (tid == 0) {
+      const bool ok = arn_push_body<S>(d.st, gk[K - 1], K - 1, d.rec_push, tc, S, blockIdx.x == 0);
+      s_push_ok = ok;
+      if (ok && blockIdx.x == 0) d.grams[K - 1] = gk[K - 1];
+    }
+    __syncthreads();
+    if (!s_push_ok) return;  // basis collapse (identical decision in every CTA)
+  }
   const double zn = sqrt(prod[K * S]);
   if (blockIdx.x == 0 && tid == 0) {
     d.rec[RecLayout::kZn] = zn;
     d.rec[RecLayout::kReorth] = 0.0;
     d.rec[RecLayout::kFirst] = -1.0;
-    d.st->reorth = 0;
   }
   for (int i = tid; i < K; i += ORTH_NT) {
     double rhs[kMaxS], h[kMaxS];
     for (int l = 0; l < S; ++l) rhs[l] = prod[i * S + l];
-    gram_solve(gk[i], rhs, h);
+    gram_solve_t<S>(gk[i], rhs, h);
     for (int l = 0; l < S; ++l) {
       hc[i * S + l] = -h[l];
       if (blockIdx.x == 0) d.rec[d.rec_h + i * S + l] = h[l];
@@ -656,6 +698,7 @@ __global__ void __launch_bounds__(ORTH_NT, 1) k_arn_step(const __grid_constant__
     orth_store(acc, red, d.partials, d.dseed);
   }
   orth_mark(d, 7);
+  orth_mark_all(d, 512);
   grid.sync();
   // ---- nu = ||seed|| and the invariant-subspace test (sstep.hpp:315-324)
   reduce_dots_dev(d.partials, G, d.dseed, 1, prod);
@@ -741,6 +784,7 @@ __global__ void __launch_bounds__(ORTH_NT, 1) k_arn_step(const __grid_constant__
       cross_block(std::false_type{}, i, d.dcross + i * S * S, 0);
   }
   orth_mark(d, 1);
+  orth_mark_all(d, 768);
   grid.sync();
   orth_mark(d, 2);
   reduce_dots_dev(d.partials, G, d.dcross, (K + 1) * S * S, prod);
@@ -802,18 +846,7 @@ __global__ void __launch_bounds__(ORTH_NT, 1) k_arn_step(const __grid_constant__
     grid.sync();
   }
   orth_mark(d, 4);
-  // ---- push_block of the new block (CTA 0): W from the pass that produced it
-  if (blockIdx.x == 0) {
-    reduce_dots_dev(d.partials, G, s_first >= 0 ? d.dwb : d.dcross + K * S * S, S * S, prod);
-    __shared__ int s_ok;
-    if (tid == 0) s_ok = arn_push_body(d.st, *gs, K, d.rec, prod, S);
-    __syncthreads();
-    if (s_ok) {
-      const uint64_t* gsrc = reinterpret_cast<const uint64_t*>(gs);
-      uint64_t* gdst = reinterpret_cast<uint64_t*>(d.grams + K);
-      for (int w = tid; w < (int)(sizeof(Gram) / 8); w += ORTH_NT) gdst[w] = gsrc[w];
-    }
-  }
+  // (push_block of this candidate: at the start of the next block iteration)
   orth_mark(d, 5);
 }
 
@@ -1131,12 +1164,13 @@ struct Engine {
     d.dwb = dl.Wb();
     d.grams = grams;
     d.rec = recp(k);
+    d.rec_push = recp(k - 1);
     d.rec_t = rl.t();
     d.rec_h = rl.h();
     d.st = st;
     d.orth_tol = 1e-8;
     static const bool trace = std::getenv("SKC_TRACE_ORTH") != nullptr;
-    if (trace) d.trace = (unsigned long long*)c.workspace("orth_trace", 256 * sizeof(unsigned long long));
+    if (trace) d.trace = (unsigned long long*)c.workspace("orth_trace", 1024 * sizeof(unsigned long long));
     const int G = c.sm_count;
     const size_t smem = orth_smem(s, k, d.P);
     // algorithmic bytes: z, Scalar1 products, seed, the powers, round-0 products, pass 0 of the
@@ -1155,8 +1189,19 @@ struct Engine {
       default: run_orth<8>(c, d, G, smem); break;
     }
     if (trace) {
-      unsigned long long t[256];
+      unsigned long long t[1024];
       CK(cudaMemcpyAsync(t, d.trace, sizeof t, cudaMemcpyDeviceToHost, c.stream));
+      for (int ph = 1; ph <= 3; ++ph) {  // spread of the per-CTA phase completion times
+        unsigned long long lo = ~0ull, hi = 0;
+        int ilo = 0, ihi = 0;
+        for (int b = 0; b < G; ++b) {
+          const unsigned long long v = t[256 * ph + b];
+          if (v < lo) lo = v, ilo = b;
+          if (v > hi) hi = v, ihi = b;
+        }
+        std::fprintf(stderr, "[skew %s] %.1f us (first CTA %d, last CTA %d; CTA0 +%.1f)\n", ph == 1 ? "Zdots" : ph == 2 ? "seed" : "cross",
+                     (hi - lo) * 1e-3, ilo, ihi, (t[256 * ph] - lo) * 1e-3);
+      }
       c.sync();
       std::fprintf(stderr, "[step k=%d] z %.1f Zdots %.1f s1 %.1f seed %.1f s2 %.1f powers %.1f r0dots %.1f | rounds:", k,
                    (t[40] - t[39]) * 1e-3, (t[6] - t[40]) * 1e-3, (t[41] - t[6]) * 1e-3, (t[7] - t[41]) * 1e-3,

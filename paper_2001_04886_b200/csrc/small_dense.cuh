@@ -176,6 +176,102 @@ SKC_HD void gram_solve(const Gram& g, const double* rhs, double* x) {
   for (int i = 0; i < n; ++i) x[g.perm[i]] = b[i];
 }
 
+#ifdef __CUDACC__
+// Compile-time-order versions for the device kernels: the same operations in the same order
+// (hence the same bits) with every array in registers instead of local memory.  The LDL^T
+// fallback (a failed Cholesky attempt: rare, ill-conditioned Gram matrices) takes the generic
+// path above.
+template <int N>
+__device__ __forceinline__ void gram_solve_t(const Gram& g, const double* rhs, double* x) {
+  if (N == 1 || g.used_ldlt) {
+    gram_solve(g, rhs, x);
+    return;
+  }
+  double f[N * N];
+#pragma unroll
+  for (int q = 0; q < N * N; ++q) f[q] = g.fac[q];
+#pragma unroll
+  for (int i = 0; i < N; ++i) {
+    double acc = rhs[i];
+#pragma unroll
+    for (int k = 0; k < i; ++k) acc -= f[i * N + k] * x[k];
+    x[i] = acc / f[i * N + i];
+  }
+#pragma unroll
+  for (int ii = N - 1; ii >= 0; --ii) {
+    double acc = x[ii];
+#pragma unroll
+    for (int k = ii + 1; k < N; ++k) acc -= f[k * N + ii] * x[k];
+    x[ii] = acc / f[ii * N + ii];
+  }
+}
+
+template <int N>
+__device__ __forceinline__ void gram_factor_t(Gram& g, const double* w) {
+  if (N == 1) {
+    gram_factor(g, w, N);
+    return;
+  }
+  g.order = N;
+  g.used_ldlt = 0;
+  g.ok = 1;
+  g.singular1 = 0;
+  double wr[N * N];
+#pragma unroll
+  for (int q = 0; q < N * N; ++q) g.w[q] = wr[q] = w[q];
+  double tr = 0.0;
+#pragma unroll
+  for (int i = 0; i < N; ++i) tr += wr[i * N + i];
+  const double floor_ = 1e-13 * sd_abs(tr) / static_cast<double>(N);
+  double f[N * N], pv[N];
+#pragma unroll
+  for (int q = 0; q < N * N; ++q) f[q] = 0.0;
+#pragma unroll
+  for (int i = 0; i < N; ++i) pv[i] = 0.0;
+  bool chol = true;
+#pragma unroll
+  for (int j = 0; j < N; ++j) {
+    if (chol) {
+      double d = wr[j * N + j];
+#pragma unroll
+      for (int k = 0; k < j; ++k) d -= f[j * N + k] * f[j * N + k];
+      if (d <= floor_) {
+        chol = false;
+      } else {
+        pv[j] = d;
+        f[j * N + j] = sqrt(d);
+#pragma unroll
+        for (int i = j + 1; i < N; ++i) {
+          double acc = wr[i * N + j];
+#pragma unroll
+          for (int k = 0; k < j; ++k) acc -= f[i * N + k] * f[j * N + k];
+          f[i * N + j] = acc / f[j * N + j];
+        }
+      }
+    }
+  }
+  if (chol) {
+#pragma unroll
+    for (int q = 0; q < N * N; ++q) g.fac[q] = f[q];
+#pragma unroll
+    for (int i = 0; i < N; ++i) g.piv[i] = pv[i];
+  } else {
+    gram_factor_ldlt(g);
+#pragma unroll
+    for (int i = 0; i < N; ++i) pv[i] = g.piv[i];
+  }
+  double pmin = sd_abs(pv[0]), pmax = pmin;
+#pragma unroll
+  for (int i = 0; i < N; ++i) {
+    const double a = sd_abs(pv[i]);
+    pmin = a < pmin ? a : pmin;
+    pmax = a > pmax ? a : pmax;
+  }
+  g.ratio = pmax == 0.0 ? 0.0 : pmin / pmax;
+  if (pmax == 0.0 || pmin / pmax < 1e-15) g.ok = 0;
+}
+#endif
+
 // R^T R = W, upper triangular (small_dense.hpp:190-206). Returns false on breakdown.
 SKC_HD bool cholesky_upper(const double* w, int n, double* r) {
   for (int i = 0; i < n * n; ++i) r[i] = 0.0;
