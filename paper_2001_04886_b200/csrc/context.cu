@@ -32,9 +32,11 @@ std::string fmt_double(double v) {
 Geo make_geo(int64_t n, int sm_count) {
   Geo g;
   g.n = n;
-  // at most two co-resident CTAs per SM; each range is a whole number of 256-point tiles
+  // at most two co-resident CTAs per SM; each range is a whole number of 256-point tiles (small
+  // problems spread over up to n / 256 CTAs: a launch-latency-bound sweep then takes one tile
+  // round trip instead of a chain of tiles on a few SMs)
   const int64_t maxg = std::min<int64_t>(2LL * sm_count, kPartialPitch);
-  int64_t G = (n + 2047) / 2048;
+  int64_t G = (n + 255) / 256;
   G = std::max<int64_t>(1, std::min(G, maxg));
   int64_t range = (n + G - 1) / G;
   range = (range + 255) / 256 * 256;

@@ -125,7 +125,7 @@ __device__ bool arn_push_body(ArnState* st, Gram& g, int k, double* rec, const d
         W[j * s + l] = avg;
         W[l * s + j] = avg;
       }
-    gram_factor(g, W, s);
+    gram_factor_dev(g, W, s);
   }
   if (!record) return g.ok;
   for (int q = 0; q < s * s; ++q) rec[RecLayout::kW + q] = W[q];
@@ -170,7 +170,7 @@ __global__ void k_arn_s1(ArnState* st, const Gram* grams, int k, double* rec, do
   for (int i = threadIdx.x; i < k; i += blockDim.x) {
     double rhs[kMaxS], h[kMaxS];
     for (int l = 0; l < s; ++l) rhs[l] = scratch[i * s + l];
-    gram_solve(grams[i], rhs, h);
+    gram_solve_dev(grams[i], rhs, h);
     for (int l = 0; l < s; ++l) {
       rec[hoff + i * s + l] = h[l];
       coef[cH + i * s + l] = -h[l];

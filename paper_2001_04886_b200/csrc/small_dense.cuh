@@ -270,6 +270,33 @@ __device__ __forceinline__ void gram_factor_t(Gram& g, const double* w) {
   g.ratio = pmax == 0.0 ? 0.0 : pmin / pmax;
   if (pmax == 0.0 || pmin / pmax < 1e-15) g.ok = 0;
 }
+
+// runtime order -> compile-time-order versions (device kernels whose order is a run-time
+// argument)
+__device__ __forceinline__ void gram_factor_dev(Gram& g, const double* w, int n) {
+  switch (n) {
+    case 2: gram_factor_t<2>(g, w); return;
+    case 3: gram_factor_t<3>(g, w); return;
+    case 4: gram_factor_t<4>(g, w); return;
+    case 5: gram_factor_t<5>(g, w); return;
+    case 6: gram_factor_t<6>(g, w); return;
+    case 7: gram_factor_t<7>(g, w); return;
+    case 8: gram_factor_t<8>(g, w); return;
+    default: gram_factor(g, w, n);
+  }
+}
+__device__ __forceinline__ void gram_solve_dev(const Gram& g, const double* rhs, double* x) {
+  switch (g.order) {
+    case 2: gram_solve_t<2>(g, rhs, x); return;
+    case 3: gram_solve_t<3>(g, rhs, x); return;
+    case 4: gram_solve_t<4>(g, rhs, x); return;
+    case 5: gram_solve_t<5>(g, rhs, x); return;
+    case 6: gram_solve_t<6>(g, rhs, x); return;
+    case 7: gram_solve_t<7>(g, rhs, x); return;
+    case 8: gram_solve_t<8>(g, rhs, x); return;
+    default: gram_solve(g, rhs, x);
+  }
+}
 #endif
 
 // R^T R = W, upper triangular (small_dense.hpp:190-206). Returns false on breakdown.

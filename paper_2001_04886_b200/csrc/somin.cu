@@ -71,7 +71,7 @@ __global__ void k_somin_start(SominState* st, const double* partials, int G, int
 __device__ void somin_factor_solve(SominState* st, Gram* gslot, double* coef, const double* W, const double* m,
                                    int s, int collapse_status) {
   Gram g;
-  gram_factor(g, W, s);
+  gram_factor_dev(g, W, s);
   if (!g.ok) {
     st->status = collapse_status;
     st->halt = 1;
@@ -81,7 +81,7 @@ __device__ void somin_factor_solve(SominState* st, Gram* gslot, double* coef, co
   }
   *gslot = g;
   double a[kMaxS];
-  gram_solve(g, m, a);
+  gram_solve_dev(g, m, a);
   for (int l = 0; l < s; ++l) {
     coef[cA(s) + l] = a[l];
     coef[cNegA(s) + l] = -a[l];
@@ -145,7 +145,7 @@ __global__ void k_somin_proj(SominState* st, const Gram* grams, const __grid_con
     const int e = t / s, jc = t % s;
     double rhs[kMaxS], x[kMaxS];
     for (int l = 0; l < s; ++l) rhs[l] = scratch[(e * s + l) * s + jc];
-    gram_solve(grams[win.idx[e]], rhs, x);
+    gram_solve_dev(grams[win.idx[e]], rhs, x);
     for (int l = 0; l < s; ++l) coef[cB(s) + e * s * s + l * s + jc] = -x[l];
   }
 }
@@ -511,7 +511,7 @@ __global__ void k_smr_solve(SmrState* st, double* coef, const double* partials, 
         W[l * s + j] = avg;
       }
     Gram gm;
-    gram_factor(gm, W, s);
+    gram_factor_dev(gm, W, s);
     if (!gm.ok) {
       st->status = kIterCollapse;
       st->halt = 1;
@@ -520,7 +520,7 @@ __global__ void k_smr_solve(SmrState* st, double* coef, const double* partials, 
       return;
     }
     double a[kMaxS];
-    gram_solve(gm, v + s * s, a);
+    gram_solve_dev(gm, v + s * s, a);
     for (int l = 0; l < s; ++l) {
       coef[l] = a[l];
       coef[s + l] = -a[l];

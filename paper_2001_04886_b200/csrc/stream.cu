@@ -328,7 +328,7 @@ __device__ __forceinline__ void mgs_scalar(const MgsScalar& sc, double* cs, doub
     double rhs[kMaxS], t[kMaxS];
 #pragma unroll
     for (int l = 0; l < S; ++l) rhs[l] = tmp[l * NC + jc];
-    gram_solve(*gs, rhs, t);
+    gram_solve_dev(*gs, rhs, t);
 #pragma unroll
     for (int l = 0; l < S; ++l) {
       cs[l * NC + jc] = -t[l];
