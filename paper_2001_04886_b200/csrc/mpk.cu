@@ -451,6 +451,64 @@ __global__ void __launch_bounds__(TXE* TYE) k_mpk3d(const __grid_constant__ MpkD
   }
 }
 
+// Small 2D grids (single GPU, no fused products): one CTA per 32 x 32 tile extended by J on each
+// side, all J levels computed in shared memory with one __syncthreads per level.  The row-
+// streaming strip kernel needs ~R + 2J dependent row steps per strip, which dominates when
+// the whole grid is only a few dozen strips (C1: 128 x 128); here a launch is one load round
+// trip plus J on-chip levels.  Level j is exact on [j, 32 - j) of the tile, so the output
+// (the inner 32 - 2J square) is bit-identical to J successive spmv calls, as in the other
+// kernels.
+constexpr int T2 = 32;
+template <int KIND, int J>
+__global__ void __launch_bounds__(T2* T2) k_mpk2t(const __grid_constant__ MpkDesc d) {
+  SKC_PDL_ENTRY();
+  if (skip_launch(d.halt, d.cond)) return;
+  __shared__ double lev[2][T2 * T2];
+  const int tid = threadIdx.x;
+  const int lx = tid % T2, ly = tid / T2;
+  const int tx = blockIdx.x % d.tiles_x, ty = blockIdx.x / d.tiles_x;
+  const int64_t nx = d.op.nx, ny = d.op.ny;
+  const int64_t x = (int64_t)tx * d.W - J + lx, y = (int64_t)ty * d.R - J + ly;
+  const bool in = x >= 0 && x < nx && y >= 0 && y < ny;
+  const bool outp = lx >= J && lx < T2 - J && ly >= J && ly < T2 - J && x < nx && y < ny;
+  const int64_t p = y * nx + x;
+  double v = 0.0;
+  if (in) v = d.scale ? __dmul_rn(d.src[p], *d.scale) : d.src[p];
+  lev[0][tid] = v;
+  if (d.out[0] && outp) d.out[0][p] = v;
+  bool pres[7];
+  int64_t nb[7];
+  pres[0] = pres[6] = false;
+  pres[1] = y > 0;
+  pres[2] = x > 0;
+  pres[3] = true;
+  pres[4] = x + 1 < nx;
+  pres[5] = y + 1 < ny;
+  nb[0] = nb[6] = p;
+  nb[1] = p - nx;
+  nb[2] = p - 1;
+  nb[3] = p;
+  nb[4] = p + 1;
+  nb[5] = p + nx;
+  double val[7];
+  if (in) coefs<2, KIND>(d.op, p, pres, nb, val);
+#pragma unroll
+  for (int j = 1; j <= J; ++j) {
+    __syncthreads();
+    const double* P = lev[(j - 1) & 1];
+    double a = 0.0;
+    if (in && lx >= j && lx < T2 - j && ly >= j && ly < T2 - j) {
+      a = __dadd_rn(a, __dmul_rn(val[1], pres[1] ? P[tid - T2] : 0.0));
+      a = __dadd_rn(a, __dmul_rn(val[2], pres[2] ? P[tid - 1] : 0.0));
+      a = __dadd_rn(a, __dmul_rn(val[3], P[tid]));
+      a = __dadd_rn(a, __dmul_rn(val[4], pres[4] ? P[tid + 1] : 0.0));
+      a = __dadd_rn(a, __dmul_rn(val[5], pres[5] ? P[tid + T2] : 0.0));
+    }
+    lev[j & 1][tid] = a;
+    if (d.out[j] && outp) d.out[j][p] = a;
+  }
+}
+
 template <class K>
 void mpk_smem_attr(K kernel, size_t bytes) {
   if (bytes > 48 * 1024) CK(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
@@ -467,6 +525,18 @@ void run2d(Ctx& c, const MpkDesc& d) {
 template <int KIND, int J>
 void launch2d(Ctx& c, MpkDesc& d) {
   const int64_t nx = d.op.nx, ny = d.op.ny;
+  if (J <= 8 && !d.nx_dots && d.op.halo_rows == 0 && d.op.rows_global == ny) {
+    const int64_t tw = T2 - 2 * J;
+    const int64_t ntile = ((nx + tw - 1) / tw) * ((ny + tw - 1) / tw);
+    if (ntile <= 2LL * c.sm_count) {  // the strip kernel would leave most SMs idle
+      d.W = d.R = (int)tw;
+      d.tiles_x = (int)((nx + tw - 1) / tw);
+      d.tiles_y = (int)((ny + tw - 1) / tw);
+      d.G = (int)ntile;
+      launch_k(c, k_mpk2t<KIND, J>, d.G, T2 * T2, 0, d);
+      return;
+    }
+  }
   d.W = 64 - 2 * J;
   d.tiles_x = (int)((nx + d.W - 1) / d.W);
   // rows per warp strip: ~16 strips per SM, at least 3J rows to bound the ghost-row overhead
