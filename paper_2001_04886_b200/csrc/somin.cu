@@ -8,11 +8,15 @@
 // kernel of the batch into a no-op once the iteration stops.  The host then replays the
 // reference's control flow on the recorded per-iteration residuals to rebuild the
 // SolveReport (history, op counters, breakdown strings) exactly.
+#include <cooperative_groups.h>
+
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 
 #include "device_util.cuh"
 #include "solver_util.hpp"
+#include "stencil.cuh"
 
 namespace skc {
 
@@ -191,6 +195,287 @@ __global__ void k_somin_push(SominState* st, Gram* grams, int slot_new, double* 
   }
 }
 
+// ---------------------------------------------------------------- persistent s-Omin (small n)
+// For problems whose vectors are L2-resident and too small to fill the GPU with one kernel per
+// operation (C1: 16 384 unknowns), one cooperative launch runs a chunk of whole s-Omin
+// iterations: every CTA owns a contiguous point range and the phases of an iteration are
+// separated by grid barriers instead of kernel boundaries --
+//   x += P a, r -= AP a and ||r||^2 | norm, termination checks | the s powers of r (a barrier
+//   between levels) and C_e = AP_e^T AR | Scalar2 solves in every CTA | the new P, AP block,
+//   W and m | push_block (factor in every CTA; CTA 0 records) and a = W^{-1} m.
+// Every CTA reduces the per-CTA partials in the same fixed order and takes the same decisions;
+// CTA 0 writes the state and the history.  The window slots follow the host deque exactly:
+// the block of iteration t lives in slot t mod (k+1), the window before iteration t's push is
+// the blocks of iterations max(0, t-k) .. t-1.  Same per-element arithmetic as the batched path.
+constexpr int PS_NT = 256;
+constexpr int PS_MAXK = 8;
+
+struct PersistDesc {
+  DevOp op;
+  int k;
+  int64_t n, P, np;
+  double* x;
+  double* r;
+  double* K;   // powers: column j at K + j*np
+  double* S0;  // slot 0 column 0; slot sl column col (P: col < s, AP: s + col) at S0 + (sl*2s + col)*np
+  double* partials;
+  int dRR, dW, dC;
+  Gram* grams;
+  double* coef;
+  SominState* st;
+  double* hist;
+  long long it_end;
+};
+
+template <int K>
+__device__ __forceinline__ void ps_store(const double (&acc)[K], double* red, double* partials, int d0) {
+  constexpr int NW = PS_NT / 32;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int q = 0; q < K; ++q) {
+    const double v = warp_sum(acc[q]);
+    if (lane == 0) red[warp * K + q] = v;
+  }
+  __syncthreads();
+  if (threadIdx.x < K) {
+    double s = 0.0;
+    for (int w = 0; w < NW; ++w) s += red[w * K + threadIdx.x];
+    partials[(int64_t)(d0 + threadIdx.x) * kPartialPitch + blockIdx.x] = s;
+  }
+  __syncthreads();
+}
+
+template <int S>
+__global__ void __launch_bounds__(PS_NT) k_somin_persist(const __grid_constant__ PersistDesc d) {
+  SKC_PDL_ENTRY();
+  if (__ldg(&d.st->halt)) return;
+  namespace cg = cooperative_groups;
+  cg::grid_group grid = cg::this_grid();
+  constexpr int NTRI = S * (S + 1) / 2;
+  __shared__ Gram gw[PS_MAXK + 1];
+  __shared__ double sa[S], sb[PS_MAXK * S * S], sv[PS_MAXK * S * S + NTRI + S];
+  __shared__ double red[(PS_NT / 32) * (NTRI + S > S * S ? NTRI + S : S * S)];
+  __shared__ int s_flag;
+  const int tid = threadIdx.x, G = gridDim.x, NSL = d.k + 1;
+  const int64_t base = (int64_t)blockIdx.x * d.P;
+  const int cnt = base >= d.n ? 0 : (int)(d.n - base < d.P ? d.n - base : d.P);
+  for (int w = tid; w < (int)(NSL * sizeof(Gram) / 8); w += PS_NT)
+    reinterpret_cast<uint64_t*>(gw)[w] = reinterpret_cast<const uint64_t*>(d.grams)[w];
+  if (tid < S) sa[tid] = d.coef[cA(S) + tid];
+  const double tol = d.st->tol, divf = d.st->divf, r0n = d.st->r0n;
+  const long long max_iter = d.st->max_iter;
+  long long t = d.st->iters;
+  __syncthreads();
+  auto pcol = [&](int sl, int col) { return d.S0 + ((int64_t)sl * 2 * S + col) * d.np; };
+  auto kcol = [&](int j) { return d.K + (int64_t)j * d.np; };
+  for (;;) {
+    // ---- x += P a ; r -= AP a ; ||r||^2 (sstep.hpp:183-193)
+    {
+      const int cur = (int)(t % NSL);
+      double rr[1] = {0.0};
+      for (int p = tid; p < cnt; p += PS_NT) {
+        const int64_t q = base + p;
+        double xv = d.x[q], rv = d.r[q];
+#pragma unroll
+        for (int l = 0; l < S; ++l) xv = __dadd_rn(xv, __dmul_rn(sa[l], pcol(cur, l)[q]));
+#pragma unroll
+        for (int l = 0; l < S; ++l) rv = __dadd_rn(rv, __dmul_rn(-sa[l], pcol(cur, S + l)[q]));
+        d.x[q] = xv;
+        d.r[q] = rv;
+        rr[0] = fma(rv, rv, rr[0]);
+      }
+      ps_store(rr, red, d.partials, d.dRR);
+    }
+    grid.sync();
+    reduce_dots_dev(d.partials, G, d.dRR, 1, sv);
+    ++t;
+    const double rn = sqrt(sv[0]);
+    {
+      int status = kRunning;
+      if (rn <= tol)
+        status = kConverged;
+      else if (rn > divf * r0n)
+        status = kDiverged;
+      else if (t >= max_iter)
+        status = kMaxIter;
+      if (blockIdx.x == 0 && tid == 0) {
+        d.st->rn = rn;
+        d.st->iters = t;
+        d.hist[t] = rn;
+        if (status) {
+          d.st->status = status;
+          d.st->halt = 1;
+        }
+      }
+      if (status) return;
+    }
+    // ---- krylov_pair(r): K[j] = A^{j+1} r (every level an exact spmv of the previous one)
+#pragma unroll 1
+    for (int j = 0; j < S; ++j) {
+      const double* src = j == 0 ? d.r : kcol(j - 1);
+      double* dst = kcol(j);
+      for (int p = tid; p < cnt; p += PS_NT) {
+        const int64_t q = base + p;
+        GridWalk w;
+        w.init(d.op, q);
+        dst[q] = apply_point(d.op, [&](int64_t o) { return src[o]; }, q, w);
+      }
+      if (j + 1 < S) grid.sync();
+    }
+    // ---- C_e = AP_e^T AR for the window (block_gram, sstep.hpp:207); own points only
+    const int nw = (int)(t < d.k ? t : d.k);  // window blocks: iterations t - nw .. t - 1
+#pragma unroll 1
+    for (int e = 0; e < nw; ++e) {
+      const int se = (int)((t - nw + e) % NSL);
+      double acc[S * S];
+#pragma unroll
+      for (int q2 = 0; q2 < S * S; ++q2) acc[q2] = 0.0;
+      for (int p = tid; p < cnt; p += PS_NT) {
+        const int64_t q = base + p;
+        double kv[S];
+#pragma unroll
+        for (int jc = 0; jc < S; ++jc) kv[jc] = kcol(jc)[q];
+#pragma unroll
+        for (int l = 0; l < S; ++l) {
+          const double ap = pcol(se, S + l)[q];
+#pragma unroll
+          for (int jc = 0; jc < S; ++jc) acc[l * S + jc] = fma(ap, kv[jc], acc[l * S + jc]);
+        }
+      }
+      ps_store(acc, red, d.partials, d.dC + e * S * S);
+    }
+    grid.sync();
+    // ---- Scalar2 (sstep.hpp:204-214): b_e = -W_e^{-1} C_e in every CTA
+    reduce_dots_dev(d.partials, G, d.dC, nw * S * S, sv);
+    for (int u = tid; u < nw * S; u += PS_NT) {
+      const int e = u / S, jc = u % S;
+      const int se = (int)((t - nw + e) % NSL);
+      double rhs[kMaxS], xx[kMaxS];
+#pragma unroll
+      for (int l = 0; l < S; ++l) rhs[l] = sv[(e * S + l) * S + jc];
+      gram_solve_t<S>(gw[se], rhs, xx);
+#pragma unroll
+      for (int l = 0; l < S; ++l) sb[e * S * S + l * S + jc] = -xx[l];
+    }
+    __syncthreads();
+    // ---- new block P = R + sum_e P_e b_e, AP = AR + sum_e AP_e b_e (window block -> column l
+    //      order, sstep.hpp:215-221), W = AP^T AP (upper triangle) and m = AP^T r
+    const int nsl = (int)(t % NSL);
+    {
+      double acc[NTRI + S];
+#pragma unroll
+      for (int q2 = 0; q2 < NTRI + S; ++q2) acc[q2] = 0.0;
+      for (int p = tid; p < cnt; p += PS_NT) {
+        const int64_t q = base + p;
+        const double rv = d.r[q];
+        double pn[S], apn[S];
+#pragma unroll
+        for (int jc = 0; jc < S; ++jc) {
+          pn[jc] = jc == 0 ? rv : kcol(jc - 1)[q];
+          apn[jc] = kcol(jc)[q];
+        }
+        for (int e = 0; e < nw; ++e) {
+          const int se = (int)((t - nw + e) % NSL);
+          const double* be = sb + e * S * S;
+#pragma unroll
+          for (int l = 0; l < S; ++l) {
+            const double pv = pcol(se, l)[q];
+#pragma unroll
+            for (int jc = 0; jc < S; ++jc) pn[jc] = __dadd_rn(pn[jc], __dmul_rn(be[l * S + jc], pv));
+          }
+#pragma unroll
+          for (int l = 0; l < S; ++l) {
+            const double apv = pcol(se, S + l)[q];
+#pragma unroll
+            for (int jc = 0; jc < S; ++jc) apn[jc] = __dadd_rn(apn[jc], __dmul_rn(be[l * S + jc], apv));
+          }
+        }
+#pragma unroll
+        for (int jc = 0; jc < S; ++jc) {
+          pcol(nsl, jc)[q] = pn[jc];
+          pcol(nsl, S + jc)[q] = apn[jc];
+        }
+        int u = 0;
+#pragma unroll
+        for (int a = 0; a < S; ++a)
+#pragma unroll
+          for (int b = a; b < S; ++b) acc[u] = fma(apn[a], apn[b], acc[u]), ++u;
+#pragma unroll
+        for (int a = 0; a < S; ++a) acc[NTRI + a] = fma(apn[a], rv, acc[NTRI + a]);
+      }
+      ps_store(acc, red, d.partials, d.dW);
+    }
+    grid.sync();
+    // ---- push_block: GramSolver(W) (breakdown = basis collapse) and a = W^{-1} m
+    reduce_dots_dev(d.partials, G, d.dW, NTRI + S, sv);
+    if (tid == 0) {
+      double W[S * S];
+      int u = 0;
+#pragma unroll
+      for (int a = 0; a < S; ++a)
+#pragma unroll
+        for (int b = a; b < S; ++b) {
+          W[a * S + b] = sv[u];
+          W[b * S + a] = sv[u];
+          ++u;
+        }
+      gram_factor_t<S>(gw[nsl], W);
+      int flag = 0;
+      if (!gw[nsl].ok) {
+        flag = kIterCollapse;
+      } else {
+        double a[kMaxS];
+        gram_solve_t<S>(gw[nsl], sv + NTRI, a);
+#pragma unroll
+        for (int l = 0; l < S; ++l) sa[l] = a[l];
+        if (!(rn > tol)) flag = kNanStop;  // NaN residual: the loop condition ends the solve
+      }
+      s_flag = flag;
+    }
+    __syncthreads();
+    if (s_flag) {
+      if (blockIdx.x == 0 && tid == 0) {
+        d.st->status = s_flag;
+        d.st->halt = 1;
+        if (s_flag == kIterCollapse) {
+          d.st->ratio = gw[nsl].ratio;
+          d.st->singular1 = gw[nsl].singular1;
+        }
+      }
+      if (s_flag == kIterCollapse) return;
+      // (NaN stop: the push itself succeeded; record it like the batched path)
+      if (blockIdx.x == 0)
+        for (int w = tid; w < (int)(sizeof(Gram) / 8); w += PS_NT)
+          reinterpret_cast<uint64_t*>(d.grams + nsl)[w] = reinterpret_cast<const uint64_t*>(gw + nsl)[w];
+      return;
+    }
+    if (blockIdx.x == 0) {
+      for (int w = tid; w < (int)(sizeof(Gram) / 8); w += PS_NT)
+        reinterpret_cast<uint64_t*>(d.grams + nsl)[w] = reinterpret_cast<const uint64_t*>(gw + nsl)[w];
+      if (tid < S) {
+        d.coef[cA(S) + tid] = sa[tid];
+        d.coef[cNegA(S) + tid] = -sa[tid];
+      }
+    }
+    if (t >= d.it_end) return;
+  }
+}
+
+template <int S>
+void run_persist(Ctx& c, const PersistDesc& d, int G, double bytes) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = G;
+  cfg.blockDim = PS_NT;
+  cfg.stream = c.stream;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeCooperative;
+  at[0].val.cooperative = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  Launch lh(c, "somin_persist", bytes);
+  CK(cudaLaunchKernelEx(&cfg, k_somin_persist<S>, d));
+}
+
 __global__ void k_any_nonzero(const double* x, int64_t n, int* flag) {
   SKC_PDL_ENTRY();
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
@@ -340,6 +625,48 @@ void somin_device(Ctx& c, const Op& op, const double* f, double* x, const SStepC
   bool gcr_full = false;
   CK(cudaMemcpyAsync(&hs, st, sizeof hs, cudaMemcpyDeviceToHost, c.stream));
   c.sync();
+  // small problems: whole iterations in one cooperative launch per chunk (see k_somin_persist)
+  static const bool persist_env = [] {
+    const char* e = std::getenv("SKC_PERSIST");
+    return !e || std::atoi(e) != 0;
+  }();
+  if (persist_env && !gcr && !cfg.debug_checks && c.world() == 1 && s <= 4 && cfg.k <= (uint64_t)PS_MAXK &&
+      n <= (1 << 18)) {
+    PersistDesc pd;
+    std::memset(&pd, 0, sizeof pd);
+    pd.op = op.d;
+    pd.k = (int)cfg.k;
+    pd.n = n;
+    const int G = (int)std::min<int64_t>(c.sm_count, (n + PS_NT - 1) / PS_NT);
+    pd.P = (n + G - 1) / G;
+    pd.np = (int64_t)np;
+    pd.x = x;
+    pd.r = r;
+    pd.K = K;
+    pd.S0 = slot_p(0, 0);
+    pd.partials = partials;
+    pd.dRR = dRR;
+    pd.dW = dW;
+    pd.dC = dC;
+    pd.grams = grams;
+    pd.coef = coef;
+    pd.st = st;
+    pd.hist = hist;
+    // algorithmic bytes of one iteration (profiling only): the batched path's operands
+    const double bytes = 8.0 * (double)n * (3.0 * (double)cfg.k * s + 7.0 * s + 6.0);
+    while (hs.status == kRunning && (uint64_t)hs.iters < cfg.max_iterations) {
+      pd.it_end = hs.iters + 4096;
+      switch (s) {
+        case 1: run_persist<1>(c, pd, G, bytes); break;
+        case 2: run_persist<2>(c, pd, G, bytes); break;
+        case 3: run_persist<3>(c, pd, G, bytes); break;
+        default: run_persist<4>(c, pd, G, bytes); break;
+      }
+      CK(cudaMemcpyAsync(&hs, st, sizeof hs, cudaMemcpyDeviceToHost, c.stream));
+      c.sync();
+    }
+    enq = cfg.max_iterations;
+  }
   while (hs.status == kRunning && enq < cfg.max_iterations) {
     const uint64_t todo = std::min<uint64_t>(batch, cfg.max_iterations - enq);
     for (uint64_t it = 0; it < todo; ++it, ++enq) {
