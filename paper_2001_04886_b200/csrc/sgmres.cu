@@ -1140,13 +1140,9 @@ struct Engine {
     d.s = s;
     d.k = k;
     d.build_next = build_next ? 1 : 0;
-    static const int zfuse_env = [] {
-      // default off: the fused products make the cross pass and the extra barrier cost about
-      // what the skipped Scalar1 sweep saves (measured 0.5-0.8% slower on C2)
-      const char* e = std::getenv("SKC_ZFUSE");
-      return e ? std::atoi(e) : 0;
-    }();
-    d.zfuse = build_next && zfuse_env ? 1 : 0;
+    // (off by default: the fused products make the cross pass and the extra barrier cost
+    // about what the skipped Scalar1 sweep saves, measured 0.5-0.8% slower on C2)
+    d.zfuse = build_next && c.zfuse ? 1 : 0;
     d.n = op.n;
     d.P = orth_points();
     d.op = op.d;

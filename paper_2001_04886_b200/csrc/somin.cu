@@ -626,11 +626,7 @@ void somin_device(Ctx& c, const Op& op, const double* f, double* x, const SStepC
   CK(cudaMemcpyAsync(&hs, st, sizeof hs, cudaMemcpyDeviceToHost, c.stream));
   c.sync();
   // small problems: whole iterations in one cooperative launch per chunk (see k_somin_persist)
-  static const bool persist_env = [] {
-    const char* e = std::getenv("SKC_PERSIST");
-    return !e || std::atoi(e) != 0;
-  }();
-  if (persist_env && !gcr && !cfg.debug_checks && c.world() == 1 && s <= 4 && cfg.k <= (uint64_t)PS_MAXK &&
+  if (c.persist && !gcr && !cfg.debug_checks && c.world() == 1 && s <= 4 && cfg.k <= (uint64_t)PS_MAXK &&
       n <= (1 << 18)) {
     PersistDesc pd;
     std::memset(&pd, 0, sizeof pd);
