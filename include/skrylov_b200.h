@@ -16,6 +16,9 @@
  *   skc_krylov_block  <- krylov_block(op, v, s)                                                     block.hpp:59-67
  *   skc_op_create_csr <- as_operator(const SparseMatrix&)                                           sparse.hpp:155-160
  *   skc_op_create_stencil (new: device-describable 5/7-point operator)
+ *   skc_op_create_ilu0 <- right_preconditioned(a, ilu0_factor(a))  (A (LU)^{-1})                 ilu0.hpp:138-146, 45-95
+ *   skc_ilu0_solve[_device] <- ilu0_apply(factors, r) -> z = (LU)^{-1} r                         ilu0.hpp:99-134
+ *   skc_ilu0_factor   <- ilu0_factor(a) values in A's pattern (host only, no GPU needed)          ilu0.hpp:45-95
  *   skc_gram_solve / skc_cholesky_upper / skc_hessenberg_lsq <- GramSolver / cholesky_upper /
  *                      hessenberg_lsq (small_dense.hpp:42-331); host-only, no GPU needed.
  *
@@ -133,9 +136,22 @@ int skc_op_create_stencil(skc_ctx* ctx, const skc_stencil_desc* desc, const doub
  * run by the stencil kernels from per-cell diagonals; anything else runs the CSR kernel. */
 int skc_op_create_csr(skc_ctx* ctx, uint64_t n, const uint64_t* row_offsets, const uint64_t* col_indices,
                       const double* values, skc_op** out);
+/* ILU(0) right preconditioning, as the reference driver composes it when `precondition` is set
+ * (solve_linear, bench.hpp:149-191): the operator A (LU)^{-1} for the solvers (iterate w from 0)
+ * and z = (LU)^{-1} w for the update x = x0 + z.  The factorization is the reference's IKJ
+ * elimination on pattern(A) (host, same operations and order); errors: a row without a
+ * diagonal -> SKC_EINVAL, "ilu0: zero pivot at row N" -> SKC_EBREAKDOWN.  One GPU only.  The
+ * triangular solves are bit-identical to ilu0_apply (level-scheduled rows, each row in the
+ * reference's order). */
+int skc_op_create_ilu0(skc_ctx* ctx, uint64_t n, const uint64_t* row_offsets, const uint64_t* col_indices,
+                       const double* values, skc_op** out);
+int skc_ilu0_solve(skc_ctx* ctx, const skc_op* ilu_op, const double* r, double* z);        /* host buffers */
+int skc_ilu0_solve_device(skc_ctx* ctx, const skc_op* ilu_op, const double* r, double* z); /* device, async */
+int skc_ilu0_factor(uint64_t n, const uint64_t* row_offsets, const uint64_t* col_indices, const double* values,
+                    double* lu_out);
 int skc_op_destroy(skc_op* op);
 int skc_op_size(const skc_op* op, uint64_t* n);
-/* 0 = general CSR, 1 = 2D stencil, 2 = 3D stencil */
+/* 0 = general CSR, 2 = 2D stencil, 3 = 3D stencil, 4 = ILU(0)-preconditioned A (LU)^{-1} */
 int skc_op_kind(const skc_op* op, int* kind);
 /* y = A x on host buffers (bit-identical to the reference spmv for the same values) */
 int skc_op_apply(skc_ctx* ctx, const skc_op* op, const double* x, double* y);

@@ -183,7 +183,14 @@ class Oracle:
         L("sarnoldi").argtypes = [P(Csr), P(dbl), u64, u64, P(dbl), P(dbl), P(dbl), P(dbl), P(dbl),
                                   P(Counter), C.c_char_p, u64]
         L("sarnoldi").restype = C.c_int
+        L("ilu0_factor").argtypes = [P(Csr), P(dbl), C.c_char_p, u64]
+        L("ilu0_factor").restype = C.c_int
+        L("ilu0_apply").argtypes = [P(Csr), P(dbl), P(dbl), P(dbl)]
+        if self.px == "ref_":
+            self.lib.ref_solve_linear.argtypes = [P(Csr), P(dbl), P(dbl), i32, P(SStepCfg), i32, P(dbl), P(Report)]
+            self.lib.ref_solve_linear.restype = C.c_int
         if self.px == "orc_":
+            self.lib.orc_set_right_preconditioner.argtypes = [P(Csr), P(dbl)]
             self.lib.orc_fill_uniform.argtypes = [u64, u64, u64, P(dbl)]
             self.lib.orc_fill_lognormal.argtypes = [u64, u64, P(dbl)]
             self.lib.orc_build_stencil_csr.argtypes = [i32, u64, u64, u64, P(dbl), P(dbl), dbl,
@@ -235,6 +242,82 @@ class Oracle:
         return self._run(name, a, f, x0, cfg)
 
     # ------------------------------------------------------------------ kernels
+    # ------------------------------------------------------------------ ILU(0) (ilu0.hpp)
+    def ilu0_factor(self, a):
+        """Factor values in A's pattern (unit-lower L below the diagonal, U on and above)."""
+        lu = np.zeros(len(a.vals))
+        err = C.create_string_buffer(512)
+        st = self.f("ilu0_factor")(C.byref(a.c), _dp(lu), err, 512)
+        if st:
+            raise OracleError(st, err.value.decode())
+        return lu
+
+    def ilu0_apply(self, a, lu, r):
+        """z = (LU)^{-1} r."""
+        lu = np.ascontiguousarray(lu, dtype=np.float64)
+        r = np.ascontiguousarray(r, dtype=np.float64)
+        z = np.zeros(a.n)
+        self.f("ilu0_apply")(C.byref(a.c), _dp(lu), _dp(r), _dp(z))
+        return z
+
+    def solve_linear(self, method, a, f, x0=None, *, precondition=True, s=2, k=2, m=5, tol=1e-6,
+                     max_iterations=100000, divergence_factor=10.0):
+        """The reference driver flow (bench.hpp:149-191) around s-Omin / s-GMRES: with
+        `precondition`, ILU(0) right preconditioning from w = 0, x = x0 + K^{-1} w; the true
+        residual recomputed and appended.  Reference build only."""
+        x0 = np.zeros(a.n) if x0 is None else np.ascontiguousarray(x0, dtype=np.float64)
+        f = np.ascontiguousarray(f, dtype=np.float64)
+        if self.px == "orc_":
+            return self._solve_linear_port(method, a, f, x0, precondition, dict(
+                s=s, k=k, m=m, tol=tol, max_iterations=max_iterations, divergence_factor=divergence_factor))
+        cfg = SStepCfg(s, k, m, tol, max_iterations, 0, 0, 0, divergence_factor)
+        x = np.zeros(a.n)
+        rep = Report()
+        st = self.lib.ref_solve_linear(C.byref(a.c), _dp(f), _dp(x0), {"somin": 0, "sgmres": 1}[method],
+                                       C.byref(cfg), int(precondition), _dp(x), C.byref(rep))
+        try:
+            if st:
+                raise OracleError(st, rep.error.decode())
+            return self._collect(rep, x)
+        finally:
+            self.f("report_free")(C.byref(rep))
+
+    def _solve_linear_port(self, method, a, f, x0, precondition, cfg):
+        """bench.hpp:149-191 with the restatement's solvers (the operator switched to A (LU)^{-1}
+        through orc_set_right_preconditioner while the solver runs)."""
+        x = np.array(x0, dtype=np.float64, copy=True)
+        if precondition:
+            lu = self.ilu0_factor(a)
+            r0 = f - self.spmv(a, x)
+            self.lib.orc_set_right_preconditioner(C.byref(a.c), _dp(lu))
+            try:
+                res = self.sstep(method, a, r0, np.zeros(a.n), **cfg)
+            finally:
+                self.lib.orc_set_right_preconditioner(C.byref(a.c), None)
+            c = list(res.op_counts)
+            c[1] += 1
+            c[2] += 1
+            z = self.ilu0_apply(a, lu, res.x)
+            x += z
+            c[2] += 1
+        else:
+            res = self.sstep(method, a, f, x, **cfg)
+            x = res.x
+            c = list(res.op_counts)
+        ax = f - self.spmv(a, x)
+        c[1] += 1
+        c[2] += 1
+        c[4] += 1
+        true_norm = float(np.sqrt(np.add.accumulate(ax * ax)[-1]))
+        res.op_counts = tuple(c)
+        res.residual_history.append(true_norm)
+        res.final_residual = true_norm
+        if res.converged and true_norm > cfg["tol"]:
+            res.converged = False
+            res.breakdown = "recomputed true residual exceeds the threshold"
+        res.x = x
+        return res
+
     def spmv(self, a, x):
         x = np.ascontiguousarray(x, dtype=np.float64)
         y = np.zeros(a.n)

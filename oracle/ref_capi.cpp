@@ -16,6 +16,8 @@
 
 #include <random>
 
+#include "skrylov/ilu0.hpp"
+#include "skrylov/kernels.hpp"
 #include "skrylov/problem.hpp"
 #include "skrylov/sparse.hpp"
 #include "skrylov/sstep.hpp"
@@ -290,6 +292,88 @@ int ref_discretize(uint64_t nx, double beta, double gamma, int32_t symmetric, ui
       (*rhs)[i] = prob.rhs[i];
       (*x0)[i] = prob.x0[i];
     }
+  });
+}
+
+// ---- ILU(0) (ilu0.hpp): factor values in A's pattern (L strict-lower entries, then U
+// entries of each row, A's columns being ascending), the apply z = (LU)^{-1} r, and the
+// right-preconditioned driver flow of solve_linear (bench.hpp:149-191; bench.hpp itself needs
+// <json.hpp> and does not build here, so its few driver lines are restated with the
+// reference's own ilu0_factor / right_preconditioned / ilu0_apply / s-step solvers)
+int ref_ilu0_factor(const orc_csr* a, double* lu_out, char* err, uint64_t errcap) {
+  return guarded(err, errcap, [&] {
+    SparseMatrix m = to_sparse(a);
+    Ilu0Factors f = ilu0_factor(m);
+    const std::size_t n = a->n;
+    std::size_t q = 0;
+    for (std::size_t i = 0; i < n; ++i) {
+      for (std::size_t p = f.l_unit.row_offsets()[i]; p < f.l_unit.row_offsets()[i + 1]; ++p)
+        lu_out[q++] = f.l_unit.values()[p];
+      for (std::size_t p = f.u_upper.row_offsets()[i]; p < f.u_upper.row_offsets()[i + 1]; ++p)
+        lu_out[q++] = f.u_upper.values()[p];
+    }
+  });
+}
+
+static Ilu0Factors factors_from(const orc_csr* a, const double* lu) {
+  std::vector<std::tuple<std::size_t, std::size_t, double>> le, ue;
+  for (std::size_t i = 0; i < a->n; ++i)
+    for (uint64_t p = a->row_offsets[i]; p < a->row_offsets[i + 1]; ++p) {
+      if (a->col_indices[p] < i)
+        le.emplace_back(i, a->col_indices[p], lu[p]);
+      else
+        ue.emplace_back(i, a->col_indices[p], lu[p]);
+    }
+  return {SparseMatrix::from_triplets(a->n, a->n, std::move(le)), SparseMatrix::from_triplets(a->n, a->n, std::move(ue))};
+}
+
+void ref_ilu0_apply(const orc_csr* a, const double* lu, const double* r, double* z) {
+  Ilu0Factors f = factors_from(a, lu);
+  ilu0_apply(f, std::span<const double>(r, a->n), std::span<double>(z, a->n));
+}
+
+// method: 0 s-Omin, 1 s-GMRES; cfg->tol is the driver's threshold
+int ref_solve_linear(const orc_csr* a, const double* f, const double* x0, int32_t method, const orc_sstep_cfg* cfg,
+                     int32_t precondition, double* x_out, orc_report* rep) {
+  return guarded(rep->error, sizeof rep->error, [&] {
+    SparseMatrix m = to_sparse(a);
+    const std::size_t n = a->n;
+    std::span<const double> fs(f, n);
+    std::vector<double> x(x0, x0 + n);
+    const SStepConfig c = sconf(cfg);
+    auto dispatch = [&](const LinearOperator& op, std::span<const double> rhs, std::vector<double>& xv) {
+      return method == 0 ? somin_solve(op, rhs, xv, c) : sgmres_solve(op, rhs, xv, c);
+    };
+    SolveReport r;
+    if (precondition) {
+      Ilu0Factors fac = ilu0_factor(m);
+      LinearOperator op = right_preconditioned(m, fac);
+      std::vector<double> r0 = spmv(m, x);
+      for (std::size_t i = 0; i < n; ++i) r0[i] = f[i] - r0[i];
+      std::vector<double> w(n, 0.0);
+      r = dispatch(op, r0, w);
+      r.op_counts.matvecs += 1;
+      r.op_counts.vec_updates += 1;
+      std::vector<double> z = ilu0_apply(fac, w);
+      axpy(1.0, z, x);
+      r.op_counts.vec_updates += 1;
+    } else {
+      r = dispatch(as_operator(m), fs, x);
+    }
+    std::vector<double> ax = spmv(m, x);
+    r.op_counts.matvecs += 1;
+    for (std::size_t i = 0; i < n; ++i) ax[i] = f[i] - ax[i];
+    r.op_counts.vec_updates += 1;
+    r.op_counts.termination_dots += 1;
+    const double true_norm = norm2(ax);
+    r.residual_history.push_back(true_norm);
+    r.final_residual = true_norm;
+    if (r.converged && true_norm > c.tol) {
+      r.converged = false;
+      r.breakdown = "recomputed true residual exceeds the threshold";
+    }
+    std::memcpy(x_out, x.data(), sizeof(double) * n);
+    fill(rep, r);
   });
 }
 

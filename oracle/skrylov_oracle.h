@@ -73,6 +73,14 @@ typedef struct {
   char error[512]; /* message of a non-zero status */
 } orc_report;
 
+/* ILU(0) (ilu0.hpp:39-134): factor values in A's pattern (unit-lower L strictly below the
+ * diagonal, U on and above it; A's columns ascending), and z = (LU)^{-1} r */
+int orc_ilu0_factor(const orc_csr* a, double* lu_out, char* err, uint64_t errcap);
+void orc_ilu0_apply(const orc_csr* a, const double* lu, const double* r, double* z);
+/* while set (lu != NULL), every solver applies A (LU)^{-1} for the matrix object `a`
+ * (right_preconditioned, ilu0.hpp:138-146); NULL clears it.  Not thread-safe (tests only). */
+void orc_set_right_preconditioner(const orc_csr* a, const double* lu);
+
 /* report lifetime */
 void orc_report_init(orc_report* r);
 void orc_report_free(orc_report* r);

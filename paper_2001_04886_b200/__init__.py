@@ -8,7 +8,7 @@ from .problems import CONFIGS, Stencil, convection_diffusion, splitmix64_uniform
 from .sstep import (  # noqa: F401
     BreakdownError, Context, CudaError, DeviceOperator, LogicError, SolveReport, SolverConfig, SStepBasis,
     SStepConfig, cholesky_upper, gmres_solve, gram_solve, hessenberg_lsq, krylov_block, sarnoldi, sgmres_solve,
-    sgmres_solve_device, smr_solve, smr_step, somin_solve, somin_solve_device,
+    sgmres_solve_device, smr_solve, smr_step, solve_linear, somin_solve, somin_solve_device, ilu0_factor,
 )
 
 __version__ = "0.1.0"

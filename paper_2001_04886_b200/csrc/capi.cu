@@ -48,8 +48,9 @@ skc::SStepCfg conv(const skc_sstep_config* c) {
   s.unbounded_window = c->unbounded_window != 0;
   s.debug_checks = c->debug_checks != 0;
   s.divergence_factor = c->divergence_factor;
-  // bench.hpp:160-166 wraps ILU(0) when precondition is set; not provided on the GPU path
-  skc::require(!s.precondition, "precondition: ILU(0) right preconditioning is not provided by the B200 path");
+  // `precondition` is honored by the driver, not the core loops (sstep.hpp:54, solvers.hpp:51):
+  // the solvers ignore it, as the reference's do; the driver composes ILU(0) right
+  // preconditioning (bench.hpp:160-171) from skc_op_create_ilu0 / skc_ilu0_solve
   return s;
 }
 
@@ -218,7 +219,61 @@ int skc_op_size(const skc_op* op, uint64_t* n) {
 int skc_op_kind(const skc_op* op, int* kind) {
   return guarded([&] {
     skc::require(op && kind, "null argument");
-    *kind = op->o.d.kind == skc::kCsr ? 0 : op->o.d.dim;
+    *kind = op->o.d.kind == skc::kIlu0 ? 4 : op->o.d.kind == skc::kCsr ? 0 : op->o.d.dim;
+  });
+}
+
+int skc_op_create_ilu0(skc_ctx* ctx, uint64_t n, const uint64_t* row_offsets, const uint64_t* col_indices,
+                       const double* values, skc_op** out) {
+  return guarded([&] {
+    skc::require(ctx && row_offsets && out, "null argument");
+    skc::require(n == 0 || (col_indices && values) || row_offsets[n] == 0, "null argument");
+    set_device(ctx);
+    auto* op = new skc_op;
+    try {
+      skc::build_ilu0_op(ctx->c, op->o, (int64_t)n, row_offsets, col_indices, values);
+    } catch (...) {
+      delete op;
+      throw;
+    }
+    *out = op;
+  });
+}
+
+int skc_ilu0_solve_device(skc_ctx* ctx, const skc_op* op, const double* r, double* z) {
+  return guarded([&] {
+    skc::require(ctx && op && r && z, "null argument");
+    skc::require(op->o.d.kind == skc::kIlu0, "ilu0_solve: operator is not ILU(0)-preconditioned");
+    set_device(ctx);
+    skc::launch_ilu0_solve(ctx->c, *op->o.ilu, r, z, nullptr, nullptr);
+  });
+}
+
+int skc_ilu0_solve(skc_ctx* ctx, const skc_op* op, const double* r, double* z) {
+  return guarded([&] {
+    skc::require(ctx && op && r && z, "null argument");
+    skc::require(op->o.d.kind == skc::kIlu0, "ilu0_solve: operator is not ILU(0)-preconditioned");
+    set_device(ctx);
+    skc::Ctx& c = ctx->c;
+    const size_t n = (size_t)op->o.n;
+    double* rd = (double*)c.workspace("io_x", n * sizeof(double));
+    double* zd = (double*)c.workspace("io_f", n * sizeof(double));
+    CK(cudaMemcpyAsync(rd, r, n * sizeof(double), cudaMemcpyHostToDevice, c.stream));
+    skc::launch_ilu0_solve(c, *op->o.ilu, rd, zd, nullptr, nullptr);
+    CK(cudaMemcpyAsync(z, zd, n * sizeof(double), cudaMemcpyDeviceToHost, c.stream));
+    c.sync();
+  });
+}
+
+int skc_ilu0_factor(uint64_t n, const uint64_t* row_offsets, const uint64_t* col_indices, const double* values,
+                    double* lu_out) {
+  return guarded([&] {
+    skc::require(row_offsets && lu_out, "null argument");
+    skc::require(n == 0 || (col_indices && values) || row_offsets[n] == 0, "null argument");
+    skc::validate_csr((int64_t)n, row_offsets, col_indices);
+    std::vector<double> lu;
+    skc::ilu0_factor_host((int64_t)n, row_offsets, col_indices, values, lu);
+    std::memcpy(lu_out, lu.data(), sizeof(double) * lu.size());
   });
 }
 
@@ -350,7 +405,6 @@ int skc_gmres_solve(skc_ctx* ctx, const skc_op* op, const double* f, double* x, 
                                             skc::Report& r) {
     skc::require(cfg != nullptr, "null config");
     skc::require(cfg->method == 3, "gmres: only method = gmres (3) runs on the B200 path");
-    skc::require(!cfg->precondition, "precondition: ILU(0) right preconditioning is not provided by the B200 path");
     skc::gmres_device(c, o, fd, xd, cfg->m, cfg->tol, cfg->max_iterations, r);
   });
 }

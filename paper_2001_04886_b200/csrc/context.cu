@@ -305,6 +305,19 @@ static bool detect_grid(int64_t n, const uint64_t* offs, const uint64_t* cols, i
   return true;
 }
 
+void validate_csr(int64_t n, const uint64_t* offs, const uint64_t* cols) {
+  // sparse.hpp:41-63 invariants
+  require(n >= 1, "SparseMatrix: empty matrix");
+  require(offs[0] == 0, "SparseMatrix: offsets must start at 0");
+  for (int64_t i = 0; i < n; ++i) {
+    require(offs[i] <= offs[i + 1], "SparseMatrix: offsets not non-decreasing");
+    for (uint64_t q = offs[i]; q < offs[i + 1]; ++q) {
+      require(cols[q] < (uint64_t)n, "SparseMatrix: column index out of range");
+      require(q == offs[i] || cols[q - 1] < cols[q], "SparseMatrix: columns not strictly increasing within a row");
+    }
+  }
+}
+
 void build_csr_op(Ctx& c, Op& op, int64_t n, const uint64_t* offs, const uint64_t* cols, const double* vals) {
   // sparse.hpp:41-63 invariants
   require(n >= 1, "SparseMatrix: empty matrix");

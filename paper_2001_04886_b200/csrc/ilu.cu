@@ -1,0 +1,216 @@
+// ilu.cu -- ILU(0) right preconditioning on the device: the operator A (LU)^{-1}
+// (right_preconditioned, ilu0.hpp:138-146) and the solve z = (LU)^{-1} r (ilu0_apply,
+// ilu0.hpp:99-127), the pieces the reference driver composes when `precondition` is set
+// (solve_linear, bench.hpp:149-191).
+//
+// The factorization is the reference's row-wise IKJ elimination restricted to pattern(A)
+// (ilu0_factor, ilu0.hpp:45-95), run once on the host (O(nnz), the same IEEE operations in the
+// same order, no FMA contraction) with the reference's error behaviour: a row without a
+// diagonal is an invalid argument, a pivot below 1e-14 max|diag(A)| a breakdown naming the row.
+//
+// The triangular solves are level-scheduled: rows are grouped by their dependency depth in L
+// (resp. U), and one cooperative launch walks the levels with a grid barrier between them,
+// every row of a level on its own thread.  Each row is evaluated exactly as the reference's
+// sequential loop does (acc -= l * z in the row's column order, then / diag for U), so the
+// result is bit-identical to ilu0_apply; only the order in which independent rows are
+// visited changes.  For a 5-point grid in natural order the levels are the anti-diagonals
+// (nx + ny - 1 of them).
+#include <cooperative_groups.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "device_util.cuh"
+#include "skc_internal.hpp"
+
+namespace skc {
+
+namespace {
+
+constexpr int TR_NT = 512;
+
+template <bool LOWER>
+__global__ void __launch_bounds__(TR_NT) k_trsv(const int64_t* __restrict__ rp, const int32_t* __restrict__ ci,
+                                                const double* __restrict__ v, const int32_t* __restrict__ perm,
+                                                const int64_t* __restrict__ lev, int nlev, const double* r, double* z,
+                                                const int* halt, const int* cond) {
+  SKC_PDL_ENTRY();
+  if (skip_launch(halt, cond)) return;
+  namespace cg = cooperative_groups;
+  cg::grid_group grid = cg::this_grid();
+  const int64_t gt = (int64_t)blockIdx.x * blockDim.x + threadIdx.x, gn = (int64_t)gridDim.x * blockDim.x;
+  for (int L = 0; L < nlev; ++L) {
+    const int64_t e = lev[L + 1];
+    for (int64_t q = lev[L] + gt; q < e; q += gn) {
+      const int i = perm[q];
+      if (LOWER) {  // unit lower: z_i = r_i - sum_j l_ij z_j
+        double acc = r[i];
+        for (int64_t p = rp[i]; p < rp[i + 1]; ++p) acc = __dsub_rn(acc, __dmul_rn(v[p], z[ci[p]]));
+        z[i] = acc;
+      } else {  // upper: z_i = (z_i - sum_{j>i} u_ij z_j) / u_ii
+        double acc = z[i], dia = 0.0;
+        for (int64_t p = rp[i]; p < rp[i + 1]; ++p) {
+          if (ci[p] == i)
+            dia = v[p];
+          else
+            acc = __dsub_rn(acc, __dmul_rn(v[p], z[ci[p]]));
+        }
+        z[i] = __ddiv_rn(acc, dia);
+      }
+    }
+    if (L + 1 < nlev) grid.sync();
+  }
+}
+
+template <bool LOWER>
+void launch_trsv(Ctx& c, const IluData& d, const double* r, double* z, const int* halt, const int* cond) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = c.sm_count;
+  cfg.blockDim = TR_NT;
+  cfg.stream = c.stream;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeCooperative;
+  at[0].val.cooperative = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  const double bytes = LOWER ? 8.0 * (2.0 * d.n) + 12.0 * d.nnz_l + 12.0 * d.n : 8.0 * (2.0 * d.n) + 12.0 * d.nnz_u + 12.0 * d.n;
+  Launch lh(c, LOWER ? "ilu_lower" : "ilu_upper", bytes);
+  if (LOWER)
+    CK(cudaLaunchKernelEx(&cfg, k_trsv<true>, d.lrp, d.lci, d.lv, d.lperm, d.llev, d.nlev_l, r, z, halt, cond));
+  else
+    CK(cudaLaunchKernelEx(&cfg, k_trsv<false>, d.urp, d.uci, d.uv, d.uperm, d.ulev, d.nlev_u, (const double*)nullptr, z,
+                          halt, cond));
+}
+
+template <class T>
+const T* upload(Op& owner, const std::vector<T>& h) {
+  void* p = nullptr;
+  CK(cudaMalloc(&p, std::max<size_t>(sizeof(T) * h.size(), 16)));
+  owner.owned.push_back(p);
+  if (!h.empty()) CK(cudaMemcpy(p, h.data(), sizeof(T) * h.size(), cudaMemcpyHostToDevice));
+  return static_cast<const T*>(p);
+}
+
+// rows grouped by level (ascending row within a level); levels from the dependency depth
+void level_schedule(int64_t n, const std::vector<int64_t>& rp, const std::vector<int32_t>& ci, bool lower,
+                    std::vector<int32_t>& perm, std::vector<int64_t>& lev) {
+  std::vector<int32_t> depth(n, 0);
+  int32_t maxd = 0;
+  auto row = [&](int64_t i) {
+    int32_t dd = 0;
+    for (int64_t p = rp[i]; p < rp[i + 1]; ++p)
+      if (ci[p] != i) dd = std::max(dd, depth[ci[p]] + 1);
+    depth[i] = dd;
+    maxd = std::max(maxd, dd);
+  };
+  if (lower)
+    for (int64_t i = 0; i < n; ++i) row(i);
+  else
+    for (int64_t i = n - 1; i >= 0; --i) row(i);
+  lev.assign((size_t)maxd + 2, 0);
+  for (int64_t i = 0; i < n; ++i) ++lev[(size_t)depth[i] + 1];
+  for (size_t k = 1; k < lev.size(); ++k) lev[k] += lev[k - 1];
+  perm.assign(n, 0);
+  std::vector<int64_t> fill(lev.begin(), lev.end() - 1);
+  for (int64_t i = 0; i < n; ++i) perm[fill[depth[i]]++] = (int32_t)i;
+}
+
+}  // namespace
+
+// ilu0_factor (ilu0.hpp:45-95) on the host, restated: the factor values in A's pattern
+void ilu0_factor_host(int64_t n, const uint64_t* offs, const uint64_t* cols, const double* vals,
+                      std::vector<double>& lu) {
+  lu.assign(vals, vals + offs[n]);
+  std::vector<uint64_t> diag(n);
+  double max_diag = 0.0;
+  for (int64_t i = 0; i < n; ++i) {
+    bool found = false;
+    for (uint64_t p = offs[i]; p < offs[i + 1]; ++p)
+      if (cols[p] == (uint64_t)i) {
+        diag[i] = p;
+        found = true;
+        max_diag = std::max(max_diag, std::abs(lu[p]));
+      }
+    require(found, "ilu0: row " + std::to_string(i + 1) + " has no diagonal entry");
+  }
+  const double pivot_floor = 1e-14 * max_diag;
+  std::vector<int64_t> pos(n, -1);
+  for (int64_t i = 0; i < n; ++i) {
+    for (uint64_t p = offs[i]; p < offs[i + 1]; ++p) pos[cols[p]] = (int64_t)p;
+    for (uint64_t p = offs[i]; p < offs[i + 1] && cols[p] < (uint64_t)i; ++p) {
+      const uint64_t k = cols[p];
+      if (std::abs(lu[diag[k]]) < pivot_floor) fail(SKC_EBREAKDOWN, "ilu0: zero pivot at row " + std::to_string(k + 1));
+      const double mult = lu[p] / lu[diag[k]];
+      lu[p] = mult;
+      for (uint64_t q = diag[k] + 1; q < offs[k + 1]; ++q) {
+        const int64_t w = pos[cols[q]];
+        if (w >= 0) lu[(size_t)w] -= mult * lu[q];
+      }
+    }
+    if (std::abs(lu[diag[i]]) < pivot_floor) fail(SKC_EBREAKDOWN, "ilu0: zero pivot at row " + std::to_string(i + 1));
+    for (uint64_t p = offs[i]; p < offs[i + 1]; ++p) pos[cols[p]] = -1;
+  }
+}
+
+void build_ilu0_op(Ctx& c, Op& op, int64_t n, const uint64_t* offs, const uint64_t* cols, const double* vals) {
+  op.ilu = std::make_unique<IluData>();
+  IluData& d = *op.ilu;
+  build_csr_op(c, d.base, n, offs, cols, vals);  // validates the CSR invariants; one GPU only
+  std::vector<double> lu;
+  ilu0_factor_host(n, offs, cols, vals, lu);
+  // split into L (strictly lower) and U (diagonal and above), A's column order kept
+  std::vector<int64_t> lrp(n + 1, 0), urp(n + 1, 0);
+  std::vector<int32_t> lci, uci;
+  std::vector<double> lv, uv;
+  for (int64_t i = 0; i < n; ++i) {
+    for (uint64_t p = offs[i]; p < offs[i + 1]; ++p) {
+      if (cols[p] < (uint64_t)i) {
+        lci.push_back((int32_t)cols[p]);
+        lv.push_back(lu[p]);
+      } else {
+        uci.push_back((int32_t)cols[p]);
+        uv.push_back(lu[p]);
+      }
+    }
+    lrp[i + 1] = (int64_t)lci.size();
+    urp[i + 1] = (int64_t)uci.size();
+  }
+  std::vector<int32_t> lperm, uperm;
+  std::vector<int64_t> llev, ulev;
+  level_schedule(n, lrp, lci, true, lperm, llev);
+  level_schedule(n, urp, uci, false, uperm, ulev);
+  d.n = n;
+  d.nnz_l = (int64_t)lv.size();
+  d.nnz_u = (int64_t)uv.size();
+  d.nlev_l = (int)llev.size() - 1;
+  d.nlev_u = (int)ulev.size() - 1;
+  d.lrp = upload(op, lrp);
+  d.lci = upload(op, lci);
+  d.lv = upload(op, lv);
+  d.urp = upload(op, urp);
+  d.uci = upload(op, uci);
+  d.uv = upload(op, uv);
+  d.lperm = upload(op, lperm);
+  d.uperm = upload(op, uperm);
+  d.llev = upload(op, llev);
+  d.ulev = upload(op, ulev);
+  op.device = c.device;
+  op.n = n;
+  op.rows = n;
+  std::memset(&op.d, 0, sizeof op.d);
+  op.d.kind = kIlu0;
+  op.d.n = n;
+  op.d.ilu = op.ilu.get();
+}
+
+// z = (LU)^{-1} r (ilu0_apply); r may alias z
+void launch_ilu0_solve(Ctx& c, const IluData& d, const double* r, double* z, const int* halt, const int* cond) {
+  launch_trsv<true>(c, d, r, z, halt, cond);
+  launch_trsv<false>(c, d, z, z, halt, cond);
+  CK(cudaGetLastError());
+}
+
+}  // namespace skc

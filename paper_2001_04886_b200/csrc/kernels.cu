@@ -79,6 +79,12 @@ __global__ void __launch_bounds__(256) k_apply_csr(const __grid_constant__ DevOp
 }
 
 void launch_apply(Ctx& c, const DevOp& op, const double* x, double* y, const int* halt, const int* cond) {
+  if (op.kind == kIlu0) {  // y = A (LU)^{-1} x (right_preconditioned, ilu0.hpp:138-146)
+    double* tmp = (double*)c.workspace("ilu_apply_tmp", sizeof(double) * (size_t)op.n);
+    launch_ilu0_solve(c, *op.ilu, x, tmp, halt, cond);
+    launch_apply(c, op.ilu->base.d, tmp, y, halt, cond);
+    return;
+  }
   if (op.kind != kCsr && c.world() > 1) {  // slabs: depth-1 matrix-powers sweep (halo exchange)
     double* outs[2] = {nullptr, y};
     launch_mpk(c, op, x, nullptr, outs, 1, 0, nullptr, 1, nullptr, 0, halt, cond);

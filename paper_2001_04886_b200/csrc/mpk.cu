@@ -606,7 +606,7 @@ void dispatch_j(Ctx& c, MpkDesc& d) {
 
 }  // namespace
 
-int mpk_max_depth(const DevOp& op) { return op.kind == kCsr ? 0 : op.dim == 2 ? MPK_MAXJ : 3; }
+int mpk_max_depth(const DevOp& op) { return op.kind == kCsr || op.kind == kIlu0 ? 0 : op.dim == 2 ? MPK_MAXJ : 3; }
 int powers_depth(const Ctx& c, const DevOp& op) { return op.dim == 3 && c.world() == 1 ? 0 : mpk_max_depth(op); }
 
 // Powers of src*scale: out[0] (level 0, may be null) .. out[J].  Products X[x] . level j for

@@ -1127,7 +1127,7 @@ struct Engine {
   // points per CTA of the on-chip orthogonalization (one CTA per SM), or 0 when it is off or
   // the candidate slices do not fit in shared memory
   int64_t orth_points() const {
-    if (!c.orth || c.world() != 1 || s < 2) return 0;
+    if (!c.orth || c.world() != 1 || s < 2 || op.d.kind == kIlu0) return 0;
     const int64_t P = ((op.n + c.sm_count - 1) / c.sm_count + 1) & ~(int64_t)1;
     return orth_smem(s, m, P) <= kOrthSmemCap ? P : 0;
   }

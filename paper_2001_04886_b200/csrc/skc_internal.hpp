@@ -29,7 +29,11 @@ void cuda_check(cudaError_t e, const char* what, const char* file, int line);
 #define CK(call) ::skc::cuda_check((call), #call, __FILE__, __LINE__)
 
 // ---------------------------------------------------------------- operator
-enum OpKind : int { kCsr = 0, kStencilConst = 1, kStencilVarK = 2, kStencilDia = 3 };
+// kIlu0: A (LU)^{-1}, ILU(0) right preconditioning (ilu0.hpp:138-146); host-dispatched only
+// (no kernel evaluates it point-wise: applies go through launch_apply)
+enum OpKind : int { kCsr = 0, kStencilConst = 1, kStencilVarK = 2, kStencilDia = 3, kIlu0 = 4 };
+
+struct IluData;
 
 // Passed by value to kernels. Natural ordering, x fastest.
 struct DevOp {
@@ -51,6 +55,7 @@ struct DevOp {
   int64_t halo_rows;
   const double* hlo;  // halo rows -halo_rows..-1 of the sweep source (valid after an exchange)
   const double* hhi;  // halo rows nrows..nrows+halo_rows-1
+  const struct IluData* ilu;  // kIlu0: host-side factors and base operator (never read on device)
 };
 
 struct Op {
@@ -62,7 +67,23 @@ struct Op {
   double* hlo = nullptr;  // halo_rows rows below the slab (rows -halo_rows..-1)
   double* hhi = nullptr;  // halo_rows rows above the slab
   int64_t rowlen = 0;     // points per slowest-dimension row (2D: nx, 3D: nx*ny)
+  std::unique_ptr<IluData> ilu;  // kIlu0
   ~Op();
+};
+
+// ILU(0) factors on the device (ilu0.hpp:39-134): unit-lower L (strictly below the diagonal)
+// and U (on and above) as CSR in A's pattern order, each with a level schedule (rows grouped
+// by dependency depth, ascending row index within a level) for the triangular solves
+struct IluData {
+  Op base;  // A itself (stencil kernels when the pattern is a 5/7-point grid, else CSR)
+  int64_t n = 0;
+  const int64_t *lrp = nullptr, *urp = nullptr;
+  const int32_t *lci = nullptr, *uci = nullptr;
+  const double *lv = nullptr, *uv = nullptr;
+  const int32_t *lperm = nullptr, *uperm = nullptr;  // rows in level order
+  const int64_t *llev = nullptr, *ulev = nullptr;    // level offsets into lperm / uperm
+  int nlev_l = 0, nlev_u = 0;
+  int64_t nnz_l = 0, nnz_u = 0;
 };
 
 // ---------------------------------------------------------------- streaming geometry
@@ -254,6 +275,12 @@ void launch_mgs(Ctx& c, const Geo& geo, int s, const double* const* Vi, double* 
 // operator helpers
 void build_stencil_op(Ctx& c, Op& op, const skc_stencil_desc& d, const double* kcell_host);
 void build_csr_op(Ctx& c, Op& op, int64_t n, const uint64_t* offs, const uint64_t* cols, const double* vals);
+void validate_csr(int64_t n, const uint64_t* offs, const uint64_t* cols);  // sparse.hpp:41-63
+// ILU(0) right preconditioning (ilu.cu): op = A (LU)^{-1}; z = (LU)^{-1} r
+void build_ilu0_op(Ctx& c, Op& op, int64_t n, const uint64_t* offs, const uint64_t* cols, const double* vals);
+void ilu0_factor_host(int64_t n, const uint64_t* offs, const uint64_t* cols, const double* vals,
+                      std::vector<double>& lu);
+void launch_ilu0_solve(Ctx& c, const IluData& d, const double* r, double* z, const int* halt, const int* cond);
 
 // ---------------------------------------------------------------- reports (host)
 struct Report {

@@ -626,7 +626,7 @@ void somin_device(Ctx& c, const Op& op, const double* f, double* x, const SStepC
   CK(cudaMemcpyAsync(&hs, st, sizeof hs, cudaMemcpyDeviceToHost, c.stream));
   c.sync();
   // small problems: whole iterations in one cooperative launch per chunk (see k_somin_persist)
-  if (c.persist && !gcr && !cfg.debug_checks && c.world() == 1 && s <= 4 && cfg.k <= (uint64_t)PS_MAXK &&
+  if (c.persist && op.d.kind != kIlu0 && !gcr && !cfg.debug_checks && c.world() == 1 && s <= 4 && cfg.k <= (uint64_t)PS_MAXK &&
       n <= (1 << 18)) {
     PersistDesc pd;
     std::memset(&pd, 0, sizeof pd);

@@ -187,6 +187,32 @@ class Context:
                                       _dp(vals), C.byref(h)))
         return DeviceOperator(self, h, n)
 
+    def ilu0(self, row_offsets, col_indices, values) -> "DeviceOperator":
+        """right_preconditioned(a, ilu0_factor(a)) (ilu0.hpp:138-146, 45-95): the operator
+        A (LU)^{-1}, ILU(0) factored on the host with the reference's algorithm; its
+        `ilu0_solve` gives z = (LU)^{-1} r.  breakdown_error ("ilu0: zero pivot at row N") is
+        raised as BreakdownError."""
+        offs = np.ascontiguousarray(row_offsets, dtype=np.uint64)
+        cols = np.ascontiguousarray(col_indices, dtype=np.uint64)
+        vals = np.ascontiguousarray(values, dtype=np.float64)
+        n = len(offs) - 1
+        h = C.c_void_p()
+        check(lib().skc_op_create_ilu0(self.h, n, offs.ctypes.data_as(P(u64)), cols.ctypes.data_as(P(u64)),
+                                       _dp(vals), C.byref(h)))
+        return DeviceOperator(self, h, n)
+
+
+def ilu0_factor(row_offsets, col_indices, values) -> np.ndarray:
+    """ilu0_factor (ilu0.hpp:45-95) on the host: the factor values in A's pattern (unit-lower L
+    strictly below the diagonal, U on and above it)."""
+    offs = np.ascontiguousarray(row_offsets, dtype=np.uint64)
+    cols = np.ascontiguousarray(col_indices, dtype=np.uint64)
+    vals = np.ascontiguousarray(values, dtype=np.float64)
+    lu = np.zeros(len(vals))
+    check(lib().skc_ilu0_factor(len(offs) - 1, offs.ctypes.data_as(P(u64)), cols.ctypes.data_as(P(u64)),
+                                _dp(vals), _dp(lu)))
+    return lu
+
 
 class DeviceOperator:
     """Device-describable operator (the GPU replacement of LinearOperator, operator.hpp:34-57)."""
@@ -205,7 +231,16 @@ class DeviceOperator:
     def kind(self) -> str:
         k = C.c_int()
         check(lib().skc_op_kind(self.h, C.byref(k)))
-        return {0: "csr", 2: "stencil2d", 3: "stencil3d"}[k.value]
+        return {0: "csr", 2: "stencil2d", 3: "stencil3d", 4: "ilu0"}[k.value]
+
+    def ilu0_solve(self, r) -> np.ndarray:
+        """z = (LU)^{-1} r for an ILU(0)-preconditioned operator (ilu0_apply, ilu0.hpp:99-127)."""
+        r = np.ascontiguousarray(r, dtype=np.float64)
+        if r.shape != (self.n,):
+            raise ValueError("ilu0_apply: dimension mismatch")
+        z = np.zeros(self.n)
+        check(lib().skc_ilu0_solve(self.ctx.h, self.h, _dp(r), _dp(z)))
+        return z
 
     def apply(self, x) -> np.ndarray:
         x = np.ascontiguousarray(x, dtype=np.float64)
@@ -252,6 +287,46 @@ def smr_solve(op, f, x, cfg: SStepConfig = SStepConfig()) -> SolveReport:
 def gmres_solve(op, f, x, cfg: SolverConfig = SolverConfig()) -> SolveReport:
     """solvers.hpp:297-359 (standard MGS-GMRES(m) on the device)."""
     return _solve(lib().skc_gmres_solve, op, f, x, cfg)
+
+
+def solve_linear(ctx: Context, row_offsets, col_indices, values, f, x0, method: str, cfg: SStepConfig,
+                 precondition: bool = True):
+    """The reference driver around the s-step solvers (solve_linear, bench.hpp:149-191), on the GPU:
+    with `precondition`, ILU(0) right preconditioning -- the solver iterates w from zero on
+    A (LU)^{-1} with the initial residual as right-hand side, then x = x0 + (LU)^{-1} w -- so the
+    residual it minimizes is the true residual; in both cases the true residual is recomputed
+    and appended to the history, and a converged solve whose true residual exceeds cfg.tol is
+    reported as not converged.  Returns (x, report).  `method` is "somin" or "sgmres";
+    cfg.tol is the driver's threshold."""
+    solve = {"somin": somin_solve, "sgmres": sgmres_solve}[method]
+    a = ctx.csr(row_offsets, col_indices, values)
+    f = np.ascontiguousarray(f, dtype=np.float64)
+    x = np.array(x0, dtype=np.float64, copy=True)
+    if precondition:
+        op = ctx.ilu0(row_offsets, col_indices, values)
+        r0 = f - a.apply(x)
+        w = np.zeros(a.n)
+        rep = solve(op, r0, w, cfg)
+        c = list(rep.op_counts)
+        c[1] += 1  # driver-side initial residual
+        c[2] += 1
+        x += op.ilu0_solve(w)  # axpy(1.0, z, x)
+        c[2] += 1
+    else:
+        rep = solve(a, f, x, cfg)
+        c = list(rep.op_counts)
+    ax = f - a.apply(x)
+    c[1] += 1
+    c[2] += 1
+    c[4] += 1
+    true_norm = float(np.sqrt(np.add.accumulate(ax * ax)[-1]))  # norm2: sequential sum
+    rep.op_counts = tuple(c)
+    rep.residual_history.append(true_norm)
+    rep.final_residual = true_norm
+    if rep.converged and true_norm > cfg.tol:
+        rep.converged = False
+        rep.breakdown = "recomputed true residual exceeds the threshold"
+    return x, rep
 
 
 def smr_step(op, x: np.ndarray, r: np.ndarray, s: int, counter: list | None = None) -> np.ndarray:

@@ -351,8 +351,6 @@ def test_config_errors(ctx):
         somin_solve(op, f, x, SStepConfig(s=2, k=0))
     with pytest.raises(ValueError, match="m must be at least 1"):
         sgmres_solve(op, f, x, SStepConfig(s=2, m=0))
-    with pytest.raises(ValueError, match="ILU"):
-        somin_solve(op, f, x, SStepConfig(s=2, precondition=True))
     with pytest.raises(ValueError):
         somin_solve(op, f[:-1], x, SStepConfig(s=2))
 
