@@ -142,6 +142,13 @@ class DeviceOperator {
   }
   skc_ctx* ctx() const { return ctx_; }
   skc_op* handle() const { return op_; }
+  // z = (LU)^{-1} r for an operator made by Context::ilu0 (ilu0_apply, ilu0.hpp:99-134)
+  std::vector<double> ilu0_apply(std::span<const double> r) const {
+    if (r.size() != n_) throw std::invalid_argument("ilu0_apply: dimension mismatch");
+    std::vector<double> z(n_, 0.0);
+    check(skc_ilu0_solve(ctx_, op_, r.data(), z.data()));
+    return z;
+  }
 
  private:
   skc_ctx* ctx_;
@@ -170,6 +177,15 @@ class Context {
   DeviceOperator stencil(const skc_stencil_desc& d, const double* kcell = nullptr) const {
     skc_op* op = nullptr;
     check(skc_op_create_stencil(h_, &d, kcell, &op));
+    return DeviceOperator(h_, op);
+  }
+  // right_preconditioned(a, ilu0_factor(a)) (ilu0.hpp:138-146, 45-95): A (LU)^{-1}; throws
+  // breakdown_error "ilu0: zero pivot at row N" like ilu0_factor
+  DeviceOperator ilu0(std::span<const std::size_t> row_offsets, std::span<const std::size_t> col_indices,
+                      std::span<const double> values) const {
+    skc_op* op = nullptr;
+    check(skc_op_create_ilu0(h_, row_offsets.size() - 1, reinterpret_cast<const uint64_t*>(row_offsets.data()),
+                             reinterpret_cast<const uint64_t*>(col_indices.data()), values.data(), &op));
     return DeviceOperator(h_, op);
   }
 
