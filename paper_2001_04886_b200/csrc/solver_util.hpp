@@ -4,6 +4,7 @@
 #pragma once
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <utility>
@@ -113,12 +114,29 @@ struct LinBuilder {
 };
 
 // Inner products L_l . R_r at dot index dot0 + l*nr + r, split over launches of GR_MAXL rows.
+// Left rows per launch: every distinct operand of a launch is staged per point tile, so many
+// operands force small tiles (kilobyte-sized bulk copies, thousands of concurrent DRAM streams;
+// measured 1.8 TB/s with 72 operands vs 6+ TB/s with ~20).  Wide Grams are therefore split into
+// launches of at most ~kGramOperands operands; each re-reads the right operands (few) once more.
+inline size_t gram_chunk(size_t nr) {
+  // measured on C4 (s = 8): Scalar1 products (nr = 1) best at ~24 operands, the cross
+  // products (nr = s = 8) at ~32
+  static const int target = [] {
+    const char* e = std::getenv("SKC_GRAM_U");
+    return e ? std::atoi(e) : 0;
+  }();
+  const int t = target > 0 ? target : nr <= 2 ? 24 : 32;
+  const int c = std::max(8, t - (int)nr);
+  return (size_t)std::min(c, GR_MAXL);
+}
+
 inline void launch_gram_list(Ctx& c, const Geo& g, const std::vector<const double*>& L,
                              const std::vector<const double*>& R, double* partials, int dot0, const int* halt,
                              const int* cond, const char* name = "gram") {
   require(!R.empty() && R.size() <= (size_t)GR_MAXR, "gram: right operand count out of range");
-  for (size_t l0 = 0; l0 < L.size(); l0 += GR_MAXL) {
-    const size_t l1 = std::min(L.size(), l0 + (size_t)GR_MAXL);
+  const size_t chunk = gram_chunk(R.size());
+  for (size_t l0 = 0; l0 < L.size(); l0 += chunk) {
+    const size_t l1 = std::min(L.size(), l0 + chunk);
     GramDesc d;
     std::memset(&d, 0, sizeof d);
     d.nl = (int)(l1 - l0);
@@ -145,8 +163,9 @@ inline void launch_gram_map(Ctx& c, const Geo& g, const std::vector<const double
                             const std::vector<const double*>& R, const std::vector<GramCol>& cols, double* partials,
                             const int* halt, const int* cond, const char* name) {
   require(!R.empty() && R.size() <= (size_t)GR_MAXR && cols.size() == R.size(), "gram: right operand count out of range");
-  for (size_t l0 = 0; l0 < L.size(); l0 += GR_MAXL) {
-    const size_t l1 = std::min(L.size(), l0 + (size_t)GR_MAXL);
+  const size_t chunk = gram_chunk(R.size());
+  for (size_t l0 = 0; l0 < L.size(); l0 += chunk) {
+    const size_t l1 = std::min(L.size(), l0 + chunk);
     GramDesc d;
     std::memset(&d, 0, sizeof d);
     d.nl = (int)(l1 - l0);
