@@ -149,6 +149,9 @@ int skc_ilu0_solve(skc_ctx* ctx, const skc_op* ilu_op, const double* r, double* 
 int skc_ilu0_solve_device(skc_ctx* ctx, const skc_op* ilu_op, const double* r, double* z); /* device, async */
 int skc_ilu0_factor(uint64_t n, const uint64_t* row_offsets, const uint64_t* col_indices, const double* values,
                     double* lu_out);
+/* seeded k = exp(N(0,1)) field of the variable-coefficient configurations (BASELINE configs[4];
+ * DESIGN.md "Inputs"), host only */
+int skc_fill_lognormal(uint64_t seed, uint64_t n, double* out);
 int skc_op_destroy(skc_op* op);
 int skc_op_size(const skc_op* op, uint64_t* n);
 /* 0 = general CSR, 2 = 2D stencil, 3 = 3D stencil, 4 = ILU(0)-preconditioned A (LU)^{-1} */

@@ -1,4 +1,5 @@
 // capi.cu -- the C ABI (include/skrylov_b200.h) over the C++ solvers.
+#include <cmath>
 #include <cstdlib>
 #include <cstring>
 #include <string>
@@ -262,6 +263,32 @@ int skc_ilu0_solve(skc_ctx* ctx, const skc_op* op, const double* r, double* z) {
     skc::launch_ilu0_solve(c, *op->o.ilu, rd, zd, nullptr, nullptr);
     CK(cudaMemcpyAsync(z, zd, n * sizeof(double), cudaMemcpyDeviceToHost, c.stream));
     c.sync();
+  });
+}
+
+// exp(N(0,1)) per element: Box-Muller on two splitmix64 draws of a counter-based stream
+// (element i uses state seed + 2i * golden gamma), glibc log/sqrt/cos/exp on the host -- the
+// variable-k fields of DESIGN.md "Inputs", identical bits wherever they are generated with
+// glibc (tests/test_host_lib.py checks the oracle's copy)
+int skc_fill_lognormal(uint64_t seed, uint64_t n, double* out) {
+  return guarded([&] {
+    skc::require(out != nullptr || n == 0, "null argument");
+    const double two_pi = 6.283185307179586476925286766559;
+    auto mix = [](uint64_t& st) {
+      uint64_t z = (st += 0x9E3779B97F4A7C15ULL);
+      z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+      z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+      return z ^ (z >> 31);
+    };
+    for (uint64_t i = 0; i < n; ++i) {
+      uint64_t st = seed + (2 * i) * 0x9E3779B97F4A7C15ULL;
+      const uint64_t z1 = mix(st);
+      const uint64_t z2 = mix(st);
+      const double u1 = ((double)(z1 >> 11) + 1.0) * 0x1.0p-53;
+      const double u2 = (double)(z2 >> 11) * 0x1.0p-53;
+      const double g = std::sqrt(-2.0 * std::log(u1)) * std::cos(two_pi * u2);
+      out[i] = std::exp(g);
+    }
   });
 }
 

@@ -74,11 +74,6 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
       "l"(src), "r"(bytes), "r"(smem_u32(bar))
       : "memory");
 }
-// Bulk L2 prefetch through the TMA engine (no shared memory, no completion tracking):
-// address 16-byte aligned, size a multiple of 16
-__device__ __forceinline__ void bulk_prefetch_l2(const void* src, uint32_t bytes) {
-  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
-}
 // L2 eviction-priority policies for cache-hinted loads/stores
 __device__ __forceinline__ uint64_t policy_evict_first() {
   uint64_t p;

@@ -33,6 +33,16 @@ def splitmix64_uniform(seed: int, n: int, offset: int = 0) -> np.ndarray:
     return 2.0 * u - 1.0
 
 
+def lognormal_k(seed: int, n: int) -> np.ndarray:
+    """Per-cell k = exp(N(0,1)) of the variable-coefficient operator (Box-Muller on splitmix64
+    draws, glibc math on the host; see skc_fill_lognormal)."""
+    import ctypes as C
+    from . import _lib
+    out = np.zeros(n)
+    _lib.check(_lib.lib().skc_fill_lognormal(seed, n, out.ctypes.data_as(C.POINTER(C.c_double))))
+    return out
+
+
 @dataclass(frozen=True)
 class Stencil:
     """h^2-scaled 5-point (dim 2) / 7-point (dim 3) convection-diffusion operator.

@@ -90,3 +90,12 @@ def test_operator_coefficients():
     assert st.coef[3] == 4.0 and st.coef[2] == -1.0 - 10.0 * h / 2.0 and st.coef[4] == -1.0 + 10.0 * h / 2.0
     st3 = convection_diffusion(3, 256, 20.0)
     assert st3.coef[3] == 6.0 and st3.n == 256 ** 3
+
+
+def test_lognormal_field_matches_oracle_generator():
+    """The product's k-field generator (skc_fill_lognormal) gives the oracle's bits."""
+    from oracle import Oracle
+    from paper_2001_04886_b200.problems import lognormal_k
+    a = lognormal_k(4886, 5000)
+    b = Oracle("port").lognormal(4886, 5000)
+    assert np.array_equal(a.view(np.uint64), b.view(np.uint64))

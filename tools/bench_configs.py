@@ -49,9 +49,8 @@ def run(name, steps_override=None):
     st = convection_diffusion(c["dim"], c["nx"], c["conv"], variable_k=c.get("vark", False))
     kcell = None
     if c.get("vark"):
-        sys.path.insert(0, os.path.join(ROOT, "oracle"))
-        from oracle import Oracle  # host generator of the seeded k field (glibc exp/log)
-        kcell = Oracle("port").lognormal(4886, st.n)
+        from paper_2001_04886_b200.problems import lognormal_k
+        kcell = lognormal_k(4886, st.n)
     f = splitmix64_uniform(20010486, st.n)
     steps = steps_override or c["steps"]
     tol = c["rel_tol"] * float(np.linalg.norm(f)) if "rel_tol" in c else 0.0
