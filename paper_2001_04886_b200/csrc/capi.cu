@@ -94,6 +94,7 @@ skc_ctx* make_ctx(int device) {
   if (const char* e = std::getenv("SKC_ORTH")) ctx->c.orth = std::atoi(e) != 0;
   if (const char* e = std::getenv("SKC_ZFUSE")) ctx->c.zfuse = std::atoi(e) != 0;
   if (const char* e = std::getenv("SKC_PERSIST")) ctx->c.persist = std::atoi(e) != 0;
+  if (const char* e = std::getenv("SKC_SPOW")) ctx->c.spow = std::atoi(e) != 0;
   return ctx;
 }
 

@@ -274,6 +274,13 @@ struct OrthDesc {
   ArnState* st;
   double orth_tol;
   unsigned long long* trace;  // optional phase timestamps (CTA 0), diagnostics
+  // row-streamed candidate powers (2D constant stencil, s <= 4): per-CTA ghost-row buffers of
+  // levels 1 and 2 (g1 + g2 doubles per CTA at ghosts); spow 0 = per-level sweeps with grid
+  // barriers.  The buffers are in (L2-resident) global memory: shared memory beyond the
+  // candidate slice would shrink the L1 share of the unified L1/shared array, whose capacity
+  // bounds the loads in flight per SM for every streaming phase (measured: -14% on C2)
+  int spow, g1, g2;
+  double* ghosts;
 };
 
 // per-CTA completion time of a phase (diagnostics): slot base + CTA index
@@ -292,6 +299,10 @@ __device__ __forceinline__ void orth_mark(const OrthDesc& d, int slot) {
     d.trace[slot] = t;
   }
 }
+
+// streamed basis loads: L2 only (no L1 allocation), so the number of loads in flight per SM is
+// not bounded by the L1 capacity left beside the candidate slice in the unified L1/shared memory
+__device__ __forceinline__ double ldcg(const double* p) { return __ldcg(p); }
 
 // fixed-order CTA reduction of K per-thread accumulators into partial column blockIdx.x
 template <int K>
@@ -402,8 +413,8 @@ __global__ void __launch_bounds__(ORTH_NT, 1) k_arn_step(const __grid_constant__
         has[u] = p < cnt;
 #pragma unroll
         for (int l = 0; l < S; ++l) {
-          v[u][l] = has[u] ? Vi[l * np + p] : 0.0;
-          w[u][l] = dots && has[u] ? Vn[l * np + p] : 0.0;
+          v[u][l] = has[u] ? ldcg(Vi + l * np + p) : 0.0;
+          w[u][l] = dots && has[u] ? ldcg(Vn + l * np + p) : 0.0;
         }
       }
 #pragma unroll
@@ -462,10 +473,10 @@ __global__ void __launch_bounds__(ORTH_NT, 1) k_arn_step(const __grid_constant__
       for (int u = 0; u < U; ++u) {
         const int p = p0 + u * ORTH_NT;
         has[u] = p < cnt;
-        b[u][0] = has[u] ? c0p[p] : 0.0;
+        b[u][0] = has[u] ? ldcg(c0p + p) : 0.0;
         zv[u] = ZD && has[u] ? zg[p] : 0.0;
 #pragma unroll
-        for (int l = 0; l < S; ++l) a[u][l] = basis && has[u] ? Li[l * np + p] : 0.0;
+        for (int l = 0; l < S; ++l) a[u][l] = basis && has[u] ? ldcg(Li + l * np + p) : 0.0;
 #pragma unroll
         for (int j = 1; j < S; ++j) b[u][j] = has[u] ? sc[(int64_t)(j - 1) * d.P + p] : 0.0;
       }
@@ -611,7 +622,7 @@ __global__ void __launch_bounds__(ORTH_NT, 1) k_arn_step(const __grid_constant__
           const bool h = p < cnt;
           zv[u] = h ? zs[p] : 0.0;
 #pragma unroll
-          for (int l = 0; l < S; ++l) v[u][l] = h ? Vi[l * np + p] : 0.0;
+          for (int l = 0; l < S; ++l) v[u][l] = h ? ldcg(Vi + l * np + p) : 0.0;
         }
 #pragma unroll
         for (int u = 0; u < ORTH_UC; ++u) {
@@ -676,7 +687,7 @@ __global__ void __launch_bounds__(ORTH_NT, 1) k_arn_step(const __grid_constant__
           const bool h = p < cnt;
           o[u] = h ? zs[p] : 0.0;
 #pragma unroll
-          for (int l = 0; l < S; ++l) v[u][l] = h ? Vi[l * np + p] : 0.0;
+          for (int l = 0; l < S; ++l) v[u][l] = h ? ldcg(Vi + l * np + p) : 0.0;
         }
 #pragma unroll
         for (int u = 0; u < ORTH_UC; ++u) {
@@ -719,6 +730,105 @@ __global__ void __launch_bounds__(ORTH_NT, 1) k_arn_step(const __grid_constant__
   //      every level is an exact spmv of the previous one; levels 1..s-1 stay in shared memory,
   //      levels 0..s-2 also go to memory for the neighbours' next level
   orth_mark(d, 44);
+  if (S <= 4 && d.spow) {
+    // Row-streamed: the slice is walked in index rows of nx points (row r = [r nx, (r+1) nx)
+    // relative to the slice start); step k computes level j on row k - 2(j-1), so every level
+    // only reads rows of the previous level finished in earlier steps (one __syncthreads per
+    // step, no grid barrier).  Level j is computed on e_j = s-1-j ghost rows beyond each slice
+    // edge, redundantly with the neighbouring CTAs (level 1 from seed / nu in memory), so the
+    // slice's last level needs nothing from other CTAs.  Ghost rows live in small per-CTA global buffers
+    // (the bottom ghosts are dead before the top ghosts are written, so both share one buffer;
+    // the host enables this only when every slice has at least 4 rows).  Each point is the
+    // same ascending-column sum as spmv, so the levels are bit-identical to the sweeps.
+    const int nx = (int)d.op.nx, ny = (int)d.op.ny;
+    const double cS = d.op.coef[1], cW = d.op.coef[2], cC = d.op.coef[3], cE = d.op.coef[4], cN = d.op.coef[5];
+    double* gh[2] = {d.ghosts + (int64_t)blockIdx.x * (d.g1 + d.g2), d.ghosts + (int64_t)blockIdx.x * (d.g1 + d.g2) + d.g1};
+    const int Rs = cnt > 0 ? (cnt + nx - 1) / nx : 0;
+    int ic[2], jc[2];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int64_t q = base + 2 * tid + h;
+      ic[h] = (int)(q % nx);
+      jc[h] = (int)(q / nx);
+    }
+    // level j value at relative index v (slice, or the level's ghost buffer)
+    auto slot = [&](int j, int v) -> double* {
+      if (v >= 0 && v < cnt) return sc + (int64_t)(j - 1) * d.P + v;
+      const int e = S - 1 - j;
+      return gh[j - 1] + (v < 0 ? v + e * nx : v - cnt);
+    };
+    const int kend = cnt > 0 ? Rs - 1 + 2 * (S - 2) : -(S - 2) - 1;
+    const int rin = cnt == Rs * nx ? Rs - 2 : Rs - 3;  // last row whose north neighbours are in the slice
+    // level 1's source rows (seed, columns c0-1 .. c0+2 of this thread's pair) in a register
+    // ring: rows k-1, k, k+1 in use, row k+2 loaded one step ahead
+    const int c0 = 2 * tid;
+    const int64_t q00 = base + c0;  // global index of (row 0, column c0)
+    auto load_row = [&](int rr, double (&o)[4]) {
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        const int64_t q = q00 + (int64_t)rr * nx + t - 1;
+        o[t] = c0 < nx && q >= 0 && q < d.n ? __ldcg(d.seed + q) : 0.0;
+      }
+    };
+    double ra[4], rb[4], rc[4], rn[4];
+    load_row(-(S - 2) - 1, ra);
+    load_row(-(S - 2), rb);
+    load_row(-(S - 2) + 1, rc);
+    for (int k = -(S - 2); k <= kend; ++k) {
+      load_row(k + 2, rn);  // (in flight during this step)
+#pragma unroll
+      for (int j = S - 1; j >= 1; --j) {
+        const int r = k - 2 * (j - 1), e = S - 1 - j;
+        if (r < -e || r > Rs - 1 + e) continue;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int c = c0 + h;
+          if (c >= nx) continue;
+          const int v = r * nx + c;
+          const int jr = jc[h] + r, i = ic[h];
+          if (v < -e * nx || v >= cnt + e * nx || jr < 0 || jr >= ny) continue;
+          double xs_, xw_, xc_, xe_, xn_;
+          if (j == 1) {  // seed / nu from the ring (multiply rounded as when level 0 is stored)
+            xs_ = __dmul_rn(ra[h + 1], inv);
+            xw_ = __dmul_rn(rb[h], inv);
+            xc_ = __dmul_rn(rb[h + 1], inv);
+            xe_ = __dmul_rn(rb[h + 2], inv);
+            xn_ = __dmul_rn(rc[h + 1], inv);
+          } else if (r >= 1 && r <= rin) {  // every neighbour inside the slice: shared memory
+            const double* Pj = sc + (int64_t)(j - 2) * d.P + v;
+            xs_ = Pj[-nx];
+            xw_ = Pj[-1];
+            xc_ = Pj[0];
+            xe_ = Pj[1];
+            xn_ = Pj[nx];
+          } else {
+            xs_ = jr > 0 ? *slot(j - 1, v - nx) : 0.0;
+            xw_ = i > 0 ? *slot(j - 1, v - 1) : 0.0;
+            xc_ = *slot(j - 1, v);
+            xe_ = i + 1 < nx ? *slot(j - 1, v + 1) : 0.0;
+            xn_ = jr + 1 < ny ? *slot(j - 1, v + nx) : 0.0;
+          }
+          double a = 0.0;
+          if (jr > 0) a = __dadd_rn(a, __dmul_rn(cS, xs_));
+          if (i > 0) a = __dadd_rn(a, __dmul_rn(cW, xw_));
+          a = __dadd_rn(a, __dmul_rn(cC, xc_));
+          if (i + 1 < nx) a = __dadd_rn(a, __dmul_rn(cE, xe_));
+          if (jr + 1 < ny) a = __dadd_rn(a, __dmul_rn(cN, xn_));
+          if (r >= 1 && r <= rin)
+            sc[(int64_t)(j - 1) * d.P + v] = a;
+          else
+            *slot(j, v) = a;
+          if (v >= 0 && v < cnt) {
+            if (j == 1) d.cand[0][base + v] = xc_;
+            if (!d.build_next) d.cand[j][base + v] = a;
+          }
+        }
+      }
+#pragma unroll
+      for (int t = 0; t < 4; ++t) ra[t] = rb[t], rb[t] = rc[t], rc[t] = rn[t];
+      __syncthreads();
+    }
+  } else
   // level 1 reads seed / nu on the fly (level 0 is stored by the same sweep); levels >= 2 read
   // their source from shared memory inside the slice
   for (int j = 1; j < S; ++j) {
@@ -744,7 +854,7 @@ __global__ void __launch_bounds__(ORTH_NT, 1) k_arn_step(const __grid_constant__
     for (int p = tid; p < cnt; p += ORTH_NT) {
 #pragma unroll
       for (int l = 0; l < S; ++l) {
-        const double lv = V0[l * np + p];
+        const double lv = ldcg(V0 + l * np + p);
 #pragma unroll
         for (int j = 0; j < NC; ++j) acc[l * NC + j] = fma(lv, sc[(int64_t)j * d.P + p], acc[l * NC + j]);
       }
@@ -829,7 +939,7 @@ __global__ void __launch_bounds__(ORTH_NT, 1) k_arn_step(const __grid_constant__
       for (int p = tid; p < cnt; p += ORTH_NT) {
 #pragma unroll
         for (int l = 0; l < S; ++l) {
-          const double lv = V0[l][p];
+          const double lv = ldcg(V0[l] + p);
 #pragma unroll
           for (int j = 0; j < NC; ++j) acc[l * NC + j] = fma(lv, sc[(int64_t)j * d.P + p], acc[l * NC + j]);
         }
@@ -854,6 +964,29 @@ size_t orth_smem(int s, int k, int64_t P) {
   return sizeof(double) * (64 + kStepH + (size_t)orth_prod_cap(k, s)) + sizeof(Gram) * (1 + (size_t)k) +
          sizeof(double) * (ORTH_NT / 32) * (s * s + s) +
          sizeof(double) * (size_t)(s - 1) * (size_t)P;
+}
+
+// ghost-row buffer sizes (doubles) of the row-streamed powers for slices of P points, or
+// false when they do not apply (the 2D constant stencil, s <= 4, nx <= 2 x threads, every
+// non-empty slice at least 4 rows)
+bool stream_powers_ghosts(const DevOp& op, int s, int64_t n, int64_t P, int G, int& g1, int& g2) {
+  g1 = g2 = 0;
+  if (op.kind != kStencilConst || op.dim != 2 || s < 2 || s > 4 || op.nx > 2 * ORTH_NT) return false;
+  const int64_t nx = op.nx;
+  for (int b = 0; b < G; ++b) {
+    const int64_t base = (int64_t)b * P;
+    if (base >= n) break;
+    const int64_t cnt = std::min(P, n - base);
+    const int64_t Rs = (cnt + nx - 1) / nx;
+    if (Rs < 4) return false;
+    for (int j = 1; j <= s - 2; ++j) {
+      const int64_t e = s - 1 - j;
+      const int64_t need = std::max(e * nx, (Rs + e) * nx - cnt);
+      int& g = j == 1 ? g1 : g2;
+      g = (int)std::max<int64_t>(g, need);
+    }
+  }
+  return true;
 }
 
 template <int S>
@@ -1170,6 +1303,11 @@ struct Engine {
     static const bool trace = std::getenv("SKC_TRACE_ORTH") != nullptr;
     if (trace) d.trace = (unsigned long long*)c.workspace("orth_trace", 1024 * sizeof(unsigned long long));
     const int G = c.sm_count;
+    int g1 = 0, g2 = 0;
+    d.spow = c.spow && stream_powers_ghosts(op.d, s, op.n, d.P, G, g1, g2);
+    d.g1 = d.spow ? g1 : 0;
+    d.g2 = d.spow ? g2 : 0;
+    if (d.spow) d.ghosts = (double*)c.workspace("orth_ghosts", sizeof(double) * (size_t)G * (g1 + g2));
     const size_t smem = orth_smem(s, k, d.P);
     // algorithmic bytes: z, Scalar1 products, seed, the powers, round-0 products, pass 0 of the
     // MGS and the cross products (the data-dependent second pass is not counted)

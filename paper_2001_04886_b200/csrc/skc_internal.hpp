@@ -175,6 +175,7 @@ struct Ctx {
   bool orth = true;  // on-chip block orthogonalization when it fits (SKC_ORTH=0 disables)
   bool zfuse = false;   // megakernel: next Scalar1 products in the cross pass (SKC_ZFUSE=1)
   bool persist = true;  // persistent s-Omin for small problems (SKC_PERSIST=0 disables)
+  bool spow = true;     // megakernel: row-streamed candidate powers (SKC_SPOW=0 disables)
   std::map<std::string, KStat> stats;
   struct Pending {
     std::string name;

@@ -184,7 +184,14 @@ SKC_HD void gram_solve(const Gram& g, const double* rhs, double* x) {
 template <int N>
 __device__ __forceinline__ void gram_solve_t(const Gram& g, const double* rhs, double* x) {
   if (N == 1 || g.used_ldlt) {
-    gram_solve(g, rhs, x);
+    // (the generic path through copies: the caller's arrays never have their address taken, so
+    // they stay in registers on the common Cholesky path)
+    double r2[kMaxS], x2[kMaxS];
+#pragma unroll
+    for (int i = 0; i < N; ++i) r2[i] = rhs[i];
+    gram_solve(g, r2, x2);
+#pragma unroll
+    for (int i = 0; i < N; ++i) x[i] = x2[i];
     return;
   }
   double f[N * N];

@@ -400,3 +400,27 @@ def test_c3_full_size_monotone_and_consistent(ctx, port):
     assert rep.iterations == 8 and all(h[t] <= h[t - 1] * (1 + 1e-12) for t in range(1, len(h)))
     r = f - port.stencil_apply(3, st.nx, st.ny, st.nz, st.coef, x)
     assert rel_diff(np.linalg.norm(r), h[-1]) <= 1e-9
+
+
+def _sgmres_fixed(nx, ny, s, m, env, monkeypatch, iters):
+    from paper_2001_04886_b200 import Context, SStepConfig, convection_diffusion, sgmres_solve, splitmix64_uniform
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    ctx = Context(0)
+    st = convection_diffusion(2, nx, 50.0, ny=ny)
+    f = splitmix64_uniform(20010486, st.n)
+    x = np.zeros(st.n)
+    rep = sgmres_solve(ctx.stencil(st), f, x, SStepConfig(s=s, m=m, tol=0.0, max_iterations=iters))
+    return rep, x
+
+
+@pytest.mark.parametrize("s", [2, 3, 4])
+def test_megakernel_streamed_powers_bit_identical(monkeypatch, s):
+    """The row-streamed candidate powers of the block-iteration kernel (slices of >= 4 grid rows:
+    here 256 x 640) give bit-identical candidates to the per-level sweeps, hence bit-identical
+    histories and iterates over two restart cycles."""
+    a, xa = _sgmres_fixed(256, 640, s, 6, {"SKC_SPOW": "1"}, monkeypatch, 2 * 6 * s)
+    b, xb = _sgmres_fixed(256, 640, s, 6, {"SKC_SPOW": "0"}, monkeypatch, 2 * 6 * s)
+    assert a.residual_history == b.residual_history and a.block_rho == b.block_rho
+    assert np.array_equal(xa.view(np.uint64), xb.view(np.uint64))
+    assert a.iterations == 2 * 6 * s
