@@ -368,6 +368,10 @@ __global__ void __launch_bounds__(ORTH_NT, 1) k_arn_step(const __grid_constant__
   const int cnt = rem <= 0 ? 0 : (int)(rem < d.P ? rem : d.P);
   const int G = gridDim.x;
   auto colp = [&](int i, int l) { return d.V + ((int64_t)i * S + l) * d.np + base; };
+  // this slice of candidate column j+1 (j = 0..s-2): the first s-2 in shared memory, the last
+  // in its basis slot in global memory -- the unified L1 keeps 124 KB instead of 60 KB, and
+  // that capacity bounds the loads in flight per SM in every streaming phase
+  auto ccol = [&](int j) -> double* { return j < NC - 1 || NC == 1 ? sc + (int64_t)j * d.P : d.cand[NC] + base; };
 
 
   // Scalar2 for block i from partials (src, srcG): every CTA solves W_i t = V_i^T cand[:,1:]
@@ -420,7 +424,7 @@ __global__ void __launch_bounds__(ORTH_NT, 1) k_arn_step(const __grid_constant__
 #pragma unroll
       for (int u = 0; u < UU; ++u)
 #pragma unroll
-        for (int j = 0; j < NC; ++j) cv[u][j] = has[u] ? sc[(int64_t)j * d.P + p0 + u * ORTH_NT] : 0.0;
+        for (int j = 0; j < NC; ++j) cv[u][j] = has[u] ? ccol(j)[p0 + u * ORTH_NT] : 0.0;
 #pragma unroll
       for (int l = 0; l < S; ++l)
 #pragma unroll
@@ -433,10 +437,10 @@ __global__ void __launch_bounds__(ORTH_NT, 1) k_arn_step(const __grid_constant__
       for (int u = 0; u < UU; ++u) {
         if (!has[u]) continue;
 #pragma unroll
-        for (int j = 0; j < NC; ++j) sc[(int64_t)j * d.P + p0 + u * ORTH_NT] = cv[u][j];
-        if (wb) {
+        for (int j = 0; j < NC; ++j) ccol(j)[p0 + u * ORTH_NT] = cv[u][j];
+        if (wb) {  // (the last column already lives in its basis slot, unless s = 2)
 #pragma unroll
-          for (int j = 0; j < NC; ++j) d.cand[j + 1][base + p0 + u * ORTH_NT] = cv[u][j];
+          for (int j = 0; j < (NC == 1 ? 1 : NC - 1); ++j) d.cand[j + 1][base + p0 + u * ORTH_NT] = cv[u][j];
         }
         if (dots) {
 #pragma unroll
@@ -478,7 +482,7 @@ __global__ void __launch_bounds__(ORTH_NT, 1) k_arn_step(const __grid_constant__
 #pragma unroll
         for (int l = 0; l < S; ++l) a[u][l] = basis && has[u] ? ldcg(Li + l * np + p) : 0.0;
 #pragma unroll
-        for (int j = 1; j < S; ++j) b[u][j] = has[u] ? sc[(int64_t)(j - 1) * d.P + p] : 0.0;
+        for (int j = 1; j < S; ++j) b[u][j] = has[u] ? ccol(j - 1)[p] : 0.0;
       }
 #pragma unroll
       for (int u = 0; u < U; ++u) {
@@ -597,7 +601,7 @@ __global__ void __launch_bounds__(ORTH_NT, 1) k_arn_step(const __grid_constant__
   // z and seed of this slice stay in shared memory (candidate columns 0 and s-2, free until
   // the powers reach them; with s = 2 seed also goes to memory for its neighbours)
   double* zs = sc;
-  double* seeds = S > 2 ? sc + (int64_t)(S - 2) * d.P : nullptr;
+  double* seeds = nullptr;  // (the column that used to hold it is now in global memory)
   if (zready) {
     for (int p = tid; p < cnt; p += ORTH_NT) zs[p] = d.z[base + p];
   } else {
@@ -753,7 +757,7 @@ __global__ void __launch_bounds__(ORTH_NT, 1) k_arn_step(const __grid_constant__
     }
     // level j value at relative index v (slice, or the level's ghost buffer)
     auto slot = [&](int j, int v) -> double* {
-      if (v >= 0 && v < cnt) return sc + (int64_t)(j - 1) * d.P + v;
+      if (v >= 0 && v < cnt) return ccol(j - 1) + v;
       const int e = S - 1 - j;
       return gh[j - 1] + (v < 0 ? v + e * nx : v - cnt);
     };
@@ -795,7 +799,7 @@ __global__ void __launch_bounds__(ORTH_NT, 1) k_arn_step(const __grid_constant__
             xe_ = __dmul_rn(rb[h + 2], inv);
             xn_ = __dmul_rn(rc[h + 1], inv);
           } else if (r >= 1 && r <= rin) {  // every neighbour inside the slice: shared memory
-            const double* Pj = sc + (int64_t)(j - 2) * d.P + v;
+            const double* Pj = ccol(j - 2) + v;
             xs_ = Pj[-nx];
             xw_ = Pj[-1];
             xc_ = Pj[0];
@@ -815,7 +819,7 @@ __global__ void __launch_bounds__(ORTH_NT, 1) k_arn_step(const __grid_constant__
           if (i + 1 < nx) a = __dadd_rn(a, __dmul_rn(cE, xe_));
           if (jr + 1 < ny) a = __dadd_rn(a, __dmul_rn(cN, xn_));
           if (r >= 1 && r <= rin)
-            sc[(int64_t)(j - 1) * d.P + v] = a;
+            ccol(j - 1)[v] = a;
           else
             *slot(j, v) = a;
           if (v >= 0 && v < cnt) {
@@ -835,10 +839,10 @@ __global__ void __launch_bounds__(ORTH_NT, 1) k_arn_step(const __grid_constant__
     if (j > 1) grid.sync();
     orth_mark(d, 44 + 2 * j - 1);
     const bool to_mem = j + 1 < S || !d.build_next;
-    apply_slice(j == 1 ? d.seed : d.cand[j - 1], j >= 2 ? sc + (int64_t)(j - 2) * d.P : seeds, j == 1 ? inv : 0.0,
+    apply_slice(j == 1 ? d.seed : d.cand[j - 1], j >= 2 ? ccol(j - 2) : seeds, j == 1 ? inv : 0.0,
                 [&](int p, double v, double xc) {
                   if (j == 1) d.cand[0][base + p] = xc;
-                  sc[(int64_t)(j - 1) * d.P + p] = v;
+                  ccol(j - 1)[p] = v;
                   if (to_mem) d.cand[j][base + p] = v;
                 });
     orth_mark(d, 44 + 2 * j);
@@ -856,7 +860,7 @@ __global__ void __launch_bounds__(ORTH_NT, 1) k_arn_step(const __grid_constant__
       for (int l = 0; l < S; ++l) {
         const double lv = ldcg(V0 + l * np + p);
 #pragma unroll
-        for (int j = 0; j < NC; ++j) acc[l * NC + j] = fma(lv, sc[(int64_t)j * d.P + p], acc[l * NC + j]);
+        for (int j = 0; j < NC; ++j) acc[l * NC + j] = fma(lv, ccol(j)[p], acc[l * NC + j]);
       }
     }
     orth_store(acc, red, d.partials, d.dr0);
@@ -877,7 +881,7 @@ __global__ void __launch_bounds__(ORTH_NT, 1) k_arn_step(const __grid_constant__
   if (d.zfuse) {
     double zz[1] = {0.0};
     double* zg = d.z + base;
-    apply_slice(d.cand[S - 1], sc + (int64_t)(S - 2) * d.P, 0.0, [&](int p, double v, double) {
+    apply_slice(d.cand[S - 1], nullptr, 0.0, [&](int p, double v, double) {
       zg[p] = v;
       zz[0] = fma(v, v, zz[0]);
     });
@@ -941,7 +945,7 @@ __global__ void __launch_bounds__(ORTH_NT, 1) k_arn_step(const __grid_constant__
         for (int l = 0; l < S; ++l) {
           const double lv = ldcg(V0[l] + p);
 #pragma unroll
-          for (int j = 0; j < NC; ++j) acc[l * NC + j] = fma(lv, sc[(int64_t)j * d.P + p], acc[l * NC + j]);
+          for (int j = 0; j < NC; ++j) acc[l * NC + j] = fma(lv, ccol(j)[p], acc[l * NC + j]);
         }
       }
       orth_store(acc, red, d.partials, d.dr0);
@@ -963,7 +967,7 @@ __global__ void __launch_bounds__(ORTH_NT, 1) k_arn_step(const __grid_constant__
 size_t orth_smem(int s, int k, int64_t P) {
   return sizeof(double) * (64 + kStepH + (size_t)orth_prod_cap(k, s)) + sizeof(Gram) * (1 + (size_t)k) +
          sizeof(double) * (ORTH_NT / 32) * (s * s + s) +
-         sizeof(double) * (size_t)(s - 1) * (size_t)P;
+         sizeof(double) * (size_t)(s > 2 ? s - 2 : 1) * (size_t)P;  // (s = 2: its one column stays on chip)
 }
 
 // ghost-row buffer sizes (doubles) of the row-streamed powers for slices of P points, or
