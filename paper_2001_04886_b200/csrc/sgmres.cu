@@ -247,7 +247,14 @@ __global__ void k_arn_check(ArnState* st, const Gram* grams, int k, double* rec,
 constexpr int ORTH_NT = 512;
 // points per thread per iteration, all their loads issued first (Scalar1 products, seed)
 constexpr int ORTH_UC = 4;
-constexpr size_t kOrthSmemCap = 220 * 1024;  // <= the 226 KB dynamic limit set at launch
+constexpr size_t kOrthSmemCap = 220 * 1024;
+// candidate columns kept in shared memory (the rest in their basis slots): shared memory is
+// carved out of the unified L1, whose remaining capacity bounds the loads in flight per SM
+// (C2, s = 4: 3 columns on chip 3697 s-steps/s, 2 columns 3750, 1 column 3635)
+#ifndef SKC_ORTH_SMEM_COLS
+#define SKC_ORTH_SMEM_COLS 2
+#endif
+constexpr int kOrthSmemCols = SKC_ORTH_SMEM_COLS;  // <= the 226 KB dynamic limit set at launch
 // reduced-product capacity: the cross test needs (k+1) s^2, a round s(s-1); even count keeps
 // the Gram copy 16-byte aligned
 __host__ __device__ inline int orth_prod_cap(int k, int s) { return ((k + 1) * s * s + 1) & ~1; }
@@ -368,10 +375,10 @@ __global__ void __launch_bounds__(ORTH_NT, 1) k_arn_step(const __grid_constant__
   const int cnt = rem <= 0 ? 0 : (int)(rem < d.P ? rem : d.P);
   const int G = gridDim.x;
   auto colp = [&](int i, int l) { return d.V + ((int64_t)i * S + l) * d.np + base; };
-  // this slice of candidate column j+1 (j = 0..s-2): the first s-2 in shared memory, the last
-  // in its basis slot in global memory -- the unified L1 keeps 124 KB instead of 60 KB, and
-  // that capacity bounds the loads in flight per SM in every streaming phase
-  auto ccol = [&](int j) -> double* { return j < NC - 1 || NC == 1 ? sc + (int64_t)j * d.P : d.cand[NC] + base; };
+  // this slice of candidate column j+1 (j = 0..s-2): the first kOrthSmemCols in shared memory,
+  // the rest in their basis slots in global memory (C2: 124 KB of unified L1 left instead of
+  // 60 KB; that capacity bounds the loads in flight per SM in every streaming phase)
+  auto ccol = [&](int j) -> double* { return j < kOrthSmemCols ? sc + (int64_t)j * d.P : d.cand[j + 1] + base; };
 
 
   // Scalar2 for block i from partials (src, srcG): every CTA solves W_i t = V_i^T cand[:,1:]
@@ -438,9 +445,9 @@ __global__ void __launch_bounds__(ORTH_NT, 1) k_arn_step(const __grid_constant__
         if (!has[u]) continue;
 #pragma unroll
         for (int j = 0; j < NC; ++j) ccol(j)[p0 + u * ORTH_NT] = cv[u][j];
-        if (wb) {  // (the last column already lives in its basis slot, unless s = 2)
+        if (wb) {  // (the columns past kOrthSmemCols already live in their basis slots)
 #pragma unroll
-          for (int j = 0; j < (NC == 1 ? 1 : NC - 1); ++j) d.cand[j + 1][base + p0 + u * ORTH_NT] = cv[u][j];
+          for (int j = 0; j < (NC < kOrthSmemCols ? NC : kOrthSmemCols); ++j) d.cand[j + 1][base + p0 + u * ORTH_NT] = cv[u][j];
         }
         if (dots) {
 #pragma unroll
@@ -839,7 +846,7 @@ __global__ void __launch_bounds__(ORTH_NT, 1) k_arn_step(const __grid_constant__
     if (j > 1) grid.sync();
     orth_mark(d, 44 + 2 * j - 1);
     const bool to_mem = j + 1 < S || !d.build_next;
-    apply_slice(j == 1 ? d.seed : d.cand[j - 1], j >= 2 ? ccol(j - 2) : seeds, j == 1 ? inv : 0.0,
+    apply_slice(j == 1 ? d.seed : d.cand[j - 1], j >= 2 && j - 2 < kOrthSmemCols ? ccol(j - 2) : seeds, j == 1 ? inv : 0.0,
                 [&](int p, double v, double xc) {
                   if (j == 1) d.cand[0][base + p] = xc;
                   ccol(j - 1)[p] = v;
@@ -967,7 +974,7 @@ __global__ void __launch_bounds__(ORTH_NT, 1) k_arn_step(const __grid_constant__
 size_t orth_smem(int s, int k, int64_t P) {
   return sizeof(double) * (64 + kStepH + (size_t)orth_prod_cap(k, s)) + sizeof(Gram) * (1 + (size_t)k) +
          sizeof(double) * (ORTH_NT / 32) * (s * s + s) +
-         sizeof(double) * (size_t)(s > 2 ? s - 2 : 1) * (size_t)P;  // (s = 2: its one column stays on chip)
+         sizeof(double) * (size_t)std::min(s - 1, kOrthSmemCols) * (size_t)P;
 }
 
 // ghost-row buffer sizes (doubles) of the row-streamed powers for slices of P points, or
