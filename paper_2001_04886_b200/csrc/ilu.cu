@@ -32,6 +32,40 @@ namespace {
 
 constexpr int TR_NT = 512;
 
+// One CTA walks every level with a block barrier between them (no grid barrier): used when the
+// widest level fits the CTA a few times over, e.g. the anti-diagonals of a 2D grid, where the
+// solve is a chain of nx + ny - 1 short levels and the cost is the per-level latency
+constexpr int TR1_NT = 1024;
+template <bool LOWER>
+__global__ void __launch_bounds__(TR1_NT) k_trsv1(const int64_t* __restrict__ rp, const int32_t* __restrict__ ci,
+                                                  const double* __restrict__ v, const int32_t* __restrict__ perm,
+                                                  const int64_t* __restrict__ lev, int nlev, const double* r, double* z,
+                                                  const int* halt, const int* cond) {
+  SKC_PDL_ENTRY();
+  if (skip_launch(halt, cond)) return;
+  for (int L = 0; L < nlev; ++L) {
+    const int64_t e = lev[L + 1];
+    for (int64_t q = lev[L] + threadIdx.x; q < e; q += TR1_NT) {
+      const int i = perm[q];
+      if (LOWER) {
+        double acc = r[i];
+        for (int64_t p = rp[i]; p < rp[i + 1]; ++p) acc = __dsub_rn(acc, __dmul_rn(v[p], z[ci[p]]));
+        z[i] = acc;
+      } else {
+        double acc = z[i], dia = 0.0;
+        for (int64_t p = rp[i]; p < rp[i + 1]; ++p) {
+          if (ci[p] == i)
+            dia = v[p];
+          else
+            acc = __dsub_rn(acc, __dmul_rn(v[p], z[ci[p]]));
+        }
+        z[i] = __ddiv_rn(acc, dia);
+      }
+    }
+    __syncthreads();
+  }
+}
+
 template <bool LOWER>
 __global__ void __launch_bounds__(TR_NT) k_trsv(const int64_t* __restrict__ rp, const int32_t* __restrict__ ci,
                                                 const double* __restrict__ v, const int32_t* __restrict__ perm,
@@ -78,6 +112,14 @@ void launch_trsv(Ctx& c, const IluData& d, const double* r, double* z, const int
   cfg.numAttrs = 1;
   const double bytes = LOWER ? 8.0 * (2.0 * d.n) + 12.0 * d.nnz_l + 12.0 * d.n : 8.0 * (2.0 * d.n) + 12.0 * d.nnz_u + 12.0 * d.n;
   Launch lh(c, LOWER ? "ilu_lower" : "ilu_upper", bytes);
+  if ((LOWER ? d.maxw_l : d.maxw_u) <= 8 * TR1_NT) {
+    if (LOWER)
+      launch_k(c, k_trsv1<true>, 1, TR1_NT, 0, d.lrp, d.lci, d.lv, d.lperm, d.llev, d.nlev_l, r, z, halt, cond);
+    else
+      launch_k(c, k_trsv1<false>, 1, TR1_NT, 0, d.urp, d.uci, d.uv, d.uperm, d.ulev, d.nlev_u, (const double*)nullptr, z,
+               halt, cond);
+    return;
+  }
   if (LOWER)
     CK(cudaLaunchKernelEx(&cfg, k_trsv<true>, d.lrp, d.lci, d.lv, d.lperm, d.llev, d.nlev_l, r, z, halt, cond));
   else
@@ -187,6 +229,8 @@ void build_ilu0_op(Ctx& c, Op& op, int64_t n, const uint64_t* offs, const uint64
   d.nnz_u = (int64_t)uv.size();
   d.nlev_l = (int)llev.size() - 1;
   d.nlev_u = (int)ulev.size() - 1;
+  for (size_t q = 0; q + 1 < llev.size(); ++q) d.maxw_l = std::max(d.maxw_l, llev[q + 1] - llev[q]);
+  for (size_t q = 0; q + 1 < ulev.size(); ++q) d.maxw_u = std::max(d.maxw_u, ulev[q + 1] - ulev[q]);
   d.lrp = upload(op, lrp);
   d.lci = upload(op, lci);
   d.lv = upload(op, lv);

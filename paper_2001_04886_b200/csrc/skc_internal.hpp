@@ -84,6 +84,7 @@ struct IluData {
   const int64_t *llev = nullptr, *ulev = nullptr;    // level offsets into lperm / uperm
   int nlev_l = 0, nlev_u = 0;
   int64_t nnz_l = 0, nnz_u = 0;
+  int64_t maxw_l = 0, maxw_u = 0;  // widest level
 };
 
 // ---------------------------------------------------------------- streaming geometry
