@@ -99,6 +99,93 @@ __global__ void __launch_bounds__(TR_NT) k_trsv(const int64_t* __restrict__ rp, 
   }
 }
 
+// Strip wavefront for a 2D 5-point grid in natural order (L: S and W neighbours; U: E and N).
+// One warp per 32-column strip; lane k takes column k of the strip (mirrored for U) and, at
+// step t, row t - k (descending rows for U): its in-row neighbour (W / E) is the value lane
+// k-1 produced one step earlier (a shuffle), its cross-row neighbour (S / N) its own previous
+// value, so the 32 lanes advance along an anti-diagonal with no barrier.  Lane 0's in-row
+// neighbour belongs to the adjacent strip (left for L, right for U): that strip publishes
+// rows-done counters (release, every 32 rows) and this one fetches the neighbour column 32
+// rows at a time (acquire).  The strip's own operands are prefetched 8 steps ahead.  Every
+// row is the reference's sequential evaluation (ilu0_apply: acc -= l * z in column order,
+// then / diag for U), so z is bit-identical to the level-scheduled solve.
+constexpr int SW_D = 8;
+template <bool LOWER>
+__global__ void __launch_bounds__(32) k_trsv_strip(const double* __restrict__ a1, const double* __restrict__ a2,
+                                                   const double* __restrict__ ac, const uint8_t* __restrict__ msk,
+                                                   int nx, int ny, const double* r, double* z, int* progress,
+                                                   const int* halt, const int* cond) {
+  SKC_PDL_ENTRY();
+  if (skip_launch(halt, cond)) return;
+  const int k = threadIdx.x, sx = blockIdx.x, nstrip = gridDim.x;
+  const int x = LOWER ? 32 * sx + k : 32 * sx + 31 - k;
+  const bool col_ok = x < nx;
+  const int nb = LOWER ? sx - 1 : sx + 1;  // the strip owning lane 0's in-row neighbour
+  const bool has_nb = nb >= 0 && nb < nstrip;
+  const int xn = LOWER ? 32 * sx - 1 : 32 * sx + 32;  // lane 0's in-row neighbour column
+  // the lane that owns the column the next strip needs (x = 32 sx + 31 for L, 32 sx for U)
+  const bool publisher = k == 31;
+  auto row_of = [&](int t) { return LOWER ? t - k : ny - 1 - (t - k); };
+  double zlast = 0.0, wchunk = 0.0;
+  // operand ring: (in-row coefficient, cross-row coefficient, diagonal / rhs, mask)
+  double q1[SW_D], q2[SW_D], qc[SW_D], qz[SW_D];
+  uint8_t qm[SW_D];
+  auto fetch = [&](int t, int u) {
+    const int y = row_of(t);
+    const bool ok = col_ok && t - k >= 0 && t - k < ny;
+    const int64_t p = (int64_t)(ok ? y : 0) * nx + (ok ? x : 0);
+    q1[u] = ok ? a1[p] : 0.0;
+    q2[u] = ok ? a2[p] : 0.0;
+    qc[u] = ok ? (LOWER ? r[p] : ac[p]) : 0.0;
+    qz[u] = !LOWER && ok ? z[p] : 0.0;  // (U: the forward solve's value, rewritten only by this lane)
+    qm[u] = ok ? msk[p] : 0;
+  };
+#pragma unroll
+  for (int u = 0; u < SW_D; ++u) fetch(u, u);
+  const int T = ny + 31;
+  for (int t0 = 0; t0 < T; t0 += SW_D) {
+#pragma unroll
+    for (int u = 0; u < SW_D; ++u) {
+      const int t = t0 + u;
+      if (t >= T) break;
+      if ((t & 31) == 0 && has_nb) {  // lane 0's in-row neighbours for rows t .. t+31
+        const int need = min(ny, t + 32);
+        int got;
+        do {
+          asm volatile("ld.acquire.gpu.b32 %0, [%1];" : "=r"(got) : "l"(progress + nb) : "memory");
+        } while (got < need);
+        const int yy = LOWER ? t + k : ny - 1 - (t + k);
+        wchunk = t + k < ny ? z[(int64_t)yy * nx + xn] : 0.0;
+      }
+      const double from_prev_lane = __shfl_up_sync(0xffffffffu, zlast, 1);
+      const double nbv = __shfl_sync(0xffffffffu, wchunk, t & 31);
+      const double in_row = k == 0 ? nbv : from_prev_lane;
+      const int y = row_of(t);
+      const bool active = col_ok && t - k >= 0 && t - k < ny;
+      if (active) {
+        const int64_t p = (int64_t)y * nx + x;
+        double acc;
+        if (LOWER) {  // acc = r - l_S z_S - l_W z_W  (columns p - nx, p - 1)
+          acc = qc[u];
+          if (qm[u] & 1) acc = __dsub_rn(acc, __dmul_rn(q2[u], zlast));
+          if (qm[u] & 2) acc = __dsub_rn(acc, __dmul_rn(q1[u], in_row));
+        } else {      // acc = (z - u_E z_E - u_N z_N) / u_C  (columns p + 1, p + nx)
+          acc = qz[u];
+          if (qm[u] & 1) acc = __dsub_rn(acc, __dmul_rn(q1[u], in_row));
+          if (qm[u] & 2) acc = __dsub_rn(acc, __dmul_rn(q2[u], zlast));
+          acc = __ddiv_rn(acc, qc[u]);
+        }
+        z[p] = acc;
+        zlast = acc;
+        const int done = t - k + 1;  // rows of this column finished
+        if (publisher && (done % 32 == 0 || done == ny))
+          asm volatile("st.release.gpu.b32 [%0], %1;" ::"l"(progress + sx), "r"(done) : "memory");
+      }
+      fetch(t + SW_D, u);
+    }
+  }
+}
+
 template <bool LOWER>
 void launch_trsv(Ctx& c, const IluData& d, const double* r, double* z, const int* halt, const int* cond) {
   cudaLaunchConfig_t cfg{};
@@ -112,6 +199,27 @@ void launch_trsv(Ctx& c, const IluData& d, const double* r, double* z, const int
   cfg.numAttrs = 1;
   const double bytes = LOWER ? 8.0 * (2.0 * d.n) + 12.0 * d.nnz_l + 12.0 * d.n : 8.0 * (2.0 * d.n) + 12.0 * d.nnz_u + 12.0 * d.n;
   Launch lh(c, LOWER ? "ilu_lower" : "ilu_upper", bytes);
+  if (d.gnx > 0 && c.ilu_strips) {
+    const int ns = (int)((d.gnx + 31) / 32);
+    int* prog = d.progress + (LOWER ? 0 : ns);
+    CK(cudaMemsetAsync(prog, 0, sizeof(int) * ns, c.stream));
+    cudaLaunchConfig_t sc{};
+    sc.gridDim = ns;
+    sc.blockDim = 32;
+    sc.stream = c.stream;
+    cudaLaunchAttribute sa[1];
+    sa[0].id = cudaLaunchAttributeCooperative;  // (all strips resident: they wait on each other)
+    sa[0].val.cooperative = 1;
+    sc.attrs = sa;
+    sc.numAttrs = 1;
+    if (LOWER)
+      CK(cudaLaunchKernelEx(&sc, k_trsv_strip<true>, d.lW, d.lS, (const double*)nullptr, d.lm, (int)d.gnx, (int)d.gny,
+                            r, z, prog, halt, cond));
+    else
+      CK(cudaLaunchKernelEx(&sc, k_trsv_strip<false>, d.uE, d.uN, d.uC, d.um, (int)d.gnx, (int)d.gny,
+                            (const double*)nullptr, z, prog, halt, cond));
+    return;
+  }
   if ((LOWER ? d.maxw_l : d.maxw_u) <= 8 * TR1_NT) {
     if (LOWER)
       launch_k(c, k_trsv1<true>, 1, TR1_NT, 0, d.lrp, d.lci, d.lv, d.lperm, d.llev, d.nlev_l, r, z, halt, cond);
@@ -229,6 +337,36 @@ void build_ilu0_op(Ctx& c, Op& op, int64_t n, const uint64_t* offs, const uint64
   d.nnz_u = (int64_t)uv.size();
   d.nlev_l = (int)llev.size() - 1;
   d.nlev_u = (int)ulev.size() - 1;
+  // a 5-point grid (the base operator recognized the pattern): factors by neighbour
+  if (d.base.d.kind == kStencilDia && d.base.d.dim == 2 && n <= 0x7fffffff) {
+    const int64_t nx = d.base.d.nx;
+    std::vector<double> lS(n, 0.0), lW(n, 0.0), uC(n, 0.0), uE(n, 0.0), uN(n, 0.0);
+    std::vector<uint8_t> lm(n, 0), um(n, 0);
+    bool ok = true;
+    for (int64_t i = 0; i < n && ok; ++i)
+      for (uint64_t p = offs[i]; p < offs[i + 1]; ++p) {
+        const int64_t off = (int64_t)cols[p] - i;
+        if (off == -nx) lS[i] = lu[p], lm[i] |= 1;
+        else if (off == -1) lW[i] = lu[p], lm[i] |= 2;
+        else if (off == 0) uC[i] = lu[p];
+        else if (off == 1) uE[i] = lu[p], um[i] |= 1;
+        else if (off == nx) uN[i] = lu[p], um[i] |= 2;
+        else ok = false;
+      }
+    if (ok) {
+      d.gnx = nx;
+      d.gny = d.base.d.ny;
+      d.lS = upload(op, lS);
+      d.lW = upload(op, lW);
+      d.uC = upload(op, uC);
+      d.uE = upload(op, uE);
+      d.uN = upload(op, uN);
+      d.lm = upload(op, lm);
+      d.um = upload(op, um);
+      std::vector<int> prog(2 * ((nx + 31) / 32), 0);
+      d.progress = const_cast<int*>(upload(op, prog));
+    }
+  }
   for (size_t q = 0; q + 1 < llev.size(); ++q) d.maxw_l = std::max(d.maxw_l, llev[q + 1] - llev[q]);
   for (size_t q = 0; q + 1 < ulev.size(); ++q) d.maxw_u = std::max(d.maxw_u, ulev[q + 1] - ulev[q]);
   d.lrp = upload(op, lrp);

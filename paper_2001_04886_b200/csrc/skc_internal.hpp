@@ -85,6 +85,12 @@ struct IluData {
   int nlev_l = 0, nlev_u = 0;
   int64_t nnz_l = 0, nnz_u = 0;
   int64_t maxw_l = 0, maxw_u = 0;  // widest level
+  // 2D 5-point grids in natural order: the factors by neighbour (L: S, W; U: C, E, N) with a
+  // presence mask per row (the pattern, not the values), for the strip-wavefront solves
+  int64_t gnx = 0, gny = 0;         // 0: not a 5-point grid
+  const double *lS = nullptr, *lW = nullptr, *uC = nullptr, *uE = nullptr, *uN = nullptr;
+  const uint8_t *lm = nullptr, *um = nullptr;
+  int* progress = nullptr;          // per-strip rows-done counters (2 x strips)
 };
 
 // ---------------------------------------------------------------- streaming geometry
@@ -177,6 +183,7 @@ struct Ctx {
   bool zfuse = false;   // megakernel: next Scalar1 products in the cross pass (SKC_ZFUSE=1)
   bool persist = true;  // persistent s-Omin for small problems (SKC_PERSIST=0 disables)
   bool spow = true;     // megakernel: row-streamed candidate powers (SKC_SPOW=0 disables)
+  bool ilu_strips = true;  // ILU(0) on 2D grids: strip-wavefront solves (SKC_ILU_STRIPS=0 disables)
   std::map<std::string, KStat> stats;
   struct Pending {
     std::string name;

@@ -118,3 +118,16 @@ def test_solve_linear_matches_reference(ctx, name):
         assert rel_vec(x, arr["x"]) <= 1e-8
     # the appended true residual of the GPU iterate is below the driver's threshold
     assert rep.residual_history[-1] <= meta["cfg"]["tol"]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", ILU_CASES)
+def test_ilu0_level_schedule_path_bit_exact(name, monkeypatch):
+    """The level-scheduled triangular solves (general patterns; SKC_ILU_STRIPS=0 forces them on
+    the 5-point grids that otherwise take the strip wavefront) are bit-exact too."""
+    from paper_2001_04886_b200 import Context
+    monkeypatch.setenv("SKC_ILU_STRIPS", "0")
+    meta, arr = case(name)
+    op = Context(0).ilu0(arr["offs"], arr["cols"], arr["vals"])
+    assert np.array_equal(_bits(op.ilu0_solve(arr["r"])), _bits(arr["z"]))
+    assert np.array_equal(_bits(op.apply(arr["r"])), _bits(arr["az"]))

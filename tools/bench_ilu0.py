@@ -55,7 +55,16 @@ def main():
         for _ in range(reps):
             op.ilu0_solve(x)
         t_solve = (time.perf_counter() - t0) / reps
-        line = f"nx={nx}: factor(host) {t_fac * 1e3:.1f} ms, A(LU)^-1 apply {t_apply * 1e3:.3f} ms, (LU)^-1 {t_solve * 1e3:.3f} ms (host round trip incl.)"
+        ctx.reset_stats()
+        ctx.set_profiling(True)
+        for _ in range(reps):
+            op.ilu0_solve(x)
+        torch.cuda.synchronize()
+        ks = ctx.kernel_stats()
+        ctx.set_profiling(False)
+        dev = sum(v["ms"] for k, v in ks.items() if k.startswith("ilu_")) / reps
+        line = (f"nx={nx}: factor(host) {t_fac * 1e3:.1f} ms, A(LU)^-1 apply {t_apply * 1e3:.3f} ms, (LU)^-1 "
+                f"{t_solve * 1e3:.3f} ms (host round trip incl.), device {dev * 1e3:.1f} us per (LU)^-1")
         for method, cfg in (("somin", dict(s=2, k=2)), ("sgmres", dict(s=2, m=5))):
             c = SStepConfig(tol=1e-8 * float(np.linalg.norm(f)), max_iterations=20000, **cfg)
             t0 = time.perf_counter()
