@@ -254,7 +254,10 @@ constexpr size_t kOrthSmemCap = 220 * 1024;
 #ifndef SKC_ORTH_SMEM_COLS
 #define SKC_ORTH_SMEM_COLS 2
 #endif
-constexpr int kOrthSmemCols = SKC_ORTH_SMEM_COLS;  // <= the 226 KB dynamic limit set at launch
+constexpr int kOrthSmemCols = SKC_ORTH_SMEM_COLS;
+#ifndef SKC_UU4
+#define SKC_UU4 3
+#endif  // <= the 226 KB dynamic limit set at launch
 // reduced-product capacity: the cross test needs (k+1) s^2, a round s(s-1); even count keeps
 // the Gram copy 16-byte aligned
 __host__ __device__ inline int orth_prod_cap(int k, int s) { return ((k + 1) * s * s + 1) & ~1; }
@@ -414,7 +417,7 @@ __global__ void __launch_bounds__(ORTH_NT, 1) k_arn_step(const __grid_constant__
     double acc[S * NC];
 #pragma unroll
     for (int q = 0; q < S * NC; ++q) acc[q] = 0.0;
-    constexpr int UU = S <= 3 ? 4 : S == 4 ? 3 : S <= 6 ? 2 : 1;
+    constexpr int UU = S <= 3 ? 4 : S == 4 ? SKC_UU4 : S <= 6 ? 2 : 1;
     for (int p0 = tid; p0 < cnt; p0 += UU * ORTH_NT) {
       bool has[UU];
       double v[UU][S], w[UU][S], cv[UU][NC];
