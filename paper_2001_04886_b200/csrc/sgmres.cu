@@ -1257,6 +1257,10 @@ struct Engine {
   ArnState* st;
   const int* halt;
   bool zfused = false;  // the next block iteration's z and Scalar1 products are already computed
+  // across GPUs the reorthogonalization decision is read back after the test (one stream sync
+  // per block iteration), so a skipped second pass spends no collective and no halo exchange:
+  // every rank reads the same decision (identical allgathered scalars)
+  int host_reorth = -1;  // -1 unknown, else the last decision
   // the restart cycle as a CUDA graph: its launch sequence and arguments are identical for
   // every cycle of a solve (all control flow is device-side), so after one direct enqueue
   // (which also performs first-use allocations and kernel attribute setup) it is captured
@@ -1480,6 +1484,7 @@ struct Engine {
   // SStepArnoldi ctor on device vector v (use_rn: its norm is st->rn)
   void ctor(const double* v, bool use_rn) {
     zfused = false;
+    host_reorth = -1;
     CK(cudaMemsetAsync(rec, 0, (size_t)(m + 1) * rl.size() * sizeof(double), c.stream));
     if (!use_rn) launch_gram_list(c, g, {v}, {v}, partials, dl.RR(), nullptr, nullptr, "gram");
     const int Gc = use_rn ? g.G : c.reduce_point(partials, g.G, dl.RR(), 1);
@@ -1503,9 +1508,10 @@ struct Engine {
     // into its cross-product pass (zfused) they are already in place, unless that iteration's
     // reorthogonalization pass changed the block: then (device flag) they are recomputed.
     const int* zcond = zfused ? &st->reorth : nullptr;
+    const bool zskip = zfused && host_reorth == 0;  // (known on the host: nothing to redo)
     zfused = false;
-    apply(col(k - 1, s - 1), z, zcond);
-    {
+    if (!zskip) {
+      apply(col(k - 1, s - 1), z, zcond);
       std::vector<const double*> L;
       for (int i = 0; i < k; ++i)
         for (int l = 0; l < s; ++l) L.push_back(col(i, l));
@@ -1533,8 +1539,16 @@ struct Engine {
       return;
     }
     double* tk = rk + rl.t();
+    bool wb_needed = true;  // the reorthogonalized W region must be made global for the push
     if (s > 1) {
       for (int pass = 0; pass < 2; ++pass) {
+        if (pass == 1 && c.world() > 1) {
+          host_reorth = read_state().reorth;
+          if (!host_reorth) {
+            wb_needed = false;
+            break;
+          }
+        }
         const int* cond = pass ? &st->reorth : nullptr;
         std::vector<const double*> Cr;
         for (int jc = 1; jc < s; ++jc) Cr.push_back(col(cb, jc));
@@ -1596,7 +1610,8 @@ struct Engine {
     // the push reads W from the reorthogonalized region when the device flag says so: make
     // both regions global (the unused one is stale but harmless)
     // (for s > 1 the dWa region was already made global together with the cross products)
-    const int Gw = s > 1 ? c.reduce_point(partials, g.G, dl.Wb(), s * s) : c.reduce_point(partials, g.G, dWa, s * s);
+    const int Gw = s > 1 ? (wb_needed ? c.reduce_point(partials, g.G, dl.Wb(), s * s) : c.world())
+                         : c.reduce_point(partials, g.G, dWa, s * s);
     launch_k(c, k_arn_push, 1, 256, 0, st, grams, cb, rk, partials, Gw, dWa, dl.Wb(), s);
     ++c.launches;
     CK(cudaGetLastError());

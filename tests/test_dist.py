@@ -74,6 +74,7 @@ def _cases():
         "somin2d": (st2, f2, None, "somin", dict(s=4, k=2, tol=t2, max_iterations=200)),
         "sgmres2d": (st2, f2, None, "sgmres", dict(s=2, m=5, tol=t2)),
         "somin3d_vark": (st3, f3, k3, "somin", dict(s=4, k=2, tol=0.0, max_iterations=20)),
+        "sgmres2d_s4m10": (st2, f2, None, "sgmres", dict(s=4, m=10, tol=t2)),
     }
 
 
@@ -125,3 +126,19 @@ def test_nccl_backend_single_rank():
     x1 = np.zeros(st.n)
     rep = somin_solve(ctx.stencil(st), f, x1, SStepConfig(**cfg))
     assert hist == rep.residual_history and np.array_equal(x, x1)
+
+
+@pytest.mark.gpu
+def test_slab_sgmres_with_reorthogonalization_passes():
+    """C2-shaped s-GMRES (s = 4, m = 10: the reorthogonalization test fires in later block
+    iterations) across 2 slab ranks: the second pass is enqueued only when the read-back
+    decision says so, identically on every rank; the solve converges to the true tolerance."""
+    from oracle import Oracle
+    case = _cases()["sgmres2d_s4m10"]
+    st, f, kcell, method, cfg = case
+    out = _spawn(dist_workers.gpu_slab_worker, 2, case)
+    x = np.concatenate([o[3] for o in out])
+    assert all(o[4] == out[0][4] and o[7] == out[0][7] for o in out)
+    assert out[0][9]
+    a = Oracle("port").stencil_csr(st.dim, st.nx, st.ny, st.nz, st.coef)
+    assert np.linalg.norm(f - Oracle("port").spmv(a, x)) <= cfg["tol"] * (1 + 1e-6)
