@@ -109,7 +109,10 @@ __global__ void __launch_bounds__(TR_NT) k_trsv(const int64_t* __restrict__ rp, 
 // rows at a time (acquire).  The strip's own operands are prefetched 8 steps ahead.  Every
 // row is the reference's sequential evaluation (ilu0_apply: acc -= l * z in column order,
 // then / diag for U), so z is bit-identical to the level-scheduled solve.
-constexpr int SW_D = 8;
+#ifndef SKC_SW_D
+#define SKC_SW_D 16
+#endif
+constexpr int SW_D = SKC_SW_D;
 template <bool LOWER>
 __global__ void __launch_bounds__(32) k_trsv_strip(const double* __restrict__ a1, const double* __restrict__ a2,
                                                    const double* __restrict__ ac, const uint8_t* __restrict__ msk,
