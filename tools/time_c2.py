@@ -43,7 +43,7 @@ def main():
             best = dt if best is None else min(best, dt)
         print(f"rep {r}: {rep.iterations} inner steps ({ss:.0f} s-steps), cycles {rep.cycles}, "
               f"{dt * 1e3:.1f} ms, {ss / dt:.0f} s-steps/s, converged {rep.converged}")
-    print(f"BEST {ss / best:.1f} s-steps/s  env PF={os.environ.get('SKC_PF', '-')} "
+    print(f"BEST {ss / best:.1f} s-steps/s  env SPOW={os.environ.get('SKC_SPOW', '-')} "
           f"ZFUSE={os.environ.get('SKC_ZFUSE', '-')} ORTH={os.environ.get('SKC_ORTH', '-')}")
 
 
