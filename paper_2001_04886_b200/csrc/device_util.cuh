@@ -29,6 +29,42 @@ __device__ __forceinline__ double warp_sum(double v) {
   return v;
 }
 
+// Warp sums of K values at once: out[q] = sum over the 32 lanes of v[q] (q < K), written by
+// one lane per value.  Recursive halving: at each of log2(P) exchange steps (P = K rounded up
+// to a power of two, at most 32 per chunk) a lane keeps one half of its values and adds the
+// partner's copy of that half, so the exchanges total ~P instead of 5K (one shuffle per value
+// per level for a butterfly of each value); the remaining lane bits are then folded by plain
+// butterflies.  Fixed order: deterministic.
+template <int K>
+__device__ __forceinline__ void warp_sums(const double (&acc)[K], double* out) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int c0 = 0; c0 < K; c0 += 32) {
+    constexpr int CH = K < 32 ? K : 32;
+    constexpr int P = CH <= 1 ? 1 : CH <= 2 ? 2 : CH <= 4 ? 4 : CH <= 8 ? 8 : CH <= 16 ? 16 : 32;
+    constexpr int M = P == 1 ? 0 : P == 2 ? 1 : P == 4 ? 2 : P == 8 ? 3 : P == 16 ? 4 : 5;
+    double v[P];
+#pragma unroll
+    for (int q = 0; q < P; ++q) v[q] = c0 + q < K ? acc[c0 + q < K ? c0 + q : 0] : 0.0;
+#pragma unroll
+    for (int t = 0; t < M; ++t) {
+      const int o = 16 >> t, h = P >> (t + 1);
+      const bool upper = (lane & o) != 0;
+#pragma unroll
+      for (int q = 0; q < h; ++q) {
+        const double send = upper ? v[q] : v[q + h];
+        const double keep = upper ? v[q + h] : v[q];
+        v[q] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+      }
+    }
+    double r = v[0];
+#pragma unroll
+    for (int o = (16 >> M); o > 0; o >>= 1) r += __shfl_xor_sync(0xffffffffu, r, o);
+    const int idx = M == 0 ? 0 : lane >> (5 - M);
+    if ((lane & ((1 << (5 - M)) - 1)) == 0 && c0 + idx < K) out[c0 + idx] = r;
+  }
+}
+
 // The flags are written only by earlier kernels on the stream, so a read-only-path load is
 // safe; it is served from L1 after the first warp per SM instead of serializing every warp
 // of the grid on one L2 line.

@@ -318,12 +318,8 @@ __device__ __forceinline__ double ldcg(const double* p) { return __ldcg(p); }
 template <int K>
 __device__ __forceinline__ void orth_store(const double (&acc)[K], double* red, double* partials, int d0) {
   constexpr int NW = ORTH_NT / 32;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-#pragma unroll
-  for (int q = 0; q < K; ++q) {
-    const double v = warp_sum(acc[q]);
-    if (lane == 0) red[warp * K + q] = v;
-  }
+  const int warp = threadIdx.x >> 5;
+  warp_sums(acc, red + warp * K);
   __syncthreads();
   if (threadIdx.x < K) {
     double s = 0.0;
@@ -337,12 +333,8 @@ __device__ __forceinline__ void orth_store(const double (&acc)[K], double* red, 
 template <int K, int K1>
 __device__ __forceinline__ void orth_store2(const double (&acc)[K], double* red, double* partials, int d0, int d1) {
   constexpr int NW = ORTH_NT / 32;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-#pragma unroll
-  for (int q = 0; q < K; ++q) {
-    const double v = warp_sum(acc[q]);
-    if (lane == 0) red[warp * K + q] = v;
-  }
+  const int warp = threadIdx.x >> 5;
+  warp_sums(acc, red + warp * K);
   __syncthreads();
   if (threadIdx.x < K) {
     double s = 0.0;
