@@ -285,11 +285,7 @@ __global__ void __launch_bounds__(MW_WARPS * 32) k_mpk2w(const __grid_constant__
   if (DOTS) {
     // fixed-order CTA reduction: product (x, level j) -> dot0 + x*J + (j-1)
     __shared__ double red[MW_WARPS][NACC];
-#pragma unroll
-    for (int q = 0; q < NACC; ++q) {
-      const double v = warp_sum(acc[q]);
-      if (lane == 0) red[wid][q] = v;
-    }
+    warp_sums(acc, red[wid]);
     __syncthreads();
     for (int e = threadIdx.x; e < NACC; e += blockDim.x) {
       double s = 0.0;
@@ -436,12 +432,8 @@ __global__ void __launch_bounds__(TXE* TYE) k_mpk3d(const __grid_constant__ MpkD
   if (DOTS) {
     constexpr int NW = NT / 32;
     __shared__ double red[NW][NACC];
-    const int lane = tid & 31, warp = tid >> 5;
-#pragma unroll
-    for (int q = 0; q < NACC; ++q) {
-      const double v = warp_sum(acc[q]);
-      if (lane == 0) red[warp][q] = v;
-    }
+    const int warp = tid >> 5;
+    warp_sums(acc, red[warp]);
     __syncthreads();
     for (int e = tid; e < NACC; e += blockDim.x) {
       double s = 0.0;

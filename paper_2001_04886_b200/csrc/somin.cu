@@ -230,12 +230,8 @@ struct PersistDesc {
 template <int K>
 __device__ __forceinline__ void ps_store(const double (&acc)[K], double* red, double* partials, int d0) {
   constexpr int NW = PS_NT / 32;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-#pragma unroll
-  for (int q = 0; q < K; ++q) {
-    const double v = warp_sum(acc[q]);
-    if (lane == 0) red[warp * K + q] = v;
-  }
+  const int warp = threadIdx.x >> 5;
+  warp_sums(acc, red + warp * K);
   __syncthreads();
   if (threadIdx.x < K) {
     double s = 0.0;

@@ -168,15 +168,7 @@ __device__ __forceinline__ void cta_store_partials(const double (&acc)[K], int n
                                                    int dot0, int G) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   __syncthreads();
-  if (warp < NCW) {
-#pragma unroll
-    for (int k = 0; k < K; ++k) {
-      if (k < nk) {
-        const double v = warp_sum(acc[k]);
-        if (lane == 0) red[warp * K + k] = v;
-      }
-    }
-  }
+  if (warp < NCW) warp_sums(acc, red + warp * K);  // (values k >= nk are summed but unused)
   __syncthreads();
   for (int k = threadIdx.x; k < nk; k += blockDim.x) {
     double s = 0.0;
@@ -526,13 +518,7 @@ __global__ void __launch_bounds__(THREADS) k_grm(const __grid_constant__ GrmDesc
   }
   __syncthreads();
   double* red = p.stages;  // [group][chunk][K]
-  if (active) {
-#pragma unroll
-    for (int k = 0; k < K; ++k) {
-      const double v = warp_sum(acc[k]);
-      if (lane == 0) red[((size_t)group * nch + chunk) * K + k] = v;
-    }
-  }
+  if (active) warp_sums(acc, red + ((size_t)group * nch + chunk) * K);
   __syncthreads();
   for (int e = threadIdx.x; e < nch * K; e += blockDim.x) {
     const int ch = e / K, k = e % K, lb = k / NR, r = k % NR;
