@@ -113,10 +113,17 @@ __global__ void __launch_bounds__(TR_NT) k_trsv(const int64_t* __restrict__ rp, 
 #define SKC_SW_D 16
 #endif
 constexpr int SW_D = SKC_SW_D;
+constexpr unsigned long long kBndSentinel = 0x7FF0DEADBEEF0001ULL;  // signalling NaN
+
+__global__ void k_fill_bits(double* p, unsigned long long bits, int64_t n) {
+  SKC_PDL_ENTRY();
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    reinterpret_cast<unsigned long long*>(p)[i] = bits;
+}
 template <bool LOWER>
 __global__ void __launch_bounds__(32) k_trsv_strip(const double* __restrict__ a1, const double* __restrict__ a2,
                                                    const double* __restrict__ ac, const uint8_t* __restrict__ msk,
-                                                   int nx, int ny, const double* r, double* z, int* progress,
+                                                   int nx, int ny, const double* r, double* z, double* bnd,
                                                    const int* halt, const int* cond) {
   SKC_PDL_ENTRY();
   if (skip_launch(halt, cond)) return;
@@ -152,13 +159,17 @@ __global__ void __launch_bounds__(32) k_trsv_strip(const double* __restrict__ a1
       const int t = t0 + u;
       if (t >= T) break;
       if ((t & 31) == 0 && has_nb) {  // lane 0's in-row neighbours for rows t .. t+31
-        const int need = min(ny, t + 32);
-        int got;
-        do {
-          asm volatile("ld.acquire.gpu.b32 %0, [%1];" : "=r"(got) : "l"(progress + nb) : "memory");
-        } while (got < need);
-        const int yy = LOWER ? t + k : ny - 1 - (t + k);
-        wchunk = t + k < ny ? z[(int64_t)yy * nx + xn] : 0.0;
+        // each lane waits for its row's value in the neighbour strip's boundary column to
+        // replace the sentinel (a signalling NaN, which arithmetic never produces), bounded
+        double w = 0.0;
+        if (t + k < ny) {
+          const volatile unsigned long long* b =
+              reinterpret_cast<const volatile unsigned long long*>(bnd + (int64_t)nb * ny + t + k);
+          unsigned long long bits = *b;
+          for (int spin = 0; bits == kBndSentinel && spin < (1 << 26); ++spin) bits = *b;
+          w = __longlong_as_double((long long)bits);
+        }
+        wchunk = w;
       }
       const double from_prev_lane = __shfl_up_sync(0xffffffffu, zlast, 1);
       const double nbv = __shfl_sync(0xffffffffu, wchunk, t & 31);
@@ -181,8 +192,7 @@ __global__ void __launch_bounds__(32) k_trsv_strip(const double* __restrict__ a1
         z[p] = acc;
         zlast = acc;
         const int done = t - k + 1;  // rows of this column finished
-        if (publisher && (done % 32 == 0 || done == ny))
-          asm volatile("st.release.gpu.b32 [%0], %1;" ::"l"(progress + sx), "r"(done) : "memory");
+        if (publisher) *reinterpret_cast<volatile double*>(bnd + (int64_t)sx * ny + (done - 1)) = acc;
       }
       fetch(t + SW_D, u);
     }
@@ -204,8 +214,10 @@ void launch_trsv(Ctx& c, const IluData& d, const double* r, double* z, const int
   Launch lh(c, LOWER ? "ilu_lower" : "ilu_upper", bytes);
   if (d.gnx > 0 && c.ilu_strips) {
     const int ns = (int)((d.gnx + 31) / 32);
-    int* prog = d.progress + (LOWER ? 0 : ns);
-    CK(cudaMemsetAsync(prog, 0, sizeof(int) * ns, c.stream));
+    double* bnd = d.bnd;
+    launch_k(c, k_fill_bits, (unsigned)std::min<int64_t>(1184, (ns * d.gny + 255) / 256), 256, 0, bnd, kBndSentinel,
+             (int64_t)ns * d.gny);
+    ++c.launches;
     cudaLaunchConfig_t sc{};
     sc.gridDim = ns;
     sc.blockDim = 32;
@@ -217,10 +229,10 @@ void launch_trsv(Ctx& c, const IluData& d, const double* r, double* z, const int
     sc.numAttrs = 1;
     if (LOWER)
       CK(cudaLaunchKernelEx(&sc, k_trsv_strip<true>, d.lW, d.lS, (const double*)nullptr, d.lm, (int)d.gnx, (int)d.gny,
-                            r, z, prog, halt, cond));
+                            r, z, bnd, halt, cond));
     else
       CK(cudaLaunchKernelEx(&sc, k_trsv_strip<false>, d.uE, d.uN, d.uC, d.um, (int)d.gnx, (int)d.gny,
-                            (const double*)nullptr, z, prog, halt, cond));
+                            (const double*)nullptr, z, bnd, halt, cond));
     return;
   }
   if ((LOWER ? d.maxw_l : d.maxw_u) <= 8 * TR1_NT) {
@@ -366,8 +378,8 @@ void build_ilu0_op(Ctx& c, Op& op, int64_t n, const uint64_t* offs, const uint64
       d.uN = upload(op, uN);
       d.lm = upload(op, lm);
       d.um = upload(op, um);
-      std::vector<int> prog(2 * ((nx + 31) / 32), 0);
-      d.progress = const_cast<int*>(upload(op, prog));
+      std::vector<double> bnd((size_t)((nx + 31) / 32) * d.base.d.ny, 0.0);
+      d.bnd = const_cast<double*>(upload(op, bnd));
     }
   }
   for (size_t q = 0; q + 1 < llev.size(); ++q) d.maxw_l = std::max(d.maxw_l, llev[q + 1] - llev[q]);

@@ -90,7 +90,7 @@ struct IluData {
   int64_t gnx = 0, gny = 0;         // 0: not a 5-point grid
   const double *lS = nullptr, *lW = nullptr, *uC = nullptr, *uE = nullptr, *uN = nullptr;
   const uint8_t *lm = nullptr, *um = nullptr;
-  int* progress = nullptr;          // per-strip rows-done counters (2 x strips)
+  double* bnd = nullptr;            // per-strip boundary column handed to the next strip
 };
 
 // ---------------------------------------------------------------- streaming geometry
