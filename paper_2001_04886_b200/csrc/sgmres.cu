@@ -245,8 +245,10 @@ __global__ void k_arn_check(ArnState* st, const Gram* grams, int k, double* rec,
 // so all CTAs take identical coefficients and the same reorthogonalization decision; CTA 0
 // writes the records and the device flags.
 constexpr int ORTH_NT = 512;
-// points per thread per iteration, all their loads issued first (Scalar1 products, seed)
-constexpr int ORTH_UC = 4;
+// points per thread per iteration, all their loads issued first (Scalar1 products, seed):
+// 8 x s loads of 8 bytes per thread ~ the unified L1 left beside the candidate slice (4 -> 8:
+// C2 3848 -> 3909 s-steps/s)
+constexpr int ORTH_UC = 8;
 constexpr size_t kOrthSmemCap = 220 * 1024;
 // candidate columns kept in shared memory (the rest in their basis slots): shared memory is
 // carved out of the unified L1, whose remaining capacity bounds the loads in flight per SM
