@@ -457,6 +457,36 @@ __global__ void __launch_bounds__(ORTH_NT, 1) k_arn_step(const __grid_constant__
     if (dots) orth_store(acc, red, d.partials, dst);
   };
 
+  // round-0 products V_0^T cand[:,1:] -> partials dr0 (sstep.hpp:341), four points per thread
+  // with all their loads issued first
+  auto r0_products = [&]() {
+    constexpr int U0 = S <= 4 ? 4 : 2;
+    double acc[S * NC];
+#pragma unroll
+    for (int q = 0; q < S * NC; ++q) acc[q] = 0.0;
+    const double* V0 = colp(0, 0);
+    const int64_t np = d.np;
+    for (int p0 = tid; p0 < cnt; p0 += U0 * ORTH_NT) {
+      double lv[U0][S], cv[U0][NC];
+#pragma unroll
+      for (int u = 0; u < U0; ++u) {
+        const int p = p0 + u * ORTH_NT;
+        const bool h = p < cnt;
+#pragma unroll
+        for (int l = 0; l < S; ++l) lv[u][l] = h ? ldcg(V0 + l * np + p) : 0.0;
+#pragma unroll
+        for (int j = 0; j < NC; ++j) cv[u][j] = h ? ccol(j)[p] : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < U0; ++u)
+#pragma unroll
+        for (int l = 0; l < S; ++l)
+#pragma unroll
+          for (int j = 0; j < NC; ++j) acc[l * NC + j] = fma(lv[u][l], cv[u][j], acc[l * NC + j]);
+    }
+    orth_store(acc, red, d.partials, d.dr0);
+  };
+
   // L-block products with the full candidate: lhs(l) . cand[:,jc] for one block of s columns
   // (block i of the basis, or the candidate itself when i == k) -> partials d0 + l*s + jc.
   // With ZD also lhs(l) . z -> partials dz0 + l: the next block iteration's Scalar1 products
@@ -854,21 +884,7 @@ __global__ void __launch_bounds__(ORTH_NT, 1) k_arn_step(const __grid_constant__
   orth_mark(d, 43);
   if (!d.build_next) return;  // the last block iteration builds the candidate only
   // ---- round-0 products V_0^T cand[:,1:] (sstep.hpp:341)
-  {
-    double acc[S * NC];
-#pragma unroll
-    for (int q = 0; q < S * NC; ++q) acc[q] = 0.0;
-    const double* V0 = colp(0, 0);
-    for (int p = tid; p < cnt; p += ORTH_NT) {
-#pragma unroll
-      for (int l = 0; l < S; ++l) {
-        const double lv = ldcg(V0 + l * np + p);
-#pragma unroll
-        for (int j = 0; j < NC; ++j) acc[l * NC + j] = fma(lv, ccol(j)[p], acc[l * NC + j]);
-      }
-    }
-    orth_store(acc, red, d.partials, d.dr0);
-  }
+  r0_products();
   grid.sync();
   orth_mark(d, 0);
   // ---- pass 0; the last round also writes the candidate back (final unless a second pass
@@ -937,23 +953,7 @@ __global__ void __launch_bounds__(ORTH_NT, 1) k_arn_step(const __grid_constant__
   orth_mark(d, 3);
   if (s_first >= 0) {
     // ---- pass 1: V_0^T cand[:,1:], k rounds with t accumulated, then W of the new candidate
-    {
-      double acc[S * NC];
-#pragma unroll
-      for (int q = 0; q < S * NC; ++q) acc[q] = 0.0;
-      const double* V0[S];
-#pragma unroll
-      for (int l = 0; l < S; ++l) V0[l] = colp(0, l);
-      for (int p = tid; p < cnt; p += ORTH_NT) {
-#pragma unroll
-        for (int l = 0; l < S; ++l) {
-          const double lv = ldcg(V0[l] + p);
-#pragma unroll
-          for (int j = 0; j < NC; ++j) acc[l * NC + j] = fma(lv, ccol(j)[p], acc[l * NC + j]);
-        }
-      }
-      orth_store(acc, red, d.partials, d.dr0);
-    }
+    r0_products();
     grid.sync();
     for (int i = 0; i < K; ++i) {
       scalar(i, (i & 1) ? d.dr1 : d.dr0, G, 1);
