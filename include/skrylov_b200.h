@@ -152,6 +152,11 @@ int skc_ilu0_factor(uint64_t n, const uint64_t* row_offsets, const uint64_t* col
 /* seeded k = exp(N(0,1)) field of the variable-coefficient configurations (BASELINE configs[4];
  * DESIGN.md "Inputs"), host only */
 int skc_fill_lognormal(uint64_t seed, uint64_t n, double* out);
+/* the paper's test problem, host only (problem.hpp:129-203 discretize(ProblemSpec{nx, beta,
+ * gamma}) + initial_guess): CSR (row_offsets n+1; col_indices / values 5n - 4nx, columns
+ * ascending), rhs, x0 and (optional, may be NULL) the analytic solution; n = nx^2 */
+int skc_discretize(uint64_t nx, double beta, double gamma, uint64_t* row_offsets, uint64_t* col_indices,
+                   double* values, double* rhs, double* x0, double* u_true);
 int skc_op_destroy(skc_op* op);
 int skc_op_size(const skc_op* op, uint64_t* n);
 /* 0 = general CSR, 2 = 2D stencil, 3 = 3D stencil, 4 = ILU(0)-preconditioned A (LU)^{-1} */

@@ -273,7 +273,7 @@ class Oracle:
         cfg = SStepCfg(s, k, m, tol, max_iterations, 0, 0, 0, divergence_factor)
         x = np.zeros(a.n)
         rep = Report()
-        st = self.lib.ref_solve_linear(C.byref(a.c), _dp(f), _dp(x0), {"somin": 0, "sgmres": 1}[method],
+        st = self.lib.ref_solve_linear(C.byref(a.c), _dp(f), _dp(x0), {"somin": 0, "sgmres": 1, "gmres": 2}[method],
                                        C.byref(cfg), int(precondition), _dp(x), C.byref(rep))
         try:
             if st:

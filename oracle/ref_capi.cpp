@@ -16,6 +16,7 @@
 
 #include <random>
 
+#include "skrylov/accounting.hpp"
 #include "skrylov/ilu0.hpp"
 #include "skrylov/kernels.hpp"
 #include "skrylov/problem.hpp"
@@ -332,7 +333,7 @@ void ref_ilu0_apply(const orc_csr* a, const double* lu, const double* r, double*
   ilu0_apply(f, std::span<const double>(r, a->n), std::span<double>(z, a->n));
 }
 
-// method: 0 s-Omin, 1 s-GMRES; cfg->tol is the driver's threshold
+// method: 0 s-Omin, 1 s-GMRES, 2 GMRES(m); cfg->tol is the driver's threshold
 int ref_solve_linear(const orc_csr* a, const double* f, const double* x0, int32_t method, const orc_sstep_cfg* cfg,
                      int32_t precondition, double* x_out, orc_report* rep) {
   return guarded(rep->error, sizeof rep->error, [&] {
@@ -342,6 +343,15 @@ int ref_solve_linear(const orc_csr* a, const double* f, const double* x0, int32_
     std::vector<double> x(x0, x0 + n);
     const SStepConfig c = sconf(cfg);
     auto dispatch = [&](const LinearOperator& op, std::span<const double> rhs, std::vector<double>& xv) {
+      if (method == 2) {  // the standard GMRES(m) (solvers.hpp:297-359), as bench.hpp:94-108 configures it
+        SolverConfig g;
+        g.method = Method::gmres;
+        g.k = c.k;
+        g.m = c.m;
+        g.tol = c.tol;
+        g.max_iterations = c.max_iterations;
+        return gmres_solve(op, rhs, xv, g);
+      }
       return method == 0 ? somin_solve(op, rhs, xv, c) : sgmres_solve(op, rhs, xv, c);
     };
     SolveReport r;
@@ -375,6 +385,49 @@ int ref_solve_linear(const orc_csr* a, const double* f, const double* x0, int32_
     std::memcpy(x_out, x.data(), sizeof(double) * n);
     fill(rep, r);
   });
+}
+
+// accounting.hpp: kind 0 predicted_omin(a, b, c), 1 predicted_gmres(a, b).gmres,
+// 2 predicted_gmres(a, b).sgmres, 3 somin_audit_slack(a), 4 gmres_audit_slack(),
+// 5 sgmres_audit_slack(a, b)
+void ref_accounting_predict(int32_t kind, uint64_t a, uint64_t b, uint64_t c, orc_counter* out) {
+  OpCounter r;
+  switch (kind) {
+    case 0: r = predicted_omin(a, b, c); break;
+    case 1: r = predicted_gmres(a, b).gmres; break;
+    case 2: r = predicted_gmres(a, b).sgmres; break;
+    case 3: r = somin_audit_slack(a); break;
+    case 4: r = gmres_audit_slack(); break;
+    default: r = sgmres_audit_slack(a, b); break;
+  }
+  *out = orc_counter{r.dotprods, r.matvecs, r.vec_updates, r.stored_vectors, r.termination_dots};
+}
+
+// audit(rep{op_history, steady_iteration}, predicted, mode 0 exact / 1 bounded / 2 off, slack):
+// flags = ok, matvecs_exact, dotprods_exact, updates_exact; diffs joined by '\n'.
+void ref_audit(const orc_counter* hist, uint64_t n_hist, uint64_t steady, const orc_counter* predicted,
+               int32_t mode, const orc_counter* slack, int32_t* flags, char* diffs, uint64_t cap) {
+  auto oc = [](const orc_counter& c) {
+    OpCounter o;
+    o.dotprods = c.dotprods;
+    o.matvecs = c.matvecs;
+    o.vec_updates = c.vec_updates;
+    o.stored_vectors = c.stored_vectors;
+    o.termination_dots = c.termination_dots;
+    return o;
+  };
+  SolveReport rep;
+  for (uint64_t i = 0; i < n_hist; ++i) rep.op_history.push_back(oc(hist[i]));
+  rep.steady_iteration = steady;
+  AuditReport v = audit(rep, oc(*predicted), mode == 0 ? AuditMode::exact : mode == 1 ? AuditMode::bounded : AuditMode::off,
+                        oc(*slack));
+  flags[0] = v.ok;
+  flags[1] = v.matvecs_exact;
+  flags[2] = v.dotprods_exact;
+  flags[3] = v.updates_exact;
+  std::string j;
+  for (std::size_t i = 0; i < v.diffs.size(); ++i) j += (i ? "\n" : "") + v.diffs[i];
+  if (cap) std::snprintf(diffs, cap, "%s", j.c_str());
 }
 
 void ref_free(void* p) { std::free(p); }

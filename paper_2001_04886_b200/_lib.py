@@ -74,7 +74,7 @@ EXPORTS = [
     "skc_gram_solve", "skc_cholesky_upper", "skc_hessenberg_lsq",
     "skc_nccl_unique_id", "skc_ctx_create_nccl", "skc_ctx_create_callback", "skc_ctx_world",
     "skc_op_create_stencil_slab", "skc_slab_range",
-    "skc_op_create_ilu0", "skc_ilu0_solve", "skc_ilu0_solve_device", "skc_ilu0_factor", "skc_fill_lognormal",
+    "skc_op_create_ilu0", "skc_ilu0_solve", "skc_ilu0_solve_device", "skc_ilu0_factor", "skc_fill_lognormal", "skc_discretize",
 ]
 
 ALLGATHER_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, P(dbl), P(dbl), u64)
@@ -136,6 +136,7 @@ def lib():
         "skc_ilu0_solve_device": [vp, vp, vp, vp],
         "skc_ilu0_factor": [u64, P(u64), P(u64), P(dbl), P(dbl)],
         "skc_fill_lognormal": [u64, u64, P(dbl)],
+        "skc_discretize": [u64, dbl, dbl, P(u64), P(u64), P(dbl), P(dbl), P(dbl), P(dbl)],
     }
     for name, args in sig.items():
         fn = getattr(L, name)

@@ -294,6 +294,73 @@ int skc_fill_lognormal(uint64_t seed, uint64_t n, double* out) {
   });
 }
 
+// The paper's test problem (problem.hpp:58-203: paper_problem + assemble, the five-point
+// finite-difference discretization of -(b u_x)_x - (c u_y)_y + d u_x + e u_y + f u on the unit
+// square, 1/h^2 scaling, natural row-major order, Dirichlet data of the manufactured solution
+// lifted into the right-hand side) and initial_guess (problem.hpp:129-135).  Host only; the
+// operations and their order follow the reference expression by expression (no contraction),
+// so the arrays are bit-identical to the reference's on glibc.  Buffers: row_offsets n+1,
+// col_indices / values 5n - 4nx (columns ascending per row), rhs / x0 / u_true n (u_true may be
+// NULL); n = nx^2.
+int skc_discretize(uint64_t nx, double beta, double gamma, uint64_t* row_offsets, uint64_t* col_indices,
+                   double* values, double* rhs, double* x0, double* u_true) {
+  return guarded([&] {
+    skc::require(nx >= 1, "assemble: nx must be at least 1");
+    skc::require(row_offsets && col_indices && values && rhs && x0, "null argument");
+    const double pi = 3.141592653589793;
+    auto b = [](double x, double y) { return std::exp(-x * y); };
+    auto c = [](double x, double y) { return std::exp(x * y); };
+    auto u = [pi](double x, double y) { return x * std::exp(x * y) * std::sin(pi * x) * std::sin(pi * y); };
+    auto g = [&](double x, double y) {  // the hand-differentiated operator applied to u
+      const double ex = std::exp(x * y);
+      const double sx = std::sin(pi * x), cx = std::cos(pi * x);
+      const double sy = std::sin(pi * y), cy = std::cos(pi * y);
+      const double uu = x * ex * sx * sy;
+      const double ux = ex * sy * ((1.0 + x * y) * sx + pi * x * cx);
+      const double uxx = ex * sy * ((y * (2.0 + x * y) - pi * pi * x) * sx + 2.0 * pi * (1.0 + x * y) * cx);
+      const double uy = x * ex * sx * (x * sy + pi * cy);
+      const double uyy = x * ex * sx * ((x * x - pi * pi) * sy + 2.0 * pi * x * cy);
+      const double cb = std::exp(-x * y), cc = std::exp(x * y), cd = beta * (x + y), ce = gamma * (x + y);
+      const double cf = 1.0 / (1.0 + x * y);
+      return cb * (y * ux - uxx) - cc * (x * uy + uyy) + cd * ux + ce * uy + (beta + gamma + cf) * uu;
+    };
+    const double h = 1.0 / (static_cast<double>(nx) + 1.0);
+    const double ih2 = 1.0 / (h * h), i2h = 1.0 / (2.0 * h);
+    uint64_t nz = 0;
+    row_offsets[0] = 0;
+    for (uint64_t j = 1; j <= nx; ++j)
+      for (uint64_t i = 1; i <= nx; ++i) {
+        const uint64_t row = (j - 1) * nx + (i - 1);
+        const double x = static_cast<double>(i) * h, y = static_cast<double>(j) * h;
+        const double xe = (static_cast<double>(i) + 0.5) * h, xw = (static_cast<double>(i) - 0.5) * h;
+        const double yn = (static_cast<double>(j) + 0.5) * h, ys = (static_cast<double>(j) - 0.5) * h;
+        const double be = b(xe, y) * ih2, bw = b(xw, y) * ih2;
+        const double cn = c(x, yn) * ih2, cs = c(x, ys) * ih2;
+        const double de = beta * ((x + h) + y) * i2h, dw = beta * ((x - h) + y) * i2h;
+        const double en = gamma * (x + (y + h)) * i2h, es = gamma * (x + (y - h)) * i2h;
+        const double diag = be + bw + cn + cs + 1.0 / (1.0 + x * y);
+        const double ce = -be + de, cw = -bw - dw, cnn = -cn + en, css = -cs - es;
+        double r = g(x, y);
+        if (u_true) u_true[row] = u(x, y);
+        // the reference lifts east, west, north, south in that order; the row's entries are
+        // stored with ascending columns (south, west, diagonal, east, north)
+        if (i >= nx) r -= ce * u(1.0, y);
+        if (i <= 1) r -= cw * u(0.0, y);
+        if (j >= nx) r -= cnn * u(x, 1.0);
+        if (j <= 1) r -= css * u(x, 0.0);
+        auto put = [&](uint64_t col, double v) { col_indices[nz] = col; values[nz++] = v; };
+        if (j > 1) put(row - nx, css);
+        if (i > 1) put(row - 1, cw);
+        put(row, diag);
+        if (i < nx) put(row + 1, ce);
+        if (j < nx) put(row + nx, cnn);
+        row_offsets[row + 1] = nz;
+        rhs[row] = r;
+      }
+    for (uint64_t i = 1; i <= nx * nx; ++i) x0[i - 1] = 0.05 * static_cast<double>(i % 50);
+  });
+}
+
 int skc_ilu0_factor(uint64_t n, const uint64_t* row_offsets, const uint64_t* col_indices, const double* values,
                     double* lu_out) {
   return guarded([&] {

@@ -14,7 +14,7 @@ numerical breakdown inside the solvers is reported in ``SolveReport.breakdown``.
 from __future__ import annotations
 
 import ctypes as C
-from dataclasses import dataclass, field
+from dataclasses import dataclass, field, replace
 
 import numpy as np
 
@@ -78,6 +78,7 @@ class SolveReport:
     fallback_cycles: int = 0
     notes: list = field(default_factory=list)
     block_rho: list = field(default_factory=list)
+    audit: object = None  # accounting.AuditReport when solve_linear ran the driver's audit
 
 
 class _Report:
@@ -214,6 +215,38 @@ def ilu0_factor(row_offsets, col_indices, values) -> np.ndarray:
     return lu
 
 
+@dataclass
+class DiscretizedProblem:
+    """problem.hpp:121-127: the CSR system (columns ascending), rhs, analytic solution, x0."""
+    nx: int
+    row_offsets: np.ndarray
+    col_indices: np.ndarray
+    values: np.ndarray
+    rhs: np.ndarray
+    u_true: np.ndarray
+    x0: np.ndarray
+
+    @property
+    def n(self) -> int:
+        return self.nx * self.nx
+
+
+def discretize(nx: int, beta: float = 1.0, gamma: float = 50.0) -> DiscretizedProblem:
+    """problem.hpp:201-203 discretize(ProblemSpec{nx, beta, gamma}): the paper's five-point
+    convection-diffusion problem (1/h^2 scaling) and initial_guess, assembled on the host by the
+    library (skc_discretize), bit-identical to the reference's."""
+    if nx < 1:
+        raise ValueError("assemble: nx must be at least 1")
+    n = nx * nx
+    nnz = 5 * n - 4 * nx
+    out = DiscretizedProblem(nx, np.zeros(n + 1, np.uint64), np.zeros(nnz, np.uint64), np.zeros(nnz),
+                             np.zeros(n), np.zeros(n), np.zeros(n))
+    check(lib().skc_discretize(nx, beta, gamma, out.row_offsets.ctypes.data_as(P(u64)),
+                               out.col_indices.ctypes.data_as(P(u64)), _dp(out.values), _dp(out.rhs),
+                               _dp(out.x0), _dp(out.u_true)))
+    return out
+
+
 class DeviceOperator:
     """Device-describable operator (the GPU replacement of LinearOperator, operator.hpp:34-57)."""
 
@@ -289,16 +322,40 @@ def gmres_solve(op, f, x, cfg: SolverConfig = SolverConfig()) -> SolveReport:
     return _solve(lib().skc_gmres_solve, op, f, x, cfg)
 
 
+def _dispatch(method: str, cfg: SStepConfig):
+    """bench.hpp:94-124 dispatch_method for the methods with a device path: smr, somin, sgcr
+    (somin with an unbounded window), sgmres, and the standard gmres (its SolverConfig built
+    from cfg's m / k / tol / max_iterations as the driver does)."""
+    if method == "smr":
+        return smr_solve, cfg
+    if method in ("somin", "sgcr"):
+        return somin_solve, replace(cfg, unbounded_window=method == "sgcr")
+    if method == "sgmres":
+        return sgmres_solve, cfg
+    if method == "gmres":
+        return gmres_solve, SolverConfig(method="gmres", k=cfg.k, m=cfg.m, tol=cfg.tol,
+                                         max_iterations=cfg.max_iterations, debug_checks=cfg.debug_checks)
+    if method in ("mr", "omin", "gcr"):
+        raise ValueError(f"solve_linear: method {method} has no device path (the standard "
+                         "non-GMRES solvers are outside the s-step hot path)")
+    raise ValueError("unknown method: " + method)
+
+
 def solve_linear(ctx: Context, row_offsets, col_indices, values, f, x0, method: str, cfg: SStepConfig,
-                 precondition: bool = True):
+                 precondition: bool = True, audit=None):
     """The reference driver around the s-step solvers (solve_linear, bench.hpp:149-191), on the GPU:
     with `precondition`, ILU(0) right preconditioning -- the solver iterates w from zero on
     A (LU)^{-1} with the initial residual as right-hand side, then x = x0 + (LU)^{-1} w -- so the
     residual it minimizes is the true residual; in both cases the true residual is recomputed
     and appended to the history, and a converged solve whose true residual exceeds cfg.tol is
-    reported as not converged.  Returns (x, report).  `method` is "somin" or "sgmres";
-    cfg.tol is the driver's threshold."""
-    solve = {"somin": somin_solve, "sgmres": sgmres_solve}[method]
+    reported as not converged.  Returns (x, report).  `method`: smr, somin, sgcr, sgmres or
+    gmres; cfg.tol is the driver's threshold.  `audit` ("exact" / "bounded" / an AuditMode;
+    None = off) runs the driver's op-count audit (bench.hpp:126-143, accounting.hpp) on the
+    report and stores the verdict in report.audit."""
+    from .accounting import run_audit
+    if not (len(row_offsets) - 1 == len(f) == len(x0)):
+        raise ValueError("solve_linear: rhs/guess dimension mismatch")
+    solve, cfg = _dispatch(method, cfg)
     a = ctx.csr(row_offsets, col_indices, values)
     f = np.ascontiguousarray(f, dtype=np.float64)
     x = np.array(x0, dtype=np.float64, copy=True)
@@ -326,6 +383,8 @@ def solve_linear(ctx: Context, row_offsets, col_indices, values, f, x0, method: 
     if rep.converged and true_norm > cfg.tol:
         rep.converged = False
         rep.breakdown = "recomputed true residual exceeds the threshold"
+    if audit is not None:
+        rep.audit = run_audit(rep, method, cfg.s if method != "gmres" else 1, cfg.k, cfg.m, audit)
     return x, rep
 
 

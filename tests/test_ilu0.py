@@ -99,16 +99,22 @@ def test_solve_linear_matches_reference(ctx, name):
     the s-step kernels) against the reference's run of it: identical iteration counts (a
     tolerance crossing may move by one s-step), op counters, breakdown, residual history within
     1e-9 over the first 50 s-steps (BASELINE's criterion) and the final iterate within 1e-8."""
-    from paper_2001_04886_b200 import SStepConfig, solve_linear
+    from paper_2001_04886_b200 import SStepConfig, run_audit, solve_linear
     meta, arr = case(name)
     cfg = SStepConfig(**meta["cfg"])
     x, rep = solve_linear(ctx, arr["offs"], arr["cols"], arr["vals"], arr["f"], arr["x0"], meta["method"], cfg,
-                          precondition=meta["precondition"])
+                          precondition=meta["precondition"], audit="bounded")
     step = cfg.s if meta["method"] == "sgmres" else 1
     assert abs(rep.iterations - meta["iterations"]) <= step
     if rep.iterations == meta["iterations"]:
         assert tuple(rep.op_counts) == tuple(int(v) for v in arr["op_counts"])
         assert rep.op_history == [tuple(int(v) for v in row) for row in arr["op_history"]]
+        # the driver's audit (bench.hpp:126-143) gives the verdict the reference's history gets
+        class RefRep:
+            op_history = arr["op_history"]
+            steady_iteration = meta["steady_iteration"]
+        want = run_audit(RefRep, meta["method"], cfg.s, cfg.k, cfg.m, "bounded")
+        assert (rep.audit.ok, rep.audit.diffs, rep.audit.matvecs_exact) == (want.ok, want.diffs, want.matvecs_exact)
     assert rep.converged == meta["converged"]
     assert rep.breakdown == meta["breakdown"]
     # (cases whose reference envelope is wider -- the unpreconditioned 1/h^2 problem, the s = 4
