@@ -207,7 +207,9 @@ def run_sweep(ctx, rc: RunConfig) -> list:
     if rc.matrix_market:
         n, ncols, a = _read_mm(rc.matrix_market)
         _require(n == ncols, "sweep: external matrix must be square")
-        f = _spmv_host(a, np.ones(n))  # manufactured unit solution
+        # manufactured unit solution f = A 1 (the device CSR product keeps spmv's row order and
+        # separate rounding, so f is the reference's bit for bit)
+        f = ctx.csr(*a).apply(np.ones(n))
         x0 = 0.05 * (np.arange(1, n + 1) % 50).astype(np.float64)  # initial_guess
         inst.append((rc.matrix_market, 0, a, f, x0))
     else:
@@ -224,19 +226,6 @@ def run_sweep(ctx, rc: RunConfig) -> list:
                 cell.error = str(e)
             cells.append(cell)
     return cells
-
-
-def _spmv_host(a, x):
-    """Row-sequential CSR product (sparse.hpp spmv order) for the manufactured right-hand side
-    of an external matrix (a data-format step before the solve, not the solve)."""
-    offs, cols, vals = a
-    y = np.zeros(len(offs) - 1)
-    for i in range(len(y)):
-        acc = 0.0
-        for p in range(int(offs[i]), int(offs[i + 1])):
-            acc += float(vals[p]) * float(x[int(cols[p])])
-        y[i] = acc
-    return y
 
 
 # ------------------------------------------------------------------ reports
