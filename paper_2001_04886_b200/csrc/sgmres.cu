@@ -1378,7 +1378,10 @@ struct Engine {
       const char* e = std::getenv("SKC_GRAPH");
       return !e || std::atoi(e) != 0;
     }();
-    const bool use_graph = graphs && c.world() == 1 && !c.profiling;
+    // the per-phase trace reads its timestamps back after every block iteration, which a
+    // stream capture cannot contain
+    static const bool trace = std::getenv("SKC_TRACE_ORTH") != nullptr;
+    const bool use_graph = graphs && !trace && c.world() == 1 && !c.profiling;
     if (!use_graph || cycles_enqueued++ == 0) return enqueue_cycle_direct();
     if (!cycle_exec) {
       const uint64_t l0 = c.launches;
