@@ -257,6 +257,9 @@ constexpr size_t kOrthSmemCap = 220 * 1024;
 #define SKC_ORTH_SMEM_COLS 2
 #endif
 constexpr int kOrthSmemCols = SKC_ORTH_SMEM_COLS;
+#ifndef SKC_HOIST
+#define SKC_HOIST 0
+#endif
 #ifndef SKC_UU4
 #define SKC_UU4 3
 #endif  // <= the 226 KB dynamic limit set at launch
@@ -403,7 +406,7 @@ __global__ void __launch_bounds__(ORTH_NT, 1) k_arn_step(const __grid_constant__
   // Points go in pairs (p, p + NT) with every basis load of the pair issued before the
   // arithmetic, so each thread keeps 2s (4s with the products) loads in flight; the products
   // still accumulate in ascending point order.
-  auto round = [&](int i, int dst, bool wb) {
+  auto round = [&](int i, int dst, bool wb, auto&& pre) {
     const bool dots = i + 1 < d.k;
     const double* Vi = colp(i, 0);
     const double* Vn = colp(dots ? i + 1 : i, 0);
@@ -412,9 +415,11 @@ __global__ void __launch_bounds__(ORTH_NT, 1) k_arn_step(const __grid_constant__
 #pragma unroll
     for (int q = 0; q < S * NC; ++q) acc[q] = 0.0;
     constexpr int UU = S <= 3 ? 4 : S == 4 ? SKC_UU4 : S <= 6 ? 2 : 1;
-    for (int p0 = tid; p0 < cnt; p0 += UU * ORTH_NT) {
-      bool has[UU];
-      double v[UU][S], w[UU][S], cv[UU][NC];
+    // (with SKC_HOIST the first points' basis loads are issued before `pre` -- the reduction
+    // and Gram solve of this round's coefficients -- so they are in flight during it)
+    bool has[UU];
+    double v[UU][S], w[UU][S];
+    auto load = [&](int p0) {
 #pragma unroll
       for (int u = 0; u < UU; ++u) {
         const int p = p0 + u * ORTH_NT;
@@ -425,6 +430,20 @@ __global__ void __launch_bounds__(ORTH_NT, 1) k_arn_step(const __grid_constant__
           w[u][l] = dots && has[u] ? ldcg(Vn + l * np + p) : 0.0;
         }
       }
+    };
+#if SKC_HOIST
+    load(tid);
+    pre();
+#else
+    pre();
+#endif
+    for (int p0 = tid; p0 < cnt; p0 += UU * ORTH_NT) {
+      double cv[UU][NC];
+#if SKC_HOIST
+      if (p0 != tid) load(p0);
+#else
+      load(p0);
+#endif
 #pragma unroll
       for (int u = 0; u < UU; ++u)
 #pragma unroll
@@ -890,9 +909,10 @@ __global__ void __launch_bounds__(ORTH_NT, 1) k_arn_step(const __grid_constant__
   // ---- pass 0; the last round also writes the candidate back (final unless a second pass
   //      runs) and, with zfuse, is followed by a barrier so z = A cand[:,s-1] can be formed
   for (int i = 0; i < K; ++i) {
-    scalar(i, (i & 1) ? d.dr1 : d.dr0, G, 0);
-    orth_mark(d, 8 + 3 * i);
-    round(i, ((i + 1) & 1) ? d.dr1 : d.dr0, i + 1 == K);
+    round(i, ((i + 1) & 1) ? d.dr1 : d.dr0, i + 1 == K, [&] {
+      scalar(i, (i & 1) ? d.dr1 : d.dr0, G, 0);
+      orth_mark(d, 8 + 3 * i);
+    });
     orth_mark(d, 9 + 3 * i);
     if (i + 1 < K || d.zfuse) grid.sync();
     orth_mark(d, 10 + 3 * i);
@@ -956,8 +976,7 @@ __global__ void __launch_bounds__(ORTH_NT, 1) k_arn_step(const __grid_constant__
     r0_products();
     grid.sync();
     for (int i = 0; i < K; ++i) {
-      scalar(i, (i & 1) ? d.dr1 : d.dr0, G, 1);
-      round(i, ((i + 1) & 1) ? d.dr1 : d.dr0, i + 1 == K);
+      round(i, ((i + 1) & 1) ? d.dr1 : d.dr0, i + 1 == K, [&] { scalar(i, (i & 1) ? d.dr1 : d.dr0, G, 1); });
       if (i + 1 < K) grid.sync();
     }
     cross_block(std::false_type{}, K, d.dwb, 0);
