@@ -252,6 +252,8 @@ def run_ours(args):
         "gpu_launches": launches, "converged": converged, "cycles_per_solve": cycles_per_solve,
         "s_steps_per_solve": rep.iterations / S, "kernels": kernels,
     }
+    if not converged:  # a step is a solve to tolerance: an unconverged solve is not a valid step
+        out["invalid"] = "solve did not converge inside the timed region"
     if rank == 0:
         clocks = clk.summary()
         out["clocks"] = clocks

@@ -53,9 +53,11 @@ struct SStepConfig {  // sstep.hpp:48-58 (same defaults)
   bool unbounded_window = false;
   bool debug_checks = false;
   double divergence_factor = 10.0;
+  bool fixed_steps = false;  // not in the reference: benchmark mode (see skrylov_b200.h)
 
   skc_sstep_config c() const {
-    return {s, k, m, tol, max_iterations, precondition, unbounded_window, debug_checks, divergence_factor};
+    return {s, k, m, tol, max_iterations, precondition, unbounded_window, debug_checks, divergence_factor,
+            fixed_steps};
   }
 };
 

@@ -199,6 +199,11 @@ class Oracle:
             self.lib.orc_csr_free.argtypes = [P(u64), P(u64), P(dbl)]
             self.lib.orc_stencil_apply.argtypes = [i32, u64, u64, u64, P(dbl), P(dbl), dbl, P(dbl), P(dbl)]
             self.lib.orc_set_dot_mode.argtypes = [C.c_int]
+            self.lib.orc_set_fixed_steps.argtypes = [C.c_int]
+
+    def set_fixed_steps(self, on: bool):
+        """Fixed-step benchmark mode (port only): bypass the Gram pivot-ratio and LSQ rank aborts."""
+        self.lib.orc_set_fixed_steps(int(bool(on)))
 
     def set_dot_mode(self, mode: int):
         """0: the reference's sequential summation; 1: blocked/tree (envelope measurement only)."""

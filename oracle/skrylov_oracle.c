@@ -87,6 +87,12 @@ static void* xcalloc(size_t n, size_t sz) { return calloc(n ? n : 1, sz); }
  * mode 3 = compensated (near-exact) summation. */
 static int g_dot_mode = 0;
 void orc_set_dot_mode(int mode) { g_dot_mode = mode; }
+/* Fixed-step benchmark mode: bypass only the Gram pivot-ratio abort
+ * (small_dense.hpp:62-64) and the Hessenberg-LSQ rank abort (small_dense.hpp:294-296), so a
+ * configuration whose reference run stops there keeps running the same kernels; results past
+ * that point are numerically meaningless.  Mirrors skc_sstep_config.fixed_steps. */
+static int g_fixed_steps = 0;
+void orc_set_fixed_steps(int on) { g_fixed_steps = on; }
 
 static double dot_tree(uint64_t n, const double* a, const double* b) {
   enum { CH = 1024, LANES = 8 };
@@ -329,7 +335,7 @@ static int gram_init(gram_t* g, uint64_t order, const double* w, orc_err* e) { /
     if (a < pmin) pmin = a;
     if (a > pmax) pmax = a;
   }
-  if (pmax == 0.0 || pmin / pmax < 1e-15) {
+  if ((pmax == 0.0 || pmin / pmax < 1e-15) && !g_fixed_steps) {
     char num[64];
     fmt_double(num, sizeof num, pmax == 0.0 ? 0.0 : pmin / pmax);
     err_set(e, ORC_EBREAK, "sym_solve: numerically singular Gram system (pivot ratio %s)", num);
@@ -465,7 +471,7 @@ static int hlsq_solve(const hlsq_t* h, double* y, orc_err* e) { /* :287-300 */
   for (uint64_t ii = m; ii-- > 0;) {
     double acc = h->rhs[ii];
     for (uint64_t k = ii + 1; k < m; ++k) acc -= hlsq_r(h, k, ii) * y[k];
-    if (fabs(hlsq_r(h, ii, ii)) <= tol) {
+    if (fabs(hlsq_r(h, ii, ii)) <= tol && !g_fixed_steps) {
       err_set(e, ORC_EBREAK, "hessenberg lsq: rank-deficient R diagonal at column %llu",
               (unsigned long long)(ii + 1));
       return e->code;

@@ -90,6 +90,9 @@ void orc_spmv(const orc_csr* a, const double* x, double* y);
 double orc_dot(uint64_t n, const double* a, const double* b);
 /* 0 = reference sequential order (default); 1 = blocked/tree order to measure the envelope */
 void orc_set_dot_mode(int mode);
+/* 1 = fixed-step benchmark mode: skip the Gram pivot-ratio and LSQ rank aborts (results past
+ * them are meaningless); 0 = the reference's behaviour (default) */
+void orc_set_fixed_steps(int on);
 int orc_krylov_block(const orc_csr* a, const double* v, uint64_t s, double* out /* n*s col-major */);
 
 /* small_dense.hpp: Gram solver (order <= 16). Returns 0 or 2 (breakdown) with message. */

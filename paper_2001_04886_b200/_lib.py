@@ -43,7 +43,7 @@ class OpCounter(C.Structure):
 class SStepConfigC(C.Structure):
     _fields_ = [("s", u64), ("k", u64), ("m", u64), ("tol", dbl), ("max_iterations", u64),
                 ("precondition", i32), ("unbounded_window", i32), ("debug_checks", i32),
-                ("divergence_factor", dbl)]
+                ("divergence_factor", dbl), ("fixed_steps", i32)]
 
 
 class SolverConfigC(C.Structure):

@@ -5,6 +5,7 @@
 #include <string>
 
 #include "skc_internal.hpp"
+#include "lsq.cuh"
 
 struct skc_ctx {
   skc::Ctx c;
@@ -49,6 +50,7 @@ skc::SStepCfg conv(const skc_sstep_config* c) {
   s.unbounded_window = c->unbounded_window != 0;
   s.debug_checks = c->debug_checks != 0;
   s.divergence_factor = c->divergence_factor;
+  s.fixed_steps = c->fixed_steps != 0;
   // `precondition` is honored by the driver, not the core loops (sstep.hpp:54, solvers.hpp:51):
   // the solvers ignore it, as the reference's do; the driver composes ILU(0) right
   // preconditioning (bench.hpp:160-171) from skc_op_create_ilu0 / skc_ilu0_solve
@@ -676,17 +678,21 @@ int skc_hessenberg_lsq(uint64_t rows, uint64_t cols, const double* g, double bet
   return guarded([&] {
     skc::require(rows >= cols + 1, "hessenberg_lsq: G must have more rows than columns");
     skc::require(beta >= 0.0, "hessenberg_lsq: beta must be non-negative");
-    skc::HessLsq lsq(beta);
+    // the device least-squares primitives (lsq.cuh), run on the host
+    std::vector<unsigned char> buf(skc::lsq_bytes((int)cols));
+    const skc::LsqView v = skc::lsq_view(buf.data(), (int)cols);
+    skc::lsq_reset(v, beta);
     for (uint64_t j = 0; j < cols; ++j) {
       for (uint64_t i = j + 2; i < rows; ++i)
         skc::require(g[i * cols + j] == 0.0, "hessenberg_lsq: G is not Hessenberg-banded");
       std::vector<double> col(j + 2);
       for (uint64_t i = 0; i <= j + 1; ++i) col[i] = g[i * cols + j];
-      lsq.append_column(std::move(col));
+      skc::lsq_append_serial(v, col.data());
     }
-    std::vector<double> y = lsq.solve();
-    std::memcpy(y_out, y.data(), y.size() * sizeof(double));
-    if (residual_out) *residual_out = lsq.residual_norm();
+    if (!skc::lsq_solve(v, false))
+      skc::fail(SKC_EBREAKDOWN, "hessenberg lsq: rank-deficient R diagonal at column " + std::to_string(v.h->rank_col));
+    std::memcpy(y_out, v.y, cols * sizeof(double));
+    if (residual_out) *residual_out = v.h->residual;
   });
 }
 

@@ -3,6 +3,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <mutex>
 #include <set>
 
 #include "skc_internal.hpp"
@@ -44,6 +45,19 @@ Geo make_geo(int64_t n, int sm_count) {
   g.G = (int)std::max<int64_t>(1, G);
   g.range = range;
   return g;
+}
+
+void ensure_smem_attr(const void* kernel, int bytes) {
+  if (bytes <= 48 * 1024) return;
+  static std::mutex mu;
+  static std::map<std::pair<const void*, int>, int> done;
+  int dev = 0;
+  CK(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lock(mu);
+  int& have = done[{kernel, dev}];
+  if (have >= bytes) return;
+  CK(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+  have = bytes;
 }
 
 // ---------------------------------------------------------------- Ctx
@@ -367,52 +381,6 @@ void build_csr_op(Ctx& c, Op& op, int64_t n, const uint64_t* offs, const uint64_
     o.vals = (const double*)dev_upload(op, vals, sizeof(double) * offs[n]);
     op.rows = n;
   }
-}
-
-// ---------------------------------------------------------------- host Hessenberg LSQ
-double HessLsq::matrix_norm() const { return std::sqrt(gnorm_sq_); }
-
-double HessLsq::append_column(std::vector<double> col) {
-  const size_t j = rcols_.size();
-  require(col.size() == j + 2, "hessenberg lsq: column must reach one row below diagonal");
-  for (double e : col) gnorm_sq_ += e * e;
-  for (size_t t = 0; t < j; ++t) {
-    const double a = col[t], b = col[t + 1];
-    col[t] = cos_[t] * a + sin_[t] * b;
-    col[t + 1] = -sin_[t] * a + cos_[t] * b;
-  }
-  const double a = col[j], b = col[j + 1];
-  const double r = std::hypot(a, b);
-  double c = 1.0, s = 0.0;
-  if (r != 0.0) {
-    c = a / r;
-    s = b / r;
-  }
-  cos_.push_back(c);
-  sin_.push_back(s);
-  col[j] = r;
-  col.pop_back();
-  rcols_.push_back(std::move(col));
-  rhs_.push_back(0.0);
-  const double ra = rhs_[j], rb = rhs_[j + 1];
-  rhs_[j] = c * ra + s * rb;
-  rhs_[j + 1] = -s * ra + c * rb;
-  residual_ = std::fabs(rhs_[j + 1]);
-  return residual_;
-}
-
-std::vector<double> HessLsq::solve() const {
-  const size_t m = rcols_.size();
-  const double tol = 1e-14 * matrix_norm();
-  std::vector<double> y(m, 0.0);
-  for (size_t ii = m; ii-- > 0;) {
-    double acc = rhs_[ii];
-    for (size_t k = ii + 1; k < m; ++k) acc -= rcols_[k][ii] * y[k];
-    if (std::fabs(rcols_[ii][ii]) <= tol)
-      fail(SKC_EBREAKDOWN, "hessenberg lsq: rank-deficient R diagonal at column " + std::to_string(ii + 1));
-    y[ii] = acc / rcols_[ii][ii];
-  }
-  return y;
 }
 
 }  // namespace skc

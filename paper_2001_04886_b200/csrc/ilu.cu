@@ -212,8 +212,16 @@ void launch_trsv(Ctx& c, const IluData& d, const double* r, double* z, const int
   cfg.numAttrs = 1;
   const double bytes = LOWER ? 8.0 * (2.0 * d.n) + 12.0 * d.nnz_l + 12.0 * d.n : 8.0 * (2.0 * d.n) + 12.0 * d.nnz_u + 12.0 * d.n;
   Launch lh(c, LOWER ? "ilu_lower" : "ilu_upper", bytes);
-  if (d.gnx > 0 && c.ilu_strips) {
-    const int ns = (int)((d.gnx + 31) / 32);
+  // the strips wait on each other, so every strip must be resident at once: use them only when
+  // the cooperative grid fits (and the grid has rows to pipeline; a 1D ny = 1 "grid" is serial)
+  const int ns = d.gnx > 0 ? (int)((d.gnx + 31) / 32) : 0;
+  bool strips = d.gnx > 0 && d.gny > 1 && c.ilu_strips;
+  if (strips) {
+    int per_sm = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_trsv_strip<LOWER>, 32, 0));
+    strips = (int64_t)ns <= (int64_t)per_sm * c.sm_count;
+  }
+  if (strips) {
     double* bnd = d.bnd;
     launch_k(c, k_fill_bits, (unsigned)std::min<int64_t>(1184, (ns * d.gny + 255) / 256), 256, 0, bnd, kBndSentinel,
              (int64_t)ns * d.gny);

@@ -501,16 +501,11 @@ __global__ void __launch_bounds__(T2* T2) k_mpk2t(const __grid_constant__ MpkDes
   }
 }
 
-template <class K>
-void mpk_smem_attr(K kernel, size_t bytes) {
-  if (bytes > 48 * 1024) CK(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
-}
 
 template <int KIND, int J, bool DOTS>
 void run2d(Ctx& c, const MpkDesc& d) {
   constexpr size_t smem = mpk2w_smem<J, DOTS>();
-  static bool attr = false;
-  if (!attr) mpk_smem_attr(k_mpk2w<KIND, J, DOTS>, smem), attr = true;
+  ensure_smem(k_mpk2w<KIND, J, DOTS>, smem);
   launch_k(c, k_mpk2w<KIND, J, DOTS>, d.G, MW_WARPS * 32, smem, d);
 }
 
@@ -548,8 +543,7 @@ template <int KIND, int J, bool DOTS>
 void run3d(Ctx& c, const MpkDesc& d) {
   constexpr int TXE = 32, TYE = 16;
   constexpr size_t smem = mpk3d_smem<J, TXE * TYE, DOTS>();
-  static bool attr = false;
-  if (!attr) mpk_smem_attr(k_mpk3d<KIND, J, TXE, TYE, DOTS>, smem), attr = true;
+  ensure_smem(k_mpk3d<KIND, J, TXE, TYE, DOTS>, smem);
   launch_k(c, k_mpk3d<KIND, J, TXE, TYE, DOTS>, d.G, TXE * TYE, smem, d);
 }
 

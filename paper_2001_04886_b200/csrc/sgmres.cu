@@ -3,14 +3,13 @@
 // s = 1 and as the basis-collapse fallback (solvers.hpp:86-110, 297-359).
 //
 // One restart cycle (constructor + m block iterations, every Scalar1/Scalar2 Gram solve,
-// block-MGS pass, reorthogonalization test and basis push) is enqueued without a host
-// round trip: the s x s solves run in single-CTA scalar kernels and write the update
-// coefficients consumed by the next streaming kernel; the conditional reorthogonalization
-// pass is predicated on a device flag.  The host synchronizes once per cycle, then runs
-// the reference's host-side recurrences on the recorded coefficients: block-Hessenberg
-// reconstruction (append_g_columns), cholesky_upper of each Gram block, the Givens
-// least-squares update and the early-exit/collapse/fallback decisions, exactly in the
-// reference's order.  A second short enqueue applies x += V y and recomputes r = f - A x.
+// block-MGS pass, reorthogonalization test and basis push, and the least-squares half: the
+// block-Hessenberg columns (append_g_columns), cholesky_upper of each Gram block, the Givens
+// update with the early exit rho <= tol, the back substitution, x += V y and r = f - A x) is
+// enqueued without a host round trip, as one CUDA graph.  The s x s solves and every decision
+// run on the device (lsq.cuh, small_dense.cuh); the host synchronizes once per cycle and
+// replays the reference's control flow on the device's records to build the SolveReport
+// (history, op counts, breakdown strings) -- it computes no numbers of its own.
 #include <cooperative_groups.h>
 
 #include <cmath>
@@ -19,6 +18,7 @@
 #include <cstring>
 
 #include "device_util.cuh"
+#include "lsq.cuh"
 #include "solver_util.hpp"
 #include "stencil.cuh"
 
@@ -26,7 +26,19 @@ namespace skc {
 
 namespace {
 
-enum : int { kArnRunning = 0, kArnCtorZero = 1, kArnCtorCollapse = 2, kArnInvariant = 3, kArnPushCollapse = 4 };
+// cycle status: running, or what stopped it (and at which block, ArnState::block)
+enum : int {
+  kArnRunning = 0,
+  kArnCtorZero = 1,       // start vector zero (the reference's require, sstep.hpp:277)
+  kArnCtorCollapse = 2,   // push_block of block 0 (basis collapse at the constructor)
+  kArnInvariant = 3,      // nu <= 1e-14 ||z|| (sstep.hpp:320-324)
+  kArnPushCollapse = 4,   // push_block of block k (sstep.hpp:375)
+  kArnCholCollapse = 5,   // cholesky_upper of block k's Gram matrix (sstep.hpp:585)
+  kArnCtorChol = 6,       // cholesky_upper of block 0 (escapes sgmres_solve, sstep.hpp:563)
+  kArnEarly = 7,          // rho <= tol after block k (sstep.hpp:600)
+};
+// end-of-cycle outcome (k_arn_finish)
+enum : int { kFinNone = 0, kFinOk = 1, kFinFallback = 2, kFinLsqFail = 3 };
 
 struct ArnState {
   int status;
@@ -35,16 +47,19 @@ struct ArnState {
   int reorth;  // reorthogonalization flag of the current block iteration
   double rn;   // latest residual norm (also the constructor's ||r||)
   int zready;  // the last block iteration's cross pass produced the next z and its products
+  int fixed;   // fixed-step benchmark mode (gram_bypass_ratio, lsq_solve)
+  int fin;     // end-of-cycle outcome (kFin*)
   int pad;
 };
 
 // record layout per block iteration k (0 = constructor)
 struct RecLayout {
   int s, m;
-  __host__ __device__ int size() const { return 8 + s * s + (m + 1) * s + (m + 1) * s * s; }
-  static constexpr int kZn = 0, kNu = 1, kInv = 2, kReorth = 3, kFirst = 4, kOk = 5, kRatio = 6, kSing = 7, kW = 8;
-  __host__ __device__ int h() const { return 8 + s * s; }
-  __host__ __device__ int t() const { return 8 + s * s + (m + 1) * s; }
+  __host__ __device__ int size() const { return 10 + s * s + (m + 1) * s + (m + 1) * s * s; }
+  static constexpr int kZn = 0, kNu = 1, kInv = 2, kReorth = 3, kFirst = 4, kOk = 5, kRatio = 6, kSing = 7,
+                       kRho = 8, kW = 10;
+  __host__ __device__ int h() const { return 10 + s * s; }
+  __host__ __device__ int t() const { return 10 + s * s + (m + 1) * s; }
 };
 
 // coefficient layout
@@ -88,6 +103,7 @@ __global__ void k_arn_ctor(ArnState* st, int use_rn, const double* partials, int
     st->block = 0;
     st->reorth = 0;
     st->zready = 0;
+    st->fin = kFinNone;
     const double nv = use_rn ? st->rn : sqrt(v[0]);
     rec0[RecLayout::kZn] = nv;
     if (!(nv > 0.0)) {
@@ -127,6 +143,7 @@ __device__ bool arn_push_body(ArnState* st, Gram& g, int k, double* rec, const d
       }
     gram_factor_dev(g, W, s);
   }
+  gram_bypass_ratio(g, st->fixed);
   if (!record) return g.ok;
   for (int q = 0; q < s * s; ++q) rec[RecLayout::kW + q] = W[q];
   rec[RecLayout::kOk] = g.ok;
@@ -141,17 +158,198 @@ __device__ bool arn_push_body(ArnState* st, Gram& g, int k, double* rec, const d
   return true;
 }
 
-__global__ void k_arn_push(ArnState* st, Gram* grams, int k, double* rec, const double* partials, int G, int dWa,
-                           int dWb, int s) {
+// ---------------------------------------------------------------- least squares of the cycle
+// Device state of sgmres_solve's cycle loop (sstep.hpp:560-600): the block Hessenberg columns,
+// the L blocks and the Givens least squares (lsq.cuh), written by one CTA after each block step.
+struct ArnLsqDesc {
+  int s, m;
+  int GL;            // row stride of gcols (m s + 2)
+  int lsq_on;        // 0: sarnoldi (Hessenberg columns only, no L / Givens)
+  double tol;        // cfg.tol (absolute)
+  double* gcols;     // block Hessenberg column j (rows 0..j+1) at j * GL, unscaled
+  double* lblk;      // upper Cholesky factor of basis block b's Gram matrix at b s^2
+  void* lsq;         // LsqView base, capacity m s
+  double* rec;       // records (RecLayout), block iteration k at k * recsz
+  int recsz, rec_t, rec_h;
+  ArnState* st;
+  Gram* grams;
+};
+__host__ __device__ inline int arn_lsq_ld(int s, int m) { return m * s + 2; }
+// shared scratch of arn_lsq_step (doubles): the s new columns twice (scaled + a copy for the norm)
+__host__ __device__ inline int arn_lsq_scratch(int s, int m) { return 2 * s * arn_lsq_ld(s, m) + 8; }
+
+// Block step k's half of the cycle loop (sstep.hpp:582-600), whole CTA:
+//   push_block of the candidate (sstep.hpp:375, 392-399; when it was built: k < m and the seed
+//   did not vanish) from its raw Gram products W, then cholesky_upper of the new Gram block
+//   (sstep.hpp:585); either failing is a basis collapse and appends nothing;
+//   append_g_columns (sstep.hpp:422-445): the s columns of step k from the t coefficients of
+//   block k-1 and this step's h, nu;
+//   apply_l (sstep.hpp:566-579) and the Givens update of each column (lsq.cuh); rho is recorded
+//   and rho <= tol stops the cycle (the next block steps return at entry).
+template <int S>
+__device__ void arn_lsq_step(const ArnLsqDesc& d, int k, bool build_next, const double* W, double* scratch) {
+  __shared__ int s_go, s_nl, s_inv;
+  const int tid = threadIdx.x;
+  double* rk = d.rec + (size_t)k * d.recsz;
+  if (tid == 0) {
+    const bool invariant = d.st->status == kArnInvariant && d.st->block == k;
+    s_inv = invariant;
+    int go = !d.st->halt || invariant, nl = k;
+    if (go && build_next && !invariant) {
+      Gram g;
+      if (!arn_push_body<S>(d.st, g, k, rk, W, S)) {
+        go = 0;
+      } else {
+        d.grams[k] = g;
+        if (d.lsq_on) {
+          double L[S * S];
+          if (!cholesky_upper(g.w, S, L)) {
+            d.st->status = kArnCholCollapse;
+            d.st->block = k;
+            d.st->halt = 1;
+            go = 0;
+          } else {
+            for (int q = 0; q < S * S; ++q) d.lblk[k * S * S + q] = L[q];
+            nl = k + 1;
+          }
+        }
+      }
+    }
+    s_go = go;
+    s_nl = nl;
+  }
+  __syncthreads();
+  if (!s_go) return;
+  const bool invariant = s_inv != 0;
+  const int q = k - 1, ld = arn_lsq_ld(S, d.m), nl = s_nl;
+  const double* rq = d.rec + (size_t)q * d.recsz + d.rec_t;  // t coefficients of block q
+  double* gs = scratch;                                       // step k's columns, unscaled
+  for (int e = tid; e < S * ld; e += blockDim.x) {
+    const int cl = e / ld, r = e - cl * ld;
+    const int j = q * S + cl;
+    if (r >= j + 2) continue;
+    double v;
+    if (cl + 1 < S) {  // A v_q^cl = v_q^{cl+1} + sum_i V_i T_i[:,cl+1] - sum_i (A V_i) T_i[:,cl]
+      v = 0.0;
+      if (r == q * S + cl + 1) v += 1.0;
+      for (int i = 0; i < q; ++i) {
+        const double* ti = rq + i * S * S;
+        if (r >= i * S && r < i * S + S) v += ti[(r - i * S) * S + cl + 1];
+#pragma unroll
+        for (int lc = 0; lc < S; ++lc) {
+          const double cf = ti[lc * S + cl];
+          if (cf == 0.0) continue;
+          const int pj = i * S + lc;  // earlier column, rows 0..pj+1
+          if (r < pj + 2) v -= cf * d.gcols[(size_t)pj * d.GL + r];
+        }
+      }
+    } else {  // A v_q^{s-1} = nu v_{q+1} + sum_i V_i h_i
+      v = r < k * S ? rk[d.rec_h + r] : rk[RecLayout::kNu];
+    }
+    d.gcols[(size_t)j * d.GL + r] = v;
+    gs[e] = v;
+  }
+  if (!d.lsq_on) {
+    __syncthreads();
+    return;
+  }
+  __syncthreads();
+  double* ls = scratch + S * ld;  // L-scaled columns
+  for (int e = tid; e < S * ld; e += blockDim.x) {
+    const int cl = e / ld, r = e - cl * ld;
+    const int len = q * S + cl + 2;
+    if (r >= len) continue;
+    const double* g = gs + cl * ld;
+    const int bi = r / S, off = bi * S, rl = r - off;
+    double v = g[r];
+    if (bi < nl) {
+      const double* lb = d.lblk + bi * S * S;
+      double acc = 0.0;
+      for (int jl = rl; jl < S && off + jl < len; ++jl) acc += lb[rl * S + jl] * g[off + jl];
+      v = acc;
+    }
+    ls[e] = v;
+  }
+  const LsqView lv = lsq_view(d.lsq, d.m * S);
+  lsq_append_cta(lv, ls, ld, S, gs, nullptr);  // (gs is free again: the norms' copy)
+  if (tid == 0) {
+    const double rho = lv.h->residual;
+    rk[RecLayout::kRho] = rho;
+    if (!invariant && build_next && rho <= d.tol) {
+      d.st->status = kArnEarly;
+      d.st->block = k;
+      d.st->halt = 1;
+    }
+  }
+  __syncthreads();
+}
+
+// the constructor's push_block of block 0, then L_0 = cholesky_upper(W_0) and
+// HessenbergLsq(rn L_0(0,0)) (sstep.hpp:562-564)
+template <int S>
+__global__ void k_arn_ctor_push(const ArnLsqDesc d, const double* partials, int G, int dW) {
   SKC_PDL_ENTRY();
-  if (arn_skip(st)) return;
+  if (d.st->halt) return;
   __shared__ double v[kMaxS * kMaxS];
-  const int dW = st->reorth ? dWb : dWa;
-  reduce_dots_dev(partials, G, dW, s * s, v);
+  reduce_dots_dev(partials, G, dW, S * S, v);
   if (threadIdx.x == 0) {
     Gram g;
-    if (arn_push_body(st, g, k, rec, v, s)) grams[k] = g;
+    if (!arn_push_body<S>(d.st, g, 0, d.rec, v, S)) return;
+    d.grams[0] = g;
+    if (!d.lsq_on) return;
+    double L[S * S];
+    if (!cholesky_upper(g.w, S, L)) {
+      d.st->status = kArnCtorChol;
+      d.st->halt = 1;
+      return;
+    }
+    for (int q = 0; q < S * S; ++q) d.lblk[q] = L[q];
+    lsq_reset(lsq_view(d.lsq, d.m * S), d.st->rn * L[0]);
   }
+}
+
+// per-round path: push + least squares of block step k (W from the pass that produced the
+// candidate: the reorthogonalized region when the flag says so)
+template <int S>
+__global__ void k_arn_lsq(const ArnLsqDesc d, int k, int build_next, const double* partials, int G, int dWa, int dWb) {
+  SKC_PDL_ENTRY();
+  extern __shared__ __align__(16) double lsq_sm[];
+  if (d.st->halt && !(d.st->status == kArnInvariant && d.st->block == k)) return;
+  double* W = lsq_sm;
+  if (build_next) reduce_dots_dev(partials, G, d.st->reorth ? dWb : dWa, S * S, W);
+  __syncthreads();
+  arn_lsq_step<S>(d, k, build_next != 0, W, lsq_sm + kMaxS * kMaxS);
+}
+
+// end of the cycle (sstep.hpp:602-625): unless the constructor failed, a collapse with the
+// residual estimate above tol hands the cycle to the fallback (x untouched); otherwise y from the
+// back substitution (its rank failure is the reference's breakdown) -- y lands in the update
+// coefficients, zero beyond the appended columns, so the fixed x update adds exact zeros there
+__global__ void k_arn_finish(const ArnLsqDesc d, double* ycoef) {
+  SKC_PDL_ENTRY();
+  const int M = d.m * d.s;
+  for (int i = threadIdx.x; i < M; i += blockDim.x) ycoef[i] = 0.0;
+  __syncthreads();
+  if (threadIdx.x != 0) return;
+  ArnState* st = d.st;
+  const int stv = st->status;
+  if (stv == kArnCtorZero || stv == kArnCtorCollapse || stv == kArnCtorChol) {
+    st->fin = kFinNone;
+    return;
+  }
+  const LsqView lv = lsq_view(d.lsq, M);
+  const bool collapsed = stv == kArnPushCollapse || stv == kArnCholCollapse;
+  const bool attainable = lv.h->cols > 0 && lv.h->residual <= d.tol;
+  if (collapsed && !attainable) {
+    st->fin = kFinFallback;
+    return;
+  }
+  if (!lsq_solve(lv, st->fixed != 0)) {
+    st->fin = kFinLsqFail;
+    return;
+  }
+  for (int i = 0; i < lv.h->cols; ++i) ycoef[i] = lv.y[i];
+  st->fin = kFinOk;
 }
 
 // Scalar1 (sstep.hpp:301-310): zn = ||z||, h_i = W_i^{-1} V_i^T z
@@ -284,8 +482,8 @@ struct OrthDesc {
   int dz, dseed, dr0, dr1, dcross, dwb;
   Gram* grams;
   double* rec;            // this block iteration's record
-  double* rec_push;       // the previous block iteration's record (its push_block)
   int rec_t, rec_h;
+  ArnLsqDesc lsq;         // the cycle's least-squares state (CTA 0 runs this step's part last)
   ArnState* st;
   double orth_tol;
   unsigned long long* trace;  // optional phase timestamps (CTA 0), diagnostics
@@ -557,20 +755,21 @@ __global__ void __launch_bounds__(ORTH_NT, 1) k_arn_step(const __grid_constant__
   // the previous block iteration's cross pass already produced z (in memory) and this
   // iteration's Scalar1 products (partials dz), unless it ran a reorthogonalization pass
   const bool zready = d.zfuse && K > 1 && __ldg(&d.st->zready) != 0;
-  // push_block of the previous block iteration's candidate (sstep.hpp:375, 392-399) runs here,
-  // off the previous kernel's tail: every CTA reduces its W (from the pass that produced the
-  // candidate) and factors it in the Scalar1 phase; CTA 0 records it and stores the factor
-  const bool push = K >= 2;
-  if (push) reduce_dots_dev(d.partials, G, __ldg(&d.st->reorth) ? d.dwb : d.dcross + (K - 1) * S * S, S * S, tc);
-  // the Gram factors of blocks 0..k-1 (k-2 with the push) into shared memory (asynchronous;
-  // waited for before Scalar1)
+  // the Gram factors of blocks 0..k-1 into shared memory (asynchronous; waited for before
+  // Scalar1).  Block k-1's push_block ran at the end of the previous launch (CTA 0's tail).
   {
     const char* gsrc = reinterpret_cast<const char*>(d.grams);
     char* gdst = reinterpret_cast<char*>(gk);
-    for (int w = tid; w < (int)((push ? K - 1 : K) * sizeof(Gram) / 8); w += ORTH_NT)
-      cp_async8(gdst + 8 * w, gsrc + 8 * w, true);
+    for (int w = tid; w < (int)(K * sizeof(Gram) / 8); w += ORTH_NT) cp_async8(gdst + 8 * w, gsrc + 8 * w, true);
     cp_async_commit();
   }
+  // CTA 0's tail: this block step's push_block and least-squares step (arn_lsq_step), run
+  // once every other CTA is done with the step's data; the candidate slice area is its scratch
+  auto lsq_tail = [&](const double* Wraw) {
+    if (blockIdx.x != 0) return;
+    __syncthreads();
+    arn_lsq_step<S>(d.lsq, K, d.build_next != 0, Wraw, sc);
+  };
   orth_mark(d, 39);
   // ---- z = A v_{k-1}^{s-1} on this slice (the source is stable; neighbours read from memory)
   // y = A x on this slice; xs (optional) is this slice of x in shared memory, read in place of
@@ -700,16 +899,6 @@ __global__ void __launch_bounds__(ORTH_NT, 1) k_arn_step(const __grid_constant__
   // from shared memory); CTA 0 records
   cp_async_wait<0>();
   reduce_dots_dev(d.partials, G, d.dz, K * S + 1, prod);  // (ends with __syncthreads)
-  if (push) {
-    __shared__ int s_push_ok;
-    if (tid == 0) {
-      const bool ok = arn_push_body<S>(d.st, gk[K - 1], K - 1, d.rec_push, tc, S, blockIdx.x == 0);
-      s_push_ok = ok;
-      if (ok && blockIdx.x == 0) d.grams[K - 1] = gk[K - 1];
-    }
-    __syncthreads();
-    if (!s_push_ok) return;  // basis collapse (identical decision in every CTA)
-  }
   const double zn = sqrt(prod[K * S]);
   if (blockIdx.x == 0 && tid == 0) {
     d.rec[RecLayout::kZn] = zn;
@@ -779,6 +968,7 @@ __global__ void __launch_bounds__(ORTH_NT, 1) k_arn_step(const __grid_constant__
       d.st->block = K;
       d.st->halt = 1;
     }
+    lsq_tail(nullptr);  // (the step's Hessenberg columns still count: sstep.hpp:319, 586)
     return;
   }
   const double inv = 1.0 / nu;
@@ -901,7 +1091,10 @@ __global__ void __launch_bounds__(ORTH_NT, 1) k_arn_step(const __grid_constant__
     orth_mark(d, 44 + 2 * j);
   }
   orth_mark(d, 43);
-  if (!d.build_next) return;  // the last block iteration builds the candidate only
+  if (!d.build_next) {  // the last block iteration builds the candidate only
+    lsq_tail(nullptr);
+    return;
+  }
   // ---- round-0 products V_0^T cand[:,1:] (sstep.hpp:341)
   r0_products();
   grid.sync();
@@ -981,16 +1174,21 @@ __global__ void __launch_bounds__(ORTH_NT, 1) k_arn_step(const __grid_constant__
     }
     cross_block(std::false_type{}, K, d.dwb, 0);
     grid.sync();
+    orth_mark(d, 4);
+    if (blockIdx.x == 0) reduce_dots_dev(d.partials, G, d.dwb, S * S, tc);  // (ends with a barrier)
+    lsq_tail(tc);
+  } else {
+    orth_mark(d, 4);
+    lsq_tail(prod + K * S * S);  // W of the candidate, reduced with the cross products
   }
-  orth_mark(d, 4);
-  // (push_block of this candidate: at the start of the next block iteration)
   orth_mark(d, 5);
 }
 
-size_t orth_smem(int s, int k, int64_t P) {
+// (the candidate slice area doubles as the least-squares tail's scratch)
+size_t orth_smem(int s, int k, int m, int64_t P) {
   return sizeof(double) * (64 + kStepH + (size_t)orth_prod_cap(k, s)) + sizeof(Gram) * (1 + (size_t)k) +
          sizeof(double) * (ORTH_NT / 32) * (s * s + s) +
-         sizeof(double) * (size_t)std::min(s - 1, kOrthSmemCols) * (size_t)P;
+         sizeof(double) * std::max((size_t)std::min(s - 1, kOrthSmemCols) * (size_t)P, (size_t)arn_lsq_scratch(s, m));
 }
 
 // ghost-row buffer sizes (doubles) of the row-streamed powers for slices of P points, or
@@ -1018,9 +1216,8 @@ bool stream_powers_ghosts(const DevOp& op, int s, int64_t n, int64_t P, int G, i
 
 template <int S>
 void run_orth(Ctx& c, const OrthDesc& d, int G, size_t smem) {
-  static bool attr = false;
   // (227 KB per block less the kernel's static shared memory)
-  if (!attr) CK(cudaFuncSetAttribute(k_arn_step<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, 226 * 1024)), attr = true;
+  ensure_smem(k_arn_step<S>, 226 * 1024);
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = G;
   cfg.blockDim = ORTH_NT;
@@ -1047,21 +1244,55 @@ __global__ void k_arn_rn(ArnState* st, const double* partials, int G, int dRR, d
 
 // ---------------------------------------------------------------- standard GMRES pieces
 struct GmState {
-  int status;  // 0 running, 1 happy breakdown
+  int status;  // 0 running, 1 happy breakdown, 2 rho <= tol
   int halt;
   int step;
-  int pad;
+  int fin;     // back substitution: 1 ok, 2 rank-deficient
   double rn;
 };
 
-__global__ void k_gm_start(GmState* st, double* coef, int cInv) {
+// cycle start: q_0 scale and HessenbergLsq(rn) (solvers.hpp:311-318)
+__global__ void k_gm_start(GmState* st, double* coef, int cInv, void* lsq, int M) {
   SKC_PDL_ENTRY();
   if (threadIdx.x == 0) {
     st->status = 0;
     st->halt = 0;
     st->step = 0;
+    st->fin = 0;
     coef[cInv] = 1.0 / st->rn;
+    lsq_reset(lsq_view(lsq, M), st->rn);
   }
+}
+
+// inner step j's least-squares column (solvers.hpp:322-335): append H[:, j] (rows 0..j) to the
+// Givens QR; rho <= tol ends the cycle (after a happy breakdown the column still counts)
+__global__ void k_gm_lsq(GmState* st, double* col, int j, void* lsq, int M, double tol) {
+  SKC_PDL_ENTRY();
+  if (threadIdx.x != 0) return;
+  const bool happy = st->status == 1 && st->step == j;
+  if (st->halt && !happy) return;
+  const LsqView v = lsq_view(lsq, M);
+  const double rho = lsq_append_serial(v, col);  // (rotated in place; col[j + 1] keeps the flag)
+  if (!happy && rho <= tol) {
+    st->status = 2;
+    st->step = j;
+    st->halt = 1;
+  }
+}
+
+// end of the cycle: y (back substitution, solvers.hpp:336-343) into the update coefficients,
+// zero past the appended columns; a rank failure leaves y = 0 (x untouched) and fin = 2
+__global__ void k_gm_finish(GmState* st, void* lsq, int M, double* ycoef, int nterm) {
+  SKC_PDL_ENTRY();
+  if (threadIdx.x != 0) return;
+  for (int i = 0; i < nterm; ++i) ycoef[i] = 0.0;
+  const LsqView v = lsq_view(lsq, M);
+  if (!lsq_solve(v, false)) {
+    st->fin = 2;
+    return;
+  }
+  for (int i = 0; i < v.h->cols && i < nterm; ++i) ycoef[i] = v.y[i];
+  st->fin = 1;
 }
 
 // col_i = q_i . w ; coefficient -col_i for the MGS update (solvers.hpp:94-97)
@@ -1130,6 +1361,7 @@ void gmres_device(Ctx& c, const Op& op, const double* f, double* x, uint64_t m64
   const int rstride = m + 3;
   double* cols = (double*)c.workspace("gm_cols", (size_t)(m + 1) * rstride * sizeof(double));
   GmState* st = (GmState*)c.workspace("gm_state", sizeof(GmState));
+  void* lsq = c.workspace("gm_lsq", lsq_bytes(m));
   const int* halt = &st->halt;
   {
     double hc[3] = {0.0, 0.0, -1.0};
@@ -1137,7 +1369,7 @@ void gmres_device(Ctx& c, const Op& op, const double* f, double* x, uint64_t m64
     GmState h{};
     CK(cudaMemcpyAsync(st, &h, sizeof h, cudaMemcpyHostToDevice, c.stream));
   }
-  auto residual = [&](bool x_zero) {
+  auto enqueue_residual = [&](bool x_zero) {
     LinBuilder lb;
     if (!x_zero) {
       launch_apply(c, op.d, x, ax, nullptr, nullptr);
@@ -1150,14 +1382,14 @@ void gmres_device(Ctx& c, const Op& op, const double* f, double* x, uint64_t m64
     lb.launch(c, g, coef, ncoef, partials, 0, nullptr, nullptr, "residual");
     launch_k(c, k_gm_rn, 1, 256, 0, st, partials, c.reduce_point(partials, g.G, 0, 1), 0);
     ++c.launches;
-    GmState h;
-    CK(cudaMemcpyAsync(&h, st, sizeof h, cudaMemcpyDeviceToHost, c.stream));
-    c.sync();
-    return h.rn;
   };
   const bool x_zero = device_is_zero(c, x, n);
   if (!x_zero) add(cnt, 0, 1, 1);
-  double rn = residual(x_zero);
+  enqueue_residual(x_zero);
+  GmState hs;
+  CK(cudaMemcpyAsync(&hs, st, sizeof hs, cudaMemcpyDeviceToHost, c.stream));
+  c.sync();
+  double rn = hs.rn;
   cnt.termination_dots += 1;
   rep.history.push_back(rn);
   rep.op_history.push_back(cnt);
@@ -1165,7 +1397,7 @@ void gmres_device(Ctx& c, const Op& op, const double* f, double* x, uint64_t m64
   while (rn > tol && rep.iterations < max_iterations) {
     const int steps = (int)std::min<uint64_t>((uint64_t)m, max_iterations - rep.iterations);
     CK(cudaMemsetAsync(cols, 0, (size_t)(m + 1) * rstride * sizeof(double), c.stream));
-    launch_k(c, k_gm_start, 1, 32, 0, st, coef, cInv);
+    launch_k(c, k_gm_start, 1, 32, 0, st, coef, cInv, lsq, m);
     ++c.launches;
     {
       LinBuilder lb;  // q_0 = r / ||r||
@@ -1195,46 +1427,43 @@ void gmres_device(Ctx& c, const Op& op, const double* f, double* x, uint64_t m64
       LinBuilder lb;
       lb.add_out(q(j), w, cInv);
       lb.launch(c, g, coef, ncoef, partials, 0, halt, nullptr, "scale");
+      launch_k(c, k_gm_lsq, 1, 32, 0, st, col, j, lsq, m, tol);
+      ++c.launches;
     }
-    CK(cudaGetLastError());
-    CK(cudaMemcpyAsync(hcols.data(), cols, hcols.size() * sizeof(double), cudaMemcpyDeviceToHost, c.stream));
-    c.sync();
-    // host: the reference's inner loop on the recorded columns
-    add(cnt, 0, 0, 1);  // q1 scaling
-    HessLsq lsq(rn);
-    bool happy = false;
-    int inner = 0;
-    for (int j = 1; j <= steps; ++j) {
-      const double* col = hcols.data() + (size_t)j * rstride;
-      const bool hp = col[j + 1] != 0.0;
-      add(cnt, (uint64_t)j + 1, 1, (uint64_t)j + (hp ? 0 : 1));
-      ++inner;
-      ++rep.iterations;
-      const double rho = lsq.append_column(std::vector<double>(col, col + j + 1));
-      if (hp) {
-        happy = true;
-        break;
-      }
-      if (rho <= tol) break;
-    }
-    std::vector<double> y;
-    try {
-      y = lsq.solve();
-    } catch (const Error& e) {
-      rep.breakdown = e.msg;
-      break;
-    }
-    CK(cudaMemcpyAsync(coef + cY, y.data(), y.size() * sizeof(double), cudaMemcpyHostToDevice, c.stream));
+    // y, x += sum y_i q_i over the cycle's columns (zero past the appended ones), r = f - A x
+    launch_k(c, k_gm_finish, 1, 32, 0, st, lsq, m, coef + cY, steps);
+    ++c.launches;
     {
-      LinBuilder lb;  // x += sum y_i q_i
+      LinBuilder lb;
       lb.add_out(x, x);
-      for (size_t i = 0; i < y.size(); ++i) lb.add_term(q((int)i), 1u, cY + (int)i);
+      for (int i = 0; i < steps; ++i) lb.add_term(q(i), 1u, cY + i);
       lb.launch(c, g, coef, ncoef, partials, 0, nullptr, nullptr, "x_update");
     }
-    add(cnt, 0, 0, y.size());
+    enqueue_residual(false);
+    CK(cudaGetLastError());
+    LsqHdr lh;
+    CK(cudaMemcpyAsync(hcols.data(), cols, hcols.size() * sizeof(double), cudaMemcpyDeviceToHost, c.stream));
+    CK(cudaMemcpyAsync(&hs, st, sizeof hs, cudaMemcpyDeviceToHost, c.stream));
+    CK(cudaMemcpyAsync(&lh, lsq, sizeof lh, cudaMemcpyDeviceToHost, c.stream));
+    c.sync();
+    // replay the reference's inner loop on the device's decisions
+    add(cnt, 0, 0, 1);  // q1 scaling
+    bool happy = false;
+    const int inner = lh.cols;
+    for (int j = 1; j <= inner; ++j) {
+      const bool hp = hcols[(size_t)j * rstride + j + 1] != 0.0;
+      add(cnt, (uint64_t)j + 1, 1, (uint64_t)j + (hp ? 0 : 1));
+      ++rep.iterations;
+      if (hp) happy = true;
+    }
+    if (hs.fin != 1) {
+      rep.breakdown = "hessenberg lsq: rank-deficient R diagonal at column " + std::to_string(lh.rank_col);
+      break;
+    }
+    add(cnt, 0, 0, (uint64_t)inner);
     add(cnt, 0, 1, 1);
     ++rep.cycles;
-    rn = residual(false);
+    rn = hs.rn;
     cnt.termination_dots += 1;
     rep.history.push_back(rn);
     if (inner == m && !happy) rep.op_history.push_back(cnt);
@@ -1249,6 +1478,21 @@ void gmres_device(Ctx& c, const Op& op, const double* f, double* x, uint64_t m64
 
 // ============================================================================ s-step Arnoldi engine
 namespace {
+
+// f(std::integral_constant<int, s>) for the block width s = 1..8
+template <class F>
+void dispatch_s(int s, F&& f) {
+  switch (s) {
+    case 1: f(std::integral_constant<int, 1>{}); break;
+    case 2: f(std::integral_constant<int, 2>{}); break;
+    case 3: f(std::integral_constant<int, 3>{}); break;
+    case 4: f(std::integral_constant<int, 4>{}); break;
+    case 5: f(std::integral_constant<int, 5>{}); break;
+    case 6: f(std::integral_constant<int, 6>{}); break;
+    case 7: f(std::integral_constant<int, 7>{}); break;
+    default: f(std::integral_constant<int, 8>{}); break;
+  }
+}
 
 struct Engine {
   Ctx& c;
@@ -1269,6 +1513,9 @@ struct Engine {
   Gram* grams;
   ArnState* st;
   const int* halt;
+  ArnLsqDesc lq{};      // least-squares state of the cycle (tol set per solve)
+  const double* fvec = nullptr;  // the solve's right-hand side and iterate (device)
+  double* xvec = nullptr;
   bool zfused = false;  // the next block iteration's z and Scalar1 products are already computed
   // across GPUs the reorthogonalization decision is read back after the test (one stream sync
   // per block iteration), so a skipped second pass spends no collective and no halo exchange:
@@ -1293,7 +1540,7 @@ struct Engine {
   int64_t orth_points() const {
     if (!c.orth || c.world() != 1 || s < 2 || op.d.kind == kIlu0) return 0;
     const int64_t P = ((op.n + c.sm_count - 1) / c.sm_count + 1) & ~(int64_t)1;
-    return orth_smem(s, m, P) <= kOrthSmemCap ? P : 0;
+    return orth_smem(s, m, m, P) <= kOrthSmemCap ? P : 0;
   }
 
   // block iteration k (z, Scalar1, seed, nu, candidate block, block MGS, reorthogonalization,
@@ -1326,7 +1573,7 @@ struct Engine {
     d.dwb = dl.Wb();
     d.grams = grams;
     d.rec = recp(k);
-    d.rec_push = recp(k - 1);
+    d.lsq = lq;
     d.rec_t = rl.t();
     d.rec_h = rl.h();
     d.st = st;
@@ -1339,12 +1586,13 @@ struct Engine {
     d.g1 = d.spow ? g1 : 0;
     d.g2 = d.spow ? g2 : 0;
     if (d.spow) d.ghosts = (double*)c.workspace("orth_ghosts", sizeof(double) * (size_t)G * (g1 + g2));
-    const size_t smem = orth_smem(s, k, d.P);
-    // algorithmic bytes: z, Scalar1 products, seed, the powers, round-0 products, pass 0 of the
-    // MGS and the cross products (the data-dependent second pass is not counted)
+    const size_t smem = orth_smem(s, k, m, d.P);
+    // algorithmic bytes, SURVEY 8(d) model (block-CGS-equivalent passes): a block step k < m
+    // moves SpMV(2) + V^T z (ks+1) + seed (ks+2) + MPK (s+1) + V^T cand (ks+s) +
+    // update/cross/Gram (ks+2s-1) = 4ks+4s+5 vectors, the last one (no build) 2ms+s+6.  The
+    // implementation's block-MGS rounds and reorthogonalization pass are its own cost.
     const double ks = (double)k * s;
-    const double bytes = 8.0 * (double)op.n *
-                         (2 + (ks + 1) + (ks + 2) + 3.0 * s + (build_next ? (2.0 * k - 1.0) * s + ks + (k + 1) + (s - 1) : 0.0));
+    const double bytes = 8.0 * (double)op.n * (build_next ? 4.0 * ks + 4.0 * s + 5.0 : 2.0 * ks + s + 6.0);
     Launch lh(c, "arn_step", bytes);
     switch (s) {
       case 2: run_orth<2>(c, d, G, smem); break;
@@ -1389,9 +1637,11 @@ struct Engine {
   void enqueue_cycle_direct() {
     ctor(r, true);
     for (int k = 1; k <= m; ++k) advance(k, k < m);
+    enqueue_finish(fvec, xvec);
   }
 
-  // ctor(r) + the m block iterations of one restart cycle
+  // ctor(r) + the m block iterations of one restart cycle + its least-squares end, x update and
+  // residual (the cycle's f and x are fixed for the solve: fvec, xvec)
   void enqueue_cycle() {
     static const bool graphs = [] {
       const char* e = std::getenv("SKC_GRAPH");
@@ -1425,7 +1675,7 @@ struct Engine {
     c.launches += cycle_launches;
   }
 
-  Engine(Ctx& ctx, const Op& o, int s_, int m_)
+  Engine(Ctx& ctx, const Op& o, int s_, int m_, bool fixed = false)
       : c(ctx), op(o), s(s_), m(m_), rl{s_, m_}, cl{s_, m_}, dl{s_, m_} {
     g = make_geo(op.n, c.sm_count);
     np = pad_n(op.n);
@@ -1443,10 +1693,25 @@ struct Engine {
     grams = (Gram*)c.workspace("arn_grams", (size_t)(m + 1) * sizeof(Gram));
     st = (ArnState*)c.workspace("arn_state", sizeof(ArnState));
     halt = &st->halt;
+    lq.s = s;
+    lq.m = m;
+    lq.GL = arn_lsq_ld(s, m);
+    lq.lsq_on = 1;
+    lq.tol = 0.0;
+    lq.gcols = (double*)c.workspace("arn_gcols", (size_t)m * s * lq.GL * sizeof(double));
+    lq.lblk = (double*)c.workspace("arn_lblk", (size_t)(m + 1) * s * s * sizeof(double));
+    lq.lsq = c.workspace("arn_lsq", lsq_bytes(m * s));
+    lq.rec = rec;
+    lq.recsz = rl.size();
+    lq.rec_t = rl.t();
+    lq.rec_h = rl.h();
+    lq.st = st;
+    lq.grams = grams;
     std::vector<double> hc(cl.size(), 0.0);
     hc[cl.M1()] = -1.0;
     CK(cudaMemcpyAsync(coef, hc.data(), hc.size() * sizeof(double), cudaMemcpyHostToDevice, c.stream));
     ArnState h{};
+    h.fixed = fixed ? 1 : 0;
     CK(cudaMemcpyAsync(st, &h, sizeof h, cudaMemcpyHostToDevice, c.stream));
   }
 
@@ -1508,9 +1773,53 @@ struct Engine {
     ++c.launches;
     krylov_into(0, v);
     gram_self_into(0, dl.Wa(), nullptr);
-    launch_k(c, k_arn_push, 1, 256, 0, st, grams, 0, recp(0), partials, c.reduce_point(partials, g.G, dl.Wa(), s * s), dl.Wa(), dl.Wb(), s);
+    const int Gw = c.reduce_point(partials, g.G, dl.Wa(), s * s);
+    dispatch_s(s, [&](auto S_) {
+      constexpr int S = decltype(S_)::value;
+      launch_k(c, k_arn_ctor_push<S>, 1, 256, 0, lq, (const double*)partials, Gw, dl.Wa());
+    });
     ++c.launches;
     CK(cudaGetLastError());
+  }
+
+  // per-round path: push_block + least squares of block step k (k_arn_lsq)
+  void lsq_step(int k, bool build_next, int Gw, int dWa) {
+    const size_t smem = sizeof(double) * (kMaxS * kMaxS + (size_t)arn_lsq_scratch(s, m));
+    dispatch_s(s, [&](auto S_) {
+      constexpr int S = decltype(S_)::value;
+      ensure_smem(k_arn_lsq<S>, smem);
+      launch_k(c, k_arn_lsq<S>, 1, 256, smem, lq, k, build_next ? 1 : 0, (const double*)partials, Gw, dWa, dl.Wb());
+    });
+    ++c.launches;
+  }
+
+  // end of the cycle on the device: y (k_arn_finish), x += V y over the m blocks (zero
+  // coefficients past the appended columns), r = f - A x and ||r|| (st->rn, rn_out)
+  void enqueue_finish(const double* f, double* x) {
+    launch_k(c, k_arn_finish, 1, 256, 0, lq, coef + cl.Y());
+    ++c.launches;
+    LinBuilder lb;
+    lb.add_out(x, x);
+    for (int bi = 0; bi < m; ++bi)
+      for (int lc = 0; lc < s; ++lc) lb.add_term(col(bi, lc), 1u, cl.Y() + bi * s + lc);
+    lb.launch(c, g, coef, cl.size(), partials, 0, nullptr, nullptr, "x_update");
+    enqueue_residual(f, x, false);
+  }
+
+  // r = f - A x (or f when x is known zero), ||r|| -> st->rn and rn_out
+  void enqueue_residual(const double* f, const double* x, bool x_zero) {
+    LinBuilder lb;
+    if (!x_zero) {
+      launch_apply(c, op.d, x, ax, nullptr, nullptr);
+      lb.add_out(r, f);
+      lb.add_term(ax, 1u, cl.M1());
+    } else {
+      lb.add_out(r, f);
+    }
+    lb.add_dot(0, 0);
+    lb.launch(c, g, coef, cl.size(), partials, dl.RR(), nullptr, nullptr, "residual");
+    launch_k(c, k_arn_rn, 1, 256, 0, st, partials, c.reduce_point(partials, g.G, dl.RR(), 1), dl.RR(), rn_out);
+    ++c.launches;
   }
 
   // SStepArnoldi::advance for block iteration k (1-based), sstep.hpp:297-379
@@ -1551,6 +1860,7 @@ struct Engine {
     const int cb = k;  // block slot k (slot m is scratch when k == m)
     const int Gfused = krylov_into(cb, seed, build_next && s > 1);
     if (!build_next) {
+      lsq_step(k, false, 0, 0);
       CK(cudaGetLastError());
       return;
     }
@@ -1628,8 +1938,7 @@ struct Engine {
     // (for s > 1 the dWa region was already made global together with the cross products)
     const int Gw = s > 1 ? (wb_needed ? c.reduce_point(partials, g.G, dl.Wb(), s * s) : c.world())
                          : c.reduce_point(partials, g.G, dWa, s * s);
-    launch_k(c, k_arn_push, 1, 256, 0, st, grams, cb, rk, partials, Gw, dWa, dl.Wb(), s);
-    ++c.launches;
+    lsq_step(k, true, Gw, dWa);
     CK(cudaGetLastError());
   }
 
@@ -1641,42 +1950,14 @@ struct Engine {
   }
 };
 
-// Host mirror of the engine bookkeeping that the reference keeps (tcoeffs_, gcols_) and the
-// op counts of each advance (sstep.hpp:297-379).
+// Host view of the cycle's device records: the op counts of each advance (sstep.hpp:297-379)
+// and the recorded Gram matrices -- bookkeeping only, no arithmetic on the solve's numbers.
 struct HostArn {
   int s, m;
   RecLayout rl;
   std::vector<double> recs;  // copied records
-  std::vector<std::vector<double>> gcols;
 
   const double* rec(int k) const { return recs.data() + (size_t)k * rl.size(); }
-  double tco(int q, int i, int l, int c) const { return rec(q)[rl.t() + i * s * s + l * s + c]; }
-
-  // append_g_columns (sstep.hpp:422-445); tcoeffs_[q] = records of block iteration q (q>=1)
-  void append_g(int k) {
-    const int q = k - 1;
-    const double* rk = rec(k);
-    for (int cloc = 0; cloc + 1 < s; ++cloc) {
-      std::vector<double> col((size_t)q * s + cloc + 2, 0.0);
-      col[(size_t)q * s + cloc + 1] += 1.0;
-      const int ntq = q;  // block q was orthogonalized against blocks 0..q-1
-      for (int i = 0; i < ntq; ++i) {
-        for (int l = 0; l < s; ++l) col[(size_t)i * s + l] += tco(q, i, l, cloc + 1);
-        for (int lc = 0; lc < s; ++lc) {
-          const double coefv = tco(q, i, lc, cloc);
-          if (coefv == 0.0) continue;
-          const auto& prev = gcols[(size_t)i * s + lc];
-          for (size_t row = 0; row < prev.size(); ++row) col[row] -= coefv * prev[row];
-        }
-      }
-      gcols.push_back(std::move(col));
-    }
-    std::vector<double> last((size_t)k * s + 1, 0.0);
-    for (int i = 0; i < k; ++i)
-      for (int l = 0; l < s; ++l) last[(size_t)i * s + l] = rk[rl.h() + i * s + l];
-    last[(size_t)k * s] = rk[RecLayout::kNu];
-    gcols.push_back(std::move(last));
-  }
 
   std::vector<double> W(int k) const {
     const double* r = rec(k);
@@ -1722,31 +2003,23 @@ void sgmres_device(Ctx& c, const Op& op, const double* f, double* x, const SStep
   const int s = (int)cfg.s, m = (int)cfg.m;
   skc_op_counter& cnt = rep.op_counts;
   cnt.stored_vectors = (uint64_t)(m + 2) * s + 2;
-  Engine E(c, op, s, m);
-  HostArn H{s, m, E.rl, {}, {}};
+  Engine E(c, op, s, m, cfg.fixed_steps);
+  E.lq.tol = cfg.tol;
+  E.fvec = f;
+  E.xvec = x;
+  HostArn H{s, m, E.rl, {}};
   H.recs.resize((size_t)(m + 1) * E.rl.size());
 
-  const bool x_zero = device_is_zero(c, x, op.n);
-  auto residual = [&](bool xz) {
-    LinBuilder lb;
-    if (!xz) {
-      launch_apply(c, op.d, x, E.ax, nullptr, nullptr);
-      lb.add_out(E.r, f);
-      lb.add_term(E.ax, 1u, E.cl.M1());
-    } else {
-      lb.add_out(E.r, f);
-    }
-    lb.add_dot(0, 0);
-    lb.launch(c, E.g, E.coef, E.cl.size(), E.partials, E.dl.RR(), nullptr, nullptr, "residual");
-    launch_k(c, k_arn_rn, 1, 256, 0, E.st, E.partials, c.reduce_point(E.partials, E.g.G, E.dl.RR(), 1), E.dl.RR(), E.rn_out);
-    ++c.launches;
+  auto read_rn = [&]() {
     double h;
     CK(cudaMemcpyAsync(&h, E.rn_out, sizeof h, cudaMemcpyDeviceToHost, c.stream));
     c.sync();
     return h;
   };
+  const bool x_zero = device_is_zero(c, x, op.n);
   if (!x_zero) add(cnt, 0, 1, 1);
-  double rn = residual(x_zero);
+  E.enqueue_residual(f, x, x_zero);
+  double rn = read_rn();
   cnt.termination_dots += 1;
   rep.history.push_back(rn);
   rep.op_history.push_back(cnt);
@@ -1764,7 +2037,8 @@ void sgmres_device(Ctx& c, const Op& op, const double* f, double* x, const SStep
     cnt.termination_dots += sub.op_counts.termination_dots;
     for (size_t i = 1; i < sub.history.size(); ++i) rep.history.push_back(sub.history[i]);
     add(cnt, 0, 1, 1);
-    rn = residual(false);
+    E.enqueue_residual(f, x, false);
+    rn = read_rn();
     cnt.termination_dots += 1;
     rep.op_history.push_back(cnt);
     return rn <= cfg.tol;
@@ -1774,11 +2048,17 @@ void sgmres_device(Ctx& c, const Op& op, const double* f, double* x, const SStep
     bool collapsed = false, exhausted = false;
     std::string collapse_msg;
     int blocks_done = 0;
-    // ---- enqueue the whole cycle, then read it back
+    // ---- the whole cycle on the device (one graph), then one read-back
     E.enqueue_cycle();
-    ArnState hs = E.read_state();
-    CK(cudaMemcpy(H.recs.data(), E.rec, H.recs.size() * sizeof(double), cudaMemcpyDeviceToHost));
-    H.gcols.clear();
+    ArnState hs;
+    LsqHdr lh;
+    double cycle_rn = 0.0;
+    CK(cudaMemcpyAsync(&hs, E.st, sizeof hs, cudaMemcpyDeviceToHost, c.stream));
+    CK(cudaMemcpyAsync(&lh, E.lq.lsq, sizeof lh, cudaMemcpyDeviceToHost, c.stream));
+    CK(cudaMemcpyAsync(&cycle_rn, E.rn_out, sizeof cycle_rn, cudaMemcpyDeviceToHost, c.stream));
+    CK(cudaMemcpyAsync(H.recs.data(), E.rec, H.recs.size() * sizeof(double), cudaMemcpyDeviceToHost, c.stream));
+    c.sync();
+    // ---- replay the reference's cycle loop (sstep.hpp:546-654) on the device's decisions
     if (hs.status == kArnCtorZero) fail(SKC_EINVAL, "s-arnoldi: start vector is zero");
     add(cnt, (uint64_t)s * (s + 1) / 2, (uint64_t)s - 1, 1);  // ctor: scale, krylov_block, push
     if (hs.status == kArnCtorCollapse) {
@@ -1789,60 +2069,33 @@ void sgmres_device(Ctx& c, const Op& op, const double* f, double* x, const SStep
       }
       break;
     }
-    std::vector<std::vector<double>> lblocks;
-    {
-      std::vector<double> L0(s * s);
-      if (!cholesky_upper(H.W(0).data(), s, L0.data())) fail(SKC_EBREAKDOWN, "cholesky: matrix not positive definite");
-      lblocks.push_back(L0);
-    }
-    HessLsq lsq(rn * lblocks[0][0]);
-    auto apply_l = [&](const std::vector<double>& gv) {  // sstep.hpp:566-579
-      std::vector<double> out(gv);
-      for (size_t bi = 0; bi < lblocks.size() && bi * s < gv.size(); ++bi) {
-        const std::vector<double>& lb = lblocks[bi];
-        const size_t off = bi * s;
-        for (size_t rl = 0; rl < (size_t)s && off + rl < gv.size(); ++rl) {
-          double acc = 0.0;
-          for (size_t jl = rl; jl < (size_t)s && off + jl < gv.size(); ++jl) acc += lb[rl * s + jl] * gv[off + jl];
-          out[off + rl] = acc;
-        }
-      }
-      return out;
-    };
+    // (cholesky_upper of block 0 escapes sgmres_solve in the reference, sstep.hpp:563)
+    if (hs.status == kArnCtorChol) fail(SKC_EBREAKDOWN, "cholesky: matrix not positive definite");
     for (int k = 1; k <= m; ++k) {
       const bool stopped_here = hs.status != kArnRunning && hs.block == k;
       const bool invariant = stopped_here && hs.status == kArnInvariant;
-      const bool push_fail = stopped_here && hs.status == kArnPushCollapse;
       H.count_advance(cnt, k, k < m, invariant ? 1 : 0);
-      H.append_g(k);
-      if (push_fail) {
+      if (stopped_here && hs.status == kArnPushCollapse) {
         collapsed = true;
         collapse_msg = gram_message((int)H.rec(k)[RecLayout::kSing], H.rec(k)[RecLayout::kRatio]);
         break;
       }
-      const bool more = !invariant;
-      if (k < m && more) {
-        std::vector<double> Lk(s * s);
-        if (!cholesky_upper(H.W(k).data(), s, Lk.data())) {
-          collapsed = true;
-          collapse_msg = "cholesky: matrix not positive definite";
-          break;
-        }
-        lblocks.push_back(Lk);
+      if (stopped_here && hs.status == kArnCholCollapse) {
+        collapsed = true;
+        collapse_msg = "cholesky: matrix not positive definite";
+        break;
       }
-      double rho = lsq.residual_norm();
-      for (int lc = 0; lc < s; ++lc) rho = lsq.append_column(apply_l(H.gcols[(size_t)(k - 1) * s + lc]));
+      const double rho = H.rec(k)[RecLayout::kRho];
       rep.block_rho.push_back(rho);
       rep.iterations += s;
       blocks_done = k;
-      if (!more) {
+      if (invariant) {
         exhausted = true;
         break;
       }
-      if (rho <= cfg.tol) break;
+      if (rho <= cfg.tol) break;  // (the device stopped the cycle here: kArnEarly)
     }
-    const bool attainable = lsq.columns() > 0 && lsq.residual_norm() <= cfg.tol;
-    if (collapsed && !attainable) {
+    if (hs.fin == kFinFallback) {  // collapsed, residual estimate above tol: x untouched
       if (!run_fallback()) {
         if (rep.iterations >= cfg.max_iterations) {
           rep.breakdown = "basis collapse (" + collapse_msg + ")";
@@ -1852,26 +2105,15 @@ void sgmres_device(Ctx& c, const Op& op, const double* f, double* x, const SStep
       }
       break;
     }
-    std::vector<double> y;
-    try {
-      y = lsq.solve();
-    } catch (const Error& e) {
-      rep.breakdown = e.msg;
+    if (hs.fin == kFinLsqFail) {  // x untouched (y = 0)
+      rep.breakdown = "hessenberg lsq: rank-deficient R diagonal at column " + std::to_string(lh.rank_col);
       break;
     }
-    // x += sum_bi sum_lc y V ; r = f - A x (sstep.hpp:622-633)
-    CK(cudaMemcpyAsync(E.coef + E.cl.Y(), y.data(), y.size() * sizeof(double), cudaMemcpyHostToDevice, c.stream));
-    {
-      LinBuilder lb;
-      lb.add_out(x, x);
-      for (int bi = 0; bi < blocks_done; ++bi)
-        for (int lc = 0; lc < s; ++lc) lb.add_term(E.col(bi, lc), 1u, E.cl.Y() + bi * s + lc);
-      lb.launch(c, E.g, E.coef, E.cl.size(), E.partials, 0, nullptr, nullptr, "x_update");
-    }
+    // x += sum_bi sum_lc y V ; r = f - A x (sstep.hpp:622-633), done on the device
     add(cnt, 0, 0, (uint64_t)blocks_done * s);
     add(cnt, 0, 1, 1);
     ++rep.cycles;
-    rn = residual(false);
+    rn = cycle_rn;
     cnt.termination_dots += 1;
     rep.history.push_back(rn);
     if (blocks_done == m && !exhausted && !collapsed) rep.op_history.push_back(cnt);
@@ -1905,7 +2147,8 @@ void sarnoldi_device(Ctx& c, const Op& op, const double* v1, uint64_t s64, uint6
   require(m64 <= 64, "sarnoldi: m_blocks above the device limit of 64");
   const int s = (int)s64, m = (int)m64;
   Engine E(c, op, s, m);
-  HostArn H{s, m, E.rl, {}, {}};
+  E.lq.lsq_on = 0;  // the basis and its Hessenberg columns only
+  HostArn H{s, m, E.rl, {}};
   H.recs.resize((size_t)(m + 1) * E.rl.size());
   E.ctor(v1, false);
   for (int k = 1; k <= m; ++k) E.advance(k, k < m);
@@ -1927,9 +2170,8 @@ void sarnoldi_device(Ctx& c, const Op& op, const double* v1, uint64_t s64, uint6
       fail(SKC_EBREAKDOWN, "sarnoldi: invariant subspace at block " + std::to_string(k));
     }
     H.count_advance(cnt, k, k < m, 0);
-    H.append_g(k);
   }
-  const size_t n = (size_t)op.n, np = E.np;
+  const size_t n = (size_t)op.n;
   out.blocks.assign((size_t)m * s * n, 0.0);
   for (int b = 0; b < m; ++b)
     for (int j = 0; j < s; ++j)
@@ -1940,14 +2182,16 @@ void sarnoldi_device(Ctx& c, const Op& op, const double* v1, uint64_t s64, uint6
     const auto w = H.W(b);
     std::copy(w.begin(), w.end(), out.grams.begin() + (size_t)b * s * s);
   }
-  const size_t rows = (size_t)(m + 1) * s, cols = (size_t)m * s;
+  // the block Hessenberg matrix (hessenberg(), sstep.hpp:383-389) from the device's columns
+  const size_t rows = (size_t)(m + 1) * s, cols = (size_t)m * s, GL = (size_t)E.lq.GL;
+  std::vector<double> gc(cols * GL);
+  CK(cudaMemcpy(gc.data(), E.lq.gcols, gc.size() * sizeof(double), cudaMemcpyDeviceToHost));
   out.hess.assign(rows * cols, 0.0);
-  for (size_t j = 0; j < H.gcols.size(); ++j)
-    for (size_t i = 0; i < H.gcols[j].size(); ++i) out.hess[i * cols + j] = H.gcols[j][i];
+  for (size_t j = 0; j < cols; ++j)
+    for (size_t i = 0; i < j + 2 && i < rows; ++i) out.hess[i * cols + j] = gc[j * GL + i];
   out.seed.assign(n, 0.0);
   CK(cudaMemcpy(out.seed.data(), E.col(m, 0), n * sizeof(double), cudaMemcpyDeviceToHost));
   out.seed_norm = H.rec(m)[RecLayout::kNu];
-  (void)np;
 }
 
 }  // namespace skc

@@ -236,6 +236,15 @@ inline void launch_k(Ctx& c, void (*kernel)(KArgs...), dim3 grid, dim3 block, si
   CK(cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...));
 }
 
+// Raise a kernel's dynamic shared-memory limit to `bytes` on the current device, once per
+// (kernel, device): the attribute is per device, so a process-wide flag would leave the second
+// GPU of a multi-context process at the 48 KB default.  Thread-safe.
+void ensure_smem_attr(const void* kernel, int bytes);
+template <typename K>
+inline void ensure_smem(K* kernel, size_t bytes) {
+  ensure_smem_attr(reinterpret_cast<const void*>(kernel), (int)bytes);
+}
+
 // RAII launch bracket
 struct Launch {
   Ctx& c;
@@ -312,6 +321,7 @@ struct SStepCfg {
   uint64_t max_iterations = 100000;
   bool precondition = false, unbounded_window = false, debug_checks = false;
   double divergence_factor = 10.0;
+  bool fixed_steps = false;  // benchmark mode: skip the Gram pivot-ratio and LSQ rank aborts
 };
 
 // solver entry points (device pointers f, x)
@@ -328,24 +338,6 @@ struct BasisOut {
 void sarnoldi_device(Ctx& c, const Op& op, const double* v1_dev, uint64_t s, uint64_t m_blocks, BasisOut& out);
 void smr_step_device(Ctx& c, const Op& op, double* x, double* r, uint64_t s, double* coeffs,
                      skc_op_counter* counter);
-
-// host Hessenberg LSQ (small_dense.hpp:239-307), run on the host on device-computed columns
-class HessLsq {
- public:
-  explicit HessLsq(double beta) : rhs_{beta}, residual_(std::fabs(beta)) {}
-  size_t columns() const { return rcols_.size(); }
-  double residual_norm() const { return residual_; }
-  double matrix_norm() const;
-  double append_column(std::vector<double> col);
-  // throws Error{SKC_EBREAKDOWN} on rank deficiency
-  std::vector<double> solve() const;
-
- private:
-  std::vector<std::vector<double>> rcols_;
-  std::vector<double> cos_, sin_, rhs_;
-  double residual_;
-  double gnorm_sq_ = 0.0;
-};
 
 std::string fmt_double(double v);  // std::to_string(double)
 

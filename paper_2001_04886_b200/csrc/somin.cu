@@ -37,7 +37,7 @@ struct SominState {
   int status;
   int halt;
   int singular1;
-  int pad;
+  int fixed;  // fixed-step benchmark mode (gram_bypass_ratio)
   long long iters;
   long long max_iter;
   double tol, divf, r0n, rn, ratio;
@@ -76,6 +76,7 @@ __device__ void somin_factor_solve(SominState* st, Gram* gslot, double* coef, co
                                    int s, int collapse_status) {
   Gram g;
   gram_factor_dev(g, W, s);
+  gram_bypass_ratio(g, st->fixed);
   if (!g.ok) {
     st->status = collapse_status;
     st->halt = 1;
@@ -416,6 +417,7 @@ __global__ void __launch_bounds__(PS_NT) k_somin_persist(const __grid_constant__
           ++u;
         }
       gram_factor_t<S>(gw[nsl], W);
+      gram_bypass_ratio(gw[nsl], d.st->fixed);
       int flag = 0;
       if (!gw[nsl].ok) {
         flag = kIterCollapse;
@@ -579,6 +581,7 @@ void somin_device(Ctx& c, const Op& op, const double* f, double* x, const SStepC
   {
     SominState h{};
     h.max_iter = (long long)cfg.max_iterations;
+    h.fixed = cfg.fixed_steps ? 1 : 0;
     h.tol = cfg.tol;
     h.divf = cfg.divergence_factor;
     CK(cudaMemcpyAsync(st, &h, sizeof h, cudaMemcpyHostToDevice, c.stream));

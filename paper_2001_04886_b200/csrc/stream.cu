@@ -573,14 +573,13 @@ int add_unique(const double** U, int& nu, int cap, const double* p) {
 }
 
 template <class K>
-void allow_smem(K kernel) {
-  CK(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+void allow_smem(K* kernel) {
+  ensure_smem(kernel, 227 * 1024);
 }
 
 template <int NOUT, int MAXD, int PPT, bool SPLIT>
 void launch_upd_t(Ctx& c, const UpdDesc& d, size_t smem, int G) {
-  static bool attr = false;
-  if (!attr) allow_smem(k_upd<NOUT, MAXD, PPT, SPLIT>), attr = true;
+  allow_smem(k_upd<NOUT, MAXD, PPT, SPLIT>);
   launch_k(c, k_upd<NOUT, MAXD, PPT, SPLIT>, G, THREADS, smem, d);
 }
 
@@ -614,8 +613,7 @@ void launch_upd_p(Ctx& c, const UpdDesc& d, size_t smem, int G, int maxd) {
 
 template <int NR, int LB>
 void launch_grm_t(Ctx& c, const GrmDesc& d, size_t smem, int G) {
-  static bool attr = false;
-  if (!attr) allow_smem(k_grm<NR, LB>), attr = true;
+  allow_smem(k_grm<NR, LB>);
   launch_k(c, k_grm<NR, LB>, G, THREADS, smem, d);
 }
 
@@ -637,12 +635,10 @@ void launch_grm_l(Ctx& c, const GrmDesc& d, size_t smem, int G) {
 template <int S, bool DOTS>
 void launch_mgs_t(Ctx& c, const MgsDesc& d, size_t smem, int G) {
   if constexpr (DOTS && S >= 6) {
-    static bool attr = false;
-    if (!attr) allow_smem(k_mgs2<S>), attr = true;
+    allow_smem(k_mgs2<S>);
     launch_k(c, k_mgs2<S>, G, THREADS, smem, d);
   } else {
-    static bool attr = false;
-    if (!attr) allow_smem(k_mgs<S, DOTS>), attr = true;
+    allow_smem(k_mgs<S, DOTS>);
     launch_k(c, k_mgs<S, DOTS>, G, THREADS, smem, d);
   }
 }

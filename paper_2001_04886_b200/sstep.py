@@ -39,10 +39,14 @@ class SStepConfig:
     unbounded_window: bool = False
     debug_checks: bool = False
     divergence_factor: float = 10.0
+    # not in the reference: fixed-step benchmark mode (bypasses only the Gram pivot-ratio and
+    # LSQ rank aborts; results past the reference's stop are meaningless, see skrylov_b200.h)
+    fixed_steps: bool = False
 
     def c(self):
         return _lib.SStepConfigC(self.s, self.k, self.m, self.tol, self.max_iterations, int(self.precondition),
-                                 int(self.unbounded_window), int(self.debug_checks), self.divergence_factor)
+                                 int(self.unbounded_window), int(self.debug_checks), self.divergence_factor,
+                                 int(self.fixed_steps))
 
 
 @dataclass
