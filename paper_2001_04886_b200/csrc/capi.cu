@@ -97,6 +97,7 @@ skc_ctx* make_ctx(int device) {
   if (const char* e = std::getenv("SKC_ZFUSE")) ctx->c.zfuse = std::atoi(e) != 0;
   if (const char* e = std::getenv("SKC_PERSIST")) ctx->c.persist = std::atoi(e) != 0;
   if (const char* e = std::getenv("SKC_SPOW")) ctx->c.spow = std::atoi(e) != 0;
+  if (const char* e = std::getenv("SKC_LSQ_OVERLAP")) ctx->c.lsq_overlap = std::atoi(e) != 0;
   if (const char* e = std::getenv("SKC_ILU_STRIPS")) ctx->c.ilu_strips = std::atoi(e) != 0;
   return ctx;
 }

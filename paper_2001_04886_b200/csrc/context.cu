@@ -141,7 +141,20 @@ Ctx::~Ctx() {
     cudaEventDestroy(p.b);
   }
   if (pinned) cudaFreeHost(pinned);
+  if (aux_stream) {
+    cudaStreamSynchronize(aux_stream);
+    cudaStreamDestroy(aux_stream);
+  }
   if (own_stream) cudaStreamDestroy(own_stream);
+}
+
+cudaStream_t Ctx::aux() {
+  if (!aux_stream) {
+    int lo = 0, hi = 0;
+    CK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+    CK(cudaStreamCreateWithPriority(&aux_stream, cudaStreamNonBlocking, hi));
+  }
+  return aux_stream;
 }
 
 Op::~Op() {

@@ -49,17 +49,24 @@ struct ArnState {
   int zready;  // the last block iteration's cross pass produced the next z and its products
   int fixed;   // fixed-step benchmark mode (gram_bypass_ratio, lsq_solve)
   int fin;     // end-of-cycle outcome (kFin*)
+  // the least-squares stream's verdict on the block steps (kArnRunning, kArnInvariant,
+  // kArnPushCollapse, kArnCholCollapse, kArnEarly) and its step; written only by
+  // k_arn_lsq, which also raises the sticky `halt` so later block steps return at entry
+  int lstatus, lblock;
   int pad;
 };
 
 // record layout per block iteration k (0 = constructor)
+// (W: the pushed Gram matrix as symmetrized by push_block; Wraw: the candidate's raw products,
+// snapshotted at the end of its block step for the least-squares stream)
 struct RecLayout {
   int s, m;
-  __host__ __device__ int size() const { return 10 + s * s + (m + 1) * s + (m + 1) * s * s; }
+  __host__ __device__ int size() const { return 10 + 2 * s * s + (m + 1) * s + (m + 1) * s * s; }
   static constexpr int kZn = 0, kNu = 1, kInv = 2, kReorth = 3, kFirst = 4, kOk = 5, kRatio = 6, kSing = 7,
                        kRho = 8, kW = 10;
-  __host__ __device__ int h() const { return 10 + s * s; }
-  __host__ __device__ int t() const { return 10 + s * s + (m + 1) * s; }
+  __host__ __device__ int wraw() const { return 10 + s * s; }
+  __host__ __device__ int h() const { return 10 + 2 * s * s; }
+  __host__ __device__ int t() const { return 10 + 2 * s * s + (m + 1) * s; }
 };
 
 // coefficient layout
@@ -104,6 +111,8 @@ __global__ void k_arn_ctor(ArnState* st, int use_rn, const double* partials, int
     st->reorth = 0;
     st->zready = 0;
     st->fin = kFinNone;
+    st->lstatus = kArnRunning;
+    st->lblock = 0;
     const double nv = use_rn ? st->rn : sqrt(v[0]);
     rec0[RecLayout::kZn] = nv;
     if (!(nv > 0.0)) {
@@ -145,7 +154,12 @@ __device__ bool arn_push_body(ArnState* st, Gram& g, int k, double* rec, const d
   }
   gram_bypass_ratio(g, st->fixed);
   if (!record) return g.ok;
-  for (int q = 0; q < s * s; ++q) rec[RecLayout::kW + q] = W[q];
+  if constexpr (S > 0) {
+#pragma unroll
+    for (int q = 0; q < S * S; ++q) rec[RecLayout::kW + q] = W[q];
+  } else {
+    for (int q = 0; q < s * s; ++q) rec[RecLayout::kW + q] = W[q];
+  }
   rec[RecLayout::kOk] = g.ok;
   rec[RecLayout::kRatio] = g.ratio;
   rec[RecLayout::kSing] = g.singular1;
@@ -156,6 +170,22 @@ __device__ bool arn_push_body(ArnState* st, Gram& g, int k, double* rec, const d
     return false;
   }
   return true;
+}
+
+// per-round path: push_block of block k from the reduced W products (the reorthogonalized region
+// when the flag says so); the raw products are kept in the record for the least-squares stream
+__global__ void k_arn_push(ArnState* st, Gram* grams, int k, double* rec, int rec_wraw, const double* partials, int G,
+                           int dWa, int dWb, int s) {
+  SKC_PDL_ENTRY();
+  if (arn_skip(st)) return;
+  __shared__ double v[kMaxS * kMaxS];
+  const int dW = st->reorth ? dWb : dWa;
+  reduce_dots_dev(partials, G, dW, s * s, v);
+  if (threadIdx.x == 0) {
+    for (int q = 0; q < s * s; ++q) rec[rec_wraw + q] = v[q];
+    Gram g;
+    if (arn_push_body(st, g, k, rec, v, s)) grams[k] = g;
+  }
 }
 
 // ---------------------------------------------------------------- least squares of the cycle
@@ -170,118 +200,275 @@ struct ArnLsqDesc {
   double* lblk;      // upper Cholesky factor of basis block b's Gram matrix at b s^2
   void* lsq;         // LsqView base, capacity m s
   double* rec;       // records (RecLayout), block iteration k at k * recsz
-  int recsz, rec_t, rec_h;
+  int recsz, rec_t, rec_h, rec_wraw;
   ArnState* st;
   Gram* grams;
+  unsigned long long* trace;  // optional per-phase timestamps (slots 70..75), diagnostics
 };
+__device__ __forceinline__ void lsq_mark(const ArnLsqDesc& d, int slot, int who = 0) {
+  if (d.trace && threadIdx.x == who) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    d.trace[slot] = t;
+  }
+}
 __host__ __device__ inline int arn_lsq_ld(int s, int m) { return m * s + 2; }
-// shared scratch of arn_lsq_step (doubles): the s new columns twice (scaled + a copy for the norm)
-__host__ __device__ inline int arn_lsq_scratch(int s, int m) { return 2 * s * arn_lsq_ld(s, m) + 8; }
+// shared scratch of arn_lsq_step (doubles) without / with the staged earlier Hessenberg columns
+__host__ __device__ inline int arn_lsq_scratch(int s, int m) {
+  const int M = m * s;
+  return 3 * s * arn_lsq_ld(s, m) + (m * s * s) + (M + 1) + (m + 1) * s * s + 2 * (M + s) + 16;
+}
+__host__ __device__ inline int arn_lsq_prev(int s, int m) {
+  const int M = m * s;
+  return M * (M + 3) / 2;
+}
 
-// Block step k's half of the cycle loop (sstep.hpp:582-600), whole CTA:
-//   push_block of the candidate (sstep.hpp:375, 392-399; when it was built: k < m and the seed
-//   did not vanish) from its raw Gram products W, then cholesky_upper of the new Gram block
-//   (sstep.hpp:585); either failing is a basis collapse and appends nothing;
+// Block step k's half of the cycle loop (sstep.hpp:582-600), one whole CTA, on the side stream
+// once block step k has finished (the next block step runs meanwhile):
+//   the push_block decision for the candidate (sstep.hpp:375, 392-399; when it was built: k < m
+//   and the seed did not vanish), recomputed from the snapshotted raw Gram products with the
+//   same arithmetic as the block step kernels' own push (hence the same verdict), then
+//   cholesky_upper of the new Gram block (sstep.hpp:585); either failing is a basis collapse
+//   and appends nothing;
 //   append_g_columns (sstep.hpp:422-445): the s columns of step k from the t coefficients of
 //   block k-1 and this step's h, nu;
 //   apply_l (sstep.hpp:566-579) and the Givens update of each column (lsq.cuh); rho is recorded
-//   and rho <= tol stops the cycle (the next block steps return at entry).
+//   and rho <= tol stops the cycle.
+// Every stop raises the sticky st->halt, so the block steps not yet started return at entry
+// (the one running meanwhile finishes; nothing reads its results).  Latency-bound serial work:
+// every operand is staged into shared memory in one parallel pass, computed there, and
+// written back without waiting.  `cap` = doubles of scratch available.
 template <int S>
-__device__ void arn_lsq_step(const ArnLsqDesc& d, int k, bool build_next, const double* W, double* scratch) {
+__device__ void arn_lsq_step(const ArnLsqDesc& d, int k, bool build_next, double* sm, int cap) {
   __shared__ int s_go, s_nl, s_inv;
-  const int tid = threadIdx.x;
+  __shared__ double s_w[S * S];
+  const int tid = threadIdx.x, nt = blockDim.x;
   double* rk = d.rec + (size_t)k * d.recsz;
+  const int q = k - 1, ld = arn_lsq_ld(S, d.m), j0 = q * S;
+  // scratch: gs | ls | cp [S ld each] | tq [q S^2] | hk [k S + 1] | lb [(k+1) S^2] | cs, sn [j0 + S] | prev
+  double* gs = sm;
+  double* ls = gs + S * ld;
+  double* cp = ls + S * ld;
+  double* tq = cp + S * ld;
+  double* hk = tq + q * S * S;
+  double* lb = hk + k * S + 1;
+  double* ccs = lb + (k + 1) * S * S;
+  double* csn = ccs + j0 + S;
+  double* prev = csn + j0 + S;
+  const int nprev = j0 * (j0 + 3) / 2;  // columns 0..j0-1, column p rows 0..p+1 at p(p+3)/2
+  const bool stage_prev = (int)(prev - sm) + nprev <= cap;
+  const LsqView lv = lsq_view(d.lsq, d.m * S);
+  lsq_mark(d, 70);
   if (tid == 0) {
-    const bool invariant = d.st->status == kArnInvariant && d.st->block == k;
+    const bool invariant = rk[RecLayout::kInv] != 0.0;
     s_inv = invariant;
-    int go = !d.st->halt || invariant, nl = k;
+    int go = d.st->lstatus == kArnRunning, nl = k;
     if (go && build_next && !invariant) {
+#pragma unroll
+      for (int e = 0; e < S * S; ++e) s_w[e] = rk[d.rec_wraw + e];
       Gram g;
-      if (!arn_push_body<S>(d.st, g, k, rk, W, S)) {
+      if (!arn_push_body<S>(d.st, g, k, rk, s_w, S, false)) {
+        d.st->lstatus = kArnPushCollapse;
+        d.st->lblock = k;
+        d.st->halt = 1;
         go = 0;
-      } else {
-        d.grams[k] = g;
-        if (d.lsq_on) {
-          double L[S * S];
-          if (!cholesky_upper(g.w, S, L)) {
-            d.st->status = kArnCholCollapse;
-            d.st->block = k;
-            d.st->halt = 1;
-            go = 0;
-          } else {
-            for (int q = 0; q < S * S; ++q) d.lblk[k * S * S + q] = L[q];
-            nl = k + 1;
-          }
+      } else if (d.lsq_on) {
+        if (!cholesky_upper(g.w, S, lb + k * S * S)) {
+          d.st->lstatus = kArnCholCollapse;
+          d.st->lblock = k;
+          d.st->halt = 1;
+          go = 0;
         }
+        nl = k + 1;
       }
     }
     s_go = go;
     s_nl = nl;
+    lsq_mark(d, 76);
+  } else {
+    // stage the operands (threads 1..): t of block q, h and nu of step k, L blocks 0..k-1,
+    // the stored rotations, the earlier Hessenberg columns -- one combined index space, eight
+    // loads in flight per thread before their shared-memory stores
+    const double* rq = d.rec + (size_t)q * d.recsz + d.rec_t;
+    const int t1 = tid - 1, n1 = nt - 1;
+    const int n_t = q * S * S, n_h = k * S + 1, n_l = d.lsq_on ? k * S * S : 0, n_c = d.lsq_on ? j0 : 0;
+    const int n_p = stage_prev ? nprev : 0;
+    const int o_h = n_t, o_l = o_h + n_h, o_c = o_l + n_l, o_s = o_c + n_c, o_p = o_s + n_c, T = o_p + n_p;
+    auto src = [&](int e) -> const double* {
+      if (e < o_h) return rq + e;
+      if (e < o_l) return e - o_h < k * S ? rk + d.rec_h + (e - o_h) : rk + RecLayout::kNu;
+      if (e < o_c) return d.lblk + (e - o_l);
+      if (e < o_s) return lv.cs + (e - o_c);
+      if (e < o_p) return lv.sn + (e - o_s);
+      const int f = e - o_p;  // -> (column p, row r), p(p+3)/2 <= f
+      int p = (int)((sqrtf(9.0f + 8.0f * (float)f) - 3.0f) * 0.5f);
+      while ((p + 1) * (p + 4) / 2 <= f) ++p;
+      while (p * (p + 3) / 2 > f) --p;
+      return d.gcols + (size_t)p * d.GL + (f - p * (p + 3) / 2);
+    };
+    auto dst = [&](int e) -> double* {
+      if (e < o_h) return tq + e;
+      if (e < o_l) return hk + (e - o_h);
+      if (e < o_c) return lb + (e - o_l);
+      if (e < o_s) return ccs + (e - o_c);
+      if (e < o_p) return csn + (e - o_s);
+      return prev + (e - o_p);
+    };
+    constexpr int U = 8;
+    for (int b = t1; b < T; b += U * n1) {
+      double v[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int e = b + u * n1;
+        v[u] = e < T ? __ldcg(src(e)) : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int e = b + u * n1;
+        if (e < T) *dst(e) = v[u];
+      }
+    }
+    lsq_mark(d, 77, 1);
   }
   __syncthreads();
+  lsq_mark(d, 71);
   if (!s_go) return;
+  if (build_next && !s_inv && d.lsq_on)  // the new L block to global memory
+    for (int e = tid; e < S * S; e += nt) d.lblk[k * S * S + e] = lb[k * S * S + e];
   const bool invariant = s_inv != 0;
-  const int q = k - 1, ld = arn_lsq_ld(S, d.m), nl = s_nl;
-  const double* rq = d.rec + (size_t)q * d.recsz + d.rec_t;  // t coefficients of block q
-  double* gs = scratch;                                       // step k's columns, unscaled
-  for (int e = tid; e < S * ld; e += blockDim.x) {
+  const int nl = s_nl;
+  auto prevv = [&](int p, int r) {
+    return stage_prev ? prev[p * (p + 3) / 2 + r] : d.gcols[(size_t)p * d.GL + r];
+  };
+  // ---- append_g_columns: the s columns of step k (column j = j0 + cl, rows 0..j+1)
+  for (int e = tid; e < S * ld; e += nt) {
     const int cl = e / ld, r = e - cl * ld;
-    const int j = q * S + cl;
+    const int j = j0 + cl;
     if (r >= j + 2) continue;
     double v;
     if (cl + 1 < S) {  // A v_q^cl = v_q^{cl+1} + sum_i V_i T_i[:,cl+1] - sum_i (A V_i) T_i[:,cl]
       v = 0.0;
-      if (r == q * S + cl + 1) v += 1.0;
+      if (r == j0 + cl + 1) v += 1.0;
       for (int i = 0; i < q; ++i) {
-        const double* ti = rq + i * S * S;
+        const double* ti = tq + i * S * S;
         if (r >= i * S && r < i * S + S) v += ti[(r - i * S) * S + cl + 1];
 #pragma unroll
         for (int lc = 0; lc < S; ++lc) {
           const double cf = ti[lc * S + cl];
           if (cf == 0.0) continue;
           const int pj = i * S + lc;  // earlier column, rows 0..pj+1
-          if (r < pj + 2) v -= cf * d.gcols[(size_t)pj * d.GL + r];
+          if (r < pj + 2) v -= cf * prevv(pj, r);
         }
       }
     } else {  // A v_q^{s-1} = nu v_{q+1} + sum_i V_i h_i
-      v = r < k * S ? rk[d.rec_h + r] : rk[RecLayout::kNu];
+      v = hk[r];
     }
-    d.gcols[(size_t)j * d.GL + r] = v;
     gs[e] = v;
+    d.gcols[(size_t)j * d.GL + r] = v;
   }
   if (!d.lsq_on) {
     __syncthreads();
     return;
   }
   __syncthreads();
-  double* ls = scratch + S * ld;  // L-scaled columns
-  for (int e = tid; e < S * ld; e += blockDim.x) {
+  lsq_mark(d, 72);
+  // ---- apply_l: the L-scaled columns (and a copy for the squared norms)
+  for (int e = tid; e < S * ld; e += nt) {
     const int cl = e / ld, r = e - cl * ld;
-    const int len = q * S + cl + 2;
+    const int len = j0 + cl + 2;
     if (r >= len) continue;
     const double* g = gs + cl * ld;
     const int bi = r / S, off = bi * S, rl = r - off;
     double v = g[r];
     if (bi < nl) {
-      const double* lb = d.lblk + bi * S * S;
+      const double* lbb = lb + bi * S * S;
       double acc = 0.0;
-      for (int jl = rl; jl < S && off + jl < len; ++jl) acc += lb[rl * S + jl] * g[off + jl];
+      for (int jl = rl; jl < S && off + jl < len; ++jl) acc += lbb[rl * S + jl] * g[off + jl];
       v = acc;
     }
     ls[e] = v;
+    cp[e] = v;
   }
-  const LsqView lv = lsq_view(d.lsq, d.m * S);
-  lsq_append_cta(lv, ls, ld, S, gs, nullptr);  // (gs is free again: the norms' copy)
+  __syncthreads();
+  lsq_mark(d, 73);
+  // ---- Givens (HessenbergLsq::append_column per column): squared norms on thread 0 from the
+  //      copy; warp 1 rotates -- lane c column c through the stored pairs, then lane 0 the pairs
+  //      made inside this step and each column's new rotation
+  __shared__ double s_res;
   if (tid == 0) {
-    const double rho = lv.h->residual;
+    double g = lv.h->gnorm_sq;
+    for (int c = 0; c < S; ++c)
+      for (int i = 0; i < j0 + c + 2; ++i) g += cp[c * ld + i] * cp[c * ld + i];
+    lv.h->gnorm_sq = g;
+  } else if (tid >= 32 && tid < 64) {
+    const int c = tid - 32;
+    if (c < S) {
+      double* col = ls + c * ld;
+      double a = col[0];
+      for (int t = 0; t < j0; ++t) {
+        const double b = col[t + 1], cc = ccs[t], ss = csn[t];
+        col[t] = cc * a + ss * b;
+        a = -ss * a + cc * b;
+      }
+      col[j0] = a;
+    }
+    __syncwarp();
+    if (c == 0) {
+      double rj = lv.rhs[j0];
+      for (int c2 = 0; c2 < S; ++c2) {
+        double* col = ls + c2 * ld;
+        const int j = j0 + c2;
+        for (int t = j0; t < j; ++t) {
+          const double a = col[t], b = col[t + 1], cc = ccs[t], ss = csn[t];
+          col[t] = cc * a + ss * b;
+          col[t + 1] = -ss * a + cc * b;
+        }
+        const double a = col[j], b = col[j + 1];
+        const double r = sd_hypot(a, b);
+        double cc = 1.0, ss = 0.0;
+        if (r != 0.0) {
+          cc = a / r;
+          ss = b / r;
+        }
+        ccs[j] = cc;
+        csn[j] = ss;
+        col[j] = r;
+        const double ra = rj, rb = 0.0;
+        const double nj = cc * ra + ss * rb;
+        rj = -ss * ra + cc * rb;
+        lv.rhs[j] = nj;
+        lv.cs[j] = cc;
+        lv.sn[j] = ss;
+      }
+      lv.rhs[j0 + S] = rj;
+      s_res = sd_abs(rj);
+    }
+  }
+  __syncthreads();
+  lsq_mark(d, 74);
+  // ---- write back R's new columns; header; record rho; early exit
+  for (int e = tid; e < S * ld; e += nt) {
+    const int cl = e / ld, r = e - cl * ld;
+    const int j = j0 + cl;
+    if (r <= j) lsq_r(lv, j, r) = ls[e];
+  }
+  lsq_mark(d, 78);
+  if (tid == 0) {
+    const double rho = s_res;
+    lv.h->cols = j0 + S;
+    lv.h->residual = rho;
     rk[RecLayout::kRho] = rho;
-    if (!invariant && build_next && rho <= d.tol) {
-      d.st->status = kArnEarly;
-      d.st->block = k;
+    if (invariant) {  // (the block step already stopped the cycle; the verdict for the host)
+      d.st->lstatus = kArnInvariant;
+      d.st->lblock = k;
+    } else if (build_next && rho <= d.tol) {
+      d.st->lstatus = kArnEarly;
+      d.st->lblock = k;
       d.st->halt = 1;
     }
   }
   __syncthreads();
+  lsq_mark(d, 75);
 }
 
 // the constructor's push_block of block 0, then L_0 = cholesky_upper(W_0) and
@@ -291,9 +478,10 @@ __global__ void k_arn_ctor_push(const ArnLsqDesc d, const double* partials, int 
   SKC_PDL_ENTRY();
   if (d.st->halt) return;
   __shared__ double v[kMaxS * kMaxS];
+  __shared__ Gram s_g0;
   reduce_dots_dev(partials, G, dW, S * S, v);
   if (threadIdx.x == 0) {
-    Gram g;
+    Gram& g = s_g0;
     if (!arn_push_body<S>(d.st, g, 0, d.rec, v, S)) return;
     d.grams[0] = g;
     if (!d.lsq_on) return;
@@ -308,17 +496,12 @@ __global__ void k_arn_ctor_push(const ArnLsqDesc d, const double* partials, int 
   }
 }
 
-// per-round path: push + least squares of block step k (W from the pass that produced the
-// candidate: the reorthogonalized region when the flag says so)
+// block step k's least squares (arn_lsq_step), on the side stream
 template <int S>
-__global__ void k_arn_lsq(const ArnLsqDesc d, int k, int build_next, const double* partials, int G, int dWa, int dWb) {
-  SKC_PDL_ENTRY();
+__global__ void k_arn_lsq(const ArnLsqDesc d, int k, int build_next, int cap) {
   extern __shared__ __align__(16) double lsq_sm[];
-  if (d.st->halt && !(d.st->status == kArnInvariant && d.st->block == k)) return;
-  double* W = lsq_sm;
-  if (build_next) reduce_dots_dev(partials, G, d.st->reorth ? dWb : dWa, S * S, W);
-  __syncthreads();
-  arn_lsq_step<S>(d, k, build_next != 0, W, lsq_sm + kMaxS * kMaxS);
+  if (d.st->lstatus != kArnRunning) return;  // (an earlier step stopped the cycle)
+  arn_lsq_step<S>(d, k, build_next != 0, lsq_sm, cap);
 }
 
 // end of the cycle (sstep.hpp:602-625): unless the constructor failed, a collapse with the
@@ -338,7 +521,8 @@ __global__ void k_arn_finish(const ArnLsqDesc d, double* ycoef) {
     return;
   }
   const LsqView lv = lsq_view(d.lsq, M);
-  const bool collapsed = stv == kArnPushCollapse || stv == kArnCholCollapse;
+  const int ls = st->lstatus;
+  const bool collapsed = ls == kArnPushCollapse || ls == kArnCholCollapse;
   const bool attainable = lv.h->cols > 0 && lv.h->residual <= d.tol;
   if (collapsed && !attainable) {
     st->fin = kFinFallback;
@@ -482,8 +666,8 @@ struct OrthDesc {
   int dz, dseed, dr0, dr1, dcross, dwb;
   Gram* grams;
   double* rec;            // this block iteration's record
-  int rec_t, rec_h;
-  ArnLsqDesc lsq;         // the cycle's least-squares state (CTA 0 runs this step's part last)
+  double* rec_push;       // the previous block iteration's record (its push_block)
+  int rec_t, rec_h, rec_wraw;
   ArnState* st;
   double orth_tol;
   unsigned long long* trace;  // optional phase timestamps (CTA 0), diagnostics
@@ -551,7 +735,9 @@ __device__ __forceinline__ void orth_store2(const double (&acc)[K], double* red,
 template <int S>
 __global__ void __launch_bounds__(ORTH_NT, 1) k_arn_step(const __grid_constant__ OrthDesc d) {
   SKC_PDL_ENTRY();
-  if (__ldg(&d.st->halt)) return;  // block-uniform, before any barrier
+  // block-uniform, before any barrier; a volatile read: the side stream's least-squares kernel
+  // may raise the flag while this grid is being scheduled
+  if (*reinterpret_cast<const volatile int*>(&d.st->halt)) return;
   namespace cg = cooperative_groups;
   cg::grid_group grid = cg::this_grid();
   constexpr int NC = S - 1;
@@ -755,21 +941,20 @@ __global__ void __launch_bounds__(ORTH_NT, 1) k_arn_step(const __grid_constant__
   // the previous block iteration's cross pass already produced z (in memory) and this
   // iteration's Scalar1 products (partials dz), unless it ran a reorthogonalization pass
   const bool zready = d.zfuse && K > 1 && __ldg(&d.st->zready) != 0;
-  // the Gram factors of blocks 0..k-1 into shared memory (asynchronous; waited for before
-  // Scalar1).  Block k-1's push_block ran at the end of the previous launch (CTA 0's tail).
+  // push_block of the previous block iteration's candidate (sstep.hpp:375, 392-399) runs here,
+  // off the previous kernel's tail: every CTA reduces its W (from the pass that produced the
+  // candidate) and factors it in the Scalar1 phase; CTA 0 records it and stores the factor
+  const bool push = K >= 2;
+  if (push) reduce_dots_dev(d.partials, G, __ldg(&d.st->reorth) ? d.dwb : d.dcross + (K - 1) * S * S, S * S, tc);
+  // the Gram factors of blocks 0..k-1 (k-2 with the push) into shared memory (asynchronous;
+  // waited for before Scalar1)
   {
     const char* gsrc = reinterpret_cast<const char*>(d.grams);
     char* gdst = reinterpret_cast<char*>(gk);
-    for (int w = tid; w < (int)(K * sizeof(Gram) / 8); w += ORTH_NT) cp_async8(gdst + 8 * w, gsrc + 8 * w, true);
+    for (int w = tid; w < (int)((push ? K - 1 : K) * sizeof(Gram) / 8); w += ORTH_NT)
+      cp_async8(gdst + 8 * w, gsrc + 8 * w, true);
     cp_async_commit();
   }
-  // CTA 0's tail: this block step's push_block and least-squares step (arn_lsq_step), run
-  // once every other CTA is done with the step's data; the candidate slice area is its scratch
-  auto lsq_tail = [&](const double* Wraw) {
-    if (blockIdx.x != 0) return;
-    __syncthreads();
-    arn_lsq_step<S>(d.lsq, K, d.build_next != 0, Wraw, sc);
-  };
   orth_mark(d, 39);
   // ---- z = A v_{k-1}^{s-1} on this slice (the source is stable; neighbours read from memory)
   // y = A x on this slice; xs (optional) is this slice of x in shared memory, read in place of
@@ -899,6 +1084,16 @@ __global__ void __launch_bounds__(ORTH_NT, 1) k_arn_step(const __grid_constant__
   // from shared memory); CTA 0 records
   cp_async_wait<0>();
   reduce_dots_dev(d.partials, G, d.dz, K * S + 1, prod);  // (ends with __syncthreads)
+  if (push) {
+    __shared__ int s_push_ok;
+    if (tid == 0) {
+      const bool ok = arn_push_body<S>(d.st, gk[K - 1], K - 1, d.rec_push, tc, S, blockIdx.x == 0);
+      s_push_ok = ok;
+      if (ok && blockIdx.x == 0) d.grams[K - 1] = gk[K - 1];
+    }
+    __syncthreads();
+    if (!s_push_ok) return;  // basis collapse (identical decision in every CTA)
+  }
   const double zn = sqrt(prod[K * S]);
   if (blockIdx.x == 0 && tid == 0) {
     d.rec[RecLayout::kZn] = zn;
@@ -968,7 +1163,6 @@ __global__ void __launch_bounds__(ORTH_NT, 1) k_arn_step(const __grid_constant__
       d.st->block = K;
       d.st->halt = 1;
     }
-    lsq_tail(nullptr);  // (the step's Hessenberg columns still count: sstep.hpp:319, 586)
     return;
   }
   const double inv = 1.0 / nu;
@@ -1091,10 +1285,7 @@ __global__ void __launch_bounds__(ORTH_NT, 1) k_arn_step(const __grid_constant__
     orth_mark(d, 44 + 2 * j);
   }
   orth_mark(d, 43);
-  if (!d.build_next) {  // the last block iteration builds the candidate only
-    lsq_tail(nullptr);
-    return;
-  }
+  if (!d.build_next) return;  // the last block iteration builds the candidate only
   // ---- round-0 products V_0^T cand[:,1:] (sstep.hpp:341)
   r0_products();
   grid.sync();
@@ -1175,20 +1366,23 @@ __global__ void __launch_bounds__(ORTH_NT, 1) k_arn_step(const __grid_constant__
     cross_block(std::false_type{}, K, d.dwb, 0);
     grid.sync();
     orth_mark(d, 4);
-    if (blockIdx.x == 0) reduce_dots_dev(d.partials, G, d.dwb, S * S, tc);  // (ends with a barrier)
-    lsq_tail(tc);
+    // the candidate's raw Gram products for the least-squares stream (its snapshot: the next
+    // block iteration reuses the partial regions)
+    if (blockIdx.x == 0) {
+      reduce_dots_dev(d.partials, G, d.dwb, S * S, tc);  // (ends with a barrier)
+      if (tid < S * S) d.rec[d.rec_wraw + tid] = tc[tid];
+    }
   } else {
     orth_mark(d, 4);
-    lsq_tail(prod + K * S * S);  // W of the candidate, reduced with the cross products
+    if (blockIdx.x == 0 && tid < S * S) d.rec[d.rec_wraw + tid] = prod[K * S * S + tid];
   }
   orth_mark(d, 5);
 }
 
-// (the candidate slice area doubles as the least-squares tail's scratch)
-size_t orth_smem(int s, int k, int m, int64_t P) {
+size_t orth_smem(int s, int k, int64_t P) {
   return sizeof(double) * (64 + kStepH + (size_t)orth_prod_cap(k, s)) + sizeof(Gram) * (1 + (size_t)k) +
          sizeof(double) * (ORTH_NT / 32) * (s * s + s) +
-         sizeof(double) * std::max((size_t)std::min(s - 1, kOrthSmemCols) * (size_t)P, (size_t)arn_lsq_scratch(s, m));
+         sizeof(double) * (size_t)std::min(s - 1, kOrthSmemCols) * (size_t)P;
 }
 
 // ghost-row buffer sizes (doubles) of the row-streamed powers for slices of P points, or
@@ -1216,8 +1410,8 @@ bool stream_powers_ghosts(const DevOp& op, int s, int64_t n, int64_t P, int G, i
 
 template <int S>
 void run_orth(Ctx& c, const OrthDesc& d, int G, size_t smem) {
-  // (227 KB per block less the kernel's static shared memory)
-  ensure_smem(k_arn_step<S>, 226 * 1024);
+  // (at most 227 KB per block less the kernel's static shared memory; orth_points caps smem)
+  ensure_smem(k_arn_step<S>, smem);
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = G;
   cfg.blockDim = ORTH_NT;
@@ -1516,6 +1710,8 @@ struct Engine {
   ArnLsqDesc lq{};      // least-squares state of the cycle (tol set per solve)
   const double* fvec = nullptr;  // the solve's right-hand side and iterate (device)
   double* xvec = nullptr;
+  cudaEvent_t ev_step = nullptr, ev_lsq = nullptr;  // side-stream fork / join
+  bool lsq_pending = false;
   bool zfused = false;  // the next block iteration's z and Scalar1 products are already computed
   // across GPUs the reorthogonalization decision is read back after the test (one stream sync
   // per block iteration), so a skipped second pass spends no collective and no halo exchange:
@@ -1533,15 +1729,21 @@ struct Engine {
   Engine& operator=(const Engine&) = delete;
   ~Engine() {
     if (cycle_exec) cudaGraphExecDestroy(cycle_exec);
+    if (ev_step) cudaEventDestroy(ev_step);
+    if (ev_lsq) cudaEventDestroy(ev_lsq);
   }
 
   // points per CTA of the on-chip orthogonalization (one CTA per SM), or 0 when it is off or
   // the candidate slices do not fit in shared memory
   int64_t orth_points() const {
     if (!c.orth || c.world() != 1 || s < 2 || op.d.kind == kIlu0) return 0;
-    const int64_t P = ((op.n + c.sm_count - 1) / c.sm_count + 1) & ~(int64_t)1;
-    return orth_smem(s, m, m, P) <= kOrthSmemCap ? P : 0;
+    const int64_t P = ((op.n + mk_ctas() - 1) / mk_ctas() + 1) & ~(int64_t)1;
+    return orth_smem(s, m, P) <= kOrthSmemCap ? P : 0;
   }
+
+  // CTAs of the block-iteration kernel: one per SM, less the one SM left to the side stream's
+  // least-squares kernels when they overlap the next block iteration
+  int mk_ctas() const { return c.lsq_overlap ? c.sm_count - 1 : c.sm_count; }
 
   // block iteration k (z, Scalar1, seed, nu, candidate block, block MGS, reorthogonalization,
   // push) in one cooperative kernel
@@ -1573,20 +1775,21 @@ struct Engine {
     d.dwb = dl.Wb();
     d.grams = grams;
     d.rec = recp(k);
-    d.lsq = lq;
+    d.rec_push = recp(k - 1);
+    d.rec_wraw = rl.wraw();
     d.rec_t = rl.t();
     d.rec_h = rl.h();
     d.st = st;
     d.orth_tol = 1e-8;
     static const bool trace = std::getenv("SKC_TRACE_ORTH") != nullptr;
     if (trace) d.trace = (unsigned long long*)c.workspace("orth_trace", 1024 * sizeof(unsigned long long));
-    const int G = c.sm_count;
+    const int G = mk_ctas();
     int g1 = 0, g2 = 0;
     d.spow = c.spow && stream_powers_ghosts(op.d, s, op.n, d.P, G, g1, g2);
     d.g1 = d.spow ? g1 : 0;
     d.g2 = d.spow ? g2 : 0;
     if (d.spow) d.ghosts = (double*)c.workspace("orth_ghosts", sizeof(double) * (size_t)G * (g1 + g2));
-    const size_t smem = orth_smem(s, k, m, d.P);
+    const size_t smem = orth_smem(s, k, d.P);
     // algorithmic bytes, SURVEY 8(d) model (block-CGS-equivalent passes): a block step k < m
     // moves SpMV(2) + V^T z (ks+1) + seed (ks+2) + MPK (s+1) + V^T cand (ks+s) +
     // update/cross/Gram (ks+2s-1) = 4ks+4s+5 vectors, the last one (no build) 2ms+s+6.  The
@@ -1603,6 +1806,7 @@ struct Engine {
       case 7: run_orth<7>(c, d, G, smem); break;
       default: run_orth<8>(c, d, G, smem); break;
     }
+    lsq_fork(k, build_next);
     if (trace) {
       unsigned long long t[1024];
       CK(cudaMemcpyAsync(t, d.trace, sizeof t, cudaMemcpyDeviceToHost, c.stream));
@@ -1631,6 +1835,10 @@ struct Engine {
                      (t[9 + 3 * i] - t[8 + 3 * i]) * 1e-3, (t[10 + 3 * i] - t[9 + 3 * i]) * 1e-3);
       std::fprintf(stderr, " | znext %.1f cross %.1f sync %.1f check %.1f pass1 %.1f push %.1f us\n", (t[60] - t[7 + 3 * k]) * 1e-3, (t[1] - t[60]) * 1e-3,
                    (t[2] - t[1]) * 1e-3, (t[3] - t[2]) * 1e-3, (t[4] - t[3]) * 1e-3, (t[5] - t[4]) * 1e-3);
+      std::fprintf(stderr, "[lsq k=%d] enter %.2f push/stage %.2f (push %.2f stage %.2f) gcols %.2f apply_l %.2f givens %.2f store %.2f (loop %.2f) us\n", k,
+                   (t[70] - t[4]) * 1e-3, (t[71] - t[70]) * 1e-3, (t[76] - t[70]) * 1e-3, (t[77] - t[70]) * 1e-3,
+                   (t[72] - t[71]) * 1e-3, (t[73] - t[72]) * 1e-3,
+                   (t[74] - t[73]) * 1e-3, (t[75] - t[74]) * 1e-3, (t[78] - t[74]) * 1e-3);
     }
   }
 
@@ -1705,11 +1913,14 @@ struct Engine {
     lq.recsz = rl.size();
     lq.rec_t = rl.t();
     lq.rec_h = rl.h();
+    lq.rec_wraw = rl.wraw();
     lq.st = st;
     lq.grams = grams;
     std::vector<double> hc(cl.size(), 0.0);
     hc[cl.M1()] = -1.0;
     CK(cudaMemcpyAsync(coef, hc.data(), hc.size() * sizeof(double), cudaMemcpyHostToDevice, c.stream));
+    CK(cudaEventCreateWithFlags(&ev_step, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&ev_lsq, cudaEventDisableTiming));
     ArnState h{};
     h.fixed = fixed ? 1 : 0;
     CK(cudaMemcpyAsync(st, &h, sizeof h, cudaMemcpyHostToDevice, c.stream));
@@ -1782,20 +1993,38 @@ struct Engine {
     CK(cudaGetLastError());
   }
 
-  // per-round path: push_block + least squares of block step k (k_arn_lsq)
-  void lsq_step(int k, bool build_next, int Gw, int dWa) {
-    const size_t smem = sizeof(double) * (kMaxS * kMaxS + (size_t)arn_lsq_scratch(s, m));
+  // block step k's least squares (k_arn_lsq) on the side stream, after the block step's kernels
+  // (the next block step does not wait for it; lsq_join does)
+  void lsq_fork(int k, bool build_next) {
+    int cap = arn_lsq_scratch(s, m);
+    if ((size_t)(cap + arn_lsq_prev(s, m)) * sizeof(double) <= 200 * 1024) cap += arn_lsq_prev(s, m);
+    const size_t smem = sizeof(double) * (size_t)cap;
+    cudaStream_t a = c.stream;
+    if (c.lsq_overlap) {
+      a = c.aux();
+      CK(cudaEventRecord(ev_step, c.stream));
+      CK(cudaStreamWaitEvent(a, ev_step, 0));
+      lsq_pending = true;
+    }
     dispatch_s(s, [&](auto S_) {
       constexpr int S = decltype(S_)::value;
       ensure_smem(k_arn_lsq<S>, smem);
-      launch_k(c, k_arn_lsq<S>, 1, 256, smem, lq, k, build_next ? 1 : 0, (const double*)partials, Gw, dWa, dl.Wb());
+      k_arn_lsq<S><<<1, 256, smem, a>>>(lq, k, build_next ? 1 : 0, cap);
     });
+    CK(cudaGetLastError());
     ++c.launches;
+  }
+  void lsq_join() {
+    if (!lsq_pending) return;
+    CK(cudaEventRecord(ev_lsq, c.aux()));
+    CK(cudaStreamWaitEvent(c.stream, ev_lsq, 0));
+    lsq_pending = false;
   }
 
   // end of the cycle on the device: y (k_arn_finish), x += V y over the m blocks (zero
   // coefficients past the appended columns), r = f - A x and ||r|| (st->rn, rn_out)
   void enqueue_finish(const double* f, double* x) {
+    lsq_join();
     launch_k(c, k_arn_finish, 1, 256, 0, lq, coef + cl.Y());
     ++c.launches;
     LinBuilder lb;
@@ -1860,7 +2089,7 @@ struct Engine {
     const int cb = k;  // block slot k (slot m is scratch when k == m)
     const int Gfused = krylov_into(cb, seed, build_next && s > 1);
     if (!build_next) {
-      lsq_step(k, false, 0, 0);
+      lsq_fork(k, false);
       CK(cudaGetLastError());
       return;
     }
@@ -1938,7 +2167,9 @@ struct Engine {
     // (for s > 1 the dWa region was already made global together with the cross products)
     const int Gw = s > 1 ? (wb_needed ? c.reduce_point(partials, g.G, dl.Wb(), s * s) : c.world())
                          : c.reduce_point(partials, g.G, dWa, s * s);
-    lsq_step(k, true, Gw, dWa);
+    launch_k(c, k_arn_push, 1, 256, 0, st, grams, cb, rk, rl.wraw(), (const double*)partials, Gw, dWa, dl.Wb(), s);
+    ++c.launches;
+    lsq_fork(k, true);
     CK(cudaGetLastError());
   }
 
@@ -2072,15 +2303,16 @@ void sgmres_device(Ctx& c, const Op& op, const double* f, double* x, const SStep
     // (cholesky_upper of block 0 escapes sgmres_solve in the reference, sstep.hpp:563)
     if (hs.status == kArnCtorChol) fail(SKC_EBREAKDOWN, "cholesky: matrix not positive definite");
     for (int k = 1; k <= m; ++k) {
-      const bool stopped_here = hs.status != kArnRunning && hs.block == k;
-      const bool invariant = stopped_here && hs.status == kArnInvariant;
+      // (the least-squares stream's verdict on the block steps; the constructor's is hs.status)
+      const bool stopped_here = hs.lstatus != kArnRunning && hs.lblock == k;
+      const bool invariant = stopped_here && hs.lstatus == kArnInvariant;
       H.count_advance(cnt, k, k < m, invariant ? 1 : 0);
-      if (stopped_here && hs.status == kArnPushCollapse) {
+      if (stopped_here && hs.lstatus == kArnPushCollapse) {
         collapsed = true;
         collapse_msg = gram_message((int)H.rec(k)[RecLayout::kSing], H.rec(k)[RecLayout::kRatio]);
         break;
       }
-      if (stopped_here && hs.status == kArnCholCollapse) {
+      if (stopped_here && hs.lstatus == kArnCholCollapse) {
         collapsed = true;
         collapse_msg = "cholesky: matrix not positive definite";
         break;
@@ -2152,6 +2384,7 @@ void sarnoldi_device(Ctx& c, const Op& op, const double* v1, uint64_t s64, uint6
   H.recs.resize((size_t)(m + 1) * E.rl.size());
   E.ctor(v1, false);
   for (int k = 1; k <= m; ++k) E.advance(k, k < m);
+  E.lsq_join();
   ArnState hs = E.read_state();
   CK(cudaMemcpy(H.recs.data(), E.rec, H.recs.size() * sizeof(double), cudaMemcpyDeviceToHost));
   if (hs.status == kArnCtorZero) fail(SKC_EINVAL, "s-arnoldi: start vector is zero");

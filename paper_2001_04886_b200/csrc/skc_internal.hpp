@@ -176,6 +176,10 @@ struct Ctx {
   int sm_count = 148;
   cudaStream_t stream = nullptr;
   cudaStream_t own_stream = nullptr;
+  // side stream for the latency-bound single-CTA least-squares kernels of s-GMRES, which run
+  // beside the next block iteration (created on first use; joined before any result is read)
+  cudaStream_t aux_stream = nullptr;
+  cudaStream_t aux();
   uint64_t launches = 0;
   bool profiling = false;
   bool pdl = true;   // programmatic dependent launch for solver kernels (SKC_PDL=0 disables)
@@ -183,6 +187,7 @@ struct Ctx {
   bool zfuse = false;   // megakernel: next Scalar1 products in the cross pass (SKC_ZFUSE=1)
   bool persist = true;  // persistent s-Omin for small problems (SKC_PERSIST=0 disables)
   bool spow = true;     // megakernel: row-streamed candidate powers (SKC_SPOW=0 disables)
+  bool lsq_overlap = true;  // s-GMRES least squares on the side stream (SKC_LSQ_OVERLAP=0: in line)
   bool ilu_strips = true;  // ILU(0) on 2D grids: strip-wavefront solves (SKC_ILU_STRIPS=0 disables)
   std::map<std::string, KStat> stats;
   struct Pending {
