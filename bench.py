@@ -348,6 +348,12 @@ def _reference_lib(need_fixed=False):
     return Oracle("port"), "port"
 
 
+def _port():
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    from oracle import Oracle
+    return Oracle("port")
+
+
 def cpu_baseline_sample(name):
     """The reference CPU path on one host core on a bounded sample of the same workload."""
     from paper_2001_04886_b200 import convection_diffusion, splitmix64_uniform
@@ -356,8 +362,9 @@ def cpu_baseline_sample(name):
     orc, kind = _reference_lib(need_fixed=fixed_mode)  # (the reference has no fixed-step mode)
     nx = c.get("cpu_nx", c["nx"])
     st = convection_diffusion(c["dim"], nx, c["conv"], variable_k=c.get("vark", False))
-    kcell = orc.lognormal(K_SEED, st.n) if c.get("vark") else None
-    a = orc.stencil_csr(c["dim"], st.nx, st.ny, st.nz, st.coef, kcell=kcell, ch2=st.ch2)
+    port = _port()  # (input assembly only: the port's CSR builder and k generator)
+    kcell = port.lognormal(K_SEED, st.n) if c.get("vark") else None
+    a = port.stencil_csr(c["dim"], st.nx, st.ny, st.nz, st.coef, kcell=kcell, ch2=st.ch2)
     f = splitmix64_uniform(SEED, st.n)
     s = c["s"]
     if c["method"] == "sgmres":
@@ -426,7 +433,7 @@ def run_reference(args):
     orc, kind = _reference_lib()
     c = CONFIGS["C2"]
     st = convection_diffusion(2, c["nx"], c["conv"])
-    a = orc.stencil_csr(2, st.nx, st.ny, 1, st.coef)
+    a = _port().stencil_csr(2, st.nx, st.ny, 1, st.coef)
     f = splitmix64_uniform(SEED, st.n)
     tol = c["rel_tol"] * float(np.linalg.norm(f))
     S, M = c["s"], c["m"]
