@@ -295,8 +295,8 @@ def measure(name, steps, warmup, cpu=True):
         tr = os.path.join(ROOT, "profiles", "ncu_traffic.json")
         if os.path.exists(tr):
             try:
-                t = json.load(open(tr)).get(name, {}).get(kname)
-                roofline["traffic"] = t
+                t = json.load(open(tr)).get(name, {})
+                roofline["traffic"] = t.get(kname) if isinstance(t, dict) else None
             except Exception:
                 pass
     kernels = {k: {"launches": v["launches"], "ms": round(v["ms"], 3),

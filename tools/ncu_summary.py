@@ -5,7 +5,7 @@
       (ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --csv).
   python tools/ncu_summary.py full <report.ncu-rep> <out.md> [traffic.json class]
       key --set full metrics per captured launch; optionally records the mean DRAM traffic per
-      launch under `class` in traffic.json (read by bench.py for roofline.traffic).
+      launch under `class` ("config/kernel") in traffic.json (read by bench.py for roofline.traffic).
 """
 import csv
 import io
@@ -92,7 +92,11 @@ def full(path, out, traffic_json=None, klass=None):
     print("\n".join(lines))
     if traffic_json and klass and traffic:
         d = json.load(open(traffic_json)) if os.path.exists(traffic_json) else {}
-        d[klass] = sum(traffic) / len(traffic)
+        if "/" in klass:  # config/kernel (what bench.py reads: traffic[config][kernel])
+            cfg, kern = klass.split("/", 1)
+            d.setdefault(cfg, {})[kern] = sum(traffic) / len(traffic)
+        else:
+            d[klass] = sum(traffic) / len(traffic)
         json.dump(d, open(traffic_json, "w"), indent=1, sort_keys=True)
 
 

@@ -1,0 +1,26 @@
+#!/bin/bash
+# On the GPU box: launch lists (per-kernel device time + DRAM bytes) and one `ncu --set full`
+# capture of the top kernel for the bench configurations; summarized here with
+#   python tools/ncu_summary.py launches gpurun_out/prof/launches_<cfg>.csv profiles/<round>_launches_<cfg>.md
+#   python tools/ncu_summary.py full gpurun_out/prof/full_<cfg>.ncu-rep profiles/<round>_ncu_full_<cfg>.md profiles/ncu_traffic.json <cfg>/<kernel>
+# Every command below first ran without ncu (bench.py exits 0) in the same round.
+set -x
+mkdir -p gpurun_out/prof
+M=gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum
+run() {  # cfg, launch-skip, launch-count, full-kernel-regex, full-skip, full-count
+  cfg=$1
+  ncu --metrics $M --clock-control none --csv -s $2 -c $3 --log-file gpurun_out/prof/launches_$cfg.csv \
+      python bench.py --config $cfg --no-secondary --steps 1 --warmup 1 > gpurun_out/prof/ncu_$cfg.log 2>&1
+  ncu --set full --import-source on --clock-control none -k regex:$4 -s $5 -c $6 -o gpurun_out/prof/full_$cfg \
+      python bench.py --config $cfg --no-secondary --steps 1 --warmup 1 > gpurun_out/prof/ncu_full_$cfg.log 2>&1
+}
+CFGS=${CFGS:-"C2 C3s4 C4"}
+for c in $CFGS; do
+  case $c in
+    C2) run C2 3000 2600 k_arn_step 100 3 ;;
+    C3s4) run C3s4 1200 1200 k_upd 40 2 ;;
+    C4) run C4 900 900 k_mgs 30 2 ;;
+    C5) run C5 1200 1200 k_upd 40 2 ;;
+  esac
+done
+ls -la gpurun_out/prof
