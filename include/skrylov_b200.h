@@ -18,7 +18,7 @@
  *   skc_op_create_stencil (new: device-describable 5/7-point operator)
  *   skc_op_create_ilu0 <- right_preconditioned(a, ilu0_factor(a))  (A (LU)^{-1})                 ilu0.hpp:138-146, 45-95
  *   skc_ilu0_solve[_device] <- ilu0_apply(factors, r) -> z = (LU)^{-1} r                         ilu0.hpp:99-134
- *   skc_ilu0_factor   <- ilu0_factor(a) values in A's pattern (host only, no GPU needed)          ilu0.hpp:45-95
+ *   skc_ilu0_factor   <- ilu0_factor(a) values in A's pattern (factored on ctx's device)           ilu0.hpp:45-95
  *   skc_gram_solve / skc_cholesky_upper / skc_hessenberg_lsq <- GramSolver / cholesky_upper /
  *                      hessenberg_lsq (small_dense.hpp:42-331); host-only, no GPU needed.
  *
@@ -156,8 +156,8 @@ int skc_op_create_ilu0(skc_ctx* ctx, uint64_t n, const uint64_t* row_offsets, co
                        const double* values, skc_op** out);
 int skc_ilu0_solve(skc_ctx* ctx, const skc_op* ilu_op, const double* r, double* z);        /* host buffers */
 int skc_ilu0_solve_device(skc_ctx* ctx, const skc_op* ilu_op, const double* r, double* z); /* device, async */
-int skc_ilu0_factor(uint64_t n, const uint64_t* row_offsets, const uint64_t* col_indices, const double* values,
-                    double* lu_out);
+int skc_ilu0_factor(skc_ctx* ctx, uint64_t n, const uint64_t* row_offsets, const uint64_t* col_indices,
+                    const double* values, double* lu_out);
 /* seeded k = exp(N(0,1)) field of the variable-coefficient configurations (BASELINE configs[4];
  * DESIGN.md "Inputs"), host only */
 int skc_fill_lognormal(uint64_t seed, uint64_t n, double* out);

@@ -134,7 +134,7 @@ def lib():
         "skc_op_create_ilu0": [vp, u64, P(u64), P(u64), P(dbl), P(vp)],
         "skc_ilu0_solve": [vp, vp, P(dbl), P(dbl)],
         "skc_ilu0_solve_device": [vp, vp, vp, vp],
-        "skc_ilu0_factor": [u64, P(u64), P(u64), P(dbl), P(dbl)],
+        "skc_ilu0_factor": [C.c_void_p, u64, P(u64), P(u64), P(dbl), P(dbl)],
         "skc_fill_lognormal": [u64, u64, P(dbl)],
         "skc_discretize": [u64, dbl, dbl, P(u64), P(u64), P(dbl), P(dbl), P(dbl), P(dbl)],
     }

@@ -75,6 +75,7 @@ int host_solve(skc_ctx* ctx, const skc_op* op, const double* f, double* x, skc_r
     solve(c, op->o, fd, xd, rep->r);
     CK(cudaMemcpyAsync(x, xd, n * sizeof(double), cudaMemcpyDeviceToHost, c.stream));
     c.sync();
+    skc::ilu0_check(c, op->o);
   });
 }
 
@@ -268,6 +269,7 @@ int skc_ilu0_solve(skc_ctx* ctx, const skc_op* op, const double* r, double* z) {
     skc::launch_ilu0_solve(c, *op->o.ilu, rd, zd, nullptr, nullptr);
     CK(cudaMemcpyAsync(z, zd, n * sizeof(double), cudaMemcpyDeviceToHost, c.stream));
     c.sync();
+    skc::ilu0_check(c, op->o);
   });
 }
 
@@ -364,14 +366,15 @@ int skc_discretize(uint64_t nx, double beta, double gamma, uint64_t* row_offsets
   });
 }
 
-int skc_ilu0_factor(uint64_t n, const uint64_t* row_offsets, const uint64_t* col_indices, const double* values,
-                    double* lu_out) {
+int skc_ilu0_factor(skc_ctx* ctx, uint64_t n, const uint64_t* row_offsets, const uint64_t* col_indices,
+                    const double* values, double* lu_out) {
   return guarded([&] {
-    skc::require(row_offsets && lu_out, "null argument");
+    skc::require(ctx && row_offsets && lu_out, "null argument");
     skc::require(n == 0 || (col_indices && values) || row_offsets[n] == 0, "null argument");
     skc::validate_csr((int64_t)n, row_offsets, col_indices);
+    set_device(ctx);
     std::vector<double> lu;
-    skc::ilu0_factor_host((int64_t)n, row_offsets, col_indices, values, lu);
+    skc::ilu0_factor_device(ctx->c, (int64_t)n, row_offsets, col_indices, values, lu);
     std::memcpy(lu_out, lu.data(), sizeof(double) * lu.size());
   });
 }
@@ -388,6 +391,7 @@ int skc_op_apply(skc_ctx* ctx, const skc_op* op, const double* x, double* y) {
     skc::launch_apply(c, op->o.d, xd, yd, nullptr, nullptr);
     CK(cudaMemcpyAsync(y, yd, n * sizeof(double), cudaMemcpyDeviceToHost, c.stream));
     c.sync();
+    skc::ilu0_check(c, op->o);
   });
 }
 

@@ -4,9 +4,13 @@
 // (solve_linear, bench.hpp:149-191).
 //
 // The factorization is the reference's row-wise IKJ elimination restricted to pattern(A)
-// (ilu0_factor, ilu0.hpp:45-95), run once on the host (O(nnz), the same IEEE operations in the
-// same order, no FMA contraction) with the reference's error behaviour: a row without a
-// diagonal is an invalid argument, a pivot below 1e-14 max|diag(A)| a breakdown naming the row.
+// (ilu0_factor, ilu0.hpp:45-95), run on the device: row i only reads the finished rows of its
+// lower neighbours, so the rows are walked in the level schedule of L (a barrier between
+// levels) and every row is eliminated by one thread in the reference's order -- its lower
+// entries by ascending column, each subtracting mult * U(k, :) from the matching entries, the
+// same IEEE operations (no contraction), hence the same bits.  The reference's error behaviour:
+// a row without a diagonal is an invalid argument (checked on the host with the pattern), a
+// pivot below 1e-14 max|diag(A)| a breakdown naming the first such row.
 //
 // The triangular solves are level-scheduled: rows are grouped by their dependency depth in L
 // (resp. U), and one cooperative launch walks the levels with a grid barrier between them,
@@ -124,7 +128,7 @@ template <bool LOWER>
 __global__ void __launch_bounds__(32) k_trsv_strip(const double* __restrict__ a1, const double* __restrict__ a2,
                                                    const double* __restrict__ ac, const uint8_t* __restrict__ msk,
                                                    int nx, int ny, const double* r, double* z, double* bnd,
-                                                   const int* halt, const int* cond) {
+                                                   int* stalled, const int* halt, const int* cond) {
   SKC_PDL_ENTRY();
   if (skip_launch(halt, cond)) return;
   const int k = threadIdx.x, sx = blockIdx.x, nstrip = gridDim.x;
@@ -167,6 +171,10 @@ __global__ void __launch_bounds__(32) k_trsv_strip(const double* __restrict__ a1
               reinterpret_cast<const volatile unsigned long long*>(bnd + (int64_t)nb * ny + t + k);
           unsigned long long bits = *b;
           for (int spin = 0; bits == kBndSentinel && spin < (1 << 26); ++spin) bits = *b;
+          if (bits == kBndSentinel) {  // the neighbour strip never delivered: flag it (the host raises)
+            atomicExch(stalled, 1);
+            bits = 0;
+          }
           w = __longlong_as_double((long long)bits);
         }
         wchunk = w;
@@ -237,10 +245,10 @@ void launch_trsv(Ctx& c, const IluData& d, const double* r, double* z, const int
     sc.numAttrs = 1;
     if (LOWER)
       CK(cudaLaunchKernelEx(&sc, k_trsv_strip<true>, d.lW, d.lS, (const double*)nullptr, d.lm, (int)d.gnx, (int)d.gny,
-                            r, z, bnd, halt, cond));
+                            r, z, bnd, d.stalled, halt, cond));
     else
       CK(cudaLaunchKernelEx(&sc, k_trsv_strip<false>, d.uE, d.uN, d.uC, d.um, (int)d.gnx, (int)d.gny,
-                            (const double*)nullptr, z, bnd, halt, cond));
+                            (const double*)nullptr, z, bnd, d.stalled, halt, cond));
     return;
   }
   if ((LOWER ? d.maxw_l : d.maxw_u) <= 8 * TR1_NT) {
@@ -293,39 +301,128 @@ void level_schedule(int64_t n, const std::vector<int64_t>& rp, const std::vector
 
 }  // namespace
 
-// ilu0_factor (ilu0.hpp:45-95) on the host, restated: the factor values in A's pattern
-void ilu0_factor_host(int64_t n, const uint64_t* offs, const uint64_t* cols, const double* vals,
-                      std::vector<double>& lu) {
-  lu.assign(vals, vals + offs[n]);
-  std::vector<uint64_t> diag(n);
+namespace {
+
+// row i of ilu0_factor (ilu0.hpp:59-90): lu holds A's values on entry and the factor on exit;
+// the rows it reads (its lower neighbours k) are finished.  Loads bypass L1 (rows finished by
+// other CTAs before the last grid barrier).
+__device__ __forceinline__ void ilu_factor_row(int i, const int64_t* __restrict__ rp, const int32_t* __restrict__ ci,
+                                               const int64_t* __restrict__ dg, double* lu, double floor_, int* fail) {
+  const int64_t b = rp[i], e = rp[i + 1];
+  for (int64_t p = b; p < e && ci[p] < i; ++p) {
+    const int k = ci[p];
+    const int64_t dk = dg[k];
+    const double mult = __ddiv_rn(__ldcg(lu + p), __ldcg(lu + dk));
+    lu[p] = mult;
+    int64_t w = p + 1;  // row i's columns above k, merged with row k's columns above its diagonal
+    const int64_t ke = rp[k + 1];
+    for (int64_t q = dk + 1; q < ke; ++q) {
+      const int c = ci[q];
+      while (w < e && ci[w] < c) ++w;
+      if (w < e && ci[w] == c) lu[w] = __dsub_rn(__ldcg(lu + w), __dmul_rn(mult, __ldcg(lu + q)));
+    }
+  }
+  if (fabs(__ldcg(lu + dg[i])) < floor_) atomicMin(fail, i);
+}
+
+// every level in one CTA (narrow levels, e.g. the anti-diagonals of a 2D grid)
+__global__ void __launch_bounds__(1024) k_ilu_factor1(const int64_t* rp, const int32_t* ci, const int64_t* dg,
+                                                       const int32_t* perm, const int64_t* lev, int nlev, double* lu,
+                                                       double floor_, int* fail) {
+  for (int L = 0; L < nlev; ++L) {
+    for (int64_t q = lev[L] + threadIdx.x; q < lev[L + 1]; q += blockDim.x) ilu_factor_row(perm[q], rp, ci, dg, lu, floor_, fail);
+    __syncthreads();
+  }
+}
+
+// wide levels: one cooperative grid, a grid barrier between levels
+__global__ void k_ilu_factor(const int64_t* rp, const int32_t* ci, const int64_t* dg, const int32_t* perm,
+                             const int64_t* lev, int nlev, double* lu, double floor_, int* fail) {
+  namespace cg = cooperative_groups;
+  cg::grid_group grid = cg::this_grid();
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int L = 0; L < nlev; ++L) {
+    for (int64_t q = lev[L] + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < lev[L + 1]; q += stride)
+      ilu_factor_row(perm[q], rp, ci, dg, lu, floor_, fail);
+    grid.sync();
+  }
+}
+
+}  // namespace
+
+// ilu0_factor (ilu0.hpp:45-95) on the device: the factor values in A's pattern, returned to the
+// host (lu).  The host checks the pattern (a diagonal in every row) and max|diag(A)|.
+void ilu0_factor_device(Ctx& c, int64_t n, const uint64_t* offs, const uint64_t* cols, const double* vals,
+                        std::vector<double>& lu) {
+  const int64_t nnz = n ? (int64_t)offs[n] : 0;
+  lu.assign(vals, vals + nnz);
+  if (n == 0) return;
+  std::vector<int64_t> rp(offs, offs + n + 1), dg(n);
+  std::vector<int32_t> ci(nnz);
   double max_diag = 0.0;
   for (int64_t i = 0; i < n; ++i) {
     bool found = false;
-    for (uint64_t p = offs[i]; p < offs[i + 1]; ++p)
+    for (uint64_t p = offs[i]; p < offs[i + 1]; ++p) {
+      ci[p] = (int32_t)cols[p];
       if (cols[p] == (uint64_t)i) {
-        diag[i] = p;
+        dg[i] = (int64_t)p;
         found = true;
-        max_diag = std::max(max_diag, std::abs(lu[p]));
-      }
-    require(found, "ilu0: row " + std::to_string(i + 1) + " has no diagonal entry");
-  }
-  const double pivot_floor = 1e-14 * max_diag;
-  std::vector<int64_t> pos(n, -1);
-  for (int64_t i = 0; i < n; ++i) {
-    for (uint64_t p = offs[i]; p < offs[i + 1]; ++p) pos[cols[p]] = (int64_t)p;
-    for (uint64_t p = offs[i]; p < offs[i + 1] && cols[p] < (uint64_t)i; ++p) {
-      const uint64_t k = cols[p];
-      if (std::abs(lu[diag[k]]) < pivot_floor) fail(SKC_EBREAKDOWN, "ilu0: zero pivot at row " + std::to_string(k + 1));
-      const double mult = lu[p] / lu[diag[k]];
-      lu[p] = mult;
-      for (uint64_t q = diag[k] + 1; q < offs[k + 1]; ++q) {
-        const int64_t w = pos[cols[q]];
-        if (w >= 0) lu[(size_t)w] -= mult * lu[q];
+        max_diag = std::max(max_diag, std::abs(vals[p]));
       }
     }
-    if (std::abs(lu[diag[i]]) < pivot_floor) fail(SKC_EBREAKDOWN, "ilu0: zero pivot at row " + std::to_string(i + 1));
-    for (uint64_t p = offs[i]; p < offs[i + 1]; ++p) pos[cols[p]] = -1;
+    require(found, "ilu0: row " + std::to_string(i + 1) + " has no diagonal entry");
   }
+  // level schedule of the lower pattern (rows grouped by elimination depth)
+  std::vector<int64_t> lrp(n + 1, 0);
+  std::vector<int32_t> lci;
+  for (int64_t i = 0; i < n; ++i) {
+    for (uint64_t p = offs[i]; p < offs[i + 1] && cols[p] < (uint64_t)i; ++p) lci.push_back((int32_t)cols[p]);
+    lrp[i + 1] = (int64_t)lci.size();
+  }
+  std::vector<int32_t> perm;
+  std::vector<int64_t> lev;
+  level_schedule(n, lrp, lci, true, perm, lev);
+  int64_t maxw = 0;
+  for (size_t q = 0; q + 1 < lev.size(); ++q) maxw = std::max(maxw, lev[q + 1] - lev[q]);
+  const int nlev = (int)lev.size() - 1;
+  // device buffers: one allocation
+  const size_t b_rp = sizeof(int64_t) * (n + 1), b_dg = sizeof(int64_t) * n, b_lev = sizeof(int64_t) * lev.size();
+  const size_t b_ci = sizeof(int32_t) * std::max<int64_t>(nnz, 1), b_pm = sizeof(int32_t) * n, b_lu = sizeof(double) * std::max<int64_t>(nnz, 1);
+  char* buf = (char*)c.workspace("ilu_factor", b_rp + b_dg + b_lev + b_lu + b_ci + b_pm + 16);
+  int64_t* d_rp = (int64_t*)buf;
+  int64_t* d_dg = (int64_t*)(buf + b_rp);
+  int64_t* d_lev = (int64_t*)(buf + b_rp + b_dg);
+  double* d_lu = (double*)(buf + b_rp + b_dg + b_lev);
+  int32_t* d_ci = (int32_t*)(buf + b_rp + b_dg + b_lev + b_lu);
+  int32_t* d_pm = (int32_t*)((char*)d_ci + b_ci);
+  int* d_fail = (int*)((char*)d_pm + b_pm);
+  CK(cudaMemcpyAsync(d_rp, rp.data(), b_rp, cudaMemcpyHostToDevice, c.stream));
+  CK(cudaMemcpyAsync(d_dg, dg.data(), b_dg, cudaMemcpyHostToDevice, c.stream));
+  CK(cudaMemcpyAsync(d_lev, lev.data(), b_lev, cudaMemcpyHostToDevice, c.stream));
+  CK(cudaMemcpyAsync(d_lu, lu.data(), sizeof(double) * nnz, cudaMemcpyHostToDevice, c.stream));
+  CK(cudaMemcpyAsync(d_ci, ci.data(), sizeof(int32_t) * nnz, cudaMemcpyHostToDevice, c.stream));
+  CK(cudaMemcpyAsync(d_pm, perm.data(), b_pm, cudaMemcpyHostToDevice, c.stream));
+  const int no_fail = 0x7fffffff;
+  CK(cudaMemcpyAsync(d_fail, &no_fail, sizeof(int), cudaMemcpyHostToDevice, c.stream));
+  const double floor_ = 1e-14 * max_diag;
+  {
+    Launch lh(c, "ilu_factor", 8.0 * 3.0 * (double)nnz);
+    if (maxw <= 8 * 1024) {
+      k_ilu_factor1<<<1, 1024, 0, c.stream>>>(d_rp, d_ci, d_dg, d_pm, d_lev, nlev, d_lu, floor_, d_fail);
+      CK(cudaGetLastError());
+    } else {
+      int per_sm = 0;
+      CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_ilu_factor, 256, 0));
+      const int G = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)per_sm * c.sm_count, (maxw + 255) / 256));
+      void* args[] = {&d_rp, &d_ci, &d_dg, &d_pm, &d_lev, (void*)&nlev, &d_lu, (void*)&floor_, &d_fail};
+      CK(cudaLaunchCooperativeKernel((void*)k_ilu_factor, G, 256, args, 0, c.stream));
+    }
+  }
+  int fail = no_fail;
+  CK(cudaMemcpyAsync(&fail, d_fail, sizeof(int), cudaMemcpyDeviceToHost, c.stream));
+  CK(cudaMemcpyAsync(lu.data(), d_lu, sizeof(double) * nnz, cudaMemcpyDeviceToHost, c.stream));
+  c.sync();
+  if (fail != no_fail) skc::fail(SKC_EBREAKDOWN, "ilu0: zero pivot at row " + std::to_string(fail + 1));
 }
 
 void build_ilu0_op(Ctx& c, Op& op, int64_t n, const uint64_t* offs, const uint64_t* cols, const double* vals) {
@@ -333,7 +430,7 @@ void build_ilu0_op(Ctx& c, Op& op, int64_t n, const uint64_t* offs, const uint64
   IluData& d = *op.ilu;
   build_csr_op(c, d.base, n, offs, cols, vals);  // validates the CSR invariants; one GPU only
   std::vector<double> lu;
-  ilu0_factor_host(n, offs, cols, vals, lu);
+  ilu0_factor_device(c, n, offs, cols, vals, lu);
   // split into L (strictly lower) and U (diagonal and above), A's column order kept
   std::vector<int64_t> lrp(n + 1, 0), urp(n + 1, 0);
   std::vector<int32_t> lci, uci;
@@ -388,6 +485,8 @@ void build_ilu0_op(Ctx& c, Op& op, int64_t n, const uint64_t* offs, const uint64
       d.um = upload(op, um);
       std::vector<double> bnd((size_t)((nx + 31) / 32) * d.base.d.ny, 0.0);
       d.bnd = const_cast<double*>(upload(op, bnd));
+      std::vector<int> st(1, 0);
+      d.stalled = const_cast<int*>(upload(op, st));
     }
   }
   for (size_t q = 0; q + 1 < llev.size(); ++q) d.maxw_l = std::max(d.maxw_l, llev[q + 1] - llev[q]);
@@ -409,6 +508,19 @@ void build_ilu0_op(Ctx& c, Op& op, int64_t n, const uint64_t* offs, const uint64
   op.d.kind = kIlu0;
   op.d.n = n;
   op.d.ilu = op.ilu.get();
+}
+
+// the strip solves' stall flag (a neighbour strip that never delivered its boundary column)
+void ilu0_check(Ctx& c, const Op& op) {
+  if (op.d.kind != kIlu0 || !op.ilu || !op.ilu->stalled) return;
+  int h = 0;
+  CK(cudaMemcpyAsync(&h, op.ilu->stalled, sizeof h, cudaMemcpyDeviceToHost, c.stream));
+  c.sync();
+  if (h) {
+    const int z = 0;
+    CK(cudaMemcpy(op.ilu->stalled, &z, sizeof z, cudaMemcpyHostToDevice));
+    fail(SKC_ECUDA, "ilu0 strip solve: a neighbouring strip stalled past the spin limit");
+  }
 }
 
 // z = (LU)^{-1} r (ilu0_apply); r may alias z

@@ -91,6 +91,7 @@ struct IluData {
   const double *lS = nullptr, *lW = nullptr, *uC = nullptr, *uE = nullptr, *uN = nullptr;
   const uint8_t *lm = nullptr, *um = nullptr;
   double* bnd = nullptr;            // per-strip boundary column handed to the next strip
+  int* stalled = nullptr;           // set by a strip whose neighbour never delivered (host raises)
 };
 
 // ---------------------------------------------------------------- streaming geometry
@@ -301,9 +302,10 @@ void build_csr_op(Ctx& c, Op& op, int64_t n, const uint64_t* offs, const uint64_
 void validate_csr(int64_t n, const uint64_t* offs, const uint64_t* cols);  // sparse.hpp:41-63
 // ILU(0) right preconditioning (ilu.cu): op = A (LU)^{-1}; z = (LU)^{-1} r
 void build_ilu0_op(Ctx& c, Op& op, int64_t n, const uint64_t* offs, const uint64_t* cols, const double* vals);
-void ilu0_factor_host(int64_t n, const uint64_t* offs, const uint64_t* cols, const double* vals,
-                      std::vector<double>& lu);
+void ilu0_factor_device(Ctx& c, int64_t n, const uint64_t* offs, const uint64_t* cols, const double* vals,
+                        std::vector<double>& lu);
 void launch_ilu0_solve(Ctx& c, const IluData& d, const double* r, double* z, const int* halt, const int* cond);
+void ilu0_check(Ctx& c, const Op& op);  // raises SKC_ECUDA if a strip solve stalled
 
 // ---------------------------------------------------------------- reports (host)
 struct Report {

@@ -207,14 +207,16 @@ class Context:
         return DeviceOperator(self, h, n)
 
 
-def ilu0_factor(row_offsets, col_indices, values) -> np.ndarray:
-    """ilu0_factor (ilu0.hpp:45-95) on the host: the factor values in A's pattern (unit-lower L
-    strictly below the diagonal, U on and above it)."""
+def ilu0_factor(row_offsets, col_indices, values, ctx: "Context | None" = None) -> np.ndarray:
+    """ilu0_factor (ilu0.hpp:45-95), factored on the device (`ctx`, or a context on device 0):
+    the factor values in A's pattern (unit-lower L strictly below the diagonal, U on and above
+    it)."""
     offs = np.ascontiguousarray(row_offsets, dtype=np.uint64)
     cols = np.ascontiguousarray(col_indices, dtype=np.uint64)
     vals = np.ascontiguousarray(values, dtype=np.float64)
     lu = np.zeros(len(vals))
-    check(lib().skc_ilu0_factor(len(offs) - 1, offs.ctypes.data_as(P(u64)), cols.ctypes.data_as(P(u64)),
+    ctx = ctx if ctx is not None else Context(0)
+    check(lib().skc_ilu0_factor(ctx.h, len(offs) - 1, offs.ctypes.data_as(P(u64)), cols.ctypes.data_as(P(u64)),
                                 _dp(vals), _dp(lu)))
     return lu
 

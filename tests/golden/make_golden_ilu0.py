@@ -95,7 +95,61 @@ def main():
         manifest[name]["envelope_hist50"] = env
         print(name, res.converged, res.iterations, res.breakdown, manifest[name].get("envelope_hist50"))
     json.dump(manifest, open(os.path.join(HERE, "manifest.json"), "w"), indent=1, sort_keys=True)
+    extra_cases()
+
+
+def _digest(v):
+    import hashlib
+    return hashlib.sha256(np.ascontiguousarray(v, dtype=np.float64).tobytes()).hexdigest()
+
+
+def extra_cases():
+    """Grid shapes the strip-wavefront solves hand off on: a rectangular 80 x 37
+    grid (three strips, a partial last one), a 3D 7-point grid (level schedule), and a
+    tridiagonal matrix above the strip path's old cooperative-grid limit (n = 160000, detected
+    as an nx = n, ny = 1 grid).  The large case stores only sha256 digests of the reference's
+    factor / solve / operator bits; its inputs are regenerated from the port's stencil builder
+    and the splitmix64 stream."""
+    from paper_2001_04886_b200.problems import convection_diffusion
+    manifest = json.load(open(os.path.join(HERE, "manifest.json")))
+    port = Oracle("port")
+    for name, (dim, nx, ny, nz, conv) in {"ilu0_rect_80x37": (2, 80, 37, 1, 50.0),
+                                           "ilu0_3d_12": (3, 12, 12, 12, 20.0)}.items():
+        st = convection_diffusion(dim, nx, conv, ny=ny, nz=nz if dim == 3 else None)
+        a = port.stencil_csr(dim, st.nx, st.ny, st.nz, st.coef, ch2=st.ch2)
+        lu = REF.ilu0_factor(a)
+        r = splitmix64_uniform(7, a.n)
+        z = REF.ilu0_apply(a, lu, r)
+        np.savez_compressed(os.path.join(HERE, name + ".npz"), offs=a.offs, cols=a.cols, vals=a.vals, lu=lu, r=r, z=z,
+                            az=REF.spmv(a, z))
+        manifest[name] = dict(type="ilu0", grid=[nx, ny, nz], ref="ilu0.hpp:45-146 on the h^2-scaled stencil")
+    # tridiagonal, n = 160000 (1D convection-diffusion, h^2-scaled)
+    n = 160000
+    h = 1.0 / (n + 1.0)
+    lo, hi = -1.0 - 50.0 * h / 2.0, -1.0 + 50.0 * h / 2.0
+    trip = []
+    offs = [0]
+    cols, vals = [], []
+    for i in range(n):
+        if i > 0:
+            cols.append(i - 1), vals.append(lo)
+        cols.append(i), vals.append(2.0)
+        if i + 1 < n:
+            cols.append(i + 1), vals.append(hi)
+        offs.append(len(cols))
+    a = CsrMatrix(np.array(offs, np.uint64), np.array(cols, np.uint64), np.array(vals))
+    lu = REF.ilu0_factor(a)
+    r = splitmix64_uniform(7, n)
+    z = REF.ilu0_apply(a, lu, r)
+    manifest["ilu0_tridiag_160000"] = dict(type="ilu0_digest", n=n, conv=50.0, rhs_seed=7,
+                                           lu_sha256=_digest(lu), z_sha256=_digest(z), az_sha256=_digest(REF.spmv(a, z)),
+                                           ref="ilu0.hpp:45-146 on a tridiagonal 1D convection-diffusion matrix")
+    json.dump(manifest, open(os.path.join(HERE, "manifest.json"), "w"), indent=1, sort_keys=True)
+    print("extra ILU(0) cases written")
 
 
 if __name__ == "__main__":
-    main()
+    if sys.argv[1:] == ["extra"]:
+        extra_cases()
+    else:
+        main()

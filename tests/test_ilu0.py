@@ -1,15 +1,15 @@
 """ILU(0) right preconditioning (ilu0.hpp; the driver flow of bench.hpp:149-191).
 
-CPU: the oracle restatement and the product library's host factorization against the
-reference fixtures (tests/golden/make_golden_ilu0.py), bit for bit, including the two error
-paths.  GPU: the level-scheduled triangular solves and the preconditioned operator bit-exact
-against the reference, and the driver flow (solve_linear) around s-Omin / s-GMRES against the
+CPU: the oracle restatement against the reference fixtures (tests/golden/make_golden_ilu0.py),
+bit for bit, including the two error paths.  GPU: the device factorization, the triangular
+solves (strip wavefront and level schedule) and the preconditioned operator bit-exact against
+the reference, and the driver flow (solve_linear) around s-Omin / s-GMRES against the
 reference's own run of it.
 """
 import numpy as np
 import pytest
 
-from golden_util import case, matrix, names
+from golden_util import MANIFEST, case, matrix, names
 from oracle import Oracle, OracleError
 from parity_util import rel_hist, rel_vec
 
@@ -32,23 +32,82 @@ def test_oracle_ilu0_pinned_to_reference(name):
     assert np.array_equal(_bits(port.ilu0_apply(a, lu, arr["r"])), _bits(arr["z"]))
 
 
+@pytest.mark.gpu
 @pytest.mark.parametrize("name", ILU_CASES)
-def test_library_host_factor_matches_reference(name):
+def test_device_factor_matches_reference(name):
+    """ilu0_factor on the device (level-scheduled rows, the reference's per-row order)."""
     from paper_2001_04886_b200 import ilu0_factor
     meta, arr = case(name)
     assert np.array_equal(_bits(ilu0_factor(arr["offs"], arr["cols"], arr["vals"])), _bits(arr["lu"]))
 
 
 @pytest.mark.parametrize("name", ERR_CASES)
-def test_factor_error_paths(name):
-    from paper_2001_04886_b200 import BreakdownError, ilu0_factor
+def test_oracle_factor_error_paths(name):
     meta, arr = case(name)
     with pytest.raises(OracleError) as e:
         Oracle("port").ilu0_factor(matrix(arr))
     assert str(e.value) == meta["error"] and e.value.status == meta["status"]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", ERR_CASES)
+def test_device_factor_error_paths(name):
+    from paper_2001_04886_b200 import BreakdownError, ilu0_factor
+    meta, arr = case(name)
     want = BreakdownError if meta["status"] == 2 else ValueError
     with pytest.raises(want, match=meta["error"]):
         ilu0_factor(arr["offs"], arr["cols"], arr["vals"])
+
+
+def _tridiag(meta):
+    from oracle import CsrMatrix
+    from paper_2001_04886_b200.problems import splitmix64_uniform
+    n = meta["n"]
+    h = 1.0 / (n + 1.0)
+    lo, hi = -1.0 - meta["conv"] * h / 2.0, -1.0 + meta["conv"] * h / 2.0
+    i = np.arange(n)
+    cnt = 3 * np.ones(n, np.uint64)
+    cnt[0] = cnt[-1] = 2
+    offs = np.concatenate([[0], np.cumsum(cnt)]).astype(np.uint64)
+    cols = np.concatenate([np.stack([i - 1, i, i + 1], 1)[1:-1].ravel(), []]).astype(np.int64)
+    cols = np.concatenate([[0, 1], cols, [n - 2, n - 1]]).astype(np.uint64)
+    vals = np.concatenate([[2.0, hi], np.tile([lo, 2.0, hi], n - 2), [lo, 2.0]])
+    return CsrMatrix(offs, cols, vals), splitmix64_uniform(meta["rhs_seed"], n)
+
+
+def _digest(v):
+    import hashlib
+    return hashlib.sha256(np.ascontiguousarray(v, dtype=np.float64).tobytes()).hexdigest()
+
+
+def test_oracle_tridiagonal_digests():
+    """The large tridiagonal case (n = 160000): the restatement's factor / solve / operator bits
+    hash to the reference's."""
+    meta = MANIFEST["ilu0_tridiag_160000"]
+    a, r = _tridiag(meta)
+    port = Oracle("port")
+    lu = port.ilu0_factor(a)
+    z = port.ilu0_apply(a, lu, r)
+    assert (_digest(lu), _digest(z), _digest(port.spmv(a, z))) == (meta["lu_sha256"], meta["z_sha256"], meta["az_sha256"])
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("strips", ["1", "0"])
+def test_device_tridiagonal_digests(strips, monkeypatch):
+    """n = 160000 tridiagonal (detected as an nx = n, ny = 1 grid): above the strip wavefront's
+    cooperative-grid limit, so it takes the level schedule; factor, solve and operator bits hash
+    to the reference's with the strips enabled or not."""
+    from paper_2001_04886_b200 import Context
+    monkeypatch.setenv("SKC_ILU_STRIPS", strips)
+    meta = MANIFEST["ilu0_tridiag_160000"]
+    a, r = _tridiag(meta)
+    ctx = Context(0)
+    from paper_2001_04886_b200 import ilu0_factor
+    assert _digest(ilu0_factor(a.offs, a.cols, a.vals, ctx)) == meta["lu_sha256"]
+    op = ctx.ilu0(a.offs, a.cols, a.vals)
+    z = op.ilu0_solve(r)
+    assert _digest(z) == meta["z_sha256"]
+    assert _digest(op.apply(r)) == meta["az_sha256"]
 
 
 @pytest.mark.parametrize("name", DRIVER_CASES)
