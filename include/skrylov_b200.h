@@ -227,6 +227,12 @@ int skc_ctx_create_nccl(int device, int rank, int world, const void* id128, skc_
 int skc_ctx_create_callback(int device, int rank, int world, skc_allgather_fn allgather, skc_halo_fn halo,
                             void* user, skc_ctx** out);
 int skc_ctx_world(const skc_ctx* ctx, int* rank, int* world);
+/* GPU-count-independent reductions: every dot product is summed over a fixed tree of 64 row
+ * groups of the global grid (rows % 64 == 0), so a solve on 1, 2, 4 or 8 GPUs gives bitwise the
+ * same results.  On by default for multi-rank contexts (SKC_PINDEP=0 turns it off); on a single
+ * GPU it is opt-in and disables the single-GPU-only kernels (block-iteration kernel, persistent
+ * s-Omin) to reproduce the slab results bit for bit.  Not in the reference. */
+int skc_ctx_set_gpu_independent(skc_ctx* ctx, int enable);
 /* slab of the global stencil owned by ctx's rank; kcell_global (n_global entries) for kind 1 */
 int skc_op_create_stencil_slab(skc_ctx* ctx, const skc_stencil_desc* global_desc, const double* kcell_global,
                                uint64_t* row_lo, uint64_t* row_hi, skc_op** out);

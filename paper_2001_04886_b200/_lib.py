@@ -72,7 +72,7 @@ EXPORTS = [
     "skc_report_get_breakdown", "skc_report_get_note", "skc_somin_solve", "skc_sgmres_solve", "skc_smr_solve",
     "skc_gmres_solve", "skc_smr_step", "skc_somin_solve_device", "skc_sgmres_solve_device", "skc_sarnoldi",
     "skc_gram_solve", "skc_cholesky_upper", "skc_hessenberg_lsq",
-    "skc_nccl_unique_id", "skc_ctx_create_nccl", "skc_ctx_create_callback", "skc_ctx_world",
+    "skc_nccl_unique_id", "skc_ctx_create_nccl", "skc_ctx_create_callback", "skc_ctx_world", "skc_ctx_set_gpu_independent",
     "skc_op_create_stencil_slab", "skc_slab_range",
     "skc_op_create_ilu0", "skc_ilu0_solve", "skc_ilu0_solve_device", "skc_ilu0_factor", "skc_fill_lognormal", "skc_discretize",
 ]
@@ -129,6 +129,7 @@ def lib():
         "skc_ctx_create_nccl": [C.c_int, C.c_int, C.c_int, vp, P(vp)],
         "skc_ctx_create_callback": [C.c_int, C.c_int, C.c_int, ALLGATHER_FN, HALO_FN, vp, P(vp)],
         "skc_ctx_world": [vp, P(C.c_int), P(C.c_int)],
+        "skc_ctx_set_gpu_independent": [vp, C.c_int],
         "skc_op_create_stencil_slab": [vp, P(StencilDescC), P(dbl), P(u64), P(u64), P(vp)],
         "skc_slab_range": [u64, C.c_int, C.c_int, P(u64), P(u64)],
         "skc_op_create_ilu0": [vp, u64, P(u64), P(u64), P(dbl), P(vp)],

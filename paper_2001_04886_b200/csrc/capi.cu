@@ -100,7 +100,15 @@ skc_ctx* make_ctx(int device) {
   if (const char* e = std::getenv("SKC_SPOW")) ctx->c.spow = std::atoi(e) != 0;
   if (const char* e = std::getenv("SKC_LSQ_OVERLAP")) ctx->c.lsq_overlap = std::atoi(e) != 0;
   if (const char* e = std::getenv("SKC_ILU_STRIPS")) ctx->c.ilu_strips = std::atoi(e) != 0;
+  if (const char* e = std::getenv("SKC_PINDEP")) ctx->c.gpu_independent = std::atoi(e) != 0;
+  if (const char* e = std::getenv("SKC_REORTH_SYNC")) ctx->c.reorth_host_sync = std::atoi(e) != 0;
   return ctx;
+}
+
+// multi-rank contexts reduce GPU-count-independently unless SKC_PINDEP=0
+void default_gpu_independent(skc_ctx* ctx) {
+  const char* e = std::getenv("SKC_PINDEP");
+  ctx->c.gpu_independent = e ? std::atoi(e) != 0 : true;
 }
 
 extern "C" {
@@ -597,6 +605,7 @@ int skc_ctx_create_nccl(int device, int rank, int world, const void* id128, skc_
       delete ctx;
       throw;
     }
+    default_gpu_independent(ctx);
     *out = ctx;
   });
 }
@@ -608,7 +617,15 @@ int skc_ctx_create_callback(int device, int rank, int world, skc_allgather_fn al
     skc::require(world >= 1 && rank >= 0 && rank < world, "skc_ctx_create_callback: bad rank/world");
     skc_ctx* ctx = make_ctx(device);
     ctx->c.comm = skc::make_callback_comm(rank, world, allgather, halo, user);
+    default_gpu_independent(ctx);
     *out = ctx;
+  });
+}
+
+int skc_ctx_set_gpu_independent(skc_ctx* ctx, int enable) {
+  return guarded([&] {
+    skc::require(ctx != nullptr, "null context");
+    ctx->c.gpu_independent = enable != 0;
   });
 }
 

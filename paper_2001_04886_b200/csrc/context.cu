@@ -44,6 +44,29 @@ Geo make_geo(int64_t n, int sm_count) {
   G = (n + range - 1) / range;
   g.G = (int)std::max<int64_t>(1, G);
   g.range = range;
+  g.cpg = g.G;
+  g.gsize = n;
+  return g;
+}
+
+Geo make_geo_for(const Ctx& c, const Op& op) {
+  const int W = c.world();
+  const int64_t R = op.d.rows_global > 0 ? op.d.rows_global : op.rows;  // global rows of the slowest dimension
+  const int64_t L = op.rowlen > 0 ? op.rowlen : (op.rows > 0 ? op.n / op.rows : 1);
+  if (!c.gpu_independent || R % kGroups != 0 || kGroups % W != 0 || L <= 0 || op.d.kind == kIlu0)
+    return make_geo(op.n, c.sm_count);
+  Geo g;
+  g.n = op.n;
+  g.gsize = (R / kGroups) * L;
+  if (g.gsize * (kGroups / W) != op.n) return make_geo(op.n, c.sm_count);
+  // about two CTAs per SM at 8 GPUs (37 per group); never below 256 points per CTA
+  g.cpg = (int)std::max<int64_t>(1, std::min<int64_t>(37, (g.gsize + 255) / 256));
+  int64_t range = (g.gsize + g.cpg - 1) / g.cpg;
+  range = (range + 255) / 256 * 256;
+  g.cpg = (int)((g.gsize + range - 1) / range);
+  g.range = range;
+  g.G = (kGroups / W) * g.cpg;
+  require(g.G <= kPartialPitch, "grouped geometry: too many partials");
   return g;
 }
 
@@ -164,6 +187,17 @@ Op::~Op() {
 
 // ---------------------------------------------------------------- multi-rank reductions / halos
 namespace {
+// grouped partials (Geo::enc): per (dot, local group) the sum of its cpg partials in order --
+// the first level of reduce_dots_dev's grouped sum -- into out[group * nd + dot]
+__global__ void k_local_group_sums(const double* partials, int ngrp, int cpg, int d0, int nd, double* out) {
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < ngrp * nd; e += gridDim.x * blockDim.x) {
+    const int grp = e / nd, d = e % nd;
+    const double* p = partials + (int64_t)(d0 + d) * kPartialPitch + (int64_t)grp * cpg;
+    double s = 0.0;
+    for (int j = 0; j < cpg; ++j) s += p[j];
+    out[e] = s;
+  }
+}
 // per-rank sums of dots [d0, d0+nd) over G CTA partials (same fixed order as the scalar kernels)
 __global__ void k_local_reduce(const double* partials, int G, int d0, int nd, double* out) {
   for (int d = blockIdx.x; d < nd; d += gridDim.x) {  // one warp per dot, fixed lane order
@@ -187,13 +221,28 @@ __global__ void k_scatter_ranks(const double* recv, int world, int nd, double* p
 int Ctx::reduce_point(double* partials, int G, int d0, int nd) {
   if (!comm || comm->world == 1 || nd <= 0) return G;
   const int W = comm->world;
-  constexpr int kRing = 16;
-  double* buf = (double*)workspace("reduce_ring", (size_t)kRing * 2 * 4096 * sizeof(double));
-  require(nd <= 4096 && (size_t)W * nd <= 4096 * 2 - 4096, "reduce_point: too many dots for one exchange");
-  double* send = buf + (size_t)(reduce_ring % kRing) * 2 * 4096;
-  double* recv = send + 4096;
+  constexpr int kRing = 16, kSlot = 32768;
+  double* buf = (double*)workspace("reduce_ring", (size_t)kRing * 2 * kSlot * sizeof(double));
+  double* send = buf + (size_t)(reduce_ring % kRing) * 2 * kSlot;
+  double* recv = send + kSlot;
   ++reduce_ring;
   ++launches;
+  if (G >> 16) {  // grouped: allgather each rank's group sums; the kGroups sums, in order, become the partials
+    const int Gn = G & 0xffff, cpg = G >> 16, ngl = Gn / cpg;
+    require((size_t)ngl * nd <= (size_t)kSlot && (size_t)W * ngl * nd <= (size_t)kSlot,
+            "reduce_point: too many dots for one exchange");
+    k_local_group_sums<<<std::max(1, std::min(64, (ngl * nd + 255) / 256)), 256, 0, stream>>>(partials, ngl, cpg, d0, nd,
+                                                                                            send);
+    CK(cudaGetLastError());
+    comm->allgather(send, recv, (size_t)ngl * nd, stream);
+    ++launches;
+    // recv[(r ngl + g) nd + d] = group (r ngl + g)'s sum: partial column r ngl + g
+    k_scatter_ranks<<<std::max(1, std::min(64, (W * ngl * nd + 255) / 256)), 256, 0, stream>>>(recv, W * ngl, nd,
+                                                                                             partials, d0);
+    CK(cudaGetLastError());
+    return (W * ngl) | (1 << 16);
+  }
+  require(nd <= 4096 && (size_t)W * nd <= (size_t)kSlot, "reduce_point: too many dots for one exchange");
   k_local_reduce<<<std::min(nd, 64), 32, 0, stream>>>(partials, G, d0, nd, send);
   CK(cudaGetLastError());
   comm->allgather(send, recv, (size_t)nd, stream);

@@ -149,8 +149,38 @@ __device__ __forceinline__ void cp_async_wait() {
 // Each dot is owned by a group of TPD lanes (TPD = 32 >> k, chosen so all dots are covered
 // in few rounds); every lane sums a fixed strided subset with four independent accumulators
 // (loads stay in flight), then the group combines in a fixed shuffle order.
+// Grouped partials (G >> 16 = cpg, Geo::enc): sum every group's cpg partials in order, then the
+// group sums in order -- a fixed tree whatever the GPU count (reduce_point allgathers the group
+// sums across ranks and passes them on with cpg = 1).  One warp per dot.
+__device__ __forceinline__ void reduce_dots_grouped(const double* __restrict__ partials, int G, int d0, int nd,
+                                                    double* out) {
+  const int Gn = G & 0xffff, cpg = G >> 16, ngrp = Gn / cpg;
+  const int lane = threadIdx.x & 31, nwarp = blockDim.x >> 5;
+  for (int d = threadIdx.x >> 5; d < nd; d += nwarp) {
+    const double* p = partials + (int64_t)(d0 + d) * kPartialPitch;
+    double gs[2] = {0.0, 0.0};  // groups lane and lane + 32 (at most 64 groups)
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int grp = lane + 32 * h;
+      if (grp < ngrp) {
+        double a = 0.0;
+        for (int j = 0; j < cpg; ++j) a += p[grp * cpg + j];
+        gs[h] = a;
+      }
+    }
+    double tot = 0.0;
+    for (int grp = 0; grp < ngrp; ++grp) tot += __shfl_sync(0xffffffffu, (grp >> 5) ? gs[1] : gs[0], grp & 31);
+    if (lane == 0) out[d] = tot;
+  }
+  __syncthreads();
+}
+
 __device__ __forceinline__ void reduce_dots_dev(const double* __restrict__ partials, int G, int d0, int nd,
                                                 double* out) {
+  if (G >> 16) {
+    reduce_dots_grouped(partials, G, d0, nd, out);
+    return;
+  }
   const int nthreads = blockDim.x;
   int tpd = 32;
   while (tpd > 1 && (nthreads / tpd) < nd) tpd >>= 1;

@@ -1543,7 +1543,7 @@ void gmres_device(Ctx& c, const Op& op, const double* f, double* x, uint64_t m64
   const int m = (int)m64;
   const int64_t n = op.n;
   const size_t np = pad_n(n);
-  const Geo g = make_geo(n, c.sm_count);
+  const Geo g = make_geo_for(c, op);
   skc_op_counter& cnt = rep.op_counts;
   cnt.stored_vectors = m64 + 4;
   double* V = (double*)c.workspace("gm_vec", (size_t)(m + 4) * np * sizeof(double));
@@ -1574,7 +1574,7 @@ void gmres_device(Ctx& c, const Op& op, const double* f, double* x, uint64_t m64
     }
     lb.add_dot(0, 0);
     lb.launch(c, g, coef, ncoef, partials, 0, nullptr, nullptr, "residual");
-    launch_k(c, k_gm_rn, 1, 256, 0, st, partials, c.reduce_point(partials, g.G, 0, 1), 0);
+    launch_k(c, k_gm_rn, 1, 256, 0, st, partials, c.reduce_point(partials, g.enc(), 0, 1), 0);
     ++c.launches;
   };
   const bool x_zero = device_is_zero(c, x, n);
@@ -1603,7 +1603,7 @@ void gmres_device(Ctx& c, const Op& op, const double* f, double* x, uint64_t m64
       launch_apply(c, op.d, q(j - 1), w, halt, nullptr);
       launch_gram_list(c, g, {q(0)}, {w}, partials, 0, halt, nullptr, "gram");
       for (int i = 0; i < j; ++i) {
-        launch_k(c, k_gm_col, 1, 256, 0, st, col, i, coef, cC, partials, c.reduce_point(partials, g.G, 0, 1), 0);
+        launch_k(c, k_gm_col, 1, 256, 0, st, col, i, coef, cC, partials, c.reduce_point(partials, g.enc(), 0, 1), 0);
         ++c.launches;
         LinBuilder lb;  // w -= col_i q_i ; next dot
         lb.add_out(w, w);
@@ -1616,7 +1616,7 @@ void gmres_device(Ctx& c, const Op& op, const double* f, double* x, uint64_t m64
         }
         lb.launch(c, g, coef, ncoef, partials, 0, halt, nullptr, "mgs_update");
       }
-      launch_k(c, k_gm_sub, 1, 256, 0, st, j, col, coef, cInv, partials, c.reduce_point(partials, g.G, 0, 1), 0);
+      launch_k(c, k_gm_sub, 1, 256, 0, st, j, col, coef, cInv, partials, c.reduce_point(partials, g.enc(), 0, 1), 0);
       ++c.launches;
       LinBuilder lb;
       lb.add_out(q(j), w, cInv);
@@ -1736,7 +1736,7 @@ struct Engine {
   // points per CTA of the on-chip orthogonalization (one CTA per SM), or 0 when it is off or
   // the candidate slices do not fit in shared memory
   int64_t orth_points() const {
-    if (!c.orth || c.world() != 1 || s < 2 || op.d.kind == kIlu0) return 0;
+    if (!c.orth || c.world() != 1 || g.grouped() || s < 2 || op.d.kind == kIlu0) return 0;
     const int64_t P = ((op.n + mk_ctas() - 1) / mk_ctas() + 1) & ~(int64_t)1;
     return orth_smem(s, m, P) <= kOrthSmemCap ? P : 0;
   }
@@ -1885,7 +1885,7 @@ struct Engine {
 
   Engine(Ctx& ctx, const Op& o, int s_, int m_, bool fixed = false)
       : c(ctx), op(o), s(s_), m(m_), rl{s_, m_}, cl{s_, m_}, dl{s_, m_} {
-    g = make_geo(op.n, c.sm_count);
+    g = make_geo_for(c, op);
     np = pad_n(op.n);
     const size_t nvec = (size_t)(m + 1) * s + 4;
     V = (double*)c.workspace("arn_vec", nvec * np * sizeof(double));
@@ -1947,7 +1947,7 @@ struct Engine {
         for (int j = 0; j <= d; ++j) outs[j] = col(b, done + j);
         if (done > 0) outs[0] = nullptr;  // already written by the previous sweep
         const double* X[kMaxS];
-        const bool fuse = dots && done == 0 && d == J && J <= kMpkMaxDotDepth;
+        const bool fuse = dots && done == 0 && d == J && J <= kMpkMaxDotDepth && !g.grouped();
         for (int l = 0; l < s; ++l) X[l] = col(0, l);
         const int G0 = launch_mpk(c, op.d, from, sc, outs, d, fuse ? s : 0, X, 1, partials, dl.D(), halt, nullptr);
         if (fuse) Gd = G0;
@@ -1979,12 +1979,12 @@ struct Engine {
     host_reorth = -1;
     CK(cudaMemsetAsync(rec, 0, (size_t)(m + 1) * rl.size() * sizeof(double), c.stream));
     if (!use_rn) launch_gram_list(c, g, {v}, {v}, partials, dl.RR(), nullptr, nullptr, "gram");
-    const int Gc = use_rn ? g.G : c.reduce_point(partials, g.G, dl.RR(), 1);
+    const int Gc = use_rn ? g.enc() : c.reduce_point(partials, g.enc(), dl.RR(), 1);
     launch_k(c, k_arn_ctor, 1, 256, 0, st, use_rn ? 1 : 0, partials, Gc, dl.RR(), recp(0), coef, cl.Inv());
     ++c.launches;
     krylov_into(0, v);
     gram_self_into(0, dl.Wa(), nullptr);
-    const int Gw = c.reduce_point(partials, g.G, dl.Wa(), s * s);
+    const int Gw = c.reduce_point(partials, g.enc(), dl.Wa(), s * s);
     dispatch_s(s, [&](auto S_) {
       constexpr int S = decltype(S_)::value;
       launch_k(c, k_arn_ctor_push<S>, 1, 256, 0, lq, (const double*)partials, Gw, dl.Wa());
@@ -2047,7 +2047,7 @@ struct Engine {
     }
     lb.add_dot(0, 0);
     lb.launch(c, g, coef, cl.size(), partials, dl.RR(), nullptr, nullptr, "residual");
-    launch_k(c, k_arn_rn, 1, 256, 0, st, partials, c.reduce_point(partials, g.G, dl.RR(), 1), dl.RR(), rn_out);
+    launch_k(c, k_arn_rn, 1, 256, 0, st, partials, c.reduce_point(partials, g.enc(), dl.RR(), 1), dl.RR(), rn_out);
     ++c.launches;
   }
 
@@ -2072,7 +2072,7 @@ struct Engine {
       L.push_back(z);
       launch_gram_list(c, g, L, {z}, partials, dl.Z(), halt, zcond, zcond ? "gram_z_redo" : "gram_z");
     }
-    launch_k(c, k_arn_s1, 1, 256, 0, st, grams, k, rk, coef, partials, c.reduce_point(partials, g.G, dl.Z(), k * s + 1), dl.Z(), s, cl.H(), scratch);
+    launch_k(c, k_arn_s1, 1, 256, 0, st, grams, k, rk, coef, partials, c.reduce_point(partials, g.enc(), dl.Z(), k * s + 1), dl.Z(), s, cl.H(), scratch);
     ++c.launches;
     // seed = z - sum_i V_i h_i ; ||seed||^2
     {
@@ -2083,7 +2083,7 @@ struct Engine {
       lb.add_dot(0, 0);
       lb.launch(c, g, coef, cl.size(), partials, dl.Seed(), halt, nullptr, "seed_update");
     }
-    launch_k(c, k_arn_s2, 1, 256, 0, st, k, rk, coef, partials, c.reduce_point(partials, g.G, dl.Seed(), 1), dl.Seed(), cl.Inv());
+    launch_k(c, k_arn_s2, 1, 256, 0, st, k, rk, coef, partials, c.reduce_point(partials, g.enc(), dl.Seed(), 1), dl.Seed(), cl.Inv());
     ++c.launches;
     // candidate block [v, .., A^{s-1} v] of the normalized seed (also on the last block)
     const int cb = k;  // block slot k (slot m is scratch when k == m)
@@ -2097,7 +2097,11 @@ struct Engine {
     bool wb_needed = true;  // the reorthogonalized W region must be made global for the push
     if (s > 1) {
       for (int pass = 0; pass < 2; ++pass) {
-        if (pass == 1 && c.world() > 1) {
+        // Across ranks the second pass is enqueued under the device flag like on one GPU: its
+        // kernels skip when the test did not fire, its collectives run (on stale, unused values)
+        // so every rank issues the same sequence without a host round trip.  SKC_REORTH_SYNC=1
+        // reads the decision back instead (one stream sync per block iteration, no idle collectives).
+        if (pass == 1 && c.world() > 1 && c.reorth_host_sync) {
           host_reorth = read_state().reorth;
           if (!host_reorth) {
             wb_needed = false;
@@ -2114,7 +2118,7 @@ struct Engine {
           launch_gram_list(c, g, L, Cr, partials, dl.D(), halt, cond, pass ? "gram_mgs_reorth" : "gram_mgs");
         }
         for (int i = 0; i < k; ++i) {
-          const int Gi = (i == 0 && have) ? Gfused : g.G;
+          const int Gi = (i == 0 && have) ? Gfused : g.enc();
           // Scalar2 against block i (sstep.hpp:338-353) runs in the update kernel's prologue:
           // t = W_i^{-1} V_i^T cand[:,1:], recorded at block i of this iteration's T area
           const MgsScalar sc{partials, c.reduce_point(partials, Gi, dl.Dr(i), s * (s - 1)), dl.Dr(i), grams + i,
@@ -2153,7 +2157,7 @@ struct Engine {
             zfused = true;
           }
           launch_gram_map(c, g, L, R, cols, partials, halt, nullptr, "gram_cross");
-          launch_k(c, k_arn_check, 1, 256, 0, st, grams, k, rk, partials, c.reduce_point(partials, g.G, dl.Cross(), k * s * s + s * s), dl.Cross(), dl.Cross() + k * s * s, s, 1e-8, scratch);
+          launch_k(c, k_arn_check, 1, 256, 0, st, grams, k, rk, partials, c.reduce_point(partials, g.enc(), dl.Cross(), k * s * s + s * s), dl.Cross(), dl.Cross() + k * s * s, s, 1e-8, scratch);
           ++c.launches;
         } else {
           gram_self_into(cb, dl.Wb(), cond, "gram_w_reorth");
@@ -2165,8 +2169,8 @@ struct Engine {
     // the push reads W from the reorthogonalized region when the device flag says so: make
     // both regions global (the unused one is stale but harmless)
     // (for s > 1 the dWa region was already made global together with the cross products)
-    const int Gw = s > 1 ? (wb_needed ? c.reduce_point(partials, g.G, dl.Wb(), s * s) : c.world())
-                         : c.reduce_point(partials, g.G, dWa, s * s);
+    const int Gw = s > 1 ? (wb_needed ? c.reduce_point(partials, g.enc(), dl.Wb(), s * s) : c.world())
+                         : c.reduce_point(partials, g.enc(), dWa, s * s);
     launch_k(c, k_arn_push, 1, 256, 0, st, grams, cb, rk, rl.wraw(), (const double*)partials, Gw, dWa, dl.Wb(), s);
     ++c.launches;
     lsq_fork(k, true);

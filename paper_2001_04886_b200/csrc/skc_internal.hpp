@@ -98,17 +98,34 @@ struct IluData {
 // Every streaming kernel of a solve uses the same fixed CTA decomposition of [0, n):
 // CTA g owns the contiguous range [g*range, min(n,(g+1)*range)) and writes one partial per
 // dot, so reductions are deterministic (fixed order, no atomics).
+// Grouped (GPU-count-independent) form: the global grid's rows are cut into kGroups equal groups
+// (every slab of 1, 2, 4 or 8 ranks is a whole number of them) and each group into cpg CTA
+// ranges of `range` points, so CTA b owns [(b / cpg) gsize + (b % cpg) range, ...) of its group
+// and every partial covers the same points whatever the GPU count; reductions then sum each
+// group's cpg partials in order and the kGroups group sums in order (reduce_dots_dev).
+// Ungrouped: cpg = G, gsize = n (CTA b owns [b range, (b+1) range)).
 struct Geo {
   int64_t n = 0;
   int G = 1;
   int64_t range = 0;
+  int cpg = 1;
+  int64_t gsize = 0;
+  bool grouped() const { return cpg != G || gsize != n; }
+  // the partial count as the reductions take it: G, or G | cpg << 16 for grouped partials
+  int enc() const { return grouped() ? (G | (cpg << 16)) : G; }
 };
 Geo make_geo(int64_t n, int sm_count);
+constexpr int kGroups = 64;
+struct Op;
+struct Ctx;
+// the geometry every streaming kernel of a solve on `op` uses: grouped when the context asks
+// for GPU-count-independent reductions and the grid qualifies, else make_geo
+Geo make_geo_for(const Ctx& c, const Op& op);
 
 constexpr int kThreads = 256;
 // every reduction partial lives at partials[dot * kPartialPitch + cta]: kernels with different
 // CTA counts can share one partial buffer without overlapping regions
-constexpr int kPartialPitch = 2048;
+constexpr int kPartialPitch = 4096;
 
 // y_o = base_o [* coef[bscale_o]] + sum_j coef[cbase_j + o] * in_j   (j ascending, o in mask_j)
 // then dots over value ids: 0..nout-1 = outputs, nout..nout+nx-1 = extra inputs.
@@ -128,6 +145,8 @@ struct LinDesc {
   double* partials;    // [(dot0 + d) * G + g]
   int dot0, G;
   int64_t n, range;
+  int cpg;             // grouped geometry (Geo): CTAs per group, points per group
+  int64_t gsize;
   const int* halt;     // skip when *halt != 0
   const int* cond;     // skip when cond != nullptr && *cond == 0
 };
@@ -145,6 +164,8 @@ struct GramDesc {
   int mapped;
   int rbase[GR_MAXR], rstride[GR_MAXR], lmax[GR_MAXR];
   int64_t n, range;
+  int cpg;
+  int64_t gsize;
   const int* halt;
   const int* cond;
 };
@@ -188,7 +209,12 @@ struct Ctx {
   bool zfuse = false;   // megakernel: next Scalar1 products in the cross pass (SKC_ZFUSE=1)
   bool persist = true;  // persistent s-Omin for small problems (SKC_PERSIST=0 disables)
   bool spow = true;     // megakernel: row-streamed candidate powers (SKC_SPOW=0 disables)
-  bool lsq_overlap = true;  // s-GMRES least squares on the side stream (SKC_LSQ_OVERLAP=0: in line)
+  // GPU-count-independent reductions (grouped geometry): bitwise the same results on 1, 2, 4
+  // or 8 GPUs; on by default across ranks, opt-in on one GPU (SKC_PINDEP=1 /
+  // skc_ctx_set_gpu_independent), where it turns the single-GPU-only kernels off
+  bool gpu_independent = false;
+  bool lsq_overlap = true;
+  bool reorth_host_sync = false;  // slabs: read the reorthogonalization decision back (SKC_REORTH_SYNC=1)  // s-GMRES least squares on the side stream (SKC_LSQ_OVERLAP=0: in line)
   bool ilu_strips = true;  // ILU(0) on 2D grids: strip-wavefront solves (SKC_ILU_STRIPS=0 disables)
   std::map<std::string, KStat> stats;
   struct Pending {

@@ -104,6 +104,10 @@ struct LinBuilder {
       d.G = g.G;
       d.n = g.n;
       d.range = g.range;
+    d.cpg = g.cpg;
+    d.gsize = g.gsize;
+      d.cpg = g.cpg;
+      d.gsize = g.gsize;
       d.halt = halt;
       d.cond = cond;
       launch_lincomb(c, d, name);
@@ -148,6 +152,8 @@ inline void launch_gram_list(Ctx& c, const Geo& g, const std::vector<const doubl
     d.G = g.G;
     d.n = g.n;
     d.range = g.range;
+    d.cpg = g.cpg;
+    d.gsize = g.gsize;
     d.halt = halt;
     d.cond = cond;
     launch_gram(c, d, name);
@@ -182,6 +188,8 @@ inline void launch_gram_map(Ctx& c, const Geo& g, const std::vector<const double
     d.G = g.G;
     d.n = g.n;
     d.range = g.range;
+    d.cpg = g.cpg;
+    d.gsize = g.gsize;
     d.halt = halt;
     d.cond = cond;
     launch_gram(c, d, name);

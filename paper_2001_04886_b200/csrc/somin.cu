@@ -552,7 +552,7 @@ void somin_device(Ctx& c, const Op& op, const double* f, double* x, const SStepC
   const int s = (int)cfg.s;
   const int64_t n = op.n;
   const size_t np = pad_n(n);
-  const Geo g = make_geo(n, c.sm_count);
+  const Geo g = make_geo_for(c, op);
   rep.steady_iteration = gcr ? cfg.max_iterations + 1 : cfg.k;
 
   // window capacity (entries) and slot count
@@ -568,7 +568,9 @@ void somin_device(Ctx& c, const Op& op, const double* f, double* x, const SStepC
   double* K = V + 2 * np;
   auto slot_p = [&](int sl, int col) { return V + (2 + s + (size_t)sl * 2 * s + col) * np; };
   auto slot_ap = [&](int sl, int col) { return V + (2 + s + (size_t)sl * 2 * s + s + col) * np; };
-  const int dRR = 0, dW = 1, dM = 1 + s * s, dC = dM + s, dX = dC + (int)kwin * s * s;
+  // dot regions: W, m (one reduction point), then ||r||^2 directly followed by the C_e products,
+  // so an s-step needs two reduction points across ranks
+  const int dW = 0, dM = s * s, dRR = dM + s, dC = dRR + 1, dX = dC + (int)kwin * s * s;
   const int ndots = dX + (int)kwin * s * s;
   double* partials = (double*)c.workspace("somin_partials", (size_t)ndots * kPartialPitch * sizeof(double));
   const int ncoef = cB(s) + (int)kwin * s * s;
@@ -595,7 +597,7 @@ void somin_device(Ctx& c, const Op& op, const double* f, double* x, const SStepC
   // ---- initial residual (solvers.hpp:58-76) and setup (sstep.hpp:164-178)
   const bool x_zero = device_is_zero(c, x, n);
   initial_residual_dev(c, op, g, f, x, r, ax, x_zero, coef, ncoef, cMinus1(s), partials, dRR);
-  launch_k(c, k_somin_start, 1, 256, 0, st, partials, c.reduce_point(partials, g.G, dRR, 1), dRR);
+  launch_k(c, k_somin_start, 1, 256, 0, st, partials, c.reduce_point(partials, g.enc(), dRR, 1), dRR);
   ++c.launches;
   CK(cudaGetLastError());
   // krylov_pair(r): P0 = [r, Ar, .., A^{s-1} r], AP0 = [Ar, .., A^s r]
@@ -609,7 +611,7 @@ void somin_device(Ctx& c, const Op& op, const double* f, double* x, const SStepC
     for (int j = 0; j < s; ++j) L.push_back(slot_ap(0, j));
     launch_gram_list(c, g, L, L, partials, dW, halt, nullptr, "gram_w");
     launch_gram_list(c, g, L, {r}, partials, dM, halt, nullptr, "gram_m");
-    launch_k(c, k_somin_setup, 1, 256, 0, st, grams, coef, partials, c.reduce_point(partials, g.G, dW, s * s + s), dW, dM, s);
+    launch_k(c, k_somin_setup, 1, 256, 0, st, grams, coef, partials, c.reduce_point(partials, g.enc(), dW, s * s + s), dW, dM, s);
     ++c.launches;
     CK(cudaGetLastError());
   }
@@ -625,7 +627,7 @@ void somin_device(Ctx& c, const Op& op, const double* f, double* x, const SStepC
   CK(cudaMemcpyAsync(&hs, st, sizeof hs, cudaMemcpyDeviceToHost, c.stream));
   c.sync();
   // small problems: whole iterations in one cooperative launch per chunk (see k_somin_persist)
-  if (c.persist && op.d.kind != kIlu0 && !gcr && !cfg.debug_checks && c.world() == 1 && s <= 4 && cfg.k <= (uint64_t)PS_MAXK &&
+  if (c.persist && !g.grouped() && op.d.kind != kIlu0 && !gcr && !cfg.debug_checks && c.world() == 1 && s <= 4 && cfg.k <= (uint64_t)PS_MAXK &&
       n <= (1 << 18)) {
     PersistDesc pd;
     std::memset(&pd, 0, sizeof pd);
@@ -676,8 +678,8 @@ void somin_device(Ctx& c, const Op& op, const double* f, double* x, const SStepC
         lb.add_dot(1, 1);
         lb.launch(c, g, coef, ncoef, partials, dRR, halt, nullptr, "xr_update");
       }
-      launch_k(c, k_somin_norm, 1, 256, 0, st, partials, c.reduce_point(partials, g.G, dRR, 1), dRR, hist);
-      ++c.launches;
+      // (the termination test on ||r|| runs after the C_e products below, sharing their reduction
+      // point: the powers and products of the final iteration are spent for nothing, once)
       // krylov_pair(r) -> K[j] = A^{j+1} r  (matrix-powers sweep)
       powers(c, op, r, K, np, s, halt);
       // C_e = AP_e^T AR   (block_gram, sstep.hpp:207)
@@ -691,8 +693,10 @@ void somin_device(Ctx& c, const Op& op, const double* f, double* x, const SStepC
         for (int j = 0; j < s; ++j) R.push_back(K + (size_t)j * np);
         launch_gram_list(c, g, L, R, partials, dC, halt, nullptr, "gram_c");
       }
-      launch_k(c, k_somin_proj, 1, 256, 0, st, grams, ws, coef, partials, c.reduce_point(partials, g.G, dC, ws.n * s * s), dC, s, scratch);
-      ++c.launches;
+      const int Grc = c.reduce_point(partials, g.enc(), dRR, 1 + ws.n * s * s);  // ||r||^2 and C_e together
+      launch_k(c, k_somin_norm, 1, 256, 0, st, partials, Grc, dRR, hist);
+      launch_k(c, k_somin_proj, 1, 256, 0, st, grams, ws, coef, partials, Grc, dC, s, scratch);
+      c.launches += 2;
       // new slot: P = R + sum_e P_e b_e ; AP = AR + sum_e AP_e b_e ; W ; m  (sstep.hpp:215-222)
       if (free_slots.empty()) {  // s-GCR window at the device limit
         gcr_full = true;
@@ -700,7 +704,7 @@ void somin_device(Ctx& c, const Op& op, const double* f, double* x, const SStepC
       }
       const int nsl = free_slots.back();
       free_slots.pop_back();
-      {
+      if (2 * s <= 8) {  // one fused launch: P and AP halves share the powers block R / AR
         LinBuilder lb;
         for (int jc = 0; jc < s; ++jc) lb.add_out(slot_p(nsl, jc), jc == 0 ? r : K + (size_t)(jc - 1) * np);
         for (int jc = 0; jc < s; ++jc) lb.add_out(slot_ap(nsl, jc), K + (size_t)jc * np);
@@ -714,6 +718,26 @@ void somin_device(Ctx& c, const Op& op, const double* f, double* x, const SStepC
           for (int b = a; b < s; ++b) lb.add_dot(s + a, s + b);
         for (int a = 0; a < s; ++a) lb.add_dot(s + a, 2 * s);
         lb.launch(c, g, coef, ncoef, partials, dW, halt, nullptr, "block_update");
+      } else {
+        // s > 4: the P half and the AP half as two launches of s outputs each.  One launch would
+        // stage 2ks + s + 2 distinct vectors per point tile (s = 8: ~41) -- kilobyte-sized bulk
+        // copies from that many streams and 2s accumulators per thread (measured 1.8 TB/s on C5);
+        // the halves re-read the s - 1 shared powers once more but stream at the narrow rate.
+        // Every output keeps its terms in the same order (same bits); W and m ride on the AP half.
+        LinBuilder lp, la;
+        for (int jc = 0; jc < s; ++jc) lp.add_out(slot_p(nsl, jc), jc == 0 ? r : K + (size_t)(jc - 1) * np);
+        for (int jc = 0; jc < s; ++jc) la.add_out(slot_ap(nsl, jc), K + (size_t)jc * np);
+        const uint16_t all = (uint16_t)((1u << s) - 1u);
+        for (size_t e = 0; e < win.size(); ++e) {
+          for (int l = 0; l < s; ++l) lp.add_term(slot_p(win[e], l), all, cB(s) + (int)e * s * s + l * s);
+          for (int l = 0; l < s; ++l) la.add_term(slot_ap(win[e], l), all, cB(s) + (int)e * s * s + l * s);
+        }
+        la.add_extra(r);
+        for (int a = 0; a < s; ++a)
+          for (int b = a; b < s; ++b) la.add_dot(a, b);
+        for (int a = 0; a < s; ++a) la.add_dot(a, s);
+        lp.launch(c, g, coef, ncoef, partials, dW, halt, nullptr, "block_update");
+        la.launch(c, g, coef, ncoef, partials, dW, halt, nullptr, "block_update");
       }
       if (cfg.debug_checks) {
         std::vector<const double*> L, R;
@@ -722,8 +746,8 @@ void somin_device(Ctx& c, const Op& op, const double* f, double* x, const SStepC
         for (int j = 0; j < s; ++j) R.push_back(slot_ap(nsl, j));
         launch_gram_list(c, g, L, R, partials, dX, halt, nullptr, "gram_debug");
       }
-      int Gp = c.reduce_point(partials, g.G, dW, s * (s + 1) / 2 + s);
-      if (cfg.debug_checks) Gp = c.reduce_point(partials, g.G, dX, ws.n * s * s);
+      int Gp = c.reduce_point(partials, g.enc(), dW, s * (s + 1) / 2 + s);
+      if (cfg.debug_checks) Gp = c.reduce_point(partials, g.enc(), dX, ws.n * s * s);
       launch_k(c, k_somin_push, 1, 256, 0, st, grams, nsl, coef, partials, Gp, dW, dW + s * (s + 1) / 2, s, cfg.debug_checks ? 1 : 0, ws, dX, scratch);
       ++c.launches;
       CK(cudaGetLastError());
@@ -878,7 +902,7 @@ static void smr_step_enqueue(Ctx& c, const Op& op, const Geo& g, double* x, doub
   for (int j = 0; j < s; ++j) AR.push_back(K + (size_t)j * np);
   launch_gram_list(c, g, AR, AR, partials, 1, halt, nullptr, "gram_w");
   launch_gram_list(c, g, AR, {r}, partials, 1 + s * s, halt, nullptr, "gram_m");
-  launch_k(c, k_smr_solve, 1, 256, 0, st, coef, partials, c.reduce_point(partials, g.G, 1, s * s + s), 1, 1 + s * s, s);
+  launch_k(c, k_smr_solve, 1, 256, 0, st, coef, partials, c.reduce_point(partials, g.enc(), 1, s * s + s), 1, 1 + s * s, s);
   ++c.launches;
   // x += R a (R = [r, A r, .., A^{s-1} r]); r -= AR a  (sstep.hpp:102-103)
   LinBuilder lb;
@@ -889,7 +913,7 @@ static void smr_step_enqueue(Ctx& c, const Op& op, const Geo& g, double* x, doub
   for (int l = 0; l < s; ++l) lb.add_term(K + (size_t)l * np, 2u, s + l - 1);
   lb.add_dot(1, 1);
   lb.launch(c, g, coef, ncoef, partials, 0, halt, nullptr, "xr_update");
-  launch_k(c, k_smr_norm, 1, 256, 0, st, partials, c.reduce_point(partials, g.G, 0, 1), 0, hist);
+  launch_k(c, k_smr_norm, 1, 256, 0, st, partials, c.reduce_point(partials, g.enc(), 0, 1), 0, hist);
   ++c.launches;
   CK(cudaGetLastError());
 }
@@ -899,7 +923,7 @@ void smr_device(Ctx& c, const Op& op, const double* f, double* x, const SStepCfg
   const int s = (int)cfg.s;
   const int64_t n = op.n;
   const size_t np = pad_n(n);
-  const Geo g = make_geo(n, c.sm_count);
+  const Geo g = make_geo_for(c, op);
   double* V = (double*)c.workspace("smr_vec", (2 + (size_t)s) * np * sizeof(double));
   double *r = V, *ax = V + np, *K = V + 2 * np;
   const int ncoef = 2 * s + 1;
@@ -919,7 +943,7 @@ void smr_device(Ctx& c, const Op& op, const double* f, double* x, const SStepCfg
   }
   const bool x_zero = device_is_zero(c, x, n);
   initial_residual_dev(c, op, g, f, x, r, ax, x_zero, coef, ncoef, 2 * s, partials, 0);
-  launch_k(c, k_smr_start, 1, 256, 0, st, partials, c.reduce_point(partials, g.G, 0, 1), 0, hist);
+  launch_k(c, k_smr_start, 1, 256, 0, st, partials, c.reduce_point(partials, g.enc(), 0, 1), 0, hist);
   ++c.launches;
   uint64_t enq = 0;
   const uint64_t batch = n <= (1 << 16) ? 32 : 8;
@@ -966,7 +990,7 @@ void smr_step_device(Ctx& c, const Op& op, double* x, double* r, uint64_t s64, d
   const int s = (int)s64;
   const int64_t n = op.n;
   const size_t np = pad_n(n);
-  const Geo g = make_geo(n, c.sm_count);
+  const Geo g = make_geo_for(c, op);
   double* K = (double*)c.workspace("smr_vec", (2 + (size_t)s) * np * sizeof(double)) + 2 * np;
   const int ncoef = 2 * s + 1;
   double* coef = (double*)c.workspace("smr_coef", ncoef * sizeof(double));

@@ -39,6 +39,8 @@ constexpr int GRM_MAXU = GR_MAXL + GR_MAXR;
 struct PipeHdr {
   int nu, T, nstage;
   int64_t n, range;
+  int cpg;
+  int64_t gsize;
   const int* halt;
   const int* cond;
 };
@@ -108,8 +110,11 @@ __device__ __forceinline__ Pipe pipe_setup(const PipeHdr& h, unsigned char* smem
   p.empty = p.full + kMaxStage;
   p.stages = reinterpret_cast<double*>(smem_raw + 64 + prefix_bytes);
   p.stage_sz = (size_t)h.nu * h.T;
-  p.r0 = (int64_t)blockIdx.x * h.range;
-  p.r1 = min(h.n, p.r0 + h.range);
+  {  // (grouped geometry: CTA b is member b % cpg of group b / cpg)
+    const int64_t grp = blockIdx.x / h.cpg, mem = blockIdx.x % h.cpg;
+    p.r0 = grp * h.gsize + mem * h.range;
+    p.r1 = min(min(h.n, (grp + 1) * h.gsize), p.r0 + h.range);
+  }
   p.ntiles = p.r1 > p.r0 ? (int)((p.r1 - p.r0 + h.T - 1) / h.T) : 0;
   if (threadIdx.x == 0) {
     for (int s = 0; s < h.nstage; ++s) {
@@ -643,12 +648,15 @@ void launch_mgs_t(Ctx& c, const MgsDesc& d, size_t smem, int G) {
   }
 }
 
-void fill_hdr(PipeHdr& h, int nu, const TileChoice& tc, int64_t n, int64_t range, const int* halt, const int* cond) {
+void fill_hdr(PipeHdr& h, int nu, const TileChoice& tc, int64_t n, int64_t range, int cpg, int64_t gsize,
+              const int* halt, const int* cond) {
   h.nu = nu;
   h.T = tc.T;
   h.nstage = tc.nstage;
   h.n = n;
   h.range = range;
+  h.cpg = cpg > 0 ? cpg : 1 << 30;
+  h.gsize = cpg > 0 ? gsize : n;
   h.halt = halt;
   h.cond = cond;
 }
@@ -733,7 +741,7 @@ void launch_lincomb(Ctx& c, const LinDesc& L, const char* name) {
   TileChoice tc;
   const int Tmax = nout_t <= 8 ? 2 * CONS : CONS;
   if (!try_pick_tiles(nu, prefix, Tmax, CONS, false, tc)) tc = pick_tiles(nu, prefix, Tmax, 64, false);
-  fill_hdr(d.h, nu, tc, L.n, L.range, L.halt, L.cond);
+  fill_hdr(d.h, nu, tc, L.n, L.range, L.cpg, L.gsize, L.halt, L.cond);
   const double bytes = 8.0 * (double)L.n * (nu + L.nout);
   Launch lh(c, name, bytes);
   switch (nout_t) {
@@ -767,7 +775,7 @@ void launch_gram(Ctx& c, const GramDesc& g, const char* name) {
   TileChoice tc = pick_tiles(nu, 0, 2048, 64);
   const size_t red = 64 + (size_t)NCW * 8 * GR_MAXR * 8;
   tc.smem = std::max(tc.smem, red);
-  fill_hdr(d.h, nu, tc, g.n, g.range, g.halt, g.cond);
+  fill_hdr(d.h, nu, tc, g.n, g.range, g.cpg, g.gsize, g.halt, g.cond);
   const double bytes = 8.0 * (double)g.n * nu;
   Launch lh(c, name, bytes);
   switch (g.nr) {
@@ -804,7 +812,7 @@ void launch_mgs(Ctx& c, const Geo& geo, int s, const double* const* Vi, double* 
   d.G = geo.G;
   TileChoice tc = pick_tiles(nu, kMgsPrefix, 2048, 64);
   tc.smem = std::max(tc.smem, 64 + (size_t)kMgsPrefix + 8 * (size_t)NCW * 56);
-  fill_hdr(d.h, nu, tc, geo.n, geo.range, halt, cond);
+  fill_hdr(d.h, nu, tc, geo.n, geo.range, geo.cpg, geo.gsize, halt, cond);
   const double bytes = 8.0 * (double)geo.n * (nu + s - 1);
   Launch lh(c, name, bytes);
 #define SKC_MGS_CASE(SV)                                                \

@@ -147,6 +147,10 @@ class Context:
     def set_stream(self, stream_handle: int):
         check(lib().skc_ctx_set_stream(self.h, stream_handle))
 
+    def set_gpu_independent(self, on: bool):
+        """GPU-count-independent reductions (bitwise the same results on 1, 2, 4 or 8 GPUs)."""
+        check(lib().skc_ctx_set_gpu_independent(self.h, int(on)))
+
     def set_profiling(self, on: bool):
         check(lib().skc_ctx_set_profiling(self.h, int(on)))
 

@@ -142,3 +142,49 @@ def test_slab_sgmres_with_reorthogonalization_passes():
     assert out[0][9]
     a = Oracle("port").stencil_csr(st.dim, st.nx, st.ny, st.nz, st.coef)
     assert np.linalg.norm(f - Oracle("port").spmv(a, x)) <= cfg["tol"] * (1 + 1e-6)
+
+
+def _pindep_cases():
+    from oracle import Oracle
+    from paper_2001_04886_b200 import convection_diffusion, splitmix64_uniform
+    st2 = convection_diffusion(2, 64, 10.0)
+    f2 = splitmix64_uniform(20010486, st2.n)
+    t2 = 1e-8 * float(np.linalg.norm(f2))
+    st2c = convection_diffusion(2, 64, 50.0)
+    f2c = splitmix64_uniform(20010486, st2c.n)
+    st3 = convection_diffusion(3, 16, 20.0, nz=64, variable_k=True)
+    k3 = Oracle("port").lognormal(4886, st3.n)
+    f3 = splitmix64_uniform(20010486, st3.n)
+    return {
+        "somin2d": (st2, f2, None, "somin", dict(s=4, k=2, tol=t2, max_iterations=200)),
+        "sgmres2d_s4m10": (st2c, f2c, None, "sgmres", dict(s=4, m=10, tol=1e-8 * float(np.linalg.norm(f2c)))),
+        "somin3d_vark": (st3, f3, k3, "somin", dict(s=4, k=2, tol=0.0, max_iterations=20)),
+    }
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", ["somin2d", "sgmres2d_s4m10", "somin3d_vark"])
+def test_results_independent_of_gpu_count(name):
+    """GPU-count-independent reductions (skc_ctx_set_gpu_independent; SURVEY 8(c) multi-GPU
+    bullet): every dot product is summed over the same tree of 64 row groups, so the slab solve
+    on 1, 2 and 4 ranks and the single-GPU solve with the option on give bitwise the same
+    residual history, op history and iterate -- including s-GMRES s=4 m=10, where a summation
+    order change would otherwise flip reorthogonalization decisions."""
+    from paper_2001_04886_b200 import Context, SStepConfig, sgmres_solve, somin_solve
+    case = _pindep_cases()[name]
+    st, f, kcell, method, cfg = case
+    runs = {}
+    for world in (1, 2, 4):
+        out = _spawn(dist_workers.gpu_slab_worker, world, case)
+        runs[world] = (out[0][4], out[0][7], np.concatenate([o[3] for o in out]))
+    ctx = Context(0)
+    ctx.set_gpu_independent(True)
+    x1 = np.zeros(st.n)
+    fn = somin_solve if method == "somin" else sgmres_solve
+    rep = fn(ctx.stencil(st, kcell=kcell), f, x1, SStepConfig(**cfg))
+    runs[0] = (rep.residual_history, rep.op_history, x1)
+    h0, oh0, xb = runs[1]
+    for world, (h, oh, x) in runs.items():
+        assert h == h0, world
+        assert oh == oh0, world
+        assert np.array_equal(x.view(np.uint64), xb.view(np.uint64)), world
