@@ -59,8 +59,9 @@ Geo make_geo_for(const Ctx& c, const Op& op) {
   g.n = op.n;
   g.gsize = (R / kGroups) * L;
   if (g.gsize * (kGroups / W) != op.n) return make_geo(op.n, c.sm_count);
-  // about two CTAs per SM at 8 GPUs (37 per group); never below 256 points per CTA
-  g.cpg = (int)std::max<int64_t>(1, std::min<int64_t>(37, (g.gsize + 255) / 256));
+  // 32 CTAs per group: 2048 partials on one GPU (the pitch), 256 per GPU at 8 GPUs; never below
+  // 256 points per CTA
+  g.cpg = (int)std::max<int64_t>(1, std::min<int64_t>(32, (g.gsize + 255) / 256));
   int64_t range = (g.gsize + g.cpg - 1) / g.cpg;
   range = (range + 255) / 256 * 256;
   g.cpg = (int)((g.gsize + range - 1) / range);

@@ -125,7 +125,7 @@ Geo make_geo_for(const Ctx& c, const Op& op);
 constexpr int kThreads = 256;
 // every reduction partial lives at partials[dot * kPartialPitch + cta]: kernels with different
 // CTA counts can share one partial buffer without overlapping regions
-constexpr int kPartialPitch = 4096;
+constexpr int kPartialPitch = 2048;
 
 // y_o = base_o [* coef[bscale_o]] + sum_j coef[cbase_j + o] * in_j   (j ascending, o in mask_j)
 // then dots over value ids: 0..nout-1 = outputs, nout..nout+nx-1 = extra inputs.
@@ -213,8 +213,8 @@ struct Ctx {
   // or 8 GPUs; on by default across ranks, opt-in on one GPU (SKC_PINDEP=1 /
   // skc_ctx_set_gpu_independent), where it turns the single-GPU-only kernels off
   bool gpu_independent = false;
-  bool lsq_overlap = true;
-  bool reorth_host_sync = false;  // slabs: read the reorthogonalization decision back (SKC_REORTH_SYNC=1)  // s-GMRES least squares on the side stream (SKC_LSQ_OVERLAP=0: in line)
+  bool lsq_overlap = true;        // s-GMRES least squares on the side stream (SKC_LSQ_OVERLAP=0: in line)
+  bool reorth_host_sync = false;  // slabs: read the reorthogonalization decision back (SKC_REORTH_SYNC=1)
   bool ilu_strips = true;  // ILU(0) on 2D grids: strip-wavefront solves (SKC_ILU_STRIPS=0 disables)
   std::map<std::string, KStat> stats;
   struct Pending {

@@ -678,8 +678,14 @@ void somin_device(Ctx& c, const Op& op, const double* f, double* x, const SStepC
         lb.add_dot(1, 1);
         lb.launch(c, g, coef, ncoef, partials, dRR, halt, nullptr, "xr_update");
       }
-      // (the termination test on ||r|| runs after the C_e products below, sharing their reduction
-      // point: the powers and products of the final iteration are spent for nothing, once)
+      // across ranks the termination test on ||r|| runs after the C_e products below, sharing
+      // their reduction point (the powers and products of the final iteration are spent for
+      // nothing, once); on one GPU it runs here
+      const bool pack_rr = c.world() > 1;
+      if (!pack_rr) {
+        launch_k(c, k_somin_norm, 1, 256, 0, st, partials, c.reduce_point(partials, g.enc(), dRR, 1), dRR, hist);
+        ++c.launches;
+      }
       // krylov_pair(r) -> K[j] = A^{j+1} r  (matrix-powers sweep)
       powers(c, op, r, K, np, s, halt);
       // C_e = AP_e^T AR   (block_gram, sstep.hpp:207)
@@ -693,10 +699,15 @@ void somin_device(Ctx& c, const Op& op, const double* f, double* x, const SStepC
         for (int j = 0; j < s; ++j) R.push_back(K + (size_t)j * np);
         launch_gram_list(c, g, L, R, partials, dC, halt, nullptr, "gram_c");
       }
-      const int Grc = c.reduce_point(partials, g.enc(), dRR, 1 + ws.n * s * s);  // ||r||^2 and C_e together
-      launch_k(c, k_somin_norm, 1, 256, 0, st, partials, Grc, dRR, hist);
-      launch_k(c, k_somin_proj, 1, 256, 0, st, grams, ws, coef, partials, Grc, dC, s, scratch);
-      c.launches += 2;
+      if (pack_rr) {
+        const int Grc = c.reduce_point(partials, g.enc(), dRR, 1 + ws.n * s * s);  // ||r||^2 and C_e together
+        launch_k(c, k_somin_norm, 1, 256, 0, st, partials, Grc, dRR, hist);
+        launch_k(c, k_somin_proj, 1, 256, 0, st, grams, ws, coef, partials, Grc, dC, s, scratch);
+        c.launches += 2;
+      } else {
+        launch_k(c, k_somin_proj, 1, 256, 0, st, grams, ws, coef, partials, c.reduce_point(partials, g.enc(), dC, ws.n * s * s), dC, s, scratch);
+        ++c.launches;
+      }
       // new slot: P = R + sum_e P_e b_e ; AP = AR + sum_e AP_e b_e ; W ; m  (sstep.hpp:215-222)
       if (free_slots.empty()) {  // s-GCR window at the device limit
         gcr_full = true;

@@ -91,7 +91,7 @@ __device__ __forceinline__ TileGeom tile_geom(const PipeHdr& h, int64_t r0, int6
   TileGeom g;
   g.start = r0 + (int64_t)t * h.T;
   g.cnt = (int)(r1 - g.start < (int64_t)h.T ? r1 - g.start : (int64_t)h.T);
-  g.bulk = (g.cnt & 1) == 0;  // bulk copies move multiples of 16 bytes
+  g.bulk = ((g.cnt | (int)g.start) & 1) == 0;  // bulk copies move 16-byte-aligned multiples of 16 bytes
   return g;
 }
 
@@ -648,14 +648,14 @@ void launch_mgs_t(Ctx& c, const MgsDesc& d, size_t smem, int G) {
   }
 }
 
-void fill_hdr(PipeHdr& h, int nu, const TileChoice& tc, int64_t n, int64_t range, int cpg, int64_t gsize,
+void fill_hdr(PipeHdr& h, int nu, const TileChoice& tc, int64_t n, int64_t range, int G, int cpg, int64_t gsize,
               const int* halt, const int* cond) {
   h.nu = nu;
   h.T = tc.T;
   h.nstage = tc.nstage;
   h.n = n;
   h.range = range;
-  h.cpg = cpg > 0 ? cpg : 1 << 30;
+  h.cpg = cpg > 0 ? cpg : G;  // (descriptors without a geometry: one group of all G CTAs)
   h.gsize = cpg > 0 ? gsize : n;
   h.halt = halt;
   h.cond = cond;
@@ -741,7 +741,7 @@ void launch_lincomb(Ctx& c, const LinDesc& L, const char* name) {
   TileChoice tc;
   const int Tmax = nout_t <= 8 ? 2 * CONS : CONS;
   if (!try_pick_tiles(nu, prefix, Tmax, CONS, false, tc)) tc = pick_tiles(nu, prefix, Tmax, 64, false);
-  fill_hdr(d.h, nu, tc, L.n, L.range, L.cpg, L.gsize, L.halt, L.cond);
+  fill_hdr(d.h, nu, tc, L.n, L.range, L.G, L.cpg, L.gsize, L.halt, L.cond);
   const double bytes = 8.0 * (double)L.n * (nu + L.nout);
   Launch lh(c, name, bytes);
   switch (nout_t) {
@@ -775,7 +775,7 @@ void launch_gram(Ctx& c, const GramDesc& g, const char* name) {
   TileChoice tc = pick_tiles(nu, 0, 2048, 64);
   const size_t red = 64 + (size_t)NCW * 8 * GR_MAXR * 8;
   tc.smem = std::max(tc.smem, red);
-  fill_hdr(d.h, nu, tc, g.n, g.range, g.cpg, g.gsize, g.halt, g.cond);
+  fill_hdr(d.h, nu, tc, g.n, g.range, g.G, g.cpg, g.gsize, g.halt, g.cond);
   const double bytes = 8.0 * (double)g.n * nu;
   Launch lh(c, name, bytes);
   switch (g.nr) {
@@ -812,7 +812,7 @@ void launch_mgs(Ctx& c, const Geo& geo, int s, const double* const* Vi, double* 
   d.G = geo.G;
   TileChoice tc = pick_tiles(nu, kMgsPrefix, 2048, 64);
   tc.smem = std::max(tc.smem, 64 + (size_t)kMgsPrefix + 8 * (size_t)NCW * 56);
-  fill_hdr(d.h, nu, tc, geo.n, geo.range, geo.cpg, geo.gsize, halt, cond);
+  fill_hdr(d.h, nu, tc, geo.n, geo.range, geo.G, geo.cpg, geo.gsize, halt, cond);
   const double bytes = 8.0 * (double)geo.n * (nu + s - 1);
   Launch lh(c, name, bytes);
 #define SKC_MGS_CASE(SV)                                                \
