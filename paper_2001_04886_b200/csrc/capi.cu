@@ -1,4 +1,5 @@
 // capi.cu -- the C ABI (include/skrylov_b200.h) over the C++ solvers.
+#include <algorithm>
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
@@ -102,6 +103,7 @@ skc_ctx* make_ctx(int device) {
   if (const char* e = std::getenv("SKC_ILU_STRIPS")) ctx->c.ilu_strips = std::atoi(e) != 0;
   if (const char* e = std::getenv("SKC_PINDEP")) ctx->c.gpu_independent = std::atoi(e) != 0;
   if (const char* e = std::getenv("SKC_REORTH_SYNC")) ctx->c.reorth_host_sync = std::atoi(e) != 0;
+  if (const char* e = std::getenv("SKC_MPK3")) ctx->c.mpk3 = std::atoi(e) != 0;
   return ctx;
 }
 
@@ -412,7 +414,20 @@ int skc_krylov_block(skc_ctx* ctx, const skc_op* op, const double* v, uint64_t s
     const size_t n = (size_t)op->o.n;
     double* b = (double*)c.workspace("io_block", n * s * sizeof(double));
     CK(cudaMemcpyAsync(b, v, n * sizeof(double), cudaMemcpyHostToDevice, c.stream));
-    for (uint64_t j = 1; j < s; ++j) skc::launch_apply(c, op->o.d, b + (j - 1) * n, b + j * n, nullptr, nullptr);
+    // the matrix-powers sweeps where the operator has them (chained by depth), else applies
+    const int maxj = s > 1 ? skc::powers_depth(c, op->o.d) : 0;
+    uint64_t done = 0;
+    while (done + 1 < s) {
+      const int J = (int)std::min<uint64_t>(s - 1 - done, maxj > 0 ? (uint64_t)maxj : 1);
+      if (maxj > 0) {
+        double* outs[skc::kMaxS + 1] = {nullptr};
+        for (int j = 1; j <= J; ++j) outs[j] = b + (done + j) * n;
+        skc::launch_mpk(c, op->o.d, b + done * n, nullptr, outs, J, 0, nullptr, 1, nullptr, 0, nullptr, nullptr);
+      } else {
+        skc::launch_apply(c, op->o.d, b + done * n, b + (done + 1) * n, nullptr, nullptr);
+      }
+      done += J;
+    }
     CK(cudaMemcpyAsync(out, b, n * s * sizeof(double), cudaMemcpyDeviceToHost, c.stream));
     c.sync();
   });

@@ -593,7 +593,13 @@ void dispatch_j(Ctx& c, MpkDesc& d) {
 }  // namespace
 
 int mpk_max_depth(const DevOp& op) { return op.kind == kCsr || op.kind == kIlu0 ? 0 : op.dim == 2 ? MPK_MAXJ : 3; }
-int powers_depth(const Ctx& c, const DevOp& op) { return op.dim == 3 && c.world() == 1 ? 0 : mpk_max_depth(op); }
+// on one GPU the constant 3D stencil takes the one-sweep 2.5D kernel (mpk3.cu, depth <= 4); the
+// other 3D operators the single-level applies (the ghost-zone tile sweep of k_mpk3d loses to
+// them there); slabs need k_mpk3d for the halos
+int powers_depth(const Ctx& c, const DevOp& op) {
+  if (op.dim == 3 && c.world() == 1) return op.kind == kStencilConst && c.mpk3 ? 4 : 0;
+  return mpk_max_depth(op);
+}
 
 // Powers of src*scale: out[0] (level 0, may be null) .. out[J].  Products X[x] . level j for
 // j >= jdot0 are written at dot0 + x*(J-jdot0+1) + (j-jdot0); returns the partial count G.
@@ -601,6 +607,7 @@ int launch_mpk(Ctx& c, const DevOp& op, const double* src, const double* scale, 
                int nxd, const double* const* X, int jdot0, double* partials, int dot0, const int* halt,
                const int* cond, const char* name) {
   require(op.kind != kCsr, "mpk: general CSR operators use repeated applies");
+  if (nxd == 0 && c.world() == 1 && c.mpk3 && launch_mpk3(c, op, src, scale, out, J, halt, cond, name)) return 0;
   require(J >= 1 && J <= mpk_max_depth(op), "mpk: depth out of range");
   require(nxd == 0 || (nxd == J + 1 && jdot0 <= 1 && J <= kMpkMaxDotDepth),
           "mpk: fused products need J+1 vectors against levels 1..J (J <= 3)");

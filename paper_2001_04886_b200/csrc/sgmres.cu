@@ -508,32 +508,61 @@ __global__ void k_arn_lsq(const ArnLsqDesc d, int k, int build_next, int cap) {
 // residual estimate above tol hands the cycle to the fallback (x untouched); otherwise y from the
 // back substitution (its rank failure is the reference's breakdown) -- y lands in the update
 // coefficients, zero beyond the appended columns, so the fixed x update adds exact zeros there
+// (the back substitution is a serial chain of M(M+1)/2 dependent steps: R, the right-hand side
+// and y are staged in shared memory when they fit -- M <= kFinSmemCols -- else read in place)
+constexpr int kFinSmemCols = 128;
+__host__ __device__ inline size_t fin_smem_doubles(int M) {
+  return M <= kFinSmemCols ? (size_t)M * (M + 1) / 2 + 2 * (size_t)M + 8 : 8;
+}
 __global__ void k_arn_finish(const ArnLsqDesc d, double* ycoef) {
   SKC_PDL_ENTRY();
+  extern __shared__ __align__(16) double fin_sm[];
+  __shared__ int s_go;
   const int M = d.m * d.s;
+  const LsqView lv = lsq_view(d.lsq, M);
+  ArnState* st = d.st;
+  if (threadIdx.x == 0) {
+    const int stv = st->status;
+    int go = 1;
+    if (stv == kArnCtorZero || stv == kArnCtorCollapse || stv == kArnCtorChol) {
+      st->fin = kFinNone;
+      go = 0;
+    } else {
+      const int ls = st->lstatus;
+      const bool collapsed = ls == kArnPushCollapse || ls == kArnCholCollapse;
+      const bool attainable = lv.h->cols > 0 && lv.h->residual <= d.tol;
+      if (collapsed && !attainable) {
+        st->fin = kFinFallback;
+        go = 0;
+      }
+    }
+    s_go = go;
+  }
   for (int i = threadIdx.x; i < M; i += blockDim.x) ycoef[i] = 0.0;
   __syncthreads();
-  if (threadIdx.x != 0) return;
-  ArnState* st = d.st;
-  const int stv = st->status;
-  if (stv == kArnCtorZero || stv == kArnCtorCollapse || stv == kArnCtorChol) {
-    st->fin = kFinNone;
-    return;
+  if (!s_go) return;
+  const int cols = lv.h->cols;
+  LsqHdr* sh = reinterpret_cast<LsqHdr*>(fin_sm);
+  LsqView sv = lv;
+  if (M <= kFinSmemCols) {  // stage R, rhs
+    double* p = fin_sm + 4;
+    sv.h = sh;
+    sv.R = p;
+    sv.rhs = p + (size_t)M * (M + 1) / 2;
+    sv.y = sv.rhs + M;
+    const int nr = cols * (cols + 1) / 2;
+    for (int e = threadIdx.x; e < nr; e += blockDim.x) sv.R[e] = lv.R[e];
+    for (int e = threadIdx.x; e < cols; e += blockDim.x) sv.rhs[e] = lv.rhs[e];
+    if (threadIdx.x == 0) *sh = *lv.h;
+    __syncthreads();
   }
-  const LsqView lv = lsq_view(d.lsq, M);
-  const int ls = st->lstatus;
-  const bool collapsed = ls == kArnPushCollapse || ls == kArnCholCollapse;
-  const bool attainable = lv.h->cols > 0 && lv.h->residual <= d.tol;
-  if (collapsed && !attainable) {
-    st->fin = kFinFallback;
-    return;
+  if (threadIdx.x == 0) {
+    const bool ok = lsq_solve(sv, st->fixed != 0);
+    lv.h->rank_col = sv.h->rank_col;
+    st->fin = ok ? kFinOk : kFinLsqFail;
+    if (ok)
+      for (int i = 0; i < cols; ++i) ycoef[i] = sv.y[i];
   }
-  if (!lsq_solve(lv, st->fixed != 0)) {
-    st->fin = kFinLsqFail;
-    return;
-  }
-  for (int i = 0; i < lv.h->cols; ++i) ycoef[i] = lv.y[i];
-  st->fin = kFinOk;
 }
 
 // Scalar1 (sstep.hpp:301-310): zn = ||z||, h_i = W_i^{-1} V_i^T z
@@ -1947,7 +1976,9 @@ struct Engine {
         for (int j = 0; j <= d; ++j) outs[j] = col(b, done + j);
         if (done > 0) outs[0] = nullptr;  // already written by the previous sweep
         const double* X[kMaxS];
-        const bool fuse = dots && done == 0 && d == J && J <= kMpkMaxDotDepth && !g.grouped();
+        // (on one GPU the 3D powers take the one-sweep kernel, which fuses no products)
+        const bool fuse = dots && done == 0 && d == J && J <= kMpkMaxDotDepth && !g.grouped() &&
+                          !(op.d.dim == 3 && c.world() == 1);
         for (int l = 0; l < s; ++l) X[l] = col(0, l);
         const int G0 = launch_mpk(c, op.d, from, sc, outs, d, fuse ? s : 0, X, 1, partials, dl.D(), halt, nullptr);
         if (fuse) Gd = G0;
@@ -2025,7 +2056,9 @@ struct Engine {
   // coefficients past the appended columns), r = f - A x and ||r|| (st->rn, rn_out)
   void enqueue_finish(const double* f, double* x) {
     lsq_join();
-    launch_k(c, k_arn_finish, 1, 256, 0, lq, coef + cl.Y());
+    const size_t fsm = sizeof(double) * fin_smem_doubles(m * s);
+    ensure_smem(k_arn_finish, fsm);
+    launch_k(c, k_arn_finish, 1, 256, fsm, lq, coef + cl.Y());
     ++c.launches;
     LinBuilder lb;
     lb.add_out(x, x);

@@ -213,6 +213,7 @@ struct Ctx {
   // or 8 GPUs; on by default across ranks, opt-in on one GPU (SKC_PINDEP=1 /
   // skc_ctx_set_gpu_independent), where it turns the single-GPU-only kernels off
   bool gpu_independent = false;
+  bool mpk3 = false;             // one-sweep 3D powers on one GPU (SKC_MPK3=1; slower than the applies so far)
   bool lsq_overlap = true;        // s-GMRES least squares on the side stream (SKC_LSQ_OVERLAP=0: in line)
   bool reorth_host_sync = false;  // slabs: read the reorthogonalization decision back (SKC_REORTH_SYNC=1)
   bool ilu_strips = true;  // ILU(0) on 2D grids: strip-wavefront solves (SKC_ILU_STRIPS=0 disables)
@@ -302,6 +303,10 @@ int mpk_max_depth(const DevOp& op);
 int powers_depth(const Ctx& c, const DevOp& op);
 constexpr int kMpkMaxDotDepth = 3;  // deepest sweep that can fuse products (launch_mpk)
 enum : uint8_t { kHintNormal = 0, kHintFirst = 1, kHintLast = 2 };  // L2 policies of streamed vectors
+// one-sweep 3D powers on one GPU (mpk3.cu): constant 7-point stencil, J <= 4; false when the
+// operator / depth does not qualify (the caller then uses launch_mpk or repeated applies)
+bool launch_mpk3(Ctx& c, const DevOp& op, const double* src, const double* scale, double* const* out, int J,
+                 const int* halt, const int* cond, const char* name = "mpk3");
 int launch_mpk(Ctx& c, const DevOp& op, const double* src, const double* scale, double* const* out, int J, int nxd,
                const double* const* X, int jdot0, double* partials, int dot0, const int* halt, const int* cond,
                const char* name = "mpk");

@@ -429,3 +429,26 @@ def test_megakernel_streamed_powers_bit_identical(monkeypatch, s):
     assert a.residual_history == b.residual_history and a.block_rho == b.block_rho
     assert np.array_equal(xa.view(np.uint64), xb.view(np.uint64))
     assert a.iterations == 2 * 6 * s
+
+
+@pytest.mark.parametrize("dims", [(37, 29, 23), (64, 48, 40)])
+@pytest.mark.parametrize("s", [2, 3, 4, 5, 8])
+def test_3d_matrix_powers_bit_exact(monkeypatch, dims, s):
+    """One-sweep 3D matrix powers (mpk3.cu: 2.5D tiles with a ghost zone, z chunks started J
+    planes early; chained past depth 4): every power bit-identical to successive single applies,
+    with and without the one-sweep kernel."""
+    from paper_2001_04886_b200 import Context, krylov_block, splitmix64_uniform
+    from paper_2001_04886_b200.problems import Stencil
+    nx, ny, nz = dims
+    h = 1.0 / (nx + 1.0)
+    lo, hi = -1.0 - 10.0 * h, -1.0 + 10.0 * h
+    st = Stencil(3, nx, ny, nz, (lo, lo, lo, 6.0, hi, hi, hi), 10.0 * h, False)
+    v = splitmix64_uniform(9, st.n)
+    blocks = {}
+    for flag in ("1", "0"):  # (1: the one-sweep kernel; 0: single-level applies)
+        monkeypatch.setenv("SKC_MPK3", flag)
+        op = Context(0).stencil(st)
+        blocks[flag] = krylov_block(op, v, s)
+        for j in range(s - 1):
+            assert np.array_equal(blocks[flag][j + 1], op.apply(blocks[flag][j])), (flag, j)
+    assert np.array_equal(blocks["1"], blocks["0"])
