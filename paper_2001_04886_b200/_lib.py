@@ -10,7 +10,7 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libskrylov_b200.so")
+LIB_PATH = os.environ.get("SKC_LIB") or os.path.join(HERE, "libskrylov_b200.so")  # (SKC_LIB: A/B builds)
 
 u64 = C.c_uint64
 i32 = C.c_int32

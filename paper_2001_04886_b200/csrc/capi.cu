@@ -96,7 +96,6 @@ skc_ctx* make_ctx(int device) {
   ctx->c.stream = ctx->c.own_stream;
   if (const char* e = std::getenv("SKC_PDL")) ctx->c.pdl = std::atoi(e) != 0;
   if (const char* e = std::getenv("SKC_ORTH")) ctx->c.orth = std::atoi(e) != 0;
-  if (const char* e = std::getenv("SKC_ZFUSE")) ctx->c.zfuse = std::atoi(e) != 0;
   if (const char* e = std::getenv("SKC_PERSIST")) ctx->c.persist = std::atoi(e) != 0;
   if (const char* e = std::getenv("SKC_SPOW")) ctx->c.spow = std::atoi(e) != 0;
   if (const char* e = std::getenv("SKC_LSQ_OVERLAP")) ctx->c.lsq_overlap = std::atoi(e) != 0;

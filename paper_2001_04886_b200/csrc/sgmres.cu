@@ -53,7 +53,10 @@ struct ArnState {
   // kArnPushCollapse, kArnCholCollapse, kArnEarly) and its step; written only by
   // k_arn_lsq, which also raises the sticky `halt` so later block steps return at entry
   int lstatus, lblock;
-  int pad;
+  // block-iteration kernel: the halt flag as CTA 0 read it (the whole grid's decision after the
+  // first grid barrier) and the monotonic arrival counter of its grid barriers
+  int hseen;
+  unsigned long long gbar;
 };
 
 // record layout per block iteration k (0 = constructor)
@@ -645,43 +648,59 @@ __global__ void k_arn_check(ArnState* st, const Gram* grams, int k, double* rec,
 }
 
 // ---------------------------------------------------------------- on-chip block orthogonalization
-// One cooperative kernel for the whole block-MGS stage of a block iteration (sstep.hpp:331-379)
-// when the candidate columns cand[:,1:] of every CTA's point slice fit in its shared memory:
-// one CTA per SM owns points [b*P, (b+1)*P) and keeps its slice of cand[:,1:] on chip for
+// One kernel for a whole block iteration (sstep.hpp:297-379) when the candidate columns
+// cand[:,1:] of every CTA's point slice fit in its shared memory: one CTA per SM owns points
+// [b*P, (b+1)*P) and keeps its slice of the candidate there for
+//   z = A v, the Scalar1 products and solves, the seed and nu, the candidate powers,
 //   pass 0: k rounds  (Scalar2 solve in every CTA, cand -= V_i t, products V_{i+1}^T cand),
 //   the cross products [V_0..V_{k-1}, cand]^T cand and the reorthogonalization test,
 //   pass 1 (only when the test fires): V_0^T cand, k more rounds (t accumulated), W = cand^T cand,
 // separated by grid-wide barriers; cand[:,1:] is written back once at the end.  Only the basis
-// blocks stream from memory.  Every CTA reduces the per-CTA partials in the same fixed order,
-// so all CTAs take identical coefficients and the same reorthogonalization decision; CTA 0
-// writes the records and the device flags.
-constexpr int ORTH_NT = 512;
-// points per thread per iteration, all their loads issued first (Scalar1 products, seed):
-// 8 x s loads of 8 bytes per thread ~ the unified L1 left beside the candidate slice (4 -> 8:
-// C2 3848 -> 3909 s-steps/s)
-constexpr int ORTH_UC = 8;
-constexpr size_t kOrthSmemCap = 220 * 1024;
-// candidate columns kept in shared memory (the rest in their basis slots): shared memory is
-// carved out of the unified L1, whose remaining capacity bounds the loads in flight per SM
-// (C2, s = 4: 3 columns on chip 3697 s-steps/s, 2 columns 3750, 1 column 3635)
+// blocks stream from memory, and they stream through the TMA engine: a producer thread walks
+// the launch's fixed schedule of (basis block, tile) jobs and issues one cp.async.bulk per column
+// of a tile into a ring of shared-memory stages (full / empty mbarriers per stage); the 16
+// consumer warps wait on a stage, compute from shared memory and release it with one arrive
+// per warp.  The producer attends neither the CTA barriers nor the grid barriers, so the next
+// phase's first tiles are in place during every reduce-and-solve and every grid barrier.
+// (Measured on C2: a bulk copy costs the TMA unit ~85 ns whatever its size up to a few KB, so
+// tiles are as large as the ring allows; the loaded latency of a copy is ~0.4 us, ~48 KB in
+// flight per SM saturate the rate, and an L2 prefetch ahead of the copies lost.)
+// Every CTA reduces the per-CTA partials in the same fixed order, so all CTAs take identical
+// coefficients and the same reorthogonalization decision; CTA 0 writes the records and the
+// device flags.
+constexpr int ORTH_NT = 512;                 // consumer threads (16 warps)
+constexpr int ORTH_THREADS = ORTH_NT + 32;   // + the producer warp
+#ifndef SKC_ORTH_U
+#define SKC_ORTH_U 2
+#endif
+constexpr int ORTH_U = SKC_ORTH_U;           // points per consumer thread per tile
+constexpr int ORTH_T = ORTH_U * ORTH_NT;     // points per tile (point p stays with thread p mod 512)
+constexpr int kOrthMaxStages = 8;
+constexpr size_t kOrthSmemCap = 226 * 1024;  // <= the 227 KB per-block limit less the static part
+// candidate columns kept in shared memory (the rest in their basis slots, read back through a
+// register prefetch): what is left of the 227 KB holds the ring's stages
 #ifndef SKC_ORTH_SMEM_COLS
 #define SKC_ORTH_SMEM_COLS 2
 #endif
 constexpr int kOrthSmemCols = SKC_ORTH_SMEM_COLS;
-#ifndef SKC_HOIST
-#define SKC_HOIST 0
-#endif
-#ifndef SKC_UU4
-#define SKC_UU4 3
-#endif  // <= the 226 KB dynamic limit set at launch
-// reduced-product capacity: the cross test needs (k+1) s^2, a round s(s-1); even count keeps
-// the Gram copy 16-byte aligned
-__host__ __device__ inline int orth_prod_cap(int k, int s) { return ((k + 1) * s * s + 1) & ~1; }
-constexpr int kStepH = 64 * kMaxS;  // -h coefficients of Scalar1 (k s <= 512)
+// reduced-product capacity: the cross test needs (k+1) s^2, a round s(s-1), Scalar1 k s + 1
+__host__ __device__ inline int orth_prod_cap(int k, int s) { return ((k + 1) * s * s + 2) & ~1; }
+__host__ __device__ inline int orth_h_cap(int k, int s) { return (k * s + 1) & ~1; }
+
+// What a block's Scalar solves and the reorthogonalization test need of its GramSolver, in
+// shared memory: the Cholesky factor and trace(W) (an LDL^T-factored block -- a failed
+// Cholesky attempt, rare -- is solved from the full record in global memory)
+template <int S>
+struct GramC {
+  double trace;
+  int used_ldlt, pad;
+  double fac[S * S];
+};
 
 struct OrthDesc {
   int s, k, build_next;
-  int zfuse;              // form the next iteration's z and Scalar1 products in the cross pass
+  int nst;                // stages of the basis ring
+  int hint;               // L2 policy of the basis copies: 0 none, 1 evict_last, 2 evict_normal, 3 evict_first
   int64_t n, P;           // points, points per CTA
   DevOp op;
   const double* vin;      // v_{k-1}^{s-1}: z = A vin
@@ -700,13 +719,9 @@ struct OrthDesc {
   ArnState* st;
   double orth_tol;
   unsigned long long* trace;  // optional phase timestamps (CTA 0), diagnostics
-  // row-streamed candidate powers (2D constant stencil, s <= 4): per-CTA ghost-row buffers of
-  // levels 1 and 2 (g1 + g2 doubles per CTA at ghosts); spow 0 = per-level sweeps with grid
-  // barriers.  The buffers are in (L2-resident) global memory: shared memory beyond the
-  // candidate slice would shrink the L1 share of the unified L1/shared array, whose capacity
-  // bounds the loads in flight per SM for every streaming phase (measured: -14% on C2)
-  int spow, g1, g2;
-  double* ghosts;
+  // level-by-level candidate powers on the slice extended by ghost rows (2D constant stencil,
+  // the ghost rows fit the ring's stages); spow 0 = per-level sweeps with grid barriers
+  int spow;
 };
 
 // per-CTA completion time of a phase (diagnostics): slot base + CTA index
@@ -726,9 +741,54 @@ __device__ __forceinline__ void orth_mark(const OrthDesc& d, int slot) {
   }
 }
 
-// streamed basis loads: L2 only (no L1 allocation), so the number of loads in flight per SM is
-// not bounded by the L1 capacity left beside the candidate slice in the unified L1/shared memory
-__device__ __forceinline__ double ldcg(const double* p) { return __ldcg(p); }
+// barrier of the 512 consumer threads (named barrier 1: the producer warp does not attend)
+__device__ __forceinline__ void csync() { asm volatile("bar.sync 1, %0;" ::"n"(ORTH_NT) : "memory"); }
+
+// Grid-wide barrier of the consumer threads: one monotonic counter (never reset: every CTA
+// passes every barrier, so arrivals [g G, (g+1) G) belong to barrier g), one atomic per CTA,
+// acquire polling.  The launch is cooperative, so all CTAs are resident.
+__device__ __forceinline__ void orth_gsync(unsigned long long* bar, unsigned G) {
+  csync();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    const unsigned long long old = atomicAdd(bar, 1ull);
+    const unsigned long long target = (old / G + 1) * G;
+    unsigned long long v;
+    do {
+      asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(bar) : "memory");
+    } while (v < target);
+    __threadfence();
+  }
+  csync();
+}
+
+// reduce_dots_dev for the consumer threads (ungrouped partials; ends with csync)
+__device__ __forceinline__ void orth_reduce(const double* __restrict__ partials, int G, int d0, int nd, double* out) {
+  int tpd = 32;
+  while (tpd > 1 && (ORTH_NT / tpd) < nd) tpd >>= 1;
+  const int groups = ORTH_NT / tpd;
+  const int grp = threadIdx.x / tpd, sub = threadIdx.x % tpd;
+  for (int d = grp; d - grp < nd; d += groups) {  // uniform trip count across the warp
+    double s = 0.0;
+    if (d < nd) {
+      const double* p = partials + (int64_t)(d0 + d) * kPartialPitch;
+      double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+      int g = sub;
+#pragma unroll 4
+      for (; g + 3 * tpd < G; g += 4 * tpd) {
+        a0 += __ldcg(p + g);
+        a1 += __ldcg(p + g + tpd);
+        a2 += __ldcg(p + g + 2 * tpd);
+        a3 += __ldcg(p + g + 3 * tpd);
+      }
+      for (; g < G; g += tpd) a0 += __ldcg(p + g);
+      s = (a0 + a1) + (a2 + a3);
+    }
+    for (int o = tpd >> 1; o > 0; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o, tpd);
+    if (sub == 0 && d < nd) out[d] = s;
+  }
+  csync();
+}
 
 // fixed-order CTA reduction of K per-thread accumulators into partial column blockIdx.x
 template <int K>
@@ -736,262 +796,404 @@ __device__ __forceinline__ void orth_store(const double (&acc)[K], double* red, 
   constexpr int NW = ORTH_NT / 32;
   const int warp = threadIdx.x >> 5;
   warp_sums(acc, red + warp * K);
-  __syncthreads();
+  csync();
   if (threadIdx.x < K) {
     double s = 0.0;
     for (int w = 0; w < NW; ++w) s += red[w * K + threadIdx.x];
     partials[(int64_t)(d0 + threadIdx.x) * kPartialPitch + blockIdx.x] = s;
   }
-  __syncthreads();
+  csync();
 }
 
-// as orth_store, products q < K1 to partials d0 + q and the rest to d1 + (q - K1)
-template <int K, int K1>
-__device__ __forceinline__ void orth_store2(const double (&acc)[K], double* red, double* partials, int d0, int d1) {
-  constexpr int NW = ORTH_NT / 32;
-  const int warp = threadIdx.x >> 5;
-  warp_sums(acc, red + warp * K);
-  __syncthreads();
-  if (threadIdx.x < K) {
-    double s = 0.0;
-    for (int w = 0; w < NW; ++w) s += red[w * K + threadIdx.x];
-    const int q = threadIdx.x;
-    partials[(int64_t)(q < K1 ? d0 + q : d1 + (q - K1)) * kPartialPitch + blockIdx.x] = s;
+// ring position: stage index and the parity of its current use
+struct OrthRing {
+  int idx;
+  uint32_t ph;
+  __device__ __forceinline__ void next(int nst) {
+    if (++idx == nst) idx = 0, ph ^= 1u;
   }
-  __syncthreads();
-}
+};
 
 template <int S>
-__global__ void __launch_bounds__(ORTH_NT, 1) k_arn_step(const __grid_constant__ OrthDesc d) {
+__global__ void __launch_bounds__(ORTH_THREADS, 1) k_arn_step(const __grid_constant__ OrthDesc d) {
   SKC_PDL_ENTRY();
-  // block-uniform, before any barrier; a volatile read: the side stream's least-squares kernel
-  // may raise the flag while this grid is being scheduled
-  if (*reinterpret_cast<const volatile int*>(&d.st->halt)) return;
-  namespace cg = cooperative_groups;
-  cg::grid_group grid = cg::this_grid();
   constexpr int NC = S - 1;
+  constexpr int T = ORTH_T, U = ORTH_U, NT = ORTH_NT;
+  constexpr int SC = NC < kOrthSmemCols ? NC : kOrthSmemCols;  // candidate columns 1..SC on chip
+  constexpr int NG = NC - SC;                                   // columns SC+1..s-1 in memory
+  constexpr int NG1 = NG > 0 ? NG : 1;
   extern __shared__ __align__(16) double dsm[];
-  // coefficients -t [64] | reduced products [(k+1) s^2] | Gram scratch | Gram factors of the
-  // k blocks | reduction scratch [16 warps][s^2 + s] | candidate slice [s-1][P]
+  // coefficients -t [s(s-1), 64] | -h [k s] | reduced products [(k+1) s^2] | the pushed block's
+  // full GramSolver | compact Gram records of the k blocks | reduction scratch [16 warps][s^2]
+  // | candidate slice [SC][P] | ring stages [nst][s][T]
   double* tc = dsm;
   double* hc = dsm + 64;
-  double* prod = hc + kStepH;
+  double* prod = hc + orth_h_cap(d.k, S);
   Gram* gs = reinterpret_cast<Gram*>(prod + orth_prod_cap(d.k, S));
-  Gram* gk = gs + 1;
+  GramC<S>* gk = reinterpret_cast<GramC<S>*>(gs + 1);
   double* red = reinterpret_cast<double*>(gk + d.k);
-  double* sc = red + (ORTH_NT / 32) * (S * S + S);
+  // (the stages are bulk-copy destinations: 16-byte aligned)
+  double* sc = reinterpret_cast<double*>((reinterpret_cast<uintptr_t>(red + (NT / 32) * (S * S)) + 15) & ~(uintptr_t)15);
+  double* stg = sc + (int64_t)(SC > 0 ? SC : 1) * d.P;
+  __shared__ __align__(8) uint64_t s_full[kOrthMaxStages], s_empty[kOrthMaxStages], s_ctl, s_go;
+  __shared__ volatile int s_quit, s_dec;
+  __shared__ int s_jp;
   __shared__ int exceed[64];
-  __shared__ int s_first;
+  __shared__ int s_first, s_push_ok;
   const int tid = threadIdx.x;
+  const int NST = d.nst;
   const int64_t base = (int64_t)blockIdx.x * d.P;
   const int64_t rem = d.n - base;
   const int cnt = rem <= 0 ? 0 : (int)(rem < d.P ? rem : d.P);
-  const int G = gridDim.x;
+  const int ntiles = (cnt + T - 1) / T;
+  const unsigned G = gridDim.x;
+  const int K = d.k;
+  const int64_t np = d.np;
   auto colp = [&](int i, int l) { return d.V + ((int64_t)i * S + l) * d.np + base; };
-  // this slice of candidate column j+1 (j = 0..s-2): the first kOrthSmemCols in shared memory,
-  // the rest in their basis slots in global memory (C2: 124 KB of unified L1 left instead of
-  // 60 KB; that capacity bounds the loads in flight per SM in every streaming phase)
-  auto ccol = [&](int j) -> double* { return j < kOrthSmemCols ? sc + (int64_t)j * d.P : d.cand[j + 1] + base; };
+  if (tid == 0) {
+    for (int q = 0; q < NST; ++q) {
+      mbar_init(&s_full[q], 1);
+      mbar_init(&s_empty[q], NT / 32);
+    }
+    mbar_init(&s_ctl, 1);
+    mbar_init(&s_go, 1);
+    s_quit = 0;
+    s_dec = 0;
+    s_jp = 0;
+    mbar_fence_init();
+  }
+  __syncthreads();
 
-
-  // Scalar2 for block i from partials (src, srcG): every CTA solves W_i t = V_i^T cand[:,1:]
-  auto scalar = [&](int i, int src, int srcG, int accumulate) {
-    reduce_dots_dev(d.partials, srcG, src, S * NC, prod);  // ends with __syncthreads
-    if (tid < NC) {
-      const int jc = tid;
-      double rhs[kMaxS], t[kMaxS];
-#pragma unroll
-      for (int l = 0; l < S; ++l) rhs[l] = prod[l * NC + jc];
-      gram_solve_t<S>(gk[i], rhs, t);
+  // ================================================================ producer (one thread)
+  // The schedule is a fixed function of (k, build_next) up to the reorthogonalization decision:
+  // Scalar1 products (blocks k-1..0) | seed (0..k-1) | round-0 products (block 0) | rounds
+  // (V_i and V_{i+1} tile by tile) | cross products (k-1..0) | the second pass' round-0 products
+  // and rounds.  The first tiles of the second pass are issued before its decision is known
+  // (block 0 was the cross pass' last block, so they come from L2); unused ones are drained by
+  // the consumers before the CTA exits, as is whatever is in flight when the block iteration
+  // stops early (s_quit).  Between the seed and the round-0 products the copies wait for the
+  // powers phase (s_go): its ghost rows live in the ring's stages.
+  if (tid >= NT) {
+    if (tid != NT) return;
+    OrthRing pp{0, 0u};
+    int jp = 0;
+    const uint64_t pol = d.hint == 1 ? policy_evict_last() : d.hint == 3 ? policy_evict_first() : policy_evict_normal();
+    auto issue = [&](const double* blk, int t) -> bool {
+      while (!mbar_try_wait(&s_empty[pp.idx], pp.ph ^ 1u))
+        if (s_quit) return false;
+      const int npts = cnt - t * T < T ? cnt - t * T : T;
+      const uint32_t bytes = (uint32_t)((npts + 1) & ~1) * 8u;
+      mbar_arrive_expect_tx(&s_full[pp.idx], S * bytes);
+      double* dst = stg + (int64_t)pp.idx * (S * T);
+      const double* src = blk + (int64_t)t * T;
 #pragma unroll
       for (int l = 0; l < S; ++l) {
-        tc[l * NC + jc] = -t[l];
+        if (d.hint)
+          bulk_g2s_hint(dst + l * T, src + l * np, bytes, &s_full[pp.idx], pol);
+        else
+          bulk_g2s(dst + l * T, src + l * np, bytes, &s_full[pp.idx]);
+      }
+      pp.next(NST);
+      ++jp;
+      return true;
+    };
+    auto sweep = [&](int i, int t0) -> bool {
+      const double* b = colp(i, 0);
+      for (int t = t0; t < ntiles; ++t)
+        if (!issue(b, t)) return false;
+      return true;
+    };
+    auto produce = [&]() {
+      for (int i = K - 1; i >= 0; --i)
+        if (!sweep(i, 0)) return;
+      for (int i = 0; i < K; ++i)
+        if (!sweep(i, 0)) return;
+      if (!d.build_next) return;
+      while (!mbar_try_wait(&s_go, 0u))  // the powers phase owns the ring until then
+        if (s_quit) return;
+      for (int pass = 0; pass < 2; ++pass) {
+        int t0 = 0;
+        if (pass == 1) {
+          const int nspec = ntiles < NST ? ntiles : NST;
+          const double* b = colp(0, 0);
+          for (; t0 < nspec; ++t0)
+            if (!issue(b, t0)) return;
+          int dec;
+          while ((dec = s_dec) == 0)
+            if (s_quit) return;
+          if (dec == 1) return;
+        }
+        if (!sweep(0, t0)) return;
+        for (int i = 0; i < K; ++i) {
+          const double* bi = colp(i, 0);
+          const double* bn = colp(i + 1 < K ? i + 1 : i, 0);
+          for (int t = 0; t < ntiles; ++t) {
+            if (!issue(bi, t)) return;
+            if (i + 1 < K && !issue(bn, t)) return;
+          }
+        }
+        if (pass == 0)
+          for (int i = K - 1; i >= 0; --i)
+            if (!sweep(i, 0)) return;
+      }
+    };
+    produce();
+    s_jp = jp;
+    mbar_arrive(&s_ctl);
+    return;
+  }
+
+  // ================================================================ consumers
+  OrthRing pc{0, 0u};
+  int jc = 0;
+  const int lane = tid & 31;
+  // wait for the next job's stage / release it
+  auto cwait = [&]() -> const double* {
+    mbar_wait(&s_full[pc.idx], pc.ph);
+    return stg + (int64_t)pc.idx * (S * T) + tid;
+  };
+  auto crel = [&]() {
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&s_empty[pc.idx]);
+    pc.next(NST);
+    ++jc;
+  };
+  // leave the kernel: stop the producer and wait for the copies still in flight
+  auto finish = [&]() {
+    csync();
+    if (tid == 0) {
+      s_quit = 1;
+      mbar_wait(&s_ctl, 0u);
+      const int jp = s_jp;
+      for (; jc < jp; ++jc) {
+        mbar_wait(&s_full[pc.idx], pc.ph);
+        pc.next(NST);
+      }
+    }
+  };
+  // this slice of candidate column j+1 (j = 0..s-2): the first SC in shared memory, the rest in
+  // their basis slots in global memory
+  auto ccol = [&](int j) -> double* { return j < SC ? sc + (int64_t)j * d.P : d.cand[j + 1] + base; };
+  // in-memory candidate column g (candidate column SC+1+g), this slice
+  auto gcol = [&](int g) -> double* { return d.cand[SC + 1 + g] + base; };
+
+  // W_i x = rhs for basis block i (Cholesky factor from shared memory; LDL^T-factored blocks
+  // from the full record)
+  auto bsolve = [&](int i, const double* rhs, double* x) {
+    if (S == 1 || gk[i].used_ldlt) {
+      double r2[kMaxS], x2[kMaxS];
+#pragma unroll
+      for (int q = 0; q < S; ++q) r2[q] = rhs[q];
+      gram_solve(i == K - 1 && K >= 2 ? *gs : d.grams[i], r2, x2);
+#pragma unroll
+      for (int q = 0; q < S; ++q) x[q] = x2[q];
+    } else {
+      chol_solve_t<S>(gk[i].fac, rhs, x);
+    }
+  };
+
+  // Scalar2 for block i from partials src: every CTA solves W_i t = V_i^T cand[:,1:]
+  auto scalar = [&](int i, int src, int accumulate) {
+    orth_reduce(d.partials, (int)G, src, S * NC, prod);  // ends with csync
+    if (tid < NC) {
+      const int jcl = tid;
+      double rhs[kMaxS], t[kMaxS];
+#pragma unroll
+      for (int l = 0; l < S; ++l) rhs[l] = prod[l * NC + jcl];
+      bsolve(i, rhs, t);
+#pragma unroll
+      for (int l = 0; l < S; ++l) {
+        tc[l * NC + jcl] = -t[l];
         if (blockIdx.x == 0) {
-          double* ta = d.rec + d.rec_t + i * S * S + l * S + (jc + 1);
+          double* ta = d.rec + d.rec_t + i * S * S + l * S + (jcl + 1);
           *ta = accumulate ? *ta + t[l] : t[l];
         }
       }
     }
-    __syncthreads();
+    csync();
   };
 
-  // cand[:,1:] -= V_i t ; products V_{i+1}^T cand[:,1:] -> partials dst (when i+1 < k).
-  // Points go in pairs (p, p + NT) with every basis load of the pair issued before the
-  // arithmetic, so each thread keeps 2s (4s with the products) loads in flight; the products
-  // still accumulate in ascending point order.
+  // the in-memory candidate columns of tile t's points of this thread (issued a tile ahead)
+  auto gload = [&](int t, double (&o)[U][NG1]) {
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+#pragma unroll
+      for (int g = 0; g < NG; ++g) {
+        const int p = t * T + u * NT + tid;
+        o[u][g] = p < cnt ? __ldcg(gcol(g) + p) : 0.0;
+      }
+  };
+
+  // cand[:,1:] -= V_i t ; products V_{i+1}^T cand[:,1:] -> partials dst (when i+1 < k).  Point
+  // p stays with thread p mod 512 and tiles go in ascending order, so the products accumulate
+  // in ascending point order per thread.
   auto round = [&](int i, int dst, bool wb, auto&& pre) {
     const bool dots = i + 1 < d.k;
-    const double* Vi = colp(i, 0);
-    const double* Vn = colp(dots ? i + 1 : i, 0);
-    const int64_t np = d.np;
     double acc[S * NC];
 #pragma unroll
     for (int q = 0; q < S * NC; ++q) acc[q] = 0.0;
-    constexpr int UU = S <= 3 ? 4 : S == 4 ? SKC_UU4 : S <= 6 ? 2 : 1;
-    // (with SKC_HOIST the first points' basis loads are issued before `pre` -- the reduction
-    // and Gram solve of this round's coefficients -- so they are in flight during it)
-    bool has[UU];
-    double v[UU][S], w[UU][S];
-    auto load = [&](int p0) {
-#pragma unroll
-      for (int u = 0; u < UU; ++u) {
-        const int p = p0 + u * ORTH_NT;
-        has[u] = p < cnt;
-#pragma unroll
-        for (int l = 0; l < S; ++l) {
-          v[u][l] = has[u] ? ldcg(Vi + l * np + p) : 0.0;
-          w[u][l] = dots && has[u] ? ldcg(Vn + l * np + p) : 0.0;
-        }
-      }
-    };
-#if SKC_HOIST
-    load(tid);
+    double gc[U][NG1], gn[U][NG1];
+    gload(0, gc);
     pre();
-#else
-    pre();
-#endif
-    for (int p0 = tid; p0 < cnt; p0 += UU * ORTH_NT) {
-      double cv[UU][NC];
-#if SKC_HOIST
-      if (p0 != tid) load(p0);
-#else
-      load(p0);
-#endif
+    for (int t = 0; t < ntiles; ++t) {
+      gload(t + 1, gn);
+      double cv[U][NC];
+      {
+        const double* sp = cwait();
 #pragma unroll
-      for (int u = 0; u < UU; ++u)
+        for (int u = 0; u < U; ++u) {
+          const int p = t * T + u * NT + tid;
+          const bool has = p < cnt;
 #pragma unroll
-        for (int j = 0; j < NC; ++j) cv[u][j] = has[u] ? ccol(j)[p0 + u * ORTH_NT] : 0.0;
+          for (int j = 0; j < SC; ++j) cv[u][j] = has ? ccol(j)[p] : 0.0;
 #pragma unroll
-      for (int l = 0; l < S; ++l)
+          for (int g = 0; g < NG; ++g) cv[u][SC + g] = gc[u][g];
 #pragma unroll
-        for (int j = 0; j < NC; ++j) {
-          const double t = tc[l * NC + j];
+          for (int l = 0; l < S; ++l) {
+            const double v = sp[l * T + u * NT];
 #pragma unroll
-          for (int u = 0; u < UU; ++u) cv[u][j] = dadd(cv[u][j], dmul(t, v[u][l]));
+            for (int j = 0; j < NC; ++j) cv[u][j] = dadd(cv[u][j], dmul(tc[l * NC + j], v));
+          }
+          if (has) {
+#pragma unroll
+            for (int j = 0; j < SC; ++j) ccol(j)[p] = cv[u][j];
+#pragma unroll
+            for (int g = 0; g < NG; ++g) gcol(g)[p] = cv[u][SC + g];
+            if (wb) {  // (the columns past SC already live in their basis slots)
+#pragma unroll
+              for (int j = 0; j < SC; ++j) d.cand[j + 1][base + p] = cv[u][j];
+            }
+          }
         }
-#pragma unroll
-      for (int u = 0; u < UU; ++u) {
-        if (!has[u]) continue;
-#pragma unroll
-        for (int j = 0; j < NC; ++j) ccol(j)[p0 + u * ORTH_NT] = cv[u][j];
-        if (wb) {  // (the columns past kOrthSmemCols already live in their basis slots)
-#pragma unroll
-          for (int j = 0; j < (NC < kOrthSmemCols ? NC : kOrthSmemCols); ++j) d.cand[j + 1][base + p0 + u * ORTH_NT] = cv[u][j];
-        }
-        if (dots) {
-#pragma unroll
-          for (int l = 0; l < S; ++l)
-#pragma unroll
-            for (int j = 0; j < NC; ++j) acc[l * NC + j] = fma(w[u][l], cv[u][j], acc[l * NC + j]);
-        }
+        crel();
       }
+      if (dots) {
+        const double* sp = cwait();
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          if (t * T + u * NT + tid < cnt) {
+#pragma unroll
+            for (int l = 0; l < S; ++l) {
+              const double w = sp[l * T + u * NT];
+#pragma unroll
+              for (int j = 0; j < NC; ++j) acc[l * NC + j] = fma(w, cv[u][j], acc[l * NC + j]);
+            }
+          }
+        }
+        crel();
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+#pragma unroll
+        for (int g = 0; g < NG; ++g) gc[u][g] = gn[u][g];
     }
     if (dots) orth_store(acc, red, d.partials, dst);
   };
 
-  // round-0 products V_0^T cand[:,1:] -> partials dr0 (sstep.hpp:341), four points per thread
-  // with all their loads issued first
+  // round-0 products V_0^T cand[:,1:] -> partials dr0 (sstep.hpp:341)
   auto r0_products = [&]() {
-    constexpr int U0 = S <= 4 ? 4 : 2;
     double acc[S * NC];
 #pragma unroll
     for (int q = 0; q < S * NC; ++q) acc[q] = 0.0;
-    const double* V0 = colp(0, 0);
-    const int64_t np = d.np;
-    for (int p0 = tid; p0 < cnt; p0 += U0 * ORTH_NT) {
-      double lv[U0][S], cv[U0][NC];
+    double gc[U][NG1], gn[U][NG1];
+    gload(0, gc);
+    for (int t = 0; t < ntiles; ++t) {
+      gload(t + 1, gn);
+      const double* sp = cwait();
 #pragma unroll
-      for (int u = 0; u < U0; ++u) {
-        const int p = p0 + u * ORTH_NT;
-        const bool h = p < cnt;
+      for (int u = 0; u < U; ++u) {
+        const int p = t * T + u * NT + tid;
+        if (p < cnt) {
+          double cv[NC];
 #pragma unroll
-        for (int l = 0; l < S; ++l) lv[u][l] = h ? ldcg(V0 + l * np + p) : 0.0;
+          for (int j = 0; j < SC; ++j) cv[j] = ccol(j)[p];
 #pragma unroll
-        for (int j = 0; j < NC; ++j) cv[u][j] = h ? ccol(j)[p] : 0.0;
+          for (int g = 0; g < NG; ++g) cv[SC + g] = gc[u][g];
+#pragma unroll
+          for (int l = 0; l < S; ++l) {
+            const double lv = sp[l * T + u * NT];
+#pragma unroll
+            for (int j = 0; j < NC; ++j) acc[l * NC + j] = fma(lv, cv[j], acc[l * NC + j]);
+          }
+        }
       }
+      crel();
 #pragma unroll
-      for (int u = 0; u < U0; ++u)
+      for (int u = 0; u < U; ++u)
 #pragma unroll
-        for (int l = 0; l < S; ++l)
-#pragma unroll
-          for (int j = 0; j < NC; ++j) acc[l * NC + j] = fma(lv[u][l], cv[u][j], acc[l * NC + j]);
+        for (int g = 0; g < NG; ++g) gc[u][g] = gn[u][g];
     }
     orth_store(acc, red, d.partials, d.dr0);
   };
 
   // L-block products with the full candidate: lhs(l) . cand[:,jc] for one block of s columns
   // (block i of the basis, or the candidate itself when i == k) -> partials d0 + l*s + jc.
-  // With ZD also lhs(l) . z -> partials dz0 + l: the next block iteration's Scalar1 products
-  // (z = A cand[:,s-1] of the final candidate, in memory at zg)
-  auto cross_block = [&](auto zd, int i, int d0, int dz0) {
-    constexpr bool ZD = decltype(zd)::value;
-    // points per thread in flight, bounded by the accumulator count (no spills at 128 registers)
-    constexpr int U = ZD ? (S <= 3 ? 4 : S == 4 ? 3 : S <= 6 ? 2 : 1) : (S <= 4 ? 4 : S <= 6 ? 2 : 1);
-    constexpr int NA = S * S + (ZD ? S : 0);
-    double acc[NA];
+  // Candidate column 0 and the columns past SC come from memory, issued a tile ahead.
+  auto cross_block = [&](int i, int d0) {
+    double acc[S * S];
 #pragma unroll
-    for (int q = 0; q < NA; ++q) acc[q] = 0.0;
+    for (int q = 0; q < S * S; ++q) acc[q] = 0.0;
     const double* c0p = d.cand0 + base;
-    const double* zg = d.z + base;
     const bool basis = i < d.k;
-    const double* Li = basis ? colp(i, 0) : c0p;
-    const int64_t np = d.np;
-    for (int p0 = tid; p0 < cnt; p0 += U * ORTH_NT) {
-      bool has[U];
-      double a[U][S], b[U][S], zv[U];
+    double gc[U][1 + NG], gn[U][1 + NG];
+    auto pfload = [&](int t, double (&o)[U][1 + NG]) {
 #pragma unroll
       for (int u = 0; u < U; ++u) {
-        const int p = p0 + u * ORTH_NT;
-        has[u] = p < cnt;
-        b[u][0] = has[u] ? ldcg(c0p + p) : 0.0;
-        zv[u] = ZD && has[u] ? zg[p] : 0.0;
+        const int p = t * T + u * NT + tid;
+        o[u][0] = p < cnt ? __ldcg(c0p + p) : 0.0;
 #pragma unroll
-        for (int l = 0; l < S; ++l) a[u][l] = basis && has[u] ? ldcg(Li + l * np + p) : 0.0;
-#pragma unroll
-        for (int j = 1; j < S; ++j) b[u][j] = has[u] ? ccol(j - 1)[p] : 0.0;
+        for (int g = 0; g < NG; ++g) o[u][1 + g] = p < cnt ? __ldcg(gcol(g) + p) : 0.0;
       }
+    };
+    pfload(0, gc);
+    for (int t = 0; t < ntiles; ++t) {
+      pfload(t + 1, gn);
+      const double* sp = basis ? cwait() : nullptr;
 #pragma unroll
       for (int u = 0; u < U; ++u) {
-        if (!has[u]) continue;
+        const int p = t * T + u * NT + tid;
+        if (p < cnt) {
+          double b[S];
+          b[0] = gc[u][0];
 #pragma unroll
-        for (int l = 0; l < S; ++l) {
-          const double av = basis ? a[u][l] : b[u][l];
+          for (int j = 0; j < SC; ++j) b[1 + j] = ccol(j)[p];
 #pragma unroll
-          for (int jc = 0; jc < S; ++jc) acc[l * S + jc] = fma(av, b[u][jc], acc[l * S + jc]);
-          if constexpr (ZD) acc[S * S + l] = fma(av, zv[u], acc[S * S + l]);
+          for (int g = 0; g < NG; ++g) b[1 + SC + g] = gc[u][1 + g];
+#pragma unroll
+          for (int l = 0; l < S; ++l) {
+            const double av = basis ? sp[l * T + u * NT] : b[l];
+#pragma unroll
+            for (int jcl = 0; jcl < S; ++jcl) acc[l * S + jcl] = fma(av, b[jcl], acc[l * S + jcl]);
+          }
         }
       }
+      if (basis) crel();
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+#pragma unroll
+        for (int g = 0; g < 1 + NG; ++g) gc[u][g] = gn[u][g];
     }
-    orth_store2<NA, S * S>(acc, red, d.partials, d0, dz0);
+    orth_store(acc, red, d.partials, d0);
   };
 
-  const int K = d.k;
-  const int64_t np = d.np;
-  // the previous block iteration's cross pass already produced z (in memory) and this
-  // iteration's Scalar1 products (partials dz), unless it ran a reorthogonalization pass
-  const bool zready = d.zfuse && K > 1 && __ldg(&d.st->zready) != 0;
   // push_block of the previous block iteration's candidate (sstep.hpp:375, 392-399) runs here,
   // off the previous kernel's tail: every CTA reduces its W (from the pass that produced the
   // candidate) and factors it in the Scalar1 phase; CTA 0 records it and stores the factor
   const bool push = K >= 2;
-  if (push) reduce_dots_dev(d.partials, G, __ldg(&d.st->reorth) ? d.dwb : d.dcross + (K - 1) * S * S, S * S, tc);
-  // the Gram factors of blocks 0..k-1 (k-2 with the push) into shared memory (asynchronous;
-  // waited for before Scalar1)
-  {
-    const char* gsrc = reinterpret_cast<const char*>(d.grams);
-    char* gdst = reinterpret_cast<char*>(gk);
-    for (int w = tid; w < (int)((push ? K - 1 : K) * sizeof(Gram) / 8); w += ORTH_NT)
-      cp_async8(gdst + 8 * w, gsrc + 8 * w, true);
-    cp_async_commit();
+  if (push)
+    orth_reduce(d.partials, (int)G, __ldg(&d.st->reorth) ? d.dwb : d.dcross + (K - 1) * S * S, S * S, tc);
+  // what the solves need of blocks 0..k-1 (k-2 with the push) into shared memory
+  for (int w = tid; w < (push ? K - 1 : K) * (S * S + 1); w += NT) {
+    const int i = w / (S * S + 1), q = w - i * (S * S + 1);
+    const Gram& g = d.grams[i];
+    if (q < S * S) {
+      gk[i].fac[q] = g.fac[q];
+    } else {
+      gk[i].trace = sd_trace(g.w, S);
+      gk[i].used_ldlt = g.used_ldlt;
+    }
   }
   orth_mark(d, 39);
-  // ---- z = A v_{k-1}^{s-1} on this slice (the source is stable; neighbours read from memory)
-  // y = A x on this slice; xs (optional) is this slice of x in shared memory, read in place of
-  // memory for the points it covers.  The 2D constant stencil takes a 32-bit fast path (same
-  // arithmetic: S, W, C, E, N in ascending column order, absent neighbours skipped).
-  // xscale (when nonzero) multiplies every source value as it is read (the source is then
-  // seed and the values level 0 = seed / nu, rounded exactly as when stored); put(p, y, x_p)
-  // also receives the point's own source value
   auto apply_slice = [&](const double* x, const double* xs, double xscale, auto&& put) {
     if (d.op.kind == kStencilConst && d.op.dim == 2) {
       const int nx = (int)d.op.nx, ny = (int)d.op.ny;
@@ -1064,43 +1266,33 @@ __global__ void __launch_bounds__(ORTH_NT, 1) k_arn_step(const __grid_constant__
     for (int p = tid; p < cnt; p += ORTH_NT, w.step(d.op, ORTH_NT))
       put(p, apply_point(d.op, fetch, base + p, w), fetch(base + p));
   };
-  // z and seed of this slice stay in shared memory (candidate columns 0 and s-2, free until
-  // the powers reach them; with s = 2 seed also goes to memory for its neighbours)
+  // z and seed of this slice stay in shared memory (candidate column 1's slot, free until the
+  // powers reach it)
   double* zs = sc;
-  double* seeds = nullptr;  // (the column that used to hold it is now in global memory)
-  if (zready) {
-    for (int p = tid; p < cnt; p += ORTH_NT) zs[p] = d.z[base + p];
-  } else {
-    apply_slice(d.vin, nullptr, 0.0, [&](int p, double v, double) { zs[p] = v; });
-  }
+  apply_slice(d.vin, nullptr, 0.0, [&](int p, double v, double) { zs[p] = v; });
   orth_mark(d, 40);
   // ---- Scalar1 products V_i^T z (i < k) -> dz + i s + l, and z.z -> dz + k s (each thread
   //      reads back its own z); blocks in descending order, so the seed sweep's first blocks
   //      are still in L2
-  if (!zready) {
+  {
     double zz[1] = {0.0};
     for (int i = K - 1; i >= 0; --i) {
       double acc[S];
 #pragma unroll
       for (int q = 0; q < S; ++q) acc[q] = 0.0;
-      const double* Vi = colp(i, 0);
-      for (int p0 = tid; p0 < cnt; p0 += ORTH_UC * ORTH_NT) {
-        double zv[ORTH_UC], v[ORTH_UC][S];
+      for (int t = 0; t < ntiles; ++t) {
+        const double* sp = cwait();
 #pragma unroll
-        for (int u = 0; u < ORTH_UC; ++u) {
-          const int p = p0 + u * ORTH_NT;
-          const bool h = p < cnt;
-          zv[u] = h ? zs[p] : 0.0;
+        for (int u = 0; u < U; ++u) {
+          const int p = t * T + u * NT + tid;
+          if (p < cnt) {
+            const double zv = zs[p];
 #pragma unroll
-          for (int l = 0; l < S; ++l) v[u][l] = h ? ldcg(Vi + l * np + p) : 0.0;
+            for (int l = 0; l < S; ++l) acc[l] = fma(sp[l * T + u * NT], zv, acc[l]);
+            if (i == 0) zz[0] = fma(zv, zv, zz[0]);
+          }
         }
-#pragma unroll
-        for (int u = 0; u < ORTH_UC; ++u) {
-          if (p0 + u * ORTH_NT >= cnt) continue;
-#pragma unroll
-          for (int l = 0; l < S; ++l) acc[l] = fma(v[u][l], zv[u], acc[l]);
-          if (i == 0) zz[0] = fma(zv[u], zv[u], zz[0]);
-        }
+        crel();
       }
       orth_store(acc, red, d.partials, d.dz + i * S);
     }
@@ -1108,20 +1300,35 @@ __global__ void __launch_bounds__(ORTH_NT, 1) k_arn_step(const __grid_constant__
   }
   orth_mark(d, 6);
   orth_mark_all(d, 256);
-  if (!zready) grid.sync();  // (with zready the products come from the previous launch)
+  // the halt flag (raised by an earlier block step, or by the side stream's least-squares
+  // kernel, possibly while this grid was being scheduled) as CTA 0 sees it now, made the whole
+  // grid's decision by the barrier
+  if (blockIdx.x == 0 && tid == 0) d.st->hseen = *reinterpret_cast<const volatile int*>(&d.st->halt);
+  orth_gsync(&d.st->gbar, G);
+  if (*reinterpret_cast<const volatile int*>(&d.st->hseen)) {
+    finish();
+    return;
+  }
   // ---- Scalar1 (sstep.hpp:301-310): zn, h_i = W_i^{-1} V_i^T z in every CTA (Gram factors
   // from shared memory); CTA 0 records
-  cp_async_wait<0>();
-  reduce_dots_dev(d.partials, G, d.dz, K * S + 1, prod);  // (ends with __syncthreads)
+  orth_reduce(d.partials, (int)G, d.dz, K * S + 1, prod);  // (ends with csync)
   if (push) {
-    __shared__ int s_push_ok;
     if (tid == 0) {
-      const bool ok = arn_push_body<S>(d.st, gk[K - 1], K - 1, d.rec_push, tc, S, blockIdx.x == 0);
+      const bool ok = arn_push_body<S>(d.st, *gs, K - 1, d.rec_push, tc, S, blockIdx.x == 0);
       s_push_ok = ok;
-      if (ok && blockIdx.x == 0) d.grams[K - 1] = gk[K - 1];
+      if (ok) {
+#pragma unroll
+        for (int q = 0; q < S * S; ++q) gk[K - 1].fac[q] = gs->fac[q];
+        gk[K - 1].trace = sd_trace(gs->w, S);
+        gk[K - 1].used_ldlt = gs->used_ldlt;
+        if (blockIdx.x == 0) d.grams[K - 1] = *gs;
+      }
     }
-    __syncthreads();
-    if (!s_push_ok) return;  // basis collapse (identical decision in every CTA)
+    csync();
+    if (!s_push_ok) {  // basis collapse (identical decision in every CTA)
+      finish();
+      return;
+    }
   }
   const double zn = sqrt(prod[K * S]);
   if (blockIdx.x == 0 && tid == 0) {
@@ -1131,58 +1338,53 @@ __global__ void __launch_bounds__(ORTH_NT, 1) k_arn_step(const __grid_constant__
   }
   for (int i = tid; i < K; i += ORTH_NT) {
     double rhs[kMaxS], h[kMaxS];
+#pragma unroll
     for (int l = 0; l < S; ++l) rhs[l] = prod[i * S + l];
-    gram_solve_t<S>(gk[i], rhs, h);
+    bsolve(i, rhs, h);
+#pragma unroll
     for (int l = 0; l < S; ++l) {
       hc[i * S + l] = -h[l];
       if (blockIdx.x == 0) d.rec[d.rec_h + i * S + l] = h[l];
     }
   }
-  __syncthreads();
+  csync();
   orth_mark(d, 41);
   // ---- seed = z - sum_i V_i h_i (terms in block order, multiply and add rounded separately),
   //      one sweep per block with the running sum in shared memory (every point stays with
   //      its thread), then ||seed||^2
   {
     for (int i = 0; i < K; ++i) {
-      const double* Vi = colp(i, 0);
       double hl[S];
 #pragma unroll
       for (int l = 0; l < S; ++l) hl[l] = hc[i * S + l];
-      for (int p0 = tid; p0 < cnt; p0 += ORTH_UC * ORTH_NT) {
-        double v[ORTH_UC][S], o[ORTH_UC];
+      for (int t = 0; t < ntiles; ++t) {
+        const double* sp = cwait();
 #pragma unroll
-        for (int u = 0; u < ORTH_UC; ++u) {
-          const int p = p0 + u * ORTH_NT;
-          const bool h = p < cnt;
-          o[u] = h ? zs[p] : 0.0;
+        for (int u = 0; u < U; ++u) {
+          const int p = t * T + u * NT + tid;
+          if (p < cnt) {
+            double o = zs[p];
 #pragma unroll
-          for (int l = 0; l < S; ++l) v[u][l] = h ? ldcg(Vi + l * np + p) : 0.0;
+            for (int l = 0; l < S; ++l) o = dadd(o, dmul(hl[l], sp[l * T + u * NT]));
+            zs[p] = o;
+          }
         }
-#pragma unroll
-        for (int u = 0; u < ORTH_UC; ++u) {
-          const int p = p0 + u * ORTH_NT;
-          if (p >= cnt) continue;
-#pragma unroll
-          for (int l = 0; l < S; ++l) o[u] = dadd(o[u], dmul(hl[l], v[u][l]));
-          zs[p] = o[u];
-        }
+        crel();
       }
     }
     double acc[1] = {0.0};
     for (int p = tid; p < cnt; p += ORTH_NT) {
       const double o = zs[p];
       d.seed[base + p] = o;
-      if (seeds) seeds[p] = o;
       acc[0] = fma(o, o, acc[0]);
     }
     orth_store(acc, red, d.partials, d.dseed);
   }
   orth_mark(d, 7);
   orth_mark_all(d, 512);
-  grid.sync();
+  orth_gsync(&d.st->gbar, G);
   // ---- nu = ||seed|| and the invariant-subspace test (sstep.hpp:315-324)
-  reduce_dots_dev(d.partials, G, d.dseed, 1, prod);
+  orth_reduce(d.partials, (int)G, d.dseed, 1, prod);
   const double nu = sqrt(prod[0]);
   if (blockIdx.x == 0 && tid == 0) d.rec[RecLayout::kNu] = nu;
   if (nu <= 1e-14 * zn) {  // identical decision in every CTA
@@ -1192,180 +1394,167 @@ __global__ void __launch_bounds__(ORTH_NT, 1) k_arn_step(const __grid_constant__
       d.st->block = K;
       d.st->halt = 1;
     }
+    finish();
     return;
   }
   const double inv = 1.0 / nu;
   orth_mark(d, 42);
   // ---- candidate block [v, A v, .., A^{s-1} v], v = seed / nu (krylov_block, block.hpp:59-67):
-  //      every level is an exact spmv of the previous one; levels 1..s-1 stay in shared memory,
-  //      levels 0..s-2 also go to memory for the neighbours' next level
+  //      every level is an exact spmv of the previous one; levels 1..s-1 stay on chip (or in
+  //      their basis slots), levels 0..s-2 also go to memory for the neighbours' next level
   orth_mark(d, 44);
-  if (S <= 4 && d.spow) {
-    // Row-streamed: the slice is walked in index rows of nx points (row r = [r nx, (r+1) nx)
-    // relative to the slice start); step k computes level j on row k - 2(j-1), so every level
-    // only reads rows of the previous level finished in earlier steps (one __syncthreads per
-    // step, no grid barrier).  Level j is computed on e_j = s-1-j ghost rows beyond each slice
-    // edge, redundantly with the neighbouring CTAs (level 1 from seed / nu in memory), so the
-    // slice's last level needs nothing from other CTAs.  Ghost rows live in small per-CTA global buffers
-    // (the bottom ghosts are dead before the top ghosts are written, so both share one buffer;
-    // the host enables this only when every slice has at least 4 rows).  Each point is the
-    // same ascending-column sum as spmv, so the levels are bit-identical to the sweeps.
+  if (d.spow) {
+    // Level by level over the slice extended by e_j = s-1-j index rows of nx points on each side
+    // (level j is needed that far for the slice's last level), redundantly with the neighbouring
+    // CTAs, so no level needs another CTA's results and CTA barriers suffice: level 1 reads
+    // seed / nu from memory (the whole seed was written before the grid barrier), the later
+    // levels read the previous one from shared memory -- the slice part in the candidate's
+    // columns, the ghost parts in the idle ring.  Each point is the same ascending-column sum
+    // as spmv, so the levels are bit-identical to successive sweeps.  (Host: 2D constant
+    // stencil, the ghost rows fit the ring.)
     const int nx = (int)d.op.nx, ny = (int)d.op.ny;
     const double cS = d.op.coef[1], cW = d.op.coef[2], cC = d.op.coef[3], cE = d.op.coef[4], cN = d.op.coef[5];
-    double* gh[2] = {d.ghosts + (int64_t)blockIdx.x * (d.g1 + d.g2), d.ghosts + (int64_t)blockIdx.x * (d.g1 + d.g2) + d.g1};
-    const int Rs = cnt > 0 ? (cnt + nx - 1) / nx : 0;
-    int ic[2], jc[2];
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      const int64_t q = base + 2 * tid + h;
-      ic[h] = (int)(q % nx);
-      jc[h] = (int)(q / nx);
-    }
-    // level j value at relative index v (slice, or the level's ghost buffer)
-    auto slot = [&](int j, int v) -> double* {
-      if (v >= 0 && v < cnt) return ccol(j - 1) + v;
+    // ghost rows of level j (1 <= j <= s-2): 2 e_j nx doubles (low side, then high side)
+    auto ghost = [&](int j) -> double* {
+      int o = 0;
+      for (int i = 1; i < j; ++i) o += 2 * (S - 1 - i) * nx;
+      return stg + o;
+    };
+    // level j (>= 1) at slice-relative index v inside its extended range
+    auto ext = [&](int j, int v) -> double* {
+      if ((unsigned)v < (unsigned)cnt) return ccol(j - 1) + v;
       const int e = S - 1 - j;
-      return gh[j - 1] + (v < 0 ? v + e * nx : v - cnt);
+      double* g = ghost(j);
+      return v < 0 ? g + (v + e * nx) : g + (e * nx + (v - cnt));
     };
-    const int kend = cnt > 0 ? Rs - 1 + 2 * (S - 2) : -(S - 2) - 1;
-    const int rin = cnt == Rs * nx ? Rs - 2 : Rs - 3;  // last row whose north neighbours are in the slice
-    // level 1's source rows (seed, columns c0-1 .. c0+2 of this thread's pair) in a register
-    // ring: rows k-1, k, k+1 in use, row k+2 loaded one step ahead
-    const int c0 = 2 * tid;
-    const int64_t q00 = base + c0;  // global index of (row 0, column c0)
-    auto load_row = [&](int rr, double (&o)[4]) {
+    const int b32 = (int)base, n32 = (int)d.n;
+    if (cnt > 0) {
 #pragma unroll
-      for (int t = 0; t < 4; ++t) {
-        const int64_t q = q00 + (int64_t)rr * nx + t - 1;
-        o[t] = c0 < nx && q >= 0 && q < d.n ? __ldcg(d.seed + q) : 0.0;
-      }
-    };
-    double ra[4], rb[4], rc[4], rn[4];
-    load_row(-(S - 2) - 1, ra);
-    load_row(-(S - 2), rb);
-    load_row(-(S - 2) + 1, rc);
-    for (int k = -(S - 2); k <= kend; ++k) {
-      load_row(k + 2, rn);  // (in flight during this step)
+      for (int j = 1; j < S; ++j) {
+        const int e = S - 1 - j;
+        int lo = -e * nx, hi = cnt + e * nx;
+        if (b32 + lo < 0) lo = -b32;
+        if (b32 + hi > n32) hi = n32 - b32;
+        constexpr int UP = 2;  // points per thread in flight
+        int ii[UP], jr[UP];
 #pragma unroll
-      for (int j = S - 1; j >= 1; --j) {
-        const int r = k - 2 * (j - 1), e = S - 1 - j;
-        if (r < -e || r > Rs - 1 + e) continue;
+        for (int u = 0; u < UP; ++u) {
+          const int q = b32 + lo + tid + u * NT;
+          ii[u] = q % nx, jr[u] = q / nx;
+        }
+        for (int v0 = lo + tid; v0 < hi; v0 += UP * NT) {
+          double xs_[UP], xw_[UP], xc_[UP], xe_[UP], xn_[UP];
 #pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          const int c = c0 + h;
-          if (c >= nx) continue;
-          const int v = r * nx + c;
-          const int jr = jc[h] + r, i = ic[h];
-          if (v < -e * nx || v >= cnt + e * nx || jr < 0 || jr >= ny) continue;
-          double xs_, xw_, xc_, xe_, xn_;
-          if (j == 1) {  // seed / nu from the ring (multiply rounded as when level 0 is stored)
-            xs_ = __dmul_rn(ra[h + 1], inv);
-            xw_ = __dmul_rn(rb[h], inv);
-            xc_ = __dmul_rn(rb[h + 1], inv);
-            xe_ = __dmul_rn(rb[h + 2], inv);
-            xn_ = __dmul_rn(rc[h + 1], inv);
-          } else if (r >= 1 && r <= rin) {  // every neighbour inside the slice: shared memory
-            const double* Pj = ccol(j - 2) + v;
-            xs_ = Pj[-nx];
-            xw_ = Pj[-1];
-            xc_ = Pj[0];
-            xe_ = Pj[1];
-            xn_ = Pj[nx];
-          } else {
-            xs_ = jr > 0 ? *slot(j - 1, v - nx) : 0.0;
-            xw_ = i > 0 ? *slot(j - 1, v - 1) : 0.0;
-            xc_ = *slot(j - 1, v);
-            xe_ = i + 1 < nx ? *slot(j - 1, v + 1) : 0.0;
-            xn_ = jr + 1 < ny ? *slot(j - 1, v + nx) : 0.0;
+          for (int u = 0; u < UP; ++u) {
+            const int v = v0 + u * NT;
+            const bool in = v < hi;
+            const bool hs = in && jr[u] > 0, hw = in && ii[u] > 0, he = in && ii[u] + 1 < nx, hn = in && jr[u] + 1 < ny;
+            if (j == 1) {  // seed / nu (the multiply rounded as when level 0 is stored)
+              const double* sq = d.seed + (b32 + v);
+              xs_[u] = hs ? __dmul_rn(sq[-nx], inv) : 0.0;
+              xw_[u] = hw ? __dmul_rn(sq[-1], inv) : 0.0;
+              xc_[u] = in ? __dmul_rn(sq[0], inv) : 0.0;
+              xe_[u] = he ? __dmul_rn(sq[1], inv) : 0.0;
+              xn_[u] = hn ? __dmul_rn(sq[nx], inv) : 0.0;
+            } else if (in && v >= nx && v + nx < cnt) {  // every neighbour inside the slice
+              const double* pj = ccol(j - 2) + v;
+              xs_[u] = pj[-nx];
+              xw_[u] = pj[-1];
+              xc_[u] = pj[0];
+              xe_[u] = pj[1];
+              xn_[u] = pj[nx];
+            } else {
+              xs_[u] = hs ? *ext(j - 1, v - nx) : 0.0;
+              xw_[u] = hw ? *ext(j - 1, v - 1) : 0.0;
+              xc_[u] = in ? *ext(j - 1, v) : 0.0;
+              xe_[u] = he ? *ext(j - 1, v + 1) : 0.0;
+              xn_[u] = hn ? *ext(j - 1, v + nx) : 0.0;
+            }
           }
-          double a = 0.0;
-          if (jr > 0) a = __dadd_rn(a, __dmul_rn(cS, xs_));
-          if (i > 0) a = __dadd_rn(a, __dmul_rn(cW, xw_));
-          a = __dadd_rn(a, __dmul_rn(cC, xc_));
-          if (i + 1 < nx) a = __dadd_rn(a, __dmul_rn(cE, xe_));
-          if (jr + 1 < ny) a = __dadd_rn(a, __dmul_rn(cN, xn_));
-          if (r >= 1 && r <= rin)
-            ccol(j - 1)[v] = a;
-          else
-            *slot(j, v) = a;
-          if (v >= 0 && v < cnt) {
-            if (j == 1) d.cand[0][base + v] = xc_;
-            if (!d.build_next) d.cand[j][base + v] = a;
+#pragma unroll
+          for (int u = 0; u < UP; ++u) {
+            const int v = v0 + u * NT;
+            if (v < hi) {
+              double a = 0.0;
+              if (jr[u] > 0) a = __dadd_rn(a, __dmul_rn(cS, xs_[u]));
+              if (ii[u] > 0) a = __dadd_rn(a, __dmul_rn(cW, xw_[u]));
+              a = __dadd_rn(a, __dmul_rn(cC, xc_[u]));
+              if (ii[u] + 1 < nx) a = __dadd_rn(a, __dmul_rn(cE, xe_[u]));
+              if (jr[u] + 1 < ny) a = __dadd_rn(a, __dmul_rn(cN, xn_[u]));
+              *ext(j, v) = a;
+              if ((unsigned)v < (unsigned)cnt) {
+                if (j == 1) d.cand[0][base + v] = xc_[u];
+                if (!d.build_next && j - 1 < SC) d.cand[j][base + v] = a;
+              }
+            }
+            ii[u] += UP * NT;
+            while (ii[u] >= nx) ii[u] -= nx, ++jr[u];
           }
         }
+        csync();
       }
+    } else {
 #pragma unroll
-      for (int t = 0; t < 4; ++t) ra[t] = rb[t], rb[t] = rc[t], rc[t] = rn[t];
-      __syncthreads();
+      for (int j = 1; j < S; ++j) csync();
     }
   } else
   // level 1 reads seed / nu on the fly (level 0 is stored by the same sweep); levels >= 2 read
   // their source from shared memory inside the slice
   for (int j = 1; j < S; ++j) {
-    if (j > 1) grid.sync();
+    if (j > 1) orth_gsync(&d.st->gbar, G);
     orth_mark(d, 44 + 2 * j - 1);
     const bool to_mem = j + 1 < S || !d.build_next;
-    apply_slice(j == 1 ? d.seed : d.cand[j - 1], j >= 2 && j - 2 < kOrthSmemCols ? ccol(j - 2) : seeds, j == 1 ? inv : 0.0,
+    apply_slice(j == 1 ? d.seed : d.cand[j - 1], j >= 2 && j - 2 < SC ? ccol(j - 2) : nullptr, j == 1 ? inv : 0.0,
                 [&](int p, double v, double xc) {
                   if (j == 1) d.cand[0][base + p] = xc;
                   ccol(j - 1)[p] = v;
-                  if (to_mem) d.cand[j][base + p] = v;
+                  if (to_mem && j - 1 < SC) d.cand[j][base + p] = v;
                 });
     orth_mark(d, 44 + 2 * j);
   }
   orth_mark(d, 43);
-  if (!d.build_next) return;  // the last block iteration builds the candidate only
+  if (!d.build_next) {  // the last block iteration builds the candidate only
+    finish();
+    return;
+  }
+  // the ring is the producer's again (the ghost rows are dead: every level ended with a barrier)
+  fence_proxy_async();
+  csync();
+  if (tid == 0) mbar_arrive(&s_go);
   // ---- round-0 products V_0^T cand[:,1:] (sstep.hpp:341)
   r0_products();
-  grid.sync();
+  orth_gsync(&d.st->gbar, G);
   orth_mark(d, 0);
-  // ---- pass 0; the last round also writes the candidate back (final unless a second pass
-  //      runs) and, with zfuse, is followed by a barrier so z = A cand[:,s-1] can be formed
+  // ---- pass 0; the last round also writes the candidate back (final unless a second pass runs)
   for (int i = 0; i < K; ++i) {
     round(i, ((i + 1) & 1) ? d.dr1 : d.dr0, i + 1 == K, [&] {
-      scalar(i, (i & 1) ? d.dr1 : d.dr0, G, 0);
+      scalar(i, (i & 1) ? d.dr1 : d.dr0, 0);
       orth_mark(d, 8 + 3 * i);
     });
     orth_mark(d, 9 + 3 * i);
-    if (i + 1 < K || d.zfuse) grid.sync();
+    if (i + 1 < K) orth_gsync(&d.st->gbar, G);
     orth_mark(d, 10 + 3 * i);
   }
-  // ---- the next block iteration's z = A cand[:,s-1] (to memory) and z.z -> dz + (k+1) s
-  if (d.zfuse) {
-    double zz[1] = {0.0};
-    double* zg = d.z + base;
-    apply_slice(d.cand[S - 1], nullptr, 0.0, [&](int p, double v, double) {
-      zg[p] = v;
-      zz[0] = fma(v, v, zz[0]);
-    });
-    orth_store(zz, red, d.partials, d.dz + (K + 1) * S);
-  }
   orth_mark(d, 60);
-  // ---- cross products and W (needs_reorth, sstep.hpp:401-414), with zfuse also the next
-  //      iteration's Scalar1 products [V_0..V_{k-1}, cand]^T z; blocks in descending order (the
-  //      last rounds' blocks are still in L2, and the next seed sweep starts at block 0)
-  for (int i = K; i >= 0; --i) {
-    if (d.zfuse)
-      cross_block(std::true_type{}, i, d.dcross + i * S * S, d.dz + i * S);
-    else
-      cross_block(std::false_type{}, i, d.dcross + i * S * S, 0);
-  }
+  // ---- cross products and W (needs_reorth, sstep.hpp:401-414); blocks in descending order (the
+  //      next seed sweep starts at block 0)
+  for (int i = K; i >= 0; --i) cross_block(i, d.dcross + i * S * S);
   orth_mark(d, 1);
   orth_mark_all(d, 768);
-  grid.sync();
+  orth_gsync(&d.st->gbar, G);
   orth_mark(d, 2);
-  reduce_dots_dev(d.partials, G, d.dcross, (K + 1) * S * S, prod);
+  orth_reduce(d.partials, (int)G, d.dcross, (K + 1) * S * S, prod);
   {
     const double* sW = prod + K * S * S;
     double cn2 = 0.0;
-    for (int jc = 0; jc < S; ++jc) cn2 += sW[jc * S + jc];
+    for (int jcl = 0; jcl < S; ++jcl) cn2 += sW[jcl * S + jcl];
     for (int i = tid; i < K; i += ORTH_NT) {
       const double* cr = prod + i * S * S;
       double acc = 0.0;
       for (int q = 0; q < S * S; ++q) acc += cr[q] * cr[q];
-      exceed[i] = sqrt(acc) > d.orth_tol * sqrt(sd_trace(gk[i].w, S)) * sqrt(cn2);
+      exceed[i] = sqrt(acc) > d.orth_tol * sqrt(gk[i].trace) * sqrt(cn2);
     }
-    __syncthreads();
+    csync();
     if (tid == 0) {
       int first = -1;
       for (int i = 0; i < K; ++i)
@@ -1374,31 +1563,32 @@ __global__ void __launch_bounds__(ORTH_NT, 1) k_arn_step(const __grid_constant__
           break;
         }
       s_first = first;
+      s_dec = first >= 0 ? 2 : 1;  // (the producer continues with the second pass, or stops)
       if (blockIdx.x == 0) {
         d.rec[RecLayout::kFirst] = first;
         d.rec[RecLayout::kReorth] = first >= 0 ? 1.0 : 0.0;
         d.st->reorth = first >= 0;
-        d.st->zready = d.zfuse && first < 0;
+        d.st->zready = 0;
       }
     }
-    __syncthreads();
+    csync();
   }
   orth_mark(d, 3);
   if (s_first >= 0) {
     // ---- pass 1: V_0^T cand[:,1:], k rounds with t accumulated, then W of the new candidate
     r0_products();
-    grid.sync();
+    orth_gsync(&d.st->gbar, G);
     for (int i = 0; i < K; ++i) {
-      round(i, ((i + 1) & 1) ? d.dr1 : d.dr0, i + 1 == K, [&] { scalar(i, (i & 1) ? d.dr1 : d.dr0, G, 1); });
-      if (i + 1 < K) grid.sync();
+      round(i, ((i + 1) & 1) ? d.dr1 : d.dr0, i + 1 == K, [&] { scalar(i, (i & 1) ? d.dr1 : d.dr0, 1); });
+      if (i + 1 < K) orth_gsync(&d.st->gbar, G);
     }
-    cross_block(std::false_type{}, K, d.dwb, 0);
-    grid.sync();
+    cross_block(K, d.dwb);
+    orth_gsync(&d.st->gbar, G);
     orth_mark(d, 4);
     // the candidate's raw Gram products for the least-squares stream (its snapshot: the next
     // block iteration reuses the partial regions)
     if (blockIdx.x == 0) {
-      reduce_dots_dev(d.partials, G, d.dwb, S * S, tc);  // (ends with a barrier)
+      orth_reduce(d.partials, (int)G, d.dwb, S * S, tc);  // (ends with a barrier)
       if (tid < S * S) d.rec[d.rec_wraw + tid] = tc[tid];
     }
   } else {
@@ -1406,44 +1596,40 @@ __global__ void __launch_bounds__(ORTH_NT, 1) k_arn_step(const __grid_constant__
     if (blockIdx.x == 0 && tid < S * S) d.rec[d.rec_wraw + tid] = prod[K * S * S + tid];
   }
   orth_mark(d, 5);
+  finish();
 }
 
-size_t orth_smem(int s, int k, int64_t P) {
-  return sizeof(double) * (64 + kStepH + (size_t)orth_prod_cap(k, s)) + sizeof(Gram) * (1 + (size_t)k) +
-         sizeof(double) * (ORTH_NT / 32) * (s * s + s) +
-         sizeof(double) * (size_t)std::min(s - 1, kOrthSmemCols) * (size_t)P;
+// dynamic shared memory of the block-iteration kernel without the ring
+size_t orth_smem_base(int s, int k, int64_t P) {
+  const size_t gramc = sizeof(double) * (2 + (size_t)s * s);  // GramC<s>
+  return sizeof(double) * (64 + (size_t)orth_h_cap(k, s) + (size_t)orth_prod_cap(k, s)) + sizeof(Gram) +
+         gramc * (size_t)k + sizeof(double) * (ORTH_NT / 32) * (s * s) + 16 +
+         sizeof(double) * (size_t)std::max(1, std::min(s - 1, kOrthSmemCols)) * (size_t)P;
 }
+inline size_t orth_stage_bytes(int s) { return sizeof(double) * (size_t)s * ORTH_T; }
+// ring stages that fit beside the largest launch of a cycle (k = m), at most kOrthMaxStages
+int orth_stages(int s, int m, int64_t P) {
+  const size_t b = orth_smem_base(s, m, P);
+  if (b >= kOrthSmemCap) return 0;
+  return (int)std::min<size_t>(kOrthMaxStages, (kOrthSmemCap - b) / orth_stage_bytes(s));
+}
+size_t orth_smem(int s, int k, int64_t P, int nst) { return orth_smem_base(s, k, P) + (size_t)nst * orth_stage_bytes(s); }
 
-// ghost-row buffer sizes (doubles) of the row-streamed powers for slices of P points, or
-// false when they do not apply (the 2D constant stencil, s <= 4, nx <= 2 x threads, every
-// non-empty slice at least 4 rows)
-bool stream_powers_ghosts(const DevOp& op, int s, int64_t n, int64_t P, int G, int& g1, int& g2) {
-  g1 = g2 = 0;
-  if (op.kind != kStencilConst || op.dim != 2 || s < 2 || s > 4 || op.nx > 2 * ORTH_NT) return false;
-  const int64_t nx = op.nx;
-  for (int b = 0; b < G; ++b) {
-    const int64_t base = (int64_t)b * P;
-    if (base >= n) break;
-    const int64_t cnt = std::min(P, n - base);
-    const int64_t Rs = (cnt + nx - 1) / nx;
-    if (Rs < 4) return false;
-    for (int j = 1; j <= s - 2; ++j) {
-      const int64_t e = s - 1 - j;
-      const int64_t need = std::max(e * nx, (Rs + e) * nx - cnt);
-      int& g = j == 1 ? g1 : g2;
-      g = (int)std::max<int64_t>(g, need);
-    }
-  }
-  return true;
+// ghost doubles of the level-by-level candidate powers (levels 1..s-2, e_j = s-1-j index rows
+// of nx points on each side), or -1 when they do not apply (2D constant stencil only)
+int64_t powers_ghost_doubles(const DevOp& op, int s, int64_t n) {
+  if (op.kind != kStencilConst || op.dim != 2 || s < 2 || n >= (int64_t)1 << 30) return -1;
+  int64_t g = 0;
+  for (int j = 1; j <= s - 2; ++j) g += 2 * (int64_t)(s - 1 - j) * op.nx;
+  return g;
 }
 
 template <int S>
 void run_orth(Ctx& c, const OrthDesc& d, int G, size_t smem) {
-  // (at most 227 KB per block less the kernel's static shared memory; orth_points caps smem)
   ensure_smem(k_arn_step<S>, smem);
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = G;
-  cfg.blockDim = ORTH_NT;
+  cfg.blockDim = ORTH_THREADS;
   cfg.dynamicSmemBytes = smem;
   cfg.stream = c.stream;
   cudaLaunchAttribute at[1];
@@ -1767,7 +1953,7 @@ struct Engine {
   int64_t orth_points() const {
     if (!c.orth || c.world() != 1 || g.grouped() || s < 2 || op.d.kind == kIlu0) return 0;
     const int64_t P = ((op.n + mk_ctas() - 1) / mk_ctas() + 1) & ~(int64_t)1;
-    return orth_smem(s, m, P) <= kOrthSmemCap ? P : 0;
+    return orth_stages(s, m, P) >= 2 ? P : 0;
   }
 
   // CTAs of the block-iteration kernel: one per SM, less the one SM left to the side stream's
@@ -1782,9 +1968,6 @@ struct Engine {
     d.s = s;
     d.k = k;
     d.build_next = build_next ? 1 : 0;
-    // (off by default: the fused products make the cross pass and the extra barrier cost
-    // about what the skipped Scalar1 sweep saves, measured 0.5-0.8% slower on C2)
-    d.zfuse = build_next && c.zfuse ? 1 : 0;
     d.n = op.n;
     d.P = orth_points();
     d.op = op.d;
@@ -1813,12 +1996,15 @@ struct Engine {
     static const bool trace = std::getenv("SKC_TRACE_ORTH") != nullptr;
     if (trace) d.trace = (unsigned long long*)c.workspace("orth_trace", 1024 * sizeof(unsigned long long));
     const int G = mk_ctas();
-    int g1 = 0, g2 = 0;
-    d.spow = c.spow && stream_powers_ghosts(op.d, s, op.n, d.P, G, g1, g2);
-    d.g1 = d.spow ? g1 : 0;
-    d.g2 = d.spow ? g2 : 0;
-    if (d.spow) d.ghosts = (double*)c.workspace("orth_ghosts", sizeof(double) * (size_t)G * (g1 + g2));
-    const size_t smem = orth_smem(s, k, d.P);
+    d.nst = orth_stages(s, m, d.P);
+    // (evict_first measured best on C2: 3913 vs 3845 s-steps/s unhinted, 3837 evict_last)
+    static const int hint = std::getenv("SKC_ORTH_HINT") ? std::atoi(std::getenv("SKC_ORTH_HINT")) : 3;
+    d.hint = hint;
+    if (const char* e = std::getenv("SKC_ORTH_NST")) d.nst = std::max(2, std::min(d.nst, std::atoi(e)));
+    // level-by-level candidate powers with the ghost rows in the (then idle) ring, when they fit
+    const int64_t gd = powers_ghost_doubles(op.d, s, op.n);
+    d.spow = c.spow && gd >= 0 && sizeof(double) * (size_t)gd <= (size_t)d.nst * orth_stage_bytes(s);
+    const size_t smem = orth_smem(s, k, d.P, d.nst);
     // algorithmic bytes, SURVEY 8(d) model (block-CGS-equivalent passes): a block step k < m
     // moves SpMV(2) + V^T z (ks+1) + seed (ks+2) + MPK (s+1) + V^T cand (ks+s) +
     // update/cross/Gram (ks+2s-1) = 4ks+4s+5 vectors, the last one (no build) 2ms+s+6.  The

@@ -206,7 +206,6 @@ struct Ctx {
   bool profiling = false;
   bool pdl = true;   // programmatic dependent launch for solver kernels (SKC_PDL=0 disables)
   bool orth = true;  // on-chip block orthogonalization when it fits (SKC_ORTH=0 disables)
-  bool zfuse = false;   // megakernel: next Scalar1 products in the cross pass (SKC_ZFUSE=1)
   bool persist = true;  // persistent s-Omin for small problems (SKC_PERSIST=0 disables)
   bool spow = true;     // megakernel: row-streamed candidate powers (SKC_SPOW=0 disables)
   // GPU-count-independent reductions (grouped geometry): bitwise the same results on 1, 2, 4

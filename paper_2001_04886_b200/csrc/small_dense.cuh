@@ -187,22 +187,12 @@ SKC_HD void gram_solve(const Gram& g, const double* rhs, double* x) {
 // (hence the same bits) with every array in registers instead of local memory.  The LDL^T
 // fallback (a failed Cholesky attempt: rare, ill-conditioned Gram matrices) takes the generic
 // path above.
+// the Cholesky path of gram_solve on the factor alone (row-major L, order N)
 template <int N>
-__device__ __forceinline__ void gram_solve_t(const Gram& g, const double* rhs, double* x) {
-  if (N == 1 || g.used_ldlt) {
-    // (the generic path through copies: the caller's arrays never have their address taken, so
-    // they stay in registers on the common Cholesky path)
-    double r2[kMaxS], x2[kMaxS];
-#pragma unroll
-    for (int i = 0; i < N; ++i) r2[i] = rhs[i];
-    gram_solve(g, r2, x2);
-#pragma unroll
-    for (int i = 0; i < N; ++i) x[i] = x2[i];
-    return;
-  }
+__device__ __forceinline__ void chol_solve_t(const double* fac, const double* rhs, double* x) {
   double f[N * N];
 #pragma unroll
-  for (int q = 0; q < N * N; ++q) f[q] = g.fac[q];
+  for (int q = 0; q < N * N; ++q) f[q] = fac[q];
 #pragma unroll
   for (int i = 0; i < N; ++i) {
     double acc = rhs[i];
@@ -217,6 +207,22 @@ __device__ __forceinline__ void gram_solve_t(const Gram& g, const double* rhs, d
     for (int k = ii + 1; k < N; ++k) acc -= f[k * N + ii] * x[k];
     x[ii] = acc / f[ii * N + ii];
   }
+}
+
+template <int N>
+__device__ __forceinline__ void gram_solve_t(const Gram& g, const double* rhs, double* x) {
+  if (N == 1 || g.used_ldlt) {
+    // (the generic path through copies: the caller's arrays never have their address taken, so
+    // they stay in registers on the common Cholesky path)
+    double r2[kMaxS], x2[kMaxS];
+#pragma unroll
+    for (int i = 0; i < N; ++i) r2[i] = rhs[i];
+    gram_solve(g, r2, x2);
+#pragma unroll
+    for (int i = 0; i < N; ++i) x[i] = x2[i];
+    return;
+  }
+  chol_solve_t<N>(g.fac, rhs, x);
 }
 
 template <int N>

@@ -86,15 +86,6 @@ def test_sgmres_per_round_kernel_path(port, name, monkeypatch):
     _check_case(port, name, *run_gpu_case(Context(0), name, True))
 
 
-@pytest.mark.parametrize("name", [n for n in SOLVE_CASES if MANIFEST[n]["method"] == "sgmres"])
-def test_sgmres_fused_scalar1_path(port, name, monkeypatch):
-    """The block-iteration kernel with the next iteration's z and Scalar1 products formed in the
-    cross pass (SKC_ZFUSE=1, off by default) against the reference."""
-    from paper_2001_04886_b200 import Context
-    monkeypatch.setenv("SKC_ZFUSE", "1")
-    _check_case(port, name, *run_gpu_case(Context(0), name, True))
-
-
 @pytest.mark.parametrize("name", [n for n in SOLVE_CASES if MANIFEST[n]["method"] == "somin"])
 def test_somin_batched_kernel_path(port, name, monkeypatch):
     """The batched per-operation s-Omin kernels (large problems, s > 4, s-GCR, debug checks,
