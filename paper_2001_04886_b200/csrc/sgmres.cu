@@ -973,7 +973,9 @@ __global__ void __launch_bounds__(ORTH_THREADS, 1) k_arn_step(const __grid_const
   };
   // this slice of candidate column j+1 (j = 0..s-2): the first SC in shared memory, the rest in
   // their basis slots in global memory
-  auto ccol = [&](int j) -> double* { return j < SC ? sc + (int64_t)j * d.P : d.cand[j + 1] + base; };
+  // (slots in reverse order: column 1 in the last slot, so that slot 0 -- z, the seed and level 0
+  // of the powers -- is not written before level 1 is complete)
+  auto ccol = [&](int j) -> double* { return j < SC ? sc + (int64_t)(SC - 1 - j) * d.P : d.cand[j + 1] + base; };
   // in-memory candidate column g (candidate column SC+1+g), this slice
   auto gcol = [&](int g) -> double* { return d.cand[SC + 1 + g] + base; };
 
@@ -1266,8 +1268,7 @@ __global__ void __launch_bounds__(ORTH_THREADS, 1) k_arn_step(const __grid_const
     for (int p = tid; p < cnt; p += ORTH_NT, w.step(d.op, ORTH_NT))
       put(p, apply_point(d.op, fetch, base + p, w), fetch(base + p));
   };
-  // z and seed of this slice stay in shared memory (candidate column 1's slot, free until the
-  // powers reach it)
+  // z and seed of this slice stay in shared memory (slot 0, free until the powers reach it)
   double* zs = sc;
   apply_slice(d.vin, nullptr, 0.0, [&](int p, double v, double) { zs[p] = v; });
   orth_mark(d, 40);
@@ -1403,34 +1404,149 @@ __global__ void __launch_bounds__(ORTH_THREADS, 1) k_arn_step(const __grid_const
   //      every level is an exact spmv of the previous one; levels 1..s-1 stay on chip (or in
   //      their basis slots), levels 0..s-2 also go to memory for the neighbours' next level
   orth_mark(d, 44);
-  if (d.spow) {
-    // Level by level over the slice extended by e_j = s-1-j index rows of nx points on each side
-    // (level j is needed that far for the slice's last level), redundantly with the neighbouring
-    // CTAs, so no level needs another CTA's results and CTA barriers suffice: level 1 reads
-    // seed / nu from memory (the whole seed was written before the grid barrier), the later
-    // levels read the previous one from shared memory -- the slice part in the candidate's
-    // columns, the ghost parts in the idle ring.  Each point is the same ascending-column sum
-    // as spmv, so the levels are bit-identical to successive sweeps.  (Host: 2D constant
-    // stencil, the ghost rows fit the ring.)
+  if (d.spow == 2) {
+    // Row-aligned slices (P a multiple of nx; host: 2D constant stencil, nx even, nx <= 2 x 512
+    // threads, the ghost rows fit the ring): level by level over the slice's grid rows extended
+    // by e_j = s-1-j rows on each side (level j is needed that far for the slice's last level),
+    // redundantly with the neighbouring CTAs, so no level needs another CTA's results and CTA
+    // barriers suffice.  Every level lives in shared memory: the slice rows in the candidate's
+    // column slots (level 0 = seed / nu in slot 0, which is next written after level 1 is
+    // done), the ghost rows in the idle ring (two regions used alternately).  A thread owns a
+    // column pair: it reads its pair of the rows r-1, r, r+1 of the previous level as 16-byte
+    // loads and takes the W / E neighbours from the adjacent lanes (shared memory at the warp
+    // edges).  Each point is the same ascending-column sum as spmv (absent neighbours skipped),
+    // so the levels are bit-identical to successive sweeps.
     const int nx = (int)d.op.nx, ny = (int)d.op.ny;
     const double cS = d.op.coef[1], cW = d.op.coef[2], cC = d.op.coef[3], cE = d.op.coef[4], cN = d.op.coef[5];
-    // ghost rows of level j (1 <= j <= s-2): 2 e_j nx doubles (low side, then high side)
-    auto ghost = [&](int j) -> double* {
-      int o = 0;
-      for (int i = 1; i < j; ++i) o += 2 * (S - 1 - i) * nx;
-      return stg + o;
+    const int R0 = (int)(base / nx), Rs = cnt / nx;
+    double* regA = stg;
+    double* regB = stg + 2 * (S - 1) * nx;
+    // row r (grid row) of level j, inside the level's extended range
+    auto rowp = [&](int j, int r) -> double* {
+      const int rr = r - R0, e = S - 1 - j;
+      if (rr >= 0 && rr < Rs) return (j == 0 ? zs : ccol(j - 1)) + rr * nx;
+      double* g = (j & 1) ? regB : regA;
+      return rr < 0 ? g + (rr + e) * nx : g + (e + rr - Rs) * nx;
     };
-    // level j (>= 1) at slice-relative index v inside its extended range
-    auto ext = [&](int j, int v) -> double* {
-      if ((unsigned)v < (unsigned)cnt) return ccol(j - 1) + v;
-      const int e = S - 1 - j;
-      double* g = ghost(j);
-      return v < 0 ? g + (v + e * nx) : g + (e * nx + (v - cnt));
-    };
-    const int b32 = (int)base, n32 = (int)d.n;
+    const int c0 = 2 * tid;
+    const bool act = c0 < nx;
+    if (cnt > 0) {
+      // level 0: the slice in place (and to memory), its ghost rows from the seed in memory
+      for (int p = tid; p < cnt; p += NT) {
+        const double v0 = __dmul_rn(zs[p], inv);
+        zs[p] = v0;
+        d.cand[0][base + p] = v0;
+      }
+      // (ghost index g: e0 rows below the slice, then e0 rows above it; four loads in flight)
+      const int e0 = S - 1, half = e0 * nx;
+      for (int g0 = tid; g0 < 2 * half; g0 += 4 * NT) {
+        double v[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int g = g0 + u * NT;
+          const int w = g < half ? g : g - half;
+          const int r = (g < half ? R0 - e0 : R0 + Rs) + w / nx;
+          v[u] = g < 2 * half && r >= 0 && r < ny ? __ldcg(d.seed + (int64_t)r * nx + w % nx) : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          if (g0 + u * NT < 2 * half) regA[g0 + u * NT] = __dmul_rn(v[u], inv);
+      }
+    }
+    csync();
+    orth_mark(d, 45);
     if (cnt > 0) {
 #pragma unroll
       for (int j = 1; j < S; ++j) {
+        if (j > 1) orth_mark(d, 44 + 2 * j - 1);
+        const int e = S - 1 - j;
+        const int rlo = R0 - e < 0 ? 0 : R0 - e, rhi = R0 + Rs + e > ny ? ny : R0 + Rs + e;
+        for (int r = rlo; r < rhi; ++r) {
+          const bool hs = r > 0, hn = r + 1 < ny;
+          const double* pc = rowp(j - 1, r);
+          const double* ps = hs ? rowp(j - 1, r - 1) : pc;
+          const double* pn = hn ? rowp(j - 1, r + 1) : pc;
+          double2 C = make_double2(0.0, 0.0), Sv = C, Nv = C;
+          if (act) {
+            C = *reinterpret_cast<const double2*>(pc + c0);
+            Sv = *reinterpret_cast<const double2*>(ps + c0);
+            Nv = *reinterpret_cast<const double2*>(pn + c0);
+          }
+          double w0 = __shfl_up_sync(0xffffffffu, C.y, 1);
+          double e1 = __shfl_down_sync(0xffffffffu, C.x, 1);
+          if (act) {
+            if (lane == 0 && c0 > 0) w0 = pc[c0 - 1];
+            if (lane == 31 && c0 + 2 < nx) e1 = pc[c0 + 2];
+            double a0 = 0.0, a1 = 0.0;
+            if (hs) {
+              a0 = __dadd_rn(a0, __dmul_rn(cS, Sv.x));
+              a1 = __dadd_rn(a1, __dmul_rn(cS, Sv.y));
+            }
+            if (c0 > 0) a0 = __dadd_rn(a0, __dmul_rn(cW, w0));
+            a1 = __dadd_rn(a1, __dmul_rn(cW, C.x));
+            a0 = __dadd_rn(a0, __dmul_rn(cC, C.x));
+            a1 = __dadd_rn(a1, __dmul_rn(cC, C.y));
+            a0 = __dadd_rn(a0, __dmul_rn(cE, C.y));
+            if (c0 + 2 < nx) a1 = __dadd_rn(a1, __dmul_rn(cE, e1));
+            if (hn) {
+              a0 = __dadd_rn(a0, __dmul_rn(cN, Nv.x));
+              a1 = __dadd_rn(a1, __dmul_rn(cN, Nv.y));
+            }
+            *reinterpret_cast<double2*>(rowp(j, r) + c0) = make_double2(a0, a1);
+            if (!d.build_next && j - 1 < SC && r >= R0 && r < R0 + Rs)
+              *reinterpret_cast<double2*>(d.cand[j] + (int64_t)r * nx + c0) = make_double2(a0, a1);
+          }
+        }
+        csync();
+        orth_mark(d, 44 + 2 * j);
+      }
+    } else {
+#pragma unroll
+      for (int j = 1; j < S; ++j) csync();
+    }
+  } else
+  if (d.spow) {
+    // Level by level over the slice extended by e_j = s-1-j index rows of nx points on each side
+    // (level j is needed that far for the slice's last level), redundantly with the neighbouring
+    // CTAs, so no level needs another CTA's results and CTA barriers suffice.  Every level lives
+    // in shared memory: the slice part in the candidate's column slots (level 0 = seed / nu in
+    // the slot of the last on-chip column, which is written after level 1 is done), the ghost
+    // parts in the idle ring (two regions used alternately).  With a single on-chip column
+    // (s = 2) level 1 reads seed / nu from memory instead.  Each point is the same
+    // ascending-column sum as spmv, so the levels are bit-identical to successive sweeps.
+    // (Host: 2D constant stencil, n < 2^30, the ghost rows fit the ring.)
+    constexpr bool L0S = SC >= 2;
+    const int nx = (int)d.op.nx, ny = (int)d.op.ny;
+    const double cS = d.op.coef[1], cW = d.op.coef[2], cC = d.op.coef[3], cE = d.op.coef[4], cN = d.op.coef[5];
+    const int b32 = (int)base, n32 = (int)d.n;
+    double* regA = stg;
+    double* regB = stg + 2 * (S - 1) * nx;
+    // level j at slice-relative index v inside its extended range
+    auto ext = [&](int j, int v) -> double* {
+      if ((unsigned)v < (unsigned)cnt) return j == 0 ? zs + v : ccol(j - 1) + v;
+      const int e = S - 1 - j;
+      double* g = (j & 1) ? regB : regA;
+      return v < 0 ? g + (v + e * nx) : g + (e * nx + (v - cnt));
+    };
+    if (L0S && cnt > 0) {
+      // level 0: the slice in place (and to memory), its ghost rows from the seed in memory
+      for (int p = tid; p < cnt; p += NT) {
+        const double v0 = __dmul_rn(zs[p], inv);
+        zs[p] = v0;
+        d.cand[0][base + p] = v0;
+      }
+      const int e0 = S - 1;
+      const int glo = b32 - e0 * nx < 0 ? -b32 : -e0 * nx;
+      const int ghi = b32 + cnt + e0 * nx > n32 ? n32 - b32 : cnt + e0 * nx;
+      for (int v = glo + tid; v < 0; v += NT) *ext(0, v) = __dmul_rn(__ldcg(d.seed + (b32 + v)), inv);
+      for (int v = cnt + tid; v < ghi; v += NT) *ext(0, v) = __dmul_rn(__ldcg(d.seed + (b32 + v)), inv);
+    }
+    if (L0S) csync();
+    orth_mark(d, 45);
+    if (cnt > 0) {
+#pragma unroll
+      for (int j = 1; j < S; ++j) {
+        if (j > 1) orth_mark(d, 44 + 2 * j - 1);
         const int e = S - 1 - j;
         int lo = -e * nx, hi = cnt + e * nx;
         if (b32 + lo < 0) lo = -b32;
@@ -1442,49 +1558,61 @@ __global__ void __launch_bounds__(ORTH_THREADS, 1) k_arn_step(const __grid_const
           const int q = b32 + lo + tid + u * NT;
           ii[u] = q % nx, jr[u] = q / nx;
         }
+        double* outs = ccol(j - 1);
+        const double* ins = j == 1 ? zs : ccol(j > 1 ? j - 2 : 0);
         for (int v0 = lo + tid; v0 < hi; v0 += UP * NT) {
-          double xs_[UP], xw_[UP], xc_[UP], xe_[UP], xn_[UP];
+          double a[UP], x0[UP];
 #pragma unroll
           for (int u = 0; u < UP; ++u) {
             const int v = v0 + u * NT;
             const bool in = v < hi;
-            const bool hs = in && jr[u] > 0, hw = in && ii[u] > 0, he = in && ii[u] + 1 < nx, hn = in && jr[u] + 1 < ny;
-            if (j == 1) {  // seed / nu (the multiply rounded as when level 0 is stored)
-              const double* sq = d.seed + (b32 + v);
-              xs_[u] = hs ? __dmul_rn(sq[-nx], inv) : 0.0;
-              xw_[u] = hw ? __dmul_rn(sq[-1], inv) : 0.0;
-              xc_[u] = in ? __dmul_rn(sq[0], inv) : 0.0;
-              xe_[u] = he ? __dmul_rn(sq[1], inv) : 0.0;
-              xn_[u] = hn ? __dmul_rn(sq[nx], inv) : 0.0;
-            } else if (in && v >= nx && v + nx < cnt) {  // every neighbour inside the slice
-              const double* pj = ccol(j - 2) + v;
-              xs_[u] = pj[-nx];
-              xw_[u] = pj[-1];
-              xc_[u] = pj[0];
-              xe_[u] = pj[1];
-              xn_[u] = pj[nx];
-            } else {
-              xs_[u] = hs ? *ext(j - 1, v - nx) : 0.0;
-              xw_[u] = hw ? *ext(j - 1, v - 1) : 0.0;
-              xc_[u] = in ? *ext(j - 1, v) : 0.0;
-              xe_[u] = he ? *ext(j - 1, v + 1) : 0.0;
-              xn_[u] = hn ? *ext(j - 1, v + nx) : 0.0;
+            a[u] = 0.0;
+            x0[u] = 0.0;
+            if ((L0S || j > 1) && in && v >= nx && v + nx < cnt && ii[u] > 0 && ii[u] + 1 < nx) {
+              // every neighbour present and inside the slice
+              const double* pj = ins + v;
+              double t = __dadd_rn(0.0, __dmul_rn(cS, pj[-nx]));
+              t = __dadd_rn(t, __dmul_rn(cW, pj[-1]));
+              x0[u] = pj[0];
+              t = __dadd_rn(t, __dmul_rn(cC, x0[u]));
+              t = __dadd_rn(t, __dmul_rn(cE, pj[1]));
+              a[u] = __dadd_rn(t, __dmul_rn(cN, pj[nx]));
+            } else if (in) {
+              const bool hs = jr[u] > 0, hw = ii[u] > 0, he = ii[u] + 1 < nx, hn = jr[u] + 1 < ny;
+              double xs_, xw_, xe_, xn_;
+              if (!L0S && j == 1) {  // seed / nu from memory (the multiply rounded as when level 0 is stored)
+                const double* sq = d.seed + (b32 + v);
+                xs_ = hs ? __dmul_rn(sq[-nx], inv) : 0.0;
+                xw_ = hw ? __dmul_rn(sq[-1], inv) : 0.0;
+                x0[u] = __dmul_rn(sq[0], inv);
+                xe_ = he ? __dmul_rn(sq[1], inv) : 0.0;
+                xn_ = hn ? __dmul_rn(sq[nx], inv) : 0.0;
+              } else {
+                xs_ = hs ? *ext(j - 1, v - nx) : 0.0;
+                xw_ = hw ? *ext(j - 1, v - 1) : 0.0;
+                x0[u] = *ext(j - 1, v);
+                xe_ = he ? *ext(j - 1, v + 1) : 0.0;
+                xn_ = hn ? *ext(j - 1, v + nx) : 0.0;
+              }
+              double t = 0.0;
+              if (hs) t = __dadd_rn(t, __dmul_rn(cS, xs_));
+              if (hw) t = __dadd_rn(t, __dmul_rn(cW, xw_));
+              t = __dadd_rn(t, __dmul_rn(cC, x0[u]));
+              if (he) t = __dadd_rn(t, __dmul_rn(cE, xe_));
+              if (hn) t = __dadd_rn(t, __dmul_rn(cN, xn_));
+              a[u] = t;
             }
           }
 #pragma unroll
           for (int u = 0; u < UP; ++u) {
             const int v = v0 + u * NT;
             if (v < hi) {
-              double a = 0.0;
-              if (jr[u] > 0) a = __dadd_rn(a, __dmul_rn(cS, xs_[u]));
-              if (ii[u] > 0) a = __dadd_rn(a, __dmul_rn(cW, xw_[u]));
-              a = __dadd_rn(a, __dmul_rn(cC, xc_[u]));
-              if (ii[u] + 1 < nx) a = __dadd_rn(a, __dmul_rn(cE, xe_[u]));
-              if (jr[u] + 1 < ny) a = __dadd_rn(a, __dmul_rn(cN, xn_[u]));
-              *ext(j, v) = a;
               if ((unsigned)v < (unsigned)cnt) {
-                if (j == 1) d.cand[0][base + v] = xc_[u];
-                if (!d.build_next && j - 1 < SC) d.cand[j][base + v] = a;
+                outs[v] = a[u];
+                if (!L0S && j == 1) d.cand[0][base + v] = x0[u];
+                if (!d.build_next && j - 1 < SC) d.cand[j][base + v] = a[u];
+              } else {
+                *ext(j, v) = a[u];
               }
             }
             ii[u] += UP * NT;
@@ -1492,6 +1620,7 @@ __global__ void __launch_bounds__(ORTH_THREADS, 1) k_arn_step(const __grid_const
           }
         }
         csync();
+        orth_mark(d, 44 + 2 * j);
       }
     } else {
 #pragma unroll
@@ -1615,13 +1744,12 @@ int orth_stages(int s, int m, int64_t P) {
 }
 size_t orth_smem(int s, int k, int64_t P, int nst) { return orth_smem_base(s, k, P) + (size_t)nst * orth_stage_bytes(s); }
 
-// ghost doubles of the level-by-level candidate powers (levels 1..s-2, e_j = s-1-j index rows
-// of nx points on each side), or -1 when they do not apply (2D constant stencil only)
+// ghost doubles of the level-by-level candidate powers (level j: e_j = s-1-j index rows of nx
+// points on each side), or -1 when they do not apply (2D constant stencil only)
 int64_t powers_ghost_doubles(const DevOp& op, int s, int64_t n) {
   if (op.kind != kStencilConst || op.dim != 2 || s < 2 || n >= (int64_t)1 << 30) return -1;
-  int64_t g = 0;
-  for (int j = 1; j <= s - 2; ++j) g += 2 * (int64_t)(s - 1 - j) * op.nx;
-  return g;
+  // two regions used alternately: levels 0, 2, .. (e_0 = s-1 rows a side) and 1, 3, .. (e_1 = s-2)
+  return s >= 3 ? 2 * (int64_t)(2 * s - 3) * op.nx : 0;
 }
 
 template <int S>
@@ -1950,10 +2078,28 @@ struct Engine {
 
   // points per CTA of the on-chip orthogonalization (one CTA per SM), or 0 when it is off or
   // the candidate slices do not fit in shared memory
-  int64_t orth_points() const {
+  // (spow: how the candidate powers run -- 2 row-aligned slices, 1 level by level on index
+  // ranges, 0 per-level sweeps with grid barriers)
+  int64_t orth_points(int* spow = nullptr) const {
+    if (spow) *spow = 0;
     if (!c.orth || c.world() != 1 || g.grouped() || s < 2 || op.d.kind == kIlu0) return 0;
-    const int64_t P = ((op.n + mk_ctas() - 1) / mk_ctas() + 1) & ~(int64_t)1;
-    return orth_stages(s, m, P) >= 2 ? P : 0;
+    const int G = mk_ctas();
+    const int64_t gd = c.spow ? powers_ghost_doubles(op.d, s, op.n) : -1;
+    auto ghosts_fit = [&](int64_t P) {
+      return gd >= 0 && sizeof(double) * (size_t)gd <= (size_t)orth_stages(s, m, P) * orth_stage_bytes(s);
+    };
+    if (gd >= 0 && s >= 3 && op.d.nx % 2 == 0 && op.d.nx <= 2 * ORTH_NT) {
+      // whole grid rows per CTA, for the row-wise candidate powers
+      const int64_t P = (op.d.ny + G - 1) / G * op.d.nx;
+      if (orth_stages(s, m, P) >= 2 && ghosts_fit(P)) {
+        if (spow) *spow = 2;
+        return P;
+      }
+    }
+    const int64_t P = ((op.n + G - 1) / G + 1) & ~(int64_t)1;
+    if (orth_stages(s, m, P) < 2) return 0;
+    if (spow) *spow = ghosts_fit(P) ? 1 : 0;
+    return P;
   }
 
   // CTAs of the block-iteration kernel: one per SM, less the one SM left to the side stream's
@@ -1969,7 +2115,7 @@ struct Engine {
     d.k = k;
     d.build_next = build_next ? 1 : 0;
     d.n = op.n;
-    d.P = orth_points();
+    d.P = orth_points(&d.spow);
     d.op = op.d;
     d.vin = col(k - 1, s - 1);
     d.z = z;
@@ -2000,10 +2146,6 @@ struct Engine {
     // (evict_first measured best on C2: 3913 vs 3845 s-steps/s unhinted, 3837 evict_last)
     static const int hint = std::getenv("SKC_ORTH_HINT") ? std::atoi(std::getenv("SKC_ORTH_HINT")) : 3;
     d.hint = hint;
-    if (const char* e = std::getenv("SKC_ORTH_NST")) d.nst = std::max(2, std::min(d.nst, std::atoi(e)));
-    // level-by-level candidate powers with the ghost rows in the (then idle) ring, when they fit
-    const int64_t gd = powers_ghost_doubles(op.d, s, op.n);
-    d.spow = c.spow && gd >= 0 && sizeof(double) * (size_t)gd <= (size_t)d.nst * orth_stage_bytes(s);
     const size_t smem = orth_smem(s, k, d.P, d.nst);
     // algorithmic bytes, SURVEY 8(d) model (block-CGS-equivalent passes): a block step k < m
     // moves SpMV(2) + V^T z (ks+1) + seed (ks+2) + MPK (s+1) + V^T cand (ks+s) +
