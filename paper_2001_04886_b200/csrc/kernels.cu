@@ -66,6 +66,89 @@ __global__ void __launch_bounds__(AZ_TX* AZ_TY) k_apply3z(const __grid_constant_
   }
 }
 
+// 3D variable-k stencil, z-marching, every face coefficient computed once: a 32 x 8 thread tile
+// of (x, y) columns walks KZ planes.  The harmonic-mean face coefficient 2 kp kq / (kp + kq)
+// (one fp64 division) is symmetric in its bits (2 kp is exact, the product and the sum
+// commute), so a thread computes only its +x, +y and +z faces and takes -x from the lane to
+// its left (lane 0 of a row is a halo column: the tiles overlap by one column in x), -y from
+// the thread row below through shared memory (row 0 of the tile recomputes it: a warp-uniform
+// branch) and -z from its own previous plane -- 3 + 1/8 + 1/16 divisions per point instead of
+// 6.  The x values of a column stay in registers across planes as in k_apply3z.  Same
+// arithmetic order as stencil_point (faces -z,-y,-x,+x,+y,+z; own k on boundary faces).
+constexpr int AV_TX = 32, AV_TY = 8, AV_KZ = 16;
+__global__ void __launch_bounds__(AV_TX* AV_TY) k_apply3z_vark(const __grid_constant__ DevOp op,
+                                                              const double* __restrict__ x, double* __restrict__ y,
+                                                              const int* halt, const int* cond) {
+  SKC_PDL_ENTRY();
+  if (skip_launch(halt, cond)) return;
+  __shared__ double sfn[2][AV_TY][AV_TX];  // the +y faces of a plane (double-buffered)
+  const int nx = (int)op.nx, ny = (int)op.ny, nz = (int)op.nz;
+  const int tx = threadIdx.x % AV_TX, ty = threadIdx.x / AV_TX;
+  const int i = blockIdx.x * (AV_TX - 1) + tx - 1;  // (lane 0: the halo column to the left)
+  const int j = blockIdx.y * AV_TY + ty;
+  const bool in = i >= 0 && i < nx && j < ny;
+  const bool outp = in && tx > 0;
+  const int l0 = blockIdx.z * AV_KZ, l1 = min(nz, l0 + AV_KZ);
+  const int64_t plane = (int64_t)nx * ny;
+  const double ch2 = op.ch2;
+  const bool hW = in && i > 0, hE = in && i + 1 < nx, hS = in && j > 0, hN = in && j + 1 < ny;
+  const int64_t c = in ? (int64_t)j * nx + i : 0;
+  const double* xc_ = x + c;
+  const double* kc_ = op.kcell + c;
+  double xm = in && l0 > 0 ? __ldg(xc_ + (int64_t)(l0 - 1) * plane) : 0.0;
+  double xc = in ? __ldg(xc_ + (int64_t)l0 * plane) : 0.0;
+  double kc = in ? __ldg(kc_ + (int64_t)l0 * plane) : 1.0;
+  double fzm = kc;  // the -z face (own k at the domain boundary)
+  if (l0 > 0) {     // (block-uniform)
+    const double km = in ? __ldg(kc_ + (int64_t)(l0 - 1) * plane) : 1.0;
+    fzm = face_k(kc, km);
+  }
+  for (int l = l0; l < l1; ++l) {
+    const int64_t o = (int64_t)l * plane;
+    const bool hZ = l + 1 < nz;
+    const double xp = in && hZ ? __ldg(xc_ + o + plane) : 0.0;
+    const double kp = in && hZ ? __ldg(kc_ + o + plane) : 1.0;
+    const double kE = hE ? __ldg(kc_ + o + 1) : 1.0, kN = hN ? __ldg(kc_ + o + nx) : 1.0;
+    const double vs = hS ? __ldg(xc_ + o - nx) : 0.0, vw = hW ? __ldg(xc_ + o - 1) : 0.0;
+    const double ve = hE ? __ldg(xc_ + o + 1) : 0.0, vn = hN ? __ldg(xc_ + o + nx) : 0.0;
+    const double fE = hE ? face_k(kc, kE) : kc;
+    const double fN = hN ? face_k(kc, kN) : kc;
+    const double fZ = hZ ? face_k(kc, kp) : kc;
+    sfn[l & 1][ty][tx] = fN;
+    double fW = __shfl_up_sync(0xffffffffu, fE, 1);
+    if (!hW) fW = kc;
+    __syncthreads();
+    double fS;
+    if (ty > 0) {
+      fS = hS ? sfn[l & 1][ty - 1][tx] : kc;
+    } else {  // (warp-uniform: the tile's first row)
+      const double kS = hS ? __ldg(kc_ + o - nx) : 1.0;
+      fS = hS ? face_k(kc, kS) : kc;
+    }
+    if (outp) {
+      double dsum = fzm;
+      dsum = __dadd_rn(dsum, fS);
+      dsum = __dadd_rn(dsum, fW);
+      dsum = __dadd_rn(dsum, fE);
+      dsum = __dadd_rn(dsum, fN);
+      dsum = __dadd_rn(dsum, fZ);
+      double a = 0.0;
+      if (l > 0) a = __dadd_rn(a, __dmul_rn(__dsub_rn(-fzm, ch2), xm));
+      if (hS) a = __dadd_rn(a, __dmul_rn(__dsub_rn(-fS, ch2), vs));
+      if (hW) a = __dadd_rn(a, __dmul_rn(__dsub_rn(-fW, ch2), vw));
+      a = __dadd_rn(a, __dmul_rn(dsum, xc));
+      if (hE) a = __dadd_rn(a, __dmul_rn(__dadd_rn(-fE, ch2), ve));
+      if (hN) a = __dadd_rn(a, __dmul_rn(__dadd_rn(-fN, ch2), vn));
+      if (hZ) a = __dadd_rn(a, __dmul_rn(__dadd_rn(-fZ, ch2), xp));
+      y[o + c] = a;
+    }
+    xm = xc;
+    xc = xp;
+    kc = kp;
+    fzm = fZ;
+  }
+}
+
 __global__ void __launch_bounds__(256) k_apply_csr(const __grid_constant__ DevOp op, const double* __restrict__ x,
                                                    double* __restrict__ y, const int* halt, const int* cond) {
   SKC_PDL_ENTRY();
@@ -109,7 +192,12 @@ void launch_apply(Ctx& c, const DevOp& op, const double* x, double* y, const int
         launch_k(c, k_apply3z, gz, AZ_TX * AZ_TY, 0, op, x, y, halt, cond);
         break;
       }
-      case 32: launch_k(c, k_apply<3, kStencilVarK>, grid, 256, 0, op, x, y, halt, cond); break;
+      case 32: {
+        const dim3 gz((unsigned)((op.nx + AV_TX - 2) / (AV_TX - 1)), (unsigned)((op.ny + AV_TY - 1) / AV_TY),
+                      (unsigned)((op.nz + AV_KZ - 1) / AV_KZ));
+        launch_k(c, k_apply3z_vark, gz, AV_TX * AV_TY, 0, op, x, y, halt, cond);
+        break;
+      }
       case 33: launch_k(c, k_apply<3, kStencilDia>, grid, 256, 0, op, x, y, halt, cond); break;
       default: fail(SKC_EINVAL, "apply: unsupported operator kind");
     }

@@ -772,14 +772,30 @@ __device__ __forceinline__ void orth_reduce(const double* __restrict__ partials,
     double s = 0.0;
     if (d < nd) {
       const double* p = partials + (int64_t)(d0 + d) * kPartialPitch;
+      // eight loads in flight per lane (the wide cross-product reductions are latency chains)
       double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
       int g = sub;
-#pragma unroll 4
+      for (; g + 7 * tpd < G; g += 8 * tpd) {
+        double v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) v[u] = __ldcg(p + g + u * tpd);
+        a0 += v[0];
+        a1 += v[1];
+        a2 += v[2];
+        a3 += v[3];
+        a0 += v[4];
+        a1 += v[5];
+        a2 += v[6];
+        a3 += v[7];
+      }
       for (; g + 3 * tpd < G; g += 4 * tpd) {
-        a0 += __ldcg(p + g);
-        a1 += __ldcg(p + g + tpd);
-        a2 += __ldcg(p + g + 2 * tpd);
-        a3 += __ldcg(p + g + 3 * tpd);
+        double v[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) v[u] = __ldcg(p + g + u * tpd);
+        a0 += v[0];
+        a1 += v[1];
+        a2 += v[2];
+        a3 += v[3];
       }
       for (; g < G; g += tpd) a0 += __ldcg(p + g);
       s = (a0 + a1) + (a2 + a3);
@@ -2084,7 +2100,8 @@ struct Engine {
     if (spow) *spow = 0;
     if (!c.orth || c.world() != 1 || g.grouped() || s < 2 || op.d.kind == kIlu0) return 0;
     const int G = mk_ctas();
-    const int64_t gd = c.spow ? powers_ghost_doubles(op.d, s, op.n) : -1;
+    // (the geometry does not depend on the SKC_SPOW switch, only the powers' algorithm does)
+    const int64_t gd = powers_ghost_doubles(op.d, s, op.n);
     auto ghosts_fit = [&](int64_t P) {
       return gd >= 0 && sizeof(double) * (size_t)gd <= (size_t)orth_stages(s, m, P) * orth_stage_bytes(s);
     };
@@ -2092,13 +2109,13 @@ struct Engine {
       // whole grid rows per CTA, for the row-wise candidate powers
       const int64_t P = (op.d.ny + G - 1) / G * op.d.nx;
       if (orth_stages(s, m, P) >= 2 && ghosts_fit(P)) {
-        if (spow) *spow = 2;
+        if (spow) *spow = c.spow ? 2 : 0;
         return P;
       }
     }
     const int64_t P = ((op.n + G - 1) / G + 1) & ~(int64_t)1;
     if (orth_stages(s, m, P) < 2) return 0;
-    if (spow) *spow = ghosts_fit(P) ? 1 : 0;
+    if (spow) *spow = c.spow && ghosts_fit(P) ? 1 : 0;
     return P;
   }
 

@@ -131,7 +131,7 @@ def test_strict_anchor_block_residuals(ctx, port):
 
 # ------------------------------------------------------------------ kernels: bit-exact
 @pytest.mark.parametrize("dim,nx,conv,vark", [(2, 37, 10.0, False), (3, 11, 20.0, False), (3, 9, 20.0, True),
-                                              (2, 13, 50.0, True)])
+                                              (2, 13, 50.0, True), (3, 37, 20.0, True), (3, 64, 20.0, True)])
 def test_apply_bit_exact(ctx, port, dim, nx, conv, vark):
     from paper_2001_04886_b200 import convection_diffusion, splitmix64_uniform
     st = convection_diffusion(dim, nx, conv, variable_k=vark)
