@@ -842,14 +842,21 @@ __global__ void __launch_bounds__(ORTH_THREADS, 1) k_arn_step(const __grid_const
   // coefficients -t [s(s-1), 64] | -h [k s] | reduced products [(k+1) s^2] | the pushed block's
   // full GramSolver | compact Gram records of the k blocks | reduction scratch [16 warps][s^2]
   // | candidate slice [SC][P] | ring stages [nst][s][T]
+  // (carved with pointer arithmetic on the shared array only -- an integer round trip would make
+  // every derived pointer generic and turn the hot loops' LDS into generic loads; the candidate
+  // slice and the stages are bulk-copy destinations: 16-byte aligned = an even double offset)
   double* tc = dsm;
   double* hc = dsm + 64;
   double* prod = hc + orth_h_cap(d.k, S);
-  Gram* gs = reinterpret_cast<Gram*>(prod + orth_prod_cap(d.k, S));
-  GramC<S>* gk = reinterpret_cast<GramC<S>*>(gs + 1);
-  double* red = reinterpret_cast<double*>(gk + d.k);
-  // (the stages are bulk-copy destinations: 16-byte aligned)
-  double* sc = reinterpret_cast<double*>((reinterpret_cast<uintptr_t>(red + (NT / 32) * (S * S)) + 15) & ~(uintptr_t)15);
+  int off = 64 + orth_h_cap(d.k, S) + orth_prod_cap(d.k, S);
+  Gram* gs = reinterpret_cast<Gram*>(dsm + off);
+  off += (int)(sizeof(Gram) / sizeof(double));
+  GramC<S>* gk = reinterpret_cast<GramC<S>*>(dsm + off);
+  off += d.k * (int)(sizeof(GramC<S>) / sizeof(double));
+  double* red = dsm + off;
+  off += (NT / 32) * (S * S);
+  off = (off + 1) & ~1;
+  double* sc = dsm + off;
   double* stg = sc + (int64_t)(SC > 0 ? SC : 1) * d.P;
   __shared__ __align__(8) uint64_t s_full[kOrthMaxStages], s_empty[kOrthMaxStages], s_ctl, s_go;
   __shared__ volatile int s_quit, s_dec;

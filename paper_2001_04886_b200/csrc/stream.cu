@@ -544,7 +544,18 @@ struct TileChoice {
 
 // Tile size / stage count: >= 3 stages where possible, then large tiles, preferring a
 // footprint that lets two CTAs share an SM.  `align` = tile granularity (points).
-bool try_pick_tiles(int nu, size_t prefix, int Tmax, int Tmin, bool fine, TileChoice& out) {
+bool try_pick_tiles(int nu, size_t prefix, int Tmax, int Tmin0, bool fine, TileChoice& out, bool upd = false) {
+  // A bulk copy costs the TMA unit ~85 ns whatever its size (measured in the block-iteration
+  // kernel), so kernels that stage many vectors per tile first try for copies of >= min_copy
+  // bytes (fewer stages, one CTA per SM) before falling back to the small-tile choices.
+  // Measured (A/B on one box): 2 KB copies for nu >= 16 -- C4 6.77 -> 6.97 s-steps/s (block-MGS
+  // update 5.5 -> 5.8 TB/s, cross products 4.5 -> 4.7); 4 KB for nu >= 24 helps only the s = 8
+  // block update of s-Omin (C5 2.55 -> 2.87 TB/s) and costs the wide Gram products.
+  static const int env_copy = std::getenv("SKC_TILE_MINCOPY") ? std::atoi(std::getenv("SKC_TILE_MINCOPY")) : -1;
+  const int min_copy = env_copy >= 0 ? env_copy : (upd && nu >= 24 ? 4096 : nu >= 16 ? 2048 : 0);
+  for (int pass = 0; pass < 2; ++pass) {
+  const int Tmin = pass == 0 ? std::max(Tmin0, min_copy / 8) : Tmin0;
+  if (pass == 0 && (min_copy == 0 || Tmin > Tmax)) continue;
   for (size_t limit : {(size_t)110 * 1024, (size_t)220 * 1024}) {
     for (int ns : {3, 4, 2}) {
       for (int T2 = 2 * Tmax; T2 >= 2 * Tmin; T2 /= 2) {
@@ -559,12 +570,13 @@ bool try_pick_tiles(int nu, size_t prefix, int Tmax, int Tmin, bool fine, TileCh
       }
     }
   }
+  }
   return false;
 }
 
-TileChoice pick_tiles(int nu, size_t prefix, int Tmax, int Tmin, bool fine = true) {
+TileChoice pick_tiles(int nu, size_t prefix, int Tmax, int Tmin, bool fine = true, bool upd = false) {
   TileChoice tc;
-  if (!try_pick_tiles(nu, prefix, Tmax, Tmin, fine, tc))
+  if (!try_pick_tiles(nu, prefix, Tmax, Tmin, fine, tc, upd))
     fail(SKC_EINVAL, "streaming kernel: too many operand vectors for shared-memory staging");
   return tc;
 }
@@ -740,7 +752,7 @@ void launch_lincomb(Ctx& c, const LinDesc& L, const char* name) {
   // fewer stages for wide updates (the seed and x updates stream up to 4 + m s vectors).
   TileChoice tc;
   const int Tmax = nout_t <= 8 ? 2 * CONS : CONS;
-  if (!try_pick_tiles(nu, prefix, Tmax, CONS, false, tc)) tc = pick_tiles(nu, prefix, Tmax, 64, false);
+  if (!try_pick_tiles(nu, prefix, Tmax, CONS, false, tc, true)) tc = pick_tiles(nu, prefix, Tmax, 64, false, true);
   fill_hdr(d.h, nu, tc, L.n, L.range, L.G, L.cpg, L.gsize, L.halt, L.cond);
   const double bytes = 8.0 * (double)L.n * (nu + L.nout);
   Launch lh(c, name, bytes);

@@ -410,13 +410,17 @@ def _sgmres_fixed(nx, ny, s, m, env, monkeypatch, iters):
     return rep, x
 
 
+@pytest.mark.parametrize("grid", [(256, 640), (251, 300), (1024, 320)])
 @pytest.mark.parametrize("s", [2, 3, 4])
-def test_megakernel_streamed_powers_bit_identical(monkeypatch, s):
-    """The row-streamed candidate powers of the block-iteration kernel (slices of >= 4 grid rows:
-    here 256 x 640) give bit-identical candidates to the per-level sweeps, hence bit-identical
+def test_megakernel_streamed_powers_bit_identical(monkeypatch, s, grid):
+    """The on-chip candidate powers of the block-iteration kernel (level by level on the slice
+    extended by ghost rows, every level in shared memory: row-aligned slices with column pairs
+    per thread -- 256 x 640, 1024 x 320 with s >= 3 -- or index ranges -- odd nx, s = 2) give
+    bit-identical candidates to the per-level sweeps with grid barriers, hence bit-identical
     histories and iterates over two restart cycles."""
-    a, xa = _sgmres_fixed(256, 640, s, 6, {"SKC_SPOW": "1"}, monkeypatch, 2 * 6 * s)
-    b, xb = _sgmres_fixed(256, 640, s, 6, {"SKC_SPOW": "0"}, monkeypatch, 2 * 6 * s)
+    nx, ny = grid
+    a, xa = _sgmres_fixed(nx, ny, s, 6, {"SKC_SPOW": "1"}, monkeypatch, 2 * 6 * s)
+    b, xb = _sgmres_fixed(nx, ny, s, 6, {"SKC_SPOW": "0"}, monkeypatch, 2 * 6 * s)
     assert a.residual_history == b.residual_history and a.block_rho == b.block_rho
     assert np.array_equal(xa.view(np.uint64), xb.view(np.uint64))
     assert a.iterations == 2 * 6 * s

@@ -3,6 +3,8 @@
   python tools/ncu_summary.py launches <launches.csv> <out.md>
       per-kernel launch count, device time, share of the captured time, DRAM bytes
       (ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --csv).
+  python tools/ncu_summary.py traffic <launches.csv[.gz]> <traffic.json> <config/kernel> <name regex>
+      mean DRAM traffic per launch of the matching kernels over the launch list -> traffic.json.
   python tools/ncu_summary.py full <report.ncu-rep> <out.md> [traffic.json class]
       key --set full metrics per captured launch; optionally records the mean DRAM traffic per
       launch under `class` ("config/kernel") in traffic.json (read by bench.py for roofline.traffic).
@@ -100,8 +102,27 @@ def full(path, out, traffic_json=None, klass=None):
         json.dump(d, open(traffic_json, "w"), indent=1, sort_keys=True)
 
 
+def traffic_from_launches(path, traffic_json, klass, pattern):
+    """Mean DRAM read+write per launch of the kernels matching `pattern` over a launch list
+    (hundreds of launches: every block step of the cycles, unlike the few --set full captures)."""
+    op = __import__("gzip").open if path.endswith(".gz") else open
+    rows = [l for l in op(path, "rt") if l.startswith('"')]
+    per = defaultdict(dict)
+    for r in csv.DictReader(io.StringIO("".join(rows))):
+        if re.search(pattern, r["Kernel Name"]):
+            per[r["ID"]][r["Metric Name"]] = float(r["Metric Value"].replace(",", ""))
+    vals = [m.get("dram__bytes_read.sum", 0.0) + m.get("dram__bytes_write.sum", 0.0) for m in per.values()]
+    d = json.load(open(traffic_json)) if os.path.exists(traffic_json) else {}
+    cfg, kern = klass.split("/", 1)
+    d.setdefault(cfg, {})[kern] = sum(vals) / max(1, len(vals))
+    json.dump(d, open(traffic_json, "w"), indent=1, sort_keys=True)
+    print(f"{klass}: {len(vals)} launches, mean DRAM traffic {d[cfg][kern] / 1e6:.1f} MB")
+
+
 if __name__ == "__main__":
     if sys.argv[1] == "launches":
         launches(sys.argv[2], sys.argv[3])
+    elif sys.argv[1] == "traffic":
+        traffic_from_launches(*sys.argv[2:6])
     else:
         full(sys.argv[2], sys.argv[3], *(sys.argv[4:6] if len(sys.argv) > 5 else (None, None)))

@@ -14,7 +14,9 @@ run() {  # cfg, launch-skip, launch-count, full-kernel-regex, full-skip, full-co
   python tools/ncu_summary.py launches gpurun_out/prof/launches_$cfg.csv gpurun_out/prof/${R}_launches_$cfg.md > /dev/null
   ncu --set full --import-source on --clock-control none -k regex:$4 -s $5 -c $6 -o /tmp/full_$cfg \
       python bench.py --config $cfg --no-secondary --steps 1 --warmup 1 > gpurun_out/prof/ncu_full_$cfg.log 2>&1
-  python tools/ncu_summary.py full /tmp/full_$cfg.ncu-rep gpurun_out/prof/${R}_ncu_full_$cfg.md gpurun_out/prof/ncu_traffic.json $cfg/$7 > /dev/null
+  python tools/ncu_summary.py full /tmp/full_$cfg.ncu-rep gpurun_out/prof/${R}_ncu_full_$cfg.md > /dev/null
+  # traffic per launch from the launch list (every launch of the captured cycles)
+  python tools/ncu_summary.py traffic gpurun_out/prof/launches_$cfg.csv gpurun_out/prof/ncu_traffic.json $cfg/$7 $4
   # (the raw report stays on the box: the merged gpurun_out/ is capped at 64 MiB)
   ls -la /tmp/full_$cfg.ncu-rep gpurun_out/prof/launches_$cfg.csv
   gzip -f gpurun_out/prof/launches_$cfg.csv
