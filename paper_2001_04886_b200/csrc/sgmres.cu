@@ -935,25 +935,30 @@ __global__ void __launch_bounds__(ORTH_THREADS, 1) k_arn_step(const __grid_const
       while (!mbar_try_wait(&s_go, 0u))  // the powers phase owns the ring until then
         if (s_quit) return;
       for (int pass = 0; pass < 2; ++pass) {
-        int t0 = 0;
-        if (pass == 1) {
-          const int nspec = ntiles < NST ? ntiles : NST;
-          const double* b = colp(0, 0);
-          for (; t0 < nspec; ++t0)
-            if (!issue(b, t0)) return;
-          int dec;
-          while ((dec = s_dec) == 0)
-            if (s_quit) return;
-          if (dec == 1) return;
-        }
-        if (!sweep(0, t0)) return;
+        // (the second pass has no round-0 product sweep: its V_0^T cand are the cross products)
+        if (pass == 0 && !sweep(0, 0)) return;
+        int spec = pass == 1 ? NST : -1;  // second pass: copies issued before its decision is known
         for (int i = 0; i < K; ++i) {
           const double* bi = colp(i, 0);
           const double* bn = colp(i + 1 < K ? i + 1 : i, 0);
           for (int t = 0; t < ntiles; ++t) {
-            if (!issue(bi, t)) return;
-            if (i + 1 < K && !issue(bn, t)) return;
+            for (int h = 0; h < (i + 1 < K ? 2 : 1); ++h) {
+              if (spec == 0) {
+                int dec;
+                while ((dec = s_dec) == 0)
+                  if (s_quit) return;
+                if (dec == 1) return;
+              }
+              if (spec >= 0) --spec;
+              if (!issue(h ? bn : bi, t)) return;
+            }
           }
+        }
+        if (spec >= 0) {  // (fewer jobs than stages: still stop on a negative decision)
+          int dec;
+          while ((dec = s_dec) == 0)
+            if (s_quit) return;
+          if (dec == 1) return;
         }
         if (pass == 0)
           for (int i = K - 1; i >= 0; --i)
@@ -1018,13 +1023,14 @@ __global__ void __launch_bounds__(ORTH_THREADS, 1) k_arn_step(const __grid_const
   };
 
   // Scalar2 for block i from partials src: every CTA solves W_i t = V_i^T cand[:,1:]
+  // (src < 0: the products are block 0 of the reduced cross products already in prod, [l][jc])
   auto scalar = [&](int i, int src, int accumulate) {
-    orth_reduce(d.partials, (int)G, src, S * NC, prod);  // ends with csync
+    if (src >= 0) orth_reduce(d.partials, (int)G, src, S * NC, prod);  // ends with csync
     if (tid < NC) {
       const int jcl = tid;
       double rhs[kMaxS], t[kMaxS];
 #pragma unroll
-      for (int l = 0; l < S; ++l) rhs[l] = prod[l * NC + jcl];
+      for (int l = 0; l < S; ++l) rhs[l] = src >= 0 ? prod[l * NC + jcl] : prod[l * S + jcl + 1];
       bsolve(i, rhs, t);
 #pragma unroll
       for (int l = 0; l < S; ++l) {
@@ -1727,11 +1733,11 @@ __global__ void __launch_bounds__(ORTH_THREADS, 1) k_arn_step(const __grid_const
   }
   orth_mark(d, 3);
   if (s_first >= 0) {
-    // ---- pass 1: V_0^T cand[:,1:], k rounds with t accumulated, then W of the new candidate
-    r0_products();
-    orth_gsync(&d.st->gbar, G);
+    // ---- pass 1: k rounds with t accumulated, then W of the new candidate.  Its round-0 products
+    //      V_0^T cand[:,1:] are block 0 of the cross products just reduced (same candidate, same
+    //      per-thread accumulation): no sweep and no barrier for them.
     for (int i = 0; i < K; ++i) {
-      round(i, ((i + 1) & 1) ? d.dr1 : d.dr0, i + 1 == K, [&] { scalar(i, (i & 1) ? d.dr1 : d.dr0, 1); });
+      round(i, ((i + 1) & 1) ? d.dr1 : d.dr0, i + 1 == K, [&] { scalar(i, i == 0 ? -1 : (i & 1) ? d.dr1 : d.dr0, 1); });
       if (i + 1 < K) orth_gsync(&d.st->gbar, G);
     }
     cross_block(K, d.dwb);

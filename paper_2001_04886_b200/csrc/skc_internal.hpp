@@ -208,6 +208,7 @@ struct Ctx {
   bool orth = true;  // on-chip block orthogonalization when it fits (SKC_ORTH=0 disables)
   bool persist = true;  // persistent s-Omin for small problems (SKC_PERSIST=0 disables)
   bool spow = true;     // megakernel: row-streamed candidate powers (SKC_SPOW=0 disables)
+  bool bupd = true;     // compile-time-shaped s-Omin half-block update at s > 4 (SKC_BUPD=0: k_upd)
   // GPU-count-independent reductions (grouped geometry): bitwise the same results on 1, 2, 4
   // or 8 GPUs; on by default across ranks, opt-in on one GPU (SKC_PINDEP=1 /
   // skc_ctx_set_gpu_independent), where it turns the single-GPU-only kernels off

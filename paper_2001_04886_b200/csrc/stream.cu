@@ -303,6 +303,117 @@ __global__ void __launch_bounds__(THREADS) k_upd(const __grid_constant__ UpdDesc
   if (MAXD > 0) cta_store_partials(acc, d.nd, sv, d.partials, d.dot0, d.G);
 }
 
+// ------------------------------------------------------------------ k_bupd
+// The s-Omin direction-block update at s > 4 (sstep.hpp:215-222), one half (P or AP) per
+// launch: S outputs y_q = base_q + sum_j c[j][q] x_j, every term dense, the coefficients one
+// contiguous [nin][S] array, plus (DOTS) the upper triangle of the outputs' Gram matrix and
+// their products with one extra vector (W and m).  k_upd walks a descriptor per term and spills
+// its 64 product accumulators (C5: 2.9 TB/s); here the shape is compile time: the term loop is
+// unrolled a block of S at a time with immediate stage offsets, the coefficients come as
+// 16-byte broadcast loads and the products accumulate in registers straight from the outputs.
+// Per-element order (multiply and add rounded separately, terms ascending) is k_upd's.
+struct BupdDesc {
+  PipeHdr h;
+  int nin, cb0;
+  const double* U[UPD_MAXU];  // [0,S) bases | [S, S+nin) terms | (DOTS) the extra vector
+  double* out[kMaxS];
+  const double* coef;
+  double* partials;
+  int dot0, G;
+};
+
+constexpr int BUPD_T = 2 * CONS;  // points per tile: two per consumer thread
+
+template <int S, bool DOTS>
+__global__ void __launch_bounds__(THREADS) k_bupd(const __grid_constant__ BupdDesc d) {
+  SKC_PDL_ENTRY();
+  if (skip_launch(d.h.halt, d.h.cond)) return;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  constexpr int T = BUPD_T;
+  constexpr int ND = DOTS ? S * (S + 1) / 2 + S : 1;
+  const int coef_slots = (d.nin * S + 15) & ~15;
+  const size_t prefix = 8 * ((size_t)coef_slots + (DOTS ? (size_t)NCW * ND : 0));
+  Pipe p = pipe_setup(d.h, smem_raw, prefix);
+  double* scoef = reinterpret_cast<double*>(smem_raw + 64);
+  double* red = scoef + coef_slots;
+  for (int t = threadIdx.x; t < d.nin * S; t += blockDim.x) scoef[t] = d.coef[d.cb0 + t];
+  __syncthreads();
+  const int warp = threadIdx.x >> 5;
+  double acc[ND];
+#pragma unroll
+  for (int k = 0; k < ND; ++k) acc[k] = 0.0;
+
+  if (warp == NCW) {
+    pipe_produce(d.h, d.U, p);
+  } else {
+    for (int t = 0; t < p.ntiles; ++t) {
+      TileGeom g;
+      const double* St = pipe_acquire(d.h, p, t, g);
+      const int p0 = threadIdx.x;
+      if (p0 < g.cnt) {
+        const bool ok1 = p0 + CONS < g.cnt;  // (the second point of a short tile: computed on stale data, not used)
+        const double* sp = St + p0;
+        double o0[S], o1[S];
+#pragma unroll
+        for (int q = 0; q < S; ++q) {
+          o0[q] = sp[q * T];
+          o1[q] = sp[q * T + CONS];
+        }
+        for (int j0 = 0; j0 < d.nin; j0 += S) {
+          const double* x = sp + (size_t)(S + j0) * T;
+          const double* cj = scoef + j0 * S;
+#pragma unroll
+          for (int l = 0; l < S; ++l) {
+            const double v0 = x[l * T], v1 = x[l * T + CONS];
+            double c[S];
+            if constexpr (S % 2 == 0) {
+#pragma unroll
+              for (int q = 0; q < S; q += 2) {
+                const double2 cc = *reinterpret_cast<const double2*>(cj + l * S + q);
+                c[q] = cc.x;
+                c[q + 1] = cc.y;
+              }
+            } else {
+#pragma unroll
+              for (int q = 0; q < S; ++q) c[q] = cj[l * S + q];
+            }
+#pragma unroll
+            for (int q = 0; q < S; ++q) {
+              o0[q] = dadd(o0[q], dmul(c[q], v0));
+              o1[q] = dadd(o1[q], dmul(c[q], v1));
+            }
+          }
+        }
+        const int64_t at = g.start + p0;
+#pragma unroll
+        for (int q = 0; q < S; ++q) {
+          d.out[q][at] = o0[q];
+          if (ok1) d.out[q][at + CONS] = o1[q];
+        }
+        if (DOTS) {
+          const double* xr = sp + (size_t)(S + d.nin) * T;
+          const double r0 = xr[0];
+          double r1 = xr[CONS];
+          if (!ok1) {
+            r1 = 0.0;
+#pragma unroll
+            for (int q = 0; q < S; ++q) o1[q] = 0.0;
+          }
+          int k = 0;
+#pragma unroll
+          for (int a = 0; a < S; ++a)
+#pragma unroll
+            for (int b = a; b < S; ++b, ++k) acc[k] = fma(o1[a], o1[b], fma(o0[a], o0[b], acc[k]));
+#pragma unroll
+          for (int a = 0; a < S; ++a, ++k) acc[k] = fma(o1[a], r1, fma(o0[a], r0, acc[k]));
+        }
+      }
+      pipe_release(d.h, p, t);
+    }
+  }
+  if (DOTS) cta_store_partials(acc, ND, red, d.partials, d.dot0, d.G);
+}
+
 // ------------------------------------------------------------------ k_mgs
 // The round's scalar step (see launch_mgs): every CTA reduces the incoming products in the
 // same fixed order and solves the same s x s system, so all CTAs apply identical t.  Whole
@@ -673,12 +784,80 @@ void fill_hdr(PipeHdr& h, int nu, const TileChoice& tc, int64_t n, int64_t range
   h.cond = cond;
 }
 
+template <int S>
+void launch_bupd_t(Ctx& c, const BupdDesc& d, size_t smem, int G, bool dots) {
+  if (dots) {
+    allow_smem(k_bupd<S, true>);
+    launch_k(c, k_bupd<S, true>, G, THREADS, smem, d);
+  } else {
+    allow_smem(k_bupd<S, false>);
+    launch_k(c, k_bupd<S, false>, G, THREADS, smem, d);
+  }
+}
+
+// The s-Omin half-block update shape (see k_bupd): S = 5..8 unscaled outputs, whole blocks of S
+// dense terms with one contiguous coefficient array, no products or exactly the upper-triangle
+// Gram of the outputs followed by their products with one extra vector.  Anything else (and
+// SKC_BUPD=0) takes k_upd.
+bool try_launch_bupd(Ctx& c, const LinDesc& L, const char* name) {
+  const int S = L.nout;
+  if (!c.bupd || S < 5 || S > kMaxS || L.nin < S || L.nin % S != 0) return false;
+  const bool dots = L.nd > 0;
+  if (dots ? (L.nx != 1 || L.nd != S * (S + 1) / 2 + S) : L.nx != 0) return false;
+  for (int q = 0; q < S; ++q)
+    if (L.bscale[q] >= 0) return false;
+  const unsigned all = (1u << S) - 1u;
+  for (int j = 0; j < L.nin; ++j)
+    if (L.mask[j] != all || L.cbase[j] != L.cbase[0] + j * S) return false;
+  if (L.cbase[0] < 0 || L.cbase[0] + L.nin * S > L.ncoef) return false;
+  if (dots) {
+    int k = 0;
+    for (int a = 0; a < S; ++a)
+      for (int b = a; b < S; ++b, ++k)
+        if (L.da[k] != a || L.db[k] != b) return false;
+    for (int a = 0; a < S; ++a, ++k)
+      if (L.da[k] != a || L.db[k] != S) return false;
+  }
+  BupdDesc d;
+  std::memset(&d, 0, sizeof d);
+  int nu = 0;
+  for (int q = 0; q < S; ++q) add_unique(d.U, nu, UPD_MAXU, L.base[q]);
+  for (int j = 0; j < L.nin; ++j) add_unique(d.U, nu, UPD_MAXU, L.in[j]);
+  if (dots) add_unique(d.U, nu, UPD_MAXU, L.xin[0]);
+  if (nu != S + L.nin + (dots ? 1 : 0)) return false;  // repeated operands: the stage slots are positional
+  for (int q = 0; q < S; ++q) d.out[q] = L.out[q];
+  d.nin = L.nin;
+  d.cb0 = L.cbase[0];
+  d.coef = L.coef;
+  d.partials = L.partials;
+  d.dot0 = L.dot0;
+  d.G = L.G;
+  const size_t prefix = 8 * ((size_t)((L.nin * S + 15) & ~15) + (dots ? (size_t)NCW * (S * (S + 1) / 2 + S) : 0));
+  const size_t stage = (size_t)nu * BUPD_T * 8;
+  const size_t room = (size_t)224 * 1024 - 64 - prefix;
+  const int ns = (int)std::min<size_t>(kMaxStage, room / stage);
+  if (ns < 2) return false;
+  const TileChoice tc{BUPD_T, ns, 64 + prefix + (size_t)ns * stage};
+  fill_hdr(d.h, nu, tc, L.n, L.range, L.G, L.cpg, L.gsize, L.halt, L.cond);
+  const double bytes = 8.0 * (double)L.n * (nu + S);
+  Launch lh(c, name, bytes);
+  switch (S) {
+    case 5: launch_bupd_t<5>(c, d, tc.smem, L.G, dots); break;
+    case 6: launch_bupd_t<6>(c, d, tc.smem, L.G, dots); break;
+    case 7: launch_bupd_t<7>(c, d, tc.smem, L.G, dots); break;
+    default: launch_bupd_t<8>(c, d, tc.smem, L.G, dots); break;
+  }
+  CK(cudaGetLastError());
+  return true;
+}
+
 }  // namespace
 
 void launch_lincomb(Ctx& c, const LinDesc& L, const char* name) {
   require(L.nin <= LC_MAXIN && L.nout <= LC_MAXOUT && L.nx <= LC_MAXX && L.nd <= LC_MAXD,
           "lincomb: descriptor too large");
   require(L.nout >= 1, "lincomb: no outputs");
+  if (try_launch_bupd(c, L, name)) return;
   static const int kOut[] = {1, 2, 3, 4, 7, 8, 16};
   int nout_t = 16;
   for (int v : kOut)

@@ -426,6 +426,30 @@ def test_megakernel_streamed_powers_bit_identical(monkeypatch, s, grid):
     assert a.iterations == 2 * 6 * s
 
 
+@pytest.mark.parametrize("dims", [(40, 33, 29), (96, 64, 50)])
+@pytest.mark.parametrize("s", [5, 6, 7, 8])
+def test_somin_half_block_update_bit_identical(monkeypatch, s, dims):
+    """The compile-time-shaped s-Omin half-block update (k_bupd: P and AP halves at s > 4, W and m
+    accumulated in registers) applies every term in k_upd's order, so the direction blocks are
+    bit-identical to the generic kernel's; only the products' per-thread summation differs in
+    nothing either (same thread-to-point map), hence identical histories and iterates.  Odd
+    sizes exercise the short last tile."""
+    from paper_2001_04886_b200 import Context, SStepConfig, convection_diffusion, somin_solve, splitmix64_uniform
+    nx, ny, nz = dims
+    st = convection_diffusion(3, nx, 20.0, ny=ny, nz=nz)
+    f = splitmix64_uniform(20010486, st.n)
+    out = {}
+    for flag in ("1", "0"):
+        monkeypatch.setenv("SKC_BUPD", flag)
+        ctx = Context(0)
+        x = np.zeros(st.n)
+        rep = somin_solve(ctx.stencil(st), f, x, SStepConfig(s=s, k=2, tol=0.0, max_iterations=6, fixed_steps=True))
+        out[flag] = (rep.residual_history, x)
+    assert out["1"][0] == out["0"][0]
+    assert np.array_equal(out["1"][1].view(np.uint64), out["0"][1].view(np.uint64))
+    assert len(out["1"][0]) == 7
+
+
 @pytest.mark.parametrize("dims", [(37, 29, 23), (64, 48, 40)])
 @pytest.mark.parametrize("s", [2, 3, 4, 5, 8])
 def test_3d_matrix_powers_bit_exact(monkeypatch, dims, s):
