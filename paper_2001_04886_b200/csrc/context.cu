@@ -323,6 +323,12 @@ void build_stencil_op(Ctx& c, Op& op, const skc_stencil_desc& d, const double* k
                     sizeof(double) * (size_t)op.rowlen);
     const double* base = (const double*)dev_upload(op, kp.data(), sizeof(double) * kp.size());
     o.kcell = base + pad * op.rowlen;
+    if (d.dim == 3 && c.world() == 1 && c.faces) {
+      // every harmonic-mean face once, at setup: the apply then streams them (no divisions)
+      double* fc = (double*)dev_upload(op, nullptr, sizeof(double) * 3 * (size_t)o.n);
+      launch_faces3(c, o, fc);
+      o.faces = fc;
+    }
   } else {
     o.kind = kStencilConst;
   }

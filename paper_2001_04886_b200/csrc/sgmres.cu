@@ -2487,6 +2487,7 @@ struct Engine {
     double* tk = rk + rl.t();
     bool wb_needed = true;  // the reorthogonalized W region must be made global for the push
     if (s > 1) {
+      int Gcross = g.enc();
       for (int pass = 0; pass < 2; ++pass) {
         // Across ranks the second pass is enqueued under the device flag like on one GPU: its
         // kernels skip when the test did not fire, its collectives run (on stale, unused values)
@@ -2503,7 +2504,8 @@ struct Engine {
         std::vector<const double*> Cr;
         for (int jc = 1; jc < s; ++jc) Cr.push_back(col(cb, jc));
         const bool have = pass == 0 && Gfused > 0;  // products already fused into the powers sweep
-        if (!have) {
+        // (the second pass' round-0 products V_0^T cand[:,1:] are block 0 of the cross products)
+        if (!have && pass == 0) {
           std::vector<const double*> L;
           for (int l = 0; l < s; ++l) L.push_back(col(0, l));
           launch_gram_list(c, g, L, Cr, partials, dl.D(), halt, cond, pass ? "gram_mgs_reorth" : "gram_mgs");
@@ -2512,8 +2514,14 @@ struct Engine {
           const int Gi = (i == 0 && have) ? Gfused : g.enc();
           // Scalar2 against block i (sstep.hpp:338-353) runs in the update kernel's prologue:
           // t = W_i^{-1} V_i^T cand[:,1:], recorded at block i of this iteration's T area
-          const MgsScalar sc{partials, c.reduce_point(partials, Gi, dl.Dr(i), s * (s - 1)), dl.Dr(i), grams + i,
-                             tk + i * s * s, pass};
+          const bool from_cross = pass == 1 && i == 0;
+          const MgsScalar sc{partials,
+                             from_cross ? Gcross : c.reduce_point(partials, Gi, dl.Dr(i), s * (s - 1)),
+                             from_cross ? dl.Cross() : dl.Dr(i),
+                             grams + i,
+                             tk + i * s * s,
+                             pass,
+                             from_cross ? 1 : 0};
           // cand[:,jc] -= sum_l t(l,jc-1) V_i[:,l]  (+ products with V_{i+1})
           const double* Vi[kMaxS];
           const double* Vn[kMaxS];
@@ -2548,7 +2556,8 @@ struct Engine {
             zfused = true;
           }
           launch_gram_map(c, g, L, R, cols, partials, halt, nullptr, "gram_cross");
-          launch_k(c, k_arn_check, 1, 256, 0, st, grams, k, rk, partials, c.reduce_point(partials, g.enc(), dl.Cross(), k * s * s + s * s), dl.Cross(), dl.Cross() + k * s * s, s, 1e-8, scratch);
+          Gcross = c.reduce_point(partials, g.enc(), dl.Cross(), k * s * s + s * s);
+          launch_k(c, k_arn_check, 1, 256, 0, st, grams, k, rk, partials, Gcross, dl.Cross(), dl.Cross() + k * s * s, s, 1e-8, scratch);
           ++c.launches;
         } else {
           gram_self_into(cb, dl.Wb(), cond, "gram_w_reorth");

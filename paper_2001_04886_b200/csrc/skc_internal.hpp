@@ -43,6 +43,7 @@ struct DevOp {
   double coef[7];  // -z,-y,-x,C,+x,+y,+z
   double ch2;
   const double* kcell;   // kStencilVarK
+  const double* faces;   // kStencilVarK, 3D on one GPU: the +x | +y | +z face coefficients of every cell (3 n)
   const double* dia;     // kStencilDia: 7 slabs of n values (slot-major), 0 where absent
   const int64_t* rowptr; // kCsr
   const int32_t* colidx;
@@ -209,6 +210,8 @@ struct Ctx {
   bool persist = true;  // persistent s-Omin for small problems (SKC_PERSIST=0 disables)
   bool spow = true;     // megakernel: row-streamed candidate powers (SKC_SPOW=0 disables)
   bool bupd = true;     // compile-time-shaped s-Omin half-block update at s > 4 (SKC_BUPD=0: k_upd)
+  bool faces = true;    // 3D variable-k apply from face coefficients computed once (SKC_FACES=0: per apply)
+  bool apply_ring = true;  // 3D applies through a shared-memory plane ring (SKC_APPLY_RING=0: z-marching registers)
   // GPU-count-independent reductions (grouped geometry): bitwise the same results on 1, 2, 4
   // or 8 GPUs; on by default across ranks, opt-in on one GPU (SKC_PINDEP=1 /
   // skc_ctx_set_gpu_independent), where it turns the single-GPU-only kernels off
@@ -323,12 +326,14 @@ struct MgsScalar {
   const Gram* gram;
   double* rec_t;
   int accumulate;
+  int full;  // the products are a full s x s block [l][jc] (block 0 of the cross products), not [l][jc-1]
 };
 void launch_mgs(Ctx& c, const Geo& geo, int s, const double* const* Vi, double* const* cand, const double* const* Vnext,
                 const MgsScalar& sc, double* partials, int dot0, const int* halt, const int* cond,
                 const char* name = "mgs_update");
 // operator helpers
 void build_stencil_op(Ctx& c, Op& op, const skc_stencil_desc& d, const double* kcell_host);
+void launch_faces3(Ctx& c, const DevOp& op, double* faces);
 void build_csr_op(Ctx& c, Op& op, int64_t n, const uint64_t* offs, const uint64_t* cols, const double* vals);
 void validate_csr(int64_t n, const uint64_t* offs, const uint64_t* cols);  // sparse.hpp:41-63
 // ILU(0) right preconditioning (ilu.cu): op = A (LU)^{-1}; z = (LU)^{-1} r

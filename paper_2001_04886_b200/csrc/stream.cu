@@ -430,12 +430,12 @@ __device__ __forceinline__ void mgs_scalar(const MgsScalar& sc, double* cs, doub
     uint64_t* dst = reinterpret_cast<uint64_t*>(gs);
     for (int w = threadIdx.x; w < (int)(sizeof(Gram) / 8); w += blockDim.x) dst[w] = src[w];
   }
-  reduce_dots_dev(sc.src, sc.src_G, sc.src_d0, S * NC, tmp);  // ends with __syncthreads
+  reduce_dots_dev(sc.src, sc.src_G, sc.src_d0, sc.full ? S * S : S * NC, tmp);  // ends with __syncthreads
   if (threadIdx.x < NC) {
     const int jc = threadIdx.x;
     double rhs[kMaxS], t[kMaxS];
 #pragma unroll
-    for (int l = 0; l < S; ++l) rhs[l] = tmp[l * NC + jc];
+    for (int l = 0; l < S; ++l) rhs[l] = sc.full ? tmp[l * S + jc + 1] : tmp[l * NC + jc];
     gram_solve_dev(*gs, rhs, t);
 #pragma unroll
     for (int l = 0; l < S; ++l) {

@@ -144,6 +144,32 @@ def test_apply_bit_exact(ctx, port, dim, nx, conv, vark):
         assert np.array_equal(op.apply(xv), want)
 
 
+@pytest.mark.parametrize("dims", [(37, 21, 19), (70, 9, 33), (5, 3, 2), (64, 16, 70), (33, 8, 5)])
+@pytest.mark.parametrize("vark", [False, True])
+def test_apply_3d_kernel_variants_bit_exact(port, monkeypatch, dims, vark):
+    """The 3D applies stream through a shared-memory plane ring (k_apply3r / k_apply3r_face: cp.async
+    copies D planes ahead; the default on one GPU), the variable-k one from face coefficients
+    computed once at operator creation.  SKC_APPLY_RING=0 takes the z-marching register kernels,
+    SKC_FACES=0 computes the faces in every apply.  Every variant is bit-identical to the
+    reference spmv, on grids that are not multiples of the tile, thinner than one tile, shorter
+    than the prefetch depth and longer than one z chunk."""
+    from paper_2001_04886_b200 import Context, splitmix64_uniform
+    from paper_2001_04886_b200.problems import Stencil
+    nx, ny, nz = dims
+    ch2 = 20.0 / (nx + 1.0) / 2.0
+    lo, hi = -1.0 - ch2, -1.0 + ch2
+    st = Stencil(3, nx, ny, nz, (lo, lo, lo, 6.0, hi, hi, hi), ch2, vark)
+    k = port.lognormal(7, st.n) if vark else None
+    a = port.stencil_csr(3, nx, ny, nz, st.coef, kcell=k, ch2=ch2)
+    xv = splitmix64_uniform(13, st.n)
+    want = port.spmv(a, xv)
+    for faces, ring in (("1", "1"), ("1", "0"), ("0", "1")) if vark else (("1", "1"), ("1", "0")):
+        monkeypatch.setenv("SKC_FACES", faces)
+        monkeypatch.setenv("SKC_APPLY_RING", ring)
+        op = Context(0).stencil(st, kcell=k)
+        assert np.array_equal(op.apply(xv), want), (faces, ring)
+
+
 def test_apply_general_csr_bit_exact(ctx, port):
     from paper_2001_04886_b200 import splitmix64_uniform
     meta, arr = case("sgmres_s2_m4_dense40")
