@@ -27,7 +27,7 @@ for c in $CFGS; do
     C2) run C2 3000 2600 k_arn_step 100 3 arn_step ;;
     C3s4) run C3s4 1200 1200 k_upd 40 2 block_update ;;
     C4) run C4 900 900 k_mgs 30 2 mgs_update ;;
-    C5) run C5 1200 1200 k_upd 40 2 block_update ;;
+    C5) run C5 1200 1200 k_bupd 40 4 block_update ;;
   esac
 done
 ls -la gpurun_out/prof
