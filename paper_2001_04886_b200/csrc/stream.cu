@@ -414,6 +414,113 @@ __global__ void __launch_bounds__(THREADS) k_bupd(const __grid_constant__ BupdDe
   if (DOTS) cta_store_partials(acc, ND, red, d.partials, d.dot0, d.G);
 }
 
+// The fused form for s <= 4 (one launch for both halves, which share the powers block): outputs
+// [P_0..P_{S-1}, AP_0..AP_{S-1}], term blocks [P_e columns, AP_e columns] per window block e, both
+// halves with the same coefficients c[e][l][q]; products = the upper triangle of AP^T AP and AP^T x.
+struct Bupd2Desc {
+  PipeHdr h;
+  int nin, cb0, nb0, ix;      // terms, coefficient offset, distinct base vectors, stage slot of the extra vector
+  const double* U[UPD_MAXU];  // [0,nb0) bases | [nb0, nb0+nin) terms | (the extra vector, unless it is a base)
+  uint8_t ub[2 * 4];          // base of output q -> stage slot
+  double* out[2 * 4];
+  const double* coef;
+  double* partials;
+  int dot0, G;
+};
+
+template <int S>
+__global__ void __launch_bounds__(THREADS) k_bupd2(const __grid_constant__ Bupd2Desc d) {
+  SKC_PDL_ENTRY();
+  if (skip_launch(d.h.halt, d.h.cond)) return;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  constexpr int T = BUPD_T, NO = 2 * S;
+  constexpr int ND = S * (S + 1) / 2 + S;
+  const int ncf = (d.nin / 2) * S;
+  const int coef_slots = (ncf + 15) & ~15;
+  const size_t prefix = 8 * ((size_t)coef_slots + (size_t)NCW * ND);
+  Pipe p = pipe_setup(d.h, smem_raw, prefix);
+  double* scoef = reinterpret_cast<double*>(smem_raw + 64);
+  double* red = scoef + coef_slots;
+  for (int t = threadIdx.x; t < ncf; t += blockDim.x) scoef[t] = d.coef[d.cb0 + t];
+  __syncthreads();
+  const int warp = threadIdx.x >> 5;
+  double acc[ND];
+#pragma unroll
+  for (int k = 0; k < ND; ++k) acc[k] = 0.0;
+
+  if (warp == NCW) {
+    pipe_produce(d.h, d.U, p);
+  } else {
+    for (int t = 0; t < p.ntiles; ++t) {
+      TileGeom g;
+      const double* St = pipe_acquire(d.h, p, t, g);
+      const int p0 = threadIdx.x;
+      if (p0 < g.cnt) {
+        const bool ok1 = p0 + CONS < g.cnt;
+        const double* sp = St + p0;
+        double o0[NO], o1[NO];
+#pragma unroll
+        for (int q = 0; q < NO; ++q) {
+          const double* b = sp + (int)d.ub[q] * T;
+          o0[q] = b[0];
+          o1[q] = b[CONS];
+        }
+        for (int j0 = 0; j0 < d.nin; j0 += NO) {
+          const double* x = sp + (size_t)(d.nb0 + j0) * T;
+          const double* cj = scoef + (j0 / 2) * S;
+#pragma unroll
+          for (int l = 0; l < S; ++l) {
+            const double vp0 = x[l * T], vp1 = x[l * T + CONS];
+            const double va0 = x[(S + l) * T], va1 = x[(S + l) * T + CONS];
+            double c[S];
+            if constexpr (S % 2 == 0) {
+#pragma unroll
+              for (int q = 0; q < S; q += 2) {
+                const double2 cc = *reinterpret_cast<const double2*>(cj + l * S + q);
+                c[q] = cc.x;
+                c[q + 1] = cc.y;
+              }
+            } else {
+#pragma unroll
+              for (int q = 0; q < S; ++q) c[q] = cj[l * S + q];
+            }
+#pragma unroll
+            for (int q = 0; q < S; ++q) {
+              o0[q] = dadd(o0[q], dmul(c[q], vp0));
+              o1[q] = dadd(o1[q], dmul(c[q], vp1));
+              o0[S + q] = dadd(o0[S + q], dmul(c[q], va0));
+              o1[S + q] = dadd(o1[S + q], dmul(c[q], va1));
+            }
+          }
+        }
+        const int64_t at = g.start + p0;
+#pragma unroll
+        for (int q = 0; q < NO; ++q) {
+          d.out[q][at] = o0[q];
+          if (ok1) d.out[q][at + CONS] = o1[q];
+        }
+        const double* xr = sp + (size_t)d.ix * T;
+        const double r0 = xr[0];
+        double r1 = xr[CONS];
+        if (!ok1) {
+          r1 = 0.0;
+#pragma unroll
+          for (int q = 0; q < S; ++q) o1[S + q] = 0.0;
+        }
+        int k = 0;
+#pragma unroll
+        for (int a = 0; a < S; ++a)
+#pragma unroll
+          for (int b = a; b < S; ++b, ++k) acc[k] = fma(o1[S + a], o1[S + b], fma(o0[S + a], o0[S + b], acc[k]));
+#pragma unroll
+        for (int a = 0; a < S; ++a, ++k) acc[k] = fma(o1[S + a], r1, fma(o0[S + a], r0, acc[k]));
+      }
+      pipe_release(d.h, p, t);
+    }
+  }
+  cta_store_partials(acc, ND, red, d.partials, d.dot0, d.G);
+}
+
 // ------------------------------------------------------------------ k_mgs
 // The round's scalar step (see launch_mgs): every CTA reduces the incoming products in the
 // same fixed order and solves the same s x s system, so all CTAs apply identical t.  Whole
@@ -851,13 +958,79 @@ bool try_launch_bupd(Ctx& c, const LinDesc& L, const char* name) {
   return true;
 }
 
+template <int S>
+void launch_bupd2_t(Ctx& c, const Bupd2Desc& d, size_t smem, int G) {
+  allow_smem(k_bupd2<S>);
+  launch_k(c, k_bupd2<S>, G, THREADS, smem, d);
+}
+
+// The fused s-Omin block update shape at s = 2..4 (see k_bupd2).
+bool try_launch_bupd2(Ctx& c, const LinDesc& L, const char* name) {
+  if (!c.bupd || L.nout % 2 != 0) return false;
+  const int S = L.nout / 2;
+  if (S < 2 || S > 4 || L.nin < 2 * S || L.nin % (2 * S) != 0) return false;
+  if (L.nx != 1 || L.nd != S * (S + 1) / 2 + S) return false;
+  for (int q = 0; q < 2 * S; ++q)
+    if (L.bscale[q] >= 0) return false;
+  const unsigned lo = (1u << S) - 1u, hi = lo << S;
+  const int cb0 = L.cbase[0];
+  for (int j = 0; j < L.nin; ++j) {
+    const int e = j / (2 * S), r = j % (2 * S);
+    const bool ap = r >= S;
+    const int l = ap ? r - S : r;
+    if (L.mask[j] != (ap ? hi : lo) || L.cbase[j] != cb0 + (e * S + l) * S - (ap ? S : 0)) return false;
+  }
+  if (cb0 < 0 || cb0 + (L.nin / 2) * S > L.ncoef) return false;
+  {
+    int k = 0;
+    for (int a = 0; a < S; ++a)
+      for (int b = a; b < S; ++b, ++k)
+        if (L.da[k] != S + a || L.db[k] != S + b) return false;
+    for (int a = 0; a < S; ++a, ++k)
+      if (L.da[k] != S + a || L.db[k] != 2 * S) return false;
+  }
+  Bupd2Desc d;
+  std::memset(&d, 0, sizeof d);
+  int nu = 0;
+  for (int q = 0; q < 2 * S; ++q) {
+    d.ub[q] = (uint8_t)add_unique(d.U, nu, UPD_MAXU, L.base[q]);
+    d.out[q] = L.out[q];
+  }
+  d.nb0 = nu;
+  for (int j = 0; j < L.nin; ++j) add_unique(d.U, nu, UPD_MAXU, L.in[j]);
+  if (nu != d.nb0 + L.nin) return false;  // repeated operands: the term slots are positional
+  d.ix = add_unique(d.U, nu, UPD_MAXU, L.xin[0]);
+  d.nin = L.nin;
+  d.cb0 = cb0;
+  d.coef = L.coef;
+  d.partials = L.partials;
+  d.dot0 = L.dot0;
+  d.G = L.G;
+  const size_t prefix = 8 * ((size_t)(((L.nin / 2) * S + 15) & ~15) + (size_t)NCW * (S * (S + 1) / 2 + S));
+  const size_t stage = (size_t)nu * BUPD_T * 8;
+  const size_t room = (size_t)224 * 1024 - 64 - prefix;
+  const int ns = (int)std::min<size_t>(kMaxStage, room / stage);
+  if (ns < 2) return false;
+  const TileChoice tc{BUPD_T, ns, 64 + prefix + (size_t)ns * stage};
+  fill_hdr(d.h, nu, tc, L.n, L.range, L.G, L.cpg, L.gsize, L.halt, L.cond);
+  const double bytes = 8.0 * (double)L.n * (nu + 2 * S);
+  Launch lh(c, name, bytes);
+  switch (S) {
+    case 2: launch_bupd2_t<2>(c, d, tc.smem, L.G); break;
+    case 3: launch_bupd2_t<3>(c, d, tc.smem, L.G); break;
+    default: launch_bupd2_t<4>(c, d, tc.smem, L.G); break;
+  }
+  CK(cudaGetLastError());
+  return true;
+}
+
 }  // namespace
 
 void launch_lincomb(Ctx& c, const LinDesc& L, const char* name) {
   require(L.nin <= LC_MAXIN && L.nout <= LC_MAXOUT && L.nx <= LC_MAXX && L.nd <= LC_MAXD,
           "lincomb: descriptor too large");
   require(L.nout >= 1, "lincomb: no outputs");
-  if (try_launch_bupd(c, L, name)) return;
+  if (try_launch_bupd(c, L, name) || try_launch_bupd2(c, L, name)) return;
   static const int kOut[] = {1, 2, 3, 4, 7, 8, 16};
   int nout_t = 16;
   for (int v : kOut)

@@ -453,13 +453,14 @@ def test_megakernel_streamed_powers_bit_identical(monkeypatch, s, grid):
 
 
 @pytest.mark.parametrize("dims", [(40, 33, 29), (96, 64, 50)])
-@pytest.mark.parametrize("s", [5, 6, 7, 8])
+@pytest.mark.parametrize("s", [2, 3, 4, 5, 6, 7, 8])
 def test_somin_half_block_update_bit_identical(monkeypatch, s, dims):
-    """The compile-time-shaped s-Omin half-block update (k_bupd: P and AP halves at s > 4, W and m
-    accumulated in registers) applies every term in k_upd's order, so the direction blocks are
-    bit-identical to the generic kernel's; only the products' per-thread summation differs in
-    nothing either (same thread-to-point map), hence identical histories and iterates.  Odd
-    sizes exercise the short last tile."""
+    """The compile-time-shaped s-Omin block updates (k_bupd: P and AP halves at s > 4; k_bupd2: both
+    halves in one launch at s <= 4; W and m accumulated in registers) apply every term in k_upd's
+    order, so the direction blocks are bit-identical to the generic kernel's, and the products
+    are summed per thread over the same points in the same order, hence identical histories
+    and iterates.  Odd sizes exercise the short last tile."""
+    monkeypatch.setenv("SKC_PERSIST", "0")
     from paper_2001_04886_b200 import Context, SStepConfig, convection_diffusion, somin_solve, splitmix64_uniform
     nx, ny, nz = dims
     st = convection_diffusion(3, nx, 20.0, ny=ny, nz=nz)
