@@ -509,6 +509,28 @@ void run2d(Ctx& c, const MpkDesc& d) {
   launch_k(c, k_mpk2w<KIND, J, DOTS>, d.G, MW_WARPS * 32, smem, d);
 }
 
+// resident CTAs per SM of the strip kernel, at most 4 (the geometry the fused products' partial
+// layout was sized for); cached per device (the attribute call precedes the query)
+template <int KIND, int J>
+int mpk2w_resident(Ctx& c, bool dots) {
+  static int cache[2][64] = {};
+  int& slot = cache[dots ? 1 : 0][c.device & 63];
+  if (slot) return slot;
+  int per_sm = 0;
+  if constexpr (J <= 3) {
+    if (dots) {
+      ensure_smem(k_mpk2w<KIND, J, true>, mpk2w_smem<J, true>());
+      CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_mpk2w<KIND, J, true>, MW_WARPS * 32,
+                                                       mpk2w_smem<J, true>()));
+      return slot = std::min(4, std::max(1, per_sm));
+    }
+  }
+  ensure_smem(k_mpk2w<KIND, J, false>, mpk2w_smem<J, false>());
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_mpk2w<KIND, J, false>, MW_WARPS * 32,
+                                                   mpk2w_smem<J, false>()));
+  return slot = std::min(4, std::max(1, per_sm));
+}
+
 template <int KIND, int J>
 void launch2d(Ctx& c, MpkDesc& d) {
   const int64_t nx = d.op.nx, ny = d.op.ny;
@@ -526,10 +548,19 @@ void launch2d(Ctx& c, MpkDesc& d) {
   }
   d.W = 64 - 2 * J;
   d.tiles_x = (int)((nx + d.W - 1) / d.W);
-  // rows per warp strip: ~16 strips per SM, at least 3J rows to bound the ghost-row overhead
-  const int64_t target = 16LL * c.sm_count;
-  int64_t R = std::max<int64_t>(3 * J, (ny * d.tiles_x + target - 1) / target);
-  R = std::min<int64_t>(R, ny);
+  // rows per warp strip: the strips fill whole waves of resident CTAs (a grid a little over one
+  // wave runs two: C4's 656 CTAs on 592 slots streamed at 3.5 TB/s), at least 3J rows per strip
+  // to bound the ghost-row overhead
+  bool dots = false;
+  if constexpr (J <= 3) dots = d.nx_dots != 0;
+  const int64_t slots = (int64_t)mpk2w_resident<KIND, J>(c, dots) * c.sm_count * MW_WARPS;  // strips per wave
+  const int64_t ty_max = std::max<int64_t>(1, ny / (3 * J));
+  int64_t ty = std::max<int64_t>(1, slots / d.tiles_x);
+  if (ty > ty_max) {  // many short strips: whole waves as far as the 3J rows allow
+    const int64_t waves = (d.tiles_x * ty_max + slots - 1) / slots;
+    ty = std::max<int64_t>(1, std::min(ty_max, waves * slots / d.tiles_x));
+  }
+  const int64_t R = std::min<int64_t>(ny, (ny + ty - 1) / ty);
   d.R = (int)R;
   d.tiles_y = (int)((ny + R - 1) / R);
   d.G = (d.tiles_x * d.tiles_y + MW_WARPS - 1) / MW_WARPS;
