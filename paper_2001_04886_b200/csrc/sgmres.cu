@@ -676,6 +676,14 @@ constexpr int ORTH_THREADS = ORTH_NT + 32;   // + the producer warp
 constexpr int ORTH_U = SKC_ORTH_U;           // points per consumer thread per tile
 constexpr int ORTH_T = ORTH_U * ORTH_NT;     // points per tile (point p stays with thread p mod 512)
 constexpr int kOrthMaxStages = 8;
+// cross products beyond this many are reduced once in the grid and published (one more grid
+// barrier) instead of in every CTA.  Measured on C2 (one box, SKC_ORTH_OWNER_DOTS = off / 96 /
+// 64 / 32 / 0): 4097 / 4144 / 4147 / 4157 / 4163 s-steps/s; the reorthogonalization test at
+// k = 9 (160 products) 14.8 -> 4.0 us.
+#ifndef SKC_ORTH_OWNER_DOTS
+#define SKC_ORTH_OWNER_DOTS 32
+#endif
+constexpr int kOrthOwnerDots = SKC_ORTH_OWNER_DOTS;
 constexpr size_t kOrthSmemCap = 226 * 1024;  // <= the 227 KB per-block limit less the static part
 // candidate columns kept in shared memory (the rest in their basis slots, read back through a
 // register prefetch): what is left of the 227 KB holds the ring's stages
@@ -722,6 +730,8 @@ struct OrthDesc {
   // level-by-level candidate powers on the slice extended by ghost rows (2D constant stencil,
   // the ghost rows fit the ring's stages); spow 0 = per-level sweeps with grid barriers
   int spow;
+  double* reduced;  // published reductions of the wide cross products ((k+1) s^2 doubles)
+  int owner_dots;   // cross products beyond this many are reduced once in the grid and published
 };
 
 // per-CTA completion time of a phase (diagnostics): slot base + CTA index
@@ -1707,7 +1717,30 @@ __global__ void __launch_bounds__(ORTH_THREADS, 1) k_arn_step(const __grid_const
   orth_mark_all(d, 768);
   orth_gsync(&d.st->gbar, G);
   orth_mark(d, 2);
-  orth_reduce(d.partials, (int)G, d.dcross, (K + 1) * S * S, prod);
+  if ((K + 1) * S * S > d.owner_dots) {
+    // Wide cross products: reducing them in every CTA reads (k+1) s^2 x G partials G times over
+    // (27.6 MB through L2 at k = 9 on C2, 13 us).  Instead warp w of the grid reduces product w
+    // (lane partial sums over g = lane, lane + 32, .., then the shuffle tree: a fixed order),
+    // publishes it, and after one more grid barrier every CTA loads the reduced values.
+    const int nd = (K + 1) * S * S;
+    const int warp = tid >> 5;
+    for (int dd = (int)blockIdx.x * (NT / 32) + warp; dd < nd; dd += (int)G * (NT / 32)) {
+      const double* p = d.partials + (int64_t)(d.dcross + dd) * kPartialPitch;
+      double v[5];
+#pragma unroll
+      for (int u = 0; u < 5; ++u) v[u] = lane + 32 * u < (int)G ? __ldcg(p + lane + 32 * u) : 0.0;
+      double a = ((v[0] + v[1]) + (v[2] + v[3])) + v[4];
+      for (int g = lane + 160; g < (int)G; g += 32) a += __ldcg(p + g);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) a += __shfl_down_sync(0xffffffffu, a, o);
+      if (lane == 0) d.reduced[dd] = a;
+    }
+    orth_gsync(&d.st->gbar, G);
+    for (int e = tid; e < nd; e += NT) prod[e] = __ldcg(d.reduced + e);
+    csync();
+  } else {
+    orth_reduce(d.partials, (int)G, d.dcross, (K + 1) * S * S, prod);
+  }
   {
     const double* sW = prod + K * S * S;
     double cn2 = 0.0;
@@ -2175,6 +2208,9 @@ struct Engine {
     d.rec_h = rl.h();
     d.st = st;
     d.orth_tol = 1e-8;
+    d.reduced = scratch;  // (the per-phase kernels that use it do not run beside this one)
+    static const int owner_dots = std::getenv("SKC_ORTH_OWNER_DOTS") ? std::atoi(std::getenv("SKC_ORTH_OWNER_DOTS")) : kOrthOwnerDots;
+    d.owner_dots = owner_dots;
     static const bool trace = std::getenv("SKC_TRACE_ORTH") != nullptr;
     if (trace) d.trace = (unsigned long long*)c.workspace("orth_trace", 1024 * sizeof(unsigned long long));
     const int G = mk_ctas();
