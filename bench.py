@@ -258,11 +258,14 @@ def measure(name, steps, warmup, cpu=True):
     # ---- e2e through the C ABI with pinned host buffers (H2D f, x0; D2H x) in the timed region
     x_host = torch.zeros(n, dtype=torch.float64, pin_memory=True).numpy()
     f_pin = torch.from_numpy(f_host).pin_memory().numpy()
+    e_steps = max(1, steps if c["nx"] ** c["dim"] <= 2 ** 24 else 1)
+    if warmup > 0:  # one untimed call: the host path's staging buffers exist before the clock starts
+        x_host[:] = 0.0
+        host_fn(op, f_pin, x_host, cfg)
     torch.cuda.synchronize()
     _barrier(ws)
     t0 = time.perf_counter()
     e_iters = 0
-    e_steps = max(1, steps if c["nx"] ** c["dim"] <= 2 ** 24 else 1)
     for _ in range(e_steps):
         x_host[:] = 0.0
         r2 = host_fn(op, f_pin, x_host, cfg)
