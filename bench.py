@@ -295,6 +295,12 @@ def measure(name, steps, warmup, cpu=True):
                     "alg_bytes_per_launch": s_["bytes"] / max(1, s_["launches"]),
                     "bytes_model": ("SURVEY 8(d): 4ks+4s+5 vectors per block step k < m, 2ms+s+6 at k = m"
                                     if kname == "arn_step" else "the kernel's distinct operand vectors read + written")}
+        if ach > peak:
+            # the measured peak is a 1:1 read+write copy; a read-dominated stream (this kernel reads
+            # several vectors per vector written) moves more than that, and operands a launch re-reads
+            # can come from the 126 MB L2 (compare "traffic", the DRAM bytes under ncu)
+            roofline["note"] = ("above the copy-measured peak: read-dominated stream (HBM reads run faster than a "
+                                "1:1 copy) and/or operands served from L2; see traffic")
         tr = os.path.join(ROOT, "profiles", "ncu_traffic.json")
         if os.path.exists(tr):
             try:
