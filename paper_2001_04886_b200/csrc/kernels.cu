@@ -5,6 +5,8 @@
 //                   spmv (sparse.hpp:135-146): acc = 0, then + v*x per present neighbour
 //                   in ascending column order, multiply and add rounded separately.
 // The streaming update / inner-product kernels live in stream.cu.
+#include <cuda.h>
+
 #include <cstdio>
 #include <cstdlib>
 
@@ -406,6 +408,127 @@ __global__ void __launch_bounds__(256) k_apply3r2(const __grid_constant__ DevOp 
 template <int D, int TY>
 static void launch_apply3r2(Ctx& c, const DevOp& op, const double* x, double* y, const int* halt, const int* cond);
 
+// The same ring fed by the TMA engine: x is described to the hardware as a 3D tensor
+// (nx, ny, nz) and one thread asks for a whole plane tile with its halo -- the box
+// [i0 - 2, i0 + TX + 2) x [j0 - 1, j0 + TY + 1) of plane q -- with one
+// cp.async.bulk.tensor.3d (SASS UTMALDG); coordinates outside the grid are zero-filled by the
+// unit, and each slot's mbarrier counts the box's bytes in.  The other 255 threads issue no
+// copies, compute no halo addresses and wait on no copy groups: the ring can run NS - 1 planes
+// ahead for one instruction per plane.  (Two columns of left halo instead of one keep the
+// pairs 16-byte aligned in the slot; a slot is padded to a multiple of 128 bytes.)
+constexpr int AT_TXP = 64, AT_TX = 2 * AT_TXP, AT_W = AT_TX + 4;
+// R = rows per thread (rows ty, ty + 4, ...): a tile is 4 R rows, a slot (4 R + 2) x AT_W doubles
+// padded to a multiple of 128 bytes
+template <int R>
+struct AtGeo {
+  static constexpr int TY = 4 * R, H = TY + 2, BOX = AT_W * H * 8, SLOT = ((BOX + 127) / 128) * 16;
+};
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* tm, int c0, int c1, int c2, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::
+          "r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(tm)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
+      : "memory");
+}
+template <int NS, int R>
+__global__ void __launch_bounds__(256) k_apply3t(const __grid_constant__ CUtensorMap tm,
+                                                 const __grid_constant__ DevOp op, const double* __restrict__ x,
+                                                 double* __restrict__ y, int kz, const int* halt, const int* cond) {
+  SKC_PDL_ENTRY();
+  if (skip_launch(halt, cond)) return;
+  using G = AtGeo<R>;
+  extern __shared__ __align__(128) double ringt[];  // [NS][SLOT], then NS mbarriers
+  uint64_t* full = reinterpret_cast<uint64_t*>(ringt + NS * G::SLOT);
+  const int nx = (int)op.nx, ny = (int)op.ny, nz = (int)op.nz;
+  const int tx = threadIdx.x % AT_TXP, ty = threadIdx.x / AT_TXP;
+  const int i0 = blockIdx.x * AT_TX, j0 = blockIdx.y * G::TY;
+  const int i = i0 + 2 * tx;
+  const int l0 = blockIdx.z * kz, l1 = min(nz, l0 + kz);
+  const int64_t plane = (int64_t)nx * ny;
+  const double c0 = op.coef[0], c1 = op.coef[1], c2 = op.coef[2], c3 = op.coef[3], c4 = op.coef[4],
+               c5 = op.coef[5], c6 = op.coef[6];
+  const bool hW = i > 0, hE = i + 2 < nx;
+  const int oc = (ty + 1) * AT_W + 2 + 2 * tx;  // the pair's offset inside a slot (row ty)
+  const int qend = min(l1, nz - 1);             // last plane this CTA reads
+  const bool lead = threadIdx.x == 0;
+  if (lead) {
+#pragma unroll
+    for (int st = 0; st < NS; ++st) mbar_init(&full[st], 1);
+    mbar_fence_init();
+  }
+  __syncthreads();
+  auto issue = [&](int p) {  // plane l0 + p into slot p % NS (the leader)
+    if (l0 + p <= qend) {
+      const int st = p % NS;
+      mbar_arrive_expect_tx(&full[st], G::BOX);
+      tma_load_3d(ringt + st * G::SLOT, &tm, i0 - 2, j0 - 1, l0 + p, &full[st]);
+    }
+  };
+  if (lead) {
+#pragma unroll
+    for (int p = 0; p < NS - 1; ++p) issue(p);
+  }
+  bool in[R];
+  double2 xm[R];
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    const int j = j0 + ty + 4 * r;
+    in[r] = i < nx && j < ny;
+    xm[r] = make_double2(0.0, 0.0);
+    if (in[r] && l0 > 0) xm[r] = *reinterpret_cast<const double2*>(x + (int64_t)j * nx + i + (int64_t)(l0 - 1) * plane);
+  }
+  double* yp = y + (int64_t)(j0 + ty) * nx + i + (int64_t)l0 * plane;
+  mbar_wait(&full[0], 0);
+  int sc = 0, s1 = 1 % NS;
+  uint32_t par1 = 0;  // parity of the phase plane p + 1 completes in its slot
+  for (int l = l0; l < l1; ++l) {
+    __syncthreads();  // everyone is done with plane p - 1: its slot takes plane p + NS - 1
+    if (lead) issue(l - l0 + NS - 1);
+    const bool hZ = l + 1 < nz;
+    if (hZ) mbar_wait(&full[s1], par1);
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      if (in[r]) {
+        const int j = j0 + ty + 4 * r;
+        const double* sl = ringt + sc * G::SLOT + oc + 4 * r * AT_W;
+        const double2 C = *reinterpret_cast<const double2*>(sl);
+        double a0 = 0.0, a1 = 0.0;
+        if (l > 0) {
+          a0 = __dadd_rn(a0, __dmul_rn(c0, xm[r].x));
+          a1 = __dadd_rn(a1, __dmul_rn(c0, xm[r].y));
+        }
+        if (j > 0) {
+          const double2 S = *reinterpret_cast<const double2*>(sl - AT_W);
+          a0 = __dadd_rn(a0, __dmul_rn(c1, S.x));
+          a1 = __dadd_rn(a1, __dmul_rn(c1, S.y));
+        }
+        if (hW) a0 = __dadd_rn(a0, __dmul_rn(c2, sl[-1]));
+        a1 = __dadd_rn(a1, __dmul_rn(c2, C.x));
+        a0 = __dadd_rn(a0, __dmul_rn(c3, C.x));
+        a1 = __dadd_rn(a1, __dmul_rn(c3, C.y));
+        a0 = __dadd_rn(a0, __dmul_rn(c4, C.y));
+        if (hE) a1 = __dadd_rn(a1, __dmul_rn(c4, sl[2]));
+        if (j + 1 < ny) {
+          const double2 N = *reinterpret_cast<const double2*>(sl + AT_W);
+          a0 = __dadd_rn(a0, __dmul_rn(c5, N.x));
+          a1 = __dadd_rn(a1, __dmul_rn(c5, N.y));
+        }
+        if (hZ) {
+          const double2 Z = *reinterpret_cast<const double2*>(ringt + s1 * G::SLOT + oc + 4 * r * AT_W);
+          a0 = __dadd_rn(a0, __dmul_rn(c6, Z.x));
+          a1 = __dadd_rn(a1, __dmul_rn(c6, Z.y));
+        }
+        *reinterpret_cast<double2*>(yp + (int64_t)(4 * r) * nx) = make_double2(a0, a1);
+        xm[r] = C;
+      }
+    }
+    yp += plane;
+    sc = s1;
+    s1 = s1 + 1 == NS ? 0 : s1 + 1;
+    if (s1 == 0) par1 ^= 1u;
+  }
+}
+
 // stored-face variable-k form of the same ring: a slot holds the x tile with its halo, the +x
 // faces with the column to the left, the +y faces with the row below, and the +z faces
 constexpr int AF2_FX = AR_W * AR_H;                 // offsets inside a slot (doubles)
@@ -696,6 +819,46 @@ static void launch_apply3r2(Ctx& c, const DevOp& op, const double* x, double* y,
   launch_k(c, k_apply3r2<D, TY>, gr, 256, smem, op, x, y, kz, halt, cond);
 }
 
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no libcuda link)
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+static EncodeTiledFn encode_tiled_fn() {
+  static EncodeTiledFn fn = [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      p = nullptr;
+    return reinterpret_cast<EncodeTiledFn>(p);
+  }();
+  return fn;
+}
+
+template <int NS, int R>
+static bool launch_apply3t(Ctx& c, const DevOp& op, const double* x, double* y, const int* halt, const int* cond) {
+  static_assert(NS >= 3, "planes p, p + 1 are read while plane p + NS - 1 lands");
+  using G = AtGeo<R>;
+  EncodeTiledFn enc = encode_tiled_fn();
+  if (!enc) return false;
+  CUtensorMap tm;
+  const cuuint64_t dims[3] = {(cuuint64_t)op.nx, (cuuint64_t)op.ny, (cuuint64_t)op.nz};
+  const cuuint64_t strides[2] = {(cuuint64_t)op.nx * 8, (cuuint64_t)op.nx * op.ny * 8};
+  const cuuint32_t box[3] = {AT_W, G::H, 1};
+  const cuuint32_t estr[3] = {1, 1, 1};
+  if (enc(&tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double*>(x), dims, strides, box, estr,
+          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+    return false;
+  const size_t smem = sizeof(double) * (size_t)NS * G::SLOT + sizeof(uint64_t) * NS;
+  ensure_smem(k_apply3t<NS, R>, smem);
+  const int64_t tx = (op.nx + AT_TX - 1) / AT_TX, ty = (op.ny + G::TY - 1) / G::TY;
+  const int kz = ring_kz(op, tx * ty, ring_slots(c, k_apply3t<NS, R>, smem));
+  const dim3 gr((unsigned)tx, (unsigned)ty, (unsigned)((op.nz + kz - 1) / kz));
+  launch_k(c, k_apply3t<NS, R>, gr, 256, smem, tm, op, x, y, kz, halt, cond);
+  return true;
+}
+
 void launch_apply(Ctx& c, const DevOp& op, const double* x, double* y, const int* halt, const int* cond) {
   if (op.kind == kIlu0) {  // y = A (LU)^{-1} x (right_preconditioned, ilu0.hpp:138-146)
     double* tmp = (double*)c.workspace("ilu_apply_tmp", sizeof(double) * (size_t)op.n);
@@ -722,6 +885,19 @@ void launch_apply(Ctx& c, const DevOp& op, const double* x, double* y, const int
       case 22: launch_k(c, k_apply<2, kStencilVarK>, grid, 256, 0, op, x, y, halt, cond); break;
       case 23: launch_k(c, k_apply<2, kStencilDia>, grid, 256, 0, op, x, y, halt, cond); break;
       case 31: {
+        if (c.apply_tma && c.apply_ring && op.nx % 2 == 0 && (((uintptr_t)x | (uintptr_t)y) & 15) == 0) {
+          // SKC_APPLY_TMA = 10 * rows-per-thread + ring slots (a bare slot count means one row)
+          const int ns = c.apply_tma % 10, rr = c.apply_tma / 10;
+          const bool ok = rr == 2   ? (ns == 4 ? launch_apply3t<4, 2>(c, op, x, y, halt, cond)
+                                               : launch_apply3t<3, 2>(c, op, x, y, halt, cond))
+                          : rr == 4 ? (ns == 4 ? launch_apply3t<4, 4>(c, op, x, y, halt, cond)
+                                               : launch_apply3t<3, 4>(c, op, x, y, halt, cond))
+                          : ns == 4 ? launch_apply3t<4, 1>(c, op, x, y, halt, cond)
+                          : ns == 6 ? launch_apply3t<6, 1>(c, op, x, y, halt, cond)
+                          : ns == 8 ? launch_apply3t<8, 1>(c, op, x, y, halt, cond)
+                                    : launch_apply3t<3, 1>(c, op, x, y, halt, cond);
+          if (ok) break;
+        }
         if (c.apply_ring && op.nx % 2 == 0 && (((uintptr_t)x | (uintptr_t)y) & 15) == 0) {
           static const int ty = std::getenv("SKC_APPLY_TY") ? std::atoi(std::getenv("SKC_APPLY_TY")) : 4;
           static const int dd = std::getenv("SKC_APPLY_D") ? std::atoi(std::getenv("SKC_APPLY_D")) : 1;

@@ -144,6 +144,32 @@ def test_apply_bit_exact(ctx, port, dim, nx, conv, vark):
         assert np.array_equal(op.apply(xv), want)
 
 
+@pytest.mark.parametrize("dims", [(70, 9, 33), (64, 16, 70), (300, 10, 20), (2, 1, 1), (128, 4, 1), (130, 5, 2),
+                                  (256, 64, 150)])
+@pytest.mark.parametrize("slots", ["0", "3", "6", "8", "23", "24", "43"])
+def test_apply_3d_tma_tensor_bit_exact(port, monkeypatch, dims, slots):
+    """The constant-stencil 3D apply fed by the TMA engine (k_apply3t: one cp.async.bulk.tensor.3d
+    per plane tile with its halo, out-of-grid coordinates zero-filled by the unit; SKC_APPLY_TMA =
+    ring slots, 0 = the cp.async ring) is bit-identical to the reference spmv (sparse.hpp:135-146) on
+    grids thinner / shorter than a tile or the ring, not multiples of the tile, several tiles
+    wide and longer than one z chunk."""
+    from paper_2001_04886_b200 import Context, splitmix64_uniform
+    from paper_2001_04886_b200.problems import Stencil
+    nx, ny, nz = dims
+    ch2 = 20.0 / (nx + 1.0) / 2.0
+    lo, hi = -1.0 - ch2, -1.0 + ch2
+    st = Stencil(3, nx, ny, nz, (lo, lo, lo, 6.0, hi, hi, hi), ch2, False)
+    a = port.stencil_csr(3, nx, ny, nz, st.coef, kcell=None, ch2=ch2)
+    xv = splitmix64_uniform(17, st.n)
+    want = port.spmv(a, xv)
+    monkeypatch.setenv("SKC_APPLY_TMA", slots)
+    op = Context(0).stencil(st)
+    got = op.apply(xv)
+    assert np.array_equal(got, want) and np.array_equal(np.signbit(got), np.signbit(want))
+    z = op.apply(-0.0 * xv)  # signed zeros come out like the reference's
+    assert np.array_equal(np.signbit(z), np.signbit(port.spmv(a, -0.0 * xv)))
+
+
 @pytest.mark.parametrize("dims", [(37, 21, 19), (70, 9, 33), (5, 3, 2), (64, 16, 70), (33, 8, 5)])
 @pytest.mark.parametrize("vark", [False, True])
 def test_apply_3d_kernel_variants_bit_exact(port, monkeypatch, dims, vark):
