@@ -431,7 +431,7 @@ __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* tm, in
       : "memory");
 }
 template <int NS, int R>
-__global__ void __launch_bounds__(256) k_apply3t(const __grid_constant__ CUtensorMap tm,
+__global__ void __launch_bounds__(256, R == 1 ? 8 : R == 2 ? 5 : 3) k_apply3t(const __grid_constant__ CUtensorMap tm,
                                                  const __grid_constant__ DevOp op, const double* __restrict__ x,
                                                  double* __restrict__ y, int kz, const int* halt, const int* cond) {
   SKC_PDL_ENTRY();
@@ -778,6 +778,159 @@ __global__ void __launch_bounds__(256) k_apply3r2_face(const __grid_constant__ D
   cp_async_wait<0>();
 }
 
+// The stored-face ring fed by the TMA engine (see k_apply3t): four boxes per plane -- the x tile
+// with its halo, the +x faces with the column to the left, the +y faces with the row below, the
+// +z faces -- land in one slot on one mbarrier.  The slot layout is fp's with every box on a
+// 128-byte boundary.
+namespace fpt {
+constexpr int TY = 8, TXP = 32, TX = 2 * TXP;
+constexpr int XW = TX + 4, XH = TY + 2, FXW = TX + 2;
+constexpr int BX = XW * XH * 8, BFX = FXW * TY * 8, BFY = TX * (TY + 1) * 8, BFZ = TX * TY * 8;  // box bytes
+constexpr int pad16(int bytes) { return ((bytes + 127) / 128) * 16; }
+constexpr int OFX = pad16(BX);
+constexpr int OFY = OFX + pad16(BFX);
+constexpr int OFZ = OFY + pad16(BFY);
+constexpr int SLOT = OFZ + pad16(BFZ);
+}  // namespace fpt
+template <int NS>
+__global__ void __launch_bounds__(256) k_apply3t_face(const __grid_constant__ CUtensorMap tmx,
+                                                      const __grid_constant__ CUtensorMap tmfx,
+                                                      const __grid_constant__ CUtensorMap tmfy,
+                                                      const __grid_constant__ CUtensorMap tmfz,
+                                                      const __grid_constant__ DevOp op, const double* __restrict__ x,
+                                                       double* __restrict__ y, int kz, const int* halt,
+                                                       const int* cond) {
+  SKC_PDL_ENTRY();
+  if (skip_launch(halt, cond)) return;
+  using namespace fpt;
+  extern __shared__ __align__(128) double fring2[];  // [NS][SLOT], then NS mbarriers
+  uint64_t* full = reinterpret_cast<uint64_t*>(fring2 + NS * SLOT);
+  const int nx = (int)op.nx, ny = (int)op.ny, nz = (int)op.nz;
+  const int tx = threadIdx.x % TXP, ty = threadIdx.x / TXP;
+  const int i = blockIdx.x * TX + 2 * tx;
+  const int j = blockIdx.y * TY + ty;
+  const bool in = i < nx && j < ny;
+  const int l0 = blockIdx.z * kz, l1 = min(nz, l0 + kz);
+  const int64_t plane = (int64_t)nx * ny;
+  const double ch2 = op.ch2;
+  const bool hW = in && i > 0, hE = in && i + 2 < nx, hS = in && j > 0, hN = in && j + 1 < ny;
+  const bool needk = in && (i == 0 || j == 0);
+  const int64_t c = in ? (int64_t)j * nx + i : 0;
+  const double* col = x + c;
+  const double* fx = op.faces + c;
+  const double* fy = fx + op.n;
+  const double* fz = fy + op.n;
+  const double* kc_ = op.kcell + c;
+  const int ox = (ty + 1) * XW + 2 + 2 * tx;
+  const int ofx = OFX + ty * FXW + 2 + 2 * tx;
+  const int ofy = OFY + (ty + 1) * TX + 2 * tx;
+  const int ofz = OFZ + ty * TX + 2 * tx;
+  const int i0 = blockIdx.x * TX, j0 = blockIdx.y * TY;
+  const int qend = min(l1, nz - 1);  // last plane this CTA reads (x only when it is l1)
+  const bool lead = threadIdx.x == 0;
+  if (lead) {
+#pragma unroll
+    for (int st = 0; st < NS; ++st) mbar_init(&full[st], 1);
+    mbar_fence_init();
+  }
+  __syncthreads();
+  auto issue = [&](int p) {  // plane l0 + p into slot p % NS (the leader)
+    const int q = l0 + p;
+    if (q <= qend) {
+      const int st = p % NS;
+      double* sl = fring2 + st * SLOT;
+      const bool faces = q < l1;
+      mbar_arrive_expect_tx(&full[st], faces ? BX + BFX + BFY + BFZ : BX);
+      tma_load_3d(sl, &tmx, i0 - 2, j0 - 1, q, &full[st]);
+      if (faces) {
+        tma_load_3d(sl + OFX, &tmfx, i0 - 2, j0, q, &full[st]);
+        tma_load_3d(sl + OFY, &tmfy, i0, j0 - 1, q, &full[st]);
+        tma_load_3d(sl + OFZ, &tmfz, i0, j0, q, &full[st]);
+      }
+    }
+  };
+  if (lead) {
+#pragma unroll
+    for (int p = 0; p < NS - 1; ++p) issue(p);
+  }
+  double2 xm = make_double2(0.0, 0.0), fzm = xm;
+  if (in) {
+    if (l0 > 0) {
+      xm = *reinterpret_cast<const double2*>(col + (int64_t)(l0 - 1) * plane);
+      fzm = *reinterpret_cast<const double2*>(fz + (int64_t)(l0 - 1) * plane);
+    } else {
+      fzm = *reinterpret_cast<const double2*>(kc_);  // own k on the domain boundary
+    }
+  }
+  mbar_wait(&full[0], 0);
+  int sc = 0, s1 = 1 % NS;
+  uint32_t par1 = 0;  // parity of the phase plane p + 1 completes in its slot
+  for (int l = l0; l < l1; ++l) {
+    __syncthreads();  // everyone is done with plane p - 1: its slot takes plane p + NS - 1
+    if (lead) issue(l - l0 + NS - 1);
+    if (l + 1 < nz) mbar_wait(&full[s1], par1);
+    if (in) {
+      const double* sl = fring2 + sc * SLOT;
+      const bool hZ = l + 1 < nz;
+      double2 kc = make_double2(0.0, 0.0);
+      if (needk) kc = *reinterpret_cast<const double2*>(kc_ + (int64_t)l * plane);
+      const double2 C = *reinterpret_cast<const double2*>(sl + ox);
+      const double2 fE = *reinterpret_cast<const double2*>(sl + ofx);
+      const double2 fN = *reinterpret_cast<const double2*>(sl + ofy);
+      const double2 fZ = *reinterpret_cast<const double2*>(sl + ofz);
+      const double fW0 = hW ? sl[ofx - 1] : kc.x;
+      const double fW1 = fE.x;  // (the pair's shared face)
+      double2 fS = kc, S = make_double2(0.0, 0.0), N = S, Z = S;
+      if (hS) {
+        fS = *reinterpret_cast<const double2*>(sl + ofy - TX);
+        S = *reinterpret_cast<const double2*>(sl + ox - XW);
+      }
+      if (hN) N = *reinterpret_cast<const double2*>(sl + ox + XW);
+      if (hZ) Z = *reinterpret_cast<const double2*>(fring2 + s1 * SLOT + ox);
+      double d0 = fzm.x, d1 = fzm.y;
+      d0 = __dadd_rn(d0, fS.x);
+      d1 = __dadd_rn(d1, fS.y);
+      d0 = __dadd_rn(d0, fW0);
+      d1 = __dadd_rn(d1, fW1);
+      d0 = __dadd_rn(d0, fE.x);
+      d1 = __dadd_rn(d1, fE.y);
+      d0 = __dadd_rn(d0, fN.x);
+      d1 = __dadd_rn(d1, fN.y);
+      d0 = __dadd_rn(d0, fZ.x);
+      d1 = __dadd_rn(d1, fZ.y);
+      double a0 = 0.0, a1 = 0.0;
+      if (l > 0) {
+        a0 = __dadd_rn(a0, __dmul_rn(__dsub_rn(-fzm.x, ch2), xm.x));
+        a1 = __dadd_rn(a1, __dmul_rn(__dsub_rn(-fzm.y, ch2), xm.y));
+      }
+      if (hS) {
+        a0 = __dadd_rn(a0, __dmul_rn(__dsub_rn(-fS.x, ch2), S.x));
+        a1 = __dadd_rn(a1, __dmul_rn(__dsub_rn(-fS.y, ch2), S.y));
+      }
+      if (hW) a0 = __dadd_rn(a0, __dmul_rn(__dsub_rn(-fW0, ch2), sl[ox - 1]));
+      a1 = __dadd_rn(a1, __dmul_rn(__dsub_rn(-fW1, ch2), C.x));
+      a0 = __dadd_rn(a0, __dmul_rn(d0, C.x));
+      a1 = __dadd_rn(a1, __dmul_rn(d1, C.y));
+      a0 = __dadd_rn(a0, __dmul_rn(__dadd_rn(-fE.x, ch2), C.y));
+      if (hE) a1 = __dadd_rn(a1, __dmul_rn(__dadd_rn(-fE.y, ch2), sl[ox + 2]));
+      if (hN) {
+        a0 = __dadd_rn(a0, __dmul_rn(__dadd_rn(-fN.x, ch2), N.x));
+        a1 = __dadd_rn(a1, __dmul_rn(__dadd_rn(-fN.y, ch2), N.y));
+      }
+      if (hZ) {
+        a0 = __dadd_rn(a0, __dmul_rn(__dadd_rn(-fZ.x, ch2), Z.x));
+        a1 = __dadd_rn(a1, __dmul_rn(__dadd_rn(-fZ.y, ch2), Z.y));
+      }
+      *reinterpret_cast<double2*>(y + (int64_t)l * plane + c) = make_double2(a0, a1);
+      xm = C;
+      fzm = fZ;
+    }
+    sc = s1;
+    s1 = s1 + 1 == NS ? 0 : s1 + 1;
+    if (s1 == 0) par1 ^= 1u;
+  }
+}
+
 // planes per CTA of the ring kernels.  A CTA walks one z chunk of one (x, y) tile; the chunks
 // are sized so that the grid is a whole number of waves of resident CTAs, as nearly as the D + 2
 // extra plane loads per chunk allow (256^3 with 16-plane chunks: 2.3 waves, i.e. a third wave at
@@ -859,6 +1012,36 @@ static bool launch_apply3t(Ctx& c, const DevOp& op, const double* x, double* y, 
   return true;
 }
 
+static bool encode_map3(CUtensorMap* tm, const double* base, const DevOp& op, int bw, int bh) {
+  EncodeTiledFn enc = encode_tiled_fn();
+  if (!enc) return false;
+  const cuuint64_t dims[3] = {(cuuint64_t)op.nx, (cuuint64_t)op.ny, (cuuint64_t)op.nz};
+  const cuuint64_t strides[2] = {(cuuint64_t)op.nx * 8, (cuuint64_t)op.nx * op.ny * 8};
+  const cuuint32_t box[3] = {(cuuint32_t)bw, (cuuint32_t)bh, 1};
+  const cuuint32_t estr[3] = {1, 1, 1};
+  return enc(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double*>(base), dims, strides, box, estr,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+template <int NS>
+static bool launch_apply3t_face(Ctx& c, const DevOp& op, const double* x, double* y, const int* halt, const int* cond) {
+  static_assert(NS >= 3, "planes p, p + 1 are read while plane p + NS - 1 lands");
+  using namespace fpt;
+  if ((((uintptr_t)op.faces) & 15) != 0 || (op.n & 1)) return false;
+  CUtensorMap tmx, tmfx, tmfy, tmfz;
+  if (!encode_map3(&tmx, x, op, XW, XH) || !encode_map3(&tmfx, op.faces, op, FXW, TY) ||
+      !encode_map3(&tmfy, op.faces + op.n, op, TX, TY + 1) || !encode_map3(&tmfz, op.faces + 2 * op.n, op, TX, TY))
+    return false;
+  const size_t smem = sizeof(double) * (size_t)NS * SLOT + sizeof(uint64_t) * NS;
+  ensure_smem(k_apply3t_face<NS>, smem);
+  const int64_t tx = (op.nx + TX - 1) / TX, ty = (op.ny + TY - 1) / TY;
+  const int kz = ring_kz(op, tx * ty, ring_slots(c, k_apply3t_face<NS>, smem));
+  const dim3 gr((unsigned)tx, (unsigned)ty, (unsigned)((op.nz + kz - 1) / kz));
+  launch_k(c, k_apply3t_face<NS>, gr, 256, smem, tmx, tmfx, tmfy, tmfz, op, x, y, kz, halt, cond);
+  return true;
+}
+
 void launch_apply(Ctx& c, const DevOp& op, const double* x, double* y, const int* halt, const int* cond) {
   if (op.kind == kIlu0) {  // y = A (LU)^{-1} x (right_preconditioned, ilu0.hpp:138-146)
     double* tmp = (double*)c.workspace("ilu_apply_tmp", sizeof(double) * (size_t)op.n);
@@ -931,6 +1114,11 @@ void launch_apply(Ctx& c, const DevOp& op, const double* x, double* y, const int
         break;
       }
       case 32: {
+        if (op.faces && c.apply_tma_face && c.apply_ring && op.nx % 2 == 0 && (((uintptr_t)x | (uintptr_t)y) & 15) == 0) {
+          const bool ok = c.apply_tma_face == 4 ? launch_apply3t_face<4>(c, op, x, y, halt, cond)
+                                                : launch_apply3t_face<3>(c, op, x, y, halt, cond);
+          if (ok) break;
+        }
         if (op.faces && c.apply_ring && op.nx % 2 == 0 && (((uintptr_t)x | (uintptr_t)y) & 15) == 0) {
           static const int dsel = std::getenv("SKC_APPLY_FD") ? std::atoi(std::getenv("SKC_APPLY_FD")) : 1;
           const int64_t tx = (op.nx + fp::TX - 1) / fp::TX, ty = (op.ny + fp::TY - 1) / fp::TY;

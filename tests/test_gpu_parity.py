@@ -170,6 +170,28 @@ def test_apply_3d_tma_tensor_bit_exact(port, monkeypatch, dims, slots):
     assert np.array_equal(np.signbit(z), np.signbit(port.spmv(a, -0.0 * xv)))
 
 
+@pytest.mark.parametrize("dims", [(70, 9, 33), (64, 16, 70), (300, 10, 20), (2, 1, 1), (64, 8, 1), (66, 9, 2),
+                                  (256, 64, 150)])
+@pytest.mark.parametrize("slots", ["3", "4"])
+def test_apply_3d_tma_stored_faces_bit_exact(port, monkeypatch, dims, slots):
+    """The variable-k 3D apply from stored faces fed by the TMA engine (k_apply3t_face: four boxes
+    per plane -- x with its halo, +x / +y / +z faces -- on one mbarrier; SKC_APPLY_TMA_FACE = ring
+    slots) is bit-identical to the reference spmv on the variable-k operator."""
+    from paper_2001_04886_b200 import Context, splitmix64_uniform
+    from paper_2001_04886_b200.problems import Stencil
+    nx, ny, nz = dims
+    ch2 = 20.0 / (nx + 1.0) / 2.0
+    lo, hi = -1.0 - ch2, -1.0 + ch2
+    st = Stencil(3, nx, ny, nz, (lo, lo, lo, 6.0, hi, hi, hi), ch2, True)
+    k = port.lognormal(7, st.n)
+    a = port.stencil_csr(3, nx, ny, nz, st.coef, kcell=k, ch2=ch2)
+    xv = splitmix64_uniform(19, st.n)
+    want = port.spmv(a, xv)
+    monkeypatch.setenv("SKC_APPLY_TMA_FACE", slots)
+    got = Context(0).stencil(st, kcell=k).apply(xv)
+    assert np.array_equal(got, want) and np.array_equal(np.signbit(got), np.signbit(want))
+
+
 @pytest.mark.parametrize("dims", [(37, 21, 19), (70, 9, 33), (5, 3, 2), (64, 16, 70), (33, 8, 5)])
 @pytest.mark.parametrize("vark", [False, True])
 def test_apply_3d_kernel_variants_bit_exact(port, monkeypatch, dims, vark):
