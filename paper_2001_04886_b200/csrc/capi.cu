@@ -101,6 +101,7 @@ skc_ctx* make_ctx(int device) {
   if (const char* e = std::getenv("SKC_BUPD")) ctx->c.bupd = std::atoi(e) != 0;
   if (const char* e = std::getenv("SKC_FACES")) ctx->c.faces = std::atoi(e) != 0;
   if (const char* e = std::getenv("SKC_APPLY_TMA")) ctx->c.apply_tma = std::atoi(e);
+  if (const char* e = std::getenv("SKC_APPLY_ALT")) ctx->c.apply_alt = std::atoi(e);
   if (const char* e = std::getenv("SKC_APPLY_TMA_FACE")) ctx->c.apply_tma_face = std::atoi(e);
   if (const char* e = std::getenv("SKC_APPLY_RING")) ctx->c.apply_ring = std::atoi(e) != 0;
   if (const char* e = std::getenv("SKC_LSQ_OVERLAP")) ctx->c.lsq_overlap = std::atoi(e) != 0;

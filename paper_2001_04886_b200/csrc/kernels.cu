@@ -430,7 +430,15 @@ __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* tm, in
       "l"(reinterpret_cast<uint64_t>(tm)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
       : "memory");
 }
-template <int NS, int R>
+__device__ __forceinline__ void tma_load_3d_hint(void* dst, const CUtensorMap* tm, int c0, int c1, int c2, uint64_t* bar,
+                                                 uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1, {%2, %3, "
+      "%4}], [%5], %6;" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(tm)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar)), "l"(pol)
+      : "memory");
+}
+template <int NS, int R, bool DN = false, bool EF = false>
 __global__ void __launch_bounds__(256, R == 1 ? 8 : R == 2 ? 5 : 3) k_apply3t(const __grid_constant__ CUtensorMap tm,
                                                  const __grid_constant__ DevOp op, const double* __restrict__ x,
                                                  double* __restrict__ y, int kz, const int* halt, const int* cond) {
@@ -449,7 +457,12 @@ __global__ void __launch_bounds__(256, R == 1 ? 8 : R == 2 ? 5 : 3) k_apply3t(co
                c5 = op.coef[5], c6 = op.coef[6];
   const bool hW = i > 0, hE = i + 2 < nx;
   const int oc = (ty + 1) * AT_W + 2 + 2 * tx;  // the pair's offset inside a slot (row ty)
-  const int qend = min(l1, nz - 1);             // last plane this CTA reads
+  // the planes are walked upwards (plane(p) = l0 + p, then plane l1 for its z neighbour) or, DN,
+  // downwards (plane(p) = l1 - 1 - p, then plane l0 - 1): chained applies alternate so that one
+  // starts on the planes its predecessor wrote last, still in L2
+  const int cnt = (l1 - l0) + ((DN ? l0 > 0 : l1 < nz) ? 1 : 0);  // planes this CTA reads
+  uint64_t pol = 0;
+  if (EF) pol = policy_evict_first();
   const bool lead = threadIdx.x == 0;
   if (lead) {
 #pragma unroll
@@ -458,10 +471,13 @@ __global__ void __launch_bounds__(256, R == 1 ? 8 : R == 2 ? 5 : 3) k_apply3t(co
   }
   __syncthreads();
   auto issue = [&](int p) {  // plane l0 + p into slot p % NS (the leader)
-    if (l0 + p <= qend) {
+    if (p < cnt) {
       const int st = p % NS;
       mbar_arrive_expect_tx(&full[st], G::BOX);
-      tma_load_3d(ringt + st * G::SLOT, &tm, i0 - 2, j0 - 1, l0 + p, &full[st]);
+      if (EF)
+        tma_load_3d_hint(ringt + st * G::SLOT, &tm, i0 - 2, j0 - 1, DN ? l1 - 1 - p : l0 + p, &full[st], pol);
+      else
+        tma_load_3d(ringt + st * G::SLOT, &tm, i0 - 2, j0 - 1, DN ? l1 - 1 - p : l0 + p, &full[st]);
     }
   };
   if (lead) {
@@ -475,17 +491,19 @@ __global__ void __launch_bounds__(256, R == 1 ? 8 : R == 2 ? 5 : 3) k_apply3t(co
     const int j = j0 + ty + 4 * r;
     in[r] = i < nx && j < ny;
     xm[r] = make_double2(0.0, 0.0);
-    if (in[r] && l0 > 0) xm[r] = *reinterpret_cast<const double2*>(x + (int64_t)j * nx + i + (int64_t)(l0 - 1) * plane);
+    if (in[r] && (DN ? l1 < nz : l0 > 0))
+      xm[r] = *reinterpret_cast<const double2*>(x + (int64_t)j * nx + i + (int64_t)(DN ? l1 : l0 - 1) * plane);
   }
-  double* yp = y + (int64_t)(j0 + ty) * nx + i + (int64_t)l0 * plane;
+  double* yp = y + (int64_t)(j0 + ty) * nx + i + (int64_t)(DN ? l1 - 1 : l0) * plane;
   mbar_wait(&full[0], 0);
   int sc = 0, s1 = 1 % NS;
   uint32_t par1 = 0;  // parity of the phase plane p + 1 completes in its slot
-  for (int l = l0; l < l1; ++l) {
+  for (int p = 0; p < l1 - l0; ++p) {
+    const int l = DN ? l1 - 1 - p : l0 + p;
     __syncthreads();  // everyone is done with plane p - 1: its slot takes plane p + NS - 1
-    if (lead) issue(l - l0 + NS - 1);
-    const bool hZ = l + 1 < nz;
-    if (hZ) mbar_wait(&full[s1], par1);
+    if (lead) issue(p + NS - 1);
+    const bool hZ = l + 1 < nz, hB = l > 0;
+    if (DN ? hB : hZ) mbar_wait(&full[s1], par1);
 #pragma unroll
     for (int r = 0; r < R; ++r) {
       if (in[r]) {
@@ -493,9 +511,10 @@ __global__ void __launch_bounds__(256, R == 1 ? 8 : R == 2 ? 5 : 3) k_apply3t(co
         const double* sl = ringt + sc * G::SLOT + oc + 4 * r * AT_W;
         const double2 C = *reinterpret_cast<const double2*>(sl);
         double a0 = 0.0, a1 = 0.0;
-        if (l > 0) {
-          a0 = __dadd_rn(a0, __dmul_rn(c0, xm[r].x));
-          a1 = __dadd_rn(a1, __dmul_rn(c0, xm[r].y));
+        if (hB) {
+          const double2 B = DN ? *reinterpret_cast<const double2*>(ringt + s1 * G::SLOT + oc + 4 * r * AT_W) : xm[r];
+          a0 = __dadd_rn(a0, __dmul_rn(c0, B.x));
+          a1 = __dadd_rn(a1, __dmul_rn(c0, B.y));
         }
         if (j > 0) {
           const double2 S = *reinterpret_cast<const double2*>(sl - AT_W);
@@ -514,7 +533,7 @@ __global__ void __launch_bounds__(256, R == 1 ? 8 : R == 2 ? 5 : 3) k_apply3t(co
           a1 = __dadd_rn(a1, __dmul_rn(c5, N.y));
         }
         if (hZ) {
-          const double2 Z = *reinterpret_cast<const double2*>(ringt + s1 * G::SLOT + oc + 4 * r * AT_W);
+          const double2 Z = DN ? xm[r] : *reinterpret_cast<const double2*>(ringt + s1 * G::SLOT + oc + 4 * r * AT_W);
           a0 = __dadd_rn(a0, __dmul_rn(c6, Z.x));
           a1 = __dadd_rn(a1, __dmul_rn(c6, Z.y));
         }
@@ -522,7 +541,7 @@ __global__ void __launch_bounds__(256, R == 1 ? 8 : R == 2 ? 5 : 3) k_apply3t(co
         xm[r] = C;
       }
     }
-    yp += plane;
+    yp += DN ? -plane : plane;
     sc = s1;
     s1 = s1 + 1 == NS ? 0 : s1 + 1;
     if (s1 == 0) par1 ^= 1u;
@@ -988,7 +1007,7 @@ static EncodeTiledFn encode_tiled_fn() {
   return fn;
 }
 
-template <int NS, int R>
+template <int NS, int R, bool DN = false, bool EF = false>
 static bool launch_apply3t(Ctx& c, const DevOp& op, const double* x, double* y, const int* halt, const int* cond) {
   static_assert(NS >= 3, "planes p, p + 1 are read while plane p + NS - 1 lands");
   using G = AtGeo<R>;
@@ -1004,11 +1023,11 @@ static bool launch_apply3t(Ctx& c, const DevOp& op, const double* x, double* y, 
           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
     return false;
   const size_t smem = sizeof(double) * (size_t)NS * G::SLOT + sizeof(uint64_t) * NS;
-  ensure_smem(k_apply3t<NS, R>, smem);
+  ensure_smem(k_apply3t<NS, R, DN, EF>, smem);
   const int64_t tx = (op.nx + AT_TX - 1) / AT_TX, ty = (op.ny + G::TY - 1) / G::TY;
-  const int kz = ring_kz(op, tx * ty, ring_slots(c, k_apply3t<NS, R>, smem));
+  const int kz = ring_kz(op, tx * ty, ring_slots(c, k_apply3t<NS, R, DN, EF>, smem));
   const dim3 gr((unsigned)tx, (unsigned)ty, (unsigned)((op.nz + kz - 1) / kz));
-  launch_k(c, k_apply3t<NS, R>, gr, 256, smem, tm, op, x, y, kz, halt, cond);
+  launch_k(c, k_apply3t<NS, R, DN, EF>, gr, 256, smem, tm, op, x, y, kz, halt, cond);
   return true;
 }
 
@@ -1069,6 +1088,14 @@ void launch_apply(Ctx& c, const DevOp& op, const double* x, double* y, const int
       case 23: launch_k(c, k_apply<2, kStencilDia>, grid, 256, 0, op, x, y, halt, cond); break;
       case 31: {
         if (c.apply_tma && c.apply_ring && op.nx % 2 == 0 && (((uintptr_t)x | (uintptr_t)y) & 15) == 0) {
+          if (c.apply_alt && c.apply_tma == 3) {  // chained applies alternate their z direction (L2 reuse)
+            c.apply_flip ^= 1;
+            const bool ok = c.apply_alt == 2 ? (c.apply_flip ? launch_apply3t<3, 1, true, true>(c, op, x, y, halt, cond)
+                                                             : launch_apply3t<3, 1, false, true>(c, op, x, y, halt, cond))
+                                             : (c.apply_flip ? launch_apply3t<3, 1, true, false>(c, op, x, y, halt, cond)
+                                                             : launch_apply3t<3, 1, false, false>(c, op, x, y, halt, cond));
+            if (ok) break;
+          }
           // SKC_APPLY_TMA = 10 * rows-per-thread + ring slots (a bare slot count means one row)
           const int ns = c.apply_tma % 10, rr = c.apply_tma / 10;
           const bool ok = rr == 2   ? (ns == 4 ? launch_apply3t<4, 2>(c, op, x, y, halt, cond)

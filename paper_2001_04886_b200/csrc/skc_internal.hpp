@@ -212,6 +212,8 @@ struct Ctx {
   bool bupd = true;     // compile-time-shaped s-Omin half-block update at s > 4 (SKC_BUPD=0: k_upd)
   bool faces = true;    // 3D variable-k apply from face coefficients computed once (SKC_FACES=0: per apply)
   int apply_tma_face = 3;  // stored-face 3D apply through the TMA engine (k_apply3t_face), value = ring slots (SKC_APPLY_TMA_FACE; 0 = the cp.async ring)
+  int apply_alt = 0;   // constant 3D apply: alternate launches walk z downwards (1), + evict_first x loads (2) (SKC_APPLY_ALT)
+  int apply_flip = 0;  // (the next direction)
   int apply_tma = 3;  // constant 3D stencil: plane tiles through the TMA engine (k_apply3t); SKC_APPLY_TMA = 10 * rows per thread + ring slots, 0 = the cp.async ring
   bool apply_ring = true;  // 3D applies through a shared-memory plane ring (SKC_APPLY_RING=0: z-marching registers)
   // GPU-count-independent reductions (grouped geometry): bitwise the same results on 1, 2, 4

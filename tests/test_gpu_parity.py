@@ -192,6 +192,28 @@ def test_apply_3d_tma_stored_faces_bit_exact(port, monkeypatch, dims, slots):
     assert np.array_equal(got, want) and np.array_equal(np.signbit(got), np.signbit(want))
 
 
+@pytest.mark.parametrize("dims", [(70, 9, 33), (64, 16, 70), (300, 10, 20), (2, 1, 1), (128, 4, 1), (130, 5, 2),
+                                  (256, 64, 150)])
+@pytest.mark.parametrize("alt", ["1", "2"])
+def test_apply_3d_tma_alternating_direction_bit_exact(port, monkeypatch, dims, alt):
+    """SKC_APPLY_ALT: successive launches of k_apply3t walk their z chunks downwards and upwards in
+    turn (2: with evict_first x loads); both directions are bit-identical to the reference spmv."""
+    from paper_2001_04886_b200 import Context, splitmix64_uniform
+    from paper_2001_04886_b200.problems import Stencil
+    nx, ny, nz = dims
+    ch2 = 20.0 / (nx + 1.0) / 2.0
+    lo, hi = -1.0 - ch2, -1.0 + ch2
+    st = Stencil(3, nx, ny, nz, (lo, lo, lo, 6.0, hi, hi, hi), ch2, False)
+    a = port.stencil_csr(3, nx, ny, nz, st.coef, kcell=None, ch2=ch2)
+    xv = splitmix64_uniform(23, st.n)
+    want = port.spmv(a, xv)
+    monkeypatch.setenv("SKC_APPLY_ALT", alt)
+    op = Context(0).stencil(st)
+    for _ in range(4):  # down, up, down, up
+        got = op.apply(xv)
+        assert np.array_equal(got, want) and np.array_equal(np.signbit(got), np.signbit(want))
+
+
 @pytest.mark.parametrize("dims", [(37, 21, 19), (70, 9, 33), (5, 3, 2), (64, 16, 70), (33, 8, 5)])
 @pytest.mark.parametrize("vark", [False, True])
 def test_apply_3d_kernel_variants_bit_exact(port, monkeypatch, dims, vark):
